@@ -1,0 +1,180 @@
+/*
+ * cdc_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU definitions of the hashless CDC
+ * operations of PAPER.md (arxiv 2508.05797, "Accelerating Data Chunking in
+ * Deduplication Systems using Vector Instructions").  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * may load this library.  It shares no code, header, table or constant with
+ * the CUDA path under paper_2508_05797_b200/ and never calls it.
+ *
+ * Conventions (DESIGN.md §3 "Readings"):
+ *   - a stream is d[0..L); chunks tile it; a chunk starting at s ends at the
+ *     exclusive offset e returned by *_chunk_end (the next chunk starts at e);
+ *   - max_size caps a chunk's length (reading R5); the paper's hashless
+ *     algorithms have no other minimum than the one their window implies
+ *     (every content boundary lies >= w bytes after the chunk start);
+ *   - window w >= 1 and max_size > w are required (checked by the caller).
+ *
+ * Every function follows the paper's description step by step; no blocking,
+ * fusion or reordering.  Parity is pinned in tests/test_oracle_*.py.
+ */
+#include <stdint.h>
+#include <stddef.h>
+
+enum { OR_MAX = 0, OR_MIN = 1 };
+enum { OR_GT = 0, OR_GEQ = 1, OR_LT = 2, OR_LEQ = 3, OR_EQ = 4 };
+enum { OR_RAM = 0, OR_AE_MAX = 1, OR_AE_MIN = 2 };
+
+/*
+ * Extreme Byte Search -- PAPER.md §4.1 (lines 324-330): "identifies the
+ * extreme byte (maximum/minimum) in a fixed-size window".  The paper returns
+ * only the value; we also return the leftmost position holding it (reading R6).
+ * Returns 0 on success, -1 for an empty region.
+ */
+int oracle_extreme_byte_search(const uint8_t *region, uint64_t n, int mode,
+                               uint8_t *value, uint64_t *pos)
+{
+    if (n == 0)
+        return -1;
+    uint8_t best = region[0];
+    uint64_t best_pos = 0;
+    for (uint64_t i = 1; i < n; i++) {
+        int better = (mode == OR_MAX) ? (region[i] > best) : (region[i] < best);
+        if (better) {
+            best = region[i];
+            best_pos = i;
+        }
+    }
+    *value = best;
+    *pos = best_pos;
+    return 0;
+}
+
+static int cmp_holds(uint8_t b, uint8_t target, int cmp)
+{
+    switch (cmp) {
+    case OR_GT:  return b > target;
+    case OR_GEQ: return b >= target;
+    case OR_LT:  return b < target;
+    case OR_LEQ: return b <= target;
+    default:     return b == target;
+    }
+}
+
+/*
+ * Range Scan -- PAPER.md §4.2 (lines 343-347): "bytes are serially compared
+ * against a target value" with one of the comparators GT, GEQ, LT, LEQ, EQ.
+ * Returns the index of the first byte b with (b cmp target), or n if none.
+ */
+uint64_t oracle_range_scan(const uint8_t *region, uint64_t n, uint8_t target, int cmp)
+{
+    for (uint64_t i = 0; i < n; i++)
+        if (cmp_holds(region[i], target, cmp))
+            return i;
+    return n;
+}
+
+/*
+ * RAM -- PAPER.md §2.1.2 (line 198, Fig. 2c) and §4.3 (line 355):
+ * "RAM begins by scanning a fixed-size window at the beginning of each chunk
+ * to find the maximum valued byte (F1).  It then begins scanning at the first
+ * byte outside the window, serially comparing these bytes against this
+ * maximum value.  A chunk boundary is inserted when the first byte that
+ * exceeds or equals the maximum is found (F3)."  The boundary byte is the
+ * last byte of the chunk (reading R2).
+ */
+uint64_t oracle_ram_chunk_end(const uint8_t *d, uint64_t L, uint64_t s,
+                              uint64_t w, uint64_t max_size)
+{
+    if (L - s <= w)                       /* window does not fit: final chunk */
+        return L;
+    uint8_t M;
+    uint64_t mpos;
+    oracle_extreme_byte_search(d + s, w, OR_MAX, &M, &mpos);   /* window [s, s+w) */
+    uint64_t limit = (L - s < max_size) ? L : s + max_size;     /* R5 cap */
+    uint64_t i = s + w + oracle_range_scan(d + s + w, limit - (s + w), M, OR_GEQ);
+    if (i < limit)
+        return i + 1;                     /* boundary byte d[i] ends the chunk */
+    return limit;                         /* max_size cap, or end of stream */
+}
+
+/*
+ * AE-Max / AE-Min -- PAPER.md §2.1.2 (lines 169-171, Fig. 2a) and §4.3
+ * (lines 357-359): find a target byte greater (AE-Max) / less (AE-Min) than
+ * all the bytes before it in the chunk; scan the fixed-size window of w bytes
+ * after the target for its maximum (minimum); if the target is not exceeded
+ * by that extreme (reading R1) insert a boundary after the window, otherwise
+ * "scanning continues for a new target byte" with a GT (LT) Range Scan.
+ *
+ * The first byte of a chunk has no byte before it and so is the first target.
+ * Because the current target t holds the running extreme of d[s..t], the next
+ * target is the first byte after t that strictly exceeds d[t]; when the window
+ * test fails that byte lies inside the window (its extreme exceeds d[t]).
+ */
+uint64_t oracle_ae_chunk_end(const uint8_t *d, uint64_t L, uint64_t s,
+                             uint64_t w, uint64_t max_size, int mode)
+{
+    uint64_t limit = (L - s < max_size) ? L : s + max_size;     /* R5 cap */
+    uint64_t t = s;                                             /* first target */
+    for (;;) {
+        /* the boundary would be the window's last byte d[t+w]; it must lie
+         * inside the chunk limit, and no later target can end earlier */
+        if (t + w >= limit)
+            return limit;
+        uint8_t ext;
+        uint64_t epos;
+        oracle_extreme_byte_search(d + t + 1, w, mode, &ext, &epos);  /* window (t, t+w] */
+        int target_wins = (mode == OR_MAX) ? (d[t] >= ext) : (d[t] <= ext);
+        if (target_wins)
+            return t + w + 1;                 /* boundary after the window */
+        int cmp = (mode == OR_MAX) ? OR_GT : OR_LT;
+        t = t + 1 + oracle_range_scan(d + t + 1, w, d[t], cmp);   /* next target */
+    }
+}
+
+uint64_t oracle_chunk_end(int algo, const uint8_t *d, uint64_t L, uint64_t s,
+                          uint64_t w, uint64_t max_size)
+{
+    if (algo == OR_RAM)
+        return oracle_ram_chunk_end(d, L, s, w, max_size);
+    return oracle_ae_chunk_end(d, L, s, w, max_size,
+                               algo == OR_AE_MAX ? OR_MAX : OR_MIN);
+}
+
+/*
+ * Whole-stream chunking: the chain s_0 = 0, s_{j+1} = chunk_end(s_j) until L.
+ * Writes the exclusive chunk end offsets (the last one is L) into out[] and
+ * returns their number (0 for an empty stream); stops early at cap entries.
+ */
+uint64_t oracle_chunk(int algo, const uint8_t *d, uint64_t L, uint64_t w,
+                      uint64_t max_size, uint64_t *out, uint64_t cap)
+{
+    uint64_t n = 0, s = 0;
+    while (s < L && n < cap) {
+        uint64_t e = oracle_chunk_end(algo, d, L, s, w, max_size);
+        out[n++] = e;
+        s = e;
+    }
+    return n;
+}
+
+/*
+ * The chain from an arbitrary start (used by tests of the speculative /
+ * range-sharded host logic): starts at `start` as if a chunk began there and
+ * records every chunk start in [start, stop) followed by the first start >= stop
+ * (or L).  Returns the number written.
+ */
+uint64_t oracle_chain_from(int algo, const uint8_t *d, uint64_t L, uint64_t start,
+                           uint64_t stop, uint64_t w, uint64_t max_size,
+                           uint64_t *out, uint64_t cap)
+{
+    uint64_t n = 0, s = start;
+    while (n < cap) {
+        out[n++] = s;
+        if (s >= stop || s >= L)
+            break;
+        s = oracle_chunk_end(algo, d, L, s, w, max_size);
+    }
+    return n;
+}

@@ -1,0 +1,281 @@
+"""Pins of the CPU oracle against things other than itself (CPU only).
+
+Each test names what fixes the expected value: a fixture built from the
+paper's text (tests/golden/), a closed form, a brute-force evaluation of the
+boundary predicate written from the paper's definition, an independent
+single-pass formulation (oracle/pyref.py), a library routine the operation
+reduces to, or a statistical closed form.
+"""
+import glob
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import dedup, pyref
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+ALGOS = ["ram", "ae_max", "ae_min"]
+
+
+# --------------------------------------------------------------------------
+# golden fixtures from the paper's text
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "*.json"))))
+def test_golden(path):
+    g = json.load(open(path))
+    data = bytes.fromhex(g["input_hex"])
+    if g["op"] == "extreme_byte_search":
+        assert oracle.extreme_byte_search(data, g["mode"]) == (g["expected"]["value"], g["expected"]["pos"])
+    elif g["op"] == "range_scan":
+        assert oracle.range_scan(data, g["target"], g["cmp"]) == g["expected"]
+    else:
+        ends = oracle.chunk(g["algo"], data, g["w"], g["max_size"]).tolist()
+        assert ends == g["expected_ends"]
+        assert pyref.chunk(g["algo"], list(data), g["w"], g["max_size"]) == g["expected_ends"]
+
+
+# --------------------------------------------------------------------------
+# primitives reduce to library routines
+# --------------------------------------------------------------------------
+def test_ebs_is_argmax_argmin():
+    rng = np.random.default_rng(0)
+    for n in [1, 2, 15, 16, 17, 63, 64, 65, 4096, 8191]:
+        r = rng.integers(0, 256, n, dtype=np.uint8)
+        assert oracle.extreme_byte_search(r, "max") == (int(r.max()), int(np.argmax(r)))
+        assert oracle.extreme_byte_search(r, "min") == (int(r.min()), int(np.argmin(r)))
+    z = np.zeros(4096, np.uint8)
+    assert oracle.extreme_byte_search(z, "max") == (0, 0)  # leftmost tie-break
+    with pytest.raises(ValueError):
+        oracle.extreme_byte_search(np.zeros(0, np.uint8))
+
+
+@pytest.mark.parametrize("cmp,fn", [("gt", np.greater), ("geq", np.greater_equal), ("lt", np.less),
+                                    ("leq", np.less_equal), ("eq", np.equal)])
+def test_range_scan_is_first_nonzero(cmp, fn):
+    rng = np.random.default_rng(1)
+    for n in [0, 1, 31, 32, 33, 1000]:
+        r = rng.integers(0, 256, n, dtype=np.uint8)
+        for t in [0, 1, 127, 128, 200, 254, 255]:
+            hits = np.nonzero(fn(r, np.uint8(t)))[0]
+            exp = int(hits[0]) if hits.size else None
+            assert oracle.range_scan(r, t, cmp) == exp
+
+
+# --------------------------------------------------------------------------
+# closed forms
+# --------------------------------------------------------------------------
+def _lens(ends):
+    e = np.asarray(ends, dtype=np.int64)
+    return np.diff(np.concatenate([[0], e]))
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("value", [0, 1, 128, 255])
+def test_constant_stream_chunks_are_w_plus_1(algo, value):
+    # constant data: RAM max = v and the first post-window byte is >= v;
+    # AE: the first byte is the target and no window byte exceeds it.
+    w, L = 37, 1000
+    ends = oracle.chunk(algo, synth.constant(L, value), w, 4 * w)
+    lens = _lens(ends)
+    assert (lens[:-1] == w + 1).all() and 1 <= lens[-1] <= w + 1
+    assert lens.size == -(-L // (w + 1))
+
+
+def test_monotone_streams():
+    w, mx = 5, 23
+    inc = np.arange(200, dtype=np.uint8)
+    dec = inc[::-1].copy()
+    # increasing: RAM window max d[s+w-1] < d[s+w] -> w+1; AE-Max: every byte
+    # beats the target -> only the cap ends chunks; AE-Min: first byte wins -> w+1
+    assert (_lens(oracle.chunk("ram", inc, w, mx))[:-1] == w + 1).all()
+    assert (_lens(oracle.chunk("ae_max", inc, w, mx))[:-1] == mx).all()
+    assert (_lens(oracle.chunk("ae_min", inc, w, mx))[:-1] == w + 1).all()
+    # decreasing: mirror images
+    assert (_lens(oracle.chunk("ram", dec, w, mx))[:-1] == mx).all()
+    assert (_lens(oracle.chunk("ae_max", dec, w, mx))[:-1] == w + 1).all()
+    assert (_lens(oracle.chunk("ae_min", dec, w, mx))[:-1] == mx).all()
+
+
+def test_degenerate_streams():
+    for algo in ALGOS:
+        assert oracle.chunk(algo, np.zeros(0, np.uint8), 4, 16).tolist() == []
+        assert oracle.chunk(algo, np.array([7], np.uint8), 4, 16).tolist() == [1]
+        # shorter than the window + 1: one final chunk
+        assert oracle.chunk(algo, np.arange(4, dtype=np.uint8), 4, 16).tolist() == [4]
+    with pytest.raises(ValueError):
+        oracle.chunk("ram", np.zeros(10, np.uint8), 4, 4)
+
+
+# --------------------------------------------------------------------------
+# brute-force predicate enumeration (definition written independently)
+# --------------------------------------------------------------------------
+def _bf_chunk_end(algo, d, s, w, max_size):
+    """Smallest valid end e, by checking the paper's boundary predicate for
+    every candidate e with Python slicing; else the cap / end of stream."""
+    L = len(d)
+    limit = min(L, s + max_size)
+    for e in range(s + 1, limit + 1):
+        b = e - 1  # boundary byte = last byte of the chunk
+        if algo == "ram":
+            # b lies outside the window and is >= the window's maximum (Fig. 2c);
+            # the first such b is taken (min over e)
+            if b >= s + w and s + w <= L and d[b] >= max(d[s:s + w]):
+                return e
+        else:
+            t = b - w  # the target whose window (t, t+w] ends at b
+            if t < s:
+                continue
+            before = d[s:t]
+            win = d[t + 1:t + w + 1]
+            if algo == "ae_max":
+                is_target = all(x < d[t] for x in before)
+                wins = d[t] >= max(win)
+            else:
+                is_target = all(x > d[t] for x in before)
+                wins = d[t] <= min(win)
+            if is_target and wins:
+                return e
+    return limit
+
+
+def _bf_chunk(algo, d, w, max_size):
+    out, s = [], 0
+    while s < len(d):
+        s = _bf_chunk_end(algo, d, s, w, max_size)
+        out.append(s)
+    return out
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_exhaustive_small_alphabet(algo):
+    alphabet = [0, 1, 2]
+    count = 0
+    for n in range(1, 8):
+        for tup in itertools.product(alphabet, repeat=n):
+            d = list(tup)
+            arr = np.array(d, dtype=np.uint8)
+            for w in (1, 2, 3):
+                for mx in (w + 1, w + 2, 6):
+                    exp = _bf_chunk(algo, d, w, mx)
+                    assert oracle.chunk(algo, arr, w, mx).tolist() == exp, (d, w, mx)
+                    assert pyref.chunk(algo, d, w, mx) == exp
+                    count += 1
+    assert count > 10000
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_random_vs_bruteforce_and_pyref(algo):
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        n = int(rng.integers(1, 400))
+        hi = int(rng.choice([2, 4, 16, 256]))
+        d = rng.integers(0, hi, n).astype(np.uint8)
+        w = int(rng.integers(1, 24))
+        mx = int(w + 1 + rng.integers(0, 60))
+        exp = _bf_chunk(algo, d.tolist(), w, mx)
+        assert oracle.chunk(algo, d, w, mx).tolist() == exp
+        assert pyref.chunk(algo, d.tolist(), w, mx) == exp
+
+
+# --------------------------------------------------------------------------
+# invariants on realistic sizes
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("gen", ["uniform", "zipf"])
+def test_invariants(algo, gen):
+    L = 1 << 20
+    d = synth.uniform(L, 11) if gen == "uniform" else synth.zipf_bytes(L, 1.1, 12)
+    w, mx = 512, 4096
+    ends = oracle.chunk(algo, d, w, mx)
+    lens = _lens(ends)
+    assert int(ends[-1]) == L and (lens > 0).all()               # chunks tile the input
+    assert (lens[:-1] >= w + 1).all() and (lens <= mx).all()     # implicit min, cap
+    # boundary property for content (non-cap) boundaries
+    s = 0
+    for e in ends[:-1].tolist():
+        if e - s < mx:
+            b = e - 1
+            if algo == "ram":
+                M = d[s:s + w].max()
+                assert d[b] >= M and (d[s + w:b] < M).all()
+            else:
+                t = b - w
+                if algo == "ae_max":
+                    assert (d[s:t] < d[t]).all() and d[t] >= d[t + 1:b + 1].max()
+                else:
+                    assert (d[s:t] > d[t]).all() and d[t] <= d[t + 1:b + 1].min()
+        s = e
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_content_defined_resync(algo):
+    """A prefix insertion shifts later boundaries by the insertion length."""
+    L = 1 << 19
+    d = synth.uniform(L, 21)
+    w, mx = 256, 2048
+    base = oracle.chunk(algo, d, w, mx)
+    ins = synth.uniform(777, 22)
+    d2 = np.concatenate([ins, d])
+    e2 = oracle.chunk(algo, d2, w, mx).astype(np.int64)
+    shifted = e2[e2 > 777] - 777
+    base = base.astype(np.int64)
+    common = np.intersect1d(base, shifted)
+    # after re-synchronisation every later boundary coincides
+    first = common[0]
+    assert (base[base >= first] == shifted[shifted >= first]).all()
+    assert first < 64 * mx
+
+
+def test_chain_from_matches_chunk():
+    d = synth.uniform(200000, 3)
+    for algo in ALGOS:
+        ends = oracle.chunk(algo, d, 300, 3000)
+        ch = oracle.chain_from(algo, d, 0, len(d), 300, 3000)
+        assert ch.tolist() == [0] + ends.tolist()
+
+
+# --------------------------------------------------------------------------
+# statistical closed form (RAM on uniform bytes)
+# --------------------------------------------------------------------------
+def test_ram_mean_chunk_length_closed_form():
+    """On i.i.d. uniform bytes the window max M of w bytes has
+    P(M <= m) = ((m+1)/256)^w, and the scan after the window is geometric with
+    success probability (256-M)/256, so E[len] = w + sum_M P(M) * 256/(256-M)
+    (no cap).  A GT instead of GEQ comparator, or a window of the wrong length,
+    moves the mean by far more than the sampling error."""
+    w = 100
+    L = 6 << 20
+    d = synth.uniform(L, 5)
+    lens = _lens(oracle.chunk("ram", d, w, 1 << 40))[:-1]
+    pm = np.array([((m + 1) / 256) ** w - (m / 256) ** w for m in range(256)])
+    expect = w + float(sum(pm[m] * 256.0 / (256 - m) for m in range(256)))
+    se = lens.std() / math.sqrt(lens.size)
+    assert abs(lens.mean() - expect) < 4 * se, (lens.mean(), expect, se)
+
+
+# --------------------------------------------------------------------------
+# dedup space savings, Eq. (1)
+# --------------------------------------------------------------------------
+def test_space_savings_closed_forms():
+    assert dedup.space_savings(100, 100) == 0.0
+    assert dedup.space_savings(200, 100) == 50.0
+    with pytest.raises(ValueError):
+        dedup.space_savings(0, 0)
+    x = synth.uniform(1 << 20, 9)
+    xx = np.concatenate([x, x])
+    w, mx = 1000, 16000
+    ends = oracle.chunk("ram", xx, w, mx)
+    total, uniq = dedup.unique_bytes([xx], [ends])
+    assert total == xx.size
+    s = dedup.space_savings(total, uniq)
+    assert 49.0 <= s <= 50.0
+    # disjoint random data: no duplicate chunks
+    y = synth.uniform(1 << 20, 10)
+    t2, u2 = dedup.unique_bytes([x, y], [oracle.chunk("ram", x, w, mx), oracle.chunk("ram", y, w, mx)])
+    assert t2 == u2
