@@ -1,0 +1,200 @@
+/*
+ * cdc_b200.h -- C ABI of the B200 (sm_100a) hashless content-defined chunker.
+ *
+ * Implements the hot path of PAPER.md (arxiv 2508.05797, "Accelerating Data
+ * Chunking in Deduplication Systems using Vector Instructions"): the RAM and
+ * AE (AE-Max / AE-Min) boundary rules of §2.1.2, built from the two patterns
+ * of §4 -- Extreme Byte Search (§4.1) and Range Scan (§4.2) -- composed as in
+ * §4.3.  The output is the list of chunk boundaries (§2.2.2 Eq. 2: chunking
+ * throughput = original data size / time to generate all chunk boundaries).
+ *
+ * Conventions (DESIGN.md §3 lists every reading of the paper):
+ *   - A stream is d[0..L).  A chunk starting at s ends at an exclusive offset
+ *     e; the next chunk starts at e.  Boundaries are reported as these
+ *     exclusive end offsets (uint64, relative to the stream start), in
+ *     increasing order; the last one equals L.  An empty stream has none.
+ *   - RAM (§2.1.2 l.198): M = max d[s..s+w); the chunk ends after the first
+ *     byte at index >= s+w with value >= M.
+ *   - AE-Max (§2.1.2 l.169, reading R1): targets are bytes strictly greater
+ *     than every earlier byte of the chunk; the chunk ends after the w-byte
+ *     window following the first target that no window byte exceeds.
+ *     AE-Min mirrors it with "less".
+ *   - max_size (reading R5) caps every chunk's length; the minimum chunk size
+ *     is the one the window implies (w+1 bytes) -- the paper defines no other.
+ *   - Results are bit-identical to the CPU oracle in oracle/ (tests/).
+ *
+ * Memory: every pointer named d_* is a device pointer (cudaMalloc'ed or a
+ * torch CUDA tensor's storage) on the current device; h_* pointers are host
+ * memory.  The library never frees caller memory.  Device-side entry points
+ * are asynchronous on `stream` (a cudaStream_t passed as void*, NULL = legacy
+ * default stream); results are valid after the stream is synchronised.
+ * Input buffers may be read up to 15 bytes past their last byte and up to 15
+ * bytes before their first byte, never crossing the 16-byte-aligned granule
+ * that holds a valid byte (so never a different page).
+ *
+ * Errors: every function returns 0 on success or a negative cdc_status; the
+ * message of the last error on the calling thread is cdc_last_error().
+ * Device-side overflow (more boundaries than the caller's capacity) is
+ * reported by the count written to d_count exceeding that capacity; the first
+ * `capacity` boundaries are still written.
+ */
+#ifndef CDC_B200_H
+#define CDC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CDC_ABI_VERSION 1
+
+typedef enum {
+    CDC_OK = 0,
+    CDC_ERR_INVALID = -1,     /* bad argument (null pointer, w == 0, max_size <= w, ...) */
+    CDC_ERR_CUDA = -2,        /* a CUDA runtime call failed (message has the CUDA error) */
+    CDC_ERR_WORKSPACE = -3,   /* workspace smaller than cdc_workspace_size() */
+    CDC_ERR_CAPACITY = -4,    /* host entry point: output capacity too small */
+    CDC_ERR_NO_DEVICE = -5    /* no sm_100 device present */
+} cdc_status;
+
+/* Algorithms: PAPER.md §2.1.2 (RAM, AE-Max, AE-Min). */
+typedef enum { CDC_RAM = 0, CDC_AE_MAX = 1, CDC_AE_MIN = 2 } cdc_algo;
+
+/* Extreme Byte Search modes (§4.1) and Range Scan comparators (§4.2). */
+typedef enum { CDC_EXT_MAX = 0, CDC_EXT_MIN = 1 } cdc_extreme_mode;
+typedef enum { CDC_GT = 0, CDC_GEQ = 1, CDC_LT = 2, CDC_LEQ = 3, CDC_EQ = 4 } cdc_cmp;
+
+typedef struct {
+    int32_t  algo;        /* cdc_algo */
+    uint32_t window;      /* w >= 1: the fixed-size window of §2.1.2 */
+    uint64_t max_size;    /* chunk length cap, > window */
+    uint64_t seg_bytes;   /* speculation segment size S (0 = automatic); multiple of 2048 */
+    uint64_t halo_bytes;  /* max speculative halo walk past a segment end (0 = automatic) */
+} cdc_params;
+
+/* Version of this ABI (CDC_ABI_VERSION). */
+int cdc_abi_version(void);
+
+/* Message of the last error on the calling thread ("" if none). */
+const char *cdc_last_error(void);
+
+/*
+ * Window size for a target average chunk size (reading R4):
+ * on i.i.d. uniform bytes both RAM and AE chunks average w + 256 bytes when
+ * w >> 256 (window, then a geometric wait for the top byte value), so
+ * w = avg - 256 for avg >= 512, and w = avg/2 below.  Writes *window.
+ */
+int cdc_window_for_avg(int32_t algo, uint64_t avg_size, uint32_t *window);
+
+/* Fill *p with defaults for `algo`/`avg_size`: window from
+ * cdc_window_for_avg, max_size = 4 * avg_size, automatic S and halo. */
+int cdc_params_default(cdc_params *p, int32_t algo, uint64_t avg_size);
+
+/* Upper bound on the number of boundaries of a stream of `len` bytes
+ * (every chunk but the last holds >= window+1 bytes). */
+uint64_t cdc_max_boundaries(const cdc_params *p, uint64_t len);
+
+/*
+ * Workspace (device bytes) needed by cdc_chunk / cdc_chunk_batch for a batch
+ * of `nfiles` streams totalling `total_len` bytes whose largest stream has
+ * `max_len` bytes (for a single stream pass nfiles = 1 and
+ * total_len = max_len = len).  The workspace must be 256-byte aligned and
+ * must not be used concurrently by two calls.
+ */
+int cdc_workspace_size(const cdc_params *p, uint64_t nfiles, uint64_t total_len,
+                       uint64_t max_len, size_t *bytes);
+
+/*
+ * Chunk one device-resident stream d_data[0..len).
+ *   d_bounds : device uint64[bounds_cap]; receives the exclusive chunk end
+ *              offsets (ascending, last = len).
+ *   d_count  : device uint64[1]; receives the number of boundaries (may
+ *              exceed bounds_cap, see overflow above).
+ * Asynchronous on `stream`.
+ */
+int cdc_chunk(const cdc_params *p, const uint8_t *d_data, uint64_t len,
+              uint64_t *d_bounds, uint64_t bounds_cap, uint64_t *d_count,
+              void *d_workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Chunk a packed batch of streams (many-file chunking, BASELINE configs[3]):
+ * stream f is d_data[d_file_offsets[f] .. d_file_offsets[f+1]),
+ * d_file_offsets is a device uint64[nfiles+1], non-decreasing.
+ * Boundaries of stream f are relative to its own start and are written to
+ * d_bounds[d_bound_offsets[f] .. d_bound_offsets[f+1]); d_bound_offsets is a
+ * device uint64[nfiles+1] written by the call (d_bound_offsets[nfiles] is the
+ * total count, also written to d_count).
+ */
+int cdc_chunk_batch(const cdc_params *p, const uint8_t *d_data,
+                    const uint64_t *d_file_offsets, uint64_t nfiles,
+                    uint64_t total_len, uint64_t max_len,
+                    uint64_t *d_bounds, uint64_t bounds_cap,
+                    uint64_t *d_bound_offsets, uint64_t *d_count,
+                    void *d_workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * End-to-end entry point with HOST buffers: copies h_data to the device,
+ * chunks it, copies the boundaries back to h_bounds (host uint64[bounds_cap])
+ * and the count to *h_count; synchronous.  Device memory is managed by the
+ * library (cached between calls on the calling thread's device).
+ * Returns CDC_ERR_CAPACITY (with *h_count set) when bounds_cap is too small.
+ */
+int cdc_chunk_host(const cdc_params *p, const uint8_t *h_data, uint64_t len,
+                   uint64_t *h_bounds, uint64_t bounds_cap, uint64_t *h_count);
+
+/*
+ * Speculative chain from an arbitrary start (range sharding across GPUs,
+ * DESIGN.md §6): treats d_data[0..len) as a stream that may continue past
+ * `len` (the caller's shard plus its halo), starts a chunk at `start` and
+ * writes every chunk start of that chain, beginning with `start`, up to and
+ * including the first start >= stop (or until the chain ends at len).
+ *   d_starts : device uint64[starts_cap], d_count : device uint64[1].
+ * *d_count receives the number written (capped reading as above); the chain
+ * ends at len when the last start plus its chunk reaches len.
+ */
+int cdc_chain(const cdc_params *p, const uint8_t *d_data, uint64_t len,
+              uint64_t start, uint64_t stop, uint64_t *d_starts,
+              uint64_t starts_cap, uint64_t *d_count, void *stream);
+
+/*
+ * Batched Extreme Byte Search (§4.1): for each region r in [0, n),
+ * region = d_data[d_off[r] .. d_off[r] + d_len[r]) (d_len[r] >= 1),
+ * writes the max (mode CDC_EXT_MAX) or min byte to d_value[r] and its
+ * leftmost offset within the region to d_pos[r].  One warp per region.
+ */
+int cdc_extreme_byte_search(const uint8_t *d_data, const uint64_t *d_off,
+                            const uint64_t *d_len, uint64_t n, int32_t mode,
+                            uint8_t *d_value, uint64_t *d_pos, void *stream);
+
+/*
+ * Batched Range Scan (§4.2): for each region r, writes to d_pos[r] the offset
+ * within the region of the first byte b with (b cmp d_target[r]), or
+ * d_len[r] if there is none.  Regions may be empty.  One warp per region.
+ */
+int cdc_range_scan(const uint8_t *d_data, const uint64_t *d_off,
+                   const uint64_t *d_len, const uint8_t *d_target, uint64_t n,
+                   int32_t cmp, uint64_t *d_pos, void *stream);
+
+/* Number of kernel launches made by the last cdc_chunk / cdc_chunk_batch
+ * call on this thread (for bench.py's gpu_launches count). */
+int cdc_last_launch_count(void);
+
+/*
+ * Per-kernel timing for measurement (bench.py's roofline): while enabled,
+ * cdc_chunk / cdc_chunk_batch record CUDA events on their stream around each
+ * of their kernels.  cdc_profile_collect synchronises on those events and
+ * writes, for the pipeline kernels in order {k_seg_prefix, k_speculate,
+ * k_resolve, k_write}, the summed milliseconds ms_sum[4] and launch counts
+ * launches[4] since the previous collect, and the number of calls; it then
+ * forgets them.  Host-side bookkeeping per calling thread.
+ */
+int cdc_profile_enable(int on);
+int cdc_profile_collect(double *ms_sum, uint64_t *launches, uint64_t *calls);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CDC_B200_H */

@@ -1,0 +1,203 @@
+"""Thin Python binding over the C ABI (argument marshalling only).
+
+Every computation runs in libcdc_b200.so's CUDA kernels; PyTorch provides the
+device memory (CUDA tensors) and the stream.  Names follow include/cdc_b200.h.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from ._lib import CdcError, cdc_params, check, lib
+
+ALGOS = {"ram": 0, "ae_max": 1, "ae_min": 2}
+MODES = {"max": 0, "min": 1}
+CMPS = {"gt": 0, "geq": 1, "lt": 2, "leq": 3, "eq": 4}
+
+__all__ = [
+    "CdcError", "ALGOS", "params", "window_for_avg", "max_boundaries", "workspace_size",
+    "chunk_async", "chunk", "chunk_batch", "chunk_host", "chain",
+    "extreme_byte_search", "range_scan", "last_launch_count", "abi_version",
+    "profile_enable", "profile_collect", "KERNELS",
+]
+
+
+KERNELS = ["k_seg_prefix", "k_speculate", "k_resolve", "k_write"]
+
+
+def profile_enable(on: bool = True) -> None:
+    check(lib.cdc_profile_enable(1 if on else 0))
+
+
+def profile_collect() -> dict:
+    """{kernel: (summed ms, launches)} since the last collect (synchronises)."""
+    ms = (ctypes.c_double * 4)()
+    n = (ctypes.c_uint64 * 4)()
+    calls = ctypes.c_uint64()
+    check(lib.cdc_profile_collect(ms, n, ctypes.byref(calls)))
+    out = {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KERNELS)}
+    out["calls"] = int(calls.value)
+    return out
+
+
+def abi_version() -> int:
+    return lib.cdc_abi_version()
+
+
+def last_launch_count() -> int:
+    return lib.cdc_last_launch_count()
+
+
+def window_for_avg(algo: str, avg_size: int) -> int:
+    w = ctypes.c_uint32()
+    check(lib.cdc_window_for_avg(ALGOS[algo], avg_size, ctypes.byref(w)))
+    return int(w.value)
+
+
+def params(algo: str, avg_size: int | None = None, window: int | None = None, max_size: int | None = None,
+           seg_bytes: int = 0, halo_bytes: int = 0) -> cdc_params:
+    p = cdc_params()
+    if avg_size is not None:
+        check(lib.cdc_params_default(ctypes.byref(p), ALGOS[algo], avg_size))
+    else:
+        p.algo = ALGOS[algo]
+    if window is not None:
+        p.window = window
+    if max_size is not None:
+        p.max_size = max_size
+    p.seg_bytes = seg_bytes
+    p.halo_bytes = halo_bytes
+    return p
+
+
+def max_boundaries(p: cdc_params, length: int) -> int:
+    return int(lib.cdc_max_boundaries(ctypes.byref(p), length))
+
+
+def workspace_size(p: cdc_params, nfiles: int, total_len: int, max_len: int) -> int:
+    n = ctypes.c_size_t()
+    check(lib.cdc_workspace_size(ctypes.byref(p), nfiles, total_len, max_len, ctypes.byref(n)))
+    return int(n.value)
+
+
+def _stream_ptr(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _dev_u8(data: torch.Tensor) -> torch.Tensor:
+    if not (isinstance(data, torch.Tensor) and data.is_cuda and data.dtype == torch.uint8):
+        raise TypeError("data must be a CUDA uint8 tensor")
+    return data.contiguous()
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    # torch's caching allocator returns 512-byte aligned blocks
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+
+
+def chunk_async(data: torch.Tensor, p: cdc_params, bounds: torch.Tensor, count: torch.Tensor,
+                workspace: torch.Tensor, stream=None) -> None:
+    """cdc_chunk on preallocated device buffers (no synchronisation)."""
+    check(lib.cdc_chunk(ctypes.byref(p), data.data_ptr(), data.numel(), bounds.data_ptr(), bounds.numel(),
+                        count.data_ptr(), workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
+
+
+def chunk(data: torch.Tensor, p: cdc_params, stream=None) -> torch.Tensor:
+    """Chunk boundaries (exclusive end offsets, int64 tensor on the device) of one stream."""
+    data = _dev_u8(data)
+    n = data.numel()
+    cap = max_boundaries(p, n)
+    bounds = torch.empty(max(cap, 1), dtype=torch.int64, device=data.device)
+    count = torch.zeros(1, dtype=torch.int64, device=data.device)
+    ws = _workspace(workspace_size(p, 1, n, n), data.device)
+    chunk_async(data, p, bounds, count, ws, stream)
+    m = int(count.item())
+    if m > cap:
+        raise CdcError(f"boundary count {m} exceeds capacity {cap}")
+    return bounds[:m]
+
+
+def chunk_batch(data: torch.Tensor, file_offsets, p: cdc_params, stream=None):
+    """Per-file boundaries of a packed batch: (bounds int64[total], bound_offsets int64[nfiles+1])."""
+    data = _dev_u8(data)
+    offs = torch.as_tensor(np.asarray(file_offsets, dtype=np.int64)).to(data.device)
+    nfiles = offs.numel() - 1
+    sizes = (offs[1:] - offs[:-1]).cpu()
+    total = int(sizes.sum()) if nfiles else 0
+    max_len = int(sizes.max()) if nfiles else 0
+    cap = int(sum(max_boundaries(p, int(s)) for s in sizes.tolist())) if nfiles < 4096 else \
+        total // (p.window + 1) + nfiles
+    bounds = torch.empty(max(cap, 1), dtype=torch.int64, device=data.device)
+    bo = torch.zeros(nfiles + 1, dtype=torch.int64, device=data.device)
+    count = torch.zeros(1, dtype=torch.int64, device=data.device)
+    ws = _workspace(workspace_size(p, nfiles, total, max_len), data.device)
+    check(lib.cdc_chunk_batch(ctypes.byref(p), data.data_ptr(), offs.data_ptr(), nfiles, total, max_len,
+                              bounds.data_ptr(), cap, bo.data_ptr(), count.data_ptr(), ws.data_ptr(), ws.numel(),
+                              _stream_ptr(stream)))
+    m = int(count.item())
+    if m > cap:
+        raise CdcError(f"boundary count {m} exceeds capacity {cap}")
+    return bounds[:m], bo
+
+
+def chunk_host(data: np.ndarray, p: cdc_params, out: np.ndarray | None = None) -> np.ndarray:
+    """cdc_chunk_host: host bytes in, host boundaries out (copies inside the call)."""
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    cap = max_boundaries(p, data.size)
+    if out is None or out.size < cap:
+        out = np.empty(max(cap, 1), dtype=np.uint64)
+    n = ctypes.c_uint64()
+    check(lib.cdc_chunk_host(ctypes.byref(p), data.ctypes.data, data.size, out.ctypes.data, out.size,
+                             ctypes.byref(n)))
+    return out[:n.value]
+
+
+def chain(data: torch.Tensor, p: cdc_params, start: int, stop: int, cap: int | None = None,
+          stream=None) -> torch.Tensor:
+    """Chunk starts of the chain begun at `start`, up to the first start >= stop."""
+    data = _dev_u8(data)
+    if cap is None:
+        cap = max_boundaries(p, max(0, min(stop, data.numel()) - start)) + 2
+    out = torch.empty(cap, dtype=torch.int64, device=data.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=data.device)
+    check(lib.cdc_chain(ctypes.byref(p), data.data_ptr(), data.numel(), start, stop, out.data_ptr(), cap,
+                        cnt.data_ptr(), _stream_ptr(stream)))
+    m = int(cnt.item())
+    if m > cap:
+        raise CdcError(f"chain length {m} exceeds capacity {cap}")
+    return out[:m]
+
+
+def _regions(offsets, lengths, device):
+    off = torch.as_tensor(np.asarray(offsets, dtype=np.int64)).to(device)
+    ln = torch.as_tensor(np.asarray(lengths, dtype=np.int64)).to(device)
+    return off, ln
+
+
+def extreme_byte_search(data: torch.Tensor, offsets, lengths, mode: str = "max", stream=None):
+    """§4.1 on many regions: (values uint8[n], leftmost positions int64[n])."""
+    data = _dev_u8(data)
+    off, ln = _regions(offsets, lengths, data.device)
+    n = off.numel()
+    if n and int(ln.min()) < 1:
+        raise CdcError("empty region")
+    val = torch.empty(n, dtype=torch.uint8, device=data.device)
+    pos = torch.empty(n, dtype=torch.int64, device=data.device)
+    check(lib.cdc_extreme_byte_search(data.data_ptr(), off.data_ptr(), ln.data_ptr(), n, MODES[mode],
+                                      val.data_ptr(), pos.data_ptr(), _stream_ptr(stream)))
+    return val, pos
+
+
+def range_scan(data: torch.Tensor, offsets, lengths, targets, cmp: str, stream=None) -> torch.Tensor:
+    """§4.2 on many regions: first matching offset per region (region length if none)."""
+    data = _dev_u8(data)
+    off, ln = _regions(offsets, lengths, data.device)
+    tg = torch.as_tensor(np.asarray(targets, dtype=np.uint8)).to(data.device)
+    n = off.numel()
+    pos = torch.empty(n, dtype=torch.int64, device=data.device)
+    check(lib.cdc_range_scan(data.data_ptr(), off.data_ptr(), ln.data_ptr(), tg.data_ptr(), n, CMPS[cmp],
+                             pos.data_ptr(), _stream_ptr(stream)))
+    return pos

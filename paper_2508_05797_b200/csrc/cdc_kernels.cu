@@ -1,0 +1,1083 @@
+// cdc_kernels.cu -- sm_100a kernels and the extern "C" ABI declared in include/cdc_b200.h.
+//
+// Pipeline of one cdc_chunk / cdc_chunk_batch call:
+//   K0 k_seg_prefix  (batch only) segment table: nseg_f = ceil(L_f / S), prefix sums
+//   K1 k_speculate   one warp per segment g: starts a chunk at the segment's first
+//                    byte (speculation), walks the chain through the segment with a
+//                    TMA-fed shared-memory ring, records the chain's starts (list(g)),
+//                    publishes them (release) for the neighbour, then keeps walking
+//                    past the segment end ("halo") until one of its starts is found
+//                    in a later segment's published list (re-synchronisation: from a
+//                    common start on, two chains are identical), the stream ends, or
+//                    the halo exceeds its cap.
+//   K2 k_resolve     one CTA: re-checks undecided halos against the complete lists,
+//                    runs fix-up walkers for halos that never met a later chain,
+//                    resolves which segments the true chain passes through (from the
+//                    stream start, following sync points), and scans the per-segment
+//                    output counts.
+//   K3 k_write       one warp per segment: writes its part of the true chain as
+//                    exclusive chunk end offsets (uint64).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/cdc_b200.h"
+#include "cdc_device.cuh"
+
+namespace cdc {
+
+constexpr int SPEC_WARPS = 4;     // warps (segments) per CTA in k_speculate
+constexpr int RESOLVE_THREADS = 1024;
+
+// ------------------------------------------------------------------ workspace
+struct Work {
+    // per segment
+    uint32_t *list;              // G x cap_list  starts relative to the segment start
+    uint32_t *halo;              // G x cap_halo  starts relative to the segment end
+    uint32_t *cnt, *hcnt;        // list / halo lengths
+    unsigned long long *pub;     // (epoch << 32) | published list length
+    int32_t *sj;                 // sync target segment, or SJ_* code
+    uint32_t *sa, *sb;           // halo entries before the sync point; its index in list(sj)
+    uint32_t *entry, *tail, *wcnt, *jump_entry;
+    uint64_t *woff;              // walker entries offset into pool
+    uint8_t *skipped;
+    uint64_t *seg_out;           // G+1 exclusive scan of output counts
+    uint32_t *exc;               // compacted exceptional segments
+    uint32_t *ranges;            // skip ranges (pairs)
+    uint64_t *pool;              // walker-produced starts (file relative)
+    uint64_t *seg_first;         // nfiles+1 (batch)
+    uint64_t *file_out;          // nfiles+1 (single stream: internal)
+    uint32_t *misc;              // [0] G, [1] n_exc, [2] n_ranges, [3] overflow flags
+    uint64_t cap_list, cap_halo, pool_cap, max_segs, exc_cap;
+};
+
+enum : int32_t { SJ_UNSYNCED = -1, SJ_STREAM_END = -2, SJ_LAST = -3 };
+
+struct Geometry {
+    const uint8_t *data;
+    const uint64_t *file_off;  // null => single stream of length L
+    uint64_t L;
+    uint64_t nfiles;
+    uint64_t S;      // segment bytes
+    uint64_t Hmax;   // halo cap
+    uint32_t w;
+    uint64_t max_size;
+    unsigned long long epoch;
+};
+
+__device__ __forceinline__ void file_bounds(const Geometry &G, uint64_t f, uint64_t &off, uint64_t &len) {
+    if (G.file_off == nullptr) {
+        off = 0;
+        len = G.L;
+    } else {
+        off = G.file_off[f];
+        len = G.file_off[f + 1] - off;
+    }
+}
+__device__ __forceinline__ uint64_t nseg_of(uint64_t len, uint64_t S) { return (len + S - 1) / S; }
+
+__device__ __forceinline__ void seg_first_of(const Geometry &G, const Work &W, uint64_t f, uint64_t &a,
+                                             uint64_t &b) {
+    if (G.file_off == nullptr) {
+        a = 0;
+        b = nseg_of(G.L, G.S);
+    } else {
+        a = W.seg_first[f];
+        b = W.seg_first[f + 1];
+    }
+}
+__device__ __forceinline__ uint64_t total_segs(const Geometry &G, const Work &W) {
+    return G.file_off == nullptr ? nseg_of(G.L, G.S) : W.seg_first[G.nfiles];
+}
+// file containing segment g: last f with seg_first[f] <= g (files with segments only)
+__device__ __forceinline__ uint64_t file_of_seg(const Geometry &G, const Work &W, uint64_t g) {
+    if (G.file_off == nullptr) return 0;
+    uint64_t lo = 0, hi = G.nfiles;  // seg_first[lo] <= g < seg_first[hi]
+    while (hi - lo > 1) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (W.seg_first[mid] <= g) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+struct SegInfo {
+    uint64_t g, f, first, last;  // segment, file, file's first and last segment
+    uint64_t foff, Lf;           // file offset in data and length
+    int64_t p, seg_end;          // segment [p, seg_end) within the file
+};
+__device__ __forceinline__ SegInfo seg_info(const Geometry &G, const Work &W, uint64_t g) {
+    SegInfo I;
+    I.g = g;
+    I.f = file_of_seg(G, W, g);
+    uint64_t a, b;
+    seg_first_of(G, W, I.f, a, b);
+    I.first = a;
+    I.last = b - 1;
+    file_bounds(G, I.f, I.foff, I.Lf);
+    I.p = (int64_t)((g - a) * G.S);
+    int64_t e = I.p + (int64_t)G.S;
+    I.seg_end = e < (int64_t)I.Lf ? e : (int64_t)I.Lf;
+    return I;
+}
+
+// warp-cooperative membership of value r in a sorted list prefix lst[0..c), with a
+// monotone cursor: returns 1 found (idx set), 0 not a member, -1 undecidable
+// (every entry of the prefix is < r).
+__device__ __forceinline__ int list_lookup(const uint32_t *lst, uint32_t c, uint32_t r, uint32_t &cursor,
+                                           uint32_t &idx) {
+    const int lane = lane_id();
+    while (cursor < c) {
+        uint32_t i = cursor + lane;
+        bool valid = i < c;
+        uint32_t v = valid ? __ldcg(lst + i) : 0u;
+        uint32_t bal = __ballot_sync(0xFFFFFFFFu, valid && v >= r);
+        if (bal) {
+            int L = __ffs(bal) - 1;
+            uint32_t vL = __shfl_sync(0xFFFFFFFFu, v, L);
+            cursor += L;
+            if (vL == r) {
+                idx = cursor;
+                return 1;
+            }
+            return 0;
+        }
+        cursor = (c - cursor > 32u) ? cursor + 32u : c;
+    }
+    return -1;
+}
+
+// ------------------------------------------------------------------ K1 emit policy
+struct SpecEmit {
+    const Geometry *G;
+    const Work *W;
+    SegInfo I;
+    uint32_t *list, *halo;
+    unsigned long long *pub;
+    uint32_t cnt, hcnt;
+    int32_t sj;
+    uint32_t sa, sb;
+    int64_t cur_j;
+    uint32_t cursor;
+
+    __device__ bool boundary(int64_t e) {
+        const int lane = lane_id();
+        if (e < I.seg_end) {
+            if (lane == 0) {
+                list[cnt] = (uint32_t)(e - I.p);
+                st_release_u64(pub, (G->epoch << 32) | (unsigned long long)(cnt + 1));
+            }
+            ++cnt;
+            return false;
+        }
+        const uint32_t h = (uint32_t)(e - I.seg_end);
+        if (lane == 0) halo[hcnt] = h;
+        ++hcnt;
+        // re-synchronisation: is e a start of the chain of the segment holding it?
+        const int64_t j = (int64_t)I.g + 1 + (e - I.seg_end) / (int64_t)G->S;
+        if (j != cur_j) {
+            cur_j = j;
+            cursor = 0;
+        }
+        const int64_t pj = I.seg_end + (j - (int64_t)I.g - 1) * (int64_t)G->S;
+        const unsigned long long pw = ld_acquire_u64(W->pub + j);
+        if ((pw >> 32) == G->epoch) {
+            const uint32_t c = (uint32_t)(pw & 0xFFFFFFFFull);
+            uint32_t idx = 0;
+            int r = list_lookup(W->list + (uint64_t)j * W->cap_list, c, (uint32_t)(e - pj), cursor, idx);
+            if (r == 1) {
+                sj = (int32_t)j;
+                sa = hcnt - 1;
+                sb = idx;
+                return true;
+            }
+        }
+        if ((uint64_t)h >= G->Hmax) {
+            sj = SJ_UNSYNCED;
+            return true;
+        }
+        return false;
+    }
+    __device__ void end() { sj = (I.seg_end >= (int64_t)I.Lf) ? SJ_LAST : SJ_STREAM_END; }
+};
+
+template <int ALGO>
+__global__ void __launch_bounds__(SPEC_WARPS * 32) k_speculate(Geometry G, Work W) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int warp = threadIdx.x >> 5;
+    const uint64_t g = (uint64_t)blockIdx.x * SPEC_WARPS + warp;
+    const uint64_t nsegs = total_segs(G, W);
+    if (g >= nsegs) return;
+    uint8_t *wbase = smem + warp * RING_SMEM;
+    WarpRing R{wbase, reinterpret_cast<uint64_t *>(wbase + RING_BYTES)};
+
+    SpecEmit em;
+    em.G = &G;
+    em.W = &W;
+    em.I = seg_info(G, W, g);
+    em.list = W.list + g * W.cap_list;
+    em.halo = W.halo + g * W.cap_halo;
+    em.pub = W.pub + g;
+    em.cnt = 1;
+    em.hcnt = 0;
+    em.sj = SJ_UNSYNCED;
+    em.sa = em.sb = 0;
+    em.cur_j = -1;
+    em.cursor = 0;
+    if (lane_id() == 0) {
+        em.list[0] = 0;  // the speculative chain starts at the segment's first byte
+        st_release_u64(em.pub, (G.epoch << 32) | 1ull);
+    }
+    const uint8_t *fbase = G.data + em.I.foff;
+    int64_t read_end = (g == em.I.last) ? (int64_t)em.I.Lf
+                                        : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
+    run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, l2_evict_first_policy(), em);
+    if (lane_id() == 0) {
+        W.cnt[g] = em.cnt;
+        W.hcnt[g] = em.hcnt;
+        W.sj[g] = em.sj;
+        W.sa[g] = em.sa;
+        W.sb[g] = em.sb;
+    }
+}
+
+// ------------------------------------------------------------------ K2 walker emit
+struct WalkEmit {
+    const Geometry *G;
+    const Work *W;
+    SegInfo I;        // segment whose chain is being continued
+    uint64_t base;    // first pool slot of this walker
+    uint64_t n;       // entries written
+    int32_t sj;
+    uint32_t sb;
+    int64_t cur_j;
+    uint32_t cursor;
+    bool overflow;
+
+    __device__ bool boundary(int64_t e) {
+        const int64_t j = (int64_t)I.g + 1 + (e - I.seg_end) / (int64_t)G->S;
+        if (j != cur_j) {
+            cur_j = j;
+            cursor = 0;
+        }
+        const int64_t pj = I.seg_end + (j - (int64_t)I.g - 1) * (int64_t)G->S;
+        uint32_t idx = 0;
+        int r = list_lookup(W->list + (uint64_t)j * W->cap_list, W->cnt[j], (uint32_t)(e - pj), cursor, idx);
+        if (r == 1) {
+            sj = (int32_t)j;
+            sb = idx;
+            return true;
+        }
+        if (base + n >= W->pool_cap) {
+            overflow = true;
+            return true;
+        }
+        if (lane_id() == 0) W->pool[base + n] = (uint64_t)e;
+        ++n;
+        return false;
+    }
+    __device__ void end() { sj = SJ_STREAM_END; }
+};
+
+// block-wide exclusive scan helper (1024 threads)
+__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t &total, uint64_t *scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) scratch[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t s = lane < nw ? scratch[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint64_t y = __shfl_up_sync(0xFFFFFFFFu, s, o);
+            if (lane >= o) s += y;
+        }
+        scratch[32 + lane] = s;
+    }
+    __syncthreads();
+    uint64_t warp_prefix = warp ? scratch[32 + warp - 1] : 0;
+    total = scratch[32 + nw - 1];
+    __syncthreads();
+    return warp_prefix + x - v;
+}
+
+template <int ALGO>
+__global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W, uint64_t *d_count,
+                                                             uint64_t *file_out) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t scratch[64];
+    __shared__ uint64_t s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const uint64_t nsegs = total_segs(G, W);
+
+    // 1. halos left undecided by K1: every list is complete now
+    for (uint64_t g = warp; g < nsegs; g += nwarps) {
+        if (W.sj[g] != SJ_UNSYNCED) continue;
+        SegInfo I = seg_info(G, W, g);
+        const uint32_t hc = W.hcnt[g];
+        int64_t cur_j = -1;
+        uint32_t cursor = 0;
+        for (uint32_t i = 0; i < hc; ++i) {
+            const int64_t e = I.seg_end + (int64_t)W.halo[g * W.cap_halo + i];
+            const int64_t j = (int64_t)g + 1 + (e - I.seg_end) / (int64_t)G.S;
+            if (j != cur_j) {
+                cur_j = j;
+                cursor = 0;
+            }
+            const int64_t pj = I.seg_end + (j - (int64_t)g - 1) * (int64_t)G.S;
+            uint32_t idx = 0;
+            if (list_lookup(W.list + (uint64_t)j * W.cap_list, W.cnt[j], (uint32_t)(e - pj), cursor, idx) == 1) {
+                if (lane == 0) {
+                    W.sj[g] = (int32_t)j;
+                    W.sa[g] = i;
+                    W.sb[g] = idx;
+                }
+                break;
+            }
+        }
+    }
+    for (uint64_t g = tid; g < nsegs; g += blockDim.x) {
+        W.skipped[g] = 0;
+        W.wcnt[g] = 0;
+        W.jump_entry[g] = 0;
+    }
+    __syncthreads();
+
+    // 2. compact the exceptional segments (sync target other than the next segment) in order
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (uint64_t base = 0; base < nsegs; base += blockDim.x) {
+        uint64_t g = base + tid;
+        uint64_t flag = 0;
+        if (g < nsegs) {
+            int32_t sj = W.sj[g];
+            flag = (sj != SJ_LAST && sj != (int32_t)(g + 1)) ? 1 : 0;
+        }
+        uint64_t tot;
+        uint64_t pos = block_exclusive_scan(flag, tot, scratch) + s_carry;
+        if (flag && pos < W.exc_cap) W.exc[pos] = (uint32_t)g;
+        __syncthreads();
+        if (tid == 0) s_carry += tot;
+        __syncthreads();
+    }
+    const uint64_t n_exc = s_carry;
+
+    // 3. serial resolution of the exceptional segments on the true chain (warp 0);
+    //    unsynced halos are continued by a walker until they meet a later chain
+    if (warp == 0) {
+        WarpRing R{smem, reinterpret_cast<uint64_t *>(smem + RING_BYTES)};
+        uint64_t reach = 0, nranges = 0, pool_used = 0;
+        bool overflow = n_exc > W.exc_cap;
+        for (uint64_t x = 0; x < n_exc && x < W.exc_cap; ++x) {
+            const uint64_t g = W.exc[x];
+            if (g < reach) continue;  // skipped by an earlier jump: not on the true chain
+            SegInfo I = seg_info(G, W, g);
+            int32_t sj = W.sj[g];
+            if (sj == SJ_UNSYNCED) {
+                WalkEmit em;
+                em.G = &G;
+                em.W = &W;
+                em.I = I;
+                em.base = pool_used;
+                em.n = 0;
+                em.sj = SJ_STREAM_END;
+                em.sb = 0;
+                em.cur_j = -1;
+                em.cursor = 0;
+                em.overflow = false;
+                const int64_t last = I.seg_end + (int64_t)W.halo[g * W.cap_halo + W.hcnt[g] - 1];
+                run_chain<ALGO>(R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
+                                l2_evict_first_policy(), em);
+                overflow |= em.overflow;
+                sj = em.sj;
+                if (lane == 0) {
+                    W.sj[g] = sj;
+                    W.sa[g] = W.hcnt[g];
+                    W.sb[g] = em.sb;
+                    W.wcnt[g] = (uint32_t)em.n;
+                    W.woff[g] = em.base;
+                }
+                pool_used += em.n;
+                if (sj == (int32_t)(g + 1)) continue;  // met the next segment's chain: no skip
+            }
+            const uint64_t target = (sj == SJ_STREAM_END) ? I.last + 1 : (uint64_t)sj;
+            if (lane == 0) {
+                W.ranges[2 * nranges] = (uint32_t)(g + 1);
+                W.ranges[2 * nranges + 1] = (uint32_t)target;
+                if (sj >= 0) W.jump_entry[target] = W.sb[g];
+            }
+            ++nranges;
+            reach = target;
+        }
+        if (lane == 0) {
+            W.misc[2] = (uint32_t)nranges;
+            W.misc[3] = overflow ? 1u : 0u;
+        }
+    }
+    __syncthreads();
+
+    // 4. mark segments the true chain jumps over
+    const uint32_t nranges = W.misc[2];
+    for (uint32_t r = warp; r < nranges; r += nwarps) {
+        const uint32_t a = W.ranges[2 * r], b = W.ranges[2 * r + 1];
+        for (uint32_t g = a + lane; g < b; g += 32) W.skipped[g] = 1;
+    }
+    __syncthreads();
+
+    // 5. per-segment output counts and their exclusive scan
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (uint64_t base = 0; base < nsegs; base += blockDim.x) {
+        const uint64_t g = base + tid;
+        uint64_t n = 0;
+        if (g < nsegs && !W.skipped[g]) {
+            SegInfo I = seg_info(G, W, g);
+            uint32_t e = 0;
+            if (g != I.first) e = W.skipped[g - 1] ? W.jump_entry[g] : W.sb[g - 1];
+            const int32_t sj = W.sj[g];
+            uint32_t tail = 0;
+            if (sj == SJ_STREAM_END) tail = W.hcnt[g];
+            else if (sj >= 0) tail = W.sa[g];
+            W.entry[g] = e;
+            W.tail[g] = tail;
+            n = (uint64_t)(W.cnt[g] - e) + tail + W.wcnt[g];
+        }
+        uint64_t tot;
+        uint64_t pos = block_exclusive_scan(n, tot, scratch) + s_carry;
+        if (g < nsegs) W.seg_out[g] = pos;
+        __syncthreads();
+        if (tid == 0) s_carry += tot;
+        __syncthreads();
+    }
+    const uint64_t total = s_carry;
+    if (tid == 0) {
+        W.seg_out[nsegs] = total;
+        *d_count = total;
+    }
+    // 6. per-file output offsets
+    const uint64_t nf = G.file_off == nullptr ? 1 : G.nfiles;
+    for (uint64_t f = tid; f <= nf; f += blockDim.x) {
+        uint64_t sf = (G.file_off == nullptr) ? (f == 0 ? 0 : nsegs) : W.seg_first[f];
+        file_out[f] = (sf >= nsegs) ? total : W.seg_out[sf];
+    }
+}
+
+// ------------------------------------------------------------------ K3 write
+__global__ void k_write(Geometry G, Work W, const uint64_t *file_out, uint64_t *bounds, uint64_t cap) {
+    const uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    const uint64_t nsegs = total_segs(G, W);
+    if (g >= nsegs) return;
+    SegInfo I = seg_info(G, W, g);
+    const uint64_t fo = file_out[I.f];
+    if (g == I.first && lane == 0 && I.Lf > 0) {
+        const uint64_t q = file_out[I.f + 1] - 1;  // a stream's last boundary is its length
+        if (q < cap) bounds[q] = I.Lf;
+    }
+    if (W.skipped[g]) return;
+    const uint32_t e = W.entry[g], cnt = W.cnt[g], tail = W.tail[g], wc = W.wcnt[g];
+    const uint64_t A = cnt - e, n = A + tail + wc, base = W.seg_out[g];
+    const uint32_t *lst = W.list + g * W.cap_list;
+    const uint32_t *hl = W.halo + g * W.cap_halo;
+    for (uint64_t i = lane; i < n; i += 32) {
+        uint64_t v;
+        if (i < A) v = (uint64_t)I.p + lst[e + i];
+        else if (i < A + tail) v = (uint64_t)I.seg_end + hl[i - A];
+        else v = W.pool[W.woff[g] + (i - A - tail)];
+        const uint64_t q = base + i;
+        if (q == fo) continue;  // the stream's first start (0) is not a boundary
+        if (q - 1 < cap) bounds[q - 1] = v;
+    }
+}
+
+// ------------------------------------------------------------------ K0 batch segment table
+__global__ void __launch_bounds__(RESOLVE_THREADS) k_seg_prefix(const uint64_t *file_off, uint64_t nfiles,
+                                                                uint64_t S, uint64_t *seg_first) {
+    __shared__ uint64_t scratch[64];
+    __shared__ uint64_t s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (uint64_t base = 0; base < nfiles; base += blockDim.x) {
+        const uint64_t f = base + threadIdx.x;
+        uint64_t n = 0;
+        if (f < nfiles) n = nseg_of(file_off[f + 1] - file_off[f], S);
+        uint64_t tot;
+        uint64_t pos = block_exclusive_scan(n, tot, scratch) + s_carry;
+        if (f < nfiles) seg_first[f] = pos;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) seg_first[nfiles] = s_carry;
+}
+
+// ------------------------------------------------------------------ chain API kernel
+struct ChainEmit {
+    uint64_t *out;
+    uint64_t cap, n;
+    int64_t stop;
+    __device__ bool boundary(int64_t e) {
+        if (lane_id() == 0 && n < cap) out[n] = (uint64_t)e;
+        ++n;
+        return e >= stop;
+    }
+    __device__ void end() {}
+};
+
+template <int ALGO>
+__global__ void __launch_bounds__(32) k_chain(const uint8_t *data, uint64_t len, uint64_t start, uint64_t stop,
+                                              uint32_t w, uint64_t max_size, uint64_t *out, uint64_t cap,
+                                              uint64_t *count) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    WarpRing R{smem, reinterpret_cast<uint64_t *>(smem + RING_BYTES)};
+    ChainEmit em{out, cap, 0, (int64_t)stop};
+    if (lane_id() == 0 && cap > 0) out[0] = start;
+    em.n = 1;
+    if (start < stop && start < len)
+        run_chain<ALGO>(R, data, (int64_t)len, (int64_t)start, (int64_t)len, w, max_size, l2_evict_first_policy(),
+                        em);
+    if (lane_id() == 0) *count = em.n;
+}
+
+// ------------------------------------------------------------------ primitives (§4.1, §4.2)
+// Region bytes are read with 16-byte aligned loads; bytes outside the region are masked.
+template <bool MAX>
+__global__ void k_ebs(const uint8_t *data, const uint64_t *off, const uint64_t *len, uint64_t n, uint8_t *value,
+                      uint64_t *pos) {
+    const uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    if (r >= n) return;
+    const uint8_t *b = data + off[r];
+    const uint64_t L = len[r];
+    const uint8_t *a0 = reinterpret_cast<const uint8_t *>(reinterpret_cast<uintptr_t>(b) & ~(uintptr_t)15);
+    const int64_t lo = b - a0, hi = lo + (int64_t)L;  // region = [lo, hi) relative to a0
+    uint32_t ah = acc_init<MAX>(), al = acc_init<MAX>();
+    for (int64_t blk = 0; blk < hi; blk += 512) {
+        const int64_t base = blk + lane * 16;
+        uint32_t bits = range_bits(lo - blk > 0 ? (int)(lo - blk) : 0, hi - blk < 512 ? (int)(hi - blk) : 512, lane * 16);
+        if (bits) {
+            uint4 v = *reinterpret_cast<const uint4 *>(a0 + base);
+            acc16<MAX>(mask_bytes(v, bits, MAX), ah, al);
+        }
+    }
+    const uint32_t m = warp_extreme<MAX>(acc_extreme<MAX>(ah, al));
+    // leftmost occurrence: Range Scan with EQ
+    for (int64_t blk = 0; blk < hi; blk += 512) {
+        const int64_t base = blk + lane * 16;
+        uint32_t bits = range_bits(lo - blk > 0 ? (int)(lo - blk) : 0, hi - blk < 512 ? (int)(hi - blk) : 512, lane * 16);
+        uint32_t hit = 0;
+        if (bits) hit = pred_bits16<CMP_EQ>(*reinterpret_cast<const uint4 *>(a0 + base), m) & bits;
+        uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit != 0);
+        if (bal) {
+            int Ln = __ffs(bal) - 1;
+            uint32_t mb = __shfl_sync(0xFFFFFFFFu, hit, Ln);
+            if (lane == 0) {
+                value[r] = (uint8_t)m;
+                pos[r] = (uint64_t)(blk + Ln * 16 + (__ffs(mb) - 1) - lo);
+            }
+            return;
+        }
+    }
+}
+
+template <int CMP>
+__global__ void k_range_scan(const uint8_t *data, const uint64_t *off, const uint64_t *len, const uint8_t *target,
+                             uint64_t n, uint64_t *pos) {
+    const uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    if (r >= n) return;
+    const uint8_t *b = data + off[r];
+    const uint64_t L = len[r];
+    const uint32_t t = target[r];
+    const uint8_t *a0 = reinterpret_cast<const uint8_t *>(reinterpret_cast<uintptr_t>(b) & ~(uintptr_t)15);
+    const int64_t lo = b - a0, hi = lo + (int64_t)L;
+    for (int64_t blk = 0; blk < hi; blk += 512) {
+        const int64_t base = blk + lane * 16;
+        uint32_t bits = range_bits(lo - blk > 0 ? (int)(lo - blk) : 0, hi - blk < 512 ? (int)(hi - blk) : 512, lane * 16);
+        uint32_t hit = 0;
+        if (bits) hit = pred_bits16<CMP>(*reinterpret_cast<const uint4 *>(a0 + base), t) & bits;
+        uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit != 0);
+        if (bal) {
+            int Ln = __ffs(bal) - 1;
+            uint32_t mb = __shfl_sync(0xFFFFFFFFu, hit, Ln);
+            if (lane == 0) pos[r] = (uint64_t)(blk + Ln * 16 + (__ffs(mb) - 1) - lo);
+            return;
+        }
+    }
+    if (lane == 0) pos[r] = L;
+}
+
+}  // namespace cdc
+
+// ====================================================================== host side
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+// Optional per-kernel timing (cdc_profile_*): CUDA events recorded on the
+// launching stream around each pipeline kernel of cdc_chunk / cdc_chunk_batch.
+constexpr int PROF_KERNELS = 4;  // k_seg_prefix, k_speculate, k_resolve, k_write
+struct ProfCall {
+    cudaEvent_t ev[PROF_KERNELS + 1];
+    bool used[PROF_KERNELS];
+};
+thread_local bool g_prof_on = false;
+thread_local std::vector<ProfCall> g_prof_calls;
+thread_local std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {
+    cudaEvent_t e;
+    if (!g_prof_pool.empty()) {
+        e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+    } else {
+        cudaEventCreate(&e);
+    }
+    return e;
+}
+std::mutex g_mu;
+unsigned long long g_epoch = 0;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char *where) {
+    return fail(CDC_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CDC_CUDA(call)                                   \
+    do {                                                 \
+        cudaError_t _e = (call);                         \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+int check_params(const cdc_params *p) {
+    if (!p) return fail(CDC_ERR_INVALID, "null params");
+    if (p->algo < CDC_RAM || p->algo > CDC_AE_MIN) return fail(CDC_ERR_INVALID, "unknown algorithm");
+    if (p->window < 1) return fail(CDC_ERR_INVALID, "window must be >= 1");
+    if (p->max_size <= p->window) return fail(CDC_ERR_INVALID, "max_size must exceed window");
+    if (p->seg_bytes % cdc::STAGE) return fail(CDC_ERR_INVALID, "seg_bytes must be a multiple of 2048");
+    if (p->seg_bytes && p->seg_bytes >= (1ull << 31)) return fail(CDC_ERR_INVALID, "seg_bytes too large");
+    if (p->halo_bytes >= (1ull << 31)) return fail(CDC_ERR_INVALID, "halo_bytes too large");
+    return CDC_OK;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+struct Plan {
+    uint64_t S, Hmax, max_segs, cap_list, cap_halo, pool_cap, exc_cap, nfiles;
+    size_t bytes;
+    size_t off[24];
+};
+
+uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// Segment size: about SEGS_PER_SM segments per SM for the total input, at least
+// 64 KiB and 4 max-size chunks, so that the re-synchronisation halo (a few chunks
+// on typical data) is small next to the segment.
+constexpr uint64_t SEGS_PER_SM = 4;
+
+void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, Plan &P) {
+    uint64_t S = p->seg_bytes;
+    if (!S) {
+        uint64_t target = (uint64_t)num_sms() * SEGS_PER_SM;
+        S = round_up(total_len / target + 1, 64 << 10);
+        uint64_t lo = std::max<uint64_t>(64 << 10, round_up(4 * p->max_size, cdc::STAGE));
+        if (S < lo) S = lo;
+        if (S > (256ull << 20)) S = 256ull << 20;
+    }
+    uint64_t H = p->halo_bytes ? p->halo_bytes : std::max<uint64_t>(2 * S, 64ull * (p->window + 1));
+    if (H >= (1ull << 31)) H = (1ull << 31) - 1;
+    P.S = S;
+    P.Hmax = H;
+    P.nfiles = nfiles;
+    P.max_segs = (nfiles <= 1) ? (max_len + S - 1) / S + 1 : total_len / S + nfiles + 1;
+    P.cap_list = S / (p->window + 1) + 2;
+    P.cap_halo = H / (p->window + 1) + 3;
+    P.pool_cap = total_len / (p->window + 1) + 2;
+    P.exc_cap = P.max_segs;
+    const uint64_t G = P.max_segs;
+    size_t sz[] = {
+        G * P.cap_list * 4,  // 0 list
+        G * P.cap_halo * 4,  // 1 halo
+        G * 4,               // 2 cnt
+        G * 4,               // 3 hcnt
+        G * 8,               // 4 pub
+        G * 4,               // 5 sj
+        G * 4,               // 6 sa
+        G * 4,               // 7 sb
+        G * 4,               // 8 entry
+        G * 4,               // 9 tail
+        G * 4,               // 10 wcnt
+        G * 4,               // 11 jump_entry
+        G * 8,               // 12 woff
+        G,                   // 13 skipped
+        (G + 1) * 8,         // 14 seg_out
+        G * 4,               // 15 exc
+        G * 8,               // 16 ranges
+        P.pool_cap * 8,      // 17 pool
+        (nfiles + 1) * 8,    // 18 seg_first
+        (nfiles + 1) * 8,    // 19 file_out
+        64,                  // 20 misc
+    };
+    size_t o = 0;
+    for (int i = 0; i < 21; ++i) {
+        P.off[i] = o;
+        o += round_up(sz[i], 256);
+    }
+    P.bytes = o;
+}
+
+cdc::Work carve(const Plan &P, void *ws) {
+    uint8_t *b = static_cast<uint8_t *>(ws);
+    cdc::Work W;
+    W.list = (uint32_t *)(b + P.off[0]);
+    W.halo = (uint32_t *)(b + P.off[1]);
+    W.cnt = (uint32_t *)(b + P.off[2]);
+    W.hcnt = (uint32_t *)(b + P.off[3]);
+    W.pub = (unsigned long long *)(b + P.off[4]);
+    W.sj = (int32_t *)(b + P.off[5]);
+    W.sa = (uint32_t *)(b + P.off[6]);
+    W.sb = (uint32_t *)(b + P.off[7]);
+    W.entry = (uint32_t *)(b + P.off[8]);
+    W.tail = (uint32_t *)(b + P.off[9]);
+    W.wcnt = (uint32_t *)(b + P.off[10]);
+    W.jump_entry = (uint32_t *)(b + P.off[11]);
+    W.woff = (uint64_t *)(b + P.off[12]);
+    W.skipped = (uint8_t *)(b + P.off[13]);
+    W.seg_out = (uint64_t *)(b + P.off[14]);
+    W.exc = (uint32_t *)(b + P.off[15]);
+    W.ranges = (uint32_t *)(b + P.off[16]);
+    W.pool = (uint64_t *)(b + P.off[17]);
+    W.seg_first = (uint64_t *)(b + P.off[18]);
+    W.file_out = (uint64_t *)(b + P.off[19]);
+    W.misc = (uint32_t *)(b + P.off[20]);
+    W.cap_list = P.cap_list;
+    W.cap_halo = P.cap_halo;
+    W.pool_cap = P.pool_cap;
+    W.max_segs = P.max_segs;
+    W.exc_cap = P.exc_cap;
+    return W;
+}
+
+template <int ALGO>
+int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::Work &W, uint64_t *d_bounds,
+                    uint64_t cap, uint64_t *d_count, uint64_t *file_out, cudaStream_t st, bool batch) {
+    static bool attr_set = false;
+    const int spec_smem = cdc::SPEC_WARPS * cdc::RING_SMEM;
+    if (!attr_set) {
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, spec_smem));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_resolve<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      cdc::RING_SMEM));
+        attr_set = true;
+    }
+    int launches = 0;
+    ProfCall pc{};
+    auto mark = [&](int i) {
+        if (g_prof_on) {
+            pc.ev[i] = prof_event();
+            cudaEventRecord(pc.ev[i], st);
+        }
+    };
+    mark(0);
+    if (batch) {
+        cdc::k_seg_prefix<<<1, cdc::RESOLVE_THREADS, 0, st>>>(G.file_off, G.nfiles, G.S, W.seg_first);
+        ++launches;
+        pc.used[0] = true;
+    }
+    mark(1);
+    const uint64_t nseg_ub = P.max_segs;
+    const uint64_t blocks = (nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS;
+    if (blocks > 0) {
+        cdc::k_speculate<ALGO><<<(unsigned)blocks, cdc::SPEC_WARPS * 32, spec_smem, st>>>(G, W);
+        ++launches;
+        pc.used[1] = true;
+    }
+    mark(2);
+    cdc::k_resolve<ALGO><<<1, cdc::RESOLVE_THREADS, cdc::RING_SMEM, st>>>(G, W, d_count, file_out);
+    ++launches;
+    pc.used[2] = true;
+    mark(3);
+    const uint64_t wthreads = nseg_ub * 32;
+    if (wthreads > 0) {
+        cdc::k_write<<<(unsigned)((wthreads + 255) / 256), 256, 0, st>>>(G, W, file_out, d_bounds, cap);
+        ++launches;
+        pc.used[3] = true;
+    }
+    mark(4);
+    if (g_prof_on) g_prof_calls.push_back(pc);
+    g_launches = launches;
+    CDC_CUDA(cudaGetLastError());
+    return CDC_OK;
+}
+
+int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file_off, uint64_t nfiles,
+              uint64_t total_len, uint64_t max_len, uint64_t *d_bounds, uint64_t cap, uint64_t *d_bound_off,
+              uint64_t *d_count, void *ws, size_t ws_bytes, void *stream, bool batch) {
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!d_count || (!d_bounds && cap) || (total_len && !d_data) || !ws)
+        return fail(CDC_ERR_INVALID, "null pointer argument");
+    if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(CDC_ERR_INVALID, "workspace must be 256-byte aligned");
+    Plan P;
+    make_plan(p, nfiles, total_len, max_len, P);
+    if (ws_bytes < P.bytes) return fail(CDC_ERR_WORKSPACE, "workspace too small");
+    cdc::Work W = carve(P, ws);
+    cdc::Geometry G;
+    G.data = d_data;
+    G.file_off = batch ? d_file_off : nullptr;
+    G.L = batch ? 0 : total_len;
+    G.nfiles = batch ? nfiles : 1;
+    G.S = P.S;
+    G.Hmax = P.Hmax;
+    G.w = p->window;
+    G.max_size = p->max_size;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        G.epoch = (++g_epoch) & 0xFFFFFFFFull;
+        if (G.epoch == 0) G.epoch = ++g_epoch & 0xFFFFFFFFull;
+    }
+    uint64_t *file_out = batch ? d_bound_off : W.file_out;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (p->algo) {
+    case CDC_RAM: return launch_pipeline<cdc::ALGO_RAM>(p, P, G, W, d_bounds, cap, d_count, file_out, st, batch);
+    case CDC_AE_MAX: return launch_pipeline<cdc::ALGO_AE_MAX>(p, P, G, W, d_bounds, cap, d_count, file_out, st, batch);
+    default: return launch_pipeline<cdc::ALGO_AE_MIN>(p, P, G, W, d_bounds, cap, d_count, file_out, st, batch);
+    }
+}
+
+// cached device buffers for cdc_chunk_host
+struct HostCache {
+    int dev = -1;
+    uint8_t *data = nullptr;
+    size_t data_cap = 0;
+    uint64_t *bounds = nullptr;
+    size_t bounds_cap = 0;
+    void *ws = nullptr;
+    size_t ws_cap = 0;
+    uint64_t *count = nullptr;
+    cudaStream_t st = nullptr;
+};
+thread_local HostCache g_hc;
+
+int ensure(void **p, size_t &cap, size_t need) {
+    if (cap >= need && *p) return CDC_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    cap = 0;
+    CDC_CUDA(cudaMalloc(p, need ? need : 16));
+    cap = need;
+    return CDC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cdc_abi_version(void) { return CDC_ABI_VERSION; }
+
+const char *cdc_last_error(void) { return g_err.c_str(); }
+
+int cdc_last_launch_count(void) { return g_launches; }
+
+int cdc_profile_enable(int on) {
+    g_prof_on = on != 0;
+    return CDC_OK;
+}
+
+int cdc_profile_collect(double *ms_sum, uint64_t *launches, uint64_t *calls) {
+    if (!ms_sum || !launches || !calls) return fail(CDC_ERR_INVALID, "null pointer");
+    for (int k = 0; k < PROF_KERNELS; ++k) {
+        ms_sum[k] = 0.0;
+        launches[k] = 0;
+    }
+    *calls = g_prof_calls.size();
+    for (ProfCall &pc : g_prof_calls) {
+        CDC_CUDA(cudaEventSynchronize(pc.ev[PROF_KERNELS]));
+        for (int k = 0; k < PROF_KERNELS; ++k) {
+            if (!pc.used[k]) continue;
+            float ms = 0.f;
+            CDC_CUDA(cudaEventElapsedTime(&ms, pc.ev[k], pc.ev[k + 1]));
+            ms_sum[k] += ms;
+            launches[k] += 1;
+        }
+        for (int k = 0; k <= PROF_KERNELS; ++k) g_prof_pool.push_back(pc.ev[k]);
+    }
+    g_prof_calls.clear();
+    return CDC_OK;
+}
+
+int cdc_window_for_avg(int32_t algo, uint64_t avg_size, uint32_t *window) {
+    if (!window) return fail(CDC_ERR_INVALID, "null window");
+    if (algo < CDC_RAM || algo > CDC_AE_MIN) return fail(CDC_ERR_INVALID, "unknown algorithm");
+    if (avg_size < 2 || avg_size > (1ull << 31)) return fail(CDC_ERR_INVALID, "avg_size out of range");
+    *window = (uint32_t)(avg_size >= 512 ? avg_size - 256 : avg_size / 2);
+    return CDC_OK;
+}
+
+int cdc_params_default(cdc_params *p, int32_t algo, uint64_t avg_size) {
+    if (!p) return fail(CDC_ERR_INVALID, "null params");
+    uint32_t w;
+    int rc = cdc_window_for_avg(algo, avg_size, &w);
+    if (rc) return rc;
+    p->algo = algo;
+    p->window = w;
+    p->max_size = 4 * avg_size;
+    p->seg_bytes = 0;
+    p->halo_bytes = 0;
+    return CDC_OK;
+}
+
+uint64_t cdc_max_boundaries(const cdc_params *p, uint64_t len) {
+    if (!p || p->window < 1) return 0;
+    return len / ((uint64_t)p->window + 1) + 1;
+}
+
+int cdc_workspace_size(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, size_t *bytes) {
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!bytes) return fail(CDC_ERR_INVALID, "null bytes");
+    Plan P;
+    make_plan(p, nfiles ? nfiles : 1, total_len, max_len, P);
+    *bytes = P.bytes;
+    return CDC_OK;
+}
+
+int cdc_chunk(const cdc_params *p, const uint8_t *d_data, uint64_t len, uint64_t *d_bounds, uint64_t bounds_cap,
+              uint64_t *d_count, void *d_workspace, size_t workspace_bytes, void *stream) {
+    return run_chunk(p, d_data, nullptr, 1, len, len, d_bounds, bounds_cap, nullptr, d_count, d_workspace,
+                     workspace_bytes, stream, false);
+}
+
+int cdc_chunk_batch(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file_offsets, uint64_t nfiles,
+                    uint64_t total_len, uint64_t max_len, uint64_t *d_bounds, uint64_t bounds_cap,
+                    uint64_t *d_bound_offsets, uint64_t *d_count, void *d_workspace, size_t workspace_bytes,
+                    void *stream) {
+    if (!d_file_offsets || !d_bound_offsets) return fail(CDC_ERR_INVALID, "null offsets");
+    if (nfiles == 0) return fail(CDC_ERR_INVALID, "nfiles must be >= 1");
+    return run_chunk(p, d_data, d_file_offsets, nfiles, total_len, max_len, d_bounds, bounds_cap, d_bound_offsets,
+                     d_count, d_workspace, workspace_bytes, stream, true);
+}
+
+int cdc_chunk_host(const cdc_params *p, const uint8_t *h_data, uint64_t len, uint64_t *h_bounds,
+                   uint64_t bounds_cap, uint64_t *h_count) {
+    int rc = check_params(p);
+    if (rc) return rc;
+    if ((!h_data && len) || !h_count || (!h_bounds && bounds_cap)) return fail(CDC_ERR_INVALID, "null pointer");
+    HostCache &C = g_hc;
+    int dev = 0;
+    CDC_CUDA(cudaGetDevice(&dev));
+    if (C.dev != dev) {
+        C = HostCache();
+        C.dev = dev;
+        CDC_CUDA(cudaStreamCreateWithFlags(&C.st, cudaStreamNonBlocking));
+    }
+    size_t wsb = 0;
+    if ((rc = cdc_workspace_size(p, 1, len, len, &wsb))) return rc;
+    const uint64_t maxb = cdc_max_boundaries(p, len);
+    if ((rc = ensure((void **)&C.data, C.data_cap, len + 32))) return rc;
+    if ((rc = ensure((void **)&C.bounds, C.bounds_cap, maxb * 8))) return rc;
+    if ((rc = ensure(&C.ws, C.ws_cap, wsb))) return rc;
+    if (!C.count) CDC_CUDA(cudaMalloc(&C.count, 8));
+    CDC_CUDA(cudaMemcpyAsync(C.data, h_data, len, cudaMemcpyHostToDevice, C.st));
+    if ((rc = cdc_chunk(p, C.data, len, C.bounds, maxb, C.count, C.ws, C.ws_cap, C.st))) return rc;
+    uint64_t n = 0;
+    CDC_CUDA(cudaMemcpyAsync(&n, C.count, 8, cudaMemcpyDeviceToHost, C.st));
+    CDC_CUDA(cudaStreamSynchronize(C.st));
+    *h_count = n;
+    const uint64_t m = n < bounds_cap ? n : bounds_cap;
+    if (m) {
+        CDC_CUDA(cudaMemcpyAsync(h_bounds, C.bounds, m * 8, cudaMemcpyDeviceToHost, C.st));
+        CDC_CUDA(cudaStreamSynchronize(C.st));
+    }
+    if (n > bounds_cap) return fail(CDC_ERR_CAPACITY, "bounds_cap too small");
+    return CDC_OK;
+}
+
+int cdc_chain(const cdc_params *p, const uint8_t *d_data, uint64_t len, uint64_t start, uint64_t stop,
+              uint64_t *d_starts, uint64_t starts_cap, uint64_t *d_count, void *stream) {
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!d_count || (!d_starts && starts_cap) || (!d_data && len)) return fail(CDC_ERR_INVALID, "null pointer");
+    if (start > len) return fail(CDC_ERR_INVALID, "start beyond len");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    static bool attr = false;
+    if (!attr) {
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM));
+        attr = true;
+    }
+    switch (p->algo) {
+    case CDC_RAM:
+        cdc::k_chain<0><<<1, 32, cdc::RING_SMEM, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
+                                                       starts_cap, d_count);
+        break;
+    case CDC_AE_MAX:
+        cdc::k_chain<1><<<1, 32, cdc::RING_SMEM, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
+                                                       starts_cap, d_count);
+        break;
+    default:
+        cdc::k_chain<2><<<1, 32, cdc::RING_SMEM, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
+                                                       starts_cap, d_count);
+    }
+    g_launches = 1;
+    CDC_CUDA(cudaGetLastError());
+    return CDC_OK;
+}
+
+int cdc_extreme_byte_search(const uint8_t *d_data, const uint64_t *d_off, const uint64_t *d_len, uint64_t n,
+                            int32_t mode, uint8_t *d_value, uint64_t *d_pos, void *stream) {
+    if (n == 0) return CDC_OK;
+    if (!d_data || !d_off || !d_len || !d_value || !d_pos) return fail(CDC_ERR_INVALID, "null pointer");
+    if (mode != CDC_EXT_MAX && mode != CDC_EXT_MIN) return fail(CDC_ERR_INVALID, "bad mode");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned blocks = (unsigned)((n * 32 + 255) / 256);
+    if (mode == CDC_EXT_MAX) cdc::k_ebs<true><<<blocks, 256, 0, st>>>(d_data, d_off, d_len, n, d_value, d_pos);
+    else cdc::k_ebs<false><<<blocks, 256, 0, st>>>(d_data, d_off, d_len, n, d_value, d_pos);
+    g_launches = 1;
+    CDC_CUDA(cudaGetLastError());
+    return CDC_OK;
+}
+
+int cdc_range_scan(const uint8_t *d_data, const uint64_t *d_off, const uint64_t *d_len, const uint8_t *d_target,
+                   uint64_t n, int32_t cmp, uint64_t *d_pos, void *stream) {
+    if (n == 0) return CDC_OK;
+    if (!d_data || !d_off || !d_len || !d_target || !d_pos) return fail(CDC_ERR_INVALID, "null pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned blocks = (unsigned)((n * 32 + 255) / 256);
+    switch (cmp) {
+    case CDC_GT: cdc::k_range_scan<cdc::CMP_GT><<<blocks, 256, 0, st>>>(d_data, d_off, d_len, d_target, n, d_pos); break;
+    case CDC_GEQ: cdc::k_range_scan<cdc::CMP_GEQ><<<blocks, 256, 0, st>>>(d_data, d_off, d_len, d_target, n, d_pos); break;
+    case CDC_LT: cdc::k_range_scan<cdc::CMP_LT><<<blocks, 256, 0, st>>>(d_data, d_off, d_len, d_target, n, d_pos); break;
+    case CDC_LEQ: cdc::k_range_scan<cdc::CMP_LEQ><<<blocks, 256, 0, st>>>(d_data, d_off, d_len, d_target, n, d_pos); break;
+    case CDC_EQ: cdc::k_range_scan<cdc::CMP_EQ><<<blocks, 256, 0, st>>>(d_data, d_off, d_len, d_target, n, d_pos); break;
+    default: return fail(CDC_ERR_INVALID, "bad comparator");
+    }
+    g_launches = 1;
+    CDC_CUDA(cudaGetLastError());
+    return CDC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+"""CPU-only checks of the boundary: the C-ABI library loads and exports every
+symbol include/cdc_b200.h declares; host-only entry points behave (no compute
+calls without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "cdc_b200.h")
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(cdc_[a-z_0-9]+)\s*\(", txt, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_cdc_build", os.path.join(ROOT, "paper_2508_05797_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.build()   # cross-compiles for sm_100a; no GPU needed
+    from paper_2508_05797_b200 import _lib
+    return _lib
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    for s in ["cdc_chunk", "cdc_chunk_batch", "cdc_chunk_host", "cdc_chain", "cdc_extreme_byte_search",
+              "cdc_range_scan", "cdc_workspace_size", "cdc_window_for_avg", "cdc_params_default",
+              "cdc_max_boundaries", "cdc_abi_version", "cdc_last_error", "cdc_last_launch_count"]:
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for s in declared_symbols():
+        assert hasattr(lib.lib, s), s
+    assert lib.lib.cdc_abi_version() == 1
+
+
+def test_host_side_helpers(lib):
+    from paper_2508_05797_b200 import api
+    assert api.window_for_avg("ram", 8192) == 7936
+    assert api.window_for_avg("ae_max", 4096) == 3840
+    assert api.window_for_avg("ram", 300) == 150
+    p = api.params("ae_max", avg_size=4096)
+    assert (p.window, p.max_size) == (3840, 16384)
+    assert api.max_boundaries(p, 0) == 1
+    assert api.max_boundaries(p, 3841 * 10) == 11
+    ws = api.workspace_size(p, 1, 256 << 20, 256 << 20)
+    assert 0 < ws < 64 << 20
+    with pytest.raises(api.CdcError):
+        api.workspace_size(api.params("ram", window=8, max_size=8), 1, 100, 100)
+    with pytest.raises(api.CdcError):
+        api.window_for_avg("ram", 1)
+
+
+def test_invalid_calls_fail_without_gpu(lib):
+    from paper_2508_05797_b200 import api
+    p = api.params("ram", window=8, max_size=64)
+    n = ctypes.c_uint64()
+    # null pointers are rejected before any CUDA call
+    assert lib.lib.cdc_chunk(ctypes.byref(p), None, 0, None, 0, None, None, 0, None) == -1
+    assert lib.lib.cdc_chunk_host(ctypes.byref(p), None, 10, None, 0, ctypes.byref(n)) == -1
+    assert b"null" in lib.lib.cdc_last_error()
