@@ -149,7 +149,8 @@ int cdc_chunk_host(const cdc_params *p, const uint8_t *h_data, uint64_t len,
  * DESIGN.md §6): treats d_data[0..len) as a stream that may continue past
  * `len` (the caller's shard plus its halo), starts a chunk at `start` and
  * writes every chunk start of that chain, beginning with `start`, up to and
- * including the first start >= stop (or until the chain ends at len).
+ * including the first start >= stop; when the chain's last chunk ends at
+ * len before reaching stop, len is written as the final position.
  *   d_starts : device uint64[starts_cap], d_count : device uint64[1].
  * *d_count receives the number written (capped reading as above); the chain
  * ends at len when the last start plus its chunk reaches len.
@@ -192,6 +193,14 @@ int cdc_last_launch_count(void);
  */
 int cdc_profile_enable(int on);
 int cdc_profile_collect(double *ms_sum, uint64_t *launches, uint64_t *calls);
+
+/* Diagnostics.  cdc_profile_query writes, for the 5 events of the last
+ * profiled call (before each of the 4 kernels and after the last), 1 if the
+ * GPU has reached it, 0 if not.  cdc_debug_progress allocates (once) a
+ * host-mapped array of 8192 x 4 uint64 progress words that the kernels then
+ * update as they run, and returns its host address (for diagnosing hangs). */
+int cdc_profile_query(int *done);
+int cdc_debug_progress(void **host_ptr);
 
 #ifdef __cplusplus
 }

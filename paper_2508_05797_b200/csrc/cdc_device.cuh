@@ -15,6 +15,7 @@
 //    that consume each byte once.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace cdc {
@@ -53,8 +54,26 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+__device__ unsigned long long *g_dbg_fwd = nullptr;  // set with g_dbg (debug only)
+// Watchdog: a stage that has not landed within ~10 s (clock64) means a lost
+// bulk copy; record the raw barrier word and trap instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return;
+    const long long t0 = clock64();
+    bool noted = false;
     while (!mbar_try_wait(bar, parity)) {
+        const long long dt = clock64() - t0;
+        if (!noted && dt > 2000000000ll) {
+            noted = true;
+            unsigned long long *p = g_dbg_fwd;
+            if (p) {
+                unsigned long long v;
+                asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(smem_addr(bar)));
+                volatile unsigned long long *q = p + (8191ull * 4);
+                q[0] = 0xBADull; q[1] = v; q[2] = parity; q[3] = ((unsigned long long)blockIdx.x << 32) | threadIdx.x;
+            }
+        }
+        if (dt > 20000000000ll) __trap();
     }
 }
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
@@ -163,6 +182,20 @@ __device__ __forceinline__ uint4 mask_bytes(const uint4 &v, uint32_t bits16, boo
 }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Debug progress words (host-mapped memory set by cdc_debug_progress); null in
+// normal runs.  Slot layout: 4 x u64 per warp: {tag|stage, c, s, aux}.
+__device__ unsigned long long *g_dbg = nullptr;
+__device__ __forceinline__ void dbg_note(uint64_t slot, uint64_t a, uint64_t b, uint64_t c2, uint64_t d) {
+    unsigned long long *p = g_dbg;
+    if (p != nullptr && lane_id() == 0 && slot < 8192) {
+        volatile unsigned long long *q = p + slot * 4;
+        q[0] = a; q[1] = b; q[2] = c2; q[3] = d;
+    }
+}
+__device__ __forceinline__ uint64_t dbg_slot() {
+    return (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5) + (gridDim.x == 1 ? 4096 : 0);
+}
 
 // ---------------------------------------------------------------- warp ring
 struct WarpRing {
@@ -300,9 +333,11 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     int64_t k = 0;
     while (!stop && k < nstages) {
         const int slot = (int)(k % NST);
+        dbg_note(dbg_slot(), (2ull << 56) | (uint64_t)k, (uint64_t)c, (uint64_t)s, (uint64_t)issued);
         mbar_wait(&R.bar[slot], (uint32_t)((k / NST) & 1));
         Step st{R.buf + slot * STAGE, B0 + k * STAGE};
         const int64_t E = st.B + STAGE;
+        dbg_note(dbg_slot(), (1ull << 56) | (uint64_t)k, (uint64_t)c, (uint64_t)s, (uint64_t)nstages);
 
         while (!stop && c < E) {
             if constexpr (ALGO == ALGO_RAM) {
@@ -367,9 +402,17 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
             ++issued;
         }
     }
+    // all bytes up to read_end consumed without the emitter stopping: the walk
+    // reached the end of the stream (read_end == Lf) inside the last chunk
+    if (!stop) {
+        if (c >= Lf) emit.end();
+        else emit.exhausted(c);
+    }
     // drain copies still in flight before the ring is reused or the CTA exits
+    dbg_note(dbg_slot(), (3ull << 56) | (uint64_t)k, (uint64_t)c, (uint64_t)s, (uint64_t)issued);
     for (int64_t j = k; j < issued; ++j) mbar_wait(&R.bar[j % NST], (uint32_t)((j / NST) & 1));
     __syncwarp();
+    dbg_note(dbg_slot(), (4ull << 56) | (uint64_t)k, (uint64_t)c, (uint64_t)s, (uint64_t)issued);
 }
 
 }  // namespace cdc

@@ -187,7 +187,8 @@ struct SpecEmit {
         const int64_t pj = I.seg_end + (j - (int64_t)I.g - 1) * (int64_t)G->S;
         const unsigned long long pw = ld_acquire_u64(W->pub + j);
         if ((pw >> 32) == G->epoch) {
-            const uint32_t c = (uint32_t)(pw & 0xFFFFFFFFull);
+            uint32_t c = (uint32_t)(pw & 0xFFFFFFFFull);
+            if (c > W->cap_list) c = 0;  // never trust a count beyond capacity
             uint32_t idx = 0;
             int r = list_lookup(W->list + (uint64_t)j * W->cap_list, c, (uint32_t)(e - pj), cursor, idx);
             if (r == 1) {
@@ -204,6 +205,7 @@ struct SpecEmit {
         return false;
     }
     __device__ void end() { sj = (I.seg_end >= (int64_t)I.Lf) ? SJ_LAST : SJ_STREAM_END; }
+    __device__ void exhausted(int64_t) { sj = SJ_UNSYNCED; }
 };
 
 template <int ALGO>
@@ -282,6 +284,7 @@ struct WalkEmit {
         return false;
     }
     __device__ void end() { sj = SJ_STREAM_END; }
+    __device__ void exhausted(int64_t) { sj = SJ_STREAM_END; }
 };
 
 // block-wide exclusive scan helper (1024 threads)
@@ -354,6 +357,7 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
     }
     __syncthreads();
 
+    dbg_note(4000 + warp, (10ull << 56), 0, 0, 0);
     // 2. compact the exceptional segments (sync target other than the next segment) in order
     if (tid == 0) s_carry = 0;
     __syncthreads();
@@ -373,6 +377,7 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
     }
     const uint64_t n_exc = s_carry;
 
+    dbg_note(4000 + warp, (11ull << 56), 0, 0, 0);
     // 3. serial resolution of the exceptional segments on the true chain (warp 0);
     //    unsynced halos are continued by a walker until they meet a later chain
     if (warp == 0) {
@@ -382,6 +387,7 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
         for (uint64_t x = 0; x < n_exc && x < W.exc_cap; ++x) {
             const uint64_t g = W.exc[x];
             if (g < reach) continue;  // skipped by an earlier jump: not on the true chain
+            dbg_note(4090, (20ull << 56) | x, g, reach, (uint64_t)(int64_t)W.sj[g]);
             SegInfo I = seg_info(G, W, g);
             int32_t sj = W.sj[g];
             if (sj == SJ_UNSYNCED) {
@@ -396,7 +402,10 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
                 em.cur_j = -1;
                 em.cursor = 0;
                 em.overflow = false;
-                const int64_t last = I.seg_end + (int64_t)W.halo[g * W.cap_halo + W.hcnt[g] - 1];
+                // resume the chain from its last recorded start
+                const uint32_t hc = W.hcnt[g];
+                const int64_t last = hc ? I.seg_end + (int64_t)W.halo[g * W.cap_halo + hc - 1]
+                                        : I.p + (int64_t)W.list[g * W.cap_list + W.cnt[g] - 1];
                 run_chain<ALGO>(R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
                                 l2_evict_first_policy(), em);
                 overflow |= em.overflow;
@@ -427,6 +436,7 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
     }
     __syncthreads();
 
+    dbg_note(4000 + warp, (12ull << 56), 0, 0, 0);
     // 4. mark segments the true chain jumps over
     const uint32_t nranges = W.misc[2];
     for (uint32_t r = warp; r < nranges; r += nwarps) {
@@ -435,6 +445,7 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
     }
     __syncthreads();
 
+    dbg_note(4000 + warp, (13ull << 56), 0, 0, 0);
     // 5. per-segment output counts and their exclusive scan
     if (tid == 0) s_carry = 0;
     __syncthreads();
@@ -526,13 +537,18 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_seg_prefix(const uint64_t *
 struct ChainEmit {
     uint64_t *out;
     uint64_t cap, n;
-    int64_t stop;
+    int64_t stop, len;
     __device__ bool boundary(int64_t e) {
         if (lane_id() == 0 && n < cap) out[n] = (uint64_t)e;
         ++n;
         return e >= stop;
     }
-    __device__ void end() {}
+    // the chain's last chunk ends at len: record len as its final position
+    __device__ void end() {
+        if (lane_id() == 0 && n < cap) out[n] = (uint64_t)len;
+        ++n;
+    }
+    __device__ void exhausted(int64_t) {}
 };
 
 template <int ALGO>
@@ -541,7 +557,7 @@ __global__ void __launch_bounds__(32) k_chain(const uint8_t *data, uint64_t len,
                                               uint64_t *count) {
     extern __shared__ __align__(128) uint8_t smem[];
     WarpRing R{smem, reinterpret_cast<uint64_t *>(smem + RING_BYTES)};
-    ChainEmit em{out, cap, 0, (int64_t)stop};
+    ChainEmit em{out, cap, 0, (int64_t)stop, (int64_t)len};
     if (lane_id() == 0 && cap > 0) out[0] = start;
     em.n = 1;
     if (start < stop && start < len)
@@ -854,9 +870,15 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     G.w = p->window;
     G.max_size = p->max_size;
     {
+        // 32-bit call tag for the published-list words: a splitmix64 hash of a
+        // process-wide counter, so stale words in a reused workspace (from an
+        // earlier call or other data) match with probability ~2^-32
         std::lock_guard<std::mutex> lk(g_mu);
-        G.epoch = (++g_epoch) & 0xFFFFFFFFull;
-        if (G.epoch == 0) G.epoch = ++g_epoch & 0xFFFFFFFFull;
+        uint64_t z = (++g_epoch) * 0x9E3779B97F4A7C15ull + reinterpret_cast<uintptr_t>(&g_epoch);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        G.epoch = (z & 0xFFFFFFFFull) | 1ull;
     }
     uint64_t *file_out = batch ? d_bound_off : W.file_out;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -900,6 +922,30 @@ int cdc_abi_version(void) { return CDC_ABI_VERSION; }
 const char *cdc_last_error(void) { return g_err.c_str(); }
 
 int cdc_last_launch_count(void) { return g_launches; }
+
+int cdc_debug_progress(void **host_ptr) {
+    // host-mapped progress words (8192 slots x 4 u64) that running kernels update
+    static unsigned long long *h = nullptr;
+    if (!h) {
+        CDC_CUDA(cudaHostAlloc((void **)&h, 8192 * 32, cudaHostAllocMapped));
+        memset(h, 0, 8192 * 32);
+        unsigned long long *d = nullptr;
+        CDC_CUDA(cudaHostGetDevicePointer((void **)&d, h, 0));
+        CDC_CUDA(cudaMemcpyToSymbol(cdc::g_dbg, &d, sizeof(d)));
+        CDC_CUDA(cudaMemcpyToSymbol(cdc::g_dbg_fwd, &d, sizeof(d)));
+    }
+    if (host_ptr) *host_ptr = h;
+    return CDC_OK;
+}
+
+int cdc_profile_query(int *done) {
+    // completion state of the events of the last profiled call (1 = reached)
+    if (!done) return fail(CDC_ERR_INVALID, "null");
+    if (g_prof_calls.empty()) return fail(CDC_ERR_INVALID, "no profiled call");
+    ProfCall &pc = g_prof_calls.back();
+    for (int k = 0; k <= PROF_KERNELS; ++k) done[k] = pc.ev[k] ? (cudaEventQuery(pc.ev[k]) == cudaSuccess) : -1;
+    return CDC_OK;
+}
 
 int cdc_profile_enable(int on) {
     g_prof_on = on != 0;
