@@ -194,13 +194,10 @@ int cdc_last_launch_count(void);
 int cdc_profile_enable(int on);
 int cdc_profile_collect(double *ms_sum, uint64_t *launches, uint64_t *calls);
 
-/* Diagnostics.  cdc_profile_query writes, for the 5 events of the last
+/* Diagnostics: cdc_profile_query writes, for the 5 events of the last
  * profiled call (before each of the 4 kernels and after the last), 1 if the
- * GPU has reached it, 0 if not.  cdc_debug_progress allocates (once) a
- * host-mapped array of 8192 x 4 uint64 progress words that the kernels then
- * update as they run, and returns its host address (for diagnosing hangs). */
+ * GPU has reached it, 0 if not (-1: event unused). */
 int cdc_profile_query(int *done);
-int cdc_debug_progress(void **host_ptr);
 
 #ifdef __cplusplus
 }

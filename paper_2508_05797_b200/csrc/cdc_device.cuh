@@ -2,17 +2,20 @@
 //
 //  * PTX wrappers: mbarrier, 1-D TMA bulk copy (cp.async.bulk -> UBLKCP),
 //    L2 evict-first policy, acquire/release flags.
-//  * Byte SIMD: Extreme Byte Search (§4.1) as a per-lane max/min tree
-//    over 16-byte vectors using the native DPX VIMNMX3.U16x2 instruction and
-//    a CREDUX warp reduction; Range Scan (§4.2) as per-byte compare masks
-//    collapsed to one bit per byte, a warp ballot and __ffs -- the GPU form of
-//    the paper's VCMP + VMASK "packed scanning".
+//  * Byte SIMD on 16-byte lane vectors: Extreme Byte Search (§4.1)
+//    as a max/min tree over the lane's 16 bytes with the native DPX
+//    VIMNMX3.U16x2 instruction, rooted in a warp CREDUX reduction; Range Scan
+//    (§4.2) as a per-lane "any byte satisfies" test, a warp ballot and __ffs,
+//    then one in-lane byte locate -- the GPU form of the paper's VCMP + VMASK
+//    "packed scanning".
 //  * run_chain: one warp walks the chunk chain of one stream from a given
-//    start, streaming the bytes through a private shared-memory ring of
-//    NST 2 KiB stages filled by TMA, and reports every chunk boundary to an
-//    Emit policy.  RAM (§2.1.2 l.198; §4.3 l.355) and AE-Max/AE-Min (§2.1.2
-//    l.169-171; §4.3 l.357-359) are written as single-pass state machines
-//    that consume each byte once.
+//    start, streaming the bytes through a private shared-memory ring of NST
+//    STAGE-byte stages filled by TMA.  RAM (§2.1.2 l.198; §4.3 l.355) and
+//    AE-Max / AE-Min (§2.1.2 l.169-171; §4.3 l.357-359) are block-granular
+//    state machines: each 512-byte warp block (32 lanes x 16 B) is loaded from
+//    shared memory once, its per-lane extreme is computed once, and every
+//    event inside the block (window end, boundary, new AE target) costs O(1)
+//    warp operations.
 #pragma once
 #include <cstdint>
 #include <cstdio>
@@ -20,8 +23,9 @@
 
 namespace cdc {
 
-constexpr int STAGE = 2048;            // bytes per TMA stage = one warp step (4 x 512 B)
-constexpr int NST = 8;                 // ring depth per warp (16 KiB)
+constexpr int BLK = 512;               // bytes per warp block: 32 lanes x 16 B
+constexpr int STAGE = 4096;            // bytes per TMA stage (8 warp blocks)
+constexpr int NST = 4;                 // ring depth per warp (16 KiB)
 constexpr int RING_BYTES = STAGE * NST;
 constexpr int RING_SMEM = RING_BYTES + NST * 8;
 
@@ -54,26 +58,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-__device__ unsigned long long *g_dbg_fwd = nullptr;  // set with g_dbg (debug only)
 // Watchdog: a stage that has not landed within ~10 s (clock64) means a lost
-// bulk copy; record the raw barrier word and trap instead of hanging the GPU.
+// bulk copy; trap instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     const long long t0 = clock64();
-    bool noted = false;
     while (!mbar_try_wait(bar, parity)) {
-        const long long dt = clock64() - t0;
-        if (!noted && dt > 2000000000ll) {
-            noted = true;
-            unsigned long long *p = g_dbg_fwd;
-            if (p) {
-                unsigned long long v;
-                asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(smem_addr(bar)));
-                volatile unsigned long long *q = p + (8191ull * 4);
-                q[0] = 0xBADull; q[1] = v; q[2] = parity; q[3] = ((unsigned long long)blockIdx.x << 32) | threadIdx.x;
-            }
-        }
-        if (dt > 20000000000ll) __trap();
+        if (clock64() - t0 > 20000000000ll) __trap();
     }
 }
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
@@ -98,12 +89,22 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // ---------------------------------------------------------------- byte SIMD
-// Max/min of bytes with the DPX 3-input u16x2 min/max: a raw word's 16-bit
-// halves carry bytes 1 and 3 in their high bytes; the word shifted left by 8
-// carries bytes 0 and 2 there.  The high byte of the u16 extreme of a set of
-// halves is the extreme of their high bytes, whatever the low bytes are.
+// Extreme of bytes with the DPX 3-input u16x2 min/max: the high byte of the
+// u16 extreme of a set of 16-bit halves is the extreme of their high bytes,
+// whatever the low bytes are.  A word's halves carry bytes 1 and 3 in their
+// high bytes; the word shifted left by 8 carries bytes 0 and 2 there.
 template <bool MAX>
 __device__ __forceinline__ uint32_t ext3(uint32_t a, uint32_t b, uint32_t c) {
     if constexpr (MAX)
@@ -112,89 +113,119 @@ __device__ __forceinline__ uint32_t ext3(uint32_t a, uint32_t b, uint32_t c) {
         return __vimin3_u16x2(a, b, c);
 }
 template <bool MAX>
-__device__ __forceinline__ void acc16(const uint4 &v, uint32_t &hi, uint32_t &lo) {
-    hi = ext3<MAX>(hi, v.x, v.y);
-    hi = ext3<MAX>(hi, v.z, v.w);
-    lo = ext3<MAX>(lo, v.x << 8, v.y << 8);
-    lo = ext3<MAX>(lo, v.z << 8, v.w << 8);
+__device__ __forceinline__ uint32_t neutral() {
+    return MAX ? 0u : 255u;
 }
 template <bool MAX>
-__device__ __forceinline__ uint32_t acc_init() {
-    return MAX ? 0u : 0xFFFFFFFFu;
-}
-// the extreme byte held by a (hi, lo) accumulator pair
-template <bool MAX>
-__device__ __forceinline__ uint32_t acc_extreme(uint32_t hi, uint32_t lo) {
-    uint32_t m = ext3<MAX>(hi, lo, acc_init<MAX>());
-    uint32_t a = m >> 24, b = (m >> 8) & 0xFFu;
+__device__ __forceinline__ uint32_t ext2(uint32_t a, uint32_t b) {
     return MAX ? max(a, b) : min(a, b);
 }
 template <bool MAX>
-__device__ __forceinline__ uint32_t warp_extreme(uint32_t v) {
+__device__ __forceinline__ bool beats(uint32_t a, uint32_t b) {  // a strictly more extreme than b
+    return MAX ? a > b : a < b;
+}
+// extreme byte of a 16-byte vector (Extreme Byte Search, §4.1, one tree leaf)
+template <bool MAX>
+__device__ __forceinline__ uint32_t vext16(const uint4 &v) {
+    const uint32_t a = ext3<MAX>(v.x, v.y, v.z);
+    const uint32_t b = ext3<MAX>(v.w, v.x << 8, v.y << 8);
+    const uint32_t c = ext3<MAX>(v.z << 8, v.w << 8, a);
+    const uint32_t m = ext3<MAX>(b, c, c);
+    return ext2<MAX>(m >> 24, (m >> 8) & 0xFFu);
+}
+// byte mask (0xFF for kept bytes) of bytes [lo, hi) of the word holding bytes [4j, 4j+4)
+__device__ __forceinline__ uint32_t word_keep(int lo, int hi, int j) {
+    int a = lo - 4 * j, z = hi - 4 * j;
+    a = a < 0 ? 0 : (a > 4 ? 4 : a);
+    z = z < 0 ? 0 : (z > 4 ? 4 : z);
+    const uint32_t up = z >= 4 ? 0xFFFFFFFFu : ((1u << (8 * z)) - 1u);
+    const uint32_t dn = a >= 4 ? 0xFFFFFFFFu : ((1u << (8 * a)) - 1u);
+    return up & ~dn;
+}
+// extreme byte of bytes [lo, hi) of a 16-byte vector (0 <= lo < hi <= 16)
+template <bool MAX>
+__device__ __forceinline__ uint32_t vext16_range(const uint4 &v, int lo, int hi) {
+    uint4 r;
+    const uint32_t k0 = word_keep(lo, hi, 0), k1 = word_keep(lo, hi, 1), k2 = word_keep(lo, hi, 2),
+                   k3 = word_keep(lo, hi, 3);
+    if (MAX) {
+        r.x = v.x & k0; r.y = v.y & k1; r.z = v.z & k2; r.w = v.w & k3;
+    } else {
+        r.x = v.x | ~k0; r.y = v.y | ~k1; r.z = v.z | ~k2; r.w = v.w | ~k3;
+    }
+    return vext16<MAX>(r);
+}
+template <bool MAX>
+__device__ __forceinline__ uint32_t warp_ext(uint32_t v) {
     if constexpr (MAX)
         return __reduce_max_sync(0xFFFFFFFFu, v);
     else
         return __reduce_min_sync(0xFFFFFFFFu, v);
 }
-
-// per-byte comparison (0xFF where true) of 4 packed bytes against a broadcast target
-template <int CMP>
-__device__ __forceinline__ uint32_t vcmp4(uint32_t x, uint32_t t4) {
-    if constexpr (CMP == CMP_GT) return __vcmpgtu4(x, t4);
-    else if constexpr (CMP == CMP_GEQ) return __vcmpgeu4(x, t4);
-    else if constexpr (CMP == CMP_LT) return __vcmpltu4(x, t4);
-    else if constexpr (CMP == CMP_LEQ) return __vcmpleu4(x, t4);
-    else return __vcmpeq4(x, t4);
+// byte j (0..15) of a 16-byte vector
+__device__ __forceinline__ uint32_t vbyte(const uint4 &v, int j) {
+    const int q = j >> 2;
+    const uint32_t wd = q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
+    return (wd >> (8 * (j & 3))) & 0xFFu;
 }
-// 0xFF/0x00 bytes -> 4 bits (byte i -> bit i)
-__device__ __forceinline__ uint32_t pack4(uint32_t m) { return ((m & 0x01010101u) * 0x01020408u) >> 24; }
-// 4 bits -> 0xFF/0x00 bytes
-__device__ __forceinline__ uint32_t unpack4(uint32_t b) { return ((b * 0x00204081u) & 0x01010101u) * 0xFFu; }
 
 template <int CMP>
-__device__ __forceinline__ uint32_t pred_bits16(const uint4 &v, uint32_t target) {
-    const uint32_t t4 = target * 0x01010101u;
-    return pack4(vcmp4<CMP>(v.x, t4)) | (pack4(vcmp4<CMP>(v.y, t4)) << 4) | (pack4(vcmp4<CMP>(v.z, t4)) << 8) |
-           (pack4(vcmp4<CMP>(v.w, t4)) << 12);
-}
-// bits of the lane's 16 bytes [base, base+16) that lie in [lo, hi)
-__device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
-    int a = lo - base, z = hi - base;
-    a = a < 0 ? 0 : a;
-    z = z > 16 ? 16 : z;
-    if (z <= a) return 0u;
-    return ((1u << z) - 1u) & ~((1u << a) - 1u);
-}
-__device__ __forceinline__ uint4 mask_bytes(const uint4 &v, uint32_t bits16, bool keep_max) {
-    // keep bytes whose bit is set; the others become neutral (0 for max, 0xFF for min)
-    uint4 m;
-    m.x = unpack4(bits16 & 0xF);
-    m.y = unpack4((bits16 >> 4) & 0xF);
-    m.z = unpack4((bits16 >> 8) & 0xF);
-    m.w = unpack4((bits16 >> 12) & 0xF);
-    uint4 r;
-    if (keep_max) {
-        r.x = v.x & m.x; r.y = v.y & m.y; r.z = v.z & m.z; r.w = v.w & m.w;
-    } else {
-        r.x = v.x | ~m.x; r.y = v.y | ~m.y; r.z = v.z | ~m.z; r.w = v.w | ~m.w;
-    }
-    return r;
+__device__ __forceinline__ bool cmp_holds(uint32_t b, uint32_t t) {
+    if constexpr (CMP == CMP_GT) return b > t;
+    else if constexpr (CMP == CMP_GEQ) return b >= t;
+    else if constexpr (CMP == CMP_LT) return b < t;
+    else if constexpr (CMP == CMP_LEQ) return b <= t;
+    else return b == t;
 }
 
-__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
-
-// Debug progress words (host-mapped memory set by cdc_debug_progress); null in
-// normal runs.  Slot layout: 4 x u64 per warp: {tag|stage, c, s, aux}.
-__device__ unsigned long long *g_dbg = nullptr;
-__device__ __forceinline__ void dbg_note(uint64_t slot, uint64_t a, uint64_t b, uint64_t c2, uint64_t d) {
-    unsigned long long *p = g_dbg;
-    if (p != nullptr && lane_id() == 0 && slot < 8192) {
-        volatile unsigned long long *q = p + slot * 4;
-        q[0] = a; q[1] = b; q[2] = c2; q[3] = d;
-    }
+// Lane-vector view of one 512-byte block of the ring: lane l holds bytes
+// [16 l, 16 l + 16) of the block in v, their extreme in full (computed once).
+struct Blk {
+    uint4 v;
+    int64_t B;  // stream position of the block's byte 0
+};
+// lane's part [a, b) (0..16) of the block range [rlo, rhi) (block-relative)
+__device__ __forceinline__ void lane_part(int rlo, int rhi, int &a, int &b) {
+    const int base = lane_id() * 16;
+    a = rlo - base;
+    b = rhi - base;
+    a = a < 0 ? 0 : (a > 16 ? 16 : a);
+    b = b < 0 ? 0 : (b > 16 ? 16 : b);
 }
-__device__ __forceinline__ uint64_t dbg_slot() {
-    return (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5) + (gridDim.x == 1 ? 4096 : 0);
+// per-lane extreme of the block range [rlo, rhi); `full` is the lane's
+// whole-vector extreme; `has` tells whether the lane holds any byte of the range
+// (lanes without one return the neutral value and must not join a ballot).
+template <bool MAX>
+__device__ __forceinline__ uint32_t lane_ext(const Blk &k, uint32_t full, int rlo, int rhi, bool &has) {
+    int a, b;
+    lane_part(rlo, rhi, a, b);
+    has = a < b;
+    if (a == 0 && b == 16) return full;
+    if (a >= b) return neutral<MAX>();
+    return vext16_range<MAX>(k.v, a, b);
+}
+// Range Scan locate (§4.2): first block-relative index in [rlo, rhi) whose byte
+// satisfies (byte CMP target), given the ballot `bal` of lanes that hold one.
+template <int CMP>
+__device__ __forceinline__ int locate(const Blk &k, uint32_t bal, int rlo, int rhi, uint32_t target) {
+    const int L = __ffs(bal) - 1;
+    uint4 u;
+    u.x = __shfl_sync(0xFFFFFFFFu, k.v.x, L);
+    u.y = __shfl_sync(0xFFFFFFFFu, k.v.y, L);
+    u.z = __shfl_sync(0xFFFFFFFFu, k.v.z, L);
+    u.w = __shfl_sync(0xFFFFFFFFu, k.v.w, L);
+    const int j = lane_id() & 15;
+    const int pos = L * 16 + j;
+    const bool hit = lane_id() < 16 && pos >= rlo && pos < rhi && cmp_holds<CMP>(vbyte(u, j), target);
+    const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, hit);
+    return L * 16 + __ffs(b2) - 1;
+}
+// byte at block-relative index r (uniform across the warp)
+__device__ __forceinline__ uint32_t byte_at(const Blk &k, int r) {
+    const int q = (r >> 2) & 3;
+    const uint32_t wd = q == 0 ? k.v.x : (q == 1 ? k.v.y : (q == 2 ? k.v.z : k.v.w));
+    const uint32_t x = __shfl_sync(0xFFFFFFFFu, wd, r >> 4);
+    return (x >> (8 * (r & 3))) & 0xFFu;
 }
 
 // ---------------------------------------------------------------- warp ring
@@ -203,87 +234,28 @@ struct WarpRing {
     uint64_t *bar;  // NST mbarriers
 };
 
-// Step-local view of one 2 KiB stage held in shared memory.
-struct Step {
-    const uint8_t *sp;  // stage buffer
-    int64_t B;          // stream position of sp[0]
-    __device__ __forceinline__ uint4 vec(int blk) const {
-        return *reinterpret_cast<const uint4 *>(sp + blk * 512 + lane_id() * 16);
-    }
-    __device__ __forceinline__ uint32_t byte_at(int64_t pos) const { return sp[pos - B]; }
-};
-
-// Extreme (max or min) of the whole stage, per lane (64 bytes per lane).
-template <bool MAX>
-__device__ __forceinline__ uint32_t step_lane_extreme(const Step &st) {
-    uint32_t hi = acc_init<MAX>(), lo = acc_init<MAX>();
-#pragma unroll
-    for (int b = 0; b < STAGE / 512; ++b) acc16<MAX>(st.vec(b), hi, lo);
-    return acc_extreme<MAX>(hi, lo);
-}
-
-// Range Scan (§4.2) inside one stage: first position in [lo, hi) whose byte
-// satisfies (byte CMP target); returns hi when there is none.
-template <int CMP>
-__device__ __forceinline__ int64_t step_find(const Step &st, int64_t lo, int64_t hi, uint32_t target) {
-    const int rlo = (int)(lo - st.B), rhi = (int)(hi - st.B);
-    if (rlo >= rhi) return hi;
-    if (rlo == 0 && rhi == STAGE) {
-        // fast reject over the whole stage with the extreme tree
-        constexpr bool MAX = (CMP == CMP_GT || CMP == CMP_GEQ);
-        if constexpr (CMP != CMP_EQ) {
-            uint32_t e = step_lane_extreme<MAX>(st);
-            bool any;
-            if constexpr (CMP == CMP_GT) any = e > target;
-            else if constexpr (CMP == CMP_GEQ) any = e >= target;
-            else if constexpr (CMP == CMP_LT) any = e < target;
-            else any = e <= target;
-            if (!__any_sync(0xFFFFFFFFu, any)) return hi;
-        }
-    }
-    const int lane = lane_id();
-    for (int b = rlo >> 9; b <= (rhi - 1) >> 9; ++b) {
-        uint32_t bits = pred_bits16<CMP>(st.vec(b), target) & range_bits(rlo, rhi, b * 512 + lane * 16);
-        uint32_t bal = __ballot_sync(0xFFFFFFFFu, bits != 0);
-        if (bal) {
-            int L = __ffs(bal) - 1;
-            uint32_t mb = __shfl_sync(0xFFFFFFFFu, bits, L);
-            return st.B + b * 512 + L * 16 + (__ffs(mb) - 1);
-        }
-    }
-    return hi;
-}
-
-// Extreme Byte Search (§4.1) accumulation of [lo, hi) of one stage into the
-// lane accumulators (the tree's leaves; the warp reduction is the root).
-template <bool MAX>
-__device__ __forceinline__ void step_accumulate(const Step &st, int64_t lo, int64_t hi, uint32_t &acc_hi,
-                                                uint32_t &acc_lo) {
-    const int rlo = (int)(lo - st.B), rhi = (int)(hi - st.B);
-    if (rlo >= rhi) return;
-    if (rlo == 0 && rhi == STAGE) {
-#pragma unroll
-        for (int b = 0; b < STAGE / 512; ++b) acc16<MAX>(st.vec(b), acc_hi, acc_lo);
-        return;
-    }
-    const int lane = lane_id();
-    for (int b = rlo >> 9; b <= (rhi - 1) >> 9; ++b) {
-        uint32_t bits = range_bits(rlo, rhi, b * 512 + lane * 16);
-        acc16<MAX>(mask_bytes(st.vec(b), bits, MAX), acc_hi, acc_lo);
-    }
-}
-
 // ---------------------------------------------------------------- chain engine
 //
 // run_chain walks the chunk chain of the stream fbase[0..Lf) that begins with
 // a chunk at `start` (0 <= start < Lf).  Every boundary e < Lf (the start of
 // the next chunk) is passed to emit.boundary(e), which returns true to stop
-// the walk; when the chain's last chunk reaches Lf, emit.end() is called.
-// Bytes are read only below read_end (the emitter must stop before needing
-// more).  All 32 lanes call this with identical arguments.
+// the walk; when the chain's last chunk reaches Lf, emit.end() is called; when
+// the bytes below read_end are exhausted first, emit.exhausted(c).  Bytes are
+// read only below read_end.  All 32 lanes call this with identical arguments.
+//
+// Semantics are those of the oracle (oracle/cdc_oracle.c), with the chunk
+// limit = min(Lf, s + max_size) (reading R5):
+//   RAM:    M = max d[s, s+w); the chunk ends after the first i in [s+w, limit)
+//           with d[i] >= M, else at limit; if s + w >= Lf it ends at Lf.
+//   AE-Max: target t = s; while t + w < limit: if no byte of (t, t+w] exceeds
+//           d[t] the chunk ends at t+w+1, else t = first byte of (t, t+w]
+//           exceeding d[t]; once t + w >= limit it ends at limit.  (AE-Min:
+//           "less" for "exceeds".)
 template <int ALGO, class Emit>
 __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf, int64_t start,
                           int64_t read_end, uint32_t w, uint64_t max_size, uint64_t policy, Emit &emit) {
+    constexpr bool MAX = (ALGO != ALGO_AE_MIN);
+    constexpr uint32_t SAT = MAX ? 255u : 0u;  // a target nothing can beat
     const int lane = lane_id();
     if (read_end > Lf) read_end = Lf;
     const uint8_t *g0 = reinterpret_cast<const uint8_t *>(reinterpret_cast<uintptr_t>(fbase + start) &
@@ -310,89 +282,142 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     };
     for (; issued < nstages && issued < NST; ++issued) issue(issued);
 
-    constexpr bool MAX = (ALGO != ALGO_AE_MIN);
+    const int64_t W = (int64_t)w;
+    const bool fastrec = w >= (uint32_t)(BLK - 1);  // AE: records inside one block never miss a deadline
     int64_t s = start;                                                           // current chunk start
     int64_t limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;  // chunk end bound
     int64_t c = s;                                                               // next byte to examine
     bool stop = false;
     // RAM state
-    int phase = 0;  // 0: window [s, s+w); 1: scan for byte >= M
-    uint32_t M = 0, acc_hi = acc_init<true>(), acc_lo = acc_init<true>();
+    bool scanning = false;  // false: window [s, s+w); true: scan for a byte >= M
+    uint32_t M = 0, acc = 0;
     // AE state
     uint32_t ext = 0;
     int64_t t = 0;
     bool pending = true;  // the chunk's first byte is the first target
 
     if constexpr (ALGO == ALGO_RAM) {
-        if (s + (int64_t)w >= Lf) {  // window does not fit: a single final chunk
+        if (s + W >= Lf) {  // window does not fit: a single final chunk
             emit.end();
             stop = true;
         }
     }
 
+    // a boundary at e: returns true when the walk stops
+    auto on_boundary = [&](int64_t e) -> bool {
+        if (e >= Lf) {
+            emit.end();
+            return true;
+        }
+        if (emit.boundary(e)) return true;
+        s = e;
+        c = e;
+        limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
+        if constexpr (ALGO == ALGO_RAM) {
+            scanning = false;
+            acc = 0;
+            if (s + W >= Lf) {
+                emit.end();
+                return true;
+            }
+        } else {
+            pending = true;
+        }
+        return false;
+    };
+
     int64_t k = 0;
     while (!stop && k < nstages) {
         const int slot = (int)(k % NST);
-        dbg_note(dbg_slot(), (2ull << 56) | (uint64_t)k, (uint64_t)c, (uint64_t)s, (uint64_t)issued);
         mbar_wait(&R.bar[slot], (uint32_t)((k / NST) & 1));
-        Step st{R.buf + slot * STAGE, B0 + k * STAGE};
-        const int64_t E = st.B + STAGE;
-        dbg_note(dbg_slot(), (1ull << 56) | (uint64_t)k, (uint64_t)c, (uint64_t)s, (uint64_t)nstages);
-
-        while (!stop && c < E) {
-            if constexpr (ALGO == ALGO_RAM) {
-                if (phase == 0) {
-                    const int64_t we = s + (int64_t)w;
-                    const int64_t hi = we < E ? we : E;
-                    step_accumulate<true>(st, c, hi, acc_hi, acc_lo);
-                    c = hi;
-                    if (c == we) {
-                        M = warp_extreme<true>(acc_extreme<true>(acc_hi, acc_lo));
-                        phase = 1;
+        const uint8_t *sp = R.buf + slot * STAGE;
+        const int64_t SB = B0 + k * STAGE;
+        const int b0 = (int)((c - SB) >> 9) > 0 ? (int)((c - SB) >> 9) : 0;
+#pragma unroll 1
+        for (int bi = b0; bi < STAGE / BLK && !stop; ++bi) {
+            Blk blk;
+            blk.B = SB + bi * BLK;
+            int64_t Bend = blk.B + BLK;
+            if (Bend > read_end) Bend = read_end;
+            if (c >= Bend) continue;
+            blk.v = *reinterpret_cast<const uint4 *>(sp + bi * BLK + lane * 16);
+            const uint32_t full = vext16<MAX>(blk.v);
+            while (c < Bend) {
+                if constexpr (ALGO == ALGO_RAM) {
+                    if (!scanning) {
+                        const int64_t we = s + W;
+                        const int64_t hi = we < Bend ? we : Bend;
+                        bool has;
+                        acc = ext2<true>(acc, lane_ext<true>(blk, full, (int)(c - blk.B), (int)(hi - blk.B), has));
+                        c = hi;
+                        if (c == we) {
+                            M = warp_ext<true>(acc);
+                            scanning = true;
+                        }
+                    } else {
+                        const int64_t hi = limit < Bend ? limit : Bend;
+                        const int rlo = (int)(c - blk.B), rhi = (int)(hi - blk.B);
+                        bool has;
+                        const uint32_t lm = lane_ext<true>(blk, full, rlo, rhi, has);
+                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has && lm >= M);
+                        int64_t e;
+                        if (bal) {
+                            e = blk.B + locate<CMP_GEQ>(blk, bal, rlo, rhi, M) + 1;  // boundary byte ends the chunk
+                        } else {
+                            c = hi;
+                            if (c != limit) continue;
+                            e = limit;  // cap or end of stream
+                        }
+                        if (on_boundary(e)) {
+                            stop = true;
+                            break;
+                        }
                     }
                 } else {
-                    const int64_t hi = limit < E ? limit : E;
-                    const int64_t i = step_find<CMP_GEQ>(st, c, hi, M);
+                    if (pending) {  // first byte of the chunk: the first target
+                        ext = byte_at(blk, (int)(c - blk.B));
+                        t = c;
+                        ++c;
+                        pending = false;
+                        continue;
+                    }
+                    const int64_t dl = t + W + 1;  // window (t, t+w] ends before dl
+                    int64_t hi = dl < limit ? dl : limit;
+                    hi = hi < Bend ? hi : Bend;
+                    if (ext != SAT) {
+                        const int rlo = (int)(c - blk.B), rhi = (int)(hi - blk.B);
+                        bool has;
+                        const uint32_t lm = lane_ext<MAX>(blk, full, rlo, rhi, has);
+                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has && beats<MAX>(lm, ext));
+                        if (bal) {
+                            if (fastrec) {
+                                // every record of [c, hi) follows its predecessor within
+                                // < BLK <= w+1 bytes, so the last one -- the first
+                                // occurrence of the range extreme -- is the new target
+                                const uint32_t m = warp_ext<MAX>(lm);
+                                const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, has && lm == m);
+                                t = blk.B + locate<CMP_EQ>(blk, b2, rlo, rhi, m);
+                                ext = m;
+                                c = hi;
+                            } else {
+                                const int r = locate<MAX ? CMP_GT : CMP_LT>(blk, bal, rlo, rhi, ext);
+                                t = blk.B + r;
+                                ext = byte_at(blk, r);
+                                c = t + 1;
+                            }
+                            continue;
+                        }
+                    }
+                    c = hi;
                     int64_t e;
-                    if (i < hi) e = i + 1;            // boundary byte ends the chunk
-                    else if (hi == limit) e = limit;  // cap or end of stream
-                    else { c = hi; continue; }
-                    if (e >= Lf) { emit.end(); stop = true; break; }
-                    if (emit.boundary(e)) { stop = true; break; }
-                    s = e; c = e; phase = 0;
-                    acc_hi = acc_init<true>(); acc_lo = acc_init<true>();
-                    limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
-                    if (s + (int64_t)w >= Lf) { emit.end(); stop = true; break; }
+                    if (c == dl && dl <= limit) e = dl;  // target unbeaten over its window
+                    else if (c == limit) e = limit;      // cap or end of stream
+                    else continue;                       // block exhausted
+                    if (on_boundary(e)) {
+                        stop = true;
+                        break;
+                    }
                 }
-            } else {
-                if (pending) {  // first byte of the chunk: the first target
-                    ext = st.byte_at(c);
-                    t = c;
-                    ++c;
-                    pending = false;
-                    continue;
-                }
-                const int64_t dl = t + (int64_t)w + 1;  // window (t, t+w] ends before dl
-                int64_t hi = dl < limit ? dl : limit;
-                hi = hi < E ? hi : E;
-                int64_t i;
-                if (ext == (MAX ? 255u : 0u)) i = hi;  // nothing can beat an absolute extreme
-                else i = step_find<MAX ? CMP_GT : CMP_LT>(st, c, hi, ext);
-                if (i < hi) {  // a new target inside the window
-                    ext = st.byte_at(i);
-                    t = i;
-                    c = i + 1;
-                    continue;
-                }
-                c = hi;
-                int64_t e;
-                if (hi == dl && dl <= limit) e = dl;  // target unbeaten over its window
-                else if (hi == limit) e = limit;      // cap or end of stream
-                else continue;                        // stage exhausted
-                if (e >= Lf) { emit.end(); stop = true; break; }
-                if (emit.boundary(e)) { stop = true; break; }
-                s = e; c = e; pending = true;
-                limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
             }
         }
         __syncwarp();
@@ -402,17 +427,14 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
             ++issued;
         }
     }
-    // all bytes up to read_end consumed without the emitter stopping: the walk
-    // reached the end of the stream (read_end == Lf) inside the last chunk
+    // all bytes below read_end consumed without the emitter stopping
     if (!stop) {
         if (c >= Lf) emit.end();
         else emit.exhausted(c);
     }
     // drain copies still in flight before the ring is reused or the CTA exits
-    dbg_note(dbg_slot(), (3ull << 56) | (uint64_t)k, (uint64_t)c, (uint64_t)s, (uint64_t)issued);
     for (int64_t j = k; j < issued; ++j) mbar_wait(&R.bar[j % NST], (uint32_t)((j / NST) & 1));
     __syncwarp();
-    dbg_note(dbg_slot(), (4ull << 56) | (uint64_t)k, (uint64_t)c, (uint64_t)s, (uint64_t)issued);
 }
 
 }  // namespace cdc

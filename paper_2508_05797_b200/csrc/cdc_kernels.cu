@@ -22,7 +22,6 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
-#include <mutex>
 #include <string>
 #include <vector>
 
@@ -40,7 +39,7 @@ struct Work {
     uint32_t *list;              // G x cap_list  starts relative to the segment start
     uint32_t *halo;              // G x cap_halo  starts relative to the segment end
     uint32_t *cnt, *hcnt;        // list / halo lengths
-    unsigned long long *pub;     // (epoch << 32) | published list length
+    unsigned long long *pub;     // PUB_OPEN, or the final list length
     int32_t *sj;                 // sync target segment, or SJ_* code
     uint32_t *sa, *sb;           // halo entries before the sync point; its index in list(sj)
     uint32_t *entry, *tail, *wcnt, *jump_entry;
@@ -67,7 +66,6 @@ struct Geometry {
     uint64_t Hmax;   // halo cap
     uint32_t w;
     uint64_t max_size;
-    unsigned long long epoch;
 };
 
 __device__ __forceinline__ void file_bounds(const Geometry &G, uint64_t f, uint64_t &off, uint64_t &len) {
@@ -126,30 +124,49 @@ __device__ __forceinline__ SegInfo seg_info(const Geometry &G, const Work &W, ui
     return I;
 }
 
-// warp-cooperative membership of value r in a sorted list prefix lst[0..c), with a
-// monotone cursor: returns 1 found (idx set), 0 not a member, -1 undecidable
-// (every entry of the prefix is < r).
-__device__ __forceinline__ int list_lookup(const uint32_t *lst, uint32_t c, uint32_t r, uint32_t &cursor,
-                                           uint32_t &idx) {
+// Published lists.  list(g) holds the chunk starts of segment g's speculative
+// chain that lie inside the segment (relative to its first byte, ascending);
+// its entries are reset to LIST_EMPTY before every call (one memset) and each
+// is written once with a single 32-bit store, so a reader sees every entry
+// either complete or empty.  pub(g) is PUB_OPEN until the walker has left its
+// segment; then it holds the final entry count (st.release after the entries).
+constexpr uint32_t LIST_EMPTY = 0xFFFFFFFFu;
+constexpr unsigned long long PUB_OPEN = ~0ull;
+
+// Warp-cooperative membership of r in list(j), scanning from a monotone
+// cursor: 1 = found (idx set), 0 = not a member, -1 = undecidable yet (an
+// entry the scan needs is not visible and the list is not known complete).
+__device__ __forceinline__ int list_lookup(const uint32_t *lst, uint64_t cap, const unsigned long long *pubp,
+                                           uint32_t r, uint32_t &cursor, uint32_t &idx) {
     const int lane = lane_id();
-    while (cursor < c) {
-        uint32_t i = cursor + lane;
-        bool valid = i < c;
-        uint32_t v = valid ? __ldcg(lst + i) : 0u;
-        uint32_t bal = __ballot_sync(0xFFFFFFFFu, valid && v >= r);
-        if (bal) {
-            int L = __ffs(bal) - 1;
-            uint32_t vL = __shfl_sync(0xFFFFFFFFu, v, L);
-            cursor += L;
+    while (cursor < cap) {
+        const uint64_t i = (uint64_t)cursor + lane;
+        const uint32_t v = i < cap ? ld_relaxed_u32(lst + i) : LIST_EMPTY;
+        const bool valid = v != LIST_EMPTY;
+        const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
+        const uint32_t gm = __ballot_sync(0xFFFFFFFFu, valid && v >= r);
+        const int fi = vm == 0xFFFFFFFFu ? 32 : __ffs(~vm) - 1;  // first empty entry
+        const int fg = gm ? __ffs(gm) - 1 : 32;                  // first entry >= r
+        if (fg < fi) {
+            const uint32_t vL = __shfl_sync(0xFFFFFFFFu, v, fg);
+            cursor += fg;
             if (vL == r) {
                 idx = cursor;
                 return 1;
             }
             return 0;
         }
-        cursor = (c - cursor > 32u) ? cursor + 32u : c;
+        if (fi < 32) {
+            // entries [cursor, cursor + fi) are all < r; the next one is empty
+            const unsigned long long pw = ld_acquire_u64(pubp);
+            const uint32_t at = cursor + fi;
+            cursor = at;
+            if (pw != PUB_OPEN && (uint64_t)pw <= at) return 0;  // the list ends before r
+            return -1;
+        }
+        cursor += 32;
     }
-    return -1;
+    return 0;
 }
 
 // ------------------------------------------------------------------ K1 emit policy
@@ -164,17 +181,22 @@ struct SpecEmit {
     uint32_t sa, sb;
     int64_t cur_j;
     uint32_t cursor;
+    bool published;
 
+    __device__ void publish() {
+        if (!published) {
+            if (lane_id() == 0) st_release_u64(pub, (unsigned long long)cnt);
+            published = true;
+        }
+    }
     __device__ bool boundary(int64_t e) {
         const int lane = lane_id();
         if (e < I.seg_end) {
-            if (lane == 0) {
-                list[cnt] = (uint32_t)(e - I.p);
-                st_release_u64(pub, (G->epoch << 32) | (unsigned long long)(cnt + 1));
-            }
+            if (lane == 0) st_relaxed_u32(list + cnt, (uint32_t)(e - I.p));
             ++cnt;
             return false;
         }
+        publish();
         const uint32_t h = (uint32_t)(e - I.seg_end);
         if (lane == 0) halo[hcnt] = h;
         ++hcnt;
@@ -185,18 +207,14 @@ struct SpecEmit {
             cursor = 0;
         }
         const int64_t pj = I.seg_end + (j - (int64_t)I.g - 1) * (int64_t)G->S;
-        const unsigned long long pw = ld_acquire_u64(W->pub + j);
-        if ((pw >> 32) == G->epoch) {
-            uint32_t c = (uint32_t)(pw & 0xFFFFFFFFull);
-            if (c > W->cap_list) c = 0;  // never trust a count beyond capacity
-            uint32_t idx = 0;
-            int r = list_lookup(W->list + (uint64_t)j * W->cap_list, c, (uint32_t)(e - pj), cursor, idx);
-            if (r == 1) {
-                sj = (int32_t)j;
-                sa = hcnt - 1;
-                sb = idx;
-                return true;
-            }
+        uint32_t idx = 0;
+        const int r = list_lookup(W->list + (uint64_t)j * W->cap_list, W->cap_list, W->pub + j, (uint32_t)(e - pj),
+                                  cursor, idx);
+        if (r == 1) {
+            sj = (int32_t)j;
+            sa = hcnt - 1;
+            sb = idx;
+            return true;
         }
         if ((uint64_t)h >= G->Hmax) {
             sj = SJ_UNSYNCED;
@@ -231,14 +249,13 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32) k_speculate(Geometry G, Work 
     em.sa = em.sb = 0;
     em.cur_j = -1;
     em.cursor = 0;
-    if (lane_id() == 0) {
-        em.list[0] = 0;  // the speculative chain starts at the segment's first byte
-        st_release_u64(em.pub, (G.epoch << 32) | 1ull);
-    }
+    em.published = false;
+    if (lane_id() == 0) st_relaxed_u32(em.list, 0u);  // the speculative chain starts at the segment's first byte
     const uint8_t *fbase = G.data + em.I.foff;
     int64_t read_end = (g == em.I.last) ? (int64_t)em.I.Lf
                                         : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
     run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, l2_evict_first_policy(), em);
+    em.publish();
     if (lane_id() == 0) {
         W.cnt[g] = em.cnt;
         W.hcnt[g] = em.hcnt;
@@ -269,7 +286,8 @@ struct WalkEmit {
         }
         const int64_t pj = I.seg_end + (j - (int64_t)I.g - 1) * (int64_t)G->S;
         uint32_t idx = 0;
-        int r = list_lookup(W->list + (uint64_t)j * W->cap_list, W->cnt[j], (uint32_t)(e - pj), cursor, idx);
+        int r = list_lookup(W->list + (uint64_t)j * W->cap_list, W->cap_list, W->pub + j, (uint32_t)(e - pj), cursor,
+                            idx);
         if (r == 1) {
             sj = (int32_t)j;
             sb = idx;
@@ -340,7 +358,8 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
             }
             const int64_t pj = I.seg_end + (j - (int64_t)g - 1) * (int64_t)G.S;
             uint32_t idx = 0;
-            if (list_lookup(W.list + (uint64_t)j * W.cap_list, W.cnt[j], (uint32_t)(e - pj), cursor, idx) == 1) {
+            if (list_lookup(W.list + (uint64_t)j * W.cap_list, W.cap_list, W.pub + j, (uint32_t)(e - pj), cursor,
+                            idx) == 1) {
                 if (lane == 0) {
                     W.sj[g] = (int32_t)j;
                     W.sa[g] = i;
@@ -357,7 +376,6 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
     }
     __syncthreads();
 
-    dbg_note(4000 + warp, (10ull << 56), 0, 0, 0);
     // 2. compact the exceptional segments (sync target other than the next segment) in order
     if (tid == 0) s_carry = 0;
     __syncthreads();
@@ -377,7 +395,6 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
     }
     const uint64_t n_exc = s_carry;
 
-    dbg_note(4000 + warp, (11ull << 56), 0, 0, 0);
     // 3. serial resolution of the exceptional segments on the true chain (warp 0);
     //    unsynced halos are continued by a walker until they meet a later chain
     if (warp == 0) {
@@ -387,7 +404,6 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
         for (uint64_t x = 0; x < n_exc && x < W.exc_cap; ++x) {
             const uint64_t g = W.exc[x];
             if (g < reach) continue;  // skipped by an earlier jump: not on the true chain
-            dbg_note(4090, (20ull << 56) | x, g, reach, (uint64_t)(int64_t)W.sj[g]);
             SegInfo I = seg_info(G, W, g);
             int32_t sj = W.sj[g];
             if (sj == SJ_UNSYNCED) {
@@ -436,7 +452,6 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
     }
     __syncthreads();
 
-    dbg_note(4000 + warp, (12ull << 56), 0, 0, 0);
     // 4. mark segments the true chain jumps over
     const uint32_t nranges = W.misc[2];
     for (uint32_t r = warp; r < nranges; r += nwarps) {
@@ -445,7 +460,6 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
     }
     __syncthreads();
 
-    dbg_note(4000 + warp, (13ull << 56), 0, 0, 0);
     // 5. per-segment output counts and their exclusive scan
     if (tid == 0) s_carry = 0;
     __syncthreads();
@@ -567,7 +581,8 @@ __global__ void __launch_bounds__(32) k_chain(const uint8_t *data, uint64_t len,
 }
 
 // ------------------------------------------------------------------ primitives (§4.1, §4.2)
-// Region bytes are read with 16-byte aligned loads; bytes outside the region are masked.
+// One warp per region.  The region is walked in 512-byte warp blocks of
+// 16-byte aligned lane vectors; bytes outside the region are masked.
 template <bool MAX>
 __global__ void k_ebs(const uint8_t *data, const uint64_t *off, const uint64_t *len, uint64_t n, uint8_t *value,
                       uint64_t *pos) {
@@ -575,32 +590,39 @@ __global__ void k_ebs(const uint8_t *data, const uint64_t *off, const uint64_t *
     const int lane = lane_id();
     if (r >= n) return;
     const uint8_t *b = data + off[r];
-    const uint64_t L = len[r];
     const uint8_t *a0 = reinterpret_cast<const uint8_t *>(reinterpret_cast<uintptr_t>(b) & ~(uintptr_t)15);
-    const int64_t lo = b - a0, hi = lo + (int64_t)L;  // region = [lo, hi) relative to a0
-    uint32_t ah = acc_init<MAX>(), al = acc_init<MAX>();
-    for (int64_t blk = 0; blk < hi; blk += 512) {
-        const int64_t base = blk + lane * 16;
-        uint32_t bits = range_bits(lo - blk > 0 ? (int)(lo - blk) : 0, hi - blk < 512 ? (int)(hi - blk) : 512, lane * 16);
-        if (bits) {
-            uint4 v = *reinterpret_cast<const uint4 *>(a0 + base);
-            acc16<MAX>(mask_bytes(v, bits, MAX), ah, al);
+    const int64_t lo = b - a0, hi = lo + (int64_t)len[r];  // region = [lo, hi) relative to a0
+    // tree leaves: per-lane extreme; root: warp reduction
+    uint32_t acc = neutral<MAX>();
+    for (int64_t B = 0; B < hi; B += BLK) {
+        const int rlo = lo - B > 0 ? (int)(lo - B) : 0, rhi = hi - B < BLK ? (int)(hi - B) : BLK;
+        int la, lb;
+        lane_part(rlo, rhi, la, lb);
+        if (la < lb) {
+            Blk k;
+            k.v = *reinterpret_cast<const uint4 *>(a0 + B + lane * 16);
+            acc = ext2<MAX>(acc, vext16_range<MAX>(k.v, la, lb));
         }
     }
-    const uint32_t m = warp_extreme<MAX>(acc_extreme<MAX>(ah, al));
+    const uint32_t m = warp_ext<MAX>(acc);
     // leftmost occurrence: Range Scan with EQ
-    for (int64_t blk = 0; blk < hi; blk += 512) {
-        const int64_t base = blk + lane * 16;
-        uint32_t bits = range_bits(lo - blk > 0 ? (int)(lo - blk) : 0, hi - blk < 512 ? (int)(hi - blk) : 512, lane * 16);
-        uint32_t hit = 0;
-        if (bits) hit = pred_bits16<CMP_EQ>(*reinterpret_cast<const uint4 *>(a0 + base), m) & bits;
-        uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit != 0);
+    for (int64_t B = 0; B < hi; B += BLK) {
+        const int rlo = lo - B > 0 ? (int)(lo - B) : 0, rhi = hi - B < BLK ? (int)(hi - B) : BLK;
+        int la, lb;
+        lane_part(rlo, rhi, la, lb);
+        Blk k;
+        k.v = make_uint4(0, 0, 0, 0);
+        uint32_t le = neutral<MAX>();
+        if (la < lb) {
+            k.v = *reinterpret_cast<const uint4 *>(a0 + B + lane * 16);
+            le = vext16_range<MAX>(k.v, la, lb);
+        }
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, la < lb && le == m);
         if (bal) {
-            int Ln = __ffs(bal) - 1;
-            uint32_t mb = __shfl_sync(0xFFFFFFFFu, hit, Ln);
+            const int q = locate<CMP_EQ>(k, bal, rlo, rhi, m);
             if (lane == 0) {
                 value[r] = (uint8_t)m;
-                pos[r] = (uint64_t)(blk + Ln * 16 + (__ffs(mb) - 1) - lo);
+                pos[r] = (uint64_t)(B + q - lo);
             }
             return;
         }
@@ -618,16 +640,22 @@ __global__ void k_range_scan(const uint8_t *data, const uint64_t *off, const uin
     const uint32_t t = target[r];
     const uint8_t *a0 = reinterpret_cast<const uint8_t *>(reinterpret_cast<uintptr_t>(b) & ~(uintptr_t)15);
     const int64_t lo = b - a0, hi = lo + (int64_t)L;
-    for (int64_t blk = 0; blk < hi; blk += 512) {
-        const int64_t base = blk + lane * 16;
-        uint32_t bits = range_bits(lo - blk > 0 ? (int)(lo - blk) : 0, hi - blk < 512 ? (int)(hi - blk) : 512, lane * 16);
-        uint32_t hit = 0;
-        if (bits) hit = pred_bits16<CMP>(*reinterpret_cast<const uint4 *>(a0 + base), t) & bits;
-        uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit != 0);
+    for (int64_t B = 0; B < hi; B += BLK) {
+        const int rlo = lo - B > 0 ? (int)(lo - B) : 0, rhi = hi - B < BLK ? (int)(hi - B) : BLK;
+        int la, lb;
+        lane_part(rlo, rhi, la, lb);
+        Blk k;
+        k.v = make_uint4(0, 0, 0, 0);
+        bool any = false;
+        if (la < lb) {
+            k.v = *reinterpret_cast<const uint4 *>(a0 + B + lane * 16);
+            // packed scan of the lane's bytes (VCMP + VMASK, §4.2)
+            for (int j = la; j < lb; ++j) any |= cmp_holds<CMP>(vbyte(k.v, j), t);
+        }
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, any);
         if (bal) {
-            int Ln = __ffs(bal) - 1;
-            uint32_t mb = __shfl_sync(0xFFFFFFFFu, hit, Ln);
-            if (lane == 0) pos[r] = (uint64_t)(blk + Ln * 16 + (__ffs(mb) - 1) - lo);
+            const int q = locate<CMP>(k, bal, rlo, rhi, t);
+            if (lane == 0) pos[r] = (uint64_t)(B + q - lo);
             return;
         }
     }
@@ -663,8 +691,6 @@ cudaEvent_t prof_event() {
     }
     return e;
 }
-std::mutex g_mu;
-unsigned long long g_epoch = 0;
 
 int fail(int code, const std::string &msg) {
     g_err = msg;
@@ -703,23 +729,24 @@ int num_sms() {
 
 struct Plan {
     uint64_t S, Hmax, max_segs, cap_list, cap_halo, pool_cap, exc_cap, nfiles;
-    size_t bytes;
+    size_t bytes, reset_bytes;
     size_t off[24];
 };
 
 uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
-// Segment size: about SEGS_PER_SM segments per SM for the total input, at least
-// 64 KiB and 4 max-size chunks, so that the re-synchronisation halo (a few chunks
-// on typical data) is small next to the segment.
-constexpr uint64_t SEGS_PER_SM = 4;
+// Segment size: about SEGS_PER_SM walkers per SM for the total input (so the
+// grid is a whole number of waves of SPEC_WARPS-warp CTAs), a multiple of the
+// TMA stage, at least 64 KiB and 4 max-size chunks, so that the
+// re-synchronisation halo (a few chunks on typical data) is small next to it.
+constexpr uint64_t SEGS_PER_SM = 8;
 
 void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, Plan &P) {
     uint64_t S = p->seg_bytes;
     if (!S) {
-        uint64_t target = (uint64_t)num_sms() * SEGS_PER_SM;
-        S = round_up(total_len / target + 1, 64 << 10);
-        uint64_t lo = std::max<uint64_t>(64 << 10, round_up(4 * p->max_size, cdc::STAGE));
+        const uint64_t target = (uint64_t)num_sms() * SEGS_PER_SM;
+        S = round_up(total_len / target + 1, cdc::STAGE);
+        const uint64_t lo = std::max<uint64_t>(64 << 10, round_up(4 * p->max_size, cdc::STAGE));
         if (S < lo) S = lo;
         if (S > (256ull << 20)) S = 256ull << 20;
     }
@@ -735,11 +762,11 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     P.exc_cap = P.max_segs;
     const uint64_t G = P.max_segs;
     size_t sz[] = {
-        G * P.cap_list * 4,  // 0 list
-        G * P.cap_halo * 4,  // 1 halo
-        G * 4,               // 2 cnt
-        G * 4,               // 3 hcnt
-        G * 8,               // 4 pub
+        G * P.cap_list * 4,  // 0 list   } reset to 0xFF by one memset per call
+        G * 8,               // 1 pub    }
+        G * P.cap_halo * 4,  // 2 halo
+        G * 4,               // 3 cnt
+        G * 4,               // 4 hcnt
         G * 4,               // 5 sj
         G * 4,               // 6 sa
         G * 4,               // 7 sb
@@ -763,16 +790,17 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
         o += round_up(sz[i], 256);
     }
     P.bytes = o;
+    P.reset_bytes = P.off[2];
 }
 
 cdc::Work carve(const Plan &P, void *ws) {
     uint8_t *b = static_cast<uint8_t *>(ws);
     cdc::Work W;
     W.list = (uint32_t *)(b + P.off[0]);
-    W.halo = (uint32_t *)(b + P.off[1]);
-    W.cnt = (uint32_t *)(b + P.off[2]);
-    W.hcnt = (uint32_t *)(b + P.off[3]);
-    W.pub = (unsigned long long *)(b + P.off[4]);
+    W.pub = (unsigned long long *)(b + P.off[1]);
+    W.halo = (uint32_t *)(b + P.off[2]);
+    W.cnt = (uint32_t *)(b + P.off[3]);
+    W.hcnt = (uint32_t *)(b + P.off[4]);
     W.sj = (int32_t *)(b + P.off[5]);
     W.sa = (uint32_t *)(b + P.off[6]);
     W.sb = (uint32_t *)(b + P.off[7]);
@@ -822,6 +850,9 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         ++launches;
         pc.used[0] = true;
     }
+    // reset the published lists (list entries -> LIST_EMPTY, pub -> PUB_OPEN)
+    CDC_CUDA(cudaMemsetAsync(W.list, 0xFF, P.reset_bytes, st));
+    ++launches;
     mark(1);
     const uint64_t nseg_ub = P.max_segs;
     const uint64_t blocks = (nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS;
@@ -869,17 +900,6 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     G.Hmax = P.Hmax;
     G.w = p->window;
     G.max_size = p->max_size;
-    {
-        // 32-bit call tag for the published-list words: a splitmix64 hash of a
-        // process-wide counter, so stale words in a reused workspace (from an
-        // earlier call or other data) match with probability ~2^-32
-        std::lock_guard<std::mutex> lk(g_mu);
-        uint64_t z = (++g_epoch) * 0x9E3779B97F4A7C15ull + reinterpret_cast<uintptr_t>(&g_epoch);
-        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-        z ^= z >> 31;
-        G.epoch = (z & 0xFFFFFFFFull) | 1ull;
-    }
     uint64_t *file_out = batch ? d_bound_off : W.file_out;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (p->algo) {
@@ -922,21 +942,6 @@ int cdc_abi_version(void) { return CDC_ABI_VERSION; }
 const char *cdc_last_error(void) { return g_err.c_str(); }
 
 int cdc_last_launch_count(void) { return g_launches; }
-
-int cdc_debug_progress(void **host_ptr) {
-    // host-mapped progress words (8192 slots x 4 u64) that running kernels update
-    static unsigned long long *h = nullptr;
-    if (!h) {
-        CDC_CUDA(cudaHostAlloc((void **)&h, 8192 * 32, cudaHostAllocMapped));
-        memset(h, 0, 8192 * 32);
-        unsigned long long *d = nullptr;
-        CDC_CUDA(cudaHostGetDevicePointer((void **)&d, h, 0));
-        CDC_CUDA(cudaMemcpyToSymbol(cdc::g_dbg, &d, sizeof(d)));
-        CDC_CUDA(cudaMemcpyToSymbol(cdc::g_dbg_fwd, &d, sizeof(d)));
-    }
-    if (host_ptr) *host_ptr = h;
-    return CDC_OK;
-}
 
 int cdc_profile_query(int *done) {
     // completion state of the events of the last profiled call (1 = reached)
