@@ -25,9 +25,9 @@ namespace cdc {
 
 constexpr int BLK = 512;               // bytes per warp block: 32 lanes x 16 B
 constexpr int STAGE = 4096;            // bytes per TMA stage (8 warp blocks)
-constexpr int NST = 4;                 // ring depth per warp (16 KiB)
+constexpr int NST = 3;                 // ring depth per warp (12 KiB)
 constexpr int RING_BYTES = STAGE * NST;
-constexpr int RING_SMEM = RING_BYTES + NST * 8;
+constexpr int RING_SMEM = (RING_BYTES + NST * 8 + 127) / 128 * 128;  // keeps every ring 128-byte aligned
 
 enum { ALGO_RAM = 0, ALGO_AE_MAX = 1, ALGO_AE_MIN = 2 };
 enum { CMP_GT = 0, CMP_GEQ = 1, CMP_LT = 2, CMP_LEQ = 3, CMP_EQ = 4 };
@@ -35,6 +35,9 @@ enum { CMP_GT = 0, CMP_GEQ = 1, CMP_LT = 2, CMP_LEQ = 3, CMP_EQ = 4 };
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_inval(uint64_t *bar) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
@@ -236,6 +239,20 @@ struct WarpRing {
 
 // ---------------------------------------------------------------- chain engine
 //
+// L2 policies of the ring's bulk copies: bytes below keep_until (a segment's
+// head, which the previous segment's halo walk reads again) are loaded with
+// `keep`, the rest with `stream` (evict-first: read once).
+struct L2Pol {
+    uint64_t stream, keep;
+    int64_t keep_until;
+};
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ L2Pol stream_policy() { return L2Pol{l2_evict_first_policy(), 0, INT64_MIN}; }
+
 // run_chain walks the chunk chain of the stream fbase[0..Lf) that begins with
 // a chunk at `start` (0 <= start < Lf).  Every boundary e < Lf (the start of
 // the next chunk) is passed to emit.boundary(e), which returns true to stop
@@ -251,11 +268,16 @@ struct WarpRing {
 //           d[t] the chunk ends at t+w+1, else t = first byte of (t, t+w]
 //           exceeding d[t]; once t + w >= limit it ends at limit.  (AE-Min:
 //           "less" for "exceeds".)
+//
+// Inside a stage every position is an int offset from the stage's first byte
+// (horizons beyond the stage clamp to FAR); the chain state between events is
+// kept as 64-bit stream positions.
 template <int ALGO, class Emit>
 __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf, int64_t start,
-                          int64_t read_end, uint32_t w, uint64_t max_size, uint64_t policy, Emit &emit) {
+                          int64_t read_end, uint32_t w, uint64_t max_size, const L2Pol &pol, Emit &emit) {
     constexpr bool MAX = (ALGO != ALGO_AE_MIN);
     constexpr uint32_t SAT = MAX ? 255u : 0u;  // a target nothing can beat
+    constexpr int FAR = 1 << 30;
     const int lane = lane_id();
     if (read_end > Lf) read_end = Lf;
     const uint8_t *g0 = reinterpret_cast<const uint8_t *>(reinterpret_cast<uintptr_t>(fbase + start) &
@@ -277,24 +299,24 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
             const int64_t off = k * STAGE;
             const uint32_t bytes = (uint32_t)(nbytes - off < STAGE ? nbytes - off : STAGE);
             mbar_arrive_expect_tx(&R.bar[slot], bytes);
-            tma_load_1d(R.buf + slot * STAGE, g0 + off, bytes, &R.bar[slot], policy);
+            tma_load_1d(R.buf + slot * STAGE, g0 + off, bytes, &R.bar[slot],
+                        B0 + off < pol.keep_until ? pol.keep : pol.stream);
         }
     };
     for (; issued < nstages && issued < NST; ++issued) issue(issued);
 
     const int64_t W = (int64_t)w;
     const bool fastrec = w >= (uint32_t)(BLK - 1);  // AE: records inside one block never miss a deadline
+    // chain state (stream positions)
     int64_t s = start;                                                           // current chunk start
     int64_t limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;  // chunk end bound
     int64_t c = s;                                                               // next byte to examine
     bool stop = false;
-    // RAM state
-    bool scanning = false;  // false: window [s, s+w); true: scan for a byte >= M
+    bool scanning = false;  // RAM: false = window [s, s+w), true = scan for a byte >= M
     uint32_t M = 0, acc = 0;
-    // AE state
-    uint32_t ext = 0;
-    int64_t t = 0;
-    bool pending = true;  // the chunk's first byte is the first target
+    uint32_t ext = 0;       // AE: current target value
+    int64_t t = 0;          // AE: current target position
+    bool pending = true;    // AE: the chunk's first byte is the first target
 
     if constexpr (ALGO == ALGO_RAM) {
         if (s + W >= Lf) {  // window does not fit: a single final chunk
@@ -329,96 +351,150 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     int64_t k = 0;
     while (!stop && k < nstages) {
         const int slot = (int)(k % NST);
-        mbar_wait(&R.bar[slot], (uint32_t)((k / NST) & 1));
-        const uint8_t *sp = R.buf + slot * STAGE;
         const int64_t SB = B0 + k * STAGE;
-        const int b0 = (int)((c - SB) >> 9) > 0 ? (int)((c - SB) >> 9) : 0;
+        const int64_t SE = SB + STAGE;
+        // a saturated AE target skips whole stages without reading them
+        bool skip = c >= SE;
+        if constexpr (ALGO != ALGO_RAM) {
+            if (!skip && !pending && ext == SAT) {
+                const int64_t h = (t + W + 1 < limit) ? t + W + 1 : limit;
+                if (h >= SE && read_end >= SE) {
+                    c = SE;
+                    skip = true;
+                }
+            }
+        }
+        mbar_wait(&R.bar[slot], (uint32_t)((k / NST) & 1));
+        if (!skip) {
+            const uint8_t *sp = R.buf + slot * STAGE;
+            auto rel = [&](int64_t x) -> int {  // x >= SB
+                const int64_t d = x - SB;
+                return d > FAR ? FAR : (int)d;
+            };
+            const int endr = rel(read_end) < STAGE ? rel(read_end) : STAGE;
+            int cr = (int)(c - SB);
+            int limr = rel(limit);
+            int hor = 0;  // RAM: window end s+w (not scanning); AE: deadline t+w+1
+            if constexpr (ALGO == ALGO_RAM) {
+                hor = scanning ? FAR : rel(s + W);
+            } else {
+                hor = pending ? FAR : rel(t + W + 1);
+            }
+            // event at stage offset er: update the chain state and the stage views
+            auto event = [&](int er) -> bool {
+                if (on_boundary(SB + er)) return true;
+                cr = er;
+                limr = rel(limit);
+                if constexpr (ALGO == ALGO_RAM) hor = rel(s + W);
+                else hor = FAR;
+                return false;
+            };
 #pragma unroll 1
-        for (int bi = b0; bi < STAGE / BLK && !stop; ++bi) {
-            Blk blk;
-            blk.B = SB + bi * BLK;
-            int64_t Bend = blk.B + BLK;
-            if (Bend > read_end) Bend = read_end;
-            if (c >= Bend) continue;
-            blk.v = *reinterpret_cast<const uint4 *>(sp + bi * BLK + lane * 16);
-            const uint32_t full = vext16<MAX>(blk.v);
-            while (c < Bend) {
-                if constexpr (ALGO == ALGO_RAM) {
-                    if (!scanning) {
-                        const int64_t we = s + W;
-                        const int64_t hi = we < Bend ? we : Bend;
-                        bool has;
-                        acc = ext2<true>(acc, lane_ext<true>(blk, full, (int)(c - blk.B), (int)(hi - blk.B), has));
-                        c = hi;
-                        if (c == we) {
-                            M = warp_ext<true>(acc);
-                            scanning = true;
+            for (int Bk = (cr >> 9) << 9; Bk < endr && !stop; Bk += BLK) {
+                const int Be = Bk + BLK < endr ? Bk + BLK : endr;
+                if constexpr (ALGO != ALGO_RAM) {
+                    if (!pending && ext == SAT) {  // skip to the event horizon without loading
+                        const int h = hor < limr ? hor : limr;
+                        if (h >= Be) {
+                            cr = Be;
+                            continue;
+                        }
+                        if (h > cr) cr = h;
+                    }
+                }
+                Blk blk;
+                blk.B = SB + Bk;
+                blk.v = *reinterpret_cast<const uint4 *>(sp + Bk + lane * 16);
+                const uint32_t full = vext16<MAX>(blk.v);
+                while (cr < Be) {
+                    if constexpr (ALGO == ALGO_RAM) {
+                        if (!scanning) {
+                            const int hi = hor < Be ? hor : Be;
+                            if (cr == Bk && hi == Bk + BLK) {
+                                acc = max(acc, full);
+                            } else {
+                                bool has;
+                                acc = max(acc, lane_ext<true>(blk, full, cr - Bk, hi - Bk, has));
+                            }
+                            cr = hi;
+                            if (cr == hor) {
+                                M = warp_ext<true>(acc);
+                                scanning = true;
+                                hor = FAR;
+                            }
+                        } else {
+                            const int hi = limr < Be ? limr : Be;
+                            uint32_t bal;
+                            if (cr == Bk && hi == Bk + BLK) {
+                                bal = __ballot_sync(0xFFFFFFFFu, full >= M);
+                            } else {
+                                bool has;
+                                const uint32_t lm = lane_ext<true>(blk, full, cr - Bk, hi - Bk, has);
+                                bal = __ballot_sync(0xFFFFFFFFu, has && lm >= M);
+                            }
+                            int er;
+                            if (bal) {
+                                er = Bk + locate<CMP_GEQ>(blk, bal, cr - Bk, hi - Bk, M) + 1;  // boundary byte ends the chunk
+                            } else {
+                                cr = hi;
+                                if (cr != limr) continue;
+                                er = limr;  // cap or end of stream
+                            }
+                            if (event(er)) {
+                                stop = true;
+                                break;
+                            }
                         }
                     } else {
-                        const int64_t hi = limit < Bend ? limit : Bend;
-                        const int rlo = (int)(c - blk.B), rhi = (int)(hi - blk.B);
-                        bool has;
-                        const uint32_t lm = lane_ext<true>(blk, full, rlo, rhi, has);
-                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has && lm >= M);
-                        int64_t e;
-                        if (bal) {
-                            e = blk.B + locate<CMP_GEQ>(blk, bal, rlo, rhi, M) + 1;  // boundary byte ends the chunk
-                        } else {
-                            c = hi;
-                            if (c != limit) continue;
-                            e = limit;  // cap or end of stream
+                        if (pending) {  // first byte of the chunk: the first target
+                            ext = byte_at(blk, cr - Bk);
+                            t = SB + cr;
+                            ++cr;
+                            hor = rel(t + W + 1);
+                            pending = false;
+                            continue;
                         }
-                        if (on_boundary(e)) {
+                        int hi = hor < limr ? hor : limr;
+                        hi = hi < Be ? hi : Be;
+                        if (ext != SAT) {
+                            const int rlo = cr - Bk, rhi = hi - Bk;
+                            bool has = true;
+                            const uint32_t lm =
+                                (rlo == 0 && rhi == BLK) ? full : lane_ext<MAX>(blk, full, rlo, rhi, has);
+                            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has && beats<MAX>(lm, ext));
+                            if (bal) {
+                                if (fastrec) {
+                                    // every record of [cr, hi) follows its predecessor within
+                                    // < BLK <= w+1 bytes, so the last one -- the first
+                                    // occurrence of the range extreme -- is the new target
+                                    const uint32_t m = warp_ext<MAX>(has ? lm : neutral<MAX>());
+                                    const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, has && lm == m);
+                                    t = blk.B + locate<CMP_EQ>(blk, b2, rlo, rhi, m);
+                                    ext = m;
+                                    cr = hi;
+                                } else {
+                                    const int r = locate<MAX ? CMP_GT : CMP_LT>(blk, bal, rlo, rhi, ext);
+                                    t = blk.B + r;
+                                    ext = byte_at(blk, r);
+                                    cr = Bk + r + 1;
+                                }
+                                hor = rel(t + W + 1);
+                                continue;
+                            }
+                        }
+                        cr = hi;
+                        int er;
+                        if (cr == hor && hor <= limr) er = hor;  // target unbeaten over its window
+                        else if (cr == limr) er = limr;         // cap or end of stream
+                        else continue;                          // block exhausted
+                        if (event(er)) {
                             stop = true;
                             break;
                         }
                     }
-                } else {
-                    if (pending) {  // first byte of the chunk: the first target
-                        ext = byte_at(blk, (int)(c - blk.B));
-                        t = c;
-                        ++c;
-                        pending = false;
-                        continue;
-                    }
-                    const int64_t dl = t + W + 1;  // window (t, t+w] ends before dl
-                    int64_t hi = dl < limit ? dl : limit;
-                    hi = hi < Bend ? hi : Bend;
-                    if (ext != SAT) {
-                        const int rlo = (int)(c - blk.B), rhi = (int)(hi - blk.B);
-                        bool has;
-                        const uint32_t lm = lane_ext<MAX>(blk, full, rlo, rhi, has);
-                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has && beats<MAX>(lm, ext));
-                        if (bal) {
-                            if (fastrec) {
-                                // every record of [c, hi) follows its predecessor within
-                                // < BLK <= w+1 bytes, so the last one -- the first
-                                // occurrence of the range extreme -- is the new target
-                                const uint32_t m = warp_ext<MAX>(lm);
-                                const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, has && lm == m);
-                                t = blk.B + locate<CMP_EQ>(blk, b2, rlo, rhi, m);
-                                ext = m;
-                                c = hi;
-                            } else {
-                                const int r = locate<MAX ? CMP_GT : CMP_LT>(blk, bal, rlo, rhi, ext);
-                                t = blk.B + r;
-                                ext = byte_at(blk, r);
-                                c = t + 1;
-                            }
-                            continue;
-                        }
-                    }
-                    c = hi;
-                    int64_t e;
-                    if (c == dl && dl <= limit) e = dl;  // target unbeaten over its window
-                    else if (c == limit) e = limit;      // cap or end of stream
-                    else continue;                       // block exhausted
-                    if (on_boundary(e)) {
-                        stop = true;
-                        break;
-                    }
                 }
             }
+            c = SB + cr;
         }
         __syncwarp();
         ++k;
@@ -434,6 +510,9 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     }
     // drain copies still in flight before the ring is reused or the CTA exits
     for (int64_t j = k; j < issued; ++j) mbar_wait(&R.bar[j % NST], (uint32_t)((j / NST) & 1));
+    __syncwarp();
+    if (lane == 0)
+        for (int i = 0; i < NST; ++i) mbar_inval(&R.bar[i]);  // the ring may be re-initialised by the caller
     __syncwarp();
 }
 

@@ -21,6 +21,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -31,6 +32,7 @@
 namespace cdc {
 
 constexpr int SPEC_WARPS = 4;     // warps (segments) per CTA in k_speculate
+constexpr int HEAD_KEEP = 16384;  // bytes of each segment head kept in L2 for the halo re-read
 constexpr int RESOLVE_THREADS = 1024;
 
 // ------------------------------------------------------------------ workspace
@@ -50,12 +52,19 @@ struct Work {
     uint32_t *ranges;            // skip ranges (pairs)
     uint64_t *pool;              // walker-produced starts (file relative)
     uint64_t *seg_first;         // nfiles+1 (batch)
+    uint32_t *seg_file;          // G: file of each segment (batch)
     uint64_t *file_out;          // nfiles+1 (single stream: internal)
     uint32_t *misc;              // [0] G, [1] n_exc, [2] n_ranges, [3] overflow flags
     uint64_t cap_list, cap_halo, pool_cap, max_segs, exc_cap;
 };
 
 enum : int32_t { SJ_UNSYNCED = -1, SJ_STREAM_END = -2, SJ_LAST = -3 };
+
+// dynamic shared memory follows the kernel's static shared variables: round the
+// ring up to 128 bytes (TMA destinations need 16, LDS.128 16; launches add 128)
+__device__ __forceinline__ uint8_t *align_smem(uint8_t *p) {
+    return reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(p) + 127) & ~static_cast<uintptr_t>(127));
+}
 
 struct Geometry {
     const uint8_t *data;
@@ -92,16 +101,10 @@ __device__ __forceinline__ void seg_first_of(const Geometry &G, const Work &W, u
 __device__ __forceinline__ uint64_t total_segs(const Geometry &G, const Work &W) {
     return G.file_off == nullptr ? nseg_of(G.L, G.S) : W.seg_first[G.nfiles];
 }
-// file containing segment g: last f with seg_first[f] <= g (files with segments only)
+// file containing segment g (batch: the map written by k_seg_prefix)
 __device__ __forceinline__ uint64_t file_of_seg(const Geometry &G, const Work &W, uint64_t g) {
     if (G.file_off == nullptr) return 0;
-    uint64_t lo = 0, hi = G.nfiles;  // seg_first[lo] <= g < seg_first[hi]
-    while (hi - lo > 1) {
-        uint64_t mid = (lo + hi) >> 1;
-        if (W.seg_first[mid] <= g) lo = mid;
-        else hi = mid;
-    }
-    return lo;
+    return W.seg_file[g];
 }
 
 struct SegInfo {
@@ -227,7 +230,7 @@ struct SpecEmit {
 };
 
 template <int ALGO>
-__global__ void __launch_bounds__(SPEC_WARPS * 32) k_speculate(Geometry G, Work W) {
+__global__ void __launch_bounds__(SPEC_WARPS * 32, 4) k_speculate(Geometry G, Work W) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const uint64_t g = (uint64_t)blockIdx.x * SPEC_WARPS + warp;
@@ -254,7 +257,9 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32) k_speculate(Geometry G, Work 
     const uint8_t *fbase = G.data + em.I.foff;
     int64_t read_end = (g == em.I.last) ? (int64_t)em.I.Lf
                                         : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
-    run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, l2_evict_first_policy(), em);
+    // the segment's head is read again by the previous segment's halo walk: keep it in L2
+    const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
+    run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
     em.publish();
     if (lane_id() == 0) {
         W.cnt[g] = em.cnt;
@@ -332,155 +337,199 @@ __device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t &t
     return warp_prefix + x - v;
 }
 
+constexpr int RPT = 8;  // k_resolve: consecutive segments per thread in the count scan
+
+// Re-check the halo of segment g (left undecided by K1) against the complete lists.
+__device__ void recheck_halo(const Geometry &G, Work &W, uint64_t g) {
+    const int lane = lane_id();
+    SegInfo I = seg_info(G, W, g);
+    const uint32_t hc = W.hcnt[g];
+    int64_t cur_j = -1;
+    uint32_t cursor = 0;
+    for (uint32_t i = 0; i < hc; ++i) {
+        const int64_t e = I.seg_end + (int64_t)W.halo[g * W.cap_halo + i];
+        const int64_t j = (int64_t)g + 1 + (e - I.seg_end) / (int64_t)G.S;
+        if (j != cur_j) {
+            cur_j = j;
+            cursor = 0;
+        }
+        const int64_t pj = I.seg_end + (j - (int64_t)g - 1) * (int64_t)G.S;
+        uint32_t idx = 0;
+        if (list_lookup(W.list + (uint64_t)j * W.cap_list, W.cap_list, W.pub + j, (uint32_t)(e - pj), cursor,
+                        idx) == 1) {
+            if (lane == 0) {
+                W.sj[g] = (int32_t)j;
+                W.sa[g] = i;
+                W.sb[g] = idx;
+            }
+            break;
+        }
+    }
+}
+
+// K2: one CTA.  Common case (every segment's chain re-synchronised with the
+// next segment's): two coalesced passes -- classify, then per-segment output
+// counts and their exclusive scan.  Exceptional segments (a sync target other
+// than the next segment, or an undecided halo) take the serial path.
 template <int ALGO>
 __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W, uint64_t *d_count,
                                                              uint64_t *file_out) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t scratch[64];
     __shared__ uint64_t s_carry;
+    __shared__ int s_flags;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = blockDim.x >> 5;
     const uint64_t nsegs = total_segs(G, W);
 
-    // 1. halos left undecided by K1: every list is complete now
-    for (uint64_t g = warp; g < nsegs; g += nwarps) {
-        if (W.sj[g] != SJ_UNSYNCED) continue;
-        SegInfo I = seg_info(G, W, g);
-        const uint32_t hc = W.hcnt[g];
-        int64_t cur_j = -1;
-        uint32_t cursor = 0;
-        for (uint32_t i = 0; i < hc; ++i) {
-            const int64_t e = I.seg_end + (int64_t)W.halo[g * W.cap_halo + i];
-            const int64_t j = (int64_t)g + 1 + (e - I.seg_end) / (int64_t)G.S;
-            if (j != cur_j) {
-                cur_j = j;
-                cursor = 0;
-            }
-            const int64_t pj = I.seg_end + (j - (int64_t)g - 1) * (int64_t)G.S;
-            uint32_t idx = 0;
-            if (list_lookup(W.list + (uint64_t)j * W.cap_list, W.cap_list, W.pub + j, (uint32_t)(e - pj), cursor,
-                            idx) == 1) {
-                if (lane == 0) {
-                    W.sj[g] = (int32_t)j;
-                    W.sa[g] = i;
-                    W.sb[g] = idx;
-                }
-                break;
-            }
-        }
-    }
-    for (uint64_t g = tid; g < nsegs; g += blockDim.x) {
-        W.skipped[g] = 0;
-        W.wcnt[g] = 0;
-        W.jump_entry[g] = 0;
-    }
+    // 1. classify (32 consecutive segments per warp step, coalesced); re-check
+    //    undecided halos now that every list is complete
+    if (tid == 0) s_flags = 0;
     __syncthreads();
-
-    // 2. compact the exceptional segments (sync target other than the next segment) in order
-    if (tid == 0) s_carry = 0;
-    __syncthreads();
-    for (uint64_t base = 0; base < nsegs; base += blockDim.x) {
-        uint64_t g = base + tid;
-        uint64_t flag = 0;
-        if (g < nsegs) {
-            int32_t sj = W.sj[g];
-            flag = (sj != SJ_LAST && sj != (int32_t)(g + 1)) ? 1 : 0;
+    int fl = 0;
+    for (uint64_t g0 = (uint64_t)warp * 32; g0 < nsegs; g0 += (uint64_t)nwarps * 32) {
+        const uint64_t g = g0 + lane;
+        const int32_t sj0 = g < nsegs ? W.sj[g] : SJ_LAST;
+        uint32_t un = __ballot_sync(0xFFFFFFFFu, sj0 == SJ_UNSYNCED);
+        while (un) {
+            const int L = __ffs(un) - 1;
+            un &= un - 1;
+            recheck_halo(G, W, g0 + L);
         }
-        uint64_t tot;
-        uint64_t pos = block_exclusive_scan(flag, tot, scratch) + s_carry;
-        if (flag && pos < W.exc_cap) W.exc[pos] = (uint32_t)g;
-        __syncthreads();
-        if (tid == 0) s_carry += tot;
-        __syncthreads();
+        __syncwarp();
+        const int32_t sj = g < nsegs ? W.sj[g] : SJ_LAST;
+        if (sj != SJ_LAST && sj != (int32_t)(g + 1)) fl = 1;
     }
-    const uint64_t n_exc = s_carry;
+    if (fl) atomicOr(&s_flags, 1);
+    __syncthreads();
+    const bool exc = s_flags != 0;
 
-    // 3. serial resolution of the exceptional segments on the true chain (warp 0);
-    //    unsynced halos are continued by a walker until they meet a later chain
-    if (warp == 0) {
-        WarpRing R{smem, reinterpret_cast<uint64_t *>(smem + RING_BYTES)};
-        uint64_t reach = 0, nranges = 0, pool_used = 0;
-        bool overflow = n_exc > W.exc_cap;
-        for (uint64_t x = 0; x < n_exc && x < W.exc_cap; ++x) {
-            const uint64_t g = W.exc[x];
-            if (g < reach) continue;  // skipped by an earlier jump: not on the true chain
-            SegInfo I = seg_info(G, W, g);
-            int32_t sj = W.sj[g];
-            if (sj == SJ_UNSYNCED) {
-                WalkEmit em;
-                em.G = &G;
-                em.W = &W;
-                em.I = I;
-                em.base = pool_used;
-                em.n = 0;
-                em.sj = SJ_STREAM_END;
-                em.sb = 0;
-                em.cur_j = -1;
-                em.cursor = 0;
-                em.overflow = false;
-                // resume the chain from its last recorded start
-                const uint32_t hc = W.hcnt[g];
-                const int64_t last = hc ? I.seg_end + (int64_t)W.halo[g * W.cap_halo + hc - 1]
-                                        : I.p + (int64_t)W.list[g * W.cap_list + W.cnt[g] - 1];
-                run_chain<ALGO>(R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
-                                l2_evict_first_policy(), em);
-                overflow |= em.overflow;
-                sj = em.sj;
-                if (lane == 0) {
-                    W.sj[g] = sj;
-                    W.sa[g] = W.hcnt[g];
-                    W.sb[g] = em.sb;
-                    W.wcnt[g] = (uint32_t)em.n;
-                    W.woff[g] = em.base;
-                }
-                pool_used += em.n;
-                if (sj == (int32_t)(g + 1)) continue;  // met the next segment's chain: no skip
+    if (exc) {
+        for (uint64_t g = tid; g < nsegs; g += blockDim.x) {
+            W.skipped[g] = 0;
+            W.wcnt[g] = 0;
+            W.jump_entry[g] = 0;
+        }
+        __syncthreads();
+        // 2. compact the exceptional segments in order
+        if (tid == 0) s_carry = 0;
+        __syncthreads();
+        for (uint64_t base = 0; base < nsegs; base += blockDim.x) {
+            uint64_t g = base + tid;
+            uint64_t flag = 0;
+            if (g < nsegs) {
+                int32_t sj = W.sj[g];
+                flag = (sj != SJ_LAST && sj != (int32_t)(g + 1)) ? 1 : 0;
             }
-            const uint64_t target = (sj == SJ_STREAM_END) ? I.last + 1 : (uint64_t)sj;
+            uint64_t tot;
+            uint64_t pos = block_exclusive_scan(flag, tot, scratch) + s_carry;
+            if (flag && pos < W.exc_cap) W.exc[pos] = (uint32_t)g;
+            __syncthreads();
+            if (tid == 0) s_carry += tot;
+            __syncthreads();
+        }
+        const uint64_t n_exc = s_carry;
+
+        // 3. serial resolution of the exceptional segments on the true chain (warp 0);
+        //    unsynced halos are continued by a walker until they meet a later chain
+        if (warp == 0) {
+            uint8_t *rb = align_smem(smem);
+            WarpRing R{rb, reinterpret_cast<uint64_t *>(rb + RING_BYTES)};
+            uint64_t reach = 0, nranges = 0, pool_used = 0;
+            bool overflow = n_exc > W.exc_cap;
+            for (uint64_t x = 0; x < n_exc && x < W.exc_cap; ++x) {
+                const uint64_t g = W.exc[x];
+                if (g < reach) continue;  // skipped by an earlier jump: not on the true chain
+                SegInfo I = seg_info(G, W, g);
+                int32_t sj = W.sj[g];
+                if (sj == SJ_UNSYNCED) {
+                    WalkEmit em;
+                    em.G = &G;
+                    em.W = &W;
+                    em.I = I;
+                    em.base = pool_used;
+                    em.n = 0;
+                    em.sj = SJ_STREAM_END;
+                    em.sb = 0;
+                    em.cur_j = -1;
+                    em.cursor = 0;
+                    em.overflow = false;
+                    // resume the chain from its last recorded start
+                    const uint32_t hc = W.hcnt[g];
+                    const int64_t last = hc ? I.seg_end + (int64_t)W.halo[g * W.cap_halo + hc - 1]
+                                            : I.p + (int64_t)W.list[g * W.cap_list + W.cnt[g] - 1];
+                    run_chain<ALGO>(R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
+                                    stream_policy(), em);
+                    overflow |= em.overflow;
+                    sj = em.sj;
+                    if (lane == 0) {
+                        W.sj[g] = sj;
+                        W.sa[g] = W.hcnt[g];
+                        W.sb[g] = em.sb;
+                        W.wcnt[g] = (uint32_t)em.n;
+                        W.woff[g] = em.base;
+                    }
+                    pool_used += em.n;
+                    if (sj == (int32_t)(g + 1)) continue;  // met the next segment's chain: no skip
+                }
+                const uint64_t target = (sj == SJ_STREAM_END) ? I.last + 1 : (uint64_t)sj;
+                if (lane == 0) {
+                    W.ranges[2 * nranges] = (uint32_t)(g + 1);
+                    W.ranges[2 * nranges + 1] = (uint32_t)target;
+                    if (sj >= 0) W.jump_entry[target] = W.sb[g];
+                }
+                ++nranges;
+                reach = target;
+            }
             if (lane == 0) {
-                W.ranges[2 * nranges] = (uint32_t)(g + 1);
-                W.ranges[2 * nranges + 1] = (uint32_t)target;
-                if (sj >= 0) W.jump_entry[target] = W.sb[g];
+                W.misc[2] = (uint32_t)nranges;
+                W.misc[3] = overflow ? 1u : 0u;
             }
-            ++nranges;
-            reach = target;
         }
-        if (lane == 0) {
-            W.misc[2] = (uint32_t)nranges;
-            W.misc[3] = overflow ? 1u : 0u;
+        __syncthreads();
+
+        // 4. mark segments the true chain jumps over
+        const uint32_t nranges = W.misc[2];
+        for (uint32_t r = warp; r < nranges; r += nwarps) {
+            const uint32_t a = W.ranges[2 * r], b = W.ranges[2 * r + 1];
+            for (uint32_t g = a + lane; g < b; g += 32) W.skipped[g] = 1;
         }
+        __syncthreads();
     }
-    __syncthreads();
+    if (tid == 0) W.misc[4] = exc ? 1u : 0u;  // k_write: skipped / wcnt are valid only if set
 
-    // 4. mark segments the true chain jumps over
-    const uint32_t nranges = W.misc[2];
-    for (uint32_t r = warp; r < nranges; r += nwarps) {
-        const uint32_t a = W.ranges[2 * r], b = W.ranges[2 * r + 1];
-        for (uint32_t g = a + lane; g < b; g += 32) W.skipped[g] = 1;
-    }
-    __syncthreads();
-
-    // 5. per-segment output counts and their exclusive scan
+    // 5. per-segment output counts (RPT consecutive segments per thread) and their exclusive scan
     if (tid == 0) s_carry = 0;
     __syncthreads();
-    for (uint64_t base = 0; base < nsegs; base += blockDim.x) {
-        const uint64_t g = base + tid;
-        uint64_t n = 0;
-        if (g < nsegs && !W.skipped[g]) {
-            SegInfo I = seg_info(G, W, g);
-            uint32_t e = 0;
-            if (g != I.first) e = W.skipped[g - 1] ? W.jump_entry[g] : W.sb[g - 1];
-            const int32_t sj = W.sj[g];
-            uint32_t tail = 0;
-            if (sj == SJ_STREAM_END) tail = W.hcnt[g];
-            else if (sj >= 0) tail = W.sa[g];
-            W.entry[g] = e;
-            W.tail[g] = tail;
-            n = (uint64_t)(W.cnt[g] - e) + tail + W.wcnt[g];
+    const uint64_t TILE = (uint64_t)blockDim.x * RPT;
+    for (uint64_t base = 0; base < nsegs; base += TILE) {
+        uint32_t nloc[RPT];
+        uint64_t tsum = 0;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const uint64_t g = base + (uint64_t)tid * RPT + i;
+            uint32_t n = 0;
+            if (g < nsegs && !(exc && W.skipped[g])) {
+                const bool first = G.file_off == nullptr ? g == 0 : W.seg_first[W.seg_file[g]] == g;
+                uint32_t e = 0;
+                if (!first) e = (exc && W.skipped[g - 1]) ? W.jump_entry[g] : W.sb[g - 1];
+                const int32_t sj = W.sj[g];
+                const uint32_t tail = sj == SJ_STREAM_END ? W.hcnt[g] : (sj >= 0 ? W.sa[g] : 0u);
+                W.entry[g] = e;
+                W.tail[g] = tail;
+                n = (W.cnt[g] - e) + tail + (exc ? W.wcnt[g] : 0u);
+            }
+            nloc[i] = n;
+            tsum += n;
         }
         uint64_t tot;
-        uint64_t pos = block_exclusive_scan(n, tot, scratch) + s_carry;
-        if (g < nsegs) W.seg_out[g] = pos;
+        uint64_t pos = block_exclusive_scan(tsum, tot, scratch) + s_carry;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const uint64_t g = base + (uint64_t)tid * RPT + i;
+            if (g < nsegs) W.seg_out[g] = pos;
+            pos += nloc[i];
+        }
         __syncthreads();
         if (tid == 0) s_carry += tot;
         __syncthreads();
@@ -510,8 +559,9 @@ __global__ void k_write(Geometry G, Work W, const uint64_t *file_out, uint64_t *
         const uint64_t q = file_out[I.f + 1] - 1;  // a stream's last boundary is its length
         if (q < cap) bounds[q] = I.Lf;
     }
-    if (W.skipped[g]) return;
-    const uint32_t e = W.entry[g], cnt = W.cnt[g], tail = W.tail[g], wc = W.wcnt[g];
+    const bool exc = W.misc[4] != 0;
+    if (exc && W.skipped[g]) return;
+    const uint32_t e = W.entry[g], cnt = W.cnt[g], tail = W.tail[g], wc = exc ? W.wcnt[g] : 0u;
     const uint64_t A = cnt - e, n = A + tail + wc, base = W.seg_out[g];
     const uint32_t *lst = W.list + g * W.cap_list;
     const uint32_t *hl = W.halo + g * W.cap_halo;
@@ -528,7 +578,8 @@ __global__ void k_write(Geometry G, Work W, const uint64_t *file_out, uint64_t *
 
 // ------------------------------------------------------------------ K0 batch segment table
 __global__ void __launch_bounds__(RESOLVE_THREADS) k_seg_prefix(const uint64_t *file_off, uint64_t nfiles,
-                                                                uint64_t S, uint64_t *seg_first) {
+                                                                uint64_t S, uint64_t *seg_first,
+                                                                uint32_t *seg_file) {
     __shared__ uint64_t scratch[64];
     __shared__ uint64_t s_carry;
     if (threadIdx.x == 0) s_carry = 0;
@@ -539,7 +590,10 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_seg_prefix(const uint64_t *
         if (f < nfiles) n = nseg_of(file_off[f + 1] - file_off[f], S);
         uint64_t tot;
         uint64_t pos = block_exclusive_scan(n, tot, scratch) + s_carry;
-        if (f < nfiles) seg_first[f] = pos;
+        if (f < nfiles) {
+            seg_first[f] = pos;
+            for (uint64_t i = 0; i < n; ++i) seg_file[pos + i] = (uint32_t)f;  // segment -> file map
+        }
         __syncthreads();
         if (threadIdx.x == 0) s_carry += tot;
         __syncthreads();
@@ -570,13 +624,13 @@ __global__ void __launch_bounds__(32) k_chain(const uint8_t *data, uint64_t len,
                                               uint32_t w, uint64_t max_size, uint64_t *out, uint64_t cap,
                                               uint64_t *count) {
     extern __shared__ __align__(128) uint8_t smem[];
-    WarpRing R{smem, reinterpret_cast<uint64_t *>(smem + RING_BYTES)};
+    uint8_t *rb = align_smem(smem);
+    WarpRing R{rb, reinterpret_cast<uint64_t *>(rb + RING_BYTES)};
     ChainEmit em{out, cap, 0, (int64_t)stop, (int64_t)len};
     if (lane_id() == 0 && cap > 0) out[0] = start;
     em.n = 1;
     if (start < stop && start < len)
-        run_chain<ALGO>(R, data, (int64_t)len, (int64_t)start, (int64_t)len, w, max_size, l2_evict_first_policy(),
-                        em);
+        run_chain<ALGO>(R, data, (int64_t)len, (int64_t)start, (int64_t)len, w, max_size, stream_policy(), em);
     if (lane_id() == 0) *count = em.n;
 }
 
@@ -705,6 +759,25 @@ int cuda_fail(cudaError_t e, const char *where) {
         if (_e != cudaSuccess) return cuda_fail(_e, #call); \
     } while (0)
 
+// CDC_SYNC_DEBUG=1 in the environment: synchronise after every kernel and name
+// the one that failed (debugging aid; never set in measurements).
+bool sync_debug() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CDC_SYNC_DEBUG");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+#define CDC_KCHECK(name, st)                                                   \
+    do {                                                                       \
+        if (sync_debug()) {                                                    \
+            cudaError_t _e = cudaStreamSynchronize(st);                        \
+            if (_e == cudaSuccess) _e = cudaGetLastError();                    \
+            if (_e != cudaSuccess) return cuda_fail(_e, name);                 \
+        }                                                                      \
+    } while (0)
+
 int check_params(const cdc_params *p) {
     if (!p) return fail(CDC_ERR_INVALID, "null params");
     if (p->algo < CDC_RAM || p->algo > CDC_AE_MIN) return fail(CDC_ERR_INVALID, "unknown algorithm");
@@ -739,7 +812,7 @@ uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 // grid is a whole number of waves of SPEC_WARPS-warp CTAs), a multiple of the
 // TMA stage, at least 64 KiB and 4 max-size chunks, so that the
 // re-synchronisation halo (a few chunks on typical data) is small next to it.
-constexpr uint64_t SEGS_PER_SM = 8;
+constexpr uint64_t SEGS_PER_SM = 16;
 
 void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, Plan &P) {
     uint64_t S = p->seg_bytes;
@@ -783,9 +856,10 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
         (nfiles + 1) * 8,    // 18 seg_first
         (nfiles + 1) * 8,    // 19 file_out
         64,                  // 20 misc
+        G * 4,               // 21 seg_file
     };
     size_t o = 0;
-    for (int i = 0; i < 21; ++i) {
+    for (int i = 0; i < 22; ++i) {
         P.off[i] = o;
         o += round_up(sz[i], 256);
     }
@@ -817,6 +891,7 @@ cdc::Work carve(const Plan &P, void *ws) {
     W.seg_first = (uint64_t *)(b + P.off[18]);
     W.file_out = (uint64_t *)(b + P.off[19]);
     W.misc = (uint32_t *)(b + P.off[20]);
+    W.seg_file = (uint32_t *)(b + P.off[21]);
     W.cap_list = P.cap_list;
     W.cap_halo = P.cap_halo;
     W.pool_cap = P.pool_cap;
@@ -833,7 +908,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     if (!attr_set) {
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_resolve<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      cdc::RING_SMEM));
+                                      cdc::RING_SMEM + 128));
         attr_set = true;
     }
     int launches = 0;
@@ -846,7 +921,9 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     };
     mark(0);
     if (batch) {
-        cdc::k_seg_prefix<<<1, cdc::RESOLVE_THREADS, 0, st>>>(G.file_off, G.nfiles, G.S, W.seg_first);
+        cdc::k_seg_prefix<<<1, cdc::RESOLVE_THREADS, 0, st>>>(G.file_off, G.nfiles, G.S, W.seg_first,
+                                                              W.seg_file);
+        CDC_KCHECK("k_seg_prefix", st);
         ++launches;
         pc.used[0] = true;
     }
@@ -858,17 +935,20 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     const uint64_t blocks = (nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS;
     if (blocks > 0) {
         cdc::k_speculate<ALGO><<<(unsigned)blocks, cdc::SPEC_WARPS * 32, spec_smem, st>>>(G, W);
+        CDC_KCHECK("k_speculate", st);
         ++launches;
         pc.used[1] = true;
     }
     mark(2);
-    cdc::k_resolve<ALGO><<<1, cdc::RESOLVE_THREADS, cdc::RING_SMEM, st>>>(G, W, d_count, file_out);
+    cdc::k_resolve<ALGO><<<1, cdc::RESOLVE_THREADS, cdc::RING_SMEM + 128, st>>>(G, W, d_count, file_out);
+    CDC_KCHECK("k_resolve", st);
     ++launches;
     pc.used[2] = true;
     mark(3);
     const uint64_t wthreads = nseg_ub * 32;
     if (wthreads > 0) {
         cdc::k_write<<<(unsigned)((wthreads + 255) / 256), 256, 0, st>>>(G, W, file_out, d_bounds, cap);
+        CDC_KCHECK("k_write", st);
         ++launches;
         pc.used[3] = true;
     }
@@ -1075,22 +1155,22 @@ int cdc_chain(const cdc_params *p, const uint8_t *d_data, uint64_t len, uint64_t
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     static bool attr = false;
     if (!attr) {
-        CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM));
-        CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM));
-        CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM + 128));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM + 128));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM + 128));
         attr = true;
     }
     switch (p->algo) {
     case CDC_RAM:
-        cdc::k_chain<0><<<1, 32, cdc::RING_SMEM, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
+        cdc::k_chain<0><<<1, 32, cdc::RING_SMEM + 128, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
                                                        starts_cap, d_count);
         break;
     case CDC_AE_MAX:
-        cdc::k_chain<1><<<1, 32, cdc::RING_SMEM, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
+        cdc::k_chain<1><<<1, 32, cdc::RING_SMEM + 128, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
                                                        starts_cap, d_count);
         break;
     default:
-        cdc::k_chain<2><<<1, 32, cdc::RING_SMEM, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
+        cdc::k_chain<2><<<1, 32, cdc::RING_SMEM + 128, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
                                                        starts_cap, d_count);
     }
     g_launches = 1;
