@@ -253,6 +253,87 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
 }
 __device__ __forceinline__ L2Pol stream_policy() { return L2Pol{l2_evict_first_policy(), 0, INT64_MIN}; }
 
+// ---------------------------------------------------------------- stage scans
+// Per-lane extreme of bytes [lo, hi) (stage offsets, lo < hi) of the 512-byte
+// block at stage offset Bk; `has` = the lane holds a byte of the range.
+template <bool MAX>
+__device__ __forceinline__ uint32_t block_lane_ext(const uint8_t *sp, int Bk, int lo, int hi, bool &has,
+                                                   uint4 &v) {
+    v = *reinterpret_cast<const uint4 *>(sp + Bk + lane_id() * 16);
+    int a, b;
+    lane_part(lo - Bk, hi - Bk, a, b);
+    has = a < b;
+    if (a == 0 && b == 16) return vext16<MAX>(v);
+    if (a >= b) return neutral<MAX>();
+    return vext16_range<MAX>(v, a, b);
+}
+
+// Extreme Byte Search (§4.1) of the stage bytes [lo, hi): per-lane extreme
+// (the tree's leaves; the caller's warp reduction is its root).  Whole blocks
+// fold into two u16x2 accumulators, 8 instructions per lane per 512 bytes.
+template <bool MAX>
+__device__ __forceinline__ uint32_t stage_lane_ext(const uint8_t *sp, int lo, int hi) {
+    uint32_t acc = neutral<MAX>();
+    if (lo >= hi) return acc;
+    int Bk = lo & ~(BLK - 1);
+    bool has;
+    uint4 v;
+    if (lo != Bk || hi < Bk + BLK) {  // partial head block
+        acc = block_lane_ext<MAX>(sp, Bk, lo, hi < Bk + BLK ? hi : Bk + BLK, has, v);
+        Bk += BLK;
+    }
+    uint32_t ah = MAX ? 0u : 0xFFFFFFFFu, al = ah;
+#pragma unroll 2
+    for (; Bk + BLK <= hi; Bk += BLK) {
+        const uint4 u = *reinterpret_cast<const uint4 *>(sp + Bk + lane_id() * 16);
+        ah = ext3<MAX>(ah, u.x, u.y);
+        ah = ext3<MAX>(ah, u.z, u.w);
+        al = ext3<MAX>(al, u.x << 8, u.y << 8);
+        al = ext3<MAX>(al, u.z << 8, u.w << 8);
+    }
+    const uint32_t m = ext3<MAX>(ah, al, al);
+    acc = ext2<MAX>(acc, ext2<MAX>(m >> 24, (m >> 8) & 0xFFu));
+    if (Bk < hi) acc = ext2<MAX>(acc, block_lane_ext<MAX>(sp, Bk, Bk, hi, has, v));  // partial tail block
+    return acc;
+}
+
+// Range Scan (§4.2), block level: first 512-byte block of the stage bytes
+// [lo, hi) holding a byte b with (b CMP target).  Returns its stage offset Bk
+// (or -1) and the ballot of the lanes holding one.
+template <int CMP>
+__device__ __forceinline__ int stage_find_block(const uint8_t *sp, int lo, int hi, uint32_t target, uint32_t &bal) {
+    constexpr bool MAX = (CMP == CMP_GT || CMP == CMP_GEQ);
+    int Bk = lo & ~(BLK - 1);
+    for (; Bk < hi; Bk += BLK) {
+        bool has;
+        uint4 v;
+        uint32_t lm;
+        if (Bk >= lo && Bk + BLK <= hi) {
+            v = *reinterpret_cast<const uint4 *>(sp + Bk + lane_id() * 16);
+            lm = vext16<MAX>(v);
+            has = true;
+        } else {
+            lm = block_lane_ext<MAX>(sp, Bk, lo > Bk ? lo : Bk, hi < Bk + BLK ? hi : Bk + BLK, has, v);
+        }
+        bal = __ballot_sync(0xFFFFFFFFu, has && cmp_holds<CMP>(lm, target));
+        if (bal) return Bk;
+    }
+    return -1;
+}
+
+// Range Scan locate: first stage offset in [lo, hi) inside lane L's 16 bytes of
+// block Bk whose byte satisfies (byte CMP target); the lane is known to hold one.
+template <int CMP>
+__device__ __forceinline__ int stage_locate(const uint8_t *sp, int Bk, uint32_t bal, int lo, int hi,
+                                            uint32_t target) {
+    const int base = Bk + (__ffs(bal) - 1) * 16;
+    const int j = lane_id() & 15;
+    const int pos = base + j;
+    const bool hit = lane_id() < 16 && pos >= lo && pos < hi && cmp_holds<CMP>(sp[pos], target);
+    return base + __ffs(__ballot_sync(0xFFFFFFFFu, hit)) - 1;
+}
+
+// ---------------------------------------------------------------- chain engine
 // run_chain walks the chunk chain of the stream fbase[0..Lf) that begins with
 // a chunk at `start` (0 <= start < Lf).  Every boundary e < Lf (the start of
 // the next chunk) is passed to emit.boundary(e), which returns true to stop
@@ -271,13 +352,17 @@ __device__ __forceinline__ L2Pol stream_policy() { return L2Pol{l2_evict_first_p
 //
 // Inside a stage every position is an int offset from the stage's first byte
 // (horizons beyond the stage clamp to FAR); the chain state between events is
-// kept as 64-bit stream positions.
+// kept as 64-bit stream positions.  Between events the walker runs one of
+// three tight loops: the RAM window's Extreme Byte Search (stage_lane_ext), a
+// block-level Range Scan for the next event (stage_find_block), or -- for an
+// AE target no byte can beat -- a direct jump to its deadline.
 template <int ALGO, class Emit>
 __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf, int64_t start,
                           int64_t read_end, uint32_t w, uint64_t max_size, const L2Pol &pol, Emit &emit) {
     constexpr bool MAX = (ALGO != ALGO_AE_MIN);
     constexpr uint32_t SAT = MAX ? 255u : 0u;  // a target nothing can beat
     constexpr int FAR = 1 << 30;
+    constexpr int CMP_BEAT = MAX ? CMP_GT : CMP_LT;
     const int lane = lane_id();
     if (read_end > Lf) read_end = Lf;
     const uint8_t *g0 = reinterpret_cast<const uint8_t *>(reinterpret_cast<uintptr_t>(fbase + start) &
@@ -293,9 +378,8 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     __syncwarp();
 
     int64_t issued = 0;
-    auto issue = [&](int64_t k) {
+    auto issue = [&](int64_t k, int slot) {
         if (lane == 0) {
-            const int slot = (int)(k % NST);
             const int64_t off = k * STAGE;
             const uint32_t bytes = (uint32_t)(nbytes - off < STAGE ? nbytes - off : STAGE);
             mbar_arrive_expect_tx(&R.bar[slot], bytes);
@@ -303,7 +387,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                         B0 + off < pol.keep_until ? pol.keep : pol.stream);
         }
     };
-    for (; issued < nstages && issued < NST; ++issued) issue(issued);
+    for (; issued < nstages && issued < NST; ++issued) issue(issued, (int)issued);
 
     const int64_t W = (int64_t)w;
     const bool fastrec = w >= (uint32_t)(BLK - 1);  // AE: records inside one block never miss a deadline
@@ -348,159 +432,124 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
         return false;
     };
 
+    int slot = 0;
+    uint32_t parity = 0;
     int64_t k = 0;
-    while (!stop && k < nstages) {
-        const int slot = (int)(k % NST);
+    for (; k < nstages && !stop; ++k) {
         const int64_t SB = B0 + k * STAGE;
-        const int64_t SE = SB + STAGE;
-        // a saturated AE target skips whole stages without reading them
-        bool skip = c >= SE;
-        if constexpr (ALGO != ALGO_RAM) {
-            if (!skip && !pending && ext == SAT) {
-                const int64_t h = (t + W + 1 < limit) ? t + W + 1 : limit;
-                if (h >= SE && read_end >= SE) {
-                    c = SE;
-                    skip = true;
-                }
-            }
+        mbar_wait(&R.bar[slot], parity);
+        const uint8_t *sp = R.buf + slot * STAGE;
+        auto rel = [&](int64_t x) -> int {  // x >= SB
+            const int64_t d = x - SB;
+            return d > FAR ? FAR : (int)d;
+        };
+        const int endr = rel(read_end) < STAGE ? rel(read_end) : STAGE;
+        int cr = (int)(c - SB);
+        int limr = rel(limit);
+        // RAM: window end s+w while not scanning; AE: target deadline t+w+1
+        int hor = FAR;
+        if constexpr (ALGO == ALGO_RAM) {
+            if (!scanning) hor = rel(s + W);
+        } else {
+            if (!pending) hor = rel(t + W + 1);
         }
-        mbar_wait(&R.bar[slot], (uint32_t)((k / NST) & 1));
-        if (!skip) {
-            const uint8_t *sp = R.buf + slot * STAGE;
-            auto rel = [&](int64_t x) -> int {  // x >= SB
-                const int64_t d = x - SB;
-                return d > FAR ? FAR : (int)d;
-            };
-            const int endr = rel(read_end) < STAGE ? rel(read_end) : STAGE;
-            int cr = (int)(c - SB);
-            int limr = rel(limit);
-            int hor = 0;  // RAM: window end s+w (not scanning); AE: deadline t+w+1
+        // a boundary at stage offset er
+        auto event = [&](int er) -> bool {
+            if (on_boundary(SB + er)) return true;
+            cr = er;
+            limr = rel(limit);
+            if constexpr (ALGO == ALGO_RAM) hor = rel(s + W);
+            else hor = FAR;
+            return false;
+        };
+        while (cr < endr) {
             if constexpr (ALGO == ALGO_RAM) {
-                hor = scanning ? FAR : rel(s + W);
-            } else {
-                hor = pending ? FAR : rel(t + W + 1);
-            }
-            // event at stage offset er: update the chain state and the stage views
-            auto event = [&](int er) -> bool {
-                if (on_boundary(SB + er)) return true;
-                cr = er;
-                limr = rel(limit);
-                if constexpr (ALGO == ALGO_RAM) hor = rel(s + W);
-                else hor = FAR;
-                return false;
-            };
-#pragma unroll 1
-            for (int Bk = (cr >> 9) << 9; Bk < endr && !stop; Bk += BLK) {
-                const int Be = Bk + BLK < endr ? Bk + BLK : endr;
-                if constexpr (ALGO != ALGO_RAM) {
-                    if (!pending && ext == SAT) {  // skip to the event horizon without loading
-                        const int h = hor < limr ? hor : limr;
-                        if (h >= Be) {
-                            cr = Be;
-                            continue;
-                        }
-                        if (h > cr) cr = h;
+                if (!scanning) {
+                    const int hi = hor < endr ? hor : endr;
+                    acc = max(acc, stage_lane_ext<true>(sp, cr, hi));
+                    cr = hi;
+                    if (cr == hor) {
+                        M = warp_ext<true>(acc);
+                        scanning = true;
+                        hor = FAR;
                     }
-                }
-                Blk blk;
-                blk.B = SB + Bk;
-                blk.v = *reinterpret_cast<const uint4 *>(sp + Bk + lane * 16);
-                const uint32_t full = vext16<MAX>(blk.v);
-                while (cr < Be) {
-                    if constexpr (ALGO == ALGO_RAM) {
-                        if (!scanning) {
-                            const int hi = hor < Be ? hor : Be;
-                            if (cr == Bk && hi == Bk + BLK) {
-                                acc = max(acc, full);
-                            } else {
-                                bool has;
-                                acc = max(acc, lane_ext<true>(blk, full, cr - Bk, hi - Bk, has));
-                            }
-                            cr = hi;
-                            if (cr == hor) {
-                                M = warp_ext<true>(acc);
-                                scanning = true;
-                                hor = FAR;
-                            }
-                        } else {
-                            const int hi = limr < Be ? limr : Be;
-                            uint32_t bal;
-                            if (cr == Bk && hi == Bk + BLK) {
-                                bal = __ballot_sync(0xFFFFFFFFu, full >= M);
-                            } else {
-                                bool has;
-                                const uint32_t lm = lane_ext<true>(blk, full, cr - Bk, hi - Bk, has);
-                                bal = __ballot_sync(0xFFFFFFFFu, has && lm >= M);
-                            }
-                            int er;
-                            if (bal) {
-                                er = Bk + locate<CMP_GEQ>(blk, bal, cr - Bk, hi - Bk, M) + 1;  // boundary byte ends the chunk
-                            } else {
-                                cr = hi;
-                                if (cr != limr) continue;
-                                er = limr;  // cap or end of stream
-                            }
-                            if (event(er)) {
-                                stop = true;
-                                break;
-                            }
-                        }
+                } else {
+                    const int hi = limr < endr ? limr : endr;
+                    uint32_t bal = 0;
+                    const int Bk = stage_find_block<CMP_GEQ>(sp, cr, hi, M, bal);
+                    int er;
+                    if (Bk >= 0) {
+                        er = stage_locate<CMP_GEQ>(sp, Bk, bal, cr, hi, M) + 1;  // boundary byte ends the chunk
                     } else {
-                        if (pending) {  // first byte of the chunk: the first target
-                            ext = byte_at(blk, cr - Bk);
-                            t = SB + cr;
-                            ++cr;
-                            hor = rel(t + W + 1);
-                            pending = false;
-                            continue;
-                        }
-                        int hi = hor < limr ? hor : limr;
-                        hi = hi < Be ? hi : Be;
-                        if (ext != SAT) {
-                            const int rlo = cr - Bk, rhi = hi - Bk;
-                            bool has = true;
-                            const uint32_t lm =
-                                (rlo == 0 && rhi == BLK) ? full : lane_ext<MAX>(blk, full, rlo, rhi, has);
-                            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has && beats<MAX>(lm, ext));
-                            if (bal) {
-                                if (fastrec) {
-                                    // every record of [cr, hi) follows its predecessor within
-                                    // < BLK <= w+1 bytes, so the last one -- the first
-                                    // occurrence of the range extreme -- is the new target
-                                    const uint32_t m = warp_ext<MAX>(has ? lm : neutral<MAX>());
-                                    const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, has && lm == m);
-                                    t = blk.B + locate<CMP_EQ>(blk, b2, rlo, rhi, m);
-                                    ext = m;
-                                    cr = hi;
-                                } else {
-                                    const int r = locate<MAX ? CMP_GT : CMP_LT>(blk, bal, rlo, rhi, ext);
-                                    t = blk.B + r;
-                                    ext = byte_at(blk, r);
-                                    cr = Bk + r + 1;
-                                }
-                                hor = rel(t + W + 1);
-                                continue;
-                            }
-                        }
                         cr = hi;
-                        int er;
-                        if (cr == hor && hor <= limr) er = hor;  // target unbeaten over its window
-                        else if (cr == limr) er = limr;         // cap or end of stream
-                        else continue;                          // block exhausted
-                        if (event(er)) {
-                            stop = true;
-                            break;
-                        }
+                        if (cr != limr) break;
+                        er = limr;  // cap or end of stream
+                    }
+                    if (event(er)) {
+                        stop = true;
+                        break;
                     }
                 }
+            } else {
+                if (pending) {  // first byte of the chunk: the first target
+                    ext = sp[cr];
+                    t = SB + cr;
+                    hor = rel(t + W + 1);
+                    ++cr;
+                    pending = false;
+                    continue;
+                }
+                int hi = hor < limr ? hor : limr;
+                hi = hi < endr ? hi : endr;
+                if (ext != SAT && cr < hi) {
+                    uint32_t bal = 0;
+                    const int Bk = stage_find_block<CMP_BEAT>(sp, cr, hi, ext, bal);
+                    if (Bk >= 0) {
+                        const int lo = cr > Bk ? cr : Bk;
+                        const int bh = hi < Bk + BLK ? hi : Bk + BLK;
+                        if (fastrec) {
+                            // every record of [lo, bh) follows its predecessor within
+                            // < BLK <= w+1 bytes, so the last one -- the first
+                            // occurrence of the range extreme -- is the new target
+                            bool has;
+                            uint4 v;
+                            const uint32_t lm = block_lane_ext<MAX>(sp, Bk, lo, bh, has, v);
+                            const uint32_t m = warp_ext<MAX>(lm);
+                            const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, has && lm == m);
+                            const int r = stage_locate<CMP_EQ>(sp, Bk, b2, lo, bh, m);
+                            t = SB + r;
+                            ext = m;
+                            cr = bh;
+                        } else {
+                            const int r = stage_locate<CMP_BEAT>(sp, Bk, bal, lo, bh, ext);
+                            t = SB + r;
+                            ext = sp[r];
+                            cr = r + 1;
+                        }
+                        hor = rel(t + W + 1);
+                        continue;
+                    }
+                }
+                cr = hi;
+                int er;
+                if (cr == hor && hor <= limr) er = hor;  // target unbeaten over its window
+                else if (cr == limr) er = limr;         // cap or end of stream
+                else break;                             // stage exhausted
+                if (event(er)) {
+                    stop = true;
+                    break;
+                }
             }
-            c = SB + cr;
         }
+        c = SB + cr;
         __syncwarp();
-        ++k;
-        if (!stop && issued < nstages) {
-            issue(issued);
+        if (!stop && issued < nstages) {  // refill this slot with stage k + NST
+            issue(issued, slot);
             ++issued;
+        }
+        if (++slot == NST) {
+            slot = 0;
+            parity ^= 1u;
         }
     }
     // all bytes below read_end consumed without the emitter stopping
@@ -508,8 +557,14 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
         if (c >= Lf) emit.end();
         else emit.exhausted(c);
     }
-    // drain copies still in flight before the ring is reused or the CTA exits
-    for (int64_t j = k; j < issued; ++j) mbar_wait(&R.bar[j % NST], (uint32_t)((j / NST) & 1));
+    // drain copies still in flight (stages k .. issued-1) before the ring is reused or the CTA exits
+    for (; k < issued; ++k) {
+        mbar_wait(&R.bar[slot], parity);
+        if (++slot == NST) {
+            slot = 0;
+            parity ^= 1u;
+        }
+    }
     __syncwarp();
     if (lane == 0)
         for (int i = 0; i < NST; ++i) mbar_inval(&R.bar[i]);  // the ring may be re-initialised by the caller
