@@ -151,6 +151,29 @@ def cpu_baseline(data_np, w, mx):
             "sample": "the full 256 MiB configs[1] stream, one pass, C oracle (gcc -O2), 1 thread"}
 
 
+def measure_e2e(cdc, p, data_np, cap, world, dist, dev, steps):
+    """Same metric through cdc_chunk_host: pinned host bytes in, host boundaries out."""
+    import torch
+    pinned = torch.empty(STREAM, dtype=torch.uint8, pin_memory=True)
+    pinned.copy_(torch.from_numpy(data_np))
+    host_in = pinned.numpy()
+    host_out = np.empty(cap, dtype=np.uint64)
+    cdc.chunk_host(host_in, p, host_out)
+    e2e_steps = max(3, min(steps, 20))
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        nb = cdc.chunk_host(host_in, p, host_out).size
+    e2e_s = time.perf_counter() - t0
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    return {"value": round(STREAM * world * e2e_steps / float(e2e_t.item()) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": STREAM, "d2h_bytes_per_step": 8 + 8 * nb,
+            "timing": "wall clock around the synchronous cdc_chunk_host call (pinned input)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -159,6 +182,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--check", action="store_true", help="verify the boundaries against the oracle once")
+    ap.add_argument("--seg-bytes", type=int, default=0, help="speculation segment size (0 = library default)")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end host-buffer measurement")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":
@@ -180,7 +205,7 @@ def main():
     # that no step finds the previous step's lines in L2 (126 MB < 2 x 256 MiB)
     bufs = [torch.from_numpy(data_np).to(dev) for _ in range(2)]
     data = bufs[0]
-    p = cdc.params(ALGO, avg_size=AVG)
+    p = cdc.params(ALGO, avg_size=AVG, seg_bytes=args.seg_bytes)
     cap = cdc.max_boundaries(p, STREAM)
     bounds = torch.empty(cap, dtype=torch.int64, device=dev)
     count = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -241,25 +266,7 @@ def main():
     share = {k: round(prof[k][0] / max(1e-9, sum(prof[x][0] for x in cdc.KERNELS)), 4) for k in cdc.KERNELS}
 
     # end to end through the public host API (pinned host input, copies inside the call)
-    e2e = None
-    pinned = torch.empty(STREAM, dtype=torch.uint8, pin_memory=True)
-    pinned.copy_(torch.from_numpy(data_np))
-    host_in = pinned.numpy()
-    host_out = np.empty(cap, dtype=np.uint64)
-    cdc.chunk_host(host_in, p, host_out)
-    e2e_steps = max(3, min(args.steps, 20))
-    if dist is not None:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        nb = cdc.chunk_host(host_in, p, host_out).size
-    e2e_s = time.perf_counter() - t0
-    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e = {"value": round(STREAM * world * e2e_steps / float(e2e_t.item()) / 1e9, 3), "unit": "GB/s",
-           "h2d_bytes_per_step": STREAM, "d2h_bytes_per_step": 8 + 8 * nb,
-           "timing": "wall clock around the synchronous cdc_chunk_host call (pinned input)"}
+    e2e = None if args.no_e2e else measure_e2e(cdc, p, data_np, cap, world, dist, dev, args.steps)
 
     if rank == 0:
         line = {

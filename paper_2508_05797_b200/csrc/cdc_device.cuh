@@ -299,22 +299,48 @@ __device__ __forceinline__ uint32_t stage_lane_ext(const uint8_t *sp, int lo, in
 
 // Range Scan (§4.2), block level: first 512-byte block of the stage bytes
 // [lo, hi) holding a byte b with (b CMP target).  Returns its stage offset Bk
-// (or -1) and the ballot of the lanes holding one.
+// (or -1), the ballot of the lanes holding one, and each lane's extreme `lm`
+// (and `has`) over that block's part of [lo, hi).  Whole blocks are tested two
+// at a time (two independent shared-memory loads and max trees in flight).
 template <int CMP>
-__device__ __forceinline__ int stage_find_block(const uint8_t *sp, int lo, int hi, uint32_t target, uint32_t &bal) {
+__device__ __forceinline__ int stage_find_block(const uint8_t *sp, int lo, int hi, uint32_t target, uint32_t &bal,
+                                                uint32_t &lm, bool &has) {
     constexpr bool MAX = (CMP == CMP_GT || CMP == CMP_GEQ);
+    const int lane16 = lane_id() * 16;
     int Bk = lo & ~(BLK - 1);
-    for (; Bk < hi; Bk += BLK) {
-        bool has;
-        uint4 v;
-        uint32_t lm;
-        if (Bk >= lo && Bk + BLK <= hi) {
-            v = *reinterpret_cast<const uint4 *>(sp + Bk + lane_id() * 16);
-            lm = vext16<MAX>(v);
-            has = true;
-        } else {
-            lm = block_lane_ext<MAX>(sp, Bk, lo > Bk ? lo : Bk, hi < Bk + BLK ? hi : Bk + BLK, has, v);
+    uint4 v;
+    if (Bk < lo || Bk + BLK > hi) {  // partial head block
+        if (Bk >= hi) return -1;
+        lm = block_lane_ext<MAX>(sp, Bk, lo, hi < Bk + BLK ? hi : Bk + BLK, has, v);
+        bal = __ballot_sync(0xFFFFFFFFu, has && cmp_holds<CMP>(lm, target));
+        if (bal) return Bk;
+        Bk += BLK;
+    }
+    has = true;
+    for (; Bk + 2 * BLK <= hi; Bk += 2 * BLK) {
+        const uint4 a = *reinterpret_cast<const uint4 *>(sp + Bk + lane16);
+        const uint4 b = *reinterpret_cast<const uint4 *>(sp + Bk + BLK + lane16);
+        const uint32_t ma = vext16<MAX>(a), mb = vext16<MAX>(b);
+        const bool ha = cmp_holds<CMP>(ma, target), hb = cmp_holds<CMP>(mb, target);
+        if (__any_sync(0xFFFFFFFFu, ha || hb)) {
+            bal = __ballot_sync(0xFFFFFFFFu, ha);
+            if (bal) {
+                lm = ma;
+                return Bk;
+            }
+            bal = __ballot_sync(0xFFFFFFFFu, hb);
+            lm = mb;
+            return Bk + BLK;
         }
+    }
+    for (; Bk + BLK <= hi; Bk += BLK) {
+        v = *reinterpret_cast<const uint4 *>(sp + Bk + lane16);
+        lm = vext16<MAX>(v);
+        bal = __ballot_sync(0xFFFFFFFFu, cmp_holds<CMP>(lm, target));
+        if (bal) return Bk;
+    }
+    if (Bk < hi) {  // partial tail block
+        lm = block_lane_ext<MAX>(sp, Bk, Bk, hi, has, v);
         bal = __ballot_sync(0xFFFFFFFFu, has && cmp_holds<CMP>(lm, target));
         if (bal) return Bk;
     }
@@ -390,6 +416,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     for (; issued < nstages && issued < NST; ++issued) issue(issued, (int)issued);
 
     const int64_t W = (int64_t)w;
+    const int W1 = w + 1 < (uint32_t)FAR ? (int)w + 1 : FAR;  // deadline distance t -> t+w+1, clamped
     const bool fastrec = w >= (uint32_t)(BLK - 1);  // AE: records inside one block never miss a deadline
     // chain state (stream positions)
     int64_t s = start;                                                           // current chunk start
@@ -475,8 +502,9 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                     }
                 } else {
                     const int hi = limr < endr ? limr : endr;
-                    uint32_t bal = 0;
-                    const int Bk = stage_find_block<CMP_GEQ>(sp, cr, hi, M, bal);
+                    uint32_t bal = 0, lm;
+                    bool has;
+                    const int Bk = stage_find_block<CMP_GEQ>(sp, cr, hi, M, bal, lm, has);
                     int er;
                     if (Bk >= 0) {
                         er = stage_locate<CMP_GEQ>(sp, Bk, bal, cr, hi, M) + 1;  // boundary byte ends the chunk
@@ -494,7 +522,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                 if (pending) {  // first byte of the chunk: the first target
                     ext = sp[cr];
                     t = SB + cr;
-                    hor = rel(t + W + 1);
+                    hor = cr + W1 < FAR ? cr + W1 : FAR;
                     ++cr;
                     pending = false;
                     continue;
@@ -502,31 +530,29 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                 int hi = hor < limr ? hor : limr;
                 hi = hi < endr ? hi : endr;
                 if (ext != SAT && cr < hi) {
-                    uint32_t bal = 0;
-                    const int Bk = stage_find_block<CMP_BEAT>(sp, cr, hi, ext, bal);
+                    uint32_t bal = 0, lm;
+                    bool has;
+                    const int Bk = stage_find_block<CMP_BEAT>(sp, cr, hi, ext, bal, lm, has);
                     if (Bk >= 0) {
                         const int lo = cr > Bk ? cr : Bk;
                         const int bh = hi < Bk + BLK ? hi : Bk + BLK;
+                        int r;
                         if (fastrec) {
                             // every record of [lo, bh) follows its predecessor within
                             // < BLK <= w+1 bytes, so the last one -- the first
                             // occurrence of the range extreme -- is the new target
-                            bool has;
-                            uint4 v;
-                            const uint32_t lm = block_lane_ext<MAX>(sp, Bk, lo, bh, has, v);
                             const uint32_t m = warp_ext<MAX>(lm);
                             const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, has && lm == m);
-                            const int r = stage_locate<CMP_EQ>(sp, Bk, b2, lo, bh, m);
-                            t = SB + r;
+                            r = stage_locate<CMP_EQ>(sp, Bk, b2, lo, bh, m);
                             ext = m;
                             cr = bh;
                         } else {
-                            const int r = stage_locate<CMP_BEAT>(sp, Bk, bal, lo, bh, ext);
-                            t = SB + r;
+                            r = stage_locate<CMP_BEAT>(sp, Bk, bal, lo, bh, ext);
                             ext = sp[r];
                             cr = r + 1;
                         }
-                        hor = rel(t + W + 1);
+                        t = SB + r;
+                        hor = r + W1 < FAR ? r + W1 : FAR;
                         continue;
                     }
                 }
