@@ -228,6 +228,7 @@ def main():
         got = bounds[:n_bounds].cpu().numpy().astype(np.uint64)
         assert got.size == exp.size and (got == exp).all(), "boundary mismatch vs oracle"
     launches_per_step = cdc.last_launch_count()
+    path_stats = cdc.stats(p, ws, 1, STREAM, STREAM)
 
     # keep the GPU loaded ~0.3 s so clock samples reflect the timed region
     with ClockSampler(local) as clk:
@@ -246,6 +247,14 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
         cdc.profile_enable(False)
+        # the same K steps without the per-kernel events, to bound their overhead
+        ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev2.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev3.record(stream)
+        torch.cuda.synchronize()
+        plain_ms = ev2.elapsed_time(ev3)
     prof = cdc.profile_collect()
     if dist is not None:
         dist.barrier()
@@ -283,6 +292,8 @@ def main():
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "kernel_ms": round(spec_avg_ms, 4), "share_of_step": share},
             "gpu_launches": launches_per_step * args.steps,
+            "path": path_stats,
+            "ms_per_step_without_kernel_events": round(plain_ms / args.steps, 4),
             "clocks": clk.summary(),
             "e2e": e2e,
         }

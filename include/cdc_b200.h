@@ -199,6 +199,19 @@ int cdc_profile_collect(double *ms_sum, uint64_t *launches, uint64_t *calls);
  * GPU has reached it, 0 if not (-1: event unused). */
 int cdc_profile_query(int *done);
 
+/*
+ * Diagnostics of the last call that used workspace d_workspace (same params
+ * and sizes as that call): synchronises `stream` and writes to stats[8]:
+ *   [0] segments G, [1] segment bytes S, [2] halo cap bytes,
+ *   [3] 1 if the fused look-back fast path produced the output (0: the
+ *       k_resolve/k_write fix-up path ran), [4] segments whose chain met the
+ *       next segment's chain, [5] segments whose halo walk gave up or was
+ *       undecided, [6] segments whose chain skipped a later segment or reached
+ *       the stream end from a non-final segment, [7] total halo chunks.
+ */
+int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len,
+              const void *d_workspace, uint64_t *stats, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,7 +20,7 @@ __all__ = [
     "CdcError", "ALGOS", "params", "window_for_avg", "max_boundaries", "workspace_size",
     "chunk_async", "chunk", "chunk_batch", "chunk_host", "chain",
     "extreme_byte_search", "range_scan", "last_launch_count", "abi_version",
-    "profile_enable", "profile_collect", "KERNELS",
+    "profile_enable", "profile_collect", "KERNELS", "stats",
 ]
 
 
@@ -40,6 +40,14 @@ def profile_collect() -> dict:
     out = {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KERNELS)}
     out["calls"] = int(calls.value)
     return out
+
+
+def stats(p: cdc_params, workspace: torch.Tensor, nfiles: int, total_len: int, max_len: int, stream=None) -> dict:
+    """Diagnostics of the last call that used `workspace` (synchronises)."""
+    out = (ctypes.c_uint64 * 8)()
+    check(lib.cdc_stats(ctypes.byref(p), nfiles, total_len, max_len, workspace.data_ptr(), out, _stream_ptr(stream)))
+    keys = ["segments", "seg_bytes", "halo_cap", "fast_path", "synced", "unsynced", "skipped_or_end", "halo_chunks"]
+    return {k: int(out[i]) for i, k in enumerate(keys)}
 
 
 def abi_version() -> int:

@@ -42,6 +42,10 @@ struct Work {
     uint32_t *halo;              // G x cap_halo  starts relative to the segment end
     uint32_t *cnt, *hcnt;        // list / halo lengths
     unsigned long long *pub;     // PUB_OPEN, or the final list length
+    unsigned long long *status;  // look-back words (ST_* flag | 62-bit signed value), reset to ~0
+    uint32_t *ctrl;              // [0] CTA ticket counter, [1] fast path valid (~0) / failed (0); reset to ~0
+    unsigned long long *grp;     // look-back group sums (reset to ~0)
+    uint32_t *gcnt;              // look-back group arrival counters (reset to ~0)
     int32_t *sj;                 // sync target segment, or SJ_* code
     uint32_t *sa, *sb;           // halo entries before the sync point; its index in list(sj)
     uint32_t *entry, *tail, *wcnt, *jump_entry;
@@ -229,14 +233,100 @@ struct SpecEmit {
     __device__ void exhausted(int64_t) { sj = SJ_UNSYNCED; }
 };
 
+// Decoupled look-back words: the top two bits say what the low 62 bits (a
+// signed value) hold.  The memset leaves every word ~0 = not ready.
+constexpr unsigned long long ST_AGG = 1ull << 62;   // a_g = (cnt + tail) - sb of this segment
+constexpr unsigned long long ST_MASK = 3ull << 62;
+__device__ __forceinline__ int64_t st_value(unsigned long long w) {
+    return (int64_t)(w << 2) >> 2;  // sign-extend the 62-bit value
+}
+__device__ __forceinline__ unsigned long long st_word(unsigned long long flag, int64_t v) {
+    return flag | ((unsigned long long)v & ~ST_MASK);
+}
+
+// Output offset of segment g's first true chain start.  With entry(g) = sb(g-1)
+// (the index in list(g) where segment g-1's chain met it; 0 at a file's first
+// segment) and n(g) = cnt(g) + tail(g) - entry(g), the exclusive prefix sum of
+// n telescopes to  sum_{h<g} a_h + sb(g-1)  with the purely local
+// a_h = cnt(h) + tail(h) - sb(h).  Two-level scan: every segment publishes a_h
+// (ST_AGG); the last segment of each group of 32 to finish publishes the
+// group's sum (ST_AGG in grp).  A segment then waits for, and sums, the groups
+// before its own and the members of its group before it: at most
+// ceil(G/1024) + 1 independent loads per lane.  Returns sum_{h<g} a_h.
+constexpr int LB_GROUP = 32;
+constexpr uint64_t LB_MAX_SEGS = 32768;  // beyond this the k_resolve scan is used
+
+// all 32 lanes
+__device__ void publish_agg(Work &W, uint64_t g, uint64_t nsegs, int64_t a) {
+    const int lane = lane_id();
+    const uint64_t grp = g / LB_GROUP;
+    const uint64_t gsz = (grp + 1) * LB_GROUP <= nsegs ? LB_GROUP : nsegs - grp * LB_GROUP;
+    uint32_t old = 0;
+    if (lane == 0) {
+        st_release_u64(W.status + g, st_word(ST_AGG, a));
+        asm volatile("atom.acq_rel.gpu.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(W.gcnt + grp) : "memory");
+    }
+    old = __shfl_sync(0xFFFFFFFFu, old, 0);
+    if (old + 1u == (uint32_t)gsz - 1u) {  // the counter starts at ~0: this is the group's last arrival
+        // one load per lane (acquire loads issued by one thread would serialise)
+        int64_t v = lane < (int)gsz ? st_value(ld_acquire_u64(W.status + grp * LB_GROUP + lane)) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (lane == 0) st_release_u64(W.grp + grp, st_word(ST_AGG, v));
+    }
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// all 32 lanes; relaxed loads issued together, then one acquire fence per lane
+__device__ int64_t lookback(const Work &W, uint64_t g) {
+    const int lane = lane_id();
+    const uint64_t grp = g / LB_GROUP;
+    const uint64_t g0 = grp * LB_GROUP;
+    for (;;) {
+        bool ok = true;
+        int64_t sum = 0;
+#pragma unroll 4
+        for (uint64_t k = lane; k < grp; k += 32) {
+            const unsigned long long wd = ld_relaxed_u64(W.grp + k);
+            ok &= (wd & ST_MASK) == ST_AGG;
+            sum += st_value(wd);
+        }
+        if (g0 + lane < g) {
+            const unsigned long long wd = ld_relaxed_u64(W.status + g0 + lane);
+            ok &= (wd & ST_MASK) == ST_AGG;
+            sum += st_value(wd);
+        }
+        if (__all_sync(0xFFFFFFFFu, ok)) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire what the observed releases published
+            __syncwarp();
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+            return sum;
+        }
+        __nanosleep(128);
+    }
+}
+
 template <int ALGO>
-__global__ void __launch_bounds__(SPEC_WARPS * 32, 4) k_speculate(Geometry G, Work W) {
+__global__ void __launch_bounds__(SPEC_WARPS * 32, 4) k_speculate(Geometry G, Work W, uint64_t *bounds,
+                                                                  uint64_t cap, uint64_t *d_count, int fused) {
     extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint32_t s_ticket;
     const int warp = threadIdx.x >> 5;
-    const uint64_t g = (uint64_t)blockIdx.x * SPEC_WARPS + warp;
+    const int lane = lane_id();
+    // CTAs take segment groups in launch order (a ticket), so every segment a
+    // look-back waits for belongs to a CTA that is already running
+    if (threadIdx.x == 0) s_ticket = atomicAdd(W.ctrl, 1u) + 1u;  // counter starts at ~0
+    __syncthreads();
+    const uint64_t g = (uint64_t)s_ticket * SPEC_WARPS + warp;
     const uint64_t nsegs = total_segs(G, W);
     if (g >= nsegs) return;
-    uint8_t *wbase = smem + warp * RING_SMEM;
+    uint8_t *wbase = align_smem(smem) + warp * RING_SMEM;
     WarpRing R{wbase, reinterpret_cast<uint64_t *>(wbase + RING_BYTES)};
 
     SpecEmit em;
@@ -253,7 +343,7 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, 4) k_speculate(Geometry G, Wo
     em.cur_j = -1;
     em.cursor = 0;
     em.published = false;
-    if (lane_id() == 0) st_relaxed_u32(em.list, 0u);  // the speculative chain starts at the segment's first byte
+    if (lane == 0) st_relaxed_u32(em.list, 0u);  // the speculative chain starts at the segment's first byte
     const uint8_t *fbase = G.data + em.I.foff;
     int64_t read_end = (g == em.I.last) ? (int64_t)em.I.Lf
                                         : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
@@ -261,12 +351,55 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, 4) k_speculate(Geometry G, Wo
     const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
     run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
     em.publish();
-    if (lane_id() == 0) {
+
+    // ---- common case, fused resolve + write: the chain met the next segment's
+    //      chain (or ended the file); anything else defers to k_resolve/k_write
+    const int fused_dbg = fused;  // debugging knob: 2 = skip the writes, 3 = skip the look-back
+    fused = fused && nsegs <= LB_MAX_SEGS;
+    const bool normal = fused && (em.sj == SJ_LAST || em.sj == (int32_t)(g + 1));
+    const uint32_t tail = em.sj == SJ_LAST ? 0u : em.sa;
+    const uint32_t sb = normal && em.sj != SJ_LAST ? em.sb : 0u;
+    const int64_t a = (int64_t)em.cnt + tail - sb;
+    if (lane == 0) {
         W.cnt[g] = em.cnt;
         W.hcnt[g] = em.hcnt;
         W.sj[g] = em.sj;
         W.sa[g] = em.sa;
         W.sb[g] = em.sb;
+        if (!normal) atomicAnd(W.ctrl + 1, 0u);  // the fast path's output is void
+    }
+    if (fused) publish_agg(W, g, nsegs, a);
+    if (!fused || fused_dbg == 3) return;
+    const int64_t excl = g == 0 ? 0 : lookback(W, g);
+    if (!normal || fused_dbg == 2) return;
+    // entry(g) = sb(g-1): the previous segment stored it before releasing its status
+    // word (observed directly, or through its group's sum) and the look-back
+    // ended with an acquire fence; lane 0 reads it and broadcasts
+    uint32_t entry = 0;
+    if (g != em.I.first && lane == 0) entry = ld_relaxed_u32(W.sb + g - 1);
+    entry = __shfl_sync(0xFFFFFFFFu, entry, 0);
+    const int64_t off = excl + entry;                     // output index of list[entry]
+    const int64_t A = (int64_t)em.cnt - entry;            // true starts from this segment's list
+    const int64_t n = A + tail;
+    if (A < 0 || off < 0) {  // inconsistent (cannot happen when every segment is normal)
+        if (lane == 0) atomicAnd(W.ctrl + 1, 0u);
+        return;
+    }
+    __syncwarp();
+    if (lane == 0) W.seg_out[g] = (uint64_t)off;
+    for (int64_t i = lane; i < n; i += 32) {
+        const uint64_t v = i < A ? (uint64_t)em.I.p + em.list[entry + i] : (uint64_t)em.I.seg_end + em.halo[i - A];
+        const uint64_t q = (uint64_t)off + i;
+        if (g == em.I.first && i == 0) continue;  // the file's first start (0) is not a boundary
+        if (q - 1 < cap) bounds[q - 1] = v;
+    }
+    if (em.sj == SJ_LAST && lane == 0) {
+        const uint64_t q = (uint64_t)(off + n) - 1;  // a file's last boundary is its length
+        if (q < cap) bounds[q] = em.I.Lf;
+        if (g == nsegs - 1) {
+            *d_count = (uint64_t)(off + n);
+            W.seg_out[nsegs] = (uint64_t)(off + n);
+        }
     }
 }
 
@@ -381,6 +514,15 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = blockDim.x >> 5;
     const uint64_t nsegs = total_segs(G, W);
+    if (nsegs > 0 && W.ctrl[1] != 0u) {
+        // k_speculate's fused look-back produced the output: only the per-file offsets remain
+        const uint64_t nf = G.file_off == nullptr ? 0 : G.nfiles;
+        for (uint64_t f = tid; f <= nf && G.file_off != nullptr; f += blockDim.x) {
+            const uint64_t sf = W.seg_first[f];
+            file_out[f] = (sf >= nsegs) ? W.seg_out[nsegs] : W.seg_out[sf];
+        }
+        return;
+    }
 
     // 1. classify (32 consecutive segments per warp step, coalesced); re-check
     //    undecided halos now that every list is complete
@@ -552,7 +694,7 @@ __global__ void k_write(Geometry G, Work W, const uint64_t *file_out, uint64_t *
     const uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = lane_id();
     const uint64_t nsegs = total_segs(G, W);
-    if (g >= nsegs) return;
+    if (g >= nsegs || W.ctrl[1] != 0u) return;  // nothing to do when the fused fast path succeeded
     SegInfo I = seg_info(G, W, g);
     const uint64_t fo = file_out[I.f];
     if (g == I.first && lane == 0 && I.Lf > 0) {
@@ -778,6 +920,16 @@ bool sync_debug() {
         }                                                                      \
     } while (0)
 
+// CDC_FUSED=0 disables the fused look-back fast path (k_resolve/k_write always run)
+int fused_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CDC_FUSED");
+        v = (e && e[0] >= '0' && e[0] <= '9') ? e[0] - '0' : 1;
+    }
+    return v;
+}
+
 int check_params(const cdc_params *p) {
     if (!p) return fail(CDC_ERR_INVALID, "null params");
     if (p->algo < CDC_RAM || p->algo > CDC_AE_MIN) return fail(CDC_ERR_INVALID, "unknown algorithm");
@@ -836,7 +988,7 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     const uint64_t G = P.max_segs;
     size_t sz[] = {
         G * P.cap_list * 4,  // 0 list   } reset to 0xFF by one memset per call
-        G * 8,               // 1 pub    }
+        G * 16 + 64 + (G / 32 + 1) * 12,  // 1 pub, status, ctrl, grp, gcnt }
         G * P.cap_halo * 4,  // 2 halo
         G * 4,               // 3 cnt
         G * 4,               // 4 hcnt
@@ -872,6 +1024,10 @@ cdc::Work carve(const Plan &P, void *ws) {
     cdc::Work W;
     W.list = (uint32_t *)(b + P.off[0]);
     W.pub = (unsigned long long *)(b + P.off[1]);
+    W.status = W.pub + P.max_segs;
+    W.ctrl = reinterpret_cast<uint32_t *>(W.status + P.max_segs);
+    W.grp = W.status + P.max_segs + 8;
+    W.gcnt = reinterpret_cast<uint32_t *>(W.grp + P.max_segs / 32 + 1);
     W.halo = (uint32_t *)(b + P.off[2]);
     W.cnt = (uint32_t *)(b + P.off[3]);
     W.hcnt = (uint32_t *)(b + P.off[4]);
@@ -904,7 +1060,7 @@ template <int ALGO>
 int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::Work &W, uint64_t *d_bounds,
                     uint64_t cap, uint64_t *d_count, uint64_t *file_out, cudaStream_t st, bool batch) {
     static bool attr_set = false;
-    const int spec_smem = cdc::SPEC_WARPS * cdc::RING_SMEM;
+    const int spec_smem = cdc::SPEC_WARPS * cdc::RING_SMEM + 128;
     if (!attr_set) {
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_resolve<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -934,7 +1090,8 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     const uint64_t nseg_ub = P.max_segs;
     const uint64_t blocks = (nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS;
     if (blocks > 0) {
-        cdc::k_speculate<ALGO><<<(unsigned)blocks, cdc::SPEC_WARPS * 32, spec_smem, st>>>(G, W);
+        cdc::k_speculate<ALGO><<<(unsigned)blocks, cdc::SPEC_WARPS * 32, spec_smem, st>>>(G, W, d_bounds, cap,
+                                                                                          d_count, fused_mode());
         CDC_KCHECK("k_speculate", st);
         ++launches;
         pc.used[1] = true;
@@ -1022,6 +1179,46 @@ int cdc_abi_version(void) { return CDC_ABI_VERSION; }
 const char *cdc_last_error(void) { return g_err.c_str(); }
 
 int cdc_last_launch_count(void) { return g_launches; }
+
+int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, const void *d_workspace,
+              uint64_t *stats, void *stream) {
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!d_workspace || !stats) return fail(CDC_ERR_INVALID, "null pointer");
+    Plan P;
+    make_plan(p, nfiles ? nfiles : 1, total_len, max_len, P);
+    cdc::Work W = carve(P, const_cast<void *>(d_workspace));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint64_t G = 0;
+    if (nfiles <= 1 && P.S) G = (max_len + P.S - 1) / P.S;
+    if (nfiles > 1) CDC_CUDA(cudaMemcpyAsync(&G, W.seg_first + nfiles, 8, cudaMemcpyDeviceToHost, st));
+    uint32_t ctrl[2] = {0, 0};
+    CDC_CUDA(cudaMemcpyAsync(ctrl, W.ctrl, 8, cudaMemcpyDeviceToHost, st));
+    CDC_CUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> sj(G);
+    std::vector<uint32_t> hc(G);
+    if (G) {
+        CDC_CUDA(cudaMemcpyAsync(sj.data(), W.sj, G * 4, cudaMemcpyDeviceToHost, st));
+        CDC_CUDA(cudaMemcpyAsync(hc.data(), W.hcnt, G * 4, cudaMemcpyDeviceToHost, st));
+        CDC_CUDA(cudaStreamSynchronize(st));
+    }
+    uint64_t met = 0, unsynced = 0, other = 0, halo = 0;
+    for (uint64_t g = 0; g < G; ++g) {
+        if (sj[g] == (int32_t)(g + 1) || sj[g] == cdc::SJ_LAST) ++met;
+        else if (sj[g] == cdc::SJ_UNSYNCED) ++unsynced;
+        else ++other;
+        halo += hc[g];
+    }
+    stats[0] = G;
+    stats[1] = P.S;
+    stats[2] = P.Hmax;
+    stats[3] = ctrl[1] != 0 ? 1 : 0;
+    stats[4] = met;
+    stats[5] = unsynced;
+    stats[6] = other;
+    stats[7] = halo;
+    return CDC_OK;
+}
 
 int cdc_profile_query(int *done) {
     // completion state of the events of the last profiled call (1 = reached)
