@@ -209,6 +209,14 @@ int cdc_profile_query(int *done);
  *       undecided, [6] segments whose chain skipped a later segment or reached
  *       the stream end from a non-final segment, [7] total halo chunks.
  */
+/*
+ * Diagnostics: while d_buf (a device uint64 array of 4 x segments entries) is
+ * set, k_speculate records per segment {globaltimer at start, at the end of the
+ * walk, at the end of its fused write, SM id | halo chunks << 32}.  NULL turns
+ * recording off.  Never set during measurements.
+ */
+int cdc_debug_timing(void *d_buf);
+
 int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len,
               const void *d_workspace, uint64_t *stats, void *stream);
 

@@ -10,6 +10,8 @@ import os
 
 from .build import LIB
 
+# CDC_LIB selects another build of the same library (tuning variants under build/)
+LIB = os.environ.get("CDC_LIB", LIB)
 if not os.path.exists(LIB):
     raise ImportError(
         f"{LIB} is missing: build it with `python paper_2508_05797_b200/build.py` "
@@ -47,6 +49,7 @@ SIGNATURES = {
     "cdc_range_scan": ([_vp, _vp, _vp, _vp, _u64, _i32, _vp, _vp], ctypes.c_int),
     "cdc_profile_enable": ([ctypes.c_int], ctypes.c_int),
     "cdc_profile_query": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "cdc_debug_timing": ([_vp], ctypes.c_int),
     "cdc_stats": ([_P, _u64, _u64, _u64, _vp, ctypes.POINTER(_u64), _vp], ctypes.c_int),
     "cdc_profile_collect": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
                             ctypes.c_int),

@@ -33,14 +33,16 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or stale():
-        cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *SOURCES]
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines: list[str] | None = None) -> str:
+    """Compile SOURCES into `out` (default: the in-tree LIB); `defines` are extra -D flags (tuning variants)."""
+    out = out or LIB
+    if force or out != LIB or stale():
+        cmd = [nvcc(), *NVCC_FLAGS, *(f"-D{d}" for d in (defines or [])), "-o", out + ".tmp", *SOURCES]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -24,8 +24,14 @@
 namespace cdc {
 
 constexpr int BLK = 512;               // bytes per warp block: 32 lanes x 16 B
-constexpr int STAGE = 4096;            // bytes per TMA stage (8 warp blocks)
-constexpr int NST = 3;                 // ring depth per warp (12 KiB)
+#ifndef CDC_STAGE
+#define CDC_STAGE 4096
+#endif
+#ifndef CDC_NST
+#define CDC_NST 3
+#endif
+constexpr int STAGE = CDC_STAGE;       // bytes per TMA stage (8 warp blocks)
+constexpr int NST = CDC_NST;           // ring depth per warp (12 KiB)
 constexpr int RING_BYTES = STAGE * NST;
 constexpr int RING_SMEM = (RING_BYTES + NST * 8 + 127) / 128 * 128;  // keeps every ring 128-byte aligned
 
@@ -63,7 +69,18 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
 }
 // Watchdog: a stage that has not landed within ~10 s (clock64) means a lost
 // bulk copy; trap instead of hanging the GPU.
+__device__ unsigned long long g_wait_ns = 0;  // diagnostic: total ns spent waiting for stages (CDC_WAIT_PROBE)
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef CDC_WAIT_PROBE
+    unsigned long long t0g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0g));
+    while (!mbar_try_wait(bar, parity)) {
+    }
+    unsigned long long t1g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1g));
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_wait_ns, t1g - t0g);
+    return;
+#endif
     if (mbar_try_wait(bar, parity)) return;
     const long long t0 = clock64();
     while (!mbar_try_wait(bar, parity)) {

@@ -32,6 +32,10 @@
 namespace cdc {
 
 constexpr int SPEC_WARPS = 4;     // warps (segments) per CTA in k_speculate
+#ifndef CDC_SPEC_CTAS_PER_SM
+#define CDC_SPEC_CTAS_PER_SM 4
+#endif
+constexpr int SPEC_CTAS_PER_SM = CDC_SPEC_CTAS_PER_SM;  // resident k_speculate CTAs per SM (smem-bound)
 constexpr int HEAD_KEEP = 16384;  // bytes of each segment head kept in L2 for the halo re-read
 constexpr int RESOLVE_THREADS = 1024;
 
@@ -90,7 +94,11 @@ __device__ __forceinline__ void file_bounds(const Geometry &G, uint64_t f, uint6
         len = G.file_off[f + 1] - off;
     }
 }
-__device__ __forceinline__ uint64_t nseg_of(uint64_t len, uint64_t S) { return (len + S - 1) / S; }
+// Segments of a file of `len` bytes: floor(len / S), at least one; the last
+// segment absorbs the remainder (S <= its length < 2S), so no segment is tiny.
+__device__ __forceinline__ uint64_t nseg_of(uint64_t len, uint64_t S) {
+    return len == 0 ? 0 : (len < S ? 1 : len / S);
+}
 
 __device__ __forceinline__ void seg_first_of(const Geometry &G, const Work &W, uint64_t f, uint64_t &a,
                                              uint64_t &b) {
@@ -127,8 +135,17 @@ __device__ __forceinline__ SegInfo seg_info(const Geometry &G, const Work &W, ui
     file_bounds(G, I.f, I.foff, I.Lf);
     I.p = (int64_t)((g - a) * G.S);
     int64_t e = I.p + (int64_t)G.S;
-    I.seg_end = e < (int64_t)I.Lf ? e : (int64_t)I.Lf;
+    I.seg_end = (g == I.last || e > (int64_t)I.Lf) ? (int64_t)I.Lf : e;
     return I;
+}
+
+// global index and first byte (file-relative) of the segment of file position e
+__device__ __forceinline__ int64_t seg_of_pos(const SegInfo &I, int64_t e, uint64_t S, int64_t &pj) {
+    int64_t k = e / (int64_t)S;
+    const int64_t kmax = (int64_t)(I.last - I.first);
+    k = k < kmax ? k : kmax;
+    pj = k * (int64_t)S;
+    return (int64_t)I.first + k;
 }
 
 // Published lists.  list(g) holds the chunk starts of segment g's speculative
@@ -208,12 +225,12 @@ struct SpecEmit {
         if (lane == 0) halo[hcnt] = h;
         ++hcnt;
         // re-synchronisation: is e a start of the chain of the segment holding it?
-        const int64_t j = (int64_t)I.g + 1 + (e - I.seg_end) / (int64_t)G->S;
+        int64_t pj;
+        const int64_t j = seg_of_pos(I, e, G->S, pj);
         if (j != cur_j) {
             cur_j = j;
             cursor = 0;
         }
-        const int64_t pj = I.seg_end + (j - (int64_t)I.g - 1) * (int64_t)G->S;
         uint32_t idx = 0;
         const int r = list_lookup(W->list + (uint64_t)j * W->cap_list, W->cap_list, W->pub + j, (uint32_t)(e - pj),
                                   cursor, idx);
@@ -232,6 +249,20 @@ struct SpecEmit {
     __device__ void end() { sj = (I.seg_end >= (int64_t)I.Lf) ? SJ_LAST : SJ_STREAM_END; }
     __device__ void exhausted(int64_t) { sj = SJ_UNSYNCED; }
 };
+
+// Optional per-segment timing record (cdc_debug_timing): 4 x u64 per segment
+// {globaltimer at start, at the end of the walk, at the end, smid | hcnt << 32}.
+__device__ unsigned long long *g_timing = nullptr;
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
+}
 
 // Decoupled look-back words: the top two bits say what the low 62 bits (a
 // signed value) hold.  The memset leaves every word ~0 = not ready.
@@ -282,38 +313,61 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     return v;
 }
 
-// all 32 lanes; relaxed loads issued together, then one acquire fence per lane
+// All 32 lanes.  Relaxed loads issued together, then one acquire fence per
+// lane.  Groups confirmed ready are not read again, and the wait backs off
+// exponentially (a waiting warp sleeps instead of stealing issue slots from
+// the walkers still running on its SM).
 __device__ int64_t lookback(const Work &W, uint64_t g) {
     const int lane = lane_id();
     const uint64_t grp = g / LB_GROUP;
     const uint64_t g0 = grp * LB_GROUP;
+    uint64_t k0 = 0;      // groups [0, k0) are summed into `done`
+    int64_t done = 0;     // per-lane partial sum of confirmed groups
+    bool own_ok = false;
+    int64_t own = 0;
+    uint32_t sleep_ns = 256;
     for (;;) {
-        bool ok = true;
-        int64_t sum = 0;
-#pragma unroll 4
-        for (uint64_t k = lane; k < grp; k += 32) {
-            const unsigned long long wd = ld_relaxed_u64(W.grp + k);
-            ok &= (wd & ST_MASK) == ST_AGG;
-            sum += st_value(wd);
+        // groups [k0, grp), 32 per step, lane-parallel
+        while (k0 < grp) {
+            const uint64_t k = k0 + lane;
+            unsigned long long wd = 0;
+            bool ok = true;
+            if (k < grp) {
+                wd = ld_relaxed_u64(W.grp + k);
+                ok = (wd & ST_MASK) == ST_AGG;
+            }
+            const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
+            const uint32_t nvalid = (uint32_t)(grp - k0 < 32 ? grp - k0 : 32);
+            const uint32_t ready = bad ? (uint32_t)(__ffs(bad) - 1) : nvalid;  // leading ready groups
+            if ((uint32_t)lane < ready) done += st_value(wd);
+            k0 += ready;
+            if (ready < nvalid) break;
         }
-        if (g0 + lane < g) {
-            const unsigned long long wd = ld_relaxed_u64(W.status + g0 + lane);
-            ok &= (wd & ST_MASK) == ST_AGG;
-            sum += st_value(wd);
+        if (!own_ok) {
+            bool ok = true;
+            own = 0;
+            if (g0 + lane < g) {
+                const unsigned long long wd = ld_relaxed_u64(W.status + g0 + lane);
+                ok = (wd & ST_MASK) == ST_AGG;
+                own = st_value(wd);
+            }
+            own_ok = __all_sync(0xFFFFFFFFu, ok);
         }
-        if (__all_sync(0xFFFFFFFFu, ok)) {
+        if (k0 == grp && own_ok) {
             asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire what the observed releases published
             __syncwarp();
+            int64_t sum = done + own;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
             return sum;
         }
-        __nanosleep(128);
+        __nanosleep(sleep_ns);
+        if (sleep_ns < 2048) sleep_ns <<= 1;
     }
 }
 
 template <int ALGO>
-__global__ void __launch_bounds__(SPEC_WARPS * 32, 4) k_speculate(Geometry G, Work W, uint64_t *bounds,
+__global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate(Geometry G, Work W, uint64_t *bounds,
                                                                   uint64_t cap, uint64_t *d_count, int fused) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_ticket;
@@ -344,6 +398,8 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, 4) k_speculate(Geometry G, Wo
     em.cursor = 0;
     em.published = false;
     if (lane == 0) st_relaxed_u32(em.list, 0u);  // the speculative chain starts at the segment's first byte
+    unsigned long long *tm = g_timing;
+    if (tm && lane == 0) tm[4 * g] = globaltimer();
     const uint8_t *fbase = G.data + em.I.foff;
     int64_t read_end = (g == em.I.last) ? (int64_t)em.I.Lf
                                         : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
@@ -351,6 +407,10 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, 4) k_speculate(Geometry G, Wo
     const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
     run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
     em.publish();
+    if (tm && lane == 0) {
+        tm[4 * g + 1] = globaltimer();
+        tm[4 * g + 3] = smid() | ((unsigned long long)em.hcnt << 32);
+    }
 
     // ---- common case, fused resolve + write: the chain met the next segment's
     //      chain (or ended the file); anything else defers to k_resolve/k_write
@@ -393,6 +453,7 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, 4) k_speculate(Geometry G, Wo
         if (g == em.I.first && i == 0) continue;  // the file's first start (0) is not a boundary
         if (q - 1 < cap) bounds[q - 1] = v;
     }
+    if (tm && lane == 0) tm[4 * g + 2] = globaltimer();
     if (em.sj == SJ_LAST && lane == 0) {
         const uint64_t q = (uint64_t)(off + n) - 1;  // a file's last boundary is its length
         if (q < cap) bounds[q] = em.I.Lf;
@@ -417,12 +478,12 @@ struct WalkEmit {
     bool overflow;
 
     __device__ bool boundary(int64_t e) {
-        const int64_t j = (int64_t)I.g + 1 + (e - I.seg_end) / (int64_t)G->S;
+        int64_t pj;
+        const int64_t j = seg_of_pos(I, e, G->S, pj);
         if (j != cur_j) {
             cur_j = j;
             cursor = 0;
         }
-        const int64_t pj = I.seg_end + (j - (int64_t)I.g - 1) * (int64_t)G->S;
         uint32_t idx = 0;
         int r = list_lookup(W->list + (uint64_t)j * W->cap_list, W->cap_list, W->pub + j, (uint32_t)(e - pj), cursor,
                             idx);
@@ -481,12 +542,12 @@ __device__ void recheck_halo(const Geometry &G, Work &W, uint64_t g) {
     uint32_t cursor = 0;
     for (uint32_t i = 0; i < hc; ++i) {
         const int64_t e = I.seg_end + (int64_t)W.halo[g * W.cap_halo + i];
-        const int64_t j = (int64_t)g + 1 + (e - I.seg_end) / (int64_t)G.S;
+        int64_t pj;
+        const int64_t j = seg_of_pos(I, e, G.S, pj);
         if (j != cur_j) {
             cur_j = j;
             cursor = 0;
         }
-        const int64_t pj = I.seg_end + (j - (int64_t)g - 1) * (int64_t)G.S;
         uint32_t idx = 0;
         if (list_lookup(W.list + (uint64_t)j * W.cap_list, W.cap_list, W.pub + j, (uint32_t)(e - pj), cursor,
                         idx) == 1) {
@@ -964,7 +1025,7 @@ uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 // grid is a whole number of waves of SPEC_WARPS-warp CTAs), a multiple of the
 // TMA stage, at least 64 KiB and 4 max-size chunks, so that the
 // re-synchronisation halo (a few chunks on typical data) is small next to it.
-constexpr uint64_t SEGS_PER_SM = 16;
+constexpr uint64_t SEGS_PER_SM = (uint64_t)cdc::SPEC_WARPS * cdc::SPEC_CTAS_PER_SM;
 
 void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, Plan &P) {
     uint64_t S = p->seg_bytes;
@@ -981,7 +1042,7 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     P.Hmax = H;
     P.nfiles = nfiles;
     P.max_segs = (nfiles <= 1) ? (max_len + S - 1) / S + 1 : total_len / S + nfiles + 1;
-    P.cap_list = S / (p->window + 1) + 2;
+    P.cap_list = 2 * S / (p->window + 1) + 2;  // the last segment of a file holds up to 2S bytes
     P.cap_halo = H / (p->window + 1) + 3;
     P.pool_cap = total_len / (p->window + 1) + 2;
     P.exc_cap = P.max_segs;
@@ -1180,6 +1241,20 @@ const char *cdc_last_error(void) { return g_err.c_str(); }
 
 int cdc_last_launch_count(void) { return g_launches; }
 
+// diagnostic (CDC_WAIT_PROBE builds): read and reset the summed stage-wait time
+extern "C" int cdc_debug_wait_ns(unsigned long long *ns) {
+    CDC_CUDA(cudaMemcpyFromSymbol(ns, cdc::g_wait_ns, sizeof(*ns)));
+    unsigned long long z = 0;
+    CDC_CUDA(cudaMemcpyToSymbol(cdc::g_wait_ns, &z, sizeof(z)));
+    return CDC_OK;
+}
+
+int cdc_debug_timing(void *d_buf) {
+    unsigned long long *p = static_cast<unsigned long long *>(d_buf);
+    CDC_CUDA(cudaMemcpyToSymbol(cdc::g_timing, &p, sizeof(p)));
+    return CDC_OK;
+}
+
 int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, const void *d_workspace,
               uint64_t *stats, void *stream) {
     int rc = check_params(p);
@@ -1190,7 +1265,7 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
     cdc::Work W = carve(P, const_cast<void *>(d_workspace));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint64_t G = 0;
-    if (nfiles <= 1 && P.S) G = (max_len + P.S - 1) / P.S;
+    if (nfiles <= 1 && P.S) G = max_len == 0 ? 0 : (max_len < P.S ? 1 : max_len / P.S);
     if (nfiles > 1) CDC_CUDA(cudaMemcpyAsync(&G, W.seg_first + nfiles, 8, cudaMemcpyDeviceToHost, st));
     uint32_t ctrl[2] = {0, 0};
     CDC_CUDA(cudaMemcpyAsync(ctrl, W.ctrl, 8, cudaMemcpyDeviceToHost, st));

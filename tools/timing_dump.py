@@ -1,0 +1,53 @@
+"""Per-segment walk timing of one configs[1] call (diagnostic; not a measurement)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+import paper_2508_05797_b200 as cdc  # noqa: E402
+from paper_2508_05797_b200._lib import lib  # noqa: E402
+
+n = 256 << 20
+algo = os.environ.get("ALGO", "ae_max")
+avg = int(os.environ.get("AVG", "4096"))
+seg = int(os.environ.get("SEG", "0"))
+d = synth.zipf_bytes(n, 1.1, 1) if os.environ.get("DATA", "zipf") == "zipf" else synth.uniform(n, 0)
+t = torch.from_numpy(d).cuda()
+p = cdc.params(algo, avg_size=avg, seg_bytes=seg)
+ws = torch.empty(cdc.workspace_size(p, 1, n, n), dtype=torch.uint8, device="cuda")
+cap = cdc.max_boundaries(p, n)
+b = torch.empty(cap, dtype=torch.int64, device="cuda")
+c = torch.zeros(1, dtype=torch.int64, device="cuda")
+for _ in range(3):
+    cdc.chunk_async(t, p, b, c, ws)
+st = cdc.stats(p, ws, 1, n, n)
+G = st["segments"]
+tm = torch.zeros(4 * G, dtype=torch.int64, device="cuda")
+lib.cdc_debug_timing(tm.data_ptr())
+cdc.chunk_async(t, p, b, c, ws)
+torch.cuda.synchronize()
+lib.cdc_debug_timing(None)
+a = tm.cpu().numpy().reshape(G, 4)
+t0 = a[:, 0].min()
+start = (a[:, 0] - t0) / 1e3
+walk = (a[:, 1] - a[:, 0]) / 1e3
+done = (a[:, 2] - t0) / 1e3
+sm = a[:, 3] & 0xFFFFFFFF
+halo = a[:, 3] >> 32
+print(st)
+print("start us: min %.1f max %.1f" % (start.min(), start.max()))
+print("walk us: min %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f mean %.1f" % (walk.min(), *np.percentile(walk, [10, 50, 90]), walk.max(), walk.mean()))
+print("walk end us (abs): p50 %.1f p90 %.1f max %.1f" % tuple(np.percentile(start + walk, [50, 90, 100])))
+print("done us (abs): p50 %.1f max %.1f" % (np.percentile(done, 50), done.max()))
+print("halo chunks: mean %.2f max %d" % (halo.mean(), halo.max()))
+# per-SM: segments and summed walk
+for s_ in np.argsort([-walk[sm == k].max() if (sm == k).any() else 0 for k in range(148)])[:5]:
+    m = sm == s_
+    print("sm", s_, "segs", m.sum(), "walk max %.1f mean %.1f" % (walk[m].max(), walk[m].mean()))
+# correlation of walk time with halo length and with g
+print("corr(walk, halo) %.2f corr(walk, g) %.2f" % (np.corrcoef(walk, halo)[0, 1], np.corrcoef(walk, np.arange(G))[0, 1]))
+slow = np.argsort(-walk)[:10]
+print("slowest segs", slow.tolist(), walk[slow].round(1).tolist(), "halo", halo[slow].tolist(), "sm", sm[slow].tolist())
