@@ -160,6 +160,20 @@ int cdc_chain(const cdc_params *p, const uint8_t *d_data, uint64_t len,
               uint64_t starts_cap, uint64_t *d_count, void *stream);
 
 /*
+ * Cross-shard re-synchronisation (range sharding across GPUs):
+ * the first element of the ascending device list d_a[0..na) that also occurs
+ * in the ascending device list d_b[0..nb).  Writes d_out[0] = its index in
+ * d_a (na when there is none) and d_out[1] = its index in d_b (-1 when there
+ * is none).  Used with d_a = the chunk starts with which shard r's chain
+ * continues past its range, d_b = the starts of shard r+1's own chain: from
+ * the first common start on the two chains are identical (content-defined
+ * boundaries depend only on the bytes after a chunk start).  na, nb < 2^32.
+ * Asynchronous on `stream`.
+ */
+int cdc_first_common(const int64_t *d_a, uint64_t na, const int64_t *d_b, uint64_t nb, int64_t *d_out,
+                     void *stream);
+
+/*
  * Batched Extreme Byte Search (§4.1): for each region r in [0, n),
  * region = d_data[d_off[r] .. d_off[r] + d_len[r]) (d_len[r] >= 1),
  * writes the max (mode CDC_EXT_MAX) or min byte to d_value[r] and its

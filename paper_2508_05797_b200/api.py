@@ -19,7 +19,7 @@ CMPS = {"gt": 0, "geq": 1, "lt": 2, "leq": 3, "eq": 4}
 __all__ = [
     "CdcError", "ALGOS", "params", "window_for_avg", "max_boundaries", "workspace_size",
     "chunk_async", "chunk", "chunk_batch", "chunk_host", "chain",
-    "extreme_byte_search", "range_scan", "last_launch_count", "abi_version",
+    "extreme_byte_search", "range_scan", "first_common", "last_launch_count", "abi_version",
     "profile_enable", "profile_collect", "KERNELS", "stats",
 ]
 
@@ -177,6 +177,16 @@ def chain(data: torch.Tensor, p: cdc_params, start: int, stop: int, cap: int | N
     if m > cap:
         raise CdcError(f"chain length {m} exceeds capacity {cap}")
     return out[:m]
+
+
+def first_common(a: torch.Tensor, b: torch.Tensor, stream=None) -> torch.Tensor:
+    """cdc_first_common: (index in a, index in b) of the first element of sorted a found in sorted b."""
+    if not (a.is_cuda and b.is_cuda and a.dtype == torch.int64 and b.dtype == torch.int64):
+        raise TypeError("a and b must be CUDA int64 tensors")
+    a, b = a.contiguous(), b.contiguous()
+    out = torch.empty(2, dtype=torch.int64, device=a.device)
+    check(lib.cdc_first_common(a.data_ptr(), a.numel(), b.data_ptr(), b.numel(), out.data_ptr(), _stream_ptr(stream)))
+    return out
 
 
 def _regions(offsets, lengths, device):

@@ -837,6 +837,38 @@ __global__ void __launch_bounds__(32) k_chain(const uint8_t *data, uint64_t len,
     if (lane_id() == 0) *count = em.n;
 }
 
+// ------------------------------------------------------------------ cross-shard re-synchronisation
+// First element of the ascending list a[0..na) that also occurs in the
+// ascending list b[0..nb): out[0] = its index in a (na if none), out[1] = its
+// index in b (-1 if none).  One CTA; every element of a is binary-searched in b
+// in parallel and the smallest hit index wins.
+__global__ void __launch_bounds__(1024) k_first_common(const int64_t *a, uint64_t na, const int64_t *b, uint64_t nb,
+                                                       int64_t *out) {
+    __shared__ unsigned long long best;  // (index in a << 32) | index in b
+    if (threadIdx.x == 0) best = ~0ull;
+    __syncthreads();
+    for (uint64_t i = threadIdx.x; i < na; i += blockDim.x) {
+        const int64_t x = a[i];
+        uint64_t lo = 0, hi = nb;  // first b[k] >= x
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (b[mid] < x) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo < nb && b[lo] == x) atomicMin(&best, ((unsigned long long)i << 32) | (unsigned long long)lo);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (best == ~0ull) {
+            out[0] = (int64_t)na;
+            out[1] = -1;
+        } else {
+            out[0] = (int64_t)(best >> 32);
+            out[1] = (int64_t)(best & 0xFFFFFFFFull);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ primitives (§4.1, §4.2)
 // One warp per region.  The region is walked in 512-byte warp blocks of
 // 16-byte aligned lane vectors; bytes outside the region are masked.
@@ -1445,6 +1477,17 @@ int cdc_chain(const cdc_params *p, const uint8_t *d_data, uint64_t len, uint64_t
         cdc::k_chain<2><<<1, 32, cdc::RING_SMEM + 128, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
                                                        starts_cap, d_count);
     }
+    g_launches = 1;
+    CDC_CUDA(cudaGetLastError());
+    return CDC_OK;
+}
+
+int cdc_first_common(const int64_t *d_a, uint64_t na, const int64_t *d_b, uint64_t nb, int64_t *d_out,
+                     void *stream) {
+    if (!d_out || (na && !d_a) || (nb && !d_b)) return fail(CDC_ERR_INVALID, "null pointer");
+    if (na >= (1ull << 32) || nb >= (1ull << 32)) return fail(CDC_ERR_INVALID, "lists longer than 2^32 entries");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cdc::k_first_common<<<1, 1024, 0, st>>>(d_a, na, d_b, nb, d_out);
     g_launches = 1;
     CDC_CUDA(cudaGetLastError());
     return CDC_OK;
