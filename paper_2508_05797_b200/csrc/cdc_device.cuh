@@ -120,6 +120,19 @@ __device__ __forceinline__ void st_relaxed_u32(uint32_t *p, uint32_t v) {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Diagnostic event counters (CDC_COUNTERS builds only): CNT(i) adds 1 per warp.
+__device__ unsigned long long g_cnt[16];
+#ifdef CDC_COUNTERS
+#define CNT(i)                                              \
+    do {                                                    \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_cnt[i], 1ull); \
+    } while (0)
+#else
+#define CNT(i) \
+    do {       \
+    } while (0)
+#endif
+
 // ---------------------------------------------------------------- byte SIMD
 // Extreme of bytes with the DPX 3-input u16x2 min/max: the high byte of the
 // u16 extreme of a set of 16-bit halves is the extreme of their high bytes,
@@ -314,6 +327,43 @@ __device__ __forceinline__ uint32_t stage_lane_ext(const uint8_t *sp, int lo, in
     return acc;
 }
 
+// RAM window (Extreme Byte Search, §4.1) with early saturation: folds the
+// per-lane max of the stage bytes [lo, hi) into acc, and stops as soon as some
+// byte equals 255 -- no byte can exceed it, so the window's maximum is known
+// and the rest of the window need not be read.  Returns true when saturated.
+__device__ __forceinline__ bool stage_window_max(const uint8_t *sp, int lo, int hi, uint32_t &acc) {
+    const int lane16 = lane_id() * 16;
+    int Bk = lo & ~(BLK - 1);
+    uint4 v;
+    bool has;
+    if (Bk < lo || Bk + BLK > hi) {  // partial head block
+        if (Bk >= hi) return false;
+        const uint32_t lm = block_lane_ext<true>(sp, Bk, lo, hi < Bk + BLK ? hi : Bk + BLK, has, v);
+        acc = max(acc, lm);
+        if (__any_sync(0xFFFFFFFFu, lm == 255u)) return true;
+        Bk += BLK;
+    }
+    for (; Bk + 2 * BLK <= hi; Bk += 2 * BLK) {
+        const uint4 a = *reinterpret_cast<const uint4 *>(sp + Bk + lane16);
+        const uint4 b = *reinterpret_cast<const uint4 *>(sp + Bk + BLK + lane16);
+        const uint32_t m = max(vext16<true>(a), vext16<true>(b));
+        acc = max(acc, m);
+        if (__any_sync(0xFFFFFFFFu, m == 255u)) return true;
+    }
+    for (; Bk + BLK <= hi; Bk += BLK) {
+        v = *reinterpret_cast<const uint4 *>(sp + Bk + lane16);
+        const uint32_t m = vext16<true>(v);
+        acc = max(acc, m);
+        if (__any_sync(0xFFFFFFFFu, m == 255u)) return true;
+    }
+    if (Bk < hi) {  // partial tail block
+        const uint32_t lm = block_lane_ext<true>(sp, Bk, Bk, hi, has, v);
+        acc = max(acc, lm);
+        if (__any_sync(0xFFFFFFFFu, lm == 255u)) return true;
+    }
+    return false;
+}
+
 // Range Scan (§4.2), block level: first 512-byte block of the stage bytes
 // [lo, hi) holding a byte b with (b CMP target).  Returns its stage offset Bk
 // (or -1), the ballot of the lanes holding one, and each lane's extreme `lm`
@@ -326,8 +376,10 @@ __device__ __forceinline__ int stage_find_block(const uint8_t *sp, int lo, int h
     const int lane16 = lane_id() * 16;
     int Bk = lo & ~(BLK - 1);
     uint4 v;
+    CNT(7);
     if (Bk < lo || Bk + BLK > hi) {  // partial head block
         if (Bk >= hi) return -1;
+        CNT(9);
         lm = block_lane_ext<MAX>(sp, Bk, lo, hi < Bk + BLK ? hi : Bk + BLK, has, v);
         bal = __ballot_sync(0xFFFFFFFFu, has && cmp_holds<CMP>(lm, target));
         if (bal) return Bk;
@@ -335,6 +387,7 @@ __device__ __forceinline__ int stage_find_block(const uint8_t *sp, int lo, int h
     }
     has = true;
     for (; Bk + 2 * BLK <= hi; Bk += 2 * BLK) {
+        CNT(8);
         const uint4 a = *reinterpret_cast<const uint4 *>(sp + Bk + lane16);
         const uint4 b = *reinterpret_cast<const uint4 *>(sp + Bk + BLK + lane16);
         const uint32_t ma = vext16<MAX>(a), mb = vext16<MAX>(b);
@@ -357,6 +410,7 @@ __device__ __forceinline__ int stage_find_block(const uint8_t *sp, int lo, int h
         if (bal) return Bk;
     }
     if (Bk < hi) {  // partial tail block
+        CNT(10);
         lm = block_lane_ext<MAX>(sp, Bk, Bk, hi, has, v);
         bal = __ballot_sync(0xFFFFFFFFu, has && cmp_holds<CMP>(lm, target));
         if (bal) return Bk;
@@ -441,6 +495,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     int64_t c = s;                                                               // next byte to examine
     bool stop = false;
     bool scanning = false;  // RAM: false = window [s, s+w), true = scan for a byte >= M
+    bool wsat = false;      // RAM: the window already holds a 255
     uint32_t M = 0, acc = 0;
     uint32_t ext = 0;       // AE: current target value
     int64_t t = 0;          // AE: current target position
@@ -465,6 +520,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
         limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
         if constexpr (ALGO == ALGO_RAM) {
             scanning = false;
+            wsat = false;
             acc = 0;
             if (s + W >= Lf) {
                 emit.end();
@@ -480,6 +536,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     uint32_t parity = 0;
     int64_t k = 0;
     for (; k < nstages && !stop; ++k) {
+        CNT(0);
         const int64_t SB = B0 + k * STAGE;
         mbar_wait(&R.bar[slot], parity);
         const uint8_t *sp = R.buf + slot * STAGE;
@@ -499,6 +556,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
         }
         // a boundary at stage offset er
         auto event = [&](int er) -> bool {
+            CNT(6);
             if (on_boundary(SB + er)) return true;
             cr = er;
             limr = rel(limit);
@@ -510,10 +568,11 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
             if constexpr (ALGO == ALGO_RAM) {
                 if (!scanning) {
                     const int hi = hor < endr ? hor : endr;
-                    acc = max(acc, stage_lane_ext<true>(sp, cr, hi));
+                    CNT(11);
+                    if (!wsat) wsat = stage_window_max(sp, cr, hi, acc);  // a saturated window skips its rest
                     cr = hi;
                     if (cr == hor) {
-                        M = warp_ext<true>(acc);
+                        M = wsat ? 255u : warp_ext<true>(acc);
                         scanning = true;
                         hor = FAR;
                     }
@@ -521,6 +580,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                     const int hi = limr < endr ? limr : endr;
                     uint32_t bal = 0, lm;
                     bool has;
+                    CNT(12);
                     const int Bk = stage_find_block<CMP_GEQ>(sp, cr, hi, M, bal, lm, has);
                     int er;
                     if (Bk >= 0) {
@@ -537,6 +597,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                 }
             } else {
                 if (pending) {  // first byte of the chunk: the first target
+                    CNT(1);
                     ext = sp[cr];
                     t = SB + cr;
                     hor = cr + W1 < FAR ? cr + W1 : FAR;
@@ -546,11 +607,14 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                 }
                 int hi = hor < limr ? hor : limr;
                 hi = hi < endr ? hi : endr;
+                if (ext == SAT) CNT(5);
                 if (ext != SAT && cr < hi) {
                     uint32_t bal = 0, lm;
                     bool has;
+                    CNT(2);
                     const int Bk = stage_find_block<CMP_BEAT>(sp, cr, hi, ext, bal, lm, has);
                     if (Bk >= 0) {
+                        CNT(3);
                         const int lo = cr > Bk ? cr : Bk;
                         const int bh = hi < Bk + BLK ? hi : Bk + BLK;
                         int r;

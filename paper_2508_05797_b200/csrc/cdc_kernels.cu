@@ -1068,7 +1068,11 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
         if (S < lo) S = lo;
         if (S > (256ull << 20)) S = 256ull << 20;
     }
-    uint64_t H = p->halo_bytes ? p->halo_bytes : std::max<uint64_t>(2 * S, 64ull * (p->window + 1));
+    // halo cap: chains started at arbitrary offsets meet within a few chunks on
+    // skewed data but only after ~(w/362)^2 chunks on uniform bytes (the phase
+    // difference of two chains random-walks): 1024 windows, <= 64 MiB
+    uint64_t H = p->halo_bytes ? p->halo_bytes
+                               : std::min<uint64_t>(std::max<uint64_t>(2 * S, 1024ull * (p->window + 1)), 64ull << 20);
     if (H >= (1ull << 31)) H = (1ull << 31) - 1;
     P.S = S;
     P.Hmax = H;
@@ -1272,6 +1276,14 @@ int cdc_abi_version(void) { return CDC_ABI_VERSION; }
 const char *cdc_last_error(void) { return g_err.c_str(); }
 
 int cdc_last_launch_count(void) { return g_launches; }
+
+// diagnostic (CDC_COUNTERS builds): read and reset the 16 event counters
+extern "C" int cdc_debug_counters(unsigned long long *out) {
+    CDC_CUDA(cudaMemcpyFromSymbol(out, cdc::g_cnt, 16 * sizeof(unsigned long long)));
+    unsigned long long z[16] = {0};
+    CDC_CUDA(cudaMemcpyToSymbol(cdc::g_cnt, z, sizeof(z)));
+    return CDC_OK;
+}
 
 // diagnostic (CDC_WAIT_PROBE builds): read and reset the summed stage-wait time
 extern "C" int cdc_debug_wait_ns(unsigned long long *ns) {

@@ -1,0 +1,44 @@
+"""Throughput of the single-GPU path on the shapes of every BASELINE config (diagnostic)."""
+import os, sys, time
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth
+import paper_2508_05797_b200 as cdc
+
+
+def run(name, data_np, algo, avg, reps=10, seg=0):
+    t = torch.from_numpy(data_np).cuda()
+    n = t.numel()
+    p = cdc.params(algo, avg_size=avg, seg_bytes=seg)
+    ws = torch.empty(cdc.workspace_size(p, 1, n, n), dtype=torch.uint8, device="cuda")
+    b = torch.empty(cdc.max_boundaries(p, n), dtype=torch.int64, device="cuda")
+    c = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        cdc.chunk_async(t, p, b, c, ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        cdc.chunk_async(t, p, b, c, ws)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    st = cdc.stats(p, ws, 1, n, n)
+    print("%-28s %-6s %5d  %8.3f ms  %8.1f GB/s  chunks %d  %s" % (name, algo, avg, ms, n / ms / 1e6, int(c.item()),
+          {k: st[k] for k in ("segments", "fast_path", "synced", "unsynced", "skipped_or_end", "halo_chunks")}),
+          flush=True)
+
+
+sel = os.environ.get("ONLY", "")
+if not sel or "c0" in sel:
+    run("c0 uniform 16MiB", synth.uniform(16 << 20, 0), "ram", 8192)
+if not sel or "c1" in sel:
+    run("c1 zipf 256MiB", synth.zipf_bytes(256 << 20, 1.1, 1), "ae_max", 4096)
+if not sel or "u256" in sel:
+    u = synth.uniform(256 << 20, 0)
+    for algo in ("ram", "ae_max"):
+        for avg in (4096, 8192, 16384):
+            run("uniform 256MiB", u, algo, avg, reps=3)
+if not sel or "c4" in sel:
+    run("c4-shape alternating 1GiB", synth.alternating(1 << 30, region=256 << 20, seed=5), "ram", 8192, reps=3)
