@@ -70,7 +70,7 @@ typedef struct {
     int32_t  algo;        /* cdc_algo */
     uint32_t window;      /* w >= 1: the fixed-size window of §2.1.2 */
     uint64_t max_size;    /* chunk length cap, > window */
-    uint64_t seg_bytes;   /* speculation segment size S (0 = automatic); multiple of 2048 */
+    uint64_t seg_bytes;   /* speculation segment size S (0 = automatic); multiple of 16 */
     uint64_t halo_bytes;  /* max speculative halo walk past a segment end (0 = automatic) */
 } cdc_params;
 

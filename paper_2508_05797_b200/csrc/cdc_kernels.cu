@@ -94,10 +94,18 @@ __device__ __forceinline__ void file_bounds(const Geometry &G, uint64_t f, uint6
         len = G.file_off[f + 1] - off;
     }
 }
-// Segments of a file of `len` bytes: floor(len / S), at least one; the last
-// segment absorbs the remainder (S <= its length < 2S), so no segment is tiny.
+// Segments of a file of `len` bytes: n = floor(len / S), at least one.  Segment
+// k covers [start(k), start(k+1)) with start(k) = k floor(len / n) rounded down
+// to 4 KiB (16 B for short files), the last one ending at len: lengths differ
+// by less than one alignment unit plus n bytes (none is tiny, none twice as
+// long) and every start is aligned for the TMA ring.
 __device__ __forceinline__ uint64_t nseg_of(uint64_t len, uint64_t S) {
     return len == 0 ? 0 : (len < S ? 1 : len / S);
+}
+__device__ __forceinline__ int64_t seg_start(uint64_t k, uint64_t n, uint64_t len) {
+    const uint64_t q = len / n;
+    const uint64_t align = q >= (64u << 10) ? 4095u : 15u;
+    return k >= n ? (int64_t)len : (int64_t)((k * q) & ~align);
 }
 
 __device__ __forceinline__ void seg_first_of(const Geometry &G, const Work &W, uint64_t f, uint64_t &a,
@@ -133,18 +141,25 @@ __device__ __forceinline__ SegInfo seg_info(const Geometry &G, const Work &W, ui
     I.first = a;
     I.last = b - 1;
     file_bounds(G, I.f, I.foff, I.Lf);
+#ifdef CDC_OLD_GEOM
     I.p = (int64_t)((g - a) * G.S);
-    int64_t e = I.p + (int64_t)G.S;
+    const int64_t e = I.p + (int64_t)G.S;
     I.seg_end = (g == I.last || e > (int64_t)I.Lf) ? (int64_t)I.Lf : e;
+#else
+    I.p = seg_start(g - a, b - a, I.Lf);
+    I.seg_end = seg_start(g - a + 1, b - a, I.Lf);
+#endif
     return I;
 }
 
 // global index and first byte (file-relative) of the segment of file position e
-__device__ __forceinline__ int64_t seg_of_pos(const SegInfo &I, int64_t e, uint64_t S, int64_t &pj) {
-    int64_t k = e / (int64_t)S;
-    const int64_t kmax = (int64_t)(I.last - I.first);
-    k = k < kmax ? k : kmax;
-    pj = k * (int64_t)S;
+__device__ __forceinline__ int64_t seg_of_pos(const SegInfo &I, int64_t e, uint64_t, int64_t &pj) {
+    const uint64_t n = I.last - I.first + 1;
+    int64_t k = e / (int64_t)(I.Lf / n);
+    if (k > (int64_t)n - 1) k = (int64_t)n - 1;
+    while (k > 0 && seg_start(k, n, I.Lf) > e) --k;
+    while (k + 1 < (int64_t)n && seg_start(k + 1, n, I.Lf) <= e) ++k;
+    pj = seg_start(k, n, I.Lf);
     return (int64_t)I.first + k;
 }
 
@@ -274,6 +289,12 @@ __device__ __forceinline__ int64_t st_value(unsigned long long w) {
 __device__ __forceinline__ unsigned long long st_word(unsigned long long flag, int64_t v) {
     return flag | ((unsigned long long)v & ~ST_MASK);
 }
+// a segment's status word: ST_AGG | sb << 32 | (uint32) a  (sb < 2^30, |a| < 2^31)
+__device__ __forceinline__ unsigned long long seg_word(uint32_t sb, int64_t a) {
+    return ST_AGG | ((unsigned long long)(sb & 0x3FFFFFFFu) << 32) | (unsigned long long)(uint32_t)(int32_t)a;
+}
+__device__ __forceinline__ int64_t seg_a(unsigned long long w) { return (int64_t)(int32_t)(uint32_t)w; }
+__device__ __forceinline__ uint32_t seg_sb(unsigned long long w) { return (uint32_t)(w >> 32) & 0x3FFFFFFFu; }
 
 // Output offset of segment g's first true chain start.  With entry(g) = sb(g-1)
 // (the index in list(g) where segment g-1's chain met it; 0 at a file's first
@@ -285,22 +306,31 @@ __device__ __forceinline__ unsigned long long st_word(unsigned long long flag, i
 // before its own and the members of its group before it: at most
 // ceil(G/1024) + 1 independent loads per lane.  Returns sum_{h<g} a_h.
 constexpr int LB_GROUP = 32;
+#ifndef CDC_SLEEP0
+#define CDC_SLEEP0 1024
+#endif
+#ifndef CDC_SLEEPMAX
+#define CDC_SLEEPMAX 4096
+#endif
+// look-back waits sleep (exponential backoff) instead of polling hard: waiting
+// warps share their SM with walkers that are still running
+constexpr uint32_t SLEEP0 = CDC_SLEEP0, SLEEPMAX = CDC_SLEEPMAX;
 constexpr uint64_t LB_MAX_SEGS = 32768;  // beyond this the k_resolve scan is used
 
 // all 32 lanes
-__device__ void publish_agg(Work &W, uint64_t g, uint64_t nsegs, int64_t a) {
+__device__ void publish_agg(Work &W, uint64_t g, uint64_t nsegs, int64_t a, uint32_t sb) {
     const int lane = lane_id();
     const uint64_t grp = g / LB_GROUP;
     const uint64_t gsz = (grp + 1) * LB_GROUP <= nsegs ? LB_GROUP : nsegs - grp * LB_GROUP;
     uint32_t old = 0;
     if (lane == 0) {
-        st_release_u64(W.status + g, st_word(ST_AGG, a));
+        st_release_u64(W.status + g, seg_word(sb, a));
         asm volatile("atom.acq_rel.gpu.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(W.gcnt + grp) : "memory");
     }
     old = __shfl_sync(0xFFFFFFFFu, old, 0);
     if (old + 1u == (uint32_t)gsz - 1u) {  // the counter starts at ~0: this is the group's last arrival
         // one load per lane (acquire loads issued by one thread would serialise)
-        int64_t v = lane < (int)gsz ? st_value(ld_acquire_u64(W.status + grp * LB_GROUP + lane)) : 0;
+        int64_t v = lane < (int)gsz ? seg_a(ld_acquire_u64(W.status + grp * LB_GROUP + lane)) : 0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
         if (lane == 0) st_release_u64(W.grp + grp, st_word(ST_AGG, v));
@@ -317,7 +347,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 // lane.  Groups confirmed ready are not read again, and the wait backs off
 // exponentially (a waiting warp sleeps instead of stealing issue slots from
 // the walkers still running on its SM).
-__device__ int64_t lookback(const Work &W, uint64_t g) {
+__device__ int64_t lookback(const Work &W, uint64_t g, uint32_t &sb_prev) {
     const int lane = lane_id();
     const uint64_t grp = g / LB_GROUP;
     const uint64_t g0 = grp * LB_GROUP;
@@ -325,7 +355,8 @@ __device__ int64_t lookback(const Work &W, uint64_t g) {
     int64_t done = 0;     // per-lane partial sum of confirmed groups
     bool own_ok = false;
     int64_t own = 0;
-    uint32_t sleep_ns = 256;
+    uint32_t sbp = 0;
+    uint32_t sleep_ns = SLEEP0;
     for (;;) {
         // groups [k0, grp), 32 per step, lane-parallel
         while (k0 < grp) {
@@ -349,7 +380,12 @@ __device__ int64_t lookback(const Work &W, uint64_t g) {
             if (g0 + lane < g) {
                 const unsigned long long wd = ld_relaxed_u64(W.status + g0 + lane);
                 ok = (wd & ST_MASK) == ST_AGG;
-                own = st_value(wd);
+                own = seg_a(wd);
+                if (g0 + lane == g - 1) sbp = seg_sb(wd);
+            } else if (lane == 31 && g0 == g) {  // g-1 ends the previous group
+                const unsigned long long wd = ld_relaxed_u64(W.status + g - 1);
+                ok = (wd & ST_MASK) == ST_AGG;
+                sbp = seg_sb(wd);
             }
             own_ok = __all_sync(0xFFFFFFFFu, ok);
         }
@@ -359,10 +395,11 @@ __device__ int64_t lookback(const Work &W, uint64_t g) {
             int64_t sum = done + own;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+            sb_prev = __reduce_or_sync(0xFFFFFFFFu, sbp);  // only one lane holds it
             return sum;
         }
         __nanosleep(sleep_ns);
-        if (sleep_ns < 2048) sleep_ns <<= 1;
+        if (sleep_ns < SLEEPMAX) sleep_ns <<= 1;
     }
 }
 
@@ -428,16 +465,28 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
         W.sb[g] = em.sb;
         if (!normal) atomicAnd(W.ctrl + 1, 0u);  // the fast path's output is void
     }
-    if (fused) publish_agg(W, g, nsegs, a);
+    // stage this segment's chain starts (list, then the halo tail) in the ring's
+    // shared memory as offsets from p, so the write after the look-back needs no
+    // global round trip (falls back to the global lists when they do not fit)
+    uint32_t *stg = reinterpret_cast<uint32_t *>(wbase);
+    const uint32_t nst = em.cnt + tail;
+#ifdef CDC_NO_STAGE
+    const bool staged = false;
+#else
+    const bool staged = nst <= (uint32_t)(RING_BYTES / 4);
+#endif
+    if (fused && normal && staged) {
+        const uint32_t hoff = (uint32_t)(em.I.seg_end - em.I.p);
+        for (uint32_t i = lane; i < nst; i += 32)
+            stg[i] = i < em.cnt ? ld_relaxed_u32(em.list + i) : hoff + em.halo[i - em.cnt];
+    }
+    if (fused) publish_agg(W, g, nsegs, a, sb);
     if (!fused || fused_dbg == 3) return;
-    const int64_t excl = g == 0 ? 0 : lookback(W, g);
-    if (!normal || fused_dbg == 2) return;
-    // entry(g) = sb(g-1): the previous segment stored it before releasing its status
-    // word (observed directly, or through its group's sum) and the look-back
-    // ended with an acquire fence; lane 0 reads it and broadcasts
     uint32_t entry = 0;
-    if (g != em.I.first && lane == 0) entry = ld_relaxed_u32(W.sb + g - 1);
-    entry = __shfl_sync(0xFFFFFFFFu, entry, 0);
+    const int64_t excl = g == 0 ? 0 : lookback(W, g, entry);
+    if (!normal || fused_dbg == 2) return;
+    // entry(g) = sb(g-1), carried in segment g-1's status word
+    if (g == em.I.first) entry = 0;
     const int64_t off = excl + entry;                     // output index of list[entry]
     const int64_t A = (int64_t)em.cnt - entry;            // true starts from this segment's list
     const int64_t n = A + tail;
@@ -448,7 +497,9 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
     __syncwarp();
     if (lane == 0) W.seg_out[g] = (uint64_t)off;
     for (int64_t i = lane; i < n; i += 32) {
-        const uint64_t v = i < A ? (uint64_t)em.I.p + em.list[entry + i] : (uint64_t)em.I.seg_end + em.halo[i - A];
+        uint64_t v;
+        if (staged) v = (uint64_t)em.I.p + stg[entry + i];
+        else v = i < A ? (uint64_t)em.I.p + em.list[entry + i] : (uint64_t)em.I.seg_end + em.halo[i - A];
         const uint64_t q = (uint64_t)off + i;
         if (g == em.I.first && i == 0) continue;  // the file's first start (0) is not a boundary
         if (q - 1 < cap) bounds[q - 1] = v;
@@ -1028,7 +1079,7 @@ int check_params(const cdc_params *p) {
     if (p->algo < CDC_RAM || p->algo > CDC_AE_MIN) return fail(CDC_ERR_INVALID, "unknown algorithm");
     if (p->window < 1) return fail(CDC_ERR_INVALID, "window must be >= 1");
     if (p->max_size <= p->window) return fail(CDC_ERR_INVALID, "max_size must exceed window");
-    if (p->seg_bytes % cdc::STAGE) return fail(CDC_ERR_INVALID, "seg_bytes must be a multiple of 2048");
+    if (p->seg_bytes % 16) return fail(CDC_ERR_INVALID, "seg_bytes must be a multiple of 16");
     if (p->seg_bytes && p->seg_bytes >= (1ull << 31)) return fail(CDC_ERR_INVALID, "seg_bytes too large");
     if (p->halo_bytes >= (1ull << 31)) return fail(CDC_ERR_INVALID, "halo_bytes too large");
     return CDC_OK;
@@ -1063,8 +1114,9 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     uint64_t S = p->seg_bytes;
     if (!S) {
         const uint64_t target = (uint64_t)num_sms() * SEGS_PER_SM;
-        S = round_up(total_len / target + 1, cdc::STAGE);
-        const uint64_t lo = std::max<uint64_t>(64 << 10, round_up(4 * p->max_size, cdc::STAGE));
+        // floor(len / target): floor(len / S) = target segments of ~equal length
+        S = total_len / target;
+        const uint64_t lo = std::max<uint64_t>(64 << 10, round_up(4 * p->max_size, 128));
         if (S < lo) S = lo;
         if (S > (256ull << 20)) S = 256ull << 20;
     }

@@ -51,3 +51,10 @@ for s_ in np.argsort([-walk[sm == k].max() if (sm == k).any() else 0 for k in ra
 print("corr(walk, halo) %.2f corr(walk, g) %.2f" % (np.corrcoef(walk, halo)[0, 1], np.corrcoef(walk, np.arange(G))[0, 1]))
 slow = np.argsort(-walk)[:10]
 print("slowest segs", slow.tolist(), walk[slow].round(1).tolist(), "halo", halo[slow].tolist(), "sm", sm[slow].tolist())
+gs = int(np.argmax(start + walk))
+we = start + walk
+print("slowest walker g*=%d walk_end %.1f done %.1f" % (gs, we[gs], done[gs]))
+late = np.argsort(-done)[:8]
+print("latest done:", [(int(g), round(float(done[g]), 1), round(float(we[g]), 1)) for g in late])
+print("done - max(walk_end of predecessors..self): p50 %.2f p99 %.2f max %.2f" % tuple(
+    np.percentile(done - np.maximum.accumulate(we), [50, 99, 100])))
