@@ -17,6 +17,9 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared",
 ]
+# -DCDC_TAIL_LAUNCH with -rdc=true and LIBS = ["-lcudadevrt"] builds the variant whose
+# k_speculate tail-launches the fix-up (slower on B200 as measured; see cdc_kernels.cu)
+LIBS: list[str] = []
 
 
 def nvcc() -> str:
@@ -37,7 +40,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     """Compile SOURCES into `out` (default: the in-tree LIB); `defines` are extra -D flags (tuning variants)."""
     out = out or LIB
     if force or out != LIB or stale():
-        cmd = [nvcc(), *NVCC_FLAGS, *(f"-D{d}" for d in (defines or [])), "-o", out + ".tmp", *SOURCES]
+        cmd = [nvcc(), *NVCC_FLAGS, *(f"-D{d}" for d in (defines or [])), "-o", out + ".tmp", *SOURCES, *LIBS]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)

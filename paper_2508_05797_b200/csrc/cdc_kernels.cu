@@ -404,20 +404,52 @@ __device__ int64_t lookback(const Work &W, uint64_t g, uint32_t &sb_prev) {
 }
 
 template <int ALGO>
+__global__ void __launch_bounds__(1024) k_resolve(Geometry G, Work W, uint64_t *d_count, uint64_t *file_out);
+__global__ void k_write(Geometry G, Work W, const uint64_t *file_out, uint64_t *bounds, uint64_t cap);
+
+template <int ALGO>
+__device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
+                                  uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused);
+
+// K1.  One warp per segment (CTAs take segment groups in ticket order).  The
+// last warp to finish tail-launches the k_resolve/k_write fix-up (device-side
+// launch, CUDA dynamic parallelism) when some segment was not normal; in the
+// common case the whole call is this kernel (plus the list-reset memset).
+template <int ALGO>
 __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate(Geometry G, Work W, uint64_t *bounds,
-                                                                  uint64_t cap, uint64_t *d_count, int fused) {
+                                                                  uint64_t cap, uint64_t *d_count, int fused,
+                                                                  int tail_fixup) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_ticket;
     const int warp = threadIdx.x >> 5;
-    const int lane = lane_id();
-    // CTAs take segment groups in launch order (a ticket), so every segment a
-    // look-back waits for belongs to a CTA that is already running
     if (threadIdx.x == 0) s_ticket = atomicAdd(W.ctrl, 1u) + 1u;  // counter starts at ~0
     __syncthreads();
     const uint64_t g = (uint64_t)s_ticket * SPEC_WARPS + warp;
     const uint64_t nsegs = total_segs(G, W);
     if (g >= nsegs) return;
-    uint8_t *wbase = align_smem(smem) + warp * RING_SMEM;
+    speculate_segment<ALGO>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused);
+    if (tail_fixup && lane_id() == 0) {
+        __threadfence();
+        const uint32_t old = atomicAdd(W.ctrl + 2, 1u);  // starts at ~0: old + 2 warps are done
+        if (old + 2u == (uint32_t)nsegs) {
+            __threadfence();
+            if (atomicOr(W.ctrl + 1, 0u) == 0u) {  // the fused fast path failed somewhere
+#ifdef CDC_TAIL_LAUNCH
+                k_resolve<ALGO><<<1, RESOLVE_THREADS, RING_SMEM + 128, cudaStreamTailLaunch>>>(G, W, d_count,
+                                                                                                 W.file_out);
+                const uint64_t wthreads = nsegs * 32;
+                k_write<<<(unsigned)((wthreads + 255) / 256), 256, 0, cudaStreamTailLaunch>>>(G, W, W.file_out,
+                                                                                            bounds, cap);
+#endif
+            }
+        }
+    }
+}
+
+template <int ALGO>
+__device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
+                                  uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused) {
+    const int lane = lane_id();
     WarpRing R{wbase, reinterpret_cast<uint64_t *>(wbase + RING_BYTES)};
 
     SpecEmit em;
@@ -1064,6 +1096,20 @@ bool sync_debug() {
         }                                                                      \
     } while (0)
 
+// CDC_TAIL_LAUNCH builds (-rdc=true -lcudadevrt) let k_speculate tail-launch the
+// fix-up kernels only when needed.  Measured on B200 the relocatable-device-code
+// build made k_speculate ~4 us slower than the two empty host launches cost, so
+// the default build launches k_resolve/k_write from the host (they exit at once
+// when the fused fast path succeeded).
+int tail_mode(bool batch) {
+#ifdef CDC_TAIL_LAUNCH
+    return batch ? 0 : 1;
+#else
+    (void)batch;
+    return 0;
+#endif
+}
+
 // CDC_FUSED=0 disables the fused look-back fast path (k_resolve/k_write always run)
 int fused_mode() {
     static int v = -1;
@@ -1207,7 +1253,8 @@ cdc::Work carve(const Plan &P, void *ws) {
 
 template <int ALGO>
 int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::Work &W, uint64_t *d_bounds,
-                    uint64_t cap, uint64_t *d_count, uint64_t *file_out, cudaStream_t st, bool batch) {
+                    uint64_t cap, uint64_t *d_count, uint64_t *file_out, cudaStream_t st, bool batch,
+                    uint64_t total_len) {
     static bool attr_set = false;
     const int spec_smem = cdc::SPEC_WARPS * cdc::RING_SMEM + 128;
     if (!attr_set) {
@@ -1240,19 +1287,30 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     const uint64_t blocks = (nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS;
     if (blocks > 0) {
         cdc::k_speculate<ALGO><<<(unsigned)blocks, cdc::SPEC_WARPS * 32, spec_smem, st>>>(G, W, d_bounds, cap,
-                                                                                          d_count, fused_mode());
+                                                                                          d_count, fused_mode(),
+                                                                                          tail_mode(batch));
         CDC_KCHECK("k_speculate", st);
         ++launches;
         pc.used[1] = true;
     }
     mark(2);
-    cdc::k_resolve<ALGO><<<1, cdc::RESOLVE_THREADS, cdc::RING_SMEM + 128, st>>>(G, W, d_count, file_out);
-    CDC_KCHECK("k_resolve", st);
-    ++launches;
-    pc.used[2] = true;
+    // single stream with segments: k_speculate's last warp tail-launches the
+    // fix-up only when needed; batches (per-file offsets) and empty streams
+    // always run k_resolve/k_write from the host
+#ifdef CDC_TAIL_LAUNCH
+    const bool tail = !batch && total_len > 0;
+#else
+    const bool tail = false;
+#endif
+    if (!tail) {
+        cdc::k_resolve<ALGO><<<1, cdc::RESOLVE_THREADS, cdc::RING_SMEM + 128, st>>>(G, W, d_count, file_out);
+        CDC_KCHECK("k_resolve", st);
+        ++launches;
+        pc.used[2] = true;
+    }
     mark(3);
     const uint64_t wthreads = nseg_ub * 32;
-    if (wthreads > 0) {
+    if (!tail && wthreads > 0) {
         cdc::k_write<<<(unsigned)((wthreads + 255) / 256), 256, 0, st>>>(G, W, file_out, d_bounds, cap);
         CDC_KCHECK("k_write", st);
         ++launches;
@@ -1289,9 +1347,9 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     uint64_t *file_out = batch ? d_bound_off : W.file_out;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (p->algo) {
-    case CDC_RAM: return launch_pipeline<cdc::ALGO_RAM>(p, P, G, W, d_bounds, cap, d_count, file_out, st, batch);
-    case CDC_AE_MAX: return launch_pipeline<cdc::ALGO_AE_MAX>(p, P, G, W, d_bounds, cap, d_count, file_out, st, batch);
-    default: return launch_pipeline<cdc::ALGO_AE_MIN>(p, P, G, W, d_bounds, cap, d_count, file_out, st, batch);
+    case CDC_RAM: return launch_pipeline<cdc::ALGO_RAM>(p, P, G, W, d_bounds, cap, d_count, file_out, st, batch, total_len);
+    case CDC_AE_MAX: return launch_pipeline<cdc::ALGO_AE_MAX>(p, P, G, W, d_bounds, cap, d_count, file_out, st, batch, total_len);
+    default: return launch_pipeline<cdc::ALGO_AE_MIN>(p, P, G, W, d_bounds, cap, d_count, file_out, st, batch, total_len);
     }
 }
 
