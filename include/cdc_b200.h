@@ -201,15 +201,16 @@ int cdc_last_launch_count(void);
  * cdc_chunk / cdc_chunk_batch record CUDA events on their stream around each
  * of their kernels.  cdc_profile_collect synchronises on those events and
  * writes, for the pipeline kernels in order {k_seg_prefix, k_speculate,
- * k_resolve, k_write}, the summed milliseconds ms_sum[4] and launch counts
- * launches[4] since the previous collect, and the number of calls; it then
- * forgets them.  Host-side bookkeeping per calling thread.
+ * k_fixup}, the summed milliseconds ms_sum[3] and launch counts launches[3]
+ * since the previous collect, and the number of calls; it then forgets them.
+ * Host-side bookkeeping per calling thread.  (The interval of a kernel runs
+ * from the event before its launch to the event after it.)
  */
 int cdc_profile_enable(int on);
 int cdc_profile_collect(double *ms_sum, uint64_t *launches, uint64_t *calls);
 
-/* Diagnostics: cdc_profile_query writes, for the 5 events of the last
- * profiled call (before each of the 4 kernels and after the last), 1 if the
+/* Diagnostics: cdc_profile_query writes, for the 4 events of the last
+ * profiled call (before each of the 3 kernels and after the last), 1 if the
  * GPU has reached it, 0 if not (-1: event unused). */
 int cdc_profile_query(int *done);
 

@@ -24,7 +24,7 @@ __all__ = [
 ]
 
 
-KERNELS = ["k_seg_prefix", "k_speculate", "k_resolve", "k_write"]
+KERNELS = ["k_seg_prefix", "k_speculate", "k_fixup"]
 
 
 def profile_enable(on: bool = True) -> None:
@@ -33,8 +33,8 @@ def profile_enable(on: bool = True) -> None:
 
 def profile_collect() -> dict:
     """{kernel: (summed ms, launches)} since the last collect (synchronises)."""
-    ms = (ctypes.c_double * 4)()
-    n = (ctypes.c_uint64 * 4)()
+    ms = (ctypes.c_double * len(KERNELS))()
+    n = (ctypes.c_uint64 * len(KERNELS))()
     calls = ctypes.c_uint64()
     check(lib.cdc_profile_collect(ms, n, ctypes.byref(calls)))
     out = {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KERNELS)}

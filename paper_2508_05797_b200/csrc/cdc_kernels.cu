@@ -10,12 +10,13 @@
 //                    in a later segment's published list (re-synchronisation: from a
 //                    common start on, two chains are identical), the stream ends, or
 //                    the halo exceeds its cap.
-//   K2 k_resolve     one CTA: re-checks undecided halos against the complete lists,
+//   K2 k_fixup       exits at once when K1's fused look-back already wrote the output;
+//                    otherwise its first CTA (resolve_block) re-checks undecided halos against the complete lists,
 //                    runs fix-up walkers for halos that never met a later chain,
 //                    resolves which segments the true chain passes through (from the
 //                    stream start, following sync points), and scans the per-segment
 //                    output counts.
-//   K3 k_write       one warp per segment: writes its part of the true chain as
+//                    and then every CTA (write_segment, one warp per segment) writes its part of the true chain as
 //                    exclusive chunk end offsets (uint64).
 #include <cuda_runtime.h>
 
@@ -404,15 +405,15 @@ __device__ int64_t lookback(const Work &W, uint64_t g, uint32_t &sb_prev) {
 }
 
 template <int ALGO>
-__global__ void __launch_bounds__(1024) k_resolve(Geometry G, Work W, uint64_t *d_count, uint64_t *file_out);
-__global__ void k_write(Geometry G, Work W, const uint64_t *file_out, uint64_t *bounds, uint64_t cap);
+__global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_count, uint64_t *file_out,
+                                                uint64_t *bounds, uint64_t cap);
 
 template <int ALGO>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
                                   uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused);
 
 // K1.  One warp per segment (CTAs take segment groups in ticket order).  The
-// last warp to finish tail-launches the k_resolve/k_write fix-up (device-side
+// last warp to finish tail-launches the k_fixup fix-up (device-side
 // launch, CUDA dynamic parallelism) when some segment was not normal; in the
 // common case the whole call is this kernel (plus the list-reset memset).
 template <int ALGO>
@@ -435,11 +436,8 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
             __threadfence();
             if (atomicOr(W.ctrl + 1, 0u) == 0u) {  // the fused fast path failed somewhere
 #ifdef CDC_TAIL_LAUNCH
-                k_resolve<ALGO><<<1, RESOLVE_THREADS, RING_SMEM + 128, cudaStreamTailLaunch>>>(G, W, d_count,
-                                                                                                 W.file_out);
-                const uint64_t wthreads = nsegs * 32;
-                k_write<<<(unsigned)((wthreads + 255) / 256), 256, 0, cudaStreamTailLaunch>>>(G, W, W.file_out,
-                                                                                            bounds, cap);
+                k_fixup<ALGO><<<(unsigned)((nsegs + 31) / 32), RESOLVE_THREADS, RING_SMEM + 128,
+                                cudaStreamTailLaunch>>>(G, W, d_count, W.file_out, bounds, cap);
 #endif
             }
         }
@@ -482,7 +480,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     }
 
     // ---- common case, fused resolve + write: the chain met the next segment's
-    //      chain (or ended the file); anything else defers to k_resolve/k_write
+    //      chain (or ended the file); anything else defers to k_fixup
     const int fused_dbg = fused;  // debugging knob: 2 = skip the writes, 3 = skip the look-back
     fused = fused && nsegs <= LB_MAX_SEGS;
     const bool normal = fused && (em.sj == SJ_LAST || em.sj == (int32_t)(g + 1));
@@ -649,8 +647,7 @@ __device__ void recheck_halo(const Geometry &G, Work &W, uint64_t g) {
 // counts and their exclusive scan.  Exceptional segments (a sync target other
 // than the next segment, or an undecided halo) take the serial path.
 template <int ALGO>
-__global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W, uint64_t *d_count,
-                                                             uint64_t *file_out) {
+__device__ void resolve_block(const Geometry &G, Work &W, uint64_t *d_count, uint64_t *file_out) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t scratch[64];
     __shared__ uint64_t s_carry;
@@ -834,11 +831,9 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_resolve(Geometry G, Work W,
 }
 
 // ------------------------------------------------------------------ K3 write
-__global__ void k_write(Geometry G, Work W, const uint64_t *file_out, uint64_t *bounds, uint64_t cap) {
-    const uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__device__ void write_segment(const Geometry &G, const Work &W, const uint64_t *file_out, uint64_t *bounds,
+                              uint64_t cap, uint64_t g) {
     const int lane = lane_id();
-    const uint64_t nsegs = total_segs(G, W);
-    if (g >= nsegs || W.ctrl[1] != 0u) return;  // nothing to do when the fused fast path succeeded
     SegInfo I = seg_info(G, W, g);
     const uint64_t fo = file_out[I.f];
     if (g == I.first && lane == 0 && I.Lf > 0) {
@@ -860,6 +855,36 @@ __global__ void k_write(Geometry G, Work W, const uint64_t *file_out, uint64_t *
         if (q == fo) continue;  // the stream's first start (0) is not a boundary
         if (q - 1 < cap) bounds[q - 1] = v;
     }
+}
+
+// K2 (fix-up, one launch): when k_speculate's fused fast path succeeded this
+// exits at once (a batch still needs its per-file offsets, computed by the
+// first CTA).  Otherwise the CTA that draws ticket 0 resolves the true chain
+// (resolve_block: one CTA of 1024 threads) and releases a flag; every CTA then
+// writes the boundaries of its 32 segments (one warp each).  Tickets make the
+// waiting safe: the resolver is the first CTA to run.
+template <int ALGO>
+__global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_count, uint64_t *file_out,
+                                                uint64_t *bounds, uint64_t cap) {
+    __shared__ uint32_t s_role;
+    const uint64_t nsegs = total_segs(G, W);
+    const bool fast = nsegs > 0 && W.ctrl[1] != 0u;
+    if (fast && G.file_off == nullptr) return;
+    if (threadIdx.x == 0) s_role = atomicAdd(W.ctrl + 3, 1u) + 1u;  // counter starts at ~0
+    __syncthreads();
+    const uint32_t role = s_role;
+    if (role == 0) {
+        resolve_block<ALGO>(G, W, d_count, file_out);
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_u64(reinterpret_cast<unsigned long long *>(W.ctrl + 4), 1ull);
+    }
+    if (fast) return;
+    if (threadIdx.x == 0) {
+        while (ld_acquire_u64(reinterpret_cast<const unsigned long long *>(W.ctrl + 4)) != 1ull) __nanosleep(256);
+    }
+    __syncthreads();
+    const uint64_t g = (uint64_t)role * 32 + (threadIdx.x >> 5);
+    if (g < nsegs) write_segment(G, W, file_out, bounds, cap, g);
 }
 
 // ------------------------------------------------------------------ K0 batch segment table
@@ -1044,7 +1069,7 @@ thread_local int g_launches = 0;
 
 // Optional per-kernel timing (cdc_profile_*): CUDA events recorded on the
 // launching stream around each pipeline kernel of cdc_chunk / cdc_chunk_batch.
-constexpr int PROF_KERNELS = 4;  // k_seg_prefix, k_speculate, k_resolve, k_write
+constexpr int PROF_KERNELS = 3;  // k_seg_prefix, k_speculate, k_fixup
 struct ProfCall {
     cudaEvent_t ev[PROF_KERNELS + 1];
     bool used[PROF_KERNELS];
@@ -1099,7 +1124,7 @@ bool sync_debug() {
 // CDC_TAIL_LAUNCH builds (-rdc=true -lcudadevrt) let k_speculate tail-launch the
 // fix-up kernels only when needed.  Measured on B200 the relocatable-device-code
 // build made k_speculate ~4 us slower than the two empty host launches cost, so
-// the default build launches k_resolve/k_write from the host (they exit at once
+// the default build launches k_fixup from the host (it exits at once
 // when the fused fast path succeeded).
 int tail_mode(bool batch) {
 #ifdef CDC_TAIL_LAUNCH
@@ -1110,7 +1135,7 @@ int tail_mode(bool batch) {
 #endif
 }
 
-// CDC_FUSED=0 disables the fused look-back fast path (k_resolve/k_write always run)
+// CDC_FUSED=0 disables the fused look-back fast path (k_fixup always resolves)
 int fused_mode() {
     static int v = -1;
     if (v < 0) {
@@ -1259,7 +1284,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     const int spec_smem = cdc::SPEC_WARPS * cdc::RING_SMEM + 128;
     if (!attr_set) {
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, spec_smem));
-        CDC_CUDA(cudaFuncSetAttribute(cdc::k_resolve<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_fixup<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       cdc::RING_SMEM + 128));
         attr_set = true;
     }
@@ -1296,27 +1321,21 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     mark(2);
     // single stream with segments: k_speculate's last warp tail-launches the
     // fix-up only when needed; batches (per-file offsets) and empty streams
-    // always run k_resolve/k_write from the host
+    // always run k_fixup from the host
 #ifdef CDC_TAIL_LAUNCH
     const bool tail = !batch && total_len > 0;
 #else
     const bool tail = false;
 #endif
     if (!tail) {
-        cdc::k_resolve<ALGO><<<1, cdc::RESOLVE_THREADS, cdc::RING_SMEM + 128, st>>>(G, W, d_count, file_out);
-        CDC_KCHECK("k_resolve", st);
+        const uint64_t fblocks = (nseg_ub + 31) / 32;
+        cdc::k_fixup<ALGO><<<(unsigned)(fblocks ? fblocks : 1), cdc::RESOLVE_THREADS, cdc::RING_SMEM + 128, st>>>(
+            G, W, d_count, file_out, d_bounds, cap);
+        CDC_KCHECK("k_fixup", st);
         ++launches;
         pc.used[2] = true;
     }
     mark(3);
-    const uint64_t wthreads = nseg_ub * 32;
-    if (!tail && wthreads > 0) {
-        cdc::k_write<<<(unsigned)((wthreads + 255) / 256), 256, 0, st>>>(G, W, file_out, d_bounds, cap);
-        CDC_KCHECK("k_write", st);
-        ++launches;
-        pc.used[3] = true;
-    }
-    mark(4);
     if (g_prof_on) g_prof_calls.push_back(pc);
     g_launches = launches;
     CDC_CUDA(cudaGetLastError());
