@@ -55,16 +55,19 @@ struct Work {
     uint32_t *sa, *sb;           // halo entries before the sync point; its index in list(sj)
     uint32_t *entry, *tail, *wcnt, *jump_entry;
     uint64_t *woff;              // walker entries offset into pool
+    uint32_t *ocnt;              // serial fix-up walker entries (pool B) per segment
+    uint64_t *ooff;              // their offset into pool B
+    uint64_t *poolb;             // serial fix-up walker starts (file relative), sized for the whole stream
     uint8_t *skipped;
     uint64_t *seg_out;           // G+1 exclusive scan of output counts
     uint32_t *exc;               // compacted exceptional segments
     uint32_t *ranges;            // skip ranges (pairs)
-    uint64_t *pool;              // walker-produced starts (file relative)
+    uint32_t *pool;              // fix-up walker starts: segment g's slice [g cap_halo, (g+1) cap_halo), relative to seg_end
     uint64_t *seg_first;         // nfiles+1 (batch)
     uint32_t *seg_file;          // G: file of each segment (batch)
     uint64_t *file_out;          // nfiles+1 (single stream: internal)
     uint32_t *misc;              // [0] G, [1] n_exc, [2] n_ranges, [3] overflow flags
-    uint64_t cap_list, cap_halo, pool_cap, max_segs, exc_cap;
+    uint64_t cap_list, cap_halo, pool_cap, max_segs, exc_cap, poolb_cap;
 };
 
 enum : int32_t { SJ_UNSYNCED = -1, SJ_STREAM_END = -2, SJ_LAST = -3 };
@@ -436,7 +439,7 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
             __threadfence();
             if (atomicOr(W.ctrl + 1, 0u) == 0u) {  // the fused fast path failed somewhere
 #ifdef CDC_TAIL_LAUNCH
-                k_fixup<ALGO><<<(unsigned)((nsegs + 31) / 32), RESOLVE_THREADS, RING_SMEM + 128,
+                k_fixup<ALGO><<<(unsigned)((nsegs + 31) / 32), RESOLVE_THREADS, FIX_SMEM,
                                 cudaStreamTailLaunch>>>(G, W, d_count, W.file_out, bounds, cap);
 #endif
             }
@@ -550,7 +553,10 @@ struct WalkEmit {
     const Geometry *G;
     const Work *W;
     SegInfo I;        // segment whose chain is being continued
-    uint64_t base;    // first pool slot of this walker
+    uint32_t *p32;    // slice of pool (entries relative to seg_end) ...
+    uint64_t *p64;    // ... or pool B (file-relative entries)
+    uint64_t base;    // first slot of this walker
+    uint64_t lim;     // end of its slots
     uint64_t n;       // entries written
     int32_t sj;
     uint32_t sb;
@@ -573,11 +579,14 @@ struct WalkEmit {
             sb = idx;
             return true;
         }
-        if (base + n >= W->pool_cap) {
+        if (base + n >= lim) {
             overflow = true;
             return true;
         }
-        if (lane_id() == 0) W->pool[base + n] = (uint64_t)e;
+        if (lane_id() == 0) {
+            if (p32) p32[base + n] = (uint32_t)(e - I.seg_end);
+            else p64[base + n] = (uint64_t)e;
+        }
         ++n;
         return false;
     }
@@ -612,32 +621,63 @@ __device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t &t
     return warp_prefix + x - v;
 }
 
-constexpr int RPT = 8;  // k_resolve: consecutive segments per thread in the count scan
+constexpr int RPT = 8;           // resolve_block: consecutive segments per thread in the count scan
+constexpr int FIX_WALKERS = 8;   // resolve_block: parallel fix-up walkers (one smem ring each)
+constexpr int FIX_STAGE = (FIX_WALKERS - 2) * RING_SMEM / 12;  // exceptional segments staged per round (+ one ring)
+constexpr int FIX_SMEM = FIX_WALKERS * RING_SMEM + 128;  // k_fixup dynamic shared memory
 
-// Re-check the halo of segment g (left undecided by K1) against the complete lists.
+// Where the true chain goes after exceptional segment g (when g is on it):
+// 0 = into the next segment (no jump), TGT_WALK = not known yet (a fix-up walk
+// must continue the chain), else the first segment after the jump.
+constexpr uint32_t TGT_WALK = 0xFFFFFFFFu;
+__device__ __forceinline__ uint32_t exc_target(const Geometry &G, const Work &W, uint64_t g) {
+    const int32_t sj = W.sj[g];
+    if (sj == SJ_UNSYNCED) return TGT_WALK;
+    if (sj == SJ_STREAM_END) {
+        uint64_t fa, fb;
+        seg_first_of(G, W, file_of_seg(G, W, g), fa, fb);
+        return (uint32_t)fb;  // past the file's last segment
+    }
+    if (sj == SJ_LAST || sj == (int32_t)(g + 1)) return 0;
+    return (uint32_t)sj;
+}
+
+// Re-check the halo of segment g (left undecided by K1) against the complete
+// lists: 32 halo entries at a time, each lane binary-searching the list of the
+// segment its entry lies in; the first entry found is the sync point.
 __device__ void recheck_halo(const Geometry &G, Work &W, uint64_t g) {
     const int lane = lane_id();
     SegInfo I = seg_info(G, W, g);
     const uint32_t hc = W.hcnt[g];
-    int64_t cur_j = -1;
-    uint32_t cursor = 0;
-    for (uint32_t i = 0; i < hc; ++i) {
-        const int64_t e = I.seg_end + (int64_t)W.halo[g * W.cap_halo + i];
-        int64_t pj;
-        const int64_t j = seg_of_pos(I, e, G.S, pj);
-        if (j != cur_j) {
-            cur_j = j;
-            cursor = 0;
-        }
+    for (uint32_t i0 = 0; i0 < hc; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        bool found = false;
+        int64_t j = 0;
         uint32_t idx = 0;
-        if (list_lookup(W.list + (uint64_t)j * W.cap_list, W.cap_list, W.pub + j, (uint32_t)(e - pj), cursor,
-                        idx) == 1) {
-            if (lane == 0) {
+        if (i < hc) {
+            const int64_t e = I.seg_end + (int64_t)W.halo[g * W.cap_halo + i];
+            int64_t pj;
+            j = seg_of_pos(I, e, G.S, pj);
+            const uint32_t r = (uint32_t)(e - pj);
+            const uint32_t *lst = W.list + (uint64_t)j * W.cap_list;
+            uint32_t lo = 0, hi = W.cnt[j];
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (lst[mid] < r) lo = mid + 1;
+                else hi = mid;
+            }
+            found = lo < W.cnt[j] && lst[lo] == r;
+            idx = lo;
+        }
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, found);
+        if (bal) {
+            const int L = __ffs(bal) - 1;
+            if (lane == L) {
                 W.sj[g] = (int32_t)j;
                 W.sa[g] = i;
                 W.sb[g] = idx;
             }
-            break;
+            return;
         }
     }
 }
@@ -691,7 +731,13 @@ __device__ void resolve_block(const Geometry &G, Work &W, uint64_t *d_count, uin
         for (uint64_t g = tid; g < nsegs; g += blockDim.x) {
             W.skipped[g] = 0;
             W.wcnt[g] = 0;
+            W.ocnt[g] = 0;
             W.jump_entry[g] = 0;
+        }
+        if (tid == 0) {
+            W.misc[2] = 0;  // ranges
+            W.misc[3] = 0;  // overflow
+            W.misc[5] = 0;  // reach
         }
         __syncthreads();
         // 2. compact the exceptional segments in order
@@ -713,61 +759,119 @@ __device__ void resolve_block(const Geometry &G, Work &W, uint64_t *d_count, uin
         }
         const uint64_t n_exc = s_carry;
 
-        // 3. serial resolution of the exceptional segments on the true chain (warp 0);
-        //    unsynced halos are continued by a walker until they meet a later chain
-        if (warp == 0) {
-            uint8_t *rb = align_smem(smem);
+        // 3a. unsynced halos, continued in parallel (FIX_WALKERS warps, one ring each)
+        //     from their last recorded start until they meet a later segment's chain;
+        //     walker g writes into its own pool slice and, should the slice fill up,
+        //     leaves the segment unsynced for the serial pass (3b)
+        if (warp < FIX_WALKERS) {
+            uint8_t *rb = align_smem(smem) + warp * RING_SMEM;
             WarpRing R{rb, reinterpret_cast<uint64_t *>(rb + RING_BYTES)};
-            uint64_t reach = 0, nranges = 0, pool_used = 0;
-            bool overflow = n_exc > W.exc_cap;
-            for (uint64_t x = 0; x < n_exc && x < W.exc_cap; ++x) {
+            for (uint64_t x = warp; x < n_exc && x < W.exc_cap; x += FIX_WALKERS) {
                 const uint64_t g = W.exc[x];
-                if (g < reach) continue;  // skipped by an earlier jump: not on the true chain
+                if (W.sj[g] != SJ_UNSYNCED) continue;
                 SegInfo I = seg_info(G, W, g);
-                int32_t sj = W.sj[g];
-                if (sj == SJ_UNSYNCED) {
-                    WalkEmit em;
-                    em.G = &G;
-                    em.W = &W;
-                    em.I = I;
-                    em.base = pool_used;
-                    em.n = 0;
-                    em.sj = SJ_STREAM_END;
-                    em.sb = 0;
-                    em.cur_j = -1;
-                    em.cursor = 0;
-                    em.overflow = false;
-                    // resume the chain from its last recorded start
-                    const uint32_t hc = W.hcnt[g];
-                    const int64_t last = hc ? I.seg_end + (int64_t)W.halo[g * W.cap_halo + hc - 1]
-                                            : I.p + (int64_t)W.list[g * W.cap_list + W.cnt[g] - 1];
-                    run_chain<ALGO>(R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
-                                    stream_policy(), em);
-                    overflow |= em.overflow;
-                    sj = em.sj;
-                    if (lane == 0) {
-                        W.sj[g] = sj;
-                        W.sa[g] = W.hcnt[g];
-                        W.sb[g] = em.sb;
-                        W.wcnt[g] = (uint32_t)em.n;
-                        W.woff[g] = em.base;
-                    }
-                    pool_used += em.n;
-                    if (sj == (int32_t)(g + 1)) continue;  // met the next segment's chain: no skip
-                }
-                const uint64_t target = (sj == SJ_STREAM_END) ? I.last + 1 : (uint64_t)sj;
+                WalkEmit em;
+                em.G = &G;
+                em.W = &W;
+                em.I = I;
+                em.p32 = W.pool;
+                em.p64 = nullptr;
+                em.base = g * W.cap_halo;
+                em.lim = em.base + W.cap_halo;
+                em.n = 0;
+                em.sj = SJ_STREAM_END;
+                em.sb = 0;
+                em.cur_j = -1;
+                em.cursor = 0;
+                em.overflow = false;
+                const uint32_t hc = W.hcnt[g];
+                const int64_t last = hc ? I.seg_end + (int64_t)W.halo[g * W.cap_halo + hc - 1]
+                                        : I.p + (int64_t)W.list[g * W.cap_list + W.cnt[g] - 1];
+                run_chain<ALGO>(R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
+                                stream_policy(), em);
                 if (lane == 0) {
-                    W.ranges[2 * nranges] = (uint32_t)(g + 1);
-                    W.ranges[2 * nranges + 1] = (uint32_t)target;
-                    if (sj >= 0) W.jump_entry[target] = W.sb[g];
+                    W.sj[g] = em.overflow ? SJ_UNSYNCED : em.sj;
+                    W.sa[g] = hc;
+                    W.sb[g] = em.sb;
+                    W.wcnt[g] = (uint32_t)em.n;
+                    W.woff[g] = em.base;
                 }
-                ++nranges;
-                reach = target;
             }
-            if (lane == 0) {
-                W.misc[2] = (uint32_t)nranges;
-                W.misc[3] = overflow ? 1u : 0u;
+        }
+        __syncthreads();
+
+        // 3b. the true chain through the exceptional segments, in order (warp 0), from
+        //     jump targets staged in shared memory; a segment still unsynced (its
+        //     slice filled up) is continued here, serially, into pool B
+        uint32_t *s_exc = reinterpret_cast<uint32_t *>(align_smem(smem));
+        uint32_t *s_tgt = s_exc + FIX_STAGE;
+        uint32_t *s_sb = s_tgt + FIX_STAGE;  // sb of the segment, or ~0 when it has no sync target
+        uint64_t reach = 0, nrng = 0, poolb_used = 0;
+        bool overflow = false;
+        for (uint64_t x0 = 0; x0 < n_exc && x0 < W.exc_cap; x0 += FIX_STAGE) {
+            const uint64_t m = (n_exc - x0 < FIX_STAGE ? n_exc - x0 : FIX_STAGE);
+            __syncthreads();
+            for (uint64_t i = tid; i < m; i += blockDim.x) {
+                const uint64_t g = W.exc[x0 + i];
+                s_exc[i] = (uint32_t)g;
+                s_tgt[i] = exc_target(G, W, g);
+                s_sb[i] = W.sj[g] >= 0 ? W.sb[g] : 0xFFFFFFFFu;
             }
+            __syncthreads();
+            if (warp == 0) {
+                for (uint64_t i = 0; i < m; ++i) {
+                    const uint64_t g = s_exc[i];
+                    if (g < reach) continue;  // skipped by an earlier jump: not on the true chain
+                    uint32_t target = s_tgt[i];
+                    if (target == TGT_WALK) {  // continue the chain from the end of its slice
+                        SegInfo I = seg_info(G, W, g);
+                        uint8_t *rb = align_smem(align_smem(smem) + 3 * FIX_STAGE * 4);  // after the staged arrays
+                        WarpRing R{rb, reinterpret_cast<uint64_t *>(rb + RING_BYTES)};
+                        WalkEmit em;
+                        em.G = &G;
+                        em.W = &W;
+                        em.I = I;
+                        em.p32 = nullptr;
+                        em.p64 = W.poolb;
+                        em.base = poolb_used;
+                        em.lim = W.poolb_cap;
+                        em.n = 0;
+                        em.sj = SJ_STREAM_END;
+                        em.sb = 0;
+                        em.cur_j = -1;
+                        em.cursor = 0;
+                        em.overflow = false;
+                        const uint32_t wc = W.wcnt[g];
+                        const int64_t last = I.seg_end + (int64_t)W.pool[W.woff[g] + wc - 1];
+                        run_chain<ALGO>(R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
+                                        stream_policy(), em);
+                        overflow |= em.overflow;
+                        if (lane == 0) {
+                            W.sj[g] = em.sj;
+                            W.sb[g] = em.sb;
+                            W.ocnt[g] = (uint32_t)em.n;
+                            W.ooff[g] = em.base;
+                        }
+                        poolb_used += em.n;
+                        __syncwarp();
+                        target = exc_target(G, W, g);
+                        if (lane == 0) s_sb[i] = W.sj[g] >= 0 ? W.sb[g] : 0xFFFFFFFFu;
+                        __syncwarp();
+                    }
+                    if (target == 0) continue;  // met the next segment's chain: no skip
+                    if (lane == 0) {
+                        W.ranges[2 * nrng] = (uint32_t)(g + 1);
+                        W.ranges[2 * nrng + 1] = target;
+                        if (s_sb[i] != 0xFFFFFFFFu) W.jump_entry[target] = s_sb[i];
+                    }
+                    ++nrng;
+                    reach = target;
+                }
+            }
+        }
+        if (warp == 0 && lane == 0) {
+            W.misc[2] = (uint32_t)nrng;
+            W.misc[3] = (overflow || n_exc > W.exc_cap) ? 1u : 0u;
         }
         __syncthreads();
 
@@ -800,7 +904,7 @@ __device__ void resolve_block(const Geometry &G, Work &W, uint64_t *d_count, uin
                 const uint32_t tail = sj == SJ_STREAM_END ? W.hcnt[g] : (sj >= 0 ? W.sa[g] : 0u);
                 W.entry[g] = e;
                 W.tail[g] = tail;
-                n = (W.cnt[g] - e) + tail + (exc ? W.wcnt[g] : 0u);
+                n = (W.cnt[g] - e) + tail + (exc ? W.wcnt[g] + W.ocnt[g] : 0u);
             }
             nloc[i] = n;
             tsum += n;
@@ -843,14 +947,16 @@ __device__ void write_segment(const Geometry &G, const Work &W, const uint64_t *
     const bool exc = W.misc[4] != 0;
     if (exc && W.skipped[g]) return;
     const uint32_t e = W.entry[g], cnt = W.cnt[g], tail = W.tail[g], wc = exc ? W.wcnt[g] : 0u;
-    const uint64_t A = cnt - e, n = A + tail + wc, base = W.seg_out[g];
+    const uint32_t oc = exc ? W.ocnt[g] : 0u;
+    const uint64_t A = cnt - e, n = A + tail + wc + oc, base = W.seg_out[g];
     const uint32_t *lst = W.list + g * W.cap_list;
     const uint32_t *hl = W.halo + g * W.cap_halo;
     for (uint64_t i = lane; i < n; i += 32) {
         uint64_t v;
         if (i < A) v = (uint64_t)I.p + lst[e + i];
         else if (i < A + tail) v = (uint64_t)I.seg_end + hl[i - A];
-        else v = W.pool[W.woff[g] + (i - A - tail)];
+        else if (i < A + tail + wc) v = (uint64_t)I.seg_end + W.pool[W.woff[g] + (i - A - tail)];
+        else v = W.poolb[W.ooff[g] + (i - A - tail - wc)];
         const uint64_t q = base + i;
         if (q == fo) continue;  // the stream's first start (0) is not a boundary
         if (q - 1 < cap) bounds[q - 1] = v;
@@ -1168,9 +1274,9 @@ int num_sms() {
 }
 
 struct Plan {
-    uint64_t S, Hmax, max_segs, cap_list, cap_halo, pool_cap, exc_cap, nfiles;
+    uint64_t S, Hmax, max_segs, cap_list, cap_halo, pool_cap, exc_cap, nfiles, poolb_cap;
     size_t bytes, reset_bytes;
-    size_t off[24];
+    size_t off[32];
 };
 
 uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
@@ -1194,8 +1300,11 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     // halo cap: chains started at arbitrary offsets meet within a few chunks on
     // skewed data but only after ~(w/362)^2 chunks on uniform bytes (the phase
     // difference of two chains random-walks): 1024 windows, <= 64 MiB
+    // (batches of many small files keep 64 windows: their segments are mostly whole
+    // files, and the fix-up walkers continue any halo that gives up)
+    const uint64_t hw = nfiles > 1 ? 64ull : 1024ull;
     uint64_t H = p->halo_bytes ? p->halo_bytes
-                               : std::min<uint64_t>(std::max<uint64_t>(2 * S, 1024ull * (p->window + 1)), 64ull << 20);
+                               : std::min<uint64_t>(std::max<uint64_t>(2 * S, hw * (p->window + 1)), 64ull << 20);
     if (H >= (1ull << 31)) H = (1ull << 31) - 1;
     P.S = S;
     P.Hmax = H;
@@ -1203,7 +1312,8 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     P.max_segs = (nfiles <= 1) ? (max_len + S - 1) / S + 1 : total_len / S + nfiles + 1;
     P.cap_list = 2 * S / (p->window + 1) + 2;  // the last segment of a file holds up to 2S bytes
     P.cap_halo = H / (p->window + 1) + 3;
-    P.pool_cap = total_len / (p->window + 1) + 2;
+    P.pool_cap = P.max_segs * P.cap_halo;  // one slice of cap_halo entries per segment
+    P.poolb_cap = total_len / (p->window + 1) + 2;
     P.exc_cap = P.max_segs;
     const uint64_t G = P.max_segs;
     size_t sz[] = {
@@ -1224,14 +1334,17 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
         (G + 1) * 8,         // 14 seg_out
         G * 4,               // 15 exc
         G * 8,               // 16 ranges
-        P.pool_cap * 8,      // 17 pool
+        P.pool_cap * 4,      // 17 pool
         (nfiles + 1) * 8,    // 18 seg_first
         (nfiles + 1) * 8,    // 19 file_out
         64,                  // 20 misc
         G * 4,               // 21 seg_file
+        G * 4,               // 22 ocnt
+        G * 8,               // 23 ooff
+        P.poolb_cap * 8,     // 24 poolb
     };
     size_t o = 0;
-    for (int i = 0; i < 22; ++i) {
+    for (int i = 0; i < 25; ++i) {
         P.off[i] = o;
         o += round_up(sz[i], 256);
     }
@@ -1263,11 +1376,15 @@ cdc::Work carve(const Plan &P, void *ws) {
     W.seg_out = (uint64_t *)(b + P.off[14]);
     W.exc = (uint32_t *)(b + P.off[15]);
     W.ranges = (uint32_t *)(b + P.off[16]);
-    W.pool = (uint64_t *)(b + P.off[17]);
+    W.pool = (uint32_t *)(b + P.off[17]);
     W.seg_first = (uint64_t *)(b + P.off[18]);
     W.file_out = (uint64_t *)(b + P.off[19]);
     W.misc = (uint32_t *)(b + P.off[20]);
     W.seg_file = (uint32_t *)(b + P.off[21]);
+    W.ocnt = (uint32_t *)(b + P.off[22]);
+    W.ooff = (uint64_t *)(b + P.off[23]);
+    W.poolb = (uint64_t *)(b + P.off[24]);
+    W.poolb_cap = P.poolb_cap;
     W.cap_list = P.cap_list;
     W.cap_halo = P.cap_halo;
     W.pool_cap = P.pool_cap;
@@ -1285,7 +1402,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     if (!attr_set) {
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_fixup<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      cdc::RING_SMEM + 128));
+                                      cdc::FIX_SMEM));
         attr_set = true;
     }
     int launches = 0;
@@ -1329,7 +1446,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
 #endif
     if (!tail) {
         const uint64_t fblocks = (nseg_ub + 31) / 32;
-        cdc::k_fixup<ALGO><<<(unsigned)(fblocks ? fblocks : 1), cdc::RESOLVE_THREADS, cdc::RING_SMEM + 128, st>>>(
+        cdc::k_fixup<ALGO><<<(unsigned)(fblocks ? fblocks : 1), cdc::RESOLVE_THREADS, cdc::FIX_SMEM, st>>>(
             G, W, d_count, file_out, d_bounds, cap);
         CDC_KCHECK("k_fixup", st);
         ++launches;

@@ -24,9 +24,15 @@ def run(name, data_np, algo, avg, reps=10, seg=0):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    cdc.profile_enable(True)
+    cdc.chunk_async(t, p, b, c, ws)
+    torch.cuda.synchronize()
+    cdc.profile_enable(False)
+    pr = cdc.profile_collect()
     st = cdc.stats(p, ws, 1, n, n)
+    st["k_ms"] = {k: round(v[0], 3) for k, v in pr.items() if k != "calls" and v[1]}
     print("%-28s %-6s %5d  %8.3f ms  %8.1f GB/s  chunks %d  %s" % (name, algo, avg, ms, n / ms / 1e6, int(c.item()),
-          {k: st[k] for k in ("segments", "fast_path", "synced", "unsynced", "skipped_or_end", "halo_chunks")}),
+          {k: st[k] for k in ("segments", "fast_path", "synced", "unsynced", "skipped_or_end", "halo_chunks", "k_ms")}),
           flush=True)
 
 
