@@ -311,10 +311,10 @@ __device__ __forceinline__ uint32_t seg_sb(unsigned long long w) { return (uint3
 // ceil(G/1024) + 1 independent loads per lane.  Returns sum_{h<g} a_h.
 constexpr int LB_GROUP = 32;
 #ifndef CDC_SLEEP0
-#define CDC_SLEEP0 1024
+#define CDC_SLEEP0 256
 #endif
 #ifndef CDC_SLEEPMAX
-#define CDC_SLEEPMAX 4096
+#define CDC_SLEEPMAX 1024
 #endif
 // look-back waits sleep (exponential backoff) instead of polling hard: waiting
 // warps share their SM with walkers that are still running
@@ -322,23 +322,25 @@ constexpr uint32_t SLEEP0 = CDC_SLEEP0, SLEEPMAX = CDC_SLEEPMAX;
 constexpr uint64_t LB_MAX_SEGS = 32768;  // beyond this the k_resolve scan is used
 
 // all 32 lanes
-__device__ void publish_agg(Work &W, uint64_t g, uint64_t nsegs, int64_t a, uint32_t sb) {
-    const int lane = lane_id();
-    const uint64_t grp = g / LB_GROUP;
-    const uint64_t gsz = (grp + 1) * LB_GROUP <= nsegs ? LB_GROUP : nsegs - grp * LB_GROUP;
-    uint32_t old = 0;
-    if (lane == 0) {
-        st_release_u64(W.status + g, seg_word(sb, a));
-        asm volatile("atom.acq_rel.gpu.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(W.gcnt + grp) : "memory");
+// Group words: one 64-bit atomic accumulator per group of 32 segments holding
+// (arrivals << 48) + sum of (a + LB_BIAS) over the arrived segments.  The
+// memset leaves ~0, so the accumulated value is the word + 1.  A group is
+// complete when its arrival count equals its size; its sum is then
+// low48 - size * LB_BIAS.  (|a| < 2^24: a = cnt + tail - sb, each bounded by a
+// segment's list or halo capacity.)
+constexpr uint64_t LB_BIAS = 1ull << 24;
+constexpr uint64_t LB_LOW48 = (1ull << 48) - 1;
+
+// all 32 lanes
+__device__ void publish_agg(Work &W, uint64_t g, uint64_t, int64_t a, uint32_t sb) {
+    // Both words are self-contained (readers need nothing else these warps
+    // wrote), so relaxed accesses suffice: no fences on the critical path.
+    if (lane_id() == 0) {
+        asm volatile("st.relaxed.gpu.u64 [%0], %1;" ::"l"(W.status + g), "l"(seg_word(sb, a)) : "memory");
+        const unsigned long long add = (1ull << 48) + (unsigned long long)(a + (int64_t)LB_BIAS);
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(W.grp + g / LB_GROUP), "l"(add) : "memory");
     }
-    old = __shfl_sync(0xFFFFFFFFu, old, 0);
-    if (old + 1u == (uint32_t)gsz - 1u) {  // the counter starts at ~0: this is the group's last arrival
-        // one load per lane (acquire loads issued by one thread would serialise)
-        int64_t v = lane < (int)gsz ? seg_a(ld_acquire_u64(W.status + grp * LB_GROUP + lane)) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-        if (lane == 0) st_release_u64(W.grp + grp, st_word(ST_AGG, v));
-    }
+    __syncwarp();
 }
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
@@ -368,13 +370,13 @@ __device__ int64_t lookback(const Work &W, uint64_t g, uint32_t &sb_prev) {
             unsigned long long wd = 0;
             bool ok = true;
             if (k < grp) {
-                wd = ld_relaxed_u64(W.grp + k);
-                ok = (wd & ST_MASK) == ST_AGG;
+                wd = ld_relaxed_u64(W.grp + k) + 1ull;  // groups before g's are full (LB_GROUP members)
+                ok = (wd >> 48) == (unsigned long long)LB_GROUP;
             }
             const uint32_t bad = __ballot_sync(0xFFFFFFFFu, !ok);
             const uint32_t nvalid = (uint32_t)(grp - k0 < 32 ? grp - k0 : 32);
             const uint32_t ready = bad ? (uint32_t)(__ffs(bad) - 1) : nvalid;  // leading ready groups
-            if ((uint32_t)lane < ready) done += st_value(wd);
+            if ((uint32_t)lane < ready) done += (int64_t)(wd & LB_LOW48) - (int64_t)(LB_GROUP * LB_BIAS);
             k0 += ready;
             if (ready < nvalid) break;
         }
@@ -394,8 +396,6 @@ __device__ int64_t lookback(const Work &W, uint64_t g, uint32_t &sb_prev) {
             own_ok = __all_sync(0xFFFFFFFFu, ok);
         }
         if (k0 == grp && own_ok) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire what the observed releases published
-            __syncwarp();
             int64_t sum = done + own;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
@@ -1429,7 +1429,9 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     const uint64_t blocks = (nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS;
     if (blocks > 0) {
         cdc::k_speculate<ALGO><<<(unsigned)blocks, cdc::SPEC_WARPS * 32, spec_smem, st>>>(G, W, d_bounds, cap,
-                                                                                          d_count, fused_mode(),
+                                                                                          d_count,
+                                                                                          (P.cap_list + P.cap_halo < (1u << 23))
+                                                                                              ? fused_mode() : 0,
                                                                                           tail_mode(batch));
         CDC_KCHECK("k_speculate", st);
         ++launches;
