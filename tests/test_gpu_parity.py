@@ -238,3 +238,39 @@ def test_invalid_params(cdc):
         cdc.chunk(torch.zeros(10, dtype=torch.uint8, device="cuda"), cdc.params("ram", window=4, max_size=4))
     with pytest.raises(cdc.CdcError):
         cdc.chunk(torch.zeros(10, dtype=torch.uint8, device="cuda"), cdc.params("ram", window=0, max_size=4))
+
+
+@pytest.mark.parametrize("case", ["fast", "fixup"])
+def test_cuda_graph_capture(cdc, case):
+    """cdc_chunk captured into a CUDA graph (as bench.py times it): replays stay
+    exact whether the fused fast path holds or the fix-up kernel has to resolve."""
+    if case == "fast":
+        d = synth.zipf_bytes(16 << 20, 1.1, 41)
+        p = cdc.params("ae_max", avg_size=4096)
+    else:  # constant bytes never re-synchronise: every halo gives up, the fix-up runs
+        d = synth.constant((3 << 20) + 5, 0)
+        p = cdc.params("ram", window=600, max_size=4000, seg_bytes=16384, halo_bytes=8192)
+    exp = oracle.chunk(["ram", "ae_max", "ae_min"][p.algo], d, p.window, p.max_size)
+    t = _dev(d)
+    n = d.size
+    ws = torch.empty(cdc.workspace_size(p, 1, n, n), dtype=torch.uint8, device="cuda")
+    cap = cdc.max_boundaries(p, n)
+    b = torch.empty(cap, dtype=torch.int64, device="cuda")
+    c = torch.zeros(1, dtype=torch.int64, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        cdc.chunk_async(t, p, b, c, ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cdc.chunk_async(t, p, b, c, ws)
+    for _ in range(3):
+        b.fill_(-1)
+        c.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        got = b[:int(c.item())].cpu().numpy().astype(np.uint64)
+        assert got.size == exp.size and (got == exp).all()
+    if case == "fixup":
+        assert cdc.stats(p, ws, 1, n, n)["fast_path"] == 0
