@@ -36,6 +36,18 @@ WORKLOAD = "configs[1]: AE (AE-Max) avg 4 KiB, single 256 MiB stream of Zipf(s=1
 REF_SLICE = 32 << 20
 
 
+def load_traffic():
+    """DRAM traffic per k_speculate launch from the committed ncu --set full capture
+    (profiles/ncu_k_speculate_latest.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_k_speculate_latest.json")) as f:
+            t = json.load(f)
+        return float(t["traffic_bytes"]) / 1e9, "dram__bytes_read.sum + dram__bytes_write.sum per launch (GB), " \
+            "profiles/ncu_k_speculate_latest.json"
+    except Exception:
+        return None, None
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -304,6 +316,7 @@ def main():
     spec_ms, spec_n = prof["k_speculate"]
     spec_avg_ms = spec_ms / max(1, spec_n)
     peak, peak_src = load_peaks()
+    traffic_gb, traffic_src = load_traffic()
     achieved = STREAM / (spec_avg_ms / 1e3) / 1e9
     share = {k: round(prof[k][0] / max(1e-9, sum(prof[x][0] for x in cdc.KERNELS)), 4) for k in cdc.KERNELS}
 
@@ -322,7 +335,8 @@ def main():
                        "parallelism": f"dp{world}: one independent stream per rank, no data-path collective"},
             "roofline": {"bound": "hbm", "kernel": "k_speculate", "achieved": round(achieved, 1),
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4), "traffic": traffic_gb,
+                         "traffic_source": traffic_src, "algorithmic_gb_per_launch": round(STREAM / 1e9, 4),
                          "kernel_ms": round(spec_avg_ms, 4), "share_of_step": share},
             "gpu_launches": launches_per_step * args.steps,
             "path": path_stats,
