@@ -225,6 +225,15 @@ int cdc_profile_query(int *done);
  *       the stream end from a non-final segment, [7] total halo chunks.
  */
 /*
+ * Host-only: the speculation geometry a call with these arguments uses:
+ * out[0] = segment bytes S, out[1] = halo cap bytes, out[2] = segments of a
+ * single stream of max_len bytes (floor(max_len / S), at least 1; segment k
+ * starts at k * floor(max_len / n) rounded down to 4 KiB when that quotient is
+ * >= 64 KiB, else to 16 B).
+ */
+int cdc_plan_info(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, uint64_t *out);
+
+/*
  * Diagnostics: while d_buf (a device uint64 array of 4 x segments entries) is
  * set, k_speculate records per segment {globaltimer at start, at the end of the
  * walk, at the end of its fused write, SM id | halo chunks << 32}.  NULL turns

@@ -51,6 +51,7 @@ SIGNATURES = {
     "cdc_profile_enable": ([ctypes.c_int], ctypes.c_int),
     "cdc_profile_query": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "cdc_debug_timing": ([_vp], ctypes.c_int),
+    "cdc_plan_info": ([_P, _u64, _u64, _u64, ctypes.POINTER(_u64)], ctypes.c_int),
     "cdc_stats": ([_P, _u64, _u64, _u64, _vp, ctypes.POINTER(_u64), _vp], ctypes.c_int),
     "cdc_profile_collect": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
                             ctypes.c_int),

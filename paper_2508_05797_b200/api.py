@@ -20,7 +20,7 @@ __all__ = [
     "CdcError", "ALGOS", "params", "window_for_avg", "max_boundaries", "workspace_size",
     "chunk_async", "chunk", "chunk_batch", "chunk_host", "chain",
     "extreme_byte_search", "range_scan", "first_common", "last_launch_count", "abi_version",
-    "profile_enable", "profile_collect", "KERNELS", "stats",
+    "profile_enable", "profile_collect", "KERNELS", "stats", "plan_info", "segment_starts",
 ]
 
 
@@ -48,6 +48,23 @@ def stats(p: cdc_params, workspace: torch.Tensor, nfiles: int, total_len: int, m
     check(lib.cdc_stats(ctypes.byref(p), nfiles, total_len, max_len, workspace.data_ptr(), out, _stream_ptr(stream)))
     keys = ["segments", "seg_bytes", "halo_cap", "fast_path", "synced", "unsynced", "skipped_or_end", "halo_chunks"]
     return {k: int(out[i]) for i, k in enumerate(keys)}
+
+
+def plan_info(p: cdc_params, nfiles: int, total_len: int, max_len: int) -> dict:
+    """Speculation geometry (host-only): segment bytes, halo cap, segments of one stream."""
+    out = (ctypes.c_uint64 * 3)()
+    check(lib.cdc_plan_info(ctypes.byref(p), nfiles, total_len, max_len, out))
+    return {"seg_bytes": int(out[0]), "halo_cap": int(out[1]), "segments": int(out[2])}
+
+
+def segment_starts(p: cdc_params, length: int) -> list:
+    """First byte of every speculation segment of a single stream (cdc_plan_info's rule)."""
+    n = plan_info(p, 1, length, length)["segments"]
+    if n == 0:
+        return []
+    q = length // n
+    mask = ~4095 if q >= (64 << 10) else ~15
+    return [(k * q) & mask for k in range(n)]
 
 
 def abi_version() -> int:

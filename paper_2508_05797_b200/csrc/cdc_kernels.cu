@@ -1541,6 +1541,18 @@ extern "C" int cdc_debug_wait_ns(unsigned long long *ns) {
     return CDC_OK;
 }
 
+int cdc_plan_info(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, uint64_t *out) {
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!out) return fail(CDC_ERR_INVALID, "null out");
+    Plan P;
+    make_plan(p, nfiles ? nfiles : 1, total_len, max_len, P);
+    out[0] = P.S;
+    out[1] = P.Hmax;
+    out[2] = max_len == 0 ? 0 : (max_len < P.S ? 1 : max_len / P.S);
+    return CDC_OK;
+}
+
 int cdc_debug_timing(void *d_buf) {
     unsigned long long *p = static_cast<unsigned long long *>(d_buf);
     CDC_CUDA(cudaMemcpyToSymbol(cdc::g_timing, &p, sizeof(p)));

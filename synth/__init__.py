@@ -127,22 +127,29 @@ def file_sizes(n_files: int, seed: int = 3, median: int = 64 << 10, sigma: float
 
 def many_files(n_files: int, seed: int = 3, median: int = 64 << 10, sigma: float = 1.5,
                cap: int = 16 << 20, uniform_frac: float = 0.7, zipf_s: float = 1.1):
-    """Packed many-file batch: returns (data uint8[total], offsets int64[n_files+1])."""
+    """Packed many-file batch: returns (data uint8[total], offsets int64[n_files+1]).
+
+    File kinds are drawn per file (uniform with probability uniform_frac, else
+    Zipf-skewed); the bytes of all uniform files come from one uniform draw and
+    those of all Zipf files from one Zipf draw, split in file order."""
     sizes = file_sizes(n_files, seed, median, sigma, cap)
     rng = _rng(seed + 1000)
     offsets = np.zeros(n_files + 1, dtype=np.int64)
     np.cumsum(sizes, out=offsets[1:])
-    data = np.empty(int(offsets[-1]), dtype=np.uint8)
     kinds = rng.random(n_files) < uniform_frac
-    cdf, perm = _zipf_table(zipf_s, rng)
-    cdf[-1] = 1.0
-    for i in range(n_files):
-        lo, hi = int(offsets[i]), int(offsets[i + 1])
-        if kinds[i]:
-            data[lo:hi] = rng.integers(0, 256, size=hi - lo, dtype=np.uint8)
+    u = rng.integers(0, 256, size=int(sizes[kinds].sum()), dtype=np.uint8)
+    z = zipf_bytes(int(sizes[~kinds].sum()), zipf_s, rng=rng)
+    ui = np.split(u, np.cumsum(sizes[kinds])[:-1]) if kinds.any() else []
+    zi = np.split(z, np.cumsum(sizes[~kinds])[:-1]) if (~kinds).any() else []
+    pieces, a, b = [], 0, 0
+    for k in kinds.tolist():
+        if k:
+            pieces.append(ui[a])
+            a += 1
         else:
-            idx = np.minimum(np.searchsorted(cdf, rng.random(hi - lo), side="right"), 255)
-            data[lo:hi] = perm[idx]
+            pieces.append(zi[b])
+            b += 1
+    data = np.concatenate(pieces) if pieces else np.zeros(0, dtype=np.uint8)
     return data, offsets
 
 
