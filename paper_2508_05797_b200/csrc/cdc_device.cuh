@@ -120,6 +120,25 @@ __device__ __forceinline__ void st_relaxed_u32(uint32_t *p, uint32_t v) {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Diagnostic per-warp cycle accounting (CDC_EVTIME builds only): ET_BEGIN(v)
+// stamps clock64, ET_ADD(i, v) adds the cycles since the stamp to bucket i.
+__device__ unsigned long long g_evt[16];
+#ifdef CDC_EVTIME
+#define ET_DECL long long et_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long et_t0 = clock64(), et_t1 = 0;
+#define ET_BEGIN(v) v = clock64()
+#define ET_ADD(i, v) et_acc[i] += clock64() - v
+#define ET_FLUSH                                                        \
+    if ((threadIdx.x & 31) == 0) {                                      \
+        for (int q = 0; q < 8; ++q) atomicAdd(&g_evt[q], (unsigned long long)et_acc[q]); \
+        atomicAdd(&g_evt[8], (unsigned long long)(clock64() - et_t0));  \
+    }
+#else
+#define ET_DECL
+#define ET_BEGIN(v)
+#define ET_ADD(i, v)
+#define ET_FLUSH
+#endif
+
 // Diagnostic event counters (CDC_COUNTERS builds only): CNT(i) adds 1 per warp.
 __device__ unsigned long long g_cnt[16];
 #ifdef CDC_COUNTERS
@@ -289,13 +308,23 @@ __device__ __forceinline__ L2Pol stream_policy() { return L2Pol{l2_evict_first_p
 template <bool MAX>
 __device__ __forceinline__ uint32_t block_lane_ext(const uint8_t *sp, int Bk, int lo, int hi, bool &has,
                                                    uint4 &v) {
+    // branch-free: a 16-bit keep mask of the lane's bytes in [lo, hi), expanded
+    // to byte masks; bytes outside become the neutral value
     v = *reinterpret_cast<const uint4 *>(sp + Bk + lane_id() * 16);
     int a, b;
     lane_part(lo - Bk, hi - Bk, a, b);
     has = a < b;
-    if (a == 0 && b == 16) return vext16<MAX>(v);
-    if (a >= b) return neutral<MAX>();
-    return vext16_range<MAX>(v, a, b);
+    const uint32_t m16 = has ? (((1u << b) - 1u) & ~((1u << a) - 1u)) : 0u;
+    auto expand = [](uint32_t nib) { return ((nib * 0x00204081u) & 0x01010101u) * 0xFFu; };
+    const uint32_t k0 = expand(m16 & 0xFu), k1 = expand((m16 >> 4) & 0xFu), k2 = expand((m16 >> 8) & 0xFu),
+                   k3 = expand(m16 >> 12);
+    uint4 r;
+    if (MAX) {
+        r.x = v.x & k0; r.y = v.y & k1; r.z = v.z & k2; r.w = v.w & k3;
+    } else {
+        r.x = v.x | ~k0; r.y = v.y | ~k1; r.z = v.z | ~k2; r.w = v.w | ~k3;
+    }
+    return vext16<MAX>(r);
 }
 
 // Extreme Byte Search (§4.1) of the stage bytes [lo, hi): per-lane extreme
@@ -386,6 +415,26 @@ __device__ __forceinline__ int stage_find_block(const uint8_t *sp, int lo, int h
         Bk += BLK;
     }
     has = true;
+    for (; Bk + 4 * BLK <= hi; Bk += 4 * BLK) {  // four blocks in flight
+        const uint4 a = *reinterpret_cast<const uint4 *>(sp + Bk + lane16);
+        const uint4 b = *reinterpret_cast<const uint4 *>(sp + Bk + BLK + lane16);
+        const uint4 c = *reinterpret_cast<const uint4 *>(sp + Bk + 2 * BLK + lane16);
+        const uint4 d = *reinterpret_cast<const uint4 *>(sp + Bk + 3 * BLK + lane16);
+        const uint32_t ma = vext16<MAX>(a), mb = vext16<MAX>(b), mc = vext16<MAX>(c), md = vext16<MAX>(d);
+        const bool ha = cmp_holds<CMP>(ma, target), hb = cmp_holds<CMP>(mb, target);
+        const bool hc = cmp_holds<CMP>(mc, target), hd = cmp_holds<CMP>(md, target);
+        if (__any_sync(0xFFFFFFFFu, ha || hb || hc || hd)) {
+            bal = __ballot_sync(0xFFFFFFFFu, ha);
+            if (bal) { lm = ma; return Bk; }
+            bal = __ballot_sync(0xFFFFFFFFu, hb);
+            if (bal) { lm = mb; return Bk + BLK; }
+            bal = __ballot_sync(0xFFFFFFFFu, hc);
+            if (bal) { lm = mc; return Bk + 2 * BLK; }
+            bal = __ballot_sync(0xFFFFFFFFu, hd);
+            lm = md;
+            return Bk + 3 * BLK;
+        }
+    }
     for (; Bk + 2 * BLK <= hi; Bk += 2 * BLK) {
         CNT(8);
         const uint4 a = *reinterpret_cast<const uint4 *>(sp + Bk + lane16);
@@ -535,6 +584,8 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     int slot = 0;
     uint32_t parity = 0;
     int64_t k = 0;
+    ET_DECL
+    ET_BEGIN(et_t1);
     for (; k < nstages && !stop; ++k) {
         CNT(0);
         const int64_t SB = B0 + k * STAGE;
@@ -564,6 +615,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
             else hor = FAR;
             return false;
         };
+        ET_ADD(0, et_t1);  // stage transition: wait + setup
         while (cr < endr) {
             if constexpr (ALGO == ALGO_RAM) {
                 if (!scanning) {
@@ -598,11 +650,14 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
             } else {
                 if (pending) {  // first byte of the chunk: the first target
                     CNT(1);
+                    long long e0;
+                    ET_BEGIN(e0);
                     ext = sp[cr];
                     t = SB + cr;
                     hor = cr + W1 < FAR ? cr + W1 : FAR;
                     ++cr;
                     pending = false;
+                    ET_ADD(4, e0);
                     continue;
                 }
                 int hi = hor < limr ? hor : limr;
@@ -612,9 +667,13 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                     uint32_t bal = 0, lm;
                     bool has;
                     CNT(2);
+                    long long e1;
+                    ET_BEGIN(e1);
                     const int Bk = stage_find_block<CMP_BEAT>(sp, cr, hi, ext, bal, lm, has);
+                    ET_ADD(1, e1);
                     if (Bk >= 0) {
                         CNT(3);
+                        ET_BEGIN(e1);
                         const int lo = cr > Bk ? cr : Bk;
                         const int bh = hi < Bk + BLK ? hi : Bk + BLK;
                         int r;
@@ -634,6 +693,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                         }
                         t = SB + r;
                         hor = r + W1 < FAR ? r + W1 : FAR;
+                        ET_ADD(2, e1);
                         continue;
                     }
                 }
@@ -642,13 +702,17 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                 if (cr == hor && hor <= limr) er = hor;  // target unbeaten over its window
                 else if (cr == limr) er = limr;         // cap or end of stream
                 else break;                             // stage exhausted
+                long long e3;
+                ET_BEGIN(e3);
                 if (event(er)) {
                     stop = true;
                     break;
                 }
+                ET_ADD(3, e3);
             }
         }
         c = SB + cr;
+        ET_BEGIN(et_t1);
         __syncwarp();
         if (!stop && issued < nstages) {  // refill this slot with stage k + NST
             issue(issued, slot);
@@ -664,6 +728,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
         if (c >= Lf) emit.end();
         else emit.exhausted(c);
     }
+    ET_FLUSH
     // drain copies still in flight (stages k .. issued-1) before the ring is reused or the CTA exits
     for (; k < issued; ++k) {
         mbar_wait(&R.bar[slot], parity);

@@ -1525,6 +1525,14 @@ const char *cdc_last_error(void) { return g_err.c_str(); }
 
 int cdc_last_launch_count(void) { return g_launches; }
 
+// diagnostic (CDC_EVTIME builds): read and reset the 16 cycle buckets
+extern "C" int cdc_debug_evtime(unsigned long long *out) {
+    CDC_CUDA(cudaMemcpyFromSymbol(out, cdc::g_evt, 16 * sizeof(unsigned long long)));
+    unsigned long long z[16] = {0};
+    CDC_CUDA(cudaMemcpyToSymbol(cdc::g_evt, z, sizeof(z)));
+    return CDC_OK;
+}
+
 // diagnostic (CDC_COUNTERS builds): read and reset the 16 event counters
 extern "C" int cdc_debug_counters(unsigned long long *out) {
     CDC_CUDA(cudaMemcpyFromSymbol(out, cdc::g_cnt, 16 * sizeof(unsigned long long)));

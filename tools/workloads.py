@@ -48,3 +48,29 @@ if not sel or "u256" in sel:
             run("uniform 256MiB", u, algo, avg, reps=3)
 if not sel or "c4" in sel:
     run("c4-shape alternating 1GiB", synth.alternating(1 << 30, region=256 << 20, seed=5), "ram", 8192, reps=3)
+
+
+def run_batch(name, data_np, offs, algo, avg, reps=3):
+    t = torch.from_numpy(data_np).cuda()
+    p = cdc.params(algo, avg_size=avg)
+    for _ in range(2):
+        cdc.chunk_batch(t, offs, p)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        b, bo = cdc.chunk_batch(t, offs, p)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    print("%-28s %-6s %5d  %8.3f ms  %8.1f GB/s  files %d chunks %d (includes host-side setup per call)" % (
+        name, algo, avg, ms, t.numel() / ms / 1e6, len(offs) - 1, int(bo[-1])), flush=True)
+
+
+if "c4big" in sel:
+    d = synth.alternating(4 << 30, region=256 << 20, seed=5)
+    run("c4-shape alternating 4GiB", d, "ram", 8192, reps=3)
+    run("c4-shape alternating 4GiB", d, "ae_max", 8192, reps=3)
+if "c3" in sel:
+    data, offs = synth.many_files(25000, seed=3)
+    run_batch("c3 many files (25k)", data, offs, "ram", 8192)
