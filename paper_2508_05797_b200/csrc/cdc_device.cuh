@@ -25,12 +25,12 @@ namespace cdc {
 
 constexpr int BLK = 512;               // bytes per warp block: 32 lanes x 16 B
 #ifndef CDC_STAGE
-#define CDC_STAGE 4096
+#define CDC_STAGE 6144
 #endif
 #ifndef CDC_NST
-#define CDC_NST 3
+#define CDC_NST 2
 #endif
-constexpr int STAGE = CDC_STAGE;       // bytes per TMA stage (8 warp blocks)
+constexpr int STAGE = CDC_STAGE;       // bytes per TMA stage (12 warp blocks)
 constexpr int NST = CDC_NST;           // ring depth per warp (12 KiB)
 constexpr int RING_BYTES = STAGE * NST;
 constexpr int RING_SMEM = (RING_BYTES + NST * 8 + 127) / 128 * 128;  // keeps every ring 128-byte aligned
@@ -125,6 +125,7 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ unsigned long long g_evt[16];
 #ifdef CDC_EVTIME
 #define ET_DECL long long et_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long et_t0 = clock64(), et_t1 = 0;
+#define ET_VAR(v) long long v;
 #define ET_BEGIN(v) v = clock64()
 #define ET_ADD(i, v) et_acc[i] += clock64() - v
 #define ET_FLUSH                                                        \
@@ -134,6 +135,7 @@ __device__ unsigned long long g_evt[16];
     }
 #else
 #define ET_DECL
+#define ET_VAR(v)
 #define ET_BEGIN(v)
 #define ET_ADD(i, v)
 #define ET_FLUSH
@@ -650,7 +652,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
             } else {
                 if (pending) {  // first byte of the chunk: the first target
                     CNT(1);
-                    long long e0;
+                    ET_VAR(e0)
                     ET_BEGIN(e0);
                     ext = sp[cr];
                     t = SB + cr;
@@ -667,7 +669,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                     uint32_t bal = 0, lm;
                     bool has;
                     CNT(2);
-                    long long e1;
+                    ET_VAR(e1)
                     ET_BEGIN(e1);
                     const int Bk = stage_find_block<CMP_BEAT>(sp, cr, hi, ext, bal, lm, has);
                     ET_ADD(1, e1);
@@ -702,7 +704,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                 if (cr == hor && hor <= limr) er = hor;  // target unbeaten over its window
                 else if (cr == limr) er = limr;         // cap or end of stream
                 else break;                             // stage exhausted
-                long long e3;
+                ET_VAR(e3)
                 ET_BEGIN(e3);
                 if (event(er)) {
                     stop = true;
