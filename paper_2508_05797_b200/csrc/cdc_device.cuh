@@ -527,13 +527,20 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
 
     int64_t issued = 0;
     auto issue = [&](int64_t k, int slot) {
-        if (lane == 0) {
-            const int64_t off = k * STAGE;
-            const uint32_t bytes = (uint32_t)(nbytes - off < STAGE ? nbytes - off : STAGE);
-            mbar_arrive_expect_tx(&R.bar[slot], bytes);
-            tma_load_1d(R.buf + slot * STAGE, g0 + off, bytes, &R.bar[slot],
-                        B0 + off < pol.keep_until ? pol.keep : pol.stream);
-        }
+        // operands computed by every lane (uniform, no divergent region); one elected lane issues
+        const int64_t off = k * STAGE;
+        const uint32_t bytes = (uint32_t)(nbytes - off < STAGE ? nbytes - off : STAGE);
+        const uint64_t policy = B0 + off < pol.keep_until ? pol.keep : pol.stream;
+        uint64_t *bar = &R.bar[slot];
+        uint8_t *dst = R.buf + slot * STAGE;
+        const uint8_t *src = g0 + off;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "elect.sync _|p, 0xffffffff;\n\t"
+            "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+            "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%2], [%3], %1, [%0], %4;\n\t"
+            "}" ::"r"(smem_addr(bar)), "r"(bytes), "r"(smem_addr(dst)), "l"(src), "l"(policy)
+            : "memory");
     };
     for (; issued < nstages && issued < NST; ++issued) issue(issued, (int)issued);
 
@@ -619,6 +626,8 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
         };
         ET_ADD(0, et_t1);  // stage transition: wait + setup
         while (cr < endr) {
+            ET_VAR(eit)
+            ET_BEGIN(eit);
             if constexpr (ALGO == ALGO_RAM) {
                 if (!scanning) {
                     const int hi = hor < endr ? hor : endr;
@@ -665,6 +674,8 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                 int hi = hor < limr ? hor : limr;
                 hi = hi < endr ? hi : endr;
                 if (ext == SAT) CNT(5);
+                const bool sat_iter = ext == SAT;
+                (void)sat_iter;
                 if (ext != SAT && cr < hi) {
                     uint32_t bal = 0, lm;
                     bool has;
@@ -700,6 +711,9 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                     }
                 }
                 cr = hi;
+#ifdef CDC_EVTIME
+                if (sat_iter) { ET_ADD(5, eit); } else { ET_ADD(6, eit); }
+#endif
                 int er;
                 if (cr == hor && hor <= limr) er = hor;  // target unbeaten over its window
                 else if (cr == limr) er = limr;         // cap or end of stream

@@ -235,7 +235,7 @@ struct SpecEmit {
     __device__ bool boundary(int64_t e) {
         const int lane = lane_id();
         if (e < I.seg_end) {
-            if (lane == 0) st_relaxed_u32(list + cnt, (uint32_t)(e - I.p));
+            if (lane == 0) __stcg(list + cnt, (uint32_t)(e - I.p));  // L2 store; readers use ld.relaxed.gpu
             ++cnt;
             return false;
         }

@@ -19,7 +19,8 @@ lib.cdc_debug_evtime(ev)
 cdc.chunk_async(t, p, b, c, ws)
 torch.cuda.synchronize()
 lib.cdc_debug_evtime(ev)
-names = ["stage transition (wait+setup)", "find_block", "record", "boundary event", "pending", "", "", "", "walk total"]
+names = ["stage transition (wait+setup)", "find_block", "record", "boundary event", "pending",
+         "iter: saturated (whole iteration)", "iter: no-hit find (whole iteration, incl. find)", "", "walk total"]
 tot = ev[8]
 chunks = int(c.item())
 for i, k in enumerate(names):
