@@ -546,7 +546,6 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
 
     const int64_t W = (int64_t)w;
     const int W1 = w + 1 < (uint32_t)FAR ? (int)w + 1 : FAR;  // deadline distance t -> t+w+1, clamped
-    const bool fastrec = w >= (uint32_t)(BLK - 1);  // AE: records inside one block never miss a deadline
     // chain state (stream positions)
     int64_t s = start;                                                           // current chunk start
     int64_t limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;  // chunk end bound
@@ -687,23 +686,42 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                     if (Bk >= 0) {
                         CNT(3);
                         ET_BEGIN(e1);
+                        // Every byte of [cr, hi) lies inside the current target's window
+                        // (hi <= t + w + 1), so the records of [cr, hi) follow one another
+                        // within w bytes and none ends the chunk: the last of them -- the
+                        // first occurrence of the range's extreme -- is the new target.
+                        // One Extreme Byte Search (§4.1) over the rest of the range (it
+                        // stops at the first block holding the saturating value) replaces
+                        // a record event per block.
                         const int lo = cr > Bk ? cr : Bk;
-                        const int bh = hi < Bk + BLK ? hi : Bk + BLK;
-                        int r;
-                        if (fastrec) {
-                            // every record of [lo, bh) follows its predecessor within
-                            // < BLK <= w+1 bytes, so the last one -- the first
-                            // occurrence of the range extreme -- is the new target
-                            const uint32_t m = warp_ext<MAX>(lm);
-                            const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, has && lm == m);
-                            r = stage_locate<CMP_EQ>(sp, Bk, b2, lo, bh, m);
-                            ext = m;
-                            cr = bh;
-                        } else {
-                            r = stage_locate<CMP_BEAT>(sp, Bk, bal, lo, bh, ext);
-                            ext = sp[r];
-                            cr = r + 1;
+                        uint32_t lacc = has ? lm : neutral<MAX>();
+                        int lblk = Bk, Bs = -1;
+                        if (__any_sync(0xFFFFFFFFu, has && lm == SAT)) Bs = Bk;
+                        for (int B = Bk + BLK; Bs < 0 && B < hi; B += BLK) {
+                            uint32_t mb;
+                            if (B + BLK <= hi) {
+                                mb = vext16<MAX>(*reinterpret_cast<const uint4 *>(sp + B + lane * 16));
+                            } else {
+                                bool h2;
+                                uint4 v2;
+                                mb = block_lane_ext<MAX>(sp, B, B, hi, h2, v2);
+                            }
+                            if (beats<MAX>(mb, lacc)) {
+                                lacc = mb;
+                                lblk = B;
+                            }
+                            if (__any_sync(0xFFFFFFFFu, mb == SAT)) Bs = B;
                         }
+                        const uint32_t m = Bs >= 0 ? SAT : warp_ext<MAX>(lacc);
+                        const int Bf = Bs >= 0 ? Bs : (int)__reduce_min_sync(0xFFFFFFFFu, lacc == m ? (uint32_t)lblk : 0x7FFFFFFFu);
+                        const int flo = lo > Bf ? lo : Bf, fhi = hi < Bf + BLK ? hi : Bf + BLK;
+                        bool hf;
+                        uint4 vf;
+                        const uint32_t lmf = block_lane_ext<MAX>(sp, Bf, flo, fhi, hf, vf);
+                        const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, hf && lmf == m);
+                        const int r = stage_locate<CMP_EQ>(sp, Bf, b2, flo, fhi, m);
+                        ext = m;
+                        cr = Bs >= 0 ? fhi : hi;  // nothing in (r, cr) beats m
                         t = SB + r;
                         hor = r + W1 < FAR ? r + W1 : FAR;
                         ET_ADD(2, e1);
