@@ -989,8 +989,8 @@ __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_
         while (ld_acquire_u64(reinterpret_cast<const unsigned long long *>(W.ctrl + 4)) != 1ull) __nanosleep(256);
     }
     __syncthreads();
-    const uint64_t g = (uint64_t)role * 32 + (threadIdx.x >> 5);
-    if (g < nsegs) write_segment(G, W, file_out, bounds, cap, g);
+    for (uint64_t g = (uint64_t)role * 32 + (threadIdx.x >> 5); g < nsegs; g += (uint64_t)gridDim.x * 32)
+        write_segment(G, W, file_out, bounds, cap, g);
 }
 
 // ------------------------------------------------------------------ K0 batch segment table
@@ -1286,6 +1286,7 @@ uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 // TMA stage, at least 64 KiB and 4 max-size chunks, so that the
 // re-synchronisation halo (a few chunks on typical data) is small next to it.
 constexpr uint64_t SEGS_PER_SM = (uint64_t)cdc::SPEC_WARPS * cdc::SPEC_CTAS_PER_SM;
+constexpr uint64_t FIX_BLOCKS = 16;  // k_fixup grid cap
 
 void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, Plan &P) {
     uint64_t S = p->seg_bytes;
@@ -1447,7 +1448,8 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     const bool tail = false;
 #endif
     if (!tail) {
-        const uint64_t fblocks = (nseg_ub + 31) / 32;
+        // a small grid: it exits at once in the common case; writers stride over segments otherwise
+        const uint64_t fblocks = std::min<uint64_t>((nseg_ub + 31) / 32, FIX_BLOCKS);
         cdc::k_fixup<ALGO><<<(unsigned)(fblocks ? fblocks : 1), cdc::RESOLVE_THREADS, cdc::FIX_SMEM, st>>>(
             G, W, d_count, file_out, d_bounds, cap);
         CDC_KCHECK("k_fixup", st);
