@@ -697,7 +697,24 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                         uint32_t lacc = has ? lm : neutral<MAX>();
                         int lblk = Bk, Bs = -1;
                         if (__any_sync(0xFFFFFFFFu, has && lm == SAT)) Bs = Bk;
-                        for (int B = Bk + BLK; Bs < 0 && B < hi; B += BLK) {
+                        int B = Bk + BLK;
+                        for (; Bs < 0 && B + 2 * BLK <= hi; B += 2 * BLK) {  // two blocks in flight
+                            const uint32_t m0 = vext16<MAX>(*reinterpret_cast<const uint4 *>(sp + B + lane * 16));
+                            const uint32_t m1 =
+                                vext16<MAX>(*reinterpret_cast<const uint4 *>(sp + B + BLK + lane * 16));
+                            if (beats<MAX>(m0, lacc)) {
+                                lacc = m0;
+                                lblk = B;
+                            }
+                            if (beats<MAX>(m1, lacc)) {
+                                lacc = m1;
+                                lblk = B + BLK;
+                            }
+                            const uint32_t s0 = __ballot_sync(0xFFFFFFFFu, m0 == SAT);
+                            const uint32_t s1 = __ballot_sync(0xFFFFFFFFu, m1 == SAT);
+                            if (s0 | s1) Bs = s0 ? B : B + BLK;
+                        }
+                        for (; Bs < 0 && B < hi; B += BLK) {
                             uint32_t mb;
                             if (B + BLK <= hi) {
                                 mb = vext16<MAX>(*reinterpret_cast<const uint4 *>(sp + B + lane * 16));
