@@ -32,9 +32,12 @@
 
 namespace cdc {
 
-constexpr int SPEC_WARPS = 4;     // warps (segments) per CTA in k_speculate
+#ifndef CDC_SPEC_WARPS
+#define CDC_SPEC_WARPS 16
+#endif
+constexpr int SPEC_WARPS = CDC_SPEC_WARPS;  // warps (segments) per CTA in k_speculate
 #ifndef CDC_SPEC_CTAS_PER_SM
-#define CDC_SPEC_CTAS_PER_SM 4
+#define CDC_SPEC_CTAS_PER_SM 1
 #endif
 constexpr int SPEC_CTAS_PER_SM = CDC_SPEC_CTAS_PER_SM;  // resident k_speculate CTAs per SM (smem-bound)
 constexpr int HEAD_KEEP = 16384;  // bytes of each segment head kept in L2 for the halo re-read
