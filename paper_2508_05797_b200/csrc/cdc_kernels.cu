@@ -286,6 +286,21 @@ __device__ __forceinline__ uint32_t smid() {
     return r;
 }
 
+// Programmatic dependent launch (PDL): the next kernel in the stream may be
+// launched before this grid completes; it waits (griddepcontrol.wait) for the
+// full completion and memory flush of its predecessor before touching its data.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// K0': reset of the published-list region (list entries, publish, look-back
+// and ticket words) to all-ones; lets k_speculate launch early (PDL).
+__global__ void __launch_bounds__(256) k_reset(uint4 *p, uint64_t n16) {
+    pdl_trigger();
+    const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = ones;
+}
+
 // Decoupled look-back words: the top two bits say what the low 62 bits (a
 // signed value) hold.  The memset leaves every word ~0 = not ready.
 constexpr unsigned long long ST_AGG = 1ull << 62;   // a_g = (cnt + tail) - sb of this segment
@@ -429,6 +444,7 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_ticket;
     const int warp = threadIdx.x >> 5;
+    pdl_wait();  // the reset of the published lists has completed
     if (threadIdx.x == 0) s_ticket = atomicAdd(W.ctrl, 1u) + 1u;  // counter starts at ~0
     __syncthreads();
     const uint64_t g = (uint64_t)s_ticket * SPEC_WARPS + warp;
@@ -517,6 +533,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
             stg[i] = i < em.cnt ? ld_relaxed_u32(em.list + i) : hoff + em.halo[i - em.cnt];
     }
     if (fused) publish_agg(W, g, nsegs, a, sb);
+    pdl_trigger();  // k_fixup may launch; it waits for this grid's completion
     if (!fused || fused_dbg == 3) return;
     uint32_t entry = 0;
     const int64_t excl = g == 0 ? 0 : lookback(W, g, entry);
@@ -976,6 +993,7 @@ template <int ALGO>
 __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_count, uint64_t *file_out,
                                                 uint64_t *bounds, uint64_t cap) {
     __shared__ uint32_t s_role;
+    pdl_wait();  // k_speculate has completed and its writes are visible
     const uint64_t nsegs = total_segs(G, W);
     const bool fast = nsegs > 0 && W.ctrl[1] != 0u;
     if (fast && G.file_off == nullptr) return;
@@ -1254,6 +1272,25 @@ int fused_mode() {
     return v;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor in the stream finishes; it calls griddepcontrol.wait
+// before reading the predecessor's results.
+template <typename... Args>
+cudaError_t launch_pdl(const void *fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void *pargs[] = {reinterpret_cast<void *>(&args)...};
+    return cudaLaunchKernelExC(&cfg, fn, pargs);
+}
+
 int check_params(const cdc_params *p) {
     if (!p) return fail(CDC_ERR_INVALID, "null params");
     if (p->algo < CDC_RAM || p->algo > CDC_AE_MIN) return fail(CDC_ERR_INVALID, "unknown algorithm");
@@ -1426,17 +1463,22 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         pc.used[0] = true;
     }
     // reset the published lists (list entries -> LIST_EMPTY, pub -> PUB_OPEN)
-    CDC_CUDA(cudaMemsetAsync(W.list, 0xFF, P.reset_bytes, st));
+    {
+        const uint64_t n16 = P.reset_bytes / 16;  // reset_bytes is a multiple of 256
+        const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());
+        cdc::k_reset<<<rb ? rb : 1, 256, 0, st>>>(reinterpret_cast<uint4 *>(W.list), n16);
+        CDC_KCHECK("k_reset", st);
+    }
     ++launches;
     mark(1);
     const uint64_t nseg_ub = P.max_segs;
     const uint64_t blocks = (nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS;
     if (blocks > 0) {
-        cdc::k_speculate<ALGO><<<(unsigned)blocks, cdc::SPEC_WARPS * 32, spec_smem, st>>>(G, W, d_bounds, cap,
-                                                                                          d_count,
-                                                                                          (P.cap_list + P.cap_halo < (1u << 23))
-                                                                                              ? fused_mode() : 0,
-                                                                                          tail_mode(batch));
+        int fused = (P.cap_list + P.cap_halo < (1u << 23)) ? fused_mode() : 0;
+        int tmode = tail_mode(batch);
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_speculate<ALGO>), dim3((unsigned)blocks),
+                            dim3(cdc::SPEC_WARPS * 32), (size_t)spec_smem, st, G, W, d_bounds, cap, d_count, fused,
+                            tmode));
         CDC_KCHECK("k_speculate", st);
         ++launches;
         pc.used[1] = true;
@@ -1453,8 +1495,9 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     if (!tail) {
         // a small grid: it exits at once in the common case; writers stride over segments otherwise
         const uint64_t fblocks = std::min<uint64_t>((nseg_ub + 31) / 32, FIX_BLOCKS);
-        cdc::k_fixup<ALGO><<<(unsigned)(fblocks ? fblocks : 1), cdc::RESOLVE_THREADS, cdc::FIX_SMEM, st>>>(
-            G, W, d_count, file_out, d_bounds, cap);
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_fixup<ALGO>), dim3((unsigned)(fblocks ? fblocks : 1)),
+                            dim3(cdc::RESOLVE_THREADS), (size_t)cdc::FIX_SMEM, st, G, W, d_count, file_out, d_bounds,
+                            cap));
         CDC_KCHECK("k_fixup", st);
         ++launches;
         pc.used[2] = true;
