@@ -245,7 +245,7 @@ def main():
     path_stats = cdc.stats(p, ws, 1, STREAM, STREAM)
 
     # The timed region replays a CUDA graph of two steps (one per input copy):
-    # the three launches of a step (memset, k_speculate, k_fixup; the last
+    # the three launches of a step (k_reset, k_speculate, k_fixup; the last
     # exits at once when the fused fast path succeeded) without
     # host launch overhead.  --no-graph times direct launches instead.
     graph = None

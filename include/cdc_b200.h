@@ -218,8 +218,8 @@ int cdc_profile_query(int *done);
  * Diagnostics of the last call that used workspace d_workspace (same params
  * and sizes as that call): synchronises `stream` and writes to stats[8]:
  *   [0] segments G, [1] segment bytes S, [2] halo cap bytes,
- *   [3] 1 if the fused look-back fast path produced the output (0: the
- *       k_resolve/k_write fix-up path ran), [4] segments whose chain met the
+ *   [3] 1 if the fused look-back fast path produced the output (0: k_fixup's
+ *       resolver and fix-up walkers ran), [4] segments whose chain met the
  *       next segment's chain, [5] segments whose halo walk gave up or was
  *       undecided, [6] segments whose chain skipped a later segment or reached
  *       the stream end from a non-final segment, [7] total halo chunks.
@@ -234,10 +234,16 @@ int cdc_profile_query(int *done);
 int cdc_plan_info(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, uint64_t *out);
 
 /*
- * Diagnostics: while d_buf (a device uint64 array of 4 x segments entries) is
- * set, k_speculate records per segment {globaltimer at start, at the end of the
- * walk, at the end of its fused write, SM id | halo chunks << 32}.  NULL turns
- * recording off.  Never set during measurements.
+ * Diagnostics: while d_buf (a device uint64 array of 8 + 4 x segments
+ * entries) is set, the kernels record globaltimer stamps.  d_buf[0..7]:
+ * k_reset first start / last end, k_speculate first CTA start / first return
+ * from its PDL wait / last walker end, k_fixup first CTA start / first return
+ * from its PDL wait / last end (the caller presets the "first" slots 0, 2, 3,
+ * 5, 6 to ~0 and the "last" slots 1, 4, 7 to 0; a k_fixup that runs the fix-up
+ * path leaves slot 7 alone).  Then per segment g, at d_buf[8 + 4g]:
+ * {at start, at the end of the walk, at the end of its fused write,
+ * SM id | halo chunks << 32}.  NULL turns recording off.  Never set during
+ * measurements.
  */
 int cdc_debug_timing(void *d_buf);
 

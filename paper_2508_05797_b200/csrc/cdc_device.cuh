@@ -658,92 +658,97 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                     }
                 }
             } else {
-                if (pending) {  // first byte of the chunk: the first target
-                    CNT(1);
-                    ET_VAR(e0)
-                    ET_BEGIN(e0);
-                    ext = sp[cr];
+                // pending: the chunk's first byte is its first target, deadline s + w + 1
+                if (pending) {
                     t = SB + cr;
                     hor = cr + W1 < FAR ? cr + W1 : FAR;
-                    ++cr;
-                    pending = false;
-                    ET_ADD(4, e0);
-                    continue;
                 }
                 int hi = hor < limr ? hor : limr;
                 hi = hi < endr ? hi : endr;
-                if (ext == SAT) CNT(5);
-                const bool sat_iter = ext == SAT;
+                if (ext == SAT && !pending) CNT(5);
+                const bool sat_iter = ext == SAT && !pending;
                 (void)sat_iter;
-                if (ext != SAT && cr < hi) {
-                    uint32_t bal = 0, lm;
-                    bool has;
+                int Bk = -1;  // first block of [cr, hi) that can hold the next target
+                uint32_t lm = 0;
+                bool has = false;
+                if (pending) {
+                    // Every byte of [s, hi) lies in the window of the first target s,
+                    // so the collapse below applies from the chunk's first byte on: the
+                    // target after [s, hi) is the first occurrence of its extreme (no
+                    // separate first-byte step and record scan).
+                    CNT(1);
+                    Bk = cr & ~(BLK - 1);
+                    uint4 v0;
+                    lm = block_lane_ext<MAX>(sp, Bk, cr, hi < Bk + BLK ? hi : Bk + BLK, has, v0);
+                    pending = false;
+                } else if (ext != SAT && cr < hi) {
+                    uint32_t bal = 0;
                     CNT(2);
                     ET_VAR(e1)
                     ET_BEGIN(e1);
-                    const int Bk = stage_find_block<CMP_BEAT>(sp, cr, hi, ext, bal, lm, has);
+                    Bk = stage_find_block<CMP_BEAT>(sp, cr, hi, ext, bal, lm, has);
                     ET_ADD(1, e1);
-                    if (Bk >= 0) {
-                        CNT(3);
-                        ET_BEGIN(e1);
-                        // Every byte of [cr, hi) lies inside the current target's window
-                        // (hi <= t + w + 1), so the records of [cr, hi) follow one another
-                        // within w bytes and none ends the chunk: the last of them -- the
-                        // first occurrence of the range's extreme -- is the new target.
-                        // One Extreme Byte Search (§4.1) over the rest of the range (it
-                        // stops at the first block holding the saturating value) replaces
-                        // a record event per block.
-                        const int lo = cr > Bk ? cr : Bk;
-                        uint32_t lacc = has ? lm : neutral<MAX>();
-                        int lblk = Bk, Bs = -1;
-                        if (__any_sync(0xFFFFFFFFu, has && lm == SAT)) Bs = Bk;
-                        int B = Bk + BLK;
-                        for (; Bs < 0 && B + 2 * BLK <= hi; B += 2 * BLK) {  // two blocks in flight
-                            const uint32_t m0 = vext16<MAX>(*reinterpret_cast<const uint4 *>(sp + B + lane * 16));
-                            const uint32_t m1 =
-                                vext16<MAX>(*reinterpret_cast<const uint4 *>(sp + B + BLK + lane * 16));
-                            if (beats<MAX>(m0, lacc)) {
-                                lacc = m0;
-                                lblk = B;
-                            }
-                            if (beats<MAX>(m1, lacc)) {
-                                lacc = m1;
-                                lblk = B + BLK;
-                            }
-                            const uint32_t s0 = __ballot_sync(0xFFFFFFFFu, m0 == SAT);
-                            const uint32_t s1 = __ballot_sync(0xFFFFFFFFu, m1 == SAT);
-                            if (s0 | s1) Bs = s0 ? B : B + BLK;
+                }
+                if (Bk >= 0) {
+                    CNT(3);
+                    ET_VAR(e2)
+                    ET_BEGIN(e2);
+                    // Every byte of [cr, hi) lies inside the current target's window
+                    // (hi <= t + w + 1), so the records of [cr, hi) follow one another
+                    // within w bytes and none ends the chunk: the last of them -- the
+                    // first occurrence of the range's extreme -- is the new target.
+                    // One Extreme Byte Search (§4.1) over the rest of the range (it
+                    // stops at the first block holding the saturating value) replaces
+                    // a record event per block.
+                    const int lo = cr > Bk ? cr : Bk;
+                    uint32_t lacc = has ? lm : neutral<MAX>();
+                    int lblk = Bk, Bs = -1;
+                    if (__any_sync(0xFFFFFFFFu, has && lm == SAT)) Bs = Bk;
+                    int B = Bk + BLK;
+                    for (; Bs < 0 && B + 2 * BLK <= hi; B += 2 * BLK) {  // two blocks in flight
+                        const uint32_t m0 = vext16<MAX>(*reinterpret_cast<const uint4 *>(sp + B + lane * 16));
+                        const uint32_t m1 = vext16<MAX>(*reinterpret_cast<const uint4 *>(sp + B + BLK + lane * 16));
+                        if (beats<MAX>(m0, lacc)) {
+                            lacc = m0;
+                            lblk = B;
                         }
-                        for (; Bs < 0 && B < hi; B += BLK) {
-                            uint32_t mb;
-                            if (B + BLK <= hi) {
-                                mb = vext16<MAX>(*reinterpret_cast<const uint4 *>(sp + B + lane * 16));
-                            } else {
-                                bool h2;
-                                uint4 v2;
-                                mb = block_lane_ext<MAX>(sp, B, B, hi, h2, v2);
-                            }
-                            if (beats<MAX>(mb, lacc)) {
-                                lacc = mb;
-                                lblk = B;
-                            }
-                            if (__any_sync(0xFFFFFFFFu, mb == SAT)) Bs = B;
+                        if (beats<MAX>(m1, lacc)) {
+                            lacc = m1;
+                            lblk = B + BLK;
                         }
-                        const uint32_t m = Bs >= 0 ? SAT : warp_ext<MAX>(lacc);
-                        const int Bf = Bs >= 0 ? Bs : (int)__reduce_min_sync(0xFFFFFFFFu, lacc == m ? (uint32_t)lblk : 0x7FFFFFFFu);
-                        const int flo = lo > Bf ? lo : Bf, fhi = hi < Bf + BLK ? hi : Bf + BLK;
-                        bool hf;
-                        uint4 vf;
-                        const uint32_t lmf = block_lane_ext<MAX>(sp, Bf, flo, fhi, hf, vf);
-                        const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, hf && lmf == m);
-                        const int r = stage_locate<CMP_EQ>(sp, Bf, b2, flo, fhi, m);
-                        ext = m;
-                        cr = Bs >= 0 ? fhi : hi;  // nothing in (r, cr) beats m
-                        t = SB + r;
-                        hor = r + W1 < FAR ? r + W1 : FAR;
-                        ET_ADD(2, e1);
-                        continue;
+                        const uint32_t s0 = __ballot_sync(0xFFFFFFFFu, m0 == SAT);
+                        const uint32_t s1 = __ballot_sync(0xFFFFFFFFu, m1 == SAT);
+                        if (s0 | s1) Bs = s0 ? B : B + BLK;
                     }
+                    for (; Bs < 0 && B < hi; B += BLK) {
+                        uint32_t mb;
+                        if (B + BLK <= hi) {
+                            mb = vext16<MAX>(*reinterpret_cast<const uint4 *>(sp + B + lane * 16));
+                        } else {
+                            bool h2;
+                            uint4 v2;
+                            mb = block_lane_ext<MAX>(sp, B, B, hi, h2, v2);
+                        }
+                        if (beats<MAX>(mb, lacc)) {
+                            lacc = mb;
+                            lblk = B;
+                        }
+                        if (__any_sync(0xFFFFFFFFu, mb == SAT)) Bs = B;
+                    }
+                    const uint32_t m = Bs >= 0 ? SAT : warp_ext<MAX>(lacc);
+                    const int Bf = Bs >= 0 ? Bs : (int)__reduce_min_sync(0xFFFFFFFFu, lacc == m ? (uint32_t)lblk : 0x7FFFFFFFu);
+                    const int flo = lo > Bf ? lo : Bf, fhi = hi < Bf + BLK ? hi : Bf + BLK;
+                    bool hf;
+                    uint4 vf;
+                    const uint32_t lmf = block_lane_ext<MAX>(sp, Bf, flo, fhi, hf, vf);
+                    const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, hf && lmf == m);
+                    const int r = stage_locate<CMP_EQ>(sp, Bf, b2, flo, fhi, m);
+                    ext = m;
+                    cr = Bs >= 0 ? fhi : hi;  // nothing in (r, cr) beats m
+                    t = SB + r;
+                    hor = r + W1 < FAR ? r + W1 : FAR;
+                    ET_ADD(2, e2);
+                    continue;
                 }
                 cr = hi;
 #ifdef CDC_EVTIME

@@ -272,13 +272,25 @@ struct SpecEmit {
     __device__ void exhausted(int64_t) { sj = SJ_UNSYNCED; }
 };
 
-// Optional per-segment timing record (cdc_debug_timing): 4 x u64 per segment
-// {globaltimer at start, at the end of the walk, at the end, smid | hcnt << 32}.
+// Optional timing record (cdc_debug_timing): TM_STAMPS launch stamps
+// (globaltimer; min slots preset to ~0 by the caller, max slots to 0), then
+// 4 x u64 per segment {at start, at the end of the walk, at the end,
+// smid | hcnt << 32}.
 __device__ unsigned long long *g_timing = nullptr;
+constexpr int TM_STAMPS = 8;
+enum : int { TM_RESET_BEGIN, TM_RESET_END, TM_SPEC_BEGIN, TM_SPEC_WAITED, TM_SPEC_END, TM_FIX_BEGIN,
+             TM_FIX_WAITED, TM_FIX_END };
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
+}
+__device__ __forceinline__ void stamp(int i) {  // one thread per CTA calls this
+    unsigned long long *tm = g_timing;
+    if (tm == nullptr) return;
+    const unsigned long long t = globaltimer();
+    if (i == TM_RESET_END || i == TM_SPEC_END || i == TM_FIX_END) atomicMax(tm + i, t);
+    else atomicMin(tm + i, t);
 }
 __device__ __forceinline__ uint32_t smid() {
     uint32_t r;
@@ -296,9 +308,11 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // and ticket words) to all-ones; lets k_speculate launch early (PDL).
 __global__ void __launch_bounds__(256) k_reset(uint4 *p, uint64_t n16) {
     pdl_trigger();
+    if (threadIdx.x == 0) stamp(TM_RESET_BEGIN);
     const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
         p[i] = ones;
+    if (threadIdx.x == 0) stamp(TM_RESET_END);
 }
 
 // Decoupled look-back words: the top two bits say what the low 62 bits (a
@@ -444,13 +458,18 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_ticket;
     const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) stamp(TM_SPEC_BEGIN);
     pdl_wait();  // the reset of the published lists has completed
-    if (threadIdx.x == 0) s_ticket = atomicAdd(W.ctrl, 1u) + 1u;  // counter starts at ~0
+    if (threadIdx.x == 0) {
+        stamp(TM_SPEC_WAITED);
+        s_ticket = atomicAdd(W.ctrl, 1u) + 1u;  // counter starts at ~0
+    }
     __syncthreads();
     const uint64_t g = (uint64_t)s_ticket * SPEC_WARPS + warp;
     const uint64_t nsegs = total_segs(G, W);
     if (g >= nsegs) return;
     speculate_segment<ALGO>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused);
+    if (lane_id() == 0) stamp(TM_SPEC_END);
     if (tail_fixup && lane_id() == 0) {
         __threadfence();
         const uint32_t old = atomicAdd(W.ctrl + 2, 1u);  // starts at ~0: old + 2 warps are done
@@ -487,7 +506,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     em.cursor = 0;
     em.published = false;
     if (lane == 0) st_relaxed_u32(em.list, 0u);  // the speculative chain starts at the segment's first byte
-    unsigned long long *tm = g_timing;
+    unsigned long long *tm = g_timing ? g_timing + TM_STAMPS : nullptr;
     if (tm && lane == 0) tm[4 * g] = globaltimer();
     const uint8_t *fbase = G.data + em.I.foff;
     int64_t read_end = (g == em.I.last) ? (int64_t)em.I.Lf
@@ -993,10 +1012,15 @@ template <int ALGO>
 __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_count, uint64_t *file_out,
                                                 uint64_t *bounds, uint64_t cap) {
     __shared__ uint32_t s_role;
+    if (threadIdx.x == 0) stamp(TM_FIX_BEGIN);
     pdl_wait();  // k_speculate has completed and its writes are visible
+    if (threadIdx.x == 0) stamp(TM_FIX_WAITED);
     const uint64_t nsegs = total_segs(G, W);
     const bool fast = nsegs > 0 && W.ctrl[1] != 0u;
-    if (fast && G.file_off == nullptr) return;
+    if (fast && G.file_off == nullptr) {
+        if (threadIdx.x == 0) stamp(TM_FIX_END);
+        return;
+    }
     if (threadIdx.x == 0) s_role = atomicAdd(W.ctrl + 3, 1u) + 1u;  // counter starts at ~0
     __syncthreads();
     const uint32_t role = s_role;

@@ -7,6 +7,6 @@ for v in ${VARIANTS:-A B C D}; do
   python - "$v" <<'PY'
 import json,sys
 l=json.loads(open(f"gpurun_out/b_{sys.argv[1]}.log").read().strip().splitlines()[-1])
-print(sys.argv[1], "step", l["ms_per_step_without_kernel_events"], "kspec", l["roofline"]["kernel_ms"], "frac", l["roofline"]["frac"], "segs", l["path"]["segments"], "fast", l["path"]["fast_path"])
+print(sys.argv[1], "step", l["ms_per_step"], "GBs", l["value"], "kspec", l["roofline"]["kernel_ms"], "frac", l["roofline"]["frac"], "segs", l["path"]["segments"], "fast", l["path"]["fast_path"])
 PY
 done

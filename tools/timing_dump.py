@@ -25,13 +25,18 @@ for _ in range(3):
     cdc.chunk_async(t, p, b, c, ws)
 st = cdc.stats(p, ws, 1, n, n)
 G = st["segments"]
-tm = torch.zeros(4 * G, dtype=torch.int64, device="cuda")
+tm = torch.zeros(8 + 4 * G, dtype=torch.int64, device="cuda")
+tm[[0, 2, 3, 5, 6]] = -1  # "first" stamps: atomicMin slots
 lib.cdc_debug_timing(tm.data_ptr())
 cdc.chunk_async(t, p, b, c, ws)
 torch.cuda.synchronize()
 lib.cdc_debug_timing(None)
-a = tm.cpu().numpy().reshape(G, 4)
+hdr = tm[:8].cpu().numpy().view(np.uint64).astype(np.float64)
+a = tm[8:].cpu().numpy().reshape(G, 4)
 t0 = a[:, 0].min()
+names = ["reset begin", "reset end", "spec begin", "spec waited", "spec end", "fix begin", "fix waited", "fix end"]
+print("launch stamps us rel. to first walker start:",
+      ", ".join(f"{k} {(v - t0) / 1e3:.2f}" if 0 < v < 2**63 else f"{k} -" for k, v in zip(names, hdr)))
 start = (a[:, 0] - t0) / 1e3
 walk = (a[:, 1] - a[:, 0]) / 1e3
 done = (a[:, 2] - t0) / 1e3
