@@ -40,7 +40,10 @@ constexpr int SPEC_WARPS = CDC_SPEC_WARPS;  // warps (segments) per CTA in k_spe
 #define CDC_SPEC_CTAS_PER_SM 1
 #endif
 constexpr int SPEC_CTAS_PER_SM = CDC_SPEC_CTAS_PER_SM;  // resident k_speculate CTAs per SM (smem-bound)
-constexpr int HEAD_KEEP = 16384;  // bytes of each segment head kept in L2 for the halo re-read
+#ifndef CDC_HEAD_KEEP
+#define CDC_HEAD_KEEP 16384
+#endif
+constexpr int HEAD_KEEP = CDC_HEAD_KEEP;  // bytes of each segment head kept in L2 for the halo re-read
 constexpr int RESOLVE_THREADS = 1024;
 
 // ------------------------------------------------------------------ workspace
@@ -216,6 +219,28 @@ __device__ __forceinline__ int list_lookup(const uint32_t *lst, uint64_t cap, co
 }
 
 // ------------------------------------------------------------------ K1 emit policy
+// Optional timing record (cdc_debug_timing): TM_STAMPS launch stamps
+// (globaltimer; min slots preset to ~0 by the caller, max slots to 0), then
+// TM_PER_SEG x u64 per segment {at start, at the end of the body walk (its
+// first boundary at or past the segment end), at the end of the walk, at the
+// end, smid | hcnt << 32}.
+__device__ unsigned long long *g_timing = nullptr;
+constexpr int TM_STAMPS = 8;
+constexpr int TM_PER_SEG = 5;
+enum : int { TM_RESET_BEGIN, TM_RESET_END, TM_SPEC_BEGIN, TM_SPEC_WAITED, TM_SPEC_END, TM_FIX_BEGIN,
+             TM_FIX_WAITED, TM_FIX_END };
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void stamp(int i) {  // one thread per CTA calls this
+    unsigned long long *tm = g_timing;
+    if (tm == nullptr) return;
+    const unsigned long long t = globaltimer();
+    if (i == TM_RESET_END || i == TM_SPEC_END || i == TM_FIX_END) atomicMax(tm + i, t);
+    else atomicMin(tm + i, t);
+}
 struct SpecEmit {
     const Geometry *G;
     const Work *W;
@@ -228,10 +253,14 @@ struct SpecEmit {
     int64_t cur_j;
     uint32_t cursor;
     bool published;
+    unsigned long long *tbody;  // diagnostics: where to stamp the end of the body walk (or null)
 
     __device__ void publish() {
         if (!published) {
-            if (lane_id() == 0) st_release_u64(pub, (unsigned long long)cnt);
+            if (lane_id() == 0) {
+                st_release_u64(pub, (unsigned long long)cnt);
+                if (tbody) *tbody = globaltimer();
+            }
             published = true;
         }
     }
@@ -272,26 +301,6 @@ struct SpecEmit {
     __device__ void exhausted(int64_t) { sj = SJ_UNSYNCED; }
 };
 
-// Optional timing record (cdc_debug_timing): TM_STAMPS launch stamps
-// (globaltimer; min slots preset to ~0 by the caller, max slots to 0), then
-// 4 x u64 per segment {at start, at the end of the walk, at the end,
-// smid | hcnt << 32}.
-__device__ unsigned long long *g_timing = nullptr;
-constexpr int TM_STAMPS = 8;
-enum : int { TM_RESET_BEGIN, TM_RESET_END, TM_SPEC_BEGIN, TM_SPEC_WAITED, TM_SPEC_END, TM_FIX_BEGIN,
-             TM_FIX_WAITED, TM_FIX_END };
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ void stamp(int i) {  // one thread per CTA calls this
-    unsigned long long *tm = g_timing;
-    if (tm == nullptr) return;
-    const unsigned long long t = globaltimer();
-    if (i == TM_RESET_END || i == TM_SPEC_END || i == TM_FIX_END) atomicMax(tm + i, t);
-    else atomicMin(tm + i, t);
-}
 __device__ __forceinline__ uint32_t smid() {
     uint32_t r;
     asm volatile("mov.u32 %0, %smid;" : "=r"(r));
@@ -507,7 +516,8 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     em.published = false;
     if (lane == 0) st_relaxed_u32(em.list, 0u);  // the speculative chain starts at the segment's first byte
     unsigned long long *tm = g_timing ? g_timing + TM_STAMPS : nullptr;
-    if (tm && lane == 0) tm[4 * g] = globaltimer();
+    em.tbody = tm ? tm + TM_PER_SEG * g + 1 : nullptr;
+    if (tm && lane == 0) tm[TM_PER_SEG * g] = globaltimer();
     const uint8_t *fbase = G.data + em.I.foff;
     int64_t read_end = (g == em.I.last) ? (int64_t)em.I.Lf
                                         : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
@@ -516,8 +526,8 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
     em.publish();
     if (tm && lane == 0) {
-        tm[4 * g + 1] = globaltimer();
-        tm[4 * g + 3] = smid() | ((unsigned long long)em.hcnt << 32);
+        tm[TM_PER_SEG * g + 2] = globaltimer();
+        tm[TM_PER_SEG * g + 4] = smid() | ((unsigned long long)em.hcnt << 32);
     }
 
     // ---- common case, fused resolve + write: the chain met the next segment's
@@ -576,7 +586,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
         if (g == em.I.first && i == 0) continue;  // the file's first start (0) is not a boundary
         if (q - 1 < cap) bounds[q - 1] = v;
     }
-    if (tm && lane == 0) tm[4 * g + 2] = globaltimer();
+    if (tm && lane == 0) tm[TM_PER_SEG * g + 3] = globaltimer();
     if (em.sj == SJ_LAST && lane == 0) {
         const uint64_t q = (uint64_t)(off + n) - 1;  // a file's last boundary is its length
         if (q < cap) bounds[q] = em.I.Lf;

@@ -78,6 +78,23 @@ def zipf_bytes(n: int, s: float = 1.1, seed: int = 1, rng: np.random.Generator |
     return out
 
 
+def saturation_edges(n: int, seed: int = 6, p: float = 1 / 700) -> np.ndarray:
+    """Bytes near both ends of the range: 255 and 0 each with probability p, the
+    rest from {1, 2, 253, 254}; half the bytes after a 255 are 254 and half
+    after a 0 are 1.  Exercises saturating extremes next to near-saturating
+    ones (test data for the kernels' saturation scan; no chunking logic)."""
+    rng = _rng(seed)
+    out = rng.choice(np.array([1, 2, 253, 254], dtype=np.uint8), size=n)
+    u = rng.random(n)
+    out[u < p] = 255
+    out[(u >= p) & (u < 2 * p)] = 0
+    if n > 1:
+        nxt = rng.random(n - 1) < 0.5
+        out[1:][(out[:-1] == 255) & nxt] = 254
+        out[1:][(out[:-1] == 0) & nxt] = 1
+    return out
+
+
 def versioned(base_size: int, n_snap: int, seed: int = 2, region: int = 64 << 10,
               zero_frac: float = 0.10, edit_frac: float = 0.01,
               run_lo: int = 1024, run_hi: int = 4096) -> list[np.ndarray]:

@@ -77,6 +77,8 @@ GENS = {
     "dec": lambda n, s: (255 - np.arange(n) % 256).astype(np.uint8),
     "runs": lambda n, s: synth.alternating(n, region=1 << 16, seed=s),
     "versioned": lambda n, s: synth.versioned(n, 1, seed=s, region=1 << 14)[1][:n],
+    "satedge": lambda n, s: synth.saturation_edges(n, s),
+    "satedge_dense": lambda n, s: synth.saturation_edges(n, s, p=1 / 40),
 }
 
 

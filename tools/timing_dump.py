@@ -25,26 +25,31 @@ for _ in range(3):
     cdc.chunk_async(t, p, b, c, ws)
 st = cdc.stats(p, ws, 1, n, n)
 G = st["segments"]
-tm = torch.zeros(8 + 4 * G, dtype=torch.int64, device="cuda")
+tm = torch.zeros(8 + 5 * G, dtype=torch.int64, device="cuda")
 tm[[0, 2, 3, 5, 6]] = -1  # "first" stamps: atomicMin slots
 lib.cdc_debug_timing(tm.data_ptr())
 cdc.chunk_async(t, p, b, c, ws)
 torch.cuda.synchronize()
 lib.cdc_debug_timing(None)
 hdr = tm[:8].cpu().numpy().view(np.uint64).astype(np.float64)
-a = tm[8:].cpu().numpy().reshape(G, 4)
+a = tm[8:].cpu().numpy().reshape(G, 5)
 t0 = a[:, 0].min()
 names = ["reset begin", "reset end", "spec begin", "spec waited", "spec end", "fix begin", "fix waited", "fix end"]
 print("launch stamps us rel. to first walker start:",
       ", ".join(f"{k} {(v - t0) / 1e3:.2f}" if 0 < v < 2**63 else f"{k} -" for k, v in zip(names, hdr)))
 start = (a[:, 0] - t0) / 1e3
-walk = (a[:, 1] - a[:, 0]) / 1e3
-done = (a[:, 2] - t0) / 1e3
-sm = a[:, 3] & 0xFFFFFFFF
-halo = a[:, 3] >> 32
+walk = (a[:, 2] - a[:, 0]) / 1e3
+body = np.where(a[:, 1] > 0, (a[:, 1] - a[:, 0]) / 1e3, walk)
+done = (a[:, 3] - t0) / 1e3
+sm = a[:, 4] & 0xFFFFFFFF
+halo = a[:, 4] >> 32
 print(st)
 print("start us: min %.1f max %.1f" % (start.min(), start.max()))
 print("walk us: min %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f mean %.1f" % (walk.min(), *np.percentile(walk, [10, 50, 90]), walk.max(), walk.mean()))
+print("body us: p10 %.1f p50 %.1f p90 %.1f max %.1f" % (*np.percentile(body, [10, 50, 90]), body.max()))
+hw = walk - body
+print("halo walk us: p50 %.1f p90 %.1f p99 %.1f max %.1f; per halo chunk us: mean %.2f" % (
+    *np.percentile(hw, [50, 90, 99]), hw.max(), hw.sum() / max(1, halo.sum())))
 print("walk end us (abs): p50 %.1f p90 %.1f max %.1f" % tuple(np.percentile(start + walk, [50, 90, 100])))
 print("done us (abs): p50 %.1f max %.1f" % (np.percentile(done, 50), done.max()))
 print("halo chunks: mean %.2f max %d" % (halo.mean(), halo.max()))
@@ -55,7 +60,7 @@ for s_ in np.argsort([-walk[sm == k].max() if (sm == k).any() else 0 for k in ra
 # correlation of walk time with halo length and with g
 print("corr(walk, halo) %.2f corr(walk, g) %.2f" % (np.corrcoef(walk, halo)[0, 1], np.corrcoef(walk, np.arange(G))[0, 1]))
 slow = np.argsort(-walk)[:10]
-print("slowest segs", slow.tolist(), walk[slow].round(1).tolist(), "halo", halo[slow].tolist(), "sm", sm[slow].tolist())
+print("slowest segs", slow.tolist(), walk[slow].round(1).tolist(), "body", body[slow].round(1).tolist(), "halo", halo[slow].tolist(), "sm", sm[slow].tolist())
 gs = int(np.argmax(start + walk))
 we = start + walk
 print("slowest walker g*=%d walk_end %.1f done %.1f" % (gs, we[gs], done[gs]))
