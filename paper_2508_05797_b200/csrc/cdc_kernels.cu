@@ -175,48 +175,86 @@ __device__ __forceinline__ int64_t seg_of_pos(const SegInfo &I, int64_t e, uint6
 
 // Published lists.  list(g) holds the chunk starts of segment g's speculative
 // chain that lie inside the segment (relative to its first byte, ascending);
-// its entries are reset to LIST_EMPTY before every call (one memset) and each
+// its entries are reset to LIST_EMPTY before every call (k_reset) and each
 // is written once with a single 32-bit store, so a reader sees every entry
 // either complete or empty.  pub(g) is PUB_OPEN until the walker has left its
 // segment; then it holds the final entry count (st.release after the entries).
 constexpr uint32_t LIST_EMPTY = 0xFFFFFFFFu;
 constexpr unsigned long long PUB_OPEN = ~0ull;
 
-// Warp-cooperative membership of r in list(j), scanning from a monotone
-// cursor: 1 = found (idx set), 0 = not a member, -1 = undecidable yet (an
-// entry the scan needs is not visible and the list is not known complete).
-__device__ __forceinline__ int list_lookup(const uint32_t *lst, uint64_t cap, const unsigned long long *pubp,
-                                           uint32_t r, uint32_t &cursor, uint32_t &idx) {
-    const int lane = lane_id();
-    while (cursor < cap) {
-        const uint64_t i = (uint64_t)cursor + lane;
-        const uint32_t v = i < cap ? ld_relaxed_u32(lst + i) : LIST_EMPTY;
-        const bool valid = v != LIST_EMPTY;
-        const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
-        const uint32_t gm = __ballot_sync(0xFFFFFFFFu, valid && v >= r);
-        const int fi = vm == 0xFFFFFFFFu ? 32 : __ffs(~vm) - 1;  // first empty entry
-        const int fg = gm ? __ffs(gm) - 1 : 32;                  // first entry >= r
-        if (fg < fi) {
-            const uint32_t vL = __shfl_sync(0xFFFFFFFFu, v, fg);
-            cursor += fg;
-            if (vL == r) {
-                idx = cursor;
-                return 1;
-            }
-            return 0;
-        }
-        if (fi < 32) {
-            // entries [cursor, cursor + fi) are all < r; the next one is empty
-            const unsigned long long pw = ld_acquire_u64(pubp);
-            const uint32_t at = cursor + fi;
-            cursor = at;
-            if (pw != PUB_OPEN && (uint64_t)pw <= at) return 0;  // the list ends before r
-            return -1;
-        }
-        cursor += 32;
+// Re-synchronisation probe of a walker's chain against the published lists:
+// warp-cooperative membership of boundary e in the list of the segment
+// holding it, scanning from a monotone cursor (boundaries come in increasing
+// order).  Returns 1 = found (idx set), 0 = not a member, -1 = undecidable yet
+// (an entry the scan needs is not visible and the list is not known
+// complete).  It caches the segment the last boundary fell in (its range, so
+// no division while e stays inside it) and one aligned window of 32 entries
+// of its list, one per lane (entries are written once, so a visible entry
+// never changes; a window with an empty entry in use is read again).
+struct ListProbe {
+    int64_t j;           // segment of the last boundary (-1: none yet)
+    int64_t lo, hi;      // its file-relative range [lo, hi)
+    uint32_t cursor;     // monotone cursor in list(j)
+    uint32_t wb;         // first entry index of the cached window (~0: none)
+    uint32_t wv;         // this lane's cached entry wb + lane
+
+    __device__ void reset() {
+        j = -1;
+        lo = hi = 0;
+        cursor = 0;
+        wb = ~0u;
     }
-    return 0;
-}
+    __device__ int probe(const Work &W, const SegInfo &I, int64_t e, int64_t &jo, uint32_t &idx) {
+        if (e < lo || e >= hi) {
+            int64_t pj;
+            j = seg_of_pos(I, e, 0, pj);
+            lo = pj;
+            const uint64_t n = I.last - I.first + 1;
+            const uint64_t k = (uint64_t)(j - (int64_t)I.first);
+            hi = k + 1 < n ? seg_start(k + 1, n, I.Lf) : (int64_t)I.Lf;
+            cursor = 0;
+            wb = ~0u;
+        }
+        jo = j;
+        const uint32_t *lst = W.list + (uint64_t)j * W.cap_list;
+        const uint64_t cap = W.cap_list;
+        const uint32_t r = (uint32_t)(e - lo);
+        const int lane = lane_id();
+        while (cursor < cap) {
+            const uint32_t B = cursor & ~31u;
+            const bool mine = (uint64_t)B + lane < cap;
+            if (B != wb || __any_sync(0xFFFFFFFFu, mine && wv == LIST_EMPTY)) {
+                wb = B;
+                wv = mine ? ld_relaxed_u32(lst + B + lane) : LIST_EMPTY;
+            }
+            const int off = (int)(cursor - B);
+            const bool inwin = lane >= off;
+            const bool valid = !inwin || wv != LIST_EMPTY;  // entries before the cursor are < r
+            const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
+            const uint32_t gm = __ballot_sync(0xFFFFFFFFu, inwin && valid && wv >= r);
+            const int fi = vm == 0xFFFFFFFFu ? 32 : __ffs(~vm) - 1;  // first empty entry
+            const int fg = gm ? __ffs(gm) - 1 : 32;                  // first entry >= r
+            if (fg < fi) {
+                const uint32_t vL = __shfl_sync(0xFFFFFFFFu, wv, fg);
+                cursor = B + (uint32_t)fg;
+                if (vL == r) {
+                    idx = cursor;
+                    return 1;
+                }
+                return 0;
+            }
+            if (fi < 32) {
+                const unsigned long long pw = ld_acquire_u64(W.pub + j);
+                const uint32_t at = B + (uint32_t)fi;
+                cursor = at;
+                if (pw != PUB_OPEN && (uint64_t)pw <= at) return 0;  // the list ends before r
+                return -1;
+            }
+            cursor = B + 32;
+        }
+        return 0;
+    }
+};
 
 // ------------------------------------------------------------------ K1 emit policy
 // Optional timing record (cdc_debug_timing): TM_STAMPS launch stamps
@@ -250,8 +288,7 @@ struct SpecEmit {
     uint32_t cnt, hcnt;
     int32_t sj;
     uint32_t sa, sb;
-    int64_t cur_j;
-    uint32_t cursor;
+    ListProbe lp;
     bool published;
     unsigned long long *tbody;  // diagnostics: where to stamp the end of the body walk (or null)
 
@@ -276,15 +313,9 @@ struct SpecEmit {
         if (lane == 0) halo[hcnt] = h;
         ++hcnt;
         // re-synchronisation: is e a start of the chain of the segment holding it?
-        int64_t pj;
-        const int64_t j = seg_of_pos(I, e, G->S, pj);
-        if (j != cur_j) {
-            cur_j = j;
-            cursor = 0;
-        }
+        int64_t j;
         uint32_t idx = 0;
-        const int r = list_lookup(W->list + (uint64_t)j * W->cap_list, W->cap_list, W->pub + j, (uint32_t)(e - pj),
-                                  cursor, idx);
+        const int r = lp.probe(*W, I, e, j, idx);
         if (r == 1) {
             sj = (int32_t)j;
             sa = hcnt - 1;
@@ -456,14 +487,12 @@ template <int ALGO>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
                                   uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused);
 
-// K1.  One warp per segment (CTAs take segment groups in ticket order).  The
-// last warp to finish tail-launches the k_fixup fix-up (device-side
-// launch, CUDA dynamic parallelism) when some segment was not normal; in the
-// common case the whole call is this kernel (plus the list-reset memset).
+// K1.  One warp per segment (CTAs take segment groups in ticket order).  In
+// the common case the fused look-back writes the output and k_fixup (launched
+// behind it with PDL) only checks that it did.
 template <int ALGO>
 __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate(Geometry G, Work W, uint64_t *bounds,
-                                                                  uint64_t cap, uint64_t *d_count, int fused,
-                                                                  int tail_fixup) {
+                                                                  uint64_t cap, uint64_t *d_count, int fused) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_ticket;
     const int warp = threadIdx.x >> 5;
@@ -479,19 +508,6 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
     if (g >= nsegs) return;
     speculate_segment<ALGO>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused);
     if (lane_id() == 0) stamp(TM_SPEC_END);
-    if (tail_fixup && lane_id() == 0) {
-        __threadfence();
-        const uint32_t old = atomicAdd(W.ctrl + 2, 1u);  // starts at ~0: old + 2 warps are done
-        if (old + 2u == (uint32_t)nsegs) {
-            __threadfence();
-            if (atomicOr(W.ctrl + 1, 0u) == 0u) {  // the fused fast path failed somewhere
-#ifdef CDC_TAIL_LAUNCH
-                k_fixup<ALGO><<<(unsigned)((nsegs + 31) / 32), RESOLVE_THREADS, FIX_SMEM,
-                                cudaStreamTailLaunch>>>(G, W, d_count, W.file_out, bounds, cap);
-#endif
-            }
-        }
-    }
 }
 
 template <int ALGO>
@@ -511,8 +527,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     em.hcnt = 0;
     em.sj = SJ_UNSYNCED;
     em.sa = em.sb = 0;
-    em.cur_j = -1;
-    em.cursor = 0;
+    em.lp.reset();
     em.published = false;
     if (lane == 0) st_relaxed_u32(em.list, 0u);  // the speculative chain starts at the segment's first byte
     unsigned long long *tm = g_timing ? g_timing + TM_STAMPS : nullptr;
@@ -609,20 +624,13 @@ struct WalkEmit {
     uint64_t n;       // entries written
     int32_t sj;
     uint32_t sb;
-    int64_t cur_j;
-    uint32_t cursor;
+    ListProbe lp;
     bool overflow;
 
     __device__ bool boundary(int64_t e) {
-        int64_t pj;
-        const int64_t j = seg_of_pos(I, e, G->S, pj);
-        if (j != cur_j) {
-            cur_j = j;
-            cursor = 0;
-        }
+        int64_t j;
         uint32_t idx = 0;
-        int r = list_lookup(W->list + (uint64_t)j * W->cap_list, W->cap_list, W->pub + j, (uint32_t)(e - pj), cursor,
-                            idx);
+        const int r = lp.probe(*W, I, e, j, idx);
         if (r == 1) {
             sj = (int32_t)j;
             sb = idx;
@@ -830,8 +838,7 @@ __device__ void resolve_block(const Geometry &G, Work &W, uint64_t *d_count, uin
                 em.n = 0;
                 em.sj = SJ_STREAM_END;
                 em.sb = 0;
-                em.cur_j = -1;
-                em.cursor = 0;
+                em.lp.reset();
                 em.overflow = false;
                 const uint32_t hc = W.hcnt[g];
                 const int64_t last = hc ? I.seg_end + (int64_t)W.halo[g * W.cap_halo + hc - 1]
@@ -887,8 +894,7 @@ __device__ void resolve_block(const Geometry &G, Work &W, uint64_t *d_count, uin
                         em.n = 0;
                         em.sj = SJ_STREAM_END;
                         em.sb = 0;
-                        em.cur_j = -1;
-                        em.cursor = 0;
+                        em.lp.reset();
                         em.overflow = false;
                         const uint32_t wc = W.wcnt[g];
                         const int64_t last = I.seg_end + (int64_t)W.pool[W.woff[g] + wc - 1];
@@ -1282,20 +1288,6 @@ bool sync_debug() {
         }                                                                      \
     } while (0)
 
-// CDC_TAIL_LAUNCH builds (-rdc=true -lcudadevrt) let k_speculate tail-launch the
-// fix-up kernels only when needed.  Measured on B200 the relocatable-device-code
-// build made k_speculate ~4 us slower than the two empty host launches cost, so
-// the default build launches k_fixup from the host (it exits at once
-// when the fused fast path succeeded).
-int tail_mode(bool batch) {
-#ifdef CDC_TAIL_LAUNCH
-    return batch ? 0 : 1;
-#else
-    (void)batch;
-    return 0;
-#endif
-}
-
 // CDC_FUSED=0 disables the fused look-back fast path (k_fixup always resolves)
 int fused_mode() {
     static int v = -1;
@@ -1509,24 +1501,14 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     const uint64_t blocks = (nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS;
     if (blocks > 0) {
         int fused = (P.cap_list + P.cap_halo < (1u << 23)) ? fused_mode() : 0;
-        int tmode = tail_mode(batch);
         CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_speculate<ALGO>), dim3((unsigned)blocks),
-                            dim3(cdc::SPEC_WARPS * 32), (size_t)spec_smem, st, G, W, d_bounds, cap, d_count, fused,
-                            tmode));
+                            dim3(cdc::SPEC_WARPS * 32), (size_t)spec_smem, st, G, W, d_bounds, cap, d_count, fused));
         CDC_KCHECK("k_speculate", st);
         ++launches;
         pc.used[1] = true;
     }
     mark(2);
-    // single stream with segments: k_speculate's last warp tail-launches the
-    // fix-up only when needed; batches (per-file offsets) and empty streams
-    // always run k_fixup from the host
-#ifdef CDC_TAIL_LAUNCH
-    const bool tail = !batch && total_len > 0;
-#else
-    const bool tail = false;
-#endif
-    if (!tail) {
+    {
         // a small grid: it exits at once in the common case; writers stride over segments otherwise
         const uint64_t fblocks = std::min<uint64_t>((nseg_ub + 31) / 32, FIX_BLOCKS);
         CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_fixup<ALGO>), dim3((unsigned)(fblocks ? fblocks : 1)),
