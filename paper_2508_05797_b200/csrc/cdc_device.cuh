@@ -124,7 +124,15 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 // stamps clock64, ET_ADD(i, v) adds the cycles since the stamp to bucket i.
 __device__ unsigned long long g_evt[16];
 #ifdef CDC_EVTIME
-#define ET_DECL long long et_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long et_t0 = clock64(), et_t1 = 0;
+#define ET_DECL long long et_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long et_t0 = clock64(), et_t1 = 0, et_h0 = 0, et_hs = 0;
+// halo phase (emitter past its segment end): bucket 7 = its stage transitions,
+// g_evt[9] = its stages, g_evt[10] = its cycles
+#define ET_HALO_STAGE(h, v)                          \
+    if (h) {                                         \
+        if (et_h0 == 0) et_h0 = v;                   \
+        et_acc[7] += clock64() - v;                  \
+        ++et_hs;                                     \
+    }
 #define ET_VAR(v) long long v;
 #define ET_BEGIN(v) v = clock64()
 #define ET_ADD(i, v) et_acc[i] += clock64() - v
@@ -132,8 +140,11 @@ __device__ unsigned long long g_evt[16];
     if ((threadIdx.x & 31) == 0) {                                      \
         for (int q = 0; q < 8; ++q) atomicAdd(&g_evt[q], (unsigned long long)et_acc[q]); \
         atomicAdd(&g_evt[8], (unsigned long long)(clock64() - et_t0));  \
+        atomicAdd(&g_evt[9], (unsigned long long)et_hs);                \
+        if (et_h0) atomicAdd(&g_evt[10], (unsigned long long)(clock64() - et_h0)); \
     }
 #else
+#define ET_HALO_STAGE(h, v)
 #define ET_DECL
 #define ET_VAR(v)
 #define ET_BEGIN(v)
@@ -623,6 +634,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
             else hor = FAR;
             return false;
         };
+        ET_HALO_STAGE(emit.in_halo(), et_t1);
         ET_ADD(0, et_t1);  // stage transition: wait + setup
         while (cr < endr) {
             ET_VAR(eit)

@@ -328,6 +328,7 @@ struct SpecEmit {
         }
         return false;
     }
+    __device__ bool in_halo() const { return published; }  // diagnostics (CDC_EVTIME)
     __device__ void end() { sj = (I.seg_end >= (int64_t)I.Lf) ? SJ_LAST : SJ_STREAM_END; }
     __device__ void exhausted(int64_t) { sj = SJ_UNSYNCED; }
 };
@@ -647,6 +648,7 @@ struct WalkEmit {
         ++n;
         return false;
     }
+    __device__ bool in_halo() const { return false; }
     __device__ void end() { sj = SJ_STREAM_END; }
     __device__ void exhausted(int64_t) { sj = SJ_STREAM_END; }
 };
@@ -1090,6 +1092,7 @@ struct ChainEmit {
         return e >= stop;
     }
     // the chain's last chunk ends at len: record len as its final position
+    __device__ bool in_halo() const { return false; }
     __device__ void end() {
         if (lane_id() == 0 && n < cap) out[n] = (uint64_t)len;
         ++n;

@@ -20,10 +20,15 @@ cdc.chunk_async(t, p, b, c, ws)
 torch.cuda.synchronize()
 lib.cdc_debug_evtime(ev)
 names = ["stage transition (wait+setup)", "find_block", "record", "boundary event", "pending",
-         "iter: saturated (whole iteration)", "iter: no-hit find (whole iteration, incl. find)", "", "walk total"]
+         "iter: saturated (whole iteration)", "iter: no-hit find (whole iteration, incl. find)",
+         "  of which halo stage transitions", "walk total"]
 tot = ev[8]
 chunks = int(c.item())
 for i, k in enumerate(names):
     if k:
         print("%-32s %14d cycles  %5.1f%%  per chunk %8.0f" % (k, ev[i], 100.0 * ev[i] / tot, ev[i] / chunks))
-print("other (loop control, sat jumps, etc.) %5.1f%%" % (100.0 * (tot - sum(ev[i] for i in range(8))) / tot))
+print("other (loop control, sat jumps, etc.) %5.1f%%" % (100.0 * (tot - sum(ev[i] for i in range(7))) / tot))
+hs, hc = ev[9], ev[10]
+if hs:
+    print("halo phase: %d stages, %d cycles (%.1f%% of walk); per halo stage %.0f cycles, of which transition %.0f"
+          % (hs, hc, 100.0 * hc / tot, hc / hs, ev[7] / hs))
