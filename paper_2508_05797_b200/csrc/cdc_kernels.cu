@@ -41,7 +41,7 @@ constexpr int SPEC_WARPS = CDC_SPEC_WARPS;  // warps (segments) per CTA in k_spe
 #endif
 constexpr int SPEC_CTAS_PER_SM = CDC_SPEC_CTAS_PER_SM;  // resident k_speculate CTAs per SM (smem-bound)
 #ifndef CDC_HEAD_KEEP
-#define CDC_HEAD_KEEP 16384
+#define CDC_HEAD_KEEP 12288
 #endif
 constexpr int HEAD_KEEP = CDC_HEAD_KEEP;  // bytes of each segment head kept in L2 for the halo re-read
 constexpr int RESOLVE_THREADS = 1024;
