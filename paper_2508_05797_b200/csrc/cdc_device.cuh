@@ -92,15 +92,6 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-// 1-D bulk copy global -> shared, completion signalled on an mbarrier (TMA; SASS UBLKCP).
-__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
-                                            uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
-        "%4;" ::"r"(smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
-        : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -285,13 +276,6 @@ __device__ __forceinline__ int locate(const Blk &k, uint32_t bal, int rlo, int r
     const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, hit);
     return L * 16 + __ffs(b2) - 1;
 }
-// byte at block-relative index r (uniform across the warp)
-__device__ __forceinline__ uint32_t byte_at(const Blk &k, int r) {
-    const int q = (r >> 2) & 3;
-    const uint32_t wd = q == 0 ? k.v.x : (q == 1 ? k.v.y : (q == 2 ? k.v.z : k.v.w));
-    const uint32_t x = __shfl_sync(0xFFFFFFFFu, wd, r >> 4);
-    return (x >> (8 * (r & 3))) & 0xFFu;
-}
 
 // ---------------------------------------------------------------- warp ring
 struct WarpRing {
@@ -340,34 +324,6 @@ __device__ __forceinline__ uint32_t block_lane_ext(const uint8_t *sp, int Bk, in
     return vext16<MAX>(r);
 }
 
-// Extreme Byte Search (§4.1) of the stage bytes [lo, hi): per-lane extreme
-// (the tree's leaves; the caller's warp reduction is its root).  Whole blocks
-// fold into two u16x2 accumulators, 8 instructions per lane per 512 bytes.
-template <bool MAX>
-__device__ __forceinline__ uint32_t stage_lane_ext(const uint8_t *sp, int lo, int hi) {
-    uint32_t acc = neutral<MAX>();
-    if (lo >= hi) return acc;
-    int Bk = lo & ~(BLK - 1);
-    bool has;
-    uint4 v;
-    if (lo != Bk || hi < Bk + BLK) {  // partial head block
-        acc = block_lane_ext<MAX>(sp, Bk, lo, hi < Bk + BLK ? hi : Bk + BLK, has, v);
-        Bk += BLK;
-    }
-    uint32_t ah = MAX ? 0u : 0xFFFFFFFFu, al = ah;
-#pragma unroll 2
-    for (; Bk + BLK <= hi; Bk += BLK) {
-        const uint4 u = *reinterpret_cast<const uint4 *>(sp + Bk + lane_id() * 16);
-        ah = ext3<MAX>(ah, u.x, u.y);
-        ah = ext3<MAX>(ah, u.z, u.w);
-        al = ext3<MAX>(al, u.x << 8, u.y << 8);
-        al = ext3<MAX>(al, u.z << 8, u.w << 8);
-    }
-    const uint32_t m = ext3<MAX>(ah, al, al);
-    acc = ext2<MAX>(acc, ext2<MAX>(m >> 24, (m >> 8) & 0xFFu));
-    if (Bk < hi) acc = ext2<MAX>(acc, block_lane_ext<MAX>(sp, Bk, Bk, hi, has, v));  // partial tail block
-    return acc;
-}
 
 // RAM window (Extreme Byte Search, §4.1) with early saturation: folds the
 // per-lane max of the stage bytes [lo, hi) into acc, and stops as soon as some
@@ -512,7 +468,7 @@ __device__ __forceinline__ int stage_locate(const uint8_t *sp, int Bk, uint32_t 
 // Inside a stage every position is an int offset from the stage's first byte
 // (horizons beyond the stage clamp to FAR); the chain state between events is
 // kept as 64-bit stream positions.  Between events the walker runs one of
-// three tight loops: the RAM window's Extreme Byte Search (stage_lane_ext), a
+// three tight loops: the RAM window's Extreme Byte Search (stage_window_max), a
 // block-level Range Scan for the next event (stage_find_block), or -- for an
 // AE target no byte can beat -- a direct jump to its deadline.
 template <int ALGO, class Emit>

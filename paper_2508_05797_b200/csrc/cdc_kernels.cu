@@ -151,14 +151,8 @@ __device__ __forceinline__ SegInfo seg_info(const Geometry &G, const Work &W, ui
     I.first = a;
     I.last = b - 1;
     file_bounds(G, I.f, I.foff, I.Lf);
-#ifdef CDC_OLD_GEOM
-    I.p = (int64_t)((g - a) * G.S);
-    const int64_t e = I.p + (int64_t)G.S;
-    I.seg_end = (g == I.last || e > (int64_t)I.Lf) ? (int64_t)I.Lf : e;
-#else
     I.p = seg_start(g - a, b - a, I.Lf);
     I.seg_end = seg_start(g - a + 1, b - a, I.Lf);
-#endif
     return I;
 }
 
@@ -357,7 +351,7 @@ __global__ void __launch_bounds__(256) k_reset(uint4 *p, uint64_t n16) {
 }
 
 // Decoupled look-back words: the top two bits say what the low 62 bits (a
-// signed value) hold.  The memset leaves every word ~0 = not ready.
+// signed value) hold.  k_reset leaves every word ~0 = not ready.
 constexpr unsigned long long ST_AGG = 1ull << 62;   // a_g = (cnt + tail) - sb of this segment
 constexpr unsigned long long ST_MASK = 3ull << 62;
 __device__ __forceinline__ int64_t st_value(unsigned long long w) {
@@ -392,12 +386,12 @@ constexpr int LB_GROUP = 32;
 // look-back waits sleep (exponential backoff) instead of polling hard: waiting
 // warps share their SM with walkers that are still running
 constexpr uint32_t SLEEP0 = CDC_SLEEP0, SLEEPMAX = CDC_SLEEPMAX;
-constexpr uint64_t LB_MAX_SEGS = 32768;  // beyond this the k_resolve scan is used
+constexpr uint64_t LB_MAX_SEGS = 32768;  // beyond this k_fixup's resolver splices the chains
 
 // all 32 lanes
 // Group words: one 64-bit atomic accumulator per group of 32 segments holding
 // (arrivals << 48) + sum of (a + LB_BIAS) over the arrived segments.  The
-// memset leaves ~0, so the accumulated value is the word + 1.  A group is
+// reset leaves ~0, so the accumulated value is the word + 1.  A group is
 // complete when its arrival count equals its size; its sum is then
 // low48 - size * LB_BIAS.  (|a| < 2^24: a = cnt + tail - sb, each bounded by a
 // segment's list or halo capacity.)
@@ -548,7 +542,6 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
 
     // ---- common case, fused resolve + write: the chain met the next segment's
     //      chain (or ended the file); anything else defers to k_fixup
-    const int fused_dbg = fused;  // debugging knob: 2 = skip the writes, 3 = skip the look-back
     fused = fused && nsegs <= LB_MAX_SEGS;
     const bool normal = fused && (em.sj == SJ_LAST || em.sj == (int32_t)(g + 1));
     const uint32_t tail = em.sj == SJ_LAST ? 0u : em.sa;
@@ -567,11 +560,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     // global round trip (falls back to the global lists when they do not fit)
     uint32_t *stg = reinterpret_cast<uint32_t *>(wbase);
     const uint32_t nst = em.cnt + tail;
-#ifdef CDC_NO_STAGE
-    const bool staged = false;
-#else
     const bool staged = nst <= (uint32_t)(RING_BYTES / 4);
-#endif
     if (fused && normal && staged) {
         const uint32_t hoff = (uint32_t)(em.I.seg_end - em.I.p);
         for (uint32_t i = lane; i < nst; i += 32)
@@ -579,10 +568,10 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     }
     if (fused) publish_agg(W, g, nsegs, a, sb);
     pdl_trigger();  // k_fixup may launch; it waits for this grid's completion
-    if (!fused || fused_dbg == 3) return;
+    if (!fused) return;
     uint32_t entry = 0;
     const int64_t excl = g == 0 ? 0 : lookback(W, g, entry);
-    if (!normal || fused_dbg == 2) return;
+    if (!normal) return;
     // entry(g) = sb(g-1), carried in segment g-1's status word
     if (g == em.I.first) entry = 0;
     const int64_t off = excl + entry;                     // output index of list[entry]
@@ -940,7 +929,7 @@ __device__ void resolve_block(const Geometry &G, Work &W, uint64_t *d_count, uin
         }
         __syncthreads();
     }
-    if (tid == 0) W.misc[4] = exc ? 1u : 0u;  // k_write: skipped / wcnt are valid only if set
+    if (tid == 0) W.misc[4] = exc ? 1u : 0u;  // the writers: skipped / wcnt are valid only if set
 
     // 5. per-segment output counts (RPT consecutive segments per thread) and their exclusive scan
     if (tid == 0) s_carry = 0;
@@ -1291,12 +1280,13 @@ bool sync_debug() {
         }                                                                      \
     } while (0)
 
-// CDC_FUSED=0 disables the fused look-back fast path (k_fixup always resolves)
+// CDC_FUSED=0 disables the fused look-back fast path (k_fixup always resolves;
+// a debugging and testing knob)
 int fused_mode() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("CDC_FUSED");
-        v = (e && e[0] >= '0' && e[0] <= '9') ? e[0] - '0' : 1;
+        v = (e && e[0] == '0') ? 0 : 1;
     }
     return v;
 }
@@ -1387,7 +1377,7 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     P.exc_cap = P.max_segs;
     const uint64_t G = P.max_segs;
     size_t sz[] = {
-        G * P.cap_list * 4,  // 0 list   } reset to 0xFF by one memset per call
+        G * P.cap_list * 4,  // 0 list   } reset to 0xFF by k_reset at every call
         G * 16 + 64 + (G / 32 + 1) * 12,  // 1 pub, status, ctrl, grp, gcnt }
         G * P.cap_halo * 4,  // 2 halo
         G * 4,               // 3 cnt
