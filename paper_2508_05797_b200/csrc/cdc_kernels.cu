@@ -487,7 +487,8 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
 // behind it with PDL) only checks that it did.
 template <int ALGO>
 __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate(Geometry G, Work W, uint64_t *bounds,
-                                                                  uint64_t cap, uint64_t *d_count, int fused) {
+                                                                  uint64_t cap, uint64_t *d_count, int fused,
+                                                                  int spw) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_ticket;
     const int warp = threadIdx.x >> 5;
@@ -498,9 +499,11 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
         s_ticket = atomicAdd(W.ctrl, 1u) + 1u;  // counter starts at ~0
     }
     __syncthreads();
-    const uint64_t g = (uint64_t)s_ticket * SPEC_WARPS + warp;
+    // spw segments per CTA (contiguous, so every predecessor is in this or an
+    // earlier ticket); fewer than SPEC_WARPS spread a small input over the SMs
+    const uint64_t g = (uint64_t)s_ticket * spw + warp;
     const uint64_t nsegs = total_segs(G, W);
-    if (g >= nsegs) return;
+    if (warp >= spw || g >= nsegs) return;
     speculate_segment<ALGO>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused);
     if (lane_id() == 0) stamp(TM_SPEC_END);
 }
@@ -1491,11 +1494,16 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     ++launches;
     mark(1);
     const uint64_t nseg_ub = P.max_segs;
-    const uint64_t blocks = (nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS;
+    // segments per CTA: SPEC_WARPS, or fewer when the input has fewer segments
+    // than walkers fit on the GPU (one walker per SM for a small stream)
+    const uint64_t nsm = (uint64_t)num_sms();
+    const int spw = (int)std::min<uint64_t>(std::max<uint64_t>((nseg_ub + nsm - 1) / nsm, 1), cdc::SPEC_WARPS);
+    const uint64_t blocks = (nseg_ub + spw - 1) / spw;
     if (blocks > 0) {
         int fused = (P.cap_list + P.cap_halo < (1u << 23)) ? fused_mode() : 0;
         CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_speculate<ALGO>), dim3((unsigned)blocks),
-                            dim3(cdc::SPEC_WARPS * 32), (size_t)spec_smem, st, G, W, d_bounds, cap, d_count, fused));
+                            dim3(cdc::SPEC_WARPS * 32), (size_t)spec_smem, st, G, W, d_bounds, cap, d_count, fused,
+                            spw));
         CDC_KCHECK("k_speculate", st);
         ++launches;
         pc.used[1] = true;

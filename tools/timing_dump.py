@@ -10,7 +10,7 @@ import synth  # noqa: E402
 import paper_2508_05797_b200 as cdc  # noqa: E402
 from paper_2508_05797_b200._lib import lib  # noqa: E402
 
-n = 256 << 20
+n = int(os.environ.get("N", 256 << 20))
 algo = os.environ.get("ALGO", "ae_max")
 avg = int(os.environ.get("AVG", "4096"))
 seg = int(os.environ.get("SEG", "0"))
