@@ -18,7 +18,7 @@ CMPS = {"gt": 0, "geq": 1, "lt": 2, "leq": 3, "eq": 4}
 
 __all__ = [
     "CdcError", "ALGOS", "params", "window_for_avg", "max_boundaries", "workspace_size",
-    "chunk_async", "chunk", "chunk_batch", "chunk_host", "chain",
+    "chunk_async", "chunk", "chunk_batch", "chunk_batch_async", "chunk_host", "chain",
     "extreme_byte_search", "range_scan", "first_common", "last_launch_count", "abi_version",
     "profile_enable", "profile_collect", "KERNELS", "stats", "plan_info", "segment_starts",
 ]
@@ -143,6 +143,16 @@ def chunk(data: torch.Tensor, p: cdc_params, stream=None) -> torch.Tensor:
     if m > cap:
         raise CdcError(f"boundary count {m} exceeds capacity {cap}")
     return bounds[:m]
+
+
+def chunk_batch_async(data: torch.Tensor, file_offsets: torch.Tensor, total_len: int, max_len: int, p: cdc_params,
+                      bounds: torch.Tensor, bound_offsets: torch.Tensor, count: torch.Tensor, workspace: torch.Tensor,
+                      stream=None) -> None:
+    """cdc_chunk_batch on preallocated device buffers (file_offsets: int64[nfiles+1] on the device; no
+    synchronisation).  total_len and max_len are the batch's byte count and largest file."""
+    check(lib.cdc_chunk_batch(ctypes.byref(p), data.data_ptr(), file_offsets.data_ptr(), file_offsets.numel() - 1,
+                              total_len, max_len, bounds.data_ptr(), bounds.numel(), bound_offsets.data_ptr(),
+                              count.data_ptr(), workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
 
 
 def chunk_batch(data: torch.Tensor, file_offsets, p: cdc_params, stream=None):

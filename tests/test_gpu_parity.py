@@ -172,6 +172,16 @@ def test_config3_many_files(cdc):
     got, bo = cdc.chunk_batch(_dev(data), offs, p)
     assert (bo.cpu().numpy() == exp_bo).all()
     assert (got.cpu().numpy().astype(np.uint64) == exp).all()
+    # the same call on preallocated device buffers, twice with one workspace
+    total, max_len = int(offs[-1]), int(np.diff(offs).max())
+    b = torch.full((exp.size + 8,), -1, dtype=torch.int64, device="cuda")
+    bo2 = torch.zeros(offs.size, dtype=torch.int64, device="cuda")
+    c = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(cdc.workspace_size(p, offs.size - 1, total, max_len), dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        cdc.chunk_batch_async(_dev(data), _dev(offs), total, max_len, p, b, bo2, c, ws)
+        assert int(c.item()) == exp.size and (bo2.cpu().numpy() == exp_bo).all()
+        assert (b[:exp.size].cpu().numpy().astype(np.uint64) == exp).all()
 
 
 @pytest.mark.parametrize("algo", ["ae_max", "ram"])

@@ -50,27 +50,51 @@ if not sel or "c4" in sel:
     run("c4-shape alternating 1GiB", synth.alternating(1 << 30, region=256 << 20, seed=5), "ram", 8192, reps=3)
 
 
-def run_batch(name, data_np, offs, algo, avg, reps=3):
+def run_batch(name, data_np, offs, algo, avg, reps=5):
+    """cdc_chunk_batch on preallocated device buffers (the host-side setup of
+    api.chunk_batch is outside the timed region)."""
     t = torch.from_numpy(data_np).cuda()
     p = cdc.params(algo, avg_size=avg)
+    sizes = np.diff(offs)
+    total, max_len = int(sizes.sum()), int(sizes.max())
+    od = torch.from_numpy(np.asarray(offs, dtype=np.int64)).cuda()
+    cap = total // (p.window + 1) + len(offs)
+    b = torch.empty(cap, dtype=torch.int64, device="cuda")
+    bo = torch.zeros(len(offs), dtype=torch.int64, device="cuda")
+    c = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(cdc.workspace_size(p, len(offs) - 1, total, max_len), dtype=torch.uint8, device="cuda")
     for _ in range(2):
-        cdc.chunk_batch(t, offs, p)
+        cdc.chunk_batch_async(t, od, total, max_len, p, b, bo, c, ws)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        b, bo = cdc.chunk_batch(t, offs, p)
+        cdc.chunk_batch_async(t, od, total, max_len, p, b, bo, c, ws)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    print("%-28s %-6s %5d  %8.3f ms  %8.1f GB/s  files %d chunks %d (includes host-side setup per call)" % (
-        name, algo, avg, ms, t.numel() / ms / 1e6, len(offs) - 1, int(bo[-1])), flush=True)
+    st = cdc.stats(p, ws, len(offs) - 1, total, max_len)
+    print("%-28s %-6s %5d  %8.3f ms  %8.1f GB/s  files %d chunks %d  %s" % (
+        name, algo, avg, ms, total / ms / 1e6, len(offs) - 1, int(c.item()),
+        {k: st[k] for k in ("segments", "fast_path", "synced", "skipped_or_end", "halo_chunks")}), flush=True)
 
 
+if "c2" in sel:  # configs[2]: the 1 GiB base and its last snapshot, AE and RAM at 4/8/16 KiB
+    snaps = synth.versioned(1 << 30, 9, seed=2)
+    for name, d in (("c2 versioned base 1GiB", snaps[0]), ("c2 versioned snap9 1GiB", snaps[-1])):
+        for algo in ("ae_max", "ram"):
+            for avg in (4096, 8192, 16384):
+                run(name, d, algo, avg, reps=3)
+    del snaps
+if "c4full" in sel:  # configs[4], one GPU's 8 GiB share of the 64 GiB stream
+    d = synth.alternating(8 << 30, region=256 << 20, seed=5)
+    run("c4 alternating 8GiB (1/8)", d, "ram", 8192, reps=3)
+    run("c4 alternating 8GiB (1/8)", d, "ae_max", 8192, reps=3)
+    del d
 if "c4big" in sel:
     d = synth.alternating(4 << 30, region=256 << 20, seed=5)
     run("c4-shape alternating 4GiB", d, "ram", 8192, reps=3)
     run("c4-shape alternating 4GiB", d, "ae_max", 8192, reps=3)
-if "c3" in sel:
-    data, offs = synth.many_files(25000, seed=3)
-    run_batch("c3 many files (25k)", data, offs, "ram", 8192)
+if "c3" in sel:  # configs[3], one GPU's share at 8 GPUs
+    data, offs = synth.many_files(12500, seed=3)
+    run_batch("c3 many files (12.5k)", data, offs, "ram", 8192)
