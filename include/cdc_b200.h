@@ -218,8 +218,9 @@ int cdc_profile_query(int *done);
  * Diagnostics of the last call that used workspace d_workspace (same params
  * and sizes as that call): synchronises `stream` and writes to stats[8]:
  *   [0] segments G, [1] segment bytes S, [2] halo cap bytes,
- *   [3] 1 if the fused look-back fast path produced the output (0: k_fixup's
- *       resolver and fix-up walkers ran), [4] segments whose chain met the
+ *   [3] 1 if the fused look-back fast path produced the output, 2 if the
+ *       transfer tables did (saturated streams), 0 if k_fixup's resolver and
+ *       fix-up walkers ran, [4] segments whose chain met the
  *       next segment's chain, [5] segments whose halo walk gave up or was
  *       undecided, [6] segments whose chain skipped a later segment or reached
  *       the stream end from a non-final segment, [7] total halo chunks.

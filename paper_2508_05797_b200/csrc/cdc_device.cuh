@@ -97,6 +97,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -446,6 +454,24 @@ __device__ __forceinline__ int stage_locate(const uint8_t *sp, int Bk, uint32_t 
     const int pos = base + j;
     const bool hit = lane_id() < 16 && pos >= lo && pos < hi && cmp_holds<CMP>(sp[pos], target);
     return base + __ffs(__ballot_sync(0xFFFFFFFFu, hit)) - 1;
+}
+
+// Saturating-byte masks (transfer tables, cdc_kernels.cu).  Exact per-byte
+// test for the saturating value (255 for MAX, 0 for MIN): a byte of t is zero
+// iff bit 7 of ((t & 0x7F..7F) + 0x7F..7F) | t is clear (no carry crosses a
+// byte).  The four flags of a word gather into 4 bits with one multiply (bits
+// 0, 8, 16, 24 -> 21..24; all partial products are distinct bits).
+template <bool MAX>
+__device__ __forceinline__ uint32_t sat_nibble(uint32_t x) {
+    const uint32_t t = MAX ? ~x : x;
+    const uint32_t z = ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t | 0x7F7F7F7Fu);  // 0x80 per zero byte of t
+    return (((z >> 7) * 0x00204081u) >> 21) & 0xFu;
+}
+// bit i set iff byte i of a lane's 16-byte vector is the saturating value
+template <bool MAX>
+__device__ __forceinline__ uint32_t sat_mask16(const uint4 &v) {
+    return sat_nibble<MAX>(v.x) | (sat_nibble<MAX>(v.y) << 4) | (sat_nibble<MAX>(v.z) << 8) |
+           (sat_nibble<MAX>(v.w) << 12);
 }
 
 // ---------------------------------------------------------------- chain engine

@@ -56,7 +56,7 @@ struct Work {
     unsigned long long *status;  // look-back words (ST_* flag | 62-bit signed value), reset to ~0
     uint32_t *ctrl;              // [0] CTA ticket counter, [1] fast path valid (~0) / failed (0); reset to ~0
     unsigned long long *grp;     // look-back group sums (reset to ~0)
-    uint32_t *gcnt;              // look-back group arrival counters (reset to ~0)
+    uint32_t *tblk;              // T-mode: per block of 32 segments, tables published (reset to ~0)
     int32_t *sj;                 // sync target segment, or SJ_* code
     uint32_t *sa, *sb;           // halo entries before the sync point; its index in list(sj)
     uint32_t *entry, *tail, *wcnt, *jump_entry;
@@ -73,10 +73,19 @@ struct Work {
     uint32_t *seg_file;          // G: file of each segment (batch)
     uint64_t *file_out;          // nfiles+1 (single stream: internal)
     uint32_t *misc;              // [0] G, [1] n_exc, [2] n_ranges, [3] overflow flags
+    // transfer tables (T-mode, saturated streams): per segment TK candidates
+    uint32_t *tl;                // G x TK link: candidate k of g -> candidate of g+1 (T_END, T_BAD)
+    uint32_t *tn;                // G x TK chain starts of candidate k inside the segment
+    uint32_t *tk;                // G: number of candidates
+    uint32_t *tp, *tq;           // G x TK: for entry k of the segment's block, its entry candidate and
+                                 // the chain starts in the block before it
+    uint32_t *tbc, *tbs;         // NB x TK: block tables (entry -> next block's entry, starts inside)
+    uint32_t *tbe;               // NB: the true chain's entry of each block (the scan)
+    uint64_t *tbo;               // NB: its output index
     uint64_t cap_list, cap_halo, pool_cap, max_segs, exc_cap, poolb_cap;
 };
 
-enum : int32_t { SJ_UNSYNCED = -1, SJ_STREAM_END = -2, SJ_LAST = -3 };
+enum : int32_t { SJ_UNSYNCED = -1, SJ_STREAM_END = -2, SJ_LAST = -3, SJ_TABLE = -4 };
 
 // dynamic shared memory follows the kernel's static shared variables: round the
 // ring up to 128 bytes (TMA destinations need 16, LDS.128 16; launches add 128)
@@ -93,6 +102,7 @@ struct Geometry {
     uint64_t Hmax;   // halo cap
     uint32_t w;
     uint64_t max_size;
+    int tmode;       // walkers may try transfer tables (single stream, one co-resident wave)
 };
 
 __device__ __forceinline__ void file_bounds(const Geometry &G, uint64_t f, uint64_t &off, uint64_t &len) {
@@ -284,6 +294,7 @@ struct SpecEmit {
     uint32_t sa, sb;
     ListProbe lp;
     bool published;
+    int tflag;                  // T-mode: 1 = stop at the first unsynced halo boundary, 2 = stopped there
     unsigned long long *tbody;  // diagnostics: where to stamp the end of the body walk (or null)
 
     __device__ void publish() {
@@ -318,6 +329,10 @@ struct SpecEmit {
         }
         if ((uint64_t)h >= G->Hmax) {
             sj = SJ_UNSYNCED;
+            return true;
+        }
+        if (tflag == 1) {  // T-mode: the tables may make the rest of the halo unnecessary
+            tflag = 2;
             return true;
         }
         return false;
@@ -508,6 +523,433 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
     if (lane_id() == 0) stamp(TM_SPEC_END);
 }
 
+// ------------------------------------------------------------------ T-mode: transfer tables
+// (DESIGN.md §6).  On saturating data (uniform bytes at w >> 256) chains that
+// start at different offsets meet only after ~(w / 362)^2 chunks, so halo
+// walks get long.  There a chunk step depends only on the positions of the
+// saturating bytes (255 for RAM and AE-Max, 0 for AE-Min):
+//   RAM (§2.1.2): the window [x, x+w) holds a saturating byte, so its maximum
+//     is saturated and the chunk ends after the first saturating byte in
+//     [x+w, limit), else at limit;
+//   AE: the first saturating byte q <= x+w is the target no byte beats (every
+//     earlier record is beaten within w), so the chunk ends at q+w+1, or at
+//     limit when q+w >= limit; if x+w >= limit it ends at limit.
+// A saturated chain that enters segment g starts at one of few candidates
+// (RAM: P+1 for a saturating position P in [p_g - 1, N(p_g + w - 1)]; AE:
+// q+w+1 for q in [p_g - w - 1, N(p_g - 1)], N = next saturating position).
+// After its body walk, walker g indexes the saturating bytes of
+// [p_g - w - 1, seg_end + max_size + 1) in its idle ring, walks every
+// candidate's chain in index space (one lane each) and publishes, per
+// candidate, the number of chain starts inside the segment and the candidate
+// of segment g+1 its chain enters.  One warp then scans the tables with
+// shuffles, and every walker writes its own part of the true chain: no halo
+// walk.  Any step that is not saturated, any exit that is not a candidate,
+// or any segment that is not dense makes the whole call fall back to the
+// halo walks (the tables are tried only for a single stream whose grid is one
+// co-resident wave, with a timeout).
+constexpr int TK = 128;                      // candidates per segment, 4 per lane
+constexpr uint32_t T_END = 0xFFFFFFFEu;      // link: the chain reached the stream end
+constexpr uint32_t T_BAD = 0xFFFFFFFFu;      // link: not resolvable in index space
+constexpr uint32_t T_DENSE = 8;              // saturating bytes per window a segment needs
+constexpr uint32_t T_IDX_CAP = (uint32_t)(RING_BYTES / 4);
+constexpr unsigned long long T_TIMEOUT_NS = 2000000ull;  // the scanner gives up after 2 ms
+// control words (ctrl[], reset to ~0 by k_reset): 6 block composers and walker
+// 0 arrived, 7 all-T (~0 yes, 0 no), 8 verdict (~0 pending, 1 tables, 0 fall
+// back), 9 and 10 walker 0's entry candidate of segment 1 and its start count
+constexpr int T_ARRIVE = 6, T_ALL = 7, T_SCAN = 8, T_E1 = 9, T_N0 = 10;
+
+__device__ __forceinline__ void t_fail(Work &W) {
+    if (ld_relaxed_u32(W.ctrl + T_ALL) != 0u) atomicAnd(W.ctrl + T_ALL, 0u);
+}
+__device__ __forceinline__ bool t_alive(const Work &W) { return ld_relaxed_u32(W.ctrl + T_ALL) != 0u; }
+
+// index of the saturating bytes of the file positions [lo, hi): ascending
+// offsets from lo into ix; returns the count, or cap + 1 when they do not fit
+template <bool MAX>
+__device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, uint32_t *ix, uint32_t cap) {
+    const int lane = lane_id();
+    const uintptr_t fb = reinterpret_cast<uintptr_t>(fbase);
+    const uintptr_t a0 = (fb + (uintptr_t)lo) & ~(uintptr_t)15;
+    const uintptr_t a1 = fb + (uintptr_t)hi;
+    uint32_t n = 0;
+    for (uintptr_t a = a0; a < a1; a += 4 * 512) {
+        uint32_t m[4], base[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uintptr_t ga = a + (uintptr_t)(u * 512 + lane * 16);
+            const int64_t pos = (int64_t)(ga - fb);  // file position of the granule's byte 0
+            base[u] = (uint32_t)(pos - lo);
+            m[u] = 0u;
+            if (ga < a1) {
+                const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(ga));
+                int x0, x1;
+                x0 = (int)(lo - pos > 0 ? (lo - pos > 16 ? 16 : lo - pos) : 0);
+                x1 = (int)(hi - pos < 16 ? (hi - pos < 0 ? 0 : hi - pos) : 16);
+                const uint32_t keep = x0 < x1 ? (((1u << x1) - 1u) & ~((1u << x0) - 1u)) : 0u;
+                m[u] = sat_mask16<MAX>(v) & keep;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint32_t mm = m[u];
+            const uint32_t c = __popc(mm);
+            uint32_t incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            if (n + tot > cap) return cap + 1;
+            uint32_t at = n + incl - c;
+            while (mm) {
+                ix[at++] = base[u] + (uint32_t)(__ffs(mm) - 1);
+                mm &= mm - 1u;
+            }
+            n += tot;
+        }
+    }
+    __syncwarp();
+    return n;
+}
+
+// first entry of ix[0..n) that is >= r
+__device__ __forceinline__ uint32_t t_lb(const uint32_t *ix, uint32_t n, uint32_t r) {
+    uint32_t a = 0, b = n;
+    while (a < b) {
+        const uint32_t m = (a + b) >> 1;
+        if (ix[m] < r) a = m + 1;
+        else b = m;
+    }
+    return a;
+}
+
+// one saturated chunk step from start x (one lane); -1 when the step is not
+// saturated or needs bytes outside the index [lo, ihi)
+template <int ALGO>
+__device__ __forceinline__ int64_t t_step(const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi, int64_t x,
+                                          int64_t w, int64_t mx, int64_t Lf) {
+    const int64_t limit = Lf - x < mx ? Lf : x + mx;
+    if constexpr (ALGO == ALGO_RAM) {
+        if (x + w >= Lf) return Lf;  // the window does not fit: a single final chunk
+        if (x + w > ihi) return -1;
+        const uint32_t i1 = t_lb(ix, n, (uint32_t)(x - lo));
+        if (i1 >= n || lo + (int64_t)ix[i1] >= x + w) return -1;  // the window holds no saturating byte
+        const uint32_t i2 = t_lb(ix, n, (uint32_t)(x + w - lo));
+        if (i2 < n && lo + (int64_t)ix[i2] < limit) return lo + (int64_t)ix[i2] + 1;
+        return limit <= ihi ? limit : -1;
+    } else {
+        if (x + w >= limit) return limit;
+        if (x + w + 1 > ihi) return -1;
+        const uint32_t i = t_lb(ix, n, (uint32_t)(x - lo));
+        if (i >= n) return -1;
+        const int64_t q = lo + (int64_t)ix[i];
+        if (q > x + w) return -1;  // no saturating byte within w: not a saturated step
+        return q + w < limit ? q + w + 1 : limit;
+    }
+}
+
+// candidates of segment [pa, ...): index range [*i0, *i0 + K) of their
+// saturating positions; K = 0 when they are not all inside the index
+template <int ALGO>
+__device__ __forceinline__ uint32_t t_cands(const uint32_t *ix, uint32_t n, int64_t lo, int64_t pa, int64_t w,
+                                            uint32_t &i0) {
+    const int64_t clo = ALGO == ALGO_RAM ? pa - 1 : pa - w - 1;  // lowest candidate position
+    const int64_t chi = ALGO == ALGO_RAM ? pa + w - 1 : pa - 1;  // the last is N(chi)
+    if (clo < lo) return 0;
+    i0 = t_lb(ix, n, (uint32_t)(clo - lo));
+    const uint32_t i1 = t_lb(ix, n, (uint32_t)(chi - lo));
+    if (i1 >= n) return 0;
+    return i1 - i0 + 1;
+}
+__device__ __forceinline__ int64_t t_start_of(int algo, int64_t satpos, int64_t w) {
+    return algo == ALGO_RAM ? satpos + 1 : satpos + w + 1;
+}
+
+// Transfer table of segment g (g >= 1) into W.tl / W.tn; false when the
+// segment cannot be resolved in index space.  ix holds the index already.
+template <int ALGO>
+__device__ bool t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint32_t *ix, uint32_t n,
+                        int64_t lo, int64_t ihi) {
+    const int lane = lane_id();
+    const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
+    uint32_t c0;
+    const uint32_t K = t_cands<ALGO>(ix, n, lo, I.p, w, c0);
+    if (K == 0 || K > (uint32_t)TK) return false;
+    // candidates of the next segment, for the links
+    uint32_t d0 = 0, KN = 0;
+    const bool last = g == I.last;
+    if (!last) {
+        KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
+        if (KN == 0 || KN > (uint32_t)TK) return false;
+    }
+    for (uint32_t k = lane; k < K; k += 32) {
+        int64_t x = t_start_of(ALGO, lo + (int64_t)ix[c0 + k], w);
+        uint32_t cnt = 0;
+        while (x >= 0 && x < I.seg_end) {
+            ++cnt;
+            x = t_step<ALGO>(ix, n, lo, ihi, x, w, mx, Lf);
+        }
+        uint32_t link = T_BAD;
+        if (x >= Lf && last) {
+            link = T_END;
+        } else if (x >= 0 && !last) {
+            // the exit must be the start of one of the next segment's candidates
+            const int64_t satpos = ALGO == ALGO_RAM ? x - 1 : x - w - 1;
+            if (satpos >= lo) {
+                const uint32_t i = t_lb(ix, n, (uint32_t)(satpos - lo));
+                if (i < n && lo + (int64_t)ix[i] == satpos && i >= d0 && i < d0 + KN) link = i - d0;
+            }
+        }
+        W.tl[g * TK + k] = link;
+        W.tn[g * TK + k] = cnt;
+    }
+    if (lane == 0) W.tk[g] = K;
+    return true;
+}
+
+// Segments 1 .. nsegs-1 form blocks of TB (segment 0 has no table: its
+// walker follows the true chain itself).  Block b holds [max(TB b, 1),
+// min(TB (b+1), nsegs)).
+constexpr int TB = 32;
+__device__ __forceinline__ uint64_t t_blk_lo(uint64_t b) { return b == 0 ? 1 : b * TB; }
+
+// gather: entry `idx` (0..TK) of a row held 4 per lane (entry u*32 + lane in r[u])
+__device__ __forceinline__ uint32_t t_gather(const uint32_t (&r)[4], uint32_t idx) {
+    const int src = (int)(idx & 31u);
+    const uint32_t v0 = __shfl_sync(0xFFFFFFFFu, r[0], src), v1 = __shfl_sync(0xFFFFFFFFu, r[1], src);
+    const uint32_t v2 = __shfl_sync(0xFFFFFFFFu, r[2], src), v3 = __shfl_sync(0xFFFFFFFFu, r[3], src);
+    const uint32_t u = idx >> 5;
+    return u == 0 ? v0 : u == 1 ? v1 : u == 2 ? v2 : v3;
+}
+
+// Compose block b's tables (the last of its walkers to publish does this):
+// for every entry candidate k of its first segment, the entry candidate and
+// the chain starts before each member (W.tp, W.tq), and the block's link and
+// start count (W.tbc, W.tbs).  Rows of the next member load while the
+// current one is gathered.
+__device__ void t_compose(Work &W, uint64_t b, uint64_t nsegs) {
+    const int lane = lane_id();
+    const uint64_t hs = t_blk_lo(b), he = (b + 1) * TB < nsegs ? (b + 1) * TB : nsegs;
+    const uint32_t K0 = W.tk[hs];
+    uint32_t cur[4], acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint32_t k = (uint32_t)(u * 32 + lane);
+        cur[u] = k < K0 ? k : T_BAD;
+        acc[u] = 0;
+    }
+    uint32_t L[4], N[4], Kh = W.tk[hs];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        L[u] = W.tl[hs * TK + u * 32 + lane];
+        N[u] = W.tn[hs * TK + u * 32 + lane];
+    }
+    for (uint64_t h = hs; h < he; ++h) {
+        uint32_t L2[4], N2[4], K2 = 0;
+        if (h + 1 < he) {
+            K2 = W.tk[h + 1];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                L2[u] = W.tl[(h + 1) * TK + u * 32 + lane];
+                N2[u] = W.tn[(h + 1) * TK + u * 32 + lane];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            W.tp[h * TK + u * 32 + lane] = cur[u];
+            W.tq[h * TK + u * 32 + lane] = acc[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t idx = cur[u] < Kh ? cur[u] : 0u;
+            const uint32_t l = t_gather(L, idx), n = t_gather(N, idx);
+            if (cur[u] < Kh) {
+                acc[u] += n;
+                cur[u] = l;
+            } else {
+                cur[u] = T_BAD;
+            }
+        }
+        if (h + 1 < he) {
+            Kh = K2;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                L[u] = L2[u];
+                N[u] = N2[u];
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        W.tbc[b * TK + u * 32 + lane] = cur[u];
+        W.tbs[b * TK + u * 32 + lane] = acc[u];
+    }
+}
+
+// The scan over blocks (the last composer does it): the true chain enters
+// segment 1 at candidate e1c after n0 starts in segment 0.  Rows load ahead
+// of the shuffle chain.  False when some block cannot continue the chain.
+__device__ bool t_scan_blocks(Work &W, uint64_t nsegs, uint32_t e1c, uint64_t n0, uint64_t *d_count) {
+    const int lane = lane_id();
+    const uint64_t NB = (nsegs + TB - 1) / TB;  // blocks 0 .. NB-1 (block 0 starts at segment 1)
+    uint32_t E = e1c;
+    uint64_t O = n0;
+    for (uint64_t b = 0; b < NB; ++b) {
+        uint32_t C[4], S[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            C[u] = W.tbc[b * TK + u * 32 + lane];
+            S[u] = W.tbs[b * TK + u * 32 + lane];
+        }
+        if (E >= (uint32_t)TK) return false;
+        if (lane == 0) {
+            W.tbe[b] = E;
+            W.tbo[b] = O;
+        }
+        const uint32_t c = t_gather(C, E), sc = t_gather(S, E);
+        if (c == T_BAD) return false;
+        O += sc;
+        E = c;
+    }
+    if (E != T_END) return false;
+    if (lane == 0) {
+        W.seg_out[nsegs] = O;
+        *d_count = O;
+    }
+    return true;
+}
+
+// One T-mode attempt of walker g after its body walk (all 32 lanes).  Returns
+// true when the call's output was produced from the tables (this walker has
+// written its part); false to fall back to the halo walk.
+template <int ALGO>
+__device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, const SpecEmit &em,
+                          uint8_t *ring, const uint8_t *fbase, uint64_t *bounds, uint64_t cap, uint64_t *d_count) {
+    constexpr bool MAX = ALGO != ALGO_AE_MIN;
+    const int lane = lane_id();
+    const SegInfo &I = em.I;
+    const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
+    uint32_t *ix = reinterpret_cast<uint32_t *>(ring);
+    const int64_t lo = I.p - w - 1 > 0 ? I.p - w - 1 : 0;
+    const int64_t ihi = I.seg_end + mx + 1 < Lf ? I.seg_end + mx + 1 : Lf;
+    uint32_t n = 0, e1c = T_BAD;
+    if (t_alive(W)) {
+        n = t_index<MAX>(fbase, lo, ihi, ix, T_IDX_CAP);
+        bool mine = n <= T_IDX_CAP && (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo);
+        if (mine && g == 0) {
+            // the true chain (this walker's) enters segment 1 at its first halo start
+            mine = false;
+            if (em.hcnt > 0) {
+                const int64_t e1 = I.seg_end + (int64_t)em.halo[0];
+                uint32_t d0;
+                const uint32_t KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
+                const int64_t satpos = ALGO == ALGO_RAM ? e1 - 1 : e1 - w - 1;
+                if (KN > 0 && KN <= (uint32_t)TK && satpos >= lo) {
+                    const uint32_t i = t_lb(ix, n, (uint32_t)(satpos - lo));
+                    if (i < n && lo + (int64_t)ix[i] == satpos && i >= d0 && i < d0 + KN) {
+                        e1c = i - d0;
+                        mine = true;
+                    }
+                }
+            }
+        } else if (mine) {
+            mine = t_table<ALGO>(G, W, g, I, ix, n, lo, ihi);
+        }
+        if (!mine) t_fail(W);
+    }
+    // arrive.  Walker 0 publishes the true chain's entry into segment 1; the
+    // last walker of a block composes the block; the last composer (or walker
+    // 0, if it comes last) scans the blocks.  The verdict word T_SCAN decides
+    // once (compare-and-swap from ~0): 1 = the tables produced the output.
+    unsigned long long *tm = g_timing ? g_timing + TM_STAMPS + TM_PER_SEG * g : nullptr;
+    const uint64_t NB = (nsegs + TB - 1) / TB;
+    bool scanner = false;
+    __syncwarp();
+    if (g == 0) {
+        if (lane == 0) {
+            st_relaxed_u32(W.ctrl + T_E1, e1c);
+            st_relaxed_u32(W.ctrl + T_N0, em.cnt);
+            __threadfence();
+            scanner = atomicAdd(W.ctrl + T_ARRIVE, 1u) + 1u == (uint32_t)NB;  // starts at ~0: +1 = arrivals - 1
+        }
+    } else {
+        const uint64_t b = g / TB;
+        const uint64_t members = ((b + 1) * TB < nsegs ? (b + 1) * TB : nsegs) - t_blk_lo(b);
+        bool composer = false;
+        if (lane == 0) {
+            if (tm) tm[2] = globaltimer();  // diagnostics: table published
+            __threadfence();
+            composer = atomicAdd(W.tblk + b, 1u) + 2u == (uint32_t)members;  // starts at ~0
+        }
+        composer = __shfl_sync(0xFFFFFFFFu, composer, 0);
+        if (composer) {
+            __threadfence();
+            if (t_alive(W)) t_compose(W, b, nsegs);
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                scanner = atomicAdd(W.ctrl + T_ARRIVE, 1u) + 1u == (uint32_t)NB;
+            }
+        }
+    }
+    scanner = __shfl_sync(0xFFFFFFFFu, scanner, 0);
+    uint32_t verdict = 0;
+    if (scanner) {  // every block composed and walker 0 arrived
+        __threadfence();
+        bool ok = t_alive(W) && nsegs >= 2;
+        const uint32_t e1 = ld_relaxed_u32(W.ctrl + T_E1), n0 = ld_relaxed_u32(W.ctrl + T_N0);
+        if (ok) ok = e1 != T_BAD && t_scan_blocks(W, nsegs, e1, n0, d_count);
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicCAS(W.ctrl + T_SCAN, ~0u, ok ? 1u : 0u);
+            if (tm) tm[3] = globaltimer();
+        }
+    }
+    if (lane == 0) {
+        const unsigned long long t0 = globaltimer();
+        uint32_t ns = 64;
+        for (;;) {
+            verdict = ld_acquire_u32(W.ctrl + T_SCAN);
+            if (verdict != ~0u) break;
+            if (!t_alive(W) || globaltimer() - t0 > T_TIMEOUT_NS) {
+                atomicCAS(W.ctrl + T_SCAN, ~0u, 0u);  // give up (unless the scan has just decided)
+                continue;
+            }
+            __nanosleep(ns);
+            if (ns < 1024) ns <<= 1;
+        }
+    }
+    verdict = __shfl_sync(0xFFFFFFFFu, verdict, 0);
+    if (verdict != 1u) return false;
+    // this segment's part of the true chain
+    if (g == 0) {
+        for (uint32_t i = lane; i < em.cnt; i += 32) {
+            const uint64_t v = (uint64_t)I.p + em.list[i];
+            if (i >= 1 && i - 1 < cap) bounds[i - 1] = v;
+        }
+    } else if (lane == 0) {
+        const uint64_t b = g / TB;
+        const uint32_t Eb = W.tbe[b];
+        const uint32_t E = W.tp[g * TK + Eb];
+        uint64_t q = W.tbo[b] + W.tq[g * TK + Eb];
+        uint32_t c0;
+        t_cands<ALGO>(ix, n, lo, I.p, w, c0);
+        int64_t x = t_start_of(ALGO, lo + (int64_t)ix[c0 + E], w);
+        while (x >= 0 && x < I.seg_end) {
+            if (q >= 1 && q - 1 < cap) bounds[q - 1] = (uint64_t)x;
+            ++q;
+            x = t_step<ALGO>(ix, n, lo, ihi, x, w, mx, Lf);
+        }
+        if (g == nsegs - 1) {
+            const uint64_t total = W.seg_out[nsegs];
+            if (total >= 1 && total - 1 < cap) bounds[total - 1] = (uint64_t)Lf;  // the last boundary is the length
+        }
+    }
+    return true;
+}
+
 template <int ALGO>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
                                   uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused) {
@@ -527,6 +969,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     em.sa = em.sb = 0;
     em.lp.reset();
     em.published = false;
+    em.tflag = G.tmode ? 1 : 0;
     if (lane == 0) st_relaxed_u32(em.list, 0u);  // the speculative chain starts at the segment's first byte
     unsigned long long *tm = g_timing ? g_timing + TM_STAMPS : nullptr;
     em.tbody = tm ? tm + TM_PER_SEG * g + 1 : nullptr;
@@ -538,6 +981,23 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
     run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
     em.publish();
+    if (G.tmode) {
+        if (t_attempt<ALGO>(G, W, g, nsegs, em, R.buf, fbase, bounds, cap, d_count)) {
+            if (lane == 0) {  // for cdc_stats: a table segment has no halo
+                W.cnt[g] = em.cnt;
+                W.hcnt[g] = 0;
+                W.sj[g] = SJ_TABLE;
+                if (tm) tm[TM_PER_SEG * g + 3] = globaltimer();
+            }
+            return;
+        }
+        if (em.tflag == 2) {  // resume the halo walk where the attempt stopped it
+            em.tflag = 0;
+            run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.seg_end + (int64_t)em.halo[em.hcnt - 1], read_end,
+                            G.w, G.max_size, stream_policy(), em);
+        }
+        em.tflag = 0;
+    }
     if (tm && lane == 0) {
         tm[TM_PER_SEG * g + 2] = globaltimer();
         tm[TM_PER_SEG * g + 4] = smid() | ((unsigned long long)em.hcnt << 32);
@@ -1283,6 +1743,16 @@ bool sync_debug() {
         }                                                                      \
     } while (0)
 
+// CDC_TMODE=0 disables the transfer-table attempt (a debugging and testing knob)
+int tmode_on() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CDC_TMODE");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v;
+}
+
 // CDC_FUSED=0 disables the fused look-back fast path (k_fixup always resolves;
 // a debugging and testing knob)
 int fused_mode() {
@@ -1338,7 +1808,7 @@ int num_sms() {
 struct Plan {
     uint64_t S, Hmax, max_segs, cap_list, cap_halo, pool_cap, exc_cap, nfiles, poolb_cap;
     size_t bytes, reset_bytes;
-    size_t off[32];
+    size_t off[40];
 };
 
 uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
@@ -1381,7 +1851,7 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     const uint64_t G = P.max_segs;
     size_t sz[] = {
         G * P.cap_list * 4,  // 0 list   } reset to 0xFF by k_reset at every call
-        G * 16 + 64 + (G / 32 + 1) * 12,  // 1 pub, status, ctrl, grp, gcnt }
+        G * 16 + 64 + (G / 32 + 1) * 12,  // 1 pub, status, ctrl, grp, tblk }
         G * P.cap_halo * 4,  // 2 halo
         G * 4,               // 3 cnt
         G * 4,               // 4 hcnt
@@ -1405,9 +1875,18 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
         G * 4,               // 22 ocnt
         G * 8,               // 23 ooff
         P.poolb_cap * 8,     // 24 poolb
+        G * cdc::TK * 4,     // 25 tl
+        G * cdc::TK * 4,     // 26 tn
+        G * 4,               // 27 tk
+        G * cdc::TK * 4,     // 28 tp
+        G * cdc::TK * 4,     // 29 tq
+        (G / cdc::TB + 2) * cdc::TK * 4,  // 30 tbc
+        (G / cdc::TB + 2) * cdc::TK * 4,  // 31 tbs
+        (G / cdc::TB + 2) * 4,            // 32 tbe
+        (G / cdc::TB + 2) * 8,            // 33 tbo
     };
     size_t o = 0;
-    for (int i = 0; i < 25; ++i) {
+    for (int i = 0; i < 34; ++i) {
         P.off[i] = o;
         o += round_up(sz[i], 256);
     }
@@ -1423,7 +1902,7 @@ cdc::Work carve(const Plan &P, void *ws) {
     W.status = W.pub + P.max_segs;
     W.ctrl = reinterpret_cast<uint32_t *>(W.status + P.max_segs);
     W.grp = W.status + P.max_segs + 8;
-    W.gcnt = reinterpret_cast<uint32_t *>(W.grp + P.max_segs / 32 + 1);
+    W.tblk = reinterpret_cast<uint32_t *>(W.grp + P.max_segs / 32 + 1);
     W.halo = (uint32_t *)(b + P.off[2]);
     W.cnt = (uint32_t *)(b + P.off[3]);
     W.hcnt = (uint32_t *)(b + P.off[4]);
@@ -1447,6 +1926,15 @@ cdc::Work carve(const Plan &P, void *ws) {
     W.ocnt = (uint32_t *)(b + P.off[22]);
     W.ooff = (uint64_t *)(b + P.off[23]);
     W.poolb = (uint64_t *)(b + P.off[24]);
+    W.tl = (uint32_t *)(b + P.off[25]);
+    W.tn = (uint32_t *)(b + P.off[26]);
+    W.tk = (uint32_t *)(b + P.off[27]);
+    W.tp = (uint32_t *)(b + P.off[28]);
+    W.tq = (uint32_t *)(b + P.off[29]);
+    W.tbc = (uint32_t *)(b + P.off[30]);
+    W.tbs = (uint32_t *)(b + P.off[31]);
+    W.tbe = (uint32_t *)(b + P.off[32]);
+    W.tbo = (uint64_t *)(b + P.off[33]);
     W.poolb_cap = P.poolb_cap;
     W.cap_list = P.cap_list;
     W.cap_halo = P.cap_halo;
@@ -1499,6 +1987,12 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     const uint64_t nsm = (uint64_t)num_sms();
     const int spw = (int)std::min<uint64_t>(std::max<uint64_t>((nseg_ub + nsm - 1) / nsm, 1), cdc::SPEC_WARPS);
     const uint64_t blocks = (nseg_ub + spw - 1) / spw;
+    // transfer tables: a single stream of at least two segments, windows long
+    // enough for slow convergence, segments short enough for their halos to
+    // matter, and a grid that is one co-resident wave (the attempt waits for
+    // every walker; it also gives up after a timeout)
+    G.tmode = (!batch && tmode_on() && p->window >= 4096 && P.S <= (1ull << 20) && nseg_ub >= 3 &&
+               blocks <= nsm) ? 1 : 0;
     if (blocks > 0) {
         int fused = (P.cap_list + P.cap_halo < (1u << 23)) ? fused_mode() : 0;
         CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_speculate<ALGO>), dim3((unsigned)blocks),
@@ -1547,6 +2041,7 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     G.Hmax = P.Hmax;
     G.w = p->window;
     G.max_size = p->max_size;
+    G.tmode = 0;
     uint64_t *file_out = batch ? d_bound_off : W.file_out;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (p->algo) {
@@ -1654,9 +2149,10 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
         CDC_CUDA(cudaMemcpyAsync(hc.data(), W.hcnt, G * 4, cudaMemcpyDeviceToHost, st));
         CDC_CUDA(cudaStreamSynchronize(st));
     }
-    uint64_t met = 0, unsynced = 0, other = 0, halo = 0;
+    uint64_t met = 0, unsynced = 0, other = 0, halo = 0, tables = 0;
     for (uint64_t g = 0; g < G; ++g) {
-        if (sj[g] == (int32_t)(g + 1) || sj[g] == cdc::SJ_LAST) ++met;
+        if (sj[g] == cdc::SJ_TABLE) ++tables;
+        if (sj[g] == (int32_t)(g + 1) || sj[g] == cdc::SJ_LAST || sj[g] == cdc::SJ_TABLE) ++met;
         else if (sj[g] == cdc::SJ_UNSYNCED) ++unsynced;
         else ++other;
         halo += hc[g];
@@ -1664,7 +2160,7 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
     stats[0] = G;
     stats[1] = P.S;
     stats[2] = P.Hmax;
-    stats[3] = ctrl[1] != 0 ? 1 : 0;
+    stats[3] = ctrl[1] == 0 ? 0 : (tables == G && G > 0 ? 2 : 1);
     stats[4] = met;
     stats[5] = unsynced;
     stats[6] = other;

@@ -1,0 +1,93 @@
+"""GPU parity of the transfer-table path (T-mode): saturated
+streams (uniform bytes at w >> 256) whose chains are resolved in index space
+instead of by halo walks, and the fallback when a stream is not saturated
+everywhere.  Every comparison is bit-exact against the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cdc(cuda_ok):
+    import paper_2508_05797_b200 as m
+    return m
+
+
+def _run(cdc, d, p):
+    t = torch.from_numpy(d).cuda()
+    n = d.size
+    ws = torch.empty(cdc.workspace_size(p, 1, n, n), dtype=torch.uint8, device="cuda")
+    b = torch.full((cdc.max_boundaries(p, n),), -1, dtype=torch.int64, device="cuda")
+    c = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cdc.chunk_async(t, p, b, c, ws)
+    got = b[:int(c.item())].cpu().numpy().astype(np.uint64)
+    return got, cdc.stats(p, ws, 1, n, n)
+
+
+@pytest.mark.parametrize("algo,avg", [("ram", 8192), ("ae_max", 8192), ("ae_min", 8192),
+                                      ("ram", 16384), ("ae_max", 16384)])
+def test_tables_uniform(cdc, algo, avg):
+    """configs[0]-shape streams (16 MiB of uniform bytes, plus a ragged tail):
+    the tables produce the output and it equals the oracle's."""
+    d = synth.uniform((16 << 20) + 777, 10)
+    p = cdc.params(algo, avg_size=avg)
+    exp = oracle.chunk(algo, d, p.window, p.max_size)
+    got, st = _run(cdc, d, p)
+    assert st["fast_path"] == 2, st
+    assert got.size == exp.size and (got == exp).all()
+
+
+def test_tables_many_small_segments(cdc):
+    """Forced 64 KiB segments: many tables, each with links into the next."""
+    d = synth.uniform(6 << 20, 11)
+    p = cdc.params("ram", avg_size=8192, seg_bytes=65536)
+    exp = oracle.chunk("ram", d, p.window, p.max_size)
+    got, st = _run(cdc, d, p)
+    assert st["fast_path"] == 2, st
+    assert got.size == exp.size and (got == exp).all()
+
+
+@pytest.mark.parametrize("algo", ["ram", "ae_max"])
+def test_tables_fallback(cdc, algo):
+    """A zero region breaks saturation: the attempt fails and the halo walks
+    resolve the stream (same boundaries as the oracle)."""
+    d = synth.uniform(16 << 20, 12)
+    d[5 << 20:(5 << 20) + 300_000] = 0
+    p = cdc.params(algo, avg_size=8192)
+    exp = oracle.chunk(algo, d, p.window, p.max_size)
+    got, st = _run(cdc, d, p)
+    assert st["fast_path"] != 2, st
+    assert got.size == exp.size and (got == exp).all()
+
+
+def test_tables_graph_replay(cdc):
+    """The table path captured in a CUDA graph replays exactly."""
+    d = synth.uniform(16 << 20, 13)
+    p = cdc.params("ram", avg_size=8192)
+    exp = oracle.chunk("ram", d, p.window, p.max_size)
+    t = torch.from_numpy(d).cuda()
+    n = d.size
+    ws = torch.empty(cdc.workspace_size(p, 1, n, n), dtype=torch.uint8, device="cuda")
+    b = torch.empty(cdc.max_boundaries(p, n), dtype=torch.int64, device="cuda")
+    c = torch.zeros(1, dtype=torch.int64, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        cdc.chunk_async(t, p, b, c, ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cdc.chunk_async(t, p, b, c, ws)
+    for _ in range(3):
+        b.fill_(-1)
+        c.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        got = b[:int(c.item())].cpu().numpy().astype(np.uint64)
+        assert got.size == exp.size and (got == exp).all()
+    assert cdc.stats(p, ws, 1, n, n)["fast_path"] == 2

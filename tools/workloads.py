@@ -73,10 +73,16 @@ def run_batch(name, data_np, offs, algo, avg, reps=5):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    cdc.profile_enable(True)
+    cdc.chunk_batch_async(t, od, total, max_len, p, b, bo, c, ws)
+    torch.cuda.synchronize()
+    cdc.profile_enable(False)
+    pr = cdc.profile_collect()
     st = cdc.stats(p, ws, len(offs) - 1, total, max_len)
+    st["k_ms"] = {k: round(v[0], 3) for k, v in pr.items() if k != "calls" and v[1]}
     print("%-28s %-6s %5d  %8.3f ms  %8.1f GB/s  files %d chunks %d  %s" % (
         name, algo, avg, ms, total / ms / 1e6, len(offs) - 1, int(c.item()),
-        {k: st[k] for k in ("segments", "fast_path", "synced", "skipped_or_end", "halo_chunks")}), flush=True)
+        {k: st[k] for k in ("segments", "fast_path", "synced", "skipped_or_end", "halo_chunks", "k_ms")}), flush=True)
 
 
 if "c2" in sel:  # configs[2]: the 1 GiB base and its last snapshot, AE and RAM at 4/8/16 KiB
