@@ -235,16 +235,17 @@ int cdc_profile_query(int *done);
 int cdc_plan_info(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, uint64_t *out);
 
 /*
- * Diagnostics: while d_buf (a device uint64 array of 8 + 5 x segments
+ * Diagnostics: while d_buf (a device uint64 array of 8 + 7 x segments
  * entries) is set, the kernels record globaltimer stamps.  d_buf[0..7]:
  * k_reset first start / last end, k_speculate first CTA start / first return
  * from its PDL wait / last walker end, k_fixup first CTA start / first return
  * from its PDL wait / last end (the caller presets the "first" slots 0, 2, 3,
  * 5, 6 to ~0 and the "last" slots 1, 4, 7 to 0; a k_fixup that runs the fix-up
- * path leaves slot 7 alone).  Then per segment g, at d_buf[8 + 5g]:
+ * path leaves slot 7 alone).  Then per segment g, at d_buf[8 + 7g]:
  * {at start, at the end of its body walk (first boundary at or past the
  * segment end; 0 if none), at the end of the walk, at the end of its fused
- * write, SM id | halo chunks << 32}.  NULL turns recording off.  Never set during
+ * write, SM id | halo chunks << 32, transfer tables: index built, table
+ * built}.  NULL turns recording off.  Never set during
  * measurements.
  */
 int cdc_debug_timing(void *d_buf);

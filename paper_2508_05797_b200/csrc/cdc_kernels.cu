@@ -265,10 +265,10 @@ struct ListProbe {
 // (globaltimer; min slots preset to ~0 by the caller, max slots to 0), then
 // TM_PER_SEG x u64 per segment {at start, at the end of the body walk (its
 // first boundary at or past the segment end), at the end of the walk, at the
-// end, smid | hcnt << 32}.
+// end, smid | hcnt << 32, T-mode: index built, table built}.
 __device__ unsigned long long *g_timing = nullptr;
 constexpr int TM_STAMPS = 8;
-constexpr int TM_PER_SEG = 5;
+constexpr int TM_PER_SEG = 7;
 enum : int { TM_RESET_BEGIN, TM_RESET_END, TM_SPEC_BEGIN, TM_SPEC_WAITED, TM_SPEC_END, TM_FIX_BEGIN,
              TM_FIX_WAITED, TM_FIX_END };
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -493,14 +493,16 @@ template <int ALGO>
 __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_count, uint64_t *file_out,
                                                 uint64_t *bounds, uint64_t cap);
 
-template <int ALGO>
+template <int ALGO, bool TM>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
                                   uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused);
 
 // K1.  One warp per segment (CTAs take segment groups in ticket order).  In
 // the common case the fused look-back writes the output and k_fixup (launched
 // behind it with PDL) only checks that it did.
-template <int ALGO>
+// TM: the variant that tries the transfer tables (saturated streams); the
+// other one carries none of their code, so the common path keeps its registers.
+template <int ALGO, bool TM>
 __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate(Geometry G, Work W, uint64_t *bounds,
                                                                   uint64_t cap, uint64_t *d_count, int fused,
                                                                   int spw) {
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
     const uint64_t g = (uint64_t)s_ticket * spw + warp;
     const uint64_t nsegs = total_segs(G, W);
     if (warp >= spw || g >= nsegs) return;
-    speculate_segment<ALGO>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused);
+    speculate_segment<ALGO, TM>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused);
     if (lane_id() == 0) stamp(TM_SPEC_END);
 }
 
@@ -564,7 +566,10 @@ __device__ __forceinline__ void t_fail(Work &W) {
 __device__ __forceinline__ bool t_alive(const Work &W) { return ld_relaxed_u32(W.ctrl + T_ALL) != 0u; }
 
 // index of the saturating bytes of the file positions [lo, hi): ascending
-// offsets from lo into ix; returns the count, or cap + 1 when they do not fit
+// offsets from lo into ix; returns the count, or cap + 1 when they do not fit.
+// Each lane takes 128 contiguous bytes (8 granules: the warp's first load
+// brings all 32 lines into L1), so lane order is position order and one warp
+// scan of the lanes' counts places every entry.
 template <bool MAX>
 __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, uint32_t *ix, uint32_t cap) {
     const int lane = lane_id();
@@ -572,42 +577,44 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, uint32
     const uintptr_t a0 = (fb + (uintptr_t)lo) & ~(uintptr_t)15;
     const uintptr_t a1 = fb + (uintptr_t)hi;
     uint32_t n = 0;
-    for (uintptr_t a = a0; a < a1; a += 4 * 512) {
-        uint32_t m[4], base[4];
+    for (uintptr_t a = a0; a < a1; a += 32 * 128) {
+        const uintptr_t la = a + (uintptr_t)lane * 128;
+        uint32_t m[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uintptr_t ga = a + (uintptr_t)(u * 512 + lane * 16);
-            const int64_t pos = (int64_t)(ga - fb);  // file position of the granule's byte 0
-            base[u] = (uint32_t)(pos - lo);
+        for (int u = 0; u < 8; ++u) {
+            const uintptr_t ga = la + (uintptr_t)(u * 16);
             m[u] = 0u;
             if (ga < a1) {
-                const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(ga));
-                int x0, x1;
-                x0 = (int)(lo - pos > 0 ? (lo - pos > 16 ? 16 : lo - pos) : 0);
-                x1 = (int)(hi - pos < 16 ? (hi - pos < 0 ? 0 : hi - pos) : 16);
+                const uint4 v = *reinterpret_cast<const uint4 *>(ga);
+                const int64_t pos = (int64_t)(ga - fb);
+                const int x0 = (int)(lo - pos > 0 ? (lo - pos > 16 ? 16 : lo - pos) : 0);
+                const int x1 = (int)(hi - pos < 16 ? (hi - pos < 0 ? 0 : hi - pos) : 16);
                 const uint32_t keep = x0 < x1 ? (((1u << x1) - 1u) & ~((1u << x0) - 1u)) : 0u;
                 m[u] = sat_mask16<MAX>(v) & keep;
             }
         }
+        uint32_t c = 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) c += __popc(m[u]);
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        if (n + tot > cap) return cap + 1;
+        uint32_t at = n + incl - c;
+        const uint32_t base = (uint32_t)((int64_t)(la - fb) - lo);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
             uint32_t mm = m[u];
-            const uint32_t c = __popc(mm);
-            uint32_t incl = c;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
-            if (n + tot > cap) return cap + 1;
-            uint32_t at = n + incl - c;
             while (mm) {
-                ix[at++] = base[u] + (uint32_t)(__ffs(mm) - 1);
+                ix[at++] = base + (uint32_t)(u * 16) + (uint32_t)(__ffs(mm) - 1);
                 mm &= mm - 1u;
             }
-            n += tot;
         }
+        n += tot;
     }
     __syncwarp();
     return n;
@@ -726,8 +733,8 @@ __device__ __forceinline__ uint32_t t_gather(const uint32_t (&r)[4], uint32_t id
 // Compose block b's tables (the last of its walkers to publish does this):
 // for every entry candidate k of its first segment, the entry candidate and
 // the chain starts before each member (W.tp, W.tq), and the block's link and
-// start count (W.tbc, W.tbs).  Rows of the next member load while the
-// current one is gathered.
+// start count (W.tbc, W.tbs).  Rows load four members at a time, so the
+// shuffle chain waits for one L2 round trip per four members.
 __device__ void t_compose(Work &W, uint64_t b, uint64_t nsegs) {
     const int lane = lane_id();
     const uint64_t hs = t_blk_lo(b), he = (b + 1) * TB < nsegs ? (b + 1) * TB : nsegs;
@@ -739,44 +746,34 @@ __device__ void t_compose(Work &W, uint64_t b, uint64_t nsegs) {
         cur[u] = k < K0 ? k : T_BAD;
         acc[u] = 0;
     }
-    uint32_t L[4], N[4], Kh = W.tk[hs];
+    for (uint64_t h0 = hs; h0 < he; h0 += 4) {
+        uint32_t L[4][4], N[4][4], Kh[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        L[u] = W.tl[hs * TK + u * 32 + lane];
-        N[u] = W.tn[hs * TK + u * 32 + lane];
-    }
-    for (uint64_t h = hs; h < he; ++h) {
-        uint32_t L2[4], N2[4], K2 = 0;
-        if (h + 1 < he) {
-            K2 = W.tk[h + 1];
+        for (int v = 0; v < 4; ++v) {
+            const uint64_t h = h0 + v;
+            Kh[v] = h < he ? W.tk[h] : 0u;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                L2[u] = W.tl[(h + 1) * TK + u * 32 + lane];
-                N2[u] = W.tn[(h + 1) * TK + u * 32 + lane];
+                L[v][u] = h < he ? W.tl[h * TK + u * 32 + lane] : T_BAD;
+                N[v][u] = h < he ? W.tn[h * TK + u * 32 + lane] : 0u;
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            W.tp[h * TK + u * 32 + lane] = cur[u];
-            W.tq[h * TK + u * 32 + lane] = acc[u];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t idx = cur[u] < Kh ? cur[u] : 0u;
-            const uint32_t l = t_gather(L, idx), n = t_gather(N, idx);
-            if (cur[u] < Kh) {
-                acc[u] += n;
-                cur[u] = l;
-            } else {
-                cur[u] = T_BAD;
-            }
-        }
-        if (h + 1 < he) {
-            Kh = K2;
+        for (int v = 0; v < 4; ++v) {
+            const uint64_t h = h0 + v;
+            if (h >= he) break;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                L[u] = L2[u];
-                N[u] = N2[u];
+                W.tp[h * TK + u * 32 + lane] = cur[u];
+                W.tq[h * TK + u * 32 + lane] = acc[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool in = cur[u] < Kh[v];
+                const uint32_t idx = in ? cur[u] : 0u;
+                const uint32_t l = t_gather(L[v], idx), n = t_gather(N[v], idx);
+                acc[u] += in ? n : 0u;
+                cur[u] = in ? l : T_BAD;
             }
         }
     }
@@ -795,22 +792,30 @@ __device__ bool t_scan_blocks(Work &W, uint64_t nsegs, uint32_t e1c, uint64_t n0
     const uint64_t NB = (nsegs + TB - 1) / TB;  // blocks 0 .. NB-1 (block 0 starts at segment 1)
     uint32_t E = e1c;
     uint64_t O = n0;
-    for (uint64_t b = 0; b < NB; ++b) {
-        uint32_t C[4], S[4];
+    for (uint64_t b0 = 0; b0 < NB; b0 += 4) {  // four blocks' rows per L2 round trip
+        uint32_t C[4][4], S[4][4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            C[u] = W.tbc[b * TK + u * 32 + lane];
-            S[u] = W.tbs[b * TK + u * 32 + lane];
+        for (int v = 0; v < 4; ++v) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                C[v][u] = b0 + v < NB ? W.tbc[(b0 + v) * TK + u * 32 + lane] : T_BAD;
+                S[v][u] = b0 + v < NB ? W.tbs[(b0 + v) * TK + u * 32 + lane] : 0u;
+            }
         }
-        if (E >= (uint32_t)TK) return false;
-        if (lane == 0) {
-            W.tbe[b] = E;
-            W.tbo[b] = O;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint64_t b = b0 + v;
+            if (b >= NB) break;
+            if (E >= (uint32_t)TK) return false;
+            if (lane == 0) {
+                W.tbe[b] = E;
+                W.tbo[b] = O;
+            }
+            const uint32_t c = t_gather(C[v], E), sc = t_gather(S[v], E);
+            if (c == T_BAD) return false;
+            O += sc;
+            E = c;
         }
-        const uint32_t c = t_gather(C, E), sc = t_gather(S, E);
-        if (c == T_BAD) return false;
-        O += sc;
-        E = c;
     }
     if (E != T_END) return false;
     if (lane == 0) {
@@ -836,6 +841,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
     uint32_t n = 0, e1c = T_BAD;
     if (t_alive(W)) {
         n = t_index<MAX>(fbase, lo, ihi, ix, T_IDX_CAP);
+        if (g_timing && lane == 0) g_timing[TM_STAMPS + TM_PER_SEG * g + 5] = globaltimer();
         bool mine = n <= T_IDX_CAP && (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo);
         if (mine && g == 0) {
             // the true chain (this walker's) enters segment 1 at its first halo start
@@ -857,6 +863,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
             mine = t_table<ALGO>(G, W, g, I, ix, n, lo, ihi);
         }
         if (!mine) t_fail(W);
+        if (g_timing && lane == 0) g_timing[TM_STAMPS + TM_PER_SEG * g + 6] = globaltimer();
     }
     // arrive.  Walker 0 publishes the true chain's entry into segment 1; the
     // last walker of a block composes the block; the last composer (or walker
@@ -950,7 +957,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
     return true;
 }
 
-template <int ALGO>
+template <int ALGO, bool TM>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
                                   uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused) {
     const int lane = lane_id();
@@ -969,7 +976,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     em.sa = em.sb = 0;
     em.lp.reset();
     em.published = false;
-    em.tflag = G.tmode ? 1 : 0;
+    em.tflag = TM ? 1 : 0;
     if (lane == 0) st_relaxed_u32(em.list, 0u);  // the speculative chain starts at the segment's first byte
     unsigned long long *tm = g_timing ? g_timing + TM_STAMPS : nullptr;
     em.tbody = tm ? tm + TM_PER_SEG * g + 1 : nullptr;
@@ -981,7 +988,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
     run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
     em.publish();
-    if (G.tmode) {
+    if constexpr (TM) {
         if (t_attempt<ALGO>(G, W, g, nsegs, em, R.buf, fbase, bounds, cap, d_count)) {
             if (lane == 0) {  // for cdc_stats: a table segment has no halo
                 W.cnt[g] = em.cnt;
@@ -1951,7 +1958,10 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     static bool attr_set = false;
     const int spec_smem = cdc::SPEC_WARPS * cdc::RING_SMEM + 128;
     if (!attr_set) {
-        CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, spec_smem));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      spec_smem));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_fixup<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       cdc::FIX_SMEM));
         attr_set = true;
@@ -1995,7 +2005,9 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
                blocks <= nsm) ? 1 : 0;
     if (blocks > 0) {
         int fused = (P.cap_list + P.cap_halo < (1u << 23)) ? fused_mode() : 0;
-        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_speculate<ALGO>), dim3((unsigned)blocks),
+        const void *kspec = G.tmode ? reinterpret_cast<const void *>(cdc::k_speculate<ALGO, true>)
+                                    : reinterpret_cast<const void *>(cdc::k_speculate<ALGO, false>);
+        CDC_CUDA(launch_pdl(kspec, dim3((unsigned)blocks),
                             dim3(cdc::SPEC_WARPS * 32), (size_t)spec_smem, st, G, W, d_bounds, cap, d_count, fused,
                             spw));
         CDC_KCHECK("k_speculate", st);

@@ -25,14 +25,14 @@ for _ in range(3):
     cdc.chunk_async(t, p, b, c, ws)
 st = cdc.stats(p, ws, 1, n, n)
 G = st["segments"]
-tm = torch.zeros(8 + 5 * G, dtype=torch.int64, device="cuda")
+tm = torch.zeros(8 + 7 * G, dtype=torch.int64, device="cuda")
 tm[[0, 2, 3, 5, 6]] = -1  # "first" stamps: atomicMin slots
 lib.cdc_debug_timing(tm.data_ptr())
 cdc.chunk_async(t, p, b, c, ws)
 torch.cuda.synchronize()
 lib.cdc_debug_timing(None)
 hdr = tm[:8].cpu().numpy().view(np.uint64).astype(np.float64)
-a = tm[8:].cpu().numpy().reshape(G, 5)
+a = tm[8:].cpu().numpy().reshape(G, 7)
 t0 = a[:, 0].min()
 names = ["reset begin", "reset end", "spec begin", "spec waited", "spec end", "fix begin", "fix waited", "fix end"]
 print("launch stamps us rel. to first walker start:",
@@ -50,6 +50,12 @@ print("body us: p10 %.1f p50 %.1f p90 %.1f max %.1f" % (*np.percentile(body, [10
 hw = walk - body
 print("halo walk us: p50 %.1f p90 %.1f p99 %.1f max %.1f; per halo chunk us: mean %.2f" % (
     *np.percentile(hw, [50, 90, 99]), hw.max(), hw.sum() / max(1, halo.sum())))
+if (a[:, 5] > 0).any():
+    ok = (a[:, 5] > 0) & (a[:, 6] > 0) & (a[:, 1] > 0)
+    ib = (a[ok, 5] - a[ok, 1]) / 1e3
+    tb = (a[ok, 6] - a[ok, 5]) / 1e3
+    print("T-mode: index pass us p50 %.1f max %.1f; table us p50 %.1f max %.1f" % (
+        np.percentile(ib, 50), ib.max(), np.percentile(tb, 50), tb.max()))
 print("walk end us (abs): p50 %.1f p90 %.1f max %.1f" % tuple(np.percentile(start + walk, [50, 90, 100])))
 print("done us (abs): p50 %.1f max %.1f" % (np.percentile(done, 50), done.max()))
 print("halo chunks: mean %.2f max %d" % (halo.mean(), halo.max()))
