@@ -294,7 +294,6 @@ struct SpecEmit {
     uint32_t sa, sb;
     ListProbe lp;
     bool published;
-    int tflag;                  // T-mode: 1 = stop at the first unsynced halo boundary, 2 = stopped there
     unsigned long long *tbody;  // diagnostics: where to stamp the end of the body walk (or null)
 
     __device__ void publish() {
@@ -329,10 +328,6 @@ struct SpecEmit {
         }
         if ((uint64_t)h >= G->Hmax) {
             sj = SJ_UNSYNCED;
-            return true;
-        }
-        if (tflag == 1) {  // T-mode: the tables may make the rest of the halo unnecessary
-            tflag = 2;
             return true;
         }
         return false;
@@ -538,27 +533,28 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
 //     limit when q+w >= limit; if x+w >= limit it ends at limit.
 // A saturated chain that enters segment g starts at one of few candidates
 // (RAM: P+1 for a saturating position P in [p_g - 1, N(p_g + w - 1)]; AE:
-// q+w+1 for q in [p_g - w - 1, N(p_g - 1)], N = next saturating position).
-// After its body walk, walker g indexes the saturating bytes of
+// q+w+1 for q in [p_g - w - 1, N(p_g - 1)], N = next saturating position;
+// segment 0: the stream start).  Before any byte walk, walker g looks at its
+// first 4 KiB; if they are dense in saturating bytes it indexes those of
 // [p_g - w - 1, seg_end + max_size + 1) in its idle ring, walks every
 // candidate's chain in index space (one lane each) and publishes, per
 // candidate, the number of chain starts inside the segment and the candidate
-// of segment g+1 its chain enters.  One warp then scans the tables with
-// shuffles, and every walker writes its own part of the true chain: no halo
-// walk.  Any step that is not saturated, any exit that is not a candidate,
-// or any segment that is not dense makes the whole call fall back to the
-// halo walks (the tables are tried only for a single stream whose grid is one
-// co-resident wave, with a timeout).
+// of segment g+1 its chain enters.  The last walker of each block of 32
+// segments composes the block's tables with shuffles, the last composer scans
+// the blocks, and every walker writes its own part of the true chain: no byte
+// walk and no halo.  Any step that is not saturated, any exit that is not a
+// candidate, or any segment that is not dense makes the whole call fall back
+// to the speculative walk (the tables are tried only for a single stream
+// whose grid is one co-resident wave, with a timeout).
 constexpr int TK = 128;                      // candidates per segment, 4 per lane
 constexpr uint32_t T_END = 0xFFFFFFFEu;      // link: the chain reached the stream end
 constexpr uint32_t T_BAD = 0xFFFFFFFFu;      // link: not resolvable in index space
 constexpr uint32_t T_DENSE = 8;              // saturating bytes per window a segment needs
 constexpr uint32_t T_IDX_CAP = (uint32_t)(RING_BYTES / 4);
 constexpr unsigned long long T_TIMEOUT_NS = 2000000ull;  // the scanner gives up after 2 ms
-// control words (ctrl[], reset to ~0 by k_reset): 6 block composers and walker
-// 0 arrived, 7 all-T (~0 yes, 0 no), 8 verdict (~0 pending, 1 tables, 0 fall
-// back), 9 and 10 walker 0's entry candidate of segment 1 and its start count
-constexpr int T_ARRIVE = 6, T_ALL = 7, T_SCAN = 8, T_E1 = 9, T_N0 = 10;
+// control words (ctrl[], reset to ~0 by k_reset): 6 block composers arrived,
+// 7 all-T (~0 yes, 0 no), 8 verdict (~0 pending, 1 tables, 0 fall back)
+constexpr int T_ARRIVE = 6, T_ALL = 7, T_SCAN = 8;
 
 __device__ __forceinline__ void t_fail(Work &W) {
     if (ld_relaxed_u32(W.ctrl + T_ALL) != 0u) atomicAnd(W.ctrl + T_ALL, 0u);
@@ -566,22 +562,25 @@ __device__ __forceinline__ void t_fail(Work &W) {
 __device__ __forceinline__ bool t_alive(const Work &W) { return ld_relaxed_u32(W.ctrl + T_ALL) != 0u; }
 
 // index of the saturating bytes of the file positions [lo, hi): ascending
-// offsets from lo into ix; returns the count, or cap + 1 when they do not fit.
-// Each lane takes 128 contiguous bytes (8 granules: the warp's first load
-// brings all 32 lines into L1), so lane order is position order and one warp
-// scan of the lanes' counts places every entry.
+// offsets from rel into ix; returns the count, or cap + 1 when they do not fit.
+// Each lane takes TIX_G contiguous granules of 16 bytes, so lane order is
+// position order and one warp scan of the lanes' counts places every entry.
+#ifndef CDC_TIX_G
+#define CDC_TIX_G 16
+#endif
+constexpr int TIX_G = CDC_TIX_G;  // 16-byte granules per lane per step of the index pass
 template <bool MAX>
-__device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, uint32_t *ix, uint32_t cap) {
+__device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_t rel, uint32_t *ix, uint32_t cap) {
     const int lane = lane_id();
     const uintptr_t fb = reinterpret_cast<uintptr_t>(fbase);
     const uintptr_t a0 = (fb + (uintptr_t)lo) & ~(uintptr_t)15;
     const uintptr_t a1 = fb + (uintptr_t)hi;
     uint32_t n = 0;
-    for (uintptr_t a = a0; a < a1; a += 32 * 128) {
-        const uintptr_t la = a + (uintptr_t)lane * 128;
-        uint32_t m[8];
+    for (uintptr_t a = a0; a < a1; a += 32 * 16 * TIX_G) {
+        const uintptr_t la = a + (uintptr_t)lane * 16 * TIX_G;
+        uint32_t m[TIX_G];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < TIX_G; ++u) {
             const uintptr_t ga = la + (uintptr_t)(u * 16);
             m[u] = 0u;
             if (ga < a1) {
@@ -595,7 +594,7 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, uint32
         }
         uint32_t c = 0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) c += __popc(m[u]);
+        for (int u = 0; u < TIX_G; ++u) c += __popc(m[u]);
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -605,9 +604,9 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, uint32
         const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
         if (n + tot > cap) return cap + 1;
         uint32_t at = n + incl - c;
-        const uint32_t base = (uint32_t)((int64_t)(la - fb) - lo);
+        const uint32_t base = (uint32_t)((int64_t)(la - fb) - rel);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < TIX_G; ++u) {
             uint32_t mm = m[u];
             while (mm) {
                 ix[at++] = base + (uint32_t)(u * 16) + (uint32_t)(__ffs(mm) - 1);
@@ -673,15 +672,23 @@ __device__ __forceinline__ int64_t t_start_of(int algo, int64_t satpos, int64_t 
     return algo == ALGO_RAM ? satpos + 1 : satpos + w + 1;
 }
 
-// Transfer table of segment g (g >= 1) into W.tl / W.tn; false when the
-// segment cannot be resolved in index space.  ix holds the index already.
+// start of candidate k of segment g (segment 0's only candidate is the
+// stream start)
+template <int ALGO>
+__device__ __forceinline__ int64_t t_cand_start(uint64_t g, const uint32_t *ix, int64_t lo, uint32_t c0, uint32_t k,
+                                                int64_t w) {
+    return g == 0 ? 0 : t_start_of(ALGO, lo + (int64_t)ix[c0 + k], w);
+}
+
+// Transfer table of segment g into W.tl / W.tn; false when the segment cannot
+// be resolved in index space.  ix holds the index already.
 template <int ALGO>
 __device__ bool t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint32_t *ix, uint32_t n,
                         int64_t lo, int64_t ihi) {
     const int lane = lane_id();
     const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
-    uint32_t c0;
-    const uint32_t K = t_cands<ALGO>(ix, n, lo, I.p, w, c0);
+    uint32_t c0 = 0;
+    const uint32_t K = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, I.p, w, c0);
     if (K == 0 || K > (uint32_t)TK) return false;
     // candidates of the next segment, for the links
     uint32_t d0 = 0, KN = 0;
@@ -691,7 +698,7 @@ __device__ bool t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I
         if (KN == 0 || KN > (uint32_t)TK) return false;
     }
     for (uint32_t k = lane; k < K; k += 32) {
-        int64_t x = t_start_of(ALGO, lo + (int64_t)ix[c0 + k], w);
+        int64_t x = t_cand_start<ALGO>(g, ix, lo, c0, k, w);
         uint32_t cnt = 0;
         while (x >= 0 && x < I.seg_end) {
             ++cnt;
@@ -715,11 +722,9 @@ __device__ bool t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I
     return true;
 }
 
-// Segments 1 .. nsegs-1 form blocks of TB (segment 0 has no table: its
-// walker follows the true chain itself).  Block b holds [max(TB b, 1),
-// min(TB (b+1), nsegs)).
+// Segments form blocks of TB: block b holds [TB b, min(TB (b+1), nsegs)).
 constexpr int TB = 32;
-__device__ __forceinline__ uint64_t t_blk_lo(uint64_t b) { return b == 0 ? 1 : b * TB; }
+__device__ __forceinline__ uint64_t t_blk_lo(uint64_t b) { return b * TB; }
 
 // gather: entry `idx` (0..TK) of a row held 4 per lane (entry u*32 + lane in r[u])
 __device__ __forceinline__ uint32_t t_gather(const uint32_t (&r)[4], uint32_t idx) {
@@ -784,14 +789,14 @@ __device__ void t_compose(Work &W, uint64_t b, uint64_t nsegs) {
     }
 }
 
-// The scan over blocks (the last composer does it): the true chain enters
-// segment 1 at candidate e1c after n0 starts in segment 0.  Rows load ahead
-// of the shuffle chain.  False when some block cannot continue the chain.
-__device__ bool t_scan_blocks(Work &W, uint64_t nsegs, uint32_t e1c, uint64_t n0, uint64_t *d_count) {
+// The scan over blocks (the last composer does it): the true chain starts
+// at segment 0's only candidate.  Rows load ahead of the shuffle chain.
+// False when some block cannot continue the chain.
+__device__ bool t_scan_blocks(Work &W, uint64_t nsegs, uint64_t *d_count) {
     const int lane = lane_id();
-    const uint64_t NB = (nsegs + TB - 1) / TB;  // blocks 0 .. NB-1 (block 0 starts at segment 1)
-    uint32_t E = e1c;
-    uint64_t O = n0;
+    const uint64_t NB = (nsegs + TB - 1) / TB;
+    uint32_t E = 0;
+    uint64_t O = 0;
     for (uint64_t b0 = 0; b0 < NB; b0 += 4) {  // four blocks' rows per L2 round trip
         uint32_t C[4][4], S[4][4];
 #pragma unroll
@@ -825,88 +830,64 @@ __device__ bool t_scan_blocks(Work &W, uint64_t nsegs, uint32_t e1c, uint64_t n0
     return true;
 }
 
-// One T-mode attempt of walker g after its body walk (all 32 lanes).  Returns
-// true when the call's output was produced from the tables (this walker has
-// written its part); false to fall back to the halo walk.
+// One T-mode attempt of walker g, before any byte walk (all 32 lanes).
+// Returns true when the call's output was produced from the tables (this
+// walker has written its part); false to fall back to the speculative walk.
 template <int ALGO>
-__device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, const SpecEmit &em,
+__device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, const SegInfo &I,
                           uint8_t *ring, const uint8_t *fbase, uint64_t *bounds, uint64_t cap, uint64_t *d_count) {
     constexpr bool MAX = ALGO != ALGO_AE_MIN;
     const int lane = lane_id();
-    const SegInfo &I = em.I;
     const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
     uint32_t *ix = reinterpret_cast<uint32_t *>(ring);
     const int64_t lo = I.p - w - 1 > 0 ? I.p - w - 1 : 0;
     const int64_t ihi = I.seg_end + mx + 1 < Lf ? I.seg_end + mx + 1 : Lf;
-    uint32_t n = 0, e1c = T_BAD;
+    unsigned long long *tm = g_timing ? g_timing + TM_STAMPS + TM_PER_SEG * g : nullptr;
+    uint32_t n = 0;
     if (t_alive(W)) {
-        n = t_index<MAX>(fbase, lo, ihi, ix, T_IDX_CAP);
-        if (g_timing && lane == 0) g_timing[TM_STAMPS + TM_PER_SEG * g + 5] = globaltimer();
-        bool mine = n <= T_IDX_CAP && (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo);
-        if (mine && g == 0) {
-            // the true chain (this walker's) enters segment 1 at its first halo start
-            mine = false;
-            if (em.hcnt > 0) {
-                const int64_t e1 = I.seg_end + (int64_t)em.halo[0];
-                uint32_t d0;
-                const uint32_t KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
-                const int64_t satpos = ALGO == ALGO_RAM ? e1 - 1 : e1 - w - 1;
-                if (KN > 0 && KN <= (uint32_t)TK && satpos >= lo) {
-                    const uint32_t i = t_lb(ix, n, (uint32_t)(satpos - lo));
-                    if (i < n && lo + (int64_t)ix[i] == satpos && i >= d0 && i < d0 + KN) {
-                        e1c = i - d0;
-                        mine = true;
-                    }
-                }
-            }
-        } else if (mine) {
-            mine = t_table<ALGO>(G, W, g, I, ix, n, lo, ihi);
+        // a cheap look at the segment's first 16 KiB first: clearly sparse, no
+        // index (half the density the full check asks for: uniform bytes at
+        // w = 8 KiB give 64 +- 8 saturating bytes there, the bar is 8)
+        const int64_t shi = I.p + 16384 < ihi ? I.p + 16384 : ihi;
+        const uint32_t ns = t_index<MAX>(fbase, I.p, shi, I.p, ix, T_IDX_CAP);
+        bool mine = 2ull * ns * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(shi - I.p);
+        if (mine) {
+            n = t_index<MAX>(fbase, lo, ihi, lo, ix, T_IDX_CAP);
+            if (tm && lane == 0) tm[5] = globaltimer();
+            mine = n <= T_IDX_CAP && (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo) &&
+                   t_table<ALGO>(G, W, g, I, ix, n, lo, ihi);
+            if (tm && lane == 0) tm[6] = globaltimer();
         }
         if (!mine) t_fail(W);
-        if (g_timing && lane == 0) g_timing[TM_STAMPS + TM_PER_SEG * g + 6] = globaltimer();
     }
-    // arrive.  Walker 0 publishes the true chain's entry into segment 1; the
-    // last walker of a block composes the block; the last composer (or walker
-    // 0, if it comes last) scans the blocks.  The verdict word T_SCAN decides
-    // once (compare-and-swap from ~0): 1 = the tables produced the output.
-    unsigned long long *tm = g_timing ? g_timing + TM_STAMPS + TM_PER_SEG * g : nullptr;
+    // arrive: the last walker of a block composes the block, the last composer
+    // scans the blocks.  The verdict word T_SCAN decides once (compare-and-
+    // swap from ~0): 1 = the tables produced the output, 0 = fall back.
     const uint64_t NB = (nsegs + TB - 1) / TB;
-    bool scanner = false;
+    const uint64_t b = g / TB;
+    const uint64_t members = ((b + 1) * TB < nsegs ? (b + 1) * TB : nsegs) - t_blk_lo(b);
+    bool composer = false, scanner = false;
     __syncwarp();
-    if (g == 0) {
+    if (lane == 0) {
+        if (tm) tm[2] = globaltimer();  // diagnostics: table published
+        __threadfence();
+        composer = atomicAdd(W.tblk + b, 1u) + 2u == (uint32_t)members;  // starts at ~0
+    }
+    composer = __shfl_sync(0xFFFFFFFFu, composer, 0);
+    if (composer) {
+        __threadfence();
+        if (t_alive(W)) t_compose(W, b, nsegs);
+        __syncwarp();
         if (lane == 0) {
-            st_relaxed_u32(W.ctrl + T_E1, e1c);
-            st_relaxed_u32(W.ctrl + T_N0, em.cnt);
             __threadfence();
-            scanner = atomicAdd(W.ctrl + T_ARRIVE, 1u) + 1u == (uint32_t)NB;  // starts at ~0: +1 = arrivals - 1
-        }
-    } else {
-        const uint64_t b = g / TB;
-        const uint64_t members = ((b + 1) * TB < nsegs ? (b + 1) * TB : nsegs) - t_blk_lo(b);
-        bool composer = false;
-        if (lane == 0) {
-            if (tm) tm[2] = globaltimer();  // diagnostics: table published
-            __threadfence();
-            composer = atomicAdd(W.tblk + b, 1u) + 2u == (uint32_t)members;  // starts at ~0
-        }
-        composer = __shfl_sync(0xFFFFFFFFu, composer, 0);
-        if (composer) {
-            __threadfence();
-            if (t_alive(W)) t_compose(W, b, nsegs);
-            __syncwarp();
-            if (lane == 0) {
-                __threadfence();
-                scanner = atomicAdd(W.ctrl + T_ARRIVE, 1u) + 1u == (uint32_t)NB;
-            }
+            scanner = atomicAdd(W.ctrl + T_ARRIVE, 1u) + 2u == (uint32_t)NB;
         }
     }
     scanner = __shfl_sync(0xFFFFFFFFu, scanner, 0);
-    uint32_t verdict = 0;
-    if (scanner) {  // every block composed and walker 0 arrived
+    if (scanner) {  // every block composed
         __threadfence();
         bool ok = t_alive(W) && nsegs >= 2;
-        const uint32_t e1 = ld_relaxed_u32(W.ctrl + T_E1), n0 = ld_relaxed_u32(W.ctrl + T_N0);
-        if (ok) ok = e1 != T_BAD && t_scan_blocks(W, nsegs, e1, n0, d_count);
+        if (ok) ok = t_scan_blocks(W, nsegs, d_count);
         __syncwarp();
         if (lane == 0) {
             __threadfence();
@@ -914,6 +895,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
             if (tm) tm[3] = globaltimer();
         }
     }
+    uint32_t verdict = 0;
     if (lane == 0) {
         const unsigned long long t0 = globaltimer();
         uint32_t ns = 64;
@@ -930,22 +912,16 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
     }
     verdict = __shfl_sync(0xFFFFFFFFu, verdict, 0);
     if (verdict != 1u) return false;
-    // this segment's part of the true chain
-    if (g == 0) {
-        for (uint32_t i = lane; i < em.cnt; i += 32) {
-            const uint64_t v = (uint64_t)I.p + em.list[i];
-            if (i >= 1 && i - 1 < cap) bounds[i - 1] = v;
-        }
-    } else if (lane == 0) {
-        const uint64_t b = g / TB;
+    // this segment's part of the true chain (lane 0 walks it in index space)
+    if (lane == 0) {
         const uint32_t Eb = W.tbe[b];
         const uint32_t E = W.tp[g * TK + Eb];
         uint64_t q = W.tbo[b] + W.tq[g * TK + Eb];
-        uint32_t c0;
-        t_cands<ALGO>(ix, n, lo, I.p, w, c0);
-        int64_t x = t_start_of(ALGO, lo + (int64_t)ix[c0 + E], w);
+        uint32_t c0 = 0;
+        if (g > 0) t_cands<ALGO>(ix, n, lo, I.p, w, c0);
+        int64_t x = t_cand_start<ALGO>(g, ix, lo, c0, E, w);
         while (x >= 0 && x < I.seg_end) {
-            if (q >= 1 && q - 1 < cap) bounds[q - 1] = (uint64_t)x;
+            if (q >= 1 && q - 1 < cap) bounds[q - 1] = (uint64_t)x;  // the stream start is not a boundary
             ++q;
             x = t_step<ALGO>(ix, n, lo, ihi, x, w, mx, Lf);
         }
@@ -976,35 +952,28 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     em.sa = em.sb = 0;
     em.lp.reset();
     em.published = false;
-    em.tflag = TM ? 1 : 0;
     if (lane == 0) st_relaxed_u32(em.list, 0u);  // the speculative chain starts at the segment's first byte
     unsigned long long *tm = g_timing ? g_timing + TM_STAMPS : nullptr;
     em.tbody = tm ? tm + TM_PER_SEG * g + 1 : nullptr;
     if (tm && lane == 0) tm[TM_PER_SEG * g] = globaltimer();
     const uint8_t *fbase = G.data + em.I.foff;
-    int64_t read_end = (g == em.I.last) ? (int64_t)em.I.Lf
-                                        : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
-    // the segment's head is read again by the previous segment's halo walk: keep it in L2
-    const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
-    run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
-    em.publish();
-    if constexpr (TM) {
-        if (t_attempt<ALGO>(G, W, g, nsegs, em, R.buf, fbase, bounds, cap, d_count)) {
+    if constexpr (TM) {  // transfer tables first: on a saturated stream no byte walk is needed
+        if (t_attempt<ALGO>(G, W, g, nsegs, em.I, R.buf, fbase, bounds, cap, d_count)) {
             if (lane == 0) {  // for cdc_stats: a table segment has no halo
-                W.cnt[g] = em.cnt;
+                W.cnt[g] = 0;
                 W.hcnt[g] = 0;
                 W.sj[g] = SJ_TABLE;
                 if (tm) tm[TM_PER_SEG * g + 3] = globaltimer();
             }
             return;
         }
-        if (em.tflag == 2) {  // resume the halo walk where the attempt stopped it
-            em.tflag = 0;
-            run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.seg_end + (int64_t)em.halo[em.hcnt - 1], read_end,
-                            G.w, G.max_size, stream_policy(), em);
-        }
-        em.tflag = 0;
     }
+    int64_t read_end = (g == em.I.last) ? (int64_t)em.I.Lf
+                                        : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
+    // the segment's head is read again by the previous segment's halo walk: keep it in L2
+    const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
+    run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
+    em.publish();
     if (tm && lane == 0) {
         tm[TM_PER_SEG * g + 2] = globaltimer();
         tm[TM_PER_SEG * g + 4] = smid() | ((unsigned long long)em.hcnt << 32);

@@ -51,11 +51,11 @@ hw = walk - body
 print("halo walk us: p50 %.1f p90 %.1f p99 %.1f max %.1f; per halo chunk us: mean %.2f" % (
     *np.percentile(hw, [50, 90, 99]), hw.max(), hw.sum() / max(1, halo.sum())))
 if (a[:, 5] > 0).any():
-    ok = (a[:, 5] > 0) & (a[:, 6] > 0) & (a[:, 1] > 0)
-    ib = (a[ok, 5] - a[ok, 1]) / 1e3
+    ok = (a[:, 5] > 0) & (a[:, 6] > 0)
+    ib = (a[ok, 5] - a[ok, 0]) / 1e3
     tb = (a[ok, 6] - a[ok, 5]) / 1e3
-    print("T-mode: index pass us p50 %.1f max %.1f; table us p50 %.1f max %.1f" % (
-        np.percentile(ib, 50), ib.max(), np.percentile(tb, 50), tb.max()))
+    print("T-mode: from start to index built us p50 %.1f max %.1f; table us p50 %.1f max %.1f" % (
+        np.percentile(ib, 50) if ib.size else 0, ib.max() if ib.size else 0, np.percentile(tb, 50) if tb.size else 0, tb.max() if tb.size else 0))
 print("walk end us (abs): p50 %.1f p90 %.1f max %.1f" % tuple(np.percentile(start + walk, [50, 90, 100])))
 print("done us (abs): p50 %.1f max %.1f" % (np.percentile(done, 50), done.max()))
 print("halo chunks: mean %.2f max %d" % (halo.mean(), halo.max()))
