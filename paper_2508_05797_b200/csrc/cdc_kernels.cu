@@ -570,13 +570,17 @@ __device__ __forceinline__ bool t_alive(const Work &W) { return ld_relaxed_u32(W
 #endif
 constexpr int TIX_G = CDC_TIX_G;  // 16-byte granules per lane per step of the index pass
 template <bool MAX>
-__device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_t rel, uint32_t *ix, uint32_t cap) {
+__device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_t rel, uint32_t *ix, uint32_t cap,
+                            const uint32_t *alive = nullptr) {
     const int lane = lane_id();
     const uintptr_t fb = reinterpret_cast<uintptr_t>(fbase);
     const uintptr_t a0 = (fb + (uintptr_t)lo) & ~(uintptr_t)15;
     const uintptr_t a1 = fb + (uintptr_t)hi;
     uint32_t n = 0;
+    int step = 0;
     for (uintptr_t a = a0; a < a1; a += 32 * 16 * TIX_G) {
+        // the attempt may already have failed elsewhere: look every 64 KiB
+        if (alive && (++step & 7) == 0 && ld_relaxed_u32(alive) == 0u) return cap + 1;
         const uintptr_t la = a + (uintptr_t)lane * 16 * TIX_G;
         uint32_t m[TIX_G];
 #pragma unroll
@@ -852,7 +856,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         const uint32_t ns = t_index<MAX>(fbase, I.p, shi, I.p, ix, T_IDX_CAP);
         bool mine = 2ull * ns * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(shi - I.p);
         if (mine) {
-            n = t_index<MAX>(fbase, lo, ihi, lo, ix, T_IDX_CAP);
+            n = t_index<MAX>(fbase, lo, ihi, lo, ix, T_IDX_CAP, W.ctrl + T_ALL);
             if (tm && lane == 0) tm[5] = globaltimer();
             mine = n <= T_IDX_CAP && (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo) &&
                    t_table<ALGO>(G, W, g, I, ix, n, lo, ihi);
@@ -1719,6 +1723,12 @@ bool sync_debug() {
         }                                                                      \
     } while (0)
 
+// Transfer tables are tried only for segments up to T_MAX_SEG: larger segments
+// amortise their halos anyway, and a failed attempt (a stream saturated only
+// in parts, such as configs[2]'s uniform base with zero-filled regions at
+// 453 KB segments) costs ~5 % there.
+constexpr uint64_t T_MAX_SEG = 256ull << 10;
+
 // CDC_TMODE=0 disables the transfer-table attempt (a debugging and testing knob)
 int tmode_on() {
     static int v = -1;
@@ -1960,7 +1970,9 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     }
     ++launches;
     mark(1);
-    const uint64_t nseg_ub = P.max_segs;
+    // segments: exact for a single stream (nseg_of), an upper bound for a batch
+    const uint64_t nseg_ub = batch ? P.max_segs
+                                   : (total_len == 0 ? 0 : (total_len < P.S ? 1 : total_len / P.S));
     // segments per CTA: SPEC_WARPS, or fewer when the input has fewer segments
     // than walkers fit on the GPU (one walker per SM for a small stream)
     const uint64_t nsm = (uint64_t)num_sms();
@@ -1970,7 +1982,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     // enough for slow convergence, segments short enough for their halos to
     // matter, and a grid that is one co-resident wave (the attempt waits for
     // every walker; it also gives up after a timeout)
-    G.tmode = (!batch && tmode_on() && p->window >= 4096 && P.S <= (1ull << 20) && nseg_ub >= 3 &&
+    G.tmode = (!batch && tmode_on() && p->window >= 4096 && P.S <= T_MAX_SEG && nseg_ub >= 3 &&
                blocks <= nsm) ? 1 : 0;
     if (blocks > 0) {
         int fused = (P.cap_list + P.cap_halo < (1u << 23)) ? fused_mode() : 0;

@@ -92,6 +92,11 @@ if "c2" in sel:  # configs[2]: the 1 GiB base and its last snapshot, AE and RAM 
             for avg in (4096, 8192, 16384):
                 run(name, d, algo, avg, reps=3)
     del snaps
+if "u1g" in sel:  # a whole 1 GiB uniform stream (453 KB segments: transfer tables near their capacity)
+    u = synth.uniform(1 << 30, 4)
+    for algo in ("ram", "ae_max"):
+        run("uniform 1GiB", u, algo, 8192, reps=3)
+    del u
 if "c4full" in sel:  # configs[4], one GPU's 8 GiB share of the 64 GiB stream
     d = synth.alternating(8 << 30, region=256 << 20, seed=5)
     run("c4 alternating 8GiB (1/8)", d, "ram", 8192, reps=3)
