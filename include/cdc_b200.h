@@ -112,7 +112,12 @@ int cdc_workspace_size(const cdc_params *p, uint64_t nfiles, uint64_t total_len,
  *              offsets (ascending, last = len).
  *   d_count  : device uint64[1]; receives the number of boundaries (may
  *              exceed bounds_cap, see overflow above).
- * Asynchronous on `stream`.
+ * Asynchronous on `stream`.  The chain is resolved by speculative segments
+ * (DESIGN.md §1); when window >= 4096 and the segments are at most 256 KiB,
+ * the walkers first try the transfer tables of DESIGN.md §6 (streams whose
+ * every chunk step is decided by saturating bytes, e.g. uniform bytes at
+ * 8-16 KiB) and fall back to the speculative walk otherwise.  The output is
+ * the same either way: PAPER.md §2.1.2's chain, bit for bit.
  */
 int cdc_chunk(const cdc_params *p, const uint8_t *d_data, uint64_t len,
               uint64_t *d_bounds, uint64_t bounds_cap, uint64_t *d_count,
