@@ -86,6 +86,7 @@ struct Work {
 };
 
 enum : int32_t { SJ_UNSYNCED = -1, SJ_STREAM_END = -2, SJ_LAST = -3, SJ_TABLE = -4 };
+constexpr int DYN_TICKET = 9;  // ctrl[9] (reset to ~0): a batch's per-warp segment tickets
 
 // dynamic shared memory follows the kernel's static shared variables: round the
 // ring up to 128 bytes (TMA destinations need 16, LDS.128 16; launches add 128)
@@ -511,10 +512,24 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
         s_ticket = atomicAdd(W.ctrl, 1u) + 1u;  // counter starts at ~0
     }
     __syncthreads();
+    const uint64_t nsegs = total_segs(G, W);
+    if (spw == 0) {
+        // a batch: every warp takes segments one at a time from a global ticket
+        // (segments of very different sizes; earlier segments are always taken
+        // first, and without the fused write no warp waits on another)
+        for (;;) {
+            uint32_t t = 0;
+            if (lane_id() == 0) t = atomicAdd(W.ctrl + DYN_TICKET, 1u) + 1u;  // counter starts at ~0
+            const uint64_t g = __shfl_sync(0xFFFFFFFFu, t, 0);
+            if (g >= nsegs) break;
+            speculate_segment<ALGO, TM>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count,
+                                        fused);
+        }
+        return;
+    }
     // spw segments per CTA (contiguous, so every predecessor is in this or an
     // earlier ticket); fewer than SPEC_WARPS spread a small input over the SMs
     const uint64_t g = (uint64_t)s_ticket * spw + warp;
-    const uint64_t nsegs = total_segs(G, W);
     if (warp >= spw || g >= nsegs) return;
     speculate_segment<ALGO, TM>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused);
     if (lane_id() == 0) stamp(TM_SPEC_END);
@@ -1976,8 +1991,13 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     // segments per CTA: SPEC_WARPS, or fewer when the input has fewer segments
     // than walkers fit on the GPU (one walker per SM for a small stream)
     const uint64_t nsm = (uint64_t)num_sms();
-    const int spw = (int)std::min<uint64_t>(std::max<uint64_t>((nseg_ub + nsm - 1) / nsm, 1), cdc::SPEC_WARPS);
-    const uint64_t blocks = (nseg_ub + spw - 1) / spw;
+    // (a batch: spw = 0, one wave of CTAs whose warps take segments from a global
+    // ticket, which balances files of very different sizes)
+    const int spw = batch ? 0
+                          : (int)std::min<uint64_t>(std::max<uint64_t>((nseg_ub + nsm - 1) / nsm, 1), cdc::SPEC_WARPS);
+    const uint64_t blocks = batch ? std::min<uint64_t>((nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS,
+                                                       nsm * cdc::SPEC_CTAS_PER_SM)
+                                  : (nseg_ub + spw - 1) / spw;
     // transfer tables: a single stream of at least two segments, windows long
     // enough for slow convergence, segments short enough for their halos to
     // matter, and a grid that is one co-resident wave (the attempt waits for
@@ -1985,7 +2005,10 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     G.tmode = (!batch && tmode_on() && p->window >= 4096 && P.S <= T_MAX_SEG && nseg_ub >= 3 &&
                blocks <= nsm) ? 1 : 0;
     if (blocks > 0) {
-        int fused = (P.cap_list + P.cap_halo < (1u << 23)) ? fused_mode() : 0;
+        // the fused look-back makes each segment wait for its predecessors: with
+        // dynamic tickets (a batch) the waits would queue behind the largest file,
+        // so a batch leaves the splice and the writes to k_fixup
+        int fused = (!batch && P.cap_list + P.cap_halo < (1u << 23)) ? fused_mode() : 0;
         const void *kspec = G.tmode ? reinterpret_cast<const void *>(cdc::k_speculate<ALGO, true>)
                                     : reinterpret_cast<const void *>(cdc::k_speculate<ALGO, false>);
         CDC_CUDA(launch_pdl(kspec, dim3((unsigned)blocks),

@@ -54,7 +54,7 @@ def run_batch(name, data_np, offs, algo, avg, reps=5):
     """cdc_chunk_batch on preallocated device buffers (the host-side setup of
     api.chunk_batch is outside the timed region)."""
     t = torch.from_numpy(data_np).cuda()
-    p = cdc.params(algo, avg_size=avg)
+    p = cdc.params(algo, avg_size=avg, seg_bytes=int(os.environ.get("SEG", "0")))
     sizes = np.diff(offs)
     total, max_len = int(sizes.sum()), int(sizes.max())
     od = torch.from_numpy(np.asarray(offs, dtype=np.int64)).cuda()
