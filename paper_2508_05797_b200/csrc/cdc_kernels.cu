@@ -491,7 +491,11 @@ __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_
 
 template <int ALGO, bool TM>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
-                                  uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused);
+                                  uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused,
+                                  int64_t pre_n = -1);
+
+template <int ALGO>
+__device__ int64_t t_coop_index(const Geometry &G, Work &W, uint64_t g, uint8_t *rings);
 
 // K1.  One warp per segment (CTAs take segment groups in ticket order).  In
 // the common case the fused look-back writes the output and k_fixup (launched
@@ -530,8 +534,16 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
     // spw segments per CTA (contiguous, so every predecessor is in this or an
     // earlier ticket); fewer than SPEC_WARPS spread a small input over the SMs
     const uint64_t g = (uint64_t)s_ticket * spw + warp;
+    int64_t pre_n = -1;
+    if constexpr (TM) {
+        if (spw == 1) {  // one segment per CTA: its 16 warps build the index together
+            if ((uint64_t)s_ticket >= nsegs) return;  // uniform across the CTA
+            pre_n = t_coop_index<ALGO>(G, W, (uint64_t)s_ticket, align_smem(smem));
+        }
+    }
     if (warp >= spw || g >= nsegs) return;
-    speculate_segment<ALGO, TM>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused);
+    speculate_segment<ALGO, TM>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused,
+                                pre_n);
     if (lane_id() == 0) stamp(TM_SPEC_END);
 }
 
@@ -854,7 +866,8 @@ __device__ bool t_scan_blocks(Work &W, uint64_t nsegs, uint64_t *d_count) {
 // walker has written its part); false to fall back to the speculative walk.
 template <int ALGO>
 __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, const SegInfo &I,
-                          uint8_t *ring, const uint8_t *fbase, uint64_t *bounds, uint64_t cap, uint64_t *d_count) {
+                          uint8_t *ring, const uint8_t *fbase, uint64_t *bounds, uint64_t cap, uint64_t *d_count,
+                          int64_t pre_n) {
     constexpr bool MAX = ALGO != ALGO_AE_MIN;
     const int lane = lane_id();
     const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
@@ -863,7 +876,14 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
     const int64_t ihi = I.seg_end + mx + 1 < Lf ? I.seg_end + mx + 1 : Lf;
     unsigned long long *tm = g_timing ? g_timing + TM_STAMPS + TM_PER_SEG * g : nullptr;
     uint32_t n = 0;
-    if (t_alive(W)) {
+    if (pre_n >= 0) {  // the CTA built the index together (t_coop_index)
+        n = (uint32_t)pre_n;
+        const bool mine = t_alive(W) && n <= T_IDX_CAP &&
+                          (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo) &&
+                          t_table<ALGO>(G, W, g, I, ix, n, lo, ihi);
+        if (tm && lane == 0) tm[6] = globaltimer();
+        if (!mine) t_fail(W);
+    } else if (t_alive(W)) {
         // a cheap look at the segment's first 16 KiB first: clearly sparse, no
         // index (half the density the full check asks for: uniform bytes at
         // w = 8 KiB give 64 +- 8 saturating bytes there, the bar is 8)
@@ -952,9 +972,66 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
     return true;
 }
 
+// T-mode, one segment per CTA (a small stream): the CTA's 16 warps index the
+// saturating bytes of [p - w - 1, seg_end + max_size + 1) together, one
+// sixteenth each into their own rings, and warp 0 concatenates the parts in
+// order into its ring.  Returns the entry count for warp 0 (T_IDX_CAP + 1:
+// not dense or too many), or -1 when the attempt is already off.  All threads
+// of the CTA call this.
+template <int ALGO>
+__device__ int64_t t_coop_index(const Geometry &G, Work &W, uint64_t g, uint8_t *rings) {
+    constexpr bool MAX = ALGO != ALGO_AE_MIN;
+    __shared__ uint32_t s_cnt[SPEC_WARPS];
+    __shared__ int s_go;
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const SegInfo I = seg_info(G, W, g);
+    const uint8_t *fbase = G.data + I.foff;
+    const int64_t w = G.w, Lf = (int64_t)I.Lf;
+    const int64_t lo = I.p - w - 1 > 0 ? I.p - w - 1 : 0;
+    const int64_t ihi = I.seg_end + (int64_t)G.max_size + 1 < Lf ? I.seg_end + (int64_t)G.max_size + 1 : Lf;
+    uint32_t *ix = reinterpret_cast<uint32_t *>(rings + warp * RING_SMEM);
+    if (warp == 0) {  // the density sample of t_attempt
+        int go = 0;
+        if (t_alive(W)) {
+            const int64_t shi = I.p + 16384 < ihi ? I.p + 16384 : ihi;
+            const uint32_t ns = t_index<MAX>(fbase, I.p, shi, I.p, ix, T_IDX_CAP);
+            go = 2ull * ns * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(shi - I.p) ? 1 : 2;
+        }
+        if (lane == 0) s_go = go;
+    }
+    __syncthreads();
+    const int go = s_go;
+    if (go == 0) return -1;
+    if (go == 1) {
+        const int64_t part = (((ihi - lo) + 16 * SPEC_WARPS - 1) / (16 * SPEC_WARPS)) * 16;
+        const int64_t a = lo + warp * part, b = a + part < ihi ? a + part : ihi;
+        const uint32_t c = a < b ? t_index<MAX>(fbase, a, b, lo, ix, T_IDX_CAP) : 0u;
+        if (lane == 0) s_cnt[warp] = c;
+    }
+    __syncthreads();
+    if (go == 2) {
+        if (warp == 0) t_fail(W);
+        return (int64_t)T_IDX_CAP + 1;
+    }
+    if (warp != 0) return 0;  // only warp 0 walks the segment
+    uint32_t n = 0;
+    for (int k = 0; k < SPEC_WARPS; ++k) {
+        const uint32_t c = s_cnt[k];
+        if (c > T_IDX_CAP || n + c > T_IDX_CAP) return (int64_t)T_IDX_CAP + 1;
+        if (k > 0) {
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(rings + k * RING_SMEM);
+            for (uint32_t i = lane; i < c; i += 32) ix[n + i] = src[i];
+        }
+        n += c;
+    }
+    __syncwarp();
+    return (int64_t)n;
+}
+
 template <int ALGO, bool TM>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
-                                  uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused) {
+                                  uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused,
+                                  int64_t pre_n) {
     const int lane = lane_id();
     WarpRing R{wbase, reinterpret_cast<uint64_t *>(wbase + RING_BYTES)};
 
@@ -977,7 +1054,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     if (tm && lane == 0) tm[TM_PER_SEG * g] = globaltimer();
     const uint8_t *fbase = G.data + em.I.foff;
     if constexpr (TM) {  // transfer tables first: on a saturated stream no byte walk is needed
-        if (t_attempt<ALGO>(G, W, g, nsegs, em.I, R.buf, fbase, bounds, cap, d_count)) {
+        if (t_attempt<ALGO>(G, W, g, nsegs, em.I, R.buf, fbase, bounds, cap, d_count, pre_n)) {
             if (lane == 0) {  // for cdc_stats: a table segment has no halo
                 W.cnt[g] = 0;
                 W.hcnt[g] = 0;
