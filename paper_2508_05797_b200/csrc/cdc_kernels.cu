@@ -76,7 +76,9 @@ struct Work {
     // transfer tables (T-mode, saturated streams): per segment TK candidates
     uint32_t *tl;                // G x TK link: candidate k of g -> candidate of g+1 (T_END, T_BAD)
     uint32_t *tn;                // G x TK chain starts of candidate k inside the segment
-    uint32_t *tk;                // G: number of candidates
+    uint32_t *tk;                // G: table rows in use (candidates, then entries from the previous segment)
+    int64_t *tex;                // G x TEX: exits of segment g that are not candidates of g+1 (its extra entries)
+    uint32_t *tnx;               // G: their count, published after phase 1 (reset to ~0)
     uint32_t *tp, *tq;           // G x TK: for entry k of the segment's block, its entry candidate and
                                  // the chain starts in the block before it
     uint32_t *tbc, *tbs;         // NB x TK: block tables (entry -> next block's entry, starts inside)
@@ -573,7 +575,8 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
 // candidate, or any segment that is not dense makes the whole call fall back
 // to the speculative walk (the tables are tried only for a single stream
 // whose grid is one co-resident wave, with a timeout).
-constexpr int TK = 128;                      // candidates per segment, 4 per lane
+constexpr int TK = 128;                      // table rows per segment (candidates + extra entries), 4 per lane
+constexpr int TEX = 32;                      // extra entries a segment can pass to the next one
 constexpr uint32_t T_END = 0xFFFFFFFEu;      // link: the chain reached the stream end
 constexpr uint32_t T_BAD = 0xFFFFFFFFu;      // link: not resolvable in index space
 constexpr uint32_t T_DENSE = 8;              // saturating bytes per window a segment needs
@@ -686,6 +689,91 @@ __device__ __forceinline__ int64_t t_step(const uint32_t *ix, uint32_t n, int64_
     }
 }
 
+// One chunk step from start x read from the bytes themselves (one lane, any
+// data): the rules of PAPER.md §2.1.2 exactly as run_chain applies them, for
+// the steps the index cannot decide (a window without a saturating byte, e.g.
+// inside a zero-filled region).  16-byte loads, a byte-extreme test per
+// granule, a byte loop only in the granule that holds the answer.
+template <bool MAX>
+__device__ __forceinline__ uint4 t_granule(const uint8_t *fbase, uintptr_t ga, int64_t a, int64_t b, int64_t &pos0) {
+    uint4 v = *reinterpret_cast<const uint4 *>(ga);
+    pos0 = (int64_t)(ga - reinterpret_cast<uintptr_t>(fbase));
+    if (pos0 < a || pos0 + 16 > b) {  // neutralise the bytes outside [a, b)
+        const int x0 = (int)(a - pos0 > 0 ? (a - pos0 > 16 ? 16 : a - pos0) : 0);
+        const int x1 = (int)(b - pos0 < 16 ? (b - pos0 < 0 ? 0 : b - pos0) : 16);
+        const uint32_t m16 = x0 < x1 ? (((1u << x1) - 1u) & ~((1u << x0) - 1u)) : 0u;
+        uint32_t k[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) k[j] = (((((m16 >> (4 * j)) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu);
+        if (MAX) { v.x &= k[0]; v.y &= k[1]; v.z &= k[2]; v.w &= k[3]; }
+        else { v.x |= ~k[0]; v.y |= ~k[1]; v.z |= ~k[2]; v.w |= ~k[3]; }
+    }
+    return v;
+}
+// extreme of the bytes [a, b) (a < b)
+template <bool MAX>
+__device__ uint32_t t_bytes_ext(const uint8_t *fbase, int64_t a, int64_t b) {
+    const uintptr_t fb = reinterpret_cast<uintptr_t>(fbase);
+    uint32_t acc = neutral<MAX>();
+    for (uintptr_t ga = (fb + (uintptr_t)a) & ~(uintptr_t)15; ga < fb + (uintptr_t)b; ga += 16) {
+        int64_t pos0;
+        acc = ext2<MAX>(acc, vext16<MAX>(t_granule<MAX>(fbase, ga, a, b, pos0)));
+        if (acc == (MAX ? 255u : 0u)) break;
+    }
+    return acc;
+}
+// first position in [a, b) whose byte satisfies (byte CMP t), or -1
+template <int CMP>
+__device__ int64_t t_bytes_find(const uint8_t *fbase, int64_t a, int64_t b, uint32_t t) {
+    constexpr bool MAX = (CMP == CMP_GT || CMP == CMP_GEQ);
+    const uintptr_t fb = reinterpret_cast<uintptr_t>(fbase);
+    for (uintptr_t ga = (fb + (uintptr_t)a) & ~(uintptr_t)15; ga < fb + (uintptr_t)b; ga += 16) {
+        int64_t pos0;
+        const uint4 v = t_granule<MAX>(fbase, ga, a, b, pos0);
+        if (!cmp_holds<CMP>(vext16<MAX>(v), t)) continue;
+        for (int j = 0; j < 16; ++j) {
+            const int64_t pos = pos0 + j;
+            if (pos >= a && pos < b && cmp_holds<CMP>(vbyte(v, j), t)) return pos;
+        }
+    }
+    return -1;
+}
+template <int ALGO>
+__device__ int64_t t_step_bytes(const uint8_t *fbase, int64_t x, int64_t w, int64_t mx, int64_t Lf) {
+    const int64_t limit = Lf - x < mx ? Lf : x + mx;
+    if constexpr (ALGO == ALGO_RAM) {
+        if (x + w >= Lf) return Lf;  // the window does not fit: a single final chunk
+        const uint32_t M = t_bytes_ext<true>(fbase, x, x + w);
+        const int64_t i = x + w < limit ? t_bytes_find<CMP_GEQ>(fbase, x + w, limit, M) : -1;
+        return i >= 0 ? i + 1 : limit;
+    } else {
+        constexpr bool MAX = ALGO == ALGO_AE_MAX;
+        constexpr int CMP = MAX ? CMP_GT : CMP_LT;
+        int64_t t = x;
+        uint32_t v = fbase[x];
+        while (t + w < limit) {
+            const int64_t r = t_bytes_find<CMP>(fbase, t + 1, t + w + 1, v);
+            if (r < 0) return t + w + 1;  // the target is unbeaten over its window
+            t = r;
+            v = fbase[r];
+        }
+        return limit;
+    }
+}
+// one chunk step: from the index when it decides the step, else from the
+// bytes while the chain's budget of byte steps lasts (a lane reads up to a
+// window per byte step; long unsaturated stretches, such as large zero-filled
+// regions, are left to the speculative walk): -1 when the budget is spent
+constexpr int T_BYTE_STEPS = 4;
+template <int ALGO>
+__device__ __forceinline__ int64_t t_next(const uint8_t *fbase, const uint32_t *ix, uint32_t n, int64_t lo,
+                                          int64_t ihi, int64_t x, int64_t w, int64_t mx, int64_t Lf, int &budget) {
+    const int64_t y = t_step<ALGO>(ix, n, lo, ihi, x, w, mx, Lf);
+    if (y >= 0) return y;
+    if (--budget < 0) return -1;
+    return t_step_bytes<ALGO>(fbase, x, w, mx, Lf);
+}
+
 // candidates of segment [pa, ...): index range [*i0, *i0 + K) of their
 // saturating positions; K = 0 when they are not all inside the index
 template <int ALGO>
@@ -711,45 +799,116 @@ __device__ __forceinline__ int64_t t_cand_start(uint64_t g, const uint32_t *ix, 
     return g == 0 ? 0 : t_start_of(ALGO, lo + (int64_t)ix[c0 + k], w);
 }
 
-// Transfer table of segment g into W.tl / W.tn; false when the segment cannot
-// be resolved in index space.  ix holds the index already.
+// link of a chain that exits segment g at x: the index of x among the
+// candidates of g+1 (d0 .. d0+KN-1 in the index), T_END at the stream end, or
+// T_BAD when x is not a candidate
 template <int ALGO>
-__device__ bool t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint32_t *ix, uint32_t n,
-                        int64_t lo, int64_t ihi) {
+__device__ __forceinline__ uint32_t t_link(const uint32_t *ix, uint32_t n, int64_t lo, int64_t x, int64_t w,
+                                           int64_t Lf, bool last, uint32_t d0, uint32_t KN) {
+    if (last) return x >= Lf ? T_END : T_BAD;
+    const int64_t satpos = ALGO == ALGO_RAM ? x - 1 : x - w - 1;
+    if (satpos < lo) return T_BAD;
+    const uint32_t i = t_lb(ix, n, (uint32_t)(satpos - lo));
+    return (i < n && lo + (int64_t)ix[i] == satpos && i >= d0 && i < d0 + KN) ? i - d0 : T_BAD;
+}
+
+// Transfer table of segment g, phase 1: the rows of its candidates (W.tl,
+// W.tn).  A chain whose exit is not a candidate of g+1 (its last step was not
+// saturated) becomes an extra entry of g+1: its start goes to W.tex[g] and
+// its link to KN + j; the count is published in W.tnx[g] for phase 2 of g+1.
+// Returns K (0 when the segment cannot be resolved in index space).
+template <int ALGO>
+__device__ uint32_t t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint8_t *fbase,
+                            const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi) {
     const int lane = lane_id();
     const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
     uint32_t c0 = 0;
     const uint32_t K = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, I.p, w, c0);
-    if (K == 0 || K > (uint32_t)TK) return false;
-    // candidates of the next segment, for the links
     uint32_t d0 = 0, KN = 0;
     const bool last = g == I.last;
-    if (!last) {
-        KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
-        if (KN == 0 || KN > (uint32_t)TK) return false;
+    if (!last) KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
+    if (K == 0 || K > (uint32_t)TK || (!last && (KN == 0 || KN > (uint32_t)TK))) {
+        if (lane == 0) st_release_u32(W.tnx + g, 0u);
+        return 0;
     }
-    for (uint32_t k = lane; k < K; k += 32) {
-        int64_t x = t_cand_start<ALGO>(g, ix, lo, c0, k, w);
+    uint32_t nx = 0;  // extra entries passed on so far
+    for (uint32_t k0 = 0; k0 < K; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        int64_t x = -1;
         uint32_t cnt = 0;
-        while (x >= 0 && x < I.seg_end) {
-            ++cnt;
-            x = t_step<ALGO>(ix, n, lo, ihi, x, w, mx, Lf);
-        }
-        uint32_t link = T_BAD;
-        if (x >= Lf && last) {
-            link = T_END;
-        } else if (x >= 0 && !last) {
-            // the exit must be the start of one of the next segment's candidates
-            const int64_t satpos = ALGO == ALGO_RAM ? x - 1 : x - w - 1;
-            if (satpos >= lo) {
-                const uint32_t i = t_lb(ix, n, (uint32_t)(satpos - lo));
-                if (i < n && lo + (int64_t)ix[i] == satpos && i >= d0 && i < d0 + KN) link = i - d0;
+        if (k < K) {
+            x = t_cand_start<ALGO>(g, ix, lo, c0, k, w);
+            int budget = T_BYTE_STEPS;
+            while (x >= 0 && x < I.seg_end) {
+                ++cnt;
+                x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
             }
         }
-        W.tl[g * TK + k] = link;
-        W.tn[g * TK + k] = cnt;
+        uint32_t link = k < K && x >= 0 ? t_link<ALGO>(ix, n, lo, x, w, Lf, last, d0, KN) : T_BAD;
+        const bool extra = k < K && x >= 0 && link == T_BAD && !last;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, extra);
+        if (extra) {
+            const uint32_t j = nx + __popc(bal & ((1u << lane) - 1u));
+            if (j < (uint32_t)TEX && KN + j < (uint32_t)TK) {
+                W.tex[g * TEX + j] = x;
+                link = KN + j;
+            }
+        }
+        nx += __popc(bal);
+        if (k < K) {
+            W.tl[g * TK + k] = link;
+            W.tn[g * TK + k] = cnt;
+        }
     }
-    if (lane == 0) W.tk[g] = K;
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();
+        st_release_u32(W.tnx + g, nx < (uint32_t)TEX ? nx : (uint32_t)TEX);
+    }
+    return K;
+}
+
+// Phase 2: the rows of the extra entries segment g-1 passed on (rows K ..
+// K+X-1).  Their exits must be candidates of g+1 (no second hand-over).
+template <int ALGO>
+__device__ bool t_table_extras(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint8_t *fbase,
+                               const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi, uint32_t K) {
+    const int lane = lane_id();
+    const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
+    uint32_t X = 0;
+    if (g > 0) {
+        if (lane == 0) {
+            const unsigned long long t0 = globaltimer();
+            uint32_t ns = 64;
+            for (;;) {
+                X = ld_acquire_u32(W.tnx + g - 1);
+                if (X != ~0u) break;
+                if (!t_alive(W) || globaltimer() - t0 > T_TIMEOUT_NS) {
+                    X = ~0u;
+                    break;
+                }
+                __nanosleep(ns);
+                if (ns < 1024) ns <<= 1;
+            }
+        }
+        X = __shfl_sync(0xFFFFFFFFu, X, 0);
+        if (X == ~0u || K + X > (uint32_t)TK) return false;
+    }
+    uint32_t d0 = 0, KN = 0;
+    const bool last = g == I.last;
+    if (!last) KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
+    for (uint32_t j = lane; j < X; j += 32) {
+        int64_t x = W.tex[(g - 1) * TEX + j];
+        uint32_t cnt = 0;
+        int budget = T_BYTE_STEPS;
+        while (x >= 0 && x < I.seg_end) {
+            ++cnt;
+            x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
+        }
+        W.tl[g * TK + K + j] = x >= 0 ? t_link<ALGO>(ix, n, lo, x, w, Lf, last, d0, KN) : T_BAD;
+        W.tn[g * TK + K + j] = cnt;
+    }
+    if (lane == 0) W.tk[g] = K + X;
     return true;
 }
 
@@ -878,9 +1037,10 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
     uint32_t n = 0;
     if (pre_n >= 0) {  // the CTA built the index together (t_coop_index)
         n = (uint32_t)pre_n;
-        const bool mine = t_alive(W) && n <= T_IDX_CAP &&
-                          (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo) &&
-                          t_table<ALGO>(G, W, g, I, ix, n, lo, ihi);
+        bool mine = t_alive(W) && n <= T_IDX_CAP &&
+                    (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo);
+        const uint32_t K = mine ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : 0u;
+        mine = K > 0 && t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, K);
         if (tm && lane == 0) tm[6] = globaltimer();
         if (!mine) t_fail(W);
     } else if (t_alive(W)) {
@@ -893,8 +1053,9 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         if (mine) {
             n = t_index<MAX>(fbase, lo, ihi, lo, ix, T_IDX_CAP, W.ctrl + T_ALL);
             if (tm && lane == 0) tm[5] = globaltimer();
-            mine = n <= T_IDX_CAP && (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo) &&
-                   t_table<ALGO>(G, W, g, I, ix, n, lo, ihi);
+            mine = n <= T_IDX_CAP && (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo);
+            const uint32_t K = mine ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : 0u;
+            mine = K > 0 && t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, K);
             if (tm && lane == 0) tm[6] = globaltimer();
         }
         if (!mine) t_fail(W);
@@ -957,12 +1118,14 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         const uint32_t E = W.tp[g * TK + Eb];
         uint64_t q = W.tbo[b] + W.tq[g * TK + Eb];
         uint32_t c0 = 0;
-        if (g > 0) t_cands<ALGO>(ix, n, lo, I.p, w, c0);
-        int64_t x = t_cand_start<ALGO>(g, ix, lo, c0, E, w);
-        while (x >= 0 && x < I.seg_end) {
+        const uint32_t Kc = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, I.p, w, c0);
+        // a candidate, or an extra entry handed over by segment g-1
+        int64_t x = E < Kc ? t_cand_start<ALGO>(g, ix, lo, c0, E, w) : W.tex[(g - 1) * TEX + (E - Kc)];
+        int budget = 1 << 30;  // the scan followed this chain: its table row was resolved
+        while (x < I.seg_end) {
             if (q >= 1 && q - 1 < cap) bounds[q - 1] = (uint64_t)x;  // the stream start is not a boundary
             ++q;
-            x = t_step<ALGO>(ix, n, lo, ihi, x, w, mx, Lf);
+            x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
         }
         if (g == nsegs - 1) {
             const uint64_t total = W.seg_out[nsegs];
@@ -1819,7 +1982,10 @@ bool sync_debug() {
 // amortise their halos anyway, and a failed attempt (a stream saturated only
 // in parts, such as configs[2]'s uniform base with zero-filled regions at
 // 453 KB segments) costs ~5 % there.
-constexpr uint64_t T_MAX_SEG = 256ull << 10;
+#ifndef CDC_T_MAX_SEG
+#define CDC_T_MAX_SEG (256ull << 10)
+#endif
+constexpr uint64_t T_MAX_SEG = CDC_T_MAX_SEG;
 
 // CDC_TMODE=0 disables the transfer-table attempt (a debugging and testing knob)
 int tmode_on() {
@@ -1929,7 +2095,7 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     const uint64_t G = P.max_segs;
     size_t sz[] = {
         G * P.cap_list * 4,  // 0 list   } reset to 0xFF by k_reset at every call
-        G * 16 + 64 + (G / 32 + 1) * 12,  // 1 pub, status, ctrl, grp, tblk }
+        G * 20 + 64 + (G / 32 + 1) * 12,  // 1 pub, status, ctrl, grp, tblk, tnx }
         G * P.cap_halo * 4,  // 2 halo
         G * 4,               // 3 cnt
         G * 4,               // 4 hcnt
@@ -1962,9 +2128,10 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
         (G / cdc::TB + 2) * cdc::TK * 4,  // 31 tbs
         (G / cdc::TB + 2) * 4,            // 32 tbe
         (G / cdc::TB + 2) * 8,            // 33 tbo
+        G * cdc::TEX * 8,                 // 34 tex
     };
     size_t o = 0;
-    for (int i = 0; i < 34; ++i) {
+    for (int i = 0; i < 35; ++i) {
         P.off[i] = o;
         o += round_up(sz[i], 256);
     }
@@ -1981,6 +2148,7 @@ cdc::Work carve(const Plan &P, void *ws) {
     W.ctrl = reinterpret_cast<uint32_t *>(W.status + P.max_segs);
     W.grp = W.status + P.max_segs + 8;
     W.tblk = reinterpret_cast<uint32_t *>(W.grp + P.max_segs / 32 + 1);
+    W.tnx = W.tblk + P.max_segs / 32 + 1;
     W.halo = (uint32_t *)(b + P.off[2]);
     W.cnt = (uint32_t *)(b + P.off[3]);
     W.hcnt = (uint32_t *)(b + P.off[4]);
@@ -2013,6 +2181,7 @@ cdc::Work carve(const Plan &P, void *ws) {
     W.tbs = (uint32_t *)(b + P.off[31]);
     W.tbe = (uint32_t *)(b + P.off[32]);
     W.tbo = (uint64_t *)(b + P.off[33]);
+    W.tex = (int64_t *)(b + P.off[34]);
     W.poolb_cap = P.poolb_cap;
     W.cap_list = P.cap_list;
     W.cap_halo = P.cap_halo;

@@ -53,11 +53,56 @@ def test_tables_many_small_segments(cdc):
 
 
 @pytest.mark.parametrize("algo", ["ram", "ae_max"])
-def test_tables_fallback(cdc, algo):
-    """A zero region breaks saturation: the attempt fails and the halo walks
-    resolve the stream (same boundaries as the oracle)."""
+def test_tables_zero_region(cdc, algo):
+    """A zero-filled region: steps inside it are not saturated and are read from
+    the bytes, and chains that leave a segment through it are handed to the
+    next segment as extra entries.  Same boundaries as the oracle."""
     d = synth.uniform(16 << 20, 12)
     d[5 << 20:(5 << 20) + 300_000] = 0
+    d[(9 << 20) - 70_000:(9 << 20) + 70_000] = 0  # across a segment boundary
+    p = cdc.params(algo, avg_size=8192)
+    exp = oracle.chunk(algo, d, p.window, p.max_size)
+    got, st = _run(cdc, d, p)
+    assert got.size == exp.size and (got == exp).all(), st
+
+
+@pytest.mark.parametrize("algo", ["ram", "ae_max", "ae_min"])
+def test_tables_short_unsaturated_runs(cdc, algo):
+    """Short runs without the saturating byte (a few KiB of 0x01 bytes, some
+    across segment boundaries): those steps are read from the bytes, chains
+    that leave a segment through one are handed to the next segment as extra
+    entries, and the tables still resolve the stream."""
+    d = synth.uniform(16 << 20, 16)
+    rng = np.random.default_rng(16)
+    starts = list(rng.integers(0, (16 << 20) - 20000, 40)) + [k * (1 << 17) - 3000 for k in range(1, 128, 9)]
+    for a in starts:
+        d[a:a + int(rng.integers(2000, 9000))] = 1
+    p = cdc.params(algo, avg_size=8192)
+    exp = oracle.chunk(algo, d, p.window, p.max_size)
+    got, st = _run(cdc, d, p)
+    assert st["fast_path"] == 2, st
+    assert got.size == exp.size and (got == exp).all()
+
+
+@pytest.mark.parametrize("algo,avg", [("ram", 8192), ("ram", 16384), ("ae_max", 8192)])
+def test_tables_versioned(cdc, algo, avg):
+    """configs[2]-like bytes (uniform with 10 % zero-filled 64 KiB regions, a
+    snapshot with edits) at a size the oracle finishes quickly."""
+    base, snap = synth.versioned(24 << 20, 1, seed=14)
+    for d in (base, snap):
+        p = cdc.params(algo, avg_size=avg)
+        exp = oracle.chunk(algo, d, p.window, p.max_size)
+        got, st = _run(cdc, d, p)
+        assert got.size == exp.size and (got == exp).all(), st
+
+
+@pytest.mark.parametrize("algo", ["ram", "ae_max"])
+def test_tables_fallback(cdc, algo):
+    """Half the stream never holds the saturating byte (bytes 1..254): its
+    segments are not dense, the attempt fails and the speculative walk
+    resolves the stream."""
+    d = synth.uniform(16 << 20, 15)
+    d[8 << 20:] = (d[8 << 20:] % 254 + 1).astype(np.uint8)
     p = cdc.params(algo, avg_size=8192)
     exp = oracle.chunk(algo, d, p.window, p.max_size)
     got, st = _run(cdc, d, p)
