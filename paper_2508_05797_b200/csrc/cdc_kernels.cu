@@ -576,11 +576,15 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
 // to the speculative walk (the tables are tried only for a single stream
 // whose grid is one co-resident wave, with a timeout).
 constexpr int TK = 128;                      // table rows per segment (candidates + extra entries), 4 per lane
-constexpr int TEX = 32;                      // extra entries a segment can pass to the next one
+constexpr int TEX = 64;                      // extra entries a segment can pass to the next one
+constexpr int TRUNS = 16;                    // constant runs a walker records (tail of its ring)
+constexpr uint32_t T_RUN_WORDS = 2 + 3 * TRUNS;  // count, TRUNS x (start, end, value), longest run
+constexpr uint32_t T_LONG_RUN = 32768;        // a constant run this long makes the attempt give up at once
 constexpr uint32_t T_END = 0xFFFFFFFEu;      // link: the chain reached the stream end
 constexpr uint32_t T_BAD = 0xFFFFFFFFu;      // link: not resolvable in index space
 constexpr uint32_t T_DENSE = 8;              // saturating bytes per window a segment needs
 constexpr uint32_t T_IDX_CAP = (uint32_t)(RING_BYTES / 4);
+constexpr uint32_t T_IX_CAP = T_IDX_CAP - T_RUN_WORDS;  // index entries; the constant runs follow them
 constexpr unsigned long long T_TIMEOUT_NS = 2000000ull;  // the scanner gives up after 2 ms
 // control words (ctrl[], reset to ~0 by k_reset): 6 block composers arrived,
 // 7 all-T (~0 yes, 0 no), 8 verdict (~0 pending, 1 tables, 0 fall back)
@@ -601,29 +605,67 @@ __device__ __forceinline__ bool t_alive(const Work &W) { return ld_relaxed_u32(W
 constexpr int TIX_G = CDC_TIX_G;  // 16-byte granules per lane per step of the index pass
 template <bool MAX>
 __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_t rel, uint32_t *ix, uint32_t cap,
-                            const uint32_t *alive = nullptr) {
+                            const uint32_t *alive = nullptr, uint32_t *runs = nullptr) {
     const int lane = lane_id();
     const uintptr_t fb = reinterpret_cast<uintptr_t>(fbase);
     const uintptr_t a0 = (fb + (uintptr_t)lo) & ~(uintptr_t)15;
     const uintptr_t a1 = fb + (uintptr_t)hi;
     uint32_t n = 0;
     int step = 0;
+    // constant runs (whole 8 KiB steps of one repeated byte): lane 0 tracks the open one
+    uint32_t nr = 0, rs = 0, re = 0, rc = 0, longest = 0;
+    bool ropen = false;
+    auto close_run = [&]() {
+        if (ropen && re - rs > longest) longest = re - rs;
+        if (ropen && nr < (uint32_t)TRUNS && lane == 0) {
+            runs[1 + 3 * nr] = rs;
+            runs[2 + 3 * nr] = re;
+            runs[3 + 3 * nr] = rc;
+        }
+        if (ropen && nr < (uint32_t)TRUNS) ++nr;
+        ropen = false;
+    };
     for (uintptr_t a = a0; a < a1; a += 32 * 16 * TIX_G) {
         // the attempt may already have failed elsewhere: look every 64 KiB
         if (alive && (++step & 7) == 0 && ld_relaxed_u32(alive) == 0u) return cap + 1;
         const uintptr_t la = a + (uintptr_t)lane * 16 * TIX_G;
         uint32_t m[TIX_G];
+        uint32_t crep = 0;
+        bool lconst = runs != nullptr;
 #pragma unroll
         for (int u = 0; u < TIX_G; ++u) {
             const uintptr_t ga = la + (uintptr_t)(u * 16);
             m[u] = 0u;
             if (ga < a1) {
                 const uint4 v = *reinterpret_cast<const uint4 *>(ga);
+                if (u == 0) crep = (v.x & 0xFFu) * 0x01010101u;
+                lconst = lconst && ((v.x ^ crep) | (v.y ^ crep) | (v.z ^ crep) | (v.w ^ crep)) == 0u;
                 const int64_t pos = (int64_t)(ga - fb);
                 const int x0 = (int)(lo - pos > 0 ? (lo - pos > 16 ? 16 : lo - pos) : 0);
                 const int x1 = (int)(hi - pos < 16 ? (hi - pos < 0 ? 0 : hi - pos) : 16);
                 const uint32_t keep = x0 < x1 ? (((1u << x1) - 1u) & ~((1u << x0) - 1u)) : 0u;
                 m[u] = sat_mask16<MAX>(v) & keep;
+            } else {
+                lconst = false;
+            }
+        }
+        if (runs != nullptr) {
+            const int64_t s0 = (int64_t)(a - fb), s1 = s0 + 32 * 16 * TIX_G;
+            const uint32_t c0rep = __shfl_sync(0xFFFFFFFFu, crep, 0);  // every lane, before any branch
+            const bool whole = __all_sync(0xFFFFFFFFu, lconst && crep == c0rep) && s0 >= lo && s1 <= hi;
+            const uint32_t c8 = c0rep & 0xFFu;
+            if (whole) {
+                if (ropen && rc == c8 && (int64_t)re + rel == s0) {
+                    re = (uint32_t)(s1 - rel);
+                } else {
+                    close_run();
+                    ropen = true;
+                    rs = (uint32_t)(s0 - rel);
+                    re = (uint32_t)(s1 - rel);
+                    rc = c8;
+                }
+            } else {
+                close_run();
             }
         }
         uint32_t c = 0;
@@ -648,6 +690,13 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_
             }
         }
         n += tot;
+    }
+    if (runs != nullptr) {
+        close_run();
+        if (lane == 0) {
+            runs[0] = nr;
+            runs[1 + 3 * TRUNS] = longest;
+        }
     }
     __syncwarp();
     return n;
@@ -764,12 +813,23 @@ __device__ int64_t t_step_bytes(const uint8_t *fbase, int64_t x, int64_t w, int6
 // bytes while the chain's budget of byte steps lasts (a lane reads up to a
 // window per byte step; long unsaturated stretches, such as large zero-filled
 // regions, are left to the speculative walk): -1 when the budget is spent
-constexpr int T_BYTE_STEPS = 4;
+#ifndef CDC_T_BYTE_STEPS
+#define CDC_T_BYTE_STEPS 4
+#endif
+constexpr int T_BYTE_STEPS = CDC_T_BYTE_STEPS;
 template <int ALGO>
 __device__ __forceinline__ int64_t t_next(const uint8_t *fbase, const uint32_t *ix, uint32_t n, int64_t lo,
                                           int64_t ihi, int64_t x, int64_t w, int64_t mx, int64_t Lf, int &budget) {
     const int64_t y = t_step<ALGO>(ix, n, lo, ihi, x, w, mx, Lf);
     if (y >= 0) return y;
+    // inside a constant run (value c) both rules end the chunk at x+w+1: RAM's
+    // window maximum is c and d[x+w] = c; AE's target c is unbeaten over (x, x+w]
+    const uint32_t *runs = ix + T_IX_CAP;
+    const int64_t limit = Lf - x < mx ? Lf : x + mx;
+    for (uint32_t r = 0; r < runs[0]; ++r) {
+        const int64_t rs = lo + (int64_t)runs[1 + 3 * r], re = lo + (int64_t)runs[2 + 3 * r];
+        if (x >= rs && x + w < re && x + w + 1 <= limit) return x + w + 1;
+    }
     if (--budget < 0) return -1;
     return t_step_bytes<ALGO>(fbase, x, w, mx, Lf);
 }
@@ -816,20 +876,23 @@ __device__ __forceinline__ uint32_t t_link(const uint32_t *ix, uint32_t n, int64
 // W.tn).  A chain whose exit is not a candidate of g+1 (its last step was not
 // saturated) becomes an extra entry of g+1: its start goes to W.tex[g] and
 // its link to KN + j; the count is published in W.tnx[g] for phase 2 of g+1.
-// Returns K (0 when the segment cannot be resolved in index space).
+// Returns K (the candidates; -1 when the segment cannot be resolved in index
+// space).
 template <int ALGO>
-__device__ uint32_t t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint8_t *fbase,
-                            const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi) {
+__device__ int t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint8_t *fbase,
+                       const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi) {
     const int lane = lane_id();
     const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
     uint32_t c0 = 0;
+    // no candidates (a segment that starts in a long constant run): every
+    // entry then comes as an extra entry from segment g-1
     const uint32_t K = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, I.p, w, c0);
     uint32_t d0 = 0, KN = 0;
     const bool last = g == I.last;
     if (!last) KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
-    if (K == 0 || K > (uint32_t)TK || (!last && (KN == 0 || KN > (uint32_t)TK))) {
+    if (K > (uint32_t)TK || KN > (uint32_t)TK) {
         if (lane == 0) st_release_u32(W.tnx + g, 0u);
-        return 0;
+        return -1;
     }
     uint32_t nx = 0;  // extra entries passed on so far
     for (uint32_t k0 = 0; k0 < K; k0 += 32) {
@@ -865,7 +928,7 @@ __device__ uint32_t t_table(const Geometry &G, Work &W, uint64_t g, const SegInf
         __threadfence();
         st_release_u32(W.tnx + g, nx < (uint32_t)TEX ? nx : (uint32_t)TEX);
     }
-    return K;
+    return (int)K;
 }
 
 // Phase 2: the rows of the extra entries segment g-1 passed on (rows K ..
@@ -1037,10 +1100,10 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
     uint32_t n = 0;
     if (pre_n >= 0) {  // the CTA built the index together (t_coop_index)
         n = (uint32_t)pre_n;
-        bool mine = t_alive(W) && n <= T_IDX_CAP &&
+        bool mine = t_alive(W) && n <= T_IX_CAP &&
                     (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo);
-        const uint32_t K = mine ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : 0u;
-        mine = K > 0 && t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, K);
+        const int K = mine ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : -1;
+        mine = K >= 0 && t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, (uint32_t)K);
         if (tm && lane == 0) tm[6] = globaltimer();
         if (!mine) t_fail(W);
     } else if (t_alive(W)) {
@@ -1051,11 +1114,14 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         const uint32_t ns = t_index<MAX>(fbase, I.p, shi, I.p, ix, T_IDX_CAP);
         bool mine = 2ull * ns * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(shi - I.p);
         if (mine) {
-            n = t_index<MAX>(fbase, lo, ihi, lo, ix, T_IDX_CAP, W.ctrl + T_ALL);
+            n = t_index<MAX>(fbase, lo, ihi, lo, ix, T_IX_CAP, W.ctrl + T_ALL, ix + T_IX_CAP);
             if (tm && lane == 0) tm[5] = globaltimer();
-            mine = n <= T_IDX_CAP && (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo);
-            const uint32_t K = mine ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : 0u;
-            mine = K > 0 && t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, K);
+            // a long constant run (a zero-filled region, say): its chains keep their
+            // phases, too many to hand over; the speculative walk is the better path
+            mine = n <= T_IX_CAP && (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo) &&
+                   ix[T_IX_CAP + 1 + 3 * TRUNS] < T_LONG_RUN;
+            const int K = mine ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : -1;
+            mine = K >= 0 && t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, (uint32_t)K);
             if (tm && lane == 0) tm[6] = globaltimer();
         }
         if (!mine) t_fail(W);
@@ -1138,7 +1204,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
 // T-mode, one segment per CTA (a small stream): the CTA's 16 warps index the
 // saturating bytes of [p - w - 1, seg_end + max_size + 1) together, one
 // sixteenth each into their own rings, and warp 0 concatenates the parts in
-// order into its ring.  Returns the entry count for warp 0 (T_IDX_CAP + 1:
+// order into its ring.  Returns the entry count for warp 0 (T_IX_CAP + 1:
 // not dense or too many), or -1 when the attempt is already off.  All threads
 // of the CTA call this.
 template <int ALGO>
@@ -1168,19 +1234,20 @@ __device__ int64_t t_coop_index(const Geometry &G, Work &W, uint64_t g, uint8_t 
     if (go == 1) {
         const int64_t part = (((ihi - lo) + 16 * SPEC_WARPS - 1) / (16 * SPEC_WARPS)) * 16;
         const int64_t a = lo + warp * part, b = a + part < ihi ? a + part : ihi;
-        const uint32_t c = a < b ? t_index<MAX>(fbase, a, b, lo, ix, T_IDX_CAP) : 0u;
+        const uint32_t c = a < b ? t_index<MAX>(fbase, a, b, lo, ix, T_IX_CAP) : 0u;
         if (lane == 0) s_cnt[warp] = c;
     }
     __syncthreads();
     if (go == 2) {
         if (warp == 0) t_fail(W);
-        return (int64_t)T_IDX_CAP + 1;
+        return (int64_t)T_IX_CAP + 1;
     }
     if (warp != 0) return 0;  // only warp 0 walks the segment
+    if (lane == 0) ix[T_IX_CAP] = 0;  // no constant runs recorded on this path (its samples reject them)
     uint32_t n = 0;
     for (int k = 0; k < SPEC_WARPS; ++k) {
         const uint32_t c = s_cnt[k];
-        if (c > T_IDX_CAP || n + c > T_IDX_CAP) return (int64_t)T_IDX_CAP + 1;
+        if (c > T_IX_CAP || n + c > T_IX_CAP) return (int64_t)T_IX_CAP + 1;
         if (k > 0) {
             const uint32_t *src = reinterpret_cast<const uint32_t *>(rings + k * RING_SMEM);
             for (uint32_t i = lane; i < c; i += 32) ix[n + i] = src[i];
