@@ -564,17 +564,19 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
 // (RAM: P+1 for a saturating position P in [p_g - 1, N(p_g + w - 1)]; AE:
 // q+w+1 for q in [p_g - w - 1, N(p_g - 1)], N = next saturating position;
 // segment 0: the stream start).  Before any byte walk, walker g looks at its
-// first 4 KiB; if they are dense in saturating bytes it indexes those of
-// [p_g - w - 1, seg_end + max_size + 1) in its idle ring, walks every
-// candidate's chain in index space (one lane each) and publishes, per
-// candidate, the number of chain starts inside the segment and the candidate
-// of segment g+1 its chain enters.  The last walker of each block of 32
-// segments composes the block's tables with shuffles, the last composer scans
-// the blocks, and every walker writes its own part of the true chain: no byte
-// walk and no halo.  Any step that is not saturated, any exit that is not a
-// candidate, or any segment that is not dense makes the whole call fall back
-// to the speculative walk (the tables are tried only for a single stream
-// whose grid is one co-resident wave, with a timeout).
+// first 16 KiB; if they are dense in saturating bytes it indexes those of
+// [p_g - w - 1, seg_end + max_size + 1) (and the long constant runs) in its
+// idle ring, walks every candidate's chain in index space (one lane each;
+// the few steps the index cannot decide are read from the bytes) and
+// publishes, per candidate, the number of chain starts inside the segment and
+// the candidate of segment g+1 its chain enters -- or, when its exit is no
+// candidate, hands that exit over as an extra entry of segment g+1.  The last
+// walker of each block of 32 segments composes the block's tables with
+// shuffles, the last composer scans the blocks, and every walker writes its
+// own part of the true chain: no byte walk and no halo.  Anything the tables
+// cannot resolve makes the whole call fall back to the speculative walk (the
+// tables are tried only for a single stream whose grid is one co-resident
+// wave, with a timeout).  DESIGN.md §6 lists every case.
 constexpr int TK = 128;                      // table rows per segment (candidates + extra entries), 4 per lane
 constexpr int TEX = 64;                      // extra entries a segment can pass to the next one
 constexpr int TRUNS = 16;                    // constant runs a walker records (tail of its ring)
