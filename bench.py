@@ -7,7 +7,7 @@ segment chunking with the fused look-back resolution and boundary write
 fused fast path succeeded) -- every row of DESIGN.md §0(a).  Workload at N=1 = BASELINE.json
 configs[1]: AE (AE-Max) at a 4 KiB target average, one 256 MiB stream of
 Zipf(s=1.1) bytes, seed 1.  With N ranks (torchrun) every rank chunks its own
-256 MiB stream (seed 1 + rank): the work shards with no collective on the data
+256 MiB stream (the configs[1] stream, seed 1, on every rank): the work shards with no collective on the data
 path ("scaling": "weak").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
@@ -214,7 +214,10 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    data_np = synth.zipf_bytes(STREAM, 1.1, 1 + rank)
+    # every rank chunks its own copy of the configs[1] stream (seed 1): equal work
+    # per rank for weak scaling (another seed permutes which byte value is the
+    # rare 255 and changes AE-Max's chunk statistics)
+    data_np = synth.zipf_bytes(STREAM, 1.1, 1)
     # two device copies of the stream at different addresses, used alternately, so
     # that no step finds the previous step's lines in L2 (126 MB < 2 x 256 MiB)
     bufs = [torch.from_numpy(data_np).to(dev) for _ in range(2)]
