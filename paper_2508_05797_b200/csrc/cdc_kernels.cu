@@ -581,7 +581,10 @@ constexpr int TK = 128;                      // table rows per segment (candidat
 constexpr int TEX = 64;                      // extra entries a segment can pass to the next one
 constexpr int TRUNS = 16;                    // constant runs a walker records (tail of its ring)
 constexpr uint32_t T_RUN_WORDS = 2 + 3 * TRUNS;  // count, TRUNS x (start, end, value), longest run
-constexpr uint32_t T_LONG_RUN = 32768;        // a constant run this long makes the attempt give up at once
+#ifndef CDC_T_LONG_RUN
+#define CDC_T_LONG_RUN 32768
+#endif
+constexpr uint32_t T_LONG_RUN = CDC_T_LONG_RUN;  // a constant run this long makes the attempt give up at once
 constexpr uint32_t T_END = 0xFFFFFFFEu;      // link: the chain reached the stream end
 constexpr uint32_t T_BAD = 0xFFFFFFFFu;      // link: not resolvable in index space
 constexpr uint32_t T_DENSE = 8;              // saturating bytes per window a segment needs
@@ -592,8 +595,11 @@ constexpr unsigned long long T_TIMEOUT_NS = 2000000ull;  // the scanner gives up
 // 7 all-T (~0 yes, 0 no), 8 verdict (~0 pending, 1 tables, 0 fall back)
 constexpr int T_ARRIVE = 6, T_ALL = 7, T_SCAN = 8;
 
-__device__ __forceinline__ void t_fail(Work &W) {
+// ctrl[12], ctrl[13]: the first failure's reason and segment (diagnostics,
+// printed by cdc_stats when CDC_TDEBUG is set)
+__device__ __forceinline__ void t_fail(Work &W, uint32_t why = 0, uint64_t g = 0) {
     if (ld_relaxed_u32(W.ctrl + T_ALL) != 0u) atomicAnd(W.ctrl + T_ALL, 0u);
+    if (why && atomicCAS(W.ctrl + 12, ~0u, why) == ~0u) W.ctrl[13] = (uint32_t)g;
 }
 __device__ __forceinline__ bool t_alive(const Work &W) { return ld_relaxed_u32(W.ctrl + T_ALL) != 0u; }
 
@@ -1066,18 +1072,27 @@ __device__ bool t_scan_blocks(Work &W, uint64_t nsegs, uint64_t *d_count) {
         for (int v = 0; v < 4; ++v) {
             const uint64_t b = b0 + v;
             if (b >= NB) break;
-            if (E >= (uint32_t)TK) return false;
+            if (E >= (uint32_t)TK) {
+                if (lane == 0) t_fail(W, E == T_END ? 9 : 7, b * TB);
+                return false;
+            }
             if (lane == 0) {
                 W.tbe[b] = E;
                 W.tbo[b] = O;
             }
             const uint32_t c = t_gather(C[v], E), sc = t_gather(S[v], E);
-            if (c == T_BAD) return false;
+            if (c == T_BAD) {
+                if (lane == 0) t_fail(W, 8, b * TB);
+                return false;
+            }
             O += sc;
             E = c;
         }
     }
-    if (E != T_END) return false;
+    if (E != T_END) {
+        if (lane == 0) t_fail(W, 11, nsegs);
+        return false;
+    }
     if (lane == 0) {
         W.seg_out[nsegs] = O;
         *d_count = O;
@@ -1115,18 +1130,23 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         const int64_t shi = I.p + 16384 < ihi ? I.p + 16384 : ihi;
         const uint32_t ns = t_index<MAX>(fbase, I.p, shi, I.p, ix, T_IDX_CAP);
         bool mine = 2ull * ns * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(shi - I.p);
+        uint32_t why = 1;
         if (mine) {
             n = t_index<MAX>(fbase, lo, ihi, lo, ix, T_IX_CAP, W.ctrl + T_ALL, ix + T_IX_CAP);
             if (tm && lane == 0) tm[5] = globaltimer();
             // a long constant run (a zero-filled region, say): its chains keep their
             // phases, too many to hand over; the speculative walk is the better path
-            mine = n <= T_IX_CAP && (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo) &&
-                   ix[T_IX_CAP + 1 + 3 * TRUNS] < T_LONG_RUN;
-            const int K = mine ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : -1;
-            mine = K >= 0 && t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, (uint32_t)K);
+            why = n > T_IX_CAP ? 2
+                : (uint64_t)n * (uint64_t)(w + 1) < (uint64_t)T_DENSE * (uint64_t)(ihi - lo) ? 3
+                : ix[T_IX_CAP + 1 + 3 * TRUNS] >= T_LONG_RUN ? 4 : 0;
+            const int K = why == 0 ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : -1;
+            if (why == 0 && K < 0) why = 5;
+            if (why == 0 && !t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, (uint32_t)K)) why = 6;
+            mine = why == 0;
             if (tm && lane == 0) tm[6] = globaltimer();
         }
-        if (!mine) t_fail(W);
+        if (!mine && lane == 0) t_fail(W, why, g);
+        __syncwarp();
     }
     // arrive: the last walker of a block composes the block, the last composer
     // scans the blocks.  The verdict word T_SCAN decides once (compare-and-
@@ -1171,6 +1191,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
             verdict = ld_acquire_u32(W.ctrl + T_SCAN);
             if (verdict != ~0u) break;
             if (!t_alive(W) || globaltimer() - t0 > T_TIMEOUT_NS) {
+                if (t_alive(W)) t_fail(W, 10, g);
                 atomicCAS(W.ctrl + T_SCAN, ~0u, 0u);  // give up (unless the scan has just decided)
                 continue;
             }
@@ -1241,7 +1262,7 @@ __device__ int64_t t_coop_index(const Geometry &G, Work &W, uint64_t g, uint8_t 
     }
     __syncthreads();
     if (go == 2) {
-        if (warp == 0) t_fail(W);
+        if (warp == 0 && lane == 0) t_fail(W, 1, g);
         return (int64_t)T_IX_CAP + 1;
     }
     if (warp != 0) return 0;  // only warp 0 walks the segment
@@ -2492,6 +2513,11 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
     stats[1] = P.S;
     stats[2] = P.Hmax;
     stats[3] = ctrl[1] == 0 ? 0 : (tables == G && G > 0 ? 2 : 1);
+    if (getenv("CDC_TDEBUG")) {  // why the transfer tables gave up (diagnostics)
+        uint32_t why[2] = {0, 0};
+        CDC_CUDA(cudaMemcpy(why, W.ctrl + 12, 8, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "cdc: transfer tables: reason %d at segment %u\n", (int)why[0], why[1]);
+    }
     stats[4] = met;
     stats[5] = unsynced;
     stats[6] = other;
