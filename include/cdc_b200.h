@@ -225,7 +225,9 @@ int cdc_profile_query(int *done);
  *   [0] segments G, [1] segment bytes S, [2] halo cap bytes,
  *   [3] 1 if the fused look-back fast path produced the output, 2 if the
  *       transfer tables did (saturated streams), 0 if k_fixup's resolver and
- *       fix-up walkers ran, [4] segments whose chain met the
+ *       fix-up walkers ran (with CDC_TDEBUG set in the environment this
+ *       call also prints why a transfer-table attempt gave up), [4] segments
+ *       whose chain met the
  *       next segment's chain, [5] segments whose halo walk gave up or was
  *       undecided, [6] segments whose chain skipped a later segment or reached
  *       the stream end from a non-final segment, [7] total halo chunks.
