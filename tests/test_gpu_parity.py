@@ -286,3 +286,29 @@ def test_cuda_graph_capture(cdc, case):
         assert got.size == exp.size and (got == exp).all()
     if case == "fixup":
         assert cdc.stats(p, ws, 1, n, n)["fast_path"] == 0
+
+
+def test_concurrent_streams(cdc):
+    """Two calls in flight at once on two CUDA streams, each with its own
+    workspace (the device state of a call lives in its workspace): both exact."""
+    d1 = synth.zipf_bytes((6 << 20) + 11, 1.1, 31)
+    d2 = synth.uniform((16 << 20) + 5, 32)
+    jobs = []
+    for d, algo, avg in ((d1, "ae_max", 4096), (d2, "ram", 8192)):
+        p = cdc.params(algo, avg_size=avg)
+        t = _dev(d)
+        n = d.size
+        ws = torch.empty(cdc.workspace_size(p, 1, n, n), dtype=torch.uint8, device="cuda")
+        b = torch.full((cdc.max_boundaries(p, n),), -1, dtype=torch.int64, device="cuda")
+        c = torch.zeros(1, dtype=torch.int64, device="cuda")
+        jobs.append((d, algo, p, t, ws, b, c, torch.cuda.Stream()))
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for d, algo, p, t, ws, b, c, s in jobs:
+            with torch.cuda.stream(s):
+                cdc.chunk_async(t, p, b, c, ws, s)
+    torch.cuda.synchronize()
+    for d, algo, p, t, ws, b, c, s in jobs:
+        exp = oracle.chunk(algo, d, p.window, p.max_size)
+        got = b[:int(c.item())].cpu().numpy().astype(np.uint64)
+        assert got.size == exp.size and (got == exp).all(), algo
