@@ -519,23 +519,17 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
     }
     __syncthreads();
     const uint64_t nsegs = total_segs(G, W);
-    if (spw == 0) {
-        // a batch: every warp takes segments one at a time from a global ticket
-        // (segments of very different sizes; earlier segments are always taken
-        // first, and without the fused write no warp waits on another)
-        for (;;) {
-            uint32_t t = 0;
-            if (lane_id() == 0) t = atomicAdd(W.ctrl + DYN_TICKET, 1u) + 1u;  // counter starts at ~0
-            const uint64_t g = __shfl_sync(0xFFFFFFFFu, t, 0);
-            if (g >= nsegs) break;
-            speculate_segment<ALGO, TM>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count,
-                                        fused);
-        }
-        return;
-    }
     // spw segments per CTA (contiguous, so every predecessor is in this or an
-    // earlier ticket); fewer than SPEC_WARPS spread a small input over the SMs
-    const uint64_t g = (uint64_t)s_ticket * spw + warp;
+    // earlier ticket); fewer than SPEC_WARPS spread a small input over the SMs.
+    // spw = 0 (a batch): every warp takes segments one at a time from a global
+    // ticket (segments of very different sizes; earlier segments are always
+    // taken first, and without the fused write no warp waits on another).
+    auto ticket = [&]() -> uint64_t {
+        uint32_t t = 0;
+        if (lane_id() == 0) t = atomicAdd(W.ctrl + DYN_TICKET, 1u) + 1u;  // counter starts at ~0
+        return __shfl_sync(0xFFFFFFFFu, t, 0);
+    };
+    uint64_t g = spw == 0 ? ticket() : (uint64_t)s_ticket * spw + warp;
     int64_t pre_n = -1;
     if constexpr (TM) {
         if (spw == 1) {  // one segment per CTA: its 16 warps build the index together
@@ -543,9 +537,13 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
             pre_n = t_coop_index<ALGO>(G, W, (uint64_t)s_ticket, align_smem(smem));
         }
     }
-    if (warp >= spw || g >= nsegs) return;
-    speculate_segment<ALGO, TM>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused,
-                                pre_n);
+    if (spw != 0 && warp >= spw) return;
+    while (g < nsegs) {  // one call site, so the walker is inlined once
+        speculate_segment<ALGO, TM>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused,
+                                    pre_n);
+        if (spw != 0) break;
+        g = ticket();
+    }
     if (lane_id() == 0) stamp(TM_SPEC_END);
 }
 
