@@ -605,6 +605,15 @@ __device__ __forceinline__ bool t_alive(const Work &W) { return ld_relaxed_u32(W
 // offsets from rel into ix; returns the count, or cap + 1 when they do not fit.
 // Each lane takes TIX_G contiguous granules of 16 bytes, so lane order is
 // position order and one warp scan of the lanes' counts places every entry.
+// any byte of a 16-byte vector equal to the saturating value (255 for MAX, 0
+// for MIN): the zero-byte test on ~x (MAX) or x (MIN), exact for "any"
+template <bool MAX>
+__device__ __forceinline__ bool t_sat_any(const uint4 &v) {
+    auto f = [](uint32_t x) {
+        return MAX ? (0xFEFEFEFEu - x) & x & 0x80808080u : (x - 0x01010101u) & ~x & 0x80808080u;
+    };
+    return (f(v.x) | f(v.y) | f(v.z) | f(v.w)) != 0u;
+}
 #ifndef CDC_TIX_G
 #define CDC_TIX_G 16
 #endif
@@ -635,26 +644,33 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_
         // the attempt may already have failed elsewhere: look every 64 KiB
         if (alive && (++step & 7) == 0 && ld_relaxed_u32(alive) == 0u) return cap + 1;
         const uintptr_t la = a + (uintptr_t)lane * 16 * TIX_G;
-        uint32_t m[TIX_G];
+        // pass 1: which granules hold a saturating byte (2 integer ops per word;
+        // a flag may sit in a byte outside [lo, hi), the exact pass drops it)
+        uint32_t hit = 0;
         uint32_t crep = 0;
         bool lconst = runs != nullptr;
 #pragma unroll
         for (int u = 0; u < TIX_G; ++u) {
             const uintptr_t ga = la + (uintptr_t)(u * 16);
-            m[u] = 0u;
             if (ga < a1) {
                 const uint4 v = *reinterpret_cast<const uint4 *>(ga);
                 if (u == 0) crep = (v.x & 0xFFu) * 0x01010101u;
                 lconst = lconst && ((v.x ^ crep) | (v.y ^ crep) | (v.z ^ crep) | (v.w ^ crep)) == 0u;
-                const int64_t pos = (int64_t)(ga - fb);
-                const int x0 = (int)(lo - pos > 0 ? (lo - pos > 16 ? 16 : lo - pos) : 0);
-                const int x1 = (int)(hi - pos < 16 ? (hi - pos < 0 ? 0 : hi - pos) : 16);
-                const uint32_t keep = x0 < x1 ? (((1u << x1) - 1u) & ~((1u << x0) - 1u)) : 0u;
-                m[u] = sat_mask16<MAX>(v) & keep;
+                if (t_sat_any<MAX>(v)) hit |= 1u << u;
             } else {
                 lconst = false;
             }
         }
+        // exact byte mask of hit granule u inside [lo, hi) (reloaded: an L1 hit)
+        auto exact = [&](int u) -> uint32_t {
+            const uintptr_t ga = la + (uintptr_t)(u * 16);
+            const uint4 v = *reinterpret_cast<const uint4 *>(ga);
+            const int64_t pos = (int64_t)(ga - fb);
+            const int x0 = (int)(lo - pos > 0 ? (lo - pos > 16 ? 16 : lo - pos) : 0);
+            const int x1 = (int)(hi - pos < 16 ? (hi - pos < 0 ? 0 : hi - pos) : 16);
+            const uint32_t keep = x0 < x1 ? (((1u << x1) - 1u) & ~((1u << x0) - 1u)) : 0u;
+            return sat_mask16<MAX>(v) & keep;
+        };
         if (runs != nullptr) {
             const int64_t s0 = (int64_t)(a - fb), s1 = s0 + 32 * 16 * TIX_G;
             const uint32_t c0rep = __shfl_sync(0xFFFFFFFFu, crep, 0);  // every lane, before any branch
@@ -675,8 +691,7 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_
             }
         }
         uint32_t c = 0;
-#pragma unroll
-        for (int u = 0; u < TIX_G; ++u) c += __popc(m[u]);
+        for (uint32_t h = hit; h; h &= h - 1u) c += __popc(exact(__ffs(h) - 1));
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -687,9 +702,9 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_
         if (n + tot > cap) return cap + 1;
         uint32_t at = n + incl - c;
         const uint32_t base = (uint32_t)((int64_t)(la - fb) - rel);
-#pragma unroll
-        for (int u = 0; u < TIX_G; ++u) {
-            uint32_t mm = m[u];
+        for (uint32_t h = hit; h; h &= h - 1u) {
+            const int u = __ffs(h) - 1;
+            uint32_t mm = exact(u);
             while (mm) {
                 ix[at++] = base + (uint32_t)(u * 16) + (uint32_t)(__ffs(mm) - 1);
                 mm &= mm - 1u;
