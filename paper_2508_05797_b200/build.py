@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcdc_b200.so")
 SOURCES = [os.path.join(CSRC, "cdc_kernels.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "cdc_device.cuh"),
+DEPS = SOURCES + [os.path.join(CSRC, "cdc_device.cuh"), os.path.join(CSRC, "cdc_tables.cuh"),
                   os.path.join(os.path.dirname(HERE), "include", "cdc_b200.h")]
 
 NVCC_FLAGS = [
@@ -17,8 +17,6 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared",
 ]
-# -DCDC_TAIL_LAUNCH with -rdc=true and LIBS = ["-lcudadevrt"] builds the variant whose
-# k_speculate tail-launches the fix-up (slower on B200 as measured; see cdc_kernels.cu)
 LIBS: list[str] = []
 
 

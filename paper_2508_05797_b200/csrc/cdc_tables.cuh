@@ -1,0 +1,752 @@
+// cdc_tables.cuh -- transfer tables for saturated streams (T-mode).
+// Included once by cdc_kernels.cu inside namespace cdc, after the workspace
+// (Work), the segment geometry (SegInfo) and the look-back words it uses.
+#pragma once
+
+// ------------------------------------------------------------------ T-mode: transfer tables
+// (DESIGN.md §6).  On saturating data (uniform bytes at w >> 256) chains that
+// start at different offsets meet only after ~(w / 362)^2 chunks, so halo
+// walks get long.  There a chunk step depends only on the positions of the
+// saturating bytes (255 for RAM and AE-Max, 0 for AE-Min):
+//   RAM (§2.1.2): the window [x, x+w) holds a saturating byte, so its maximum
+//     is saturated and the chunk ends after the first saturating byte in
+//     [x+w, limit), else at limit;
+//   AE: the first saturating byte q <= x+w is the target no byte beats (every
+//     earlier record is beaten within w), so the chunk ends at q+w+1, or at
+//     limit when q+w >= limit; if x+w >= limit it ends at limit.
+// A saturated chain that enters segment g starts at one of few candidates
+// (RAM: P+1 for a saturating position P in [p_g - 1, N(p_g + w - 1)]; AE:
+// q+w+1 for q in [p_g - w - 1, N(p_g - 1)], N = next saturating position;
+// segment 0: the stream start).  Before any byte walk, walker g looks at its
+// first 16 KiB; if they are dense in saturating bytes it indexes those of
+// [p_g - w - 1, seg_end + max_size + 1) (and the long constant runs) in its
+// idle ring, walks every candidate's chain in index space (one lane each;
+// the few steps the index cannot decide are read from the bytes) and
+// publishes, per candidate, the number of chain starts inside the segment and
+// the candidate of segment g+1 its chain enters -- or, when its exit is no
+// candidate, hands that exit over as an extra entry of segment g+1.  The last
+// walker of each block of 32 segments composes the block's tables with
+// shuffles, the last composer scans the blocks, and every walker writes its
+// own part of the true chain: no byte walk and no halo.  Anything the tables
+// cannot resolve makes the whole call fall back to the speculative walk (the
+// tables are tried only for a single stream whose grid is one co-resident
+// wave, with a timeout).  DESIGN.md §6 lists every case.
+constexpr int TK = 128;                      // table rows per segment (candidates + extra entries), 4 per lane
+constexpr int TEX = 64;                      // extra entries a segment can pass to the next one
+constexpr int TRUNS = 16;                    // constant runs a walker records (tail of its ring)
+constexpr uint32_t T_RUN_WORDS = 2 + 3 * TRUNS;  // count, TRUNS x (start, end, value), longest run
+#ifndef CDC_T_LONG_RUN
+#define CDC_T_LONG_RUN 32768
+#endif
+constexpr uint32_t T_LONG_RUN = CDC_T_LONG_RUN;  // a constant run this long makes the attempt give up at once
+constexpr uint32_t T_END = 0xFFFFFFFEu;      // link: the chain reached the stream end
+constexpr uint32_t T_BAD = 0xFFFFFFFFu;      // link: not resolvable in index space
+constexpr uint32_t T_DENSE = 8;              // saturating bytes per window a segment needs
+constexpr uint32_t T_IDX_CAP = (uint32_t)(RING_BYTES / 4);
+constexpr uint32_t T_IX_CAP = T_IDX_CAP - T_RUN_WORDS;  // index entries; the constant runs follow them
+constexpr unsigned long long T_TIMEOUT_NS = 2000000ull;  // the scanner gives up after 2 ms
+// control words (ctrl[], reset to ~0 by k_reset): 6 block composers arrived,
+// 7 all-T (~0 yes, 0 no), 8 verdict (~0 pending, 1 tables, 0 fall back)
+constexpr int T_ARRIVE = 6, T_ALL = 7, T_SCAN = 8;
+
+// ctrl[12], ctrl[13]: the first failure's reason and segment (diagnostics,
+// printed by cdc_stats when CDC_TDEBUG is set)
+__device__ __forceinline__ void t_fail(Work &W, uint32_t why = 0, uint64_t g = 0) {
+    if (ld_relaxed_u32(W.ctrl + T_ALL) != 0u) atomicAnd(W.ctrl + T_ALL, 0u);
+    if (why && atomicCAS(W.ctrl + 12, ~0u, why) == ~0u) W.ctrl[13] = (uint32_t)g;
+}
+__device__ __forceinline__ bool t_alive(const Work &W) { return ld_relaxed_u32(W.ctrl + T_ALL) != 0u; }
+
+// index of the saturating bytes of the file positions [lo, hi): ascending
+// offsets from rel into ix; returns the count, or cap + 1 when they do not fit.
+// Each lane takes TIX_G contiguous granules of 16 bytes, so lane order is
+// position order and one warp scan of the lanes' counts places every entry.
+// any byte of a 16-byte vector equal to the saturating value (255 for MAX, 0
+// for MIN): the zero-byte test on ~x (MAX) or x (MIN), exact for "any"
+template <bool MAX>
+__device__ __forceinline__ bool t_sat_any(const uint4 &v) {
+    auto f = [](uint32_t x) {
+        return MAX ? (0xFEFEFEFEu - x) & x & 0x80808080u : (x - 0x01010101u) & ~x & 0x80808080u;
+    };
+    return (f(v.x) | f(v.y) | f(v.z) | f(v.w)) != 0u;
+}
+#ifndef CDC_TIX_G
+#define CDC_TIX_G 16
+#endif
+constexpr int TIX_G = CDC_TIX_G;  // 16-byte granules per lane per step of the index pass
+template <bool MAX>
+__device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_t rel, uint32_t *ix, uint32_t cap,
+                            const uint32_t *alive = nullptr, uint32_t *runs = nullptr) {
+    const int lane = lane_id();
+    const uintptr_t fb = reinterpret_cast<uintptr_t>(fbase);
+    const uintptr_t a0 = (fb + (uintptr_t)lo) & ~(uintptr_t)15;
+    const uintptr_t a1 = fb + (uintptr_t)hi;
+    uint32_t n = 0;
+    int step = 0;
+    // constant runs (whole 8 KiB steps of one repeated byte): lane 0 tracks the open one
+    uint32_t nr = 0, rs = 0, re = 0, rc = 0, longest = 0;
+    bool ropen = false;
+    auto close_run = [&]() {
+        if (ropen && re - rs > longest) longest = re - rs;
+        if (ropen && nr < (uint32_t)TRUNS && lane == 0) {
+            runs[1 + 3 * nr] = rs;
+            runs[2 + 3 * nr] = re;
+            runs[3 + 3 * nr] = rc;
+        }
+        if (ropen && nr < (uint32_t)TRUNS) ++nr;
+        ropen = false;
+    };
+    for (uintptr_t a = a0; a < a1; a += 32 * 16 * TIX_G) {
+        // the attempt may already have failed elsewhere: look every 64 KiB
+        if (alive && (++step & 7) == 0 && ld_relaxed_u32(alive) == 0u) return cap + 1;
+        const uintptr_t la = a + (uintptr_t)lane * 16 * TIX_G;
+        // pass 1: which granules hold a saturating byte (2 integer ops per word;
+        // a flag may sit in a byte outside [lo, hi), the exact pass drops it)
+        uint32_t hit = 0;
+        uint32_t crep = 0;
+        bool lconst = runs != nullptr;
+#pragma unroll
+        for (int u = 0; u < TIX_G; ++u) {
+            const uintptr_t ga = la + (uintptr_t)(u * 16);
+            if (ga < a1) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(ga);
+                if (u == 0) crep = (v.x & 0xFFu) * 0x01010101u;
+                lconst = lconst && ((v.x ^ crep) | (v.y ^ crep) | (v.z ^ crep) | (v.w ^ crep)) == 0u;
+                if (t_sat_any<MAX>(v)) hit |= 1u << u;
+            } else {
+                lconst = false;
+            }
+        }
+        // exact byte mask of hit granule u inside [lo, hi) (reloaded: an L1 hit)
+        auto exact = [&](int u) -> uint32_t {
+            const uintptr_t ga = la + (uintptr_t)(u * 16);
+            const uint4 v = *reinterpret_cast<const uint4 *>(ga);
+            const int64_t pos = (int64_t)(ga - fb);
+            const int x0 = (int)(lo - pos > 0 ? (lo - pos > 16 ? 16 : lo - pos) : 0);
+            const int x1 = (int)(hi - pos < 16 ? (hi - pos < 0 ? 0 : hi - pos) : 16);
+            const uint32_t keep = x0 < x1 ? (((1u << x1) - 1u) & ~((1u << x0) - 1u)) : 0u;
+            return sat_mask16<MAX>(v) & keep;
+        };
+        if (runs != nullptr) {
+            const int64_t s0 = (int64_t)(a - fb), s1 = s0 + 32 * 16 * TIX_G;
+            const uint32_t c0rep = __shfl_sync(0xFFFFFFFFu, crep, 0);  // every lane, before any branch
+            const bool whole = __all_sync(0xFFFFFFFFu, lconst && crep == c0rep) && s0 >= lo && s1 <= hi;
+            const uint32_t c8 = c0rep & 0xFFu;
+            if (whole) {
+                if (ropen && rc == c8 && (int64_t)re + rel == s0) {
+                    re = (uint32_t)(s1 - rel);
+                } else {
+                    close_run();
+                    ropen = true;
+                    rs = (uint32_t)(s0 - rel);
+                    re = (uint32_t)(s1 - rel);
+                    rc = c8;
+                }
+            } else {
+                close_run();
+            }
+        }
+        uint32_t c = 0;
+        for (uint32_t h = hit; h; h &= h - 1u) c += __popc(exact(__ffs(h) - 1));
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        if (n + tot > cap) return cap + 1;
+        uint32_t at = n + incl - c;
+        const uint32_t base = (uint32_t)((int64_t)(la - fb) - rel);
+        for (uint32_t h = hit; h; h &= h - 1u) {
+            const int u = __ffs(h) - 1;
+            uint32_t mm = exact(u);
+            while (mm) {
+                ix[at++] = base + (uint32_t)(u * 16) + (uint32_t)(__ffs(mm) - 1);
+                mm &= mm - 1u;
+            }
+        }
+        n += tot;
+    }
+    if (runs != nullptr) {
+        close_run();
+        if (lane == 0) {
+            runs[0] = nr;
+            runs[1 + 3 * TRUNS] = longest;
+        }
+    }
+    __syncwarp();
+    return n;
+}
+
+// first entry of ix[0..n) that is >= r
+__device__ __forceinline__ uint32_t t_lb(const uint32_t *ix, uint32_t n, uint32_t r) {
+    uint32_t a = 0, b = n;
+    while (a < b) {
+        const uint32_t m = (a + b) >> 1;
+        if (ix[m] < r) a = m + 1;
+        else b = m;
+    }
+    return a;
+}
+
+// one saturated chunk step from start x (one lane); -1 when the step is not
+// saturated or needs bytes outside the index [lo, ihi)
+template <int ALGO>
+__device__ __forceinline__ int64_t t_step(const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi, int64_t x,
+                                          int64_t w, int64_t mx, int64_t Lf) {
+    const int64_t limit = Lf - x < mx ? Lf : x + mx;
+    if constexpr (ALGO == ALGO_RAM) {
+        if (x + w >= Lf) return Lf;  // the window does not fit: a single final chunk
+        if (x + w > ihi) return -1;
+        const uint32_t i1 = t_lb(ix, n, (uint32_t)(x - lo));
+        if (i1 >= n || lo + (int64_t)ix[i1] >= x + w) return -1;  // the window holds no saturating byte
+        const uint32_t i2 = t_lb(ix, n, (uint32_t)(x + w - lo));
+        if (i2 < n && lo + (int64_t)ix[i2] < limit) return lo + (int64_t)ix[i2] + 1;
+        return limit <= ihi ? limit : -1;
+    } else {
+        if (x + w >= limit) return limit;
+        if (x + w + 1 > ihi) return -1;
+        const uint32_t i = t_lb(ix, n, (uint32_t)(x - lo));
+        if (i >= n) return -1;
+        const int64_t q = lo + (int64_t)ix[i];
+        if (q > x + w) return -1;  // no saturating byte within w: not a saturated step
+        return q + w < limit ? q + w + 1 : limit;
+    }
+}
+
+// One chunk step from start x read from the bytes themselves (one lane, any
+// data): the rules of PAPER.md §2.1.2 exactly as run_chain applies them, for
+// the steps the index cannot decide (a window without a saturating byte, e.g.
+// inside a zero-filled region).  16-byte loads, a byte-extreme test per
+// granule, a byte loop only in the granule that holds the answer.
+template <bool MAX>
+__device__ __forceinline__ uint4 t_granule(const uint8_t *fbase, uintptr_t ga, int64_t a, int64_t b, int64_t &pos0) {
+    uint4 v = *reinterpret_cast<const uint4 *>(ga);
+    pos0 = (int64_t)(ga - reinterpret_cast<uintptr_t>(fbase));
+    if (pos0 < a || pos0 + 16 > b) {  // neutralise the bytes outside [a, b)
+        const int x0 = (int)(a - pos0 > 0 ? (a - pos0 > 16 ? 16 : a - pos0) : 0);
+        const int x1 = (int)(b - pos0 < 16 ? (b - pos0 < 0 ? 0 : b - pos0) : 16);
+        const uint32_t m16 = x0 < x1 ? (((1u << x1) - 1u) & ~((1u << x0) - 1u)) : 0u;
+        uint32_t k[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) k[j] = (((((m16 >> (4 * j)) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu);
+        if (MAX) { v.x &= k[0]; v.y &= k[1]; v.z &= k[2]; v.w &= k[3]; }
+        else { v.x |= ~k[0]; v.y |= ~k[1]; v.z |= ~k[2]; v.w |= ~k[3]; }
+    }
+    return v;
+}
+// extreme of the bytes [a, b) (a < b)
+template <bool MAX>
+__device__ uint32_t t_bytes_ext(const uint8_t *fbase, int64_t a, int64_t b) {
+    const uintptr_t fb = reinterpret_cast<uintptr_t>(fbase);
+    uint32_t acc = neutral<MAX>();
+    for (uintptr_t ga = (fb + (uintptr_t)a) & ~(uintptr_t)15; ga < fb + (uintptr_t)b; ga += 16) {
+        int64_t pos0;
+        acc = ext2<MAX>(acc, vext16<MAX>(t_granule<MAX>(fbase, ga, a, b, pos0)));
+        if (acc == (MAX ? 255u : 0u)) break;
+    }
+    return acc;
+}
+// first position in [a, b) whose byte satisfies (byte CMP t), or -1
+template <int CMP>
+__device__ int64_t t_bytes_find(const uint8_t *fbase, int64_t a, int64_t b, uint32_t t) {
+    constexpr bool MAX = (CMP == CMP_GT || CMP == CMP_GEQ);
+    const uintptr_t fb = reinterpret_cast<uintptr_t>(fbase);
+    for (uintptr_t ga = (fb + (uintptr_t)a) & ~(uintptr_t)15; ga < fb + (uintptr_t)b; ga += 16) {
+        int64_t pos0;
+        const uint4 v = t_granule<MAX>(fbase, ga, a, b, pos0);
+        if (!cmp_holds<CMP>(vext16<MAX>(v), t)) continue;
+        for (int j = 0; j < 16; ++j) {
+            const int64_t pos = pos0 + j;
+            if (pos >= a && pos < b && cmp_holds<CMP>(vbyte(v, j), t)) return pos;
+        }
+    }
+    return -1;
+}
+template <int ALGO>
+__device__ int64_t t_step_bytes(const uint8_t *fbase, int64_t x, int64_t w, int64_t mx, int64_t Lf) {
+    const int64_t limit = Lf - x < mx ? Lf : x + mx;
+    if constexpr (ALGO == ALGO_RAM) {
+        if (x + w >= Lf) return Lf;  // the window does not fit: a single final chunk
+        const uint32_t M = t_bytes_ext<true>(fbase, x, x + w);
+        const int64_t i = x + w < limit ? t_bytes_find<CMP_GEQ>(fbase, x + w, limit, M) : -1;
+        return i >= 0 ? i + 1 : limit;
+    } else {
+        constexpr bool MAX = ALGO == ALGO_AE_MAX;
+        constexpr int CMP = MAX ? CMP_GT : CMP_LT;
+        int64_t t = x;
+        uint32_t v = fbase[x];
+        while (t + w < limit) {
+            const int64_t r = t_bytes_find<CMP>(fbase, t + 1, t + w + 1, v);
+            if (r < 0) return t + w + 1;  // the target is unbeaten over its window
+            t = r;
+            v = fbase[r];
+        }
+        return limit;
+    }
+}
+// one chunk step: from the index when it decides the step, else from the
+// bytes while the chain's budget of byte steps lasts (a lane reads up to a
+// window per byte step; long unsaturated stretches, such as large zero-filled
+// regions, are left to the speculative walk): -1 when the budget is spent
+#ifndef CDC_T_BYTE_STEPS
+#define CDC_T_BYTE_STEPS 4
+#endif
+constexpr int T_BYTE_STEPS = CDC_T_BYTE_STEPS;
+template <int ALGO>
+__device__ __forceinline__ int64_t t_next(const uint8_t *fbase, const uint32_t *ix, uint32_t n, int64_t lo,
+                                          int64_t ihi, int64_t x, int64_t w, int64_t mx, int64_t Lf, int &budget) {
+    const int64_t y = t_step<ALGO>(ix, n, lo, ihi, x, w, mx, Lf);
+    if (y >= 0) return y;
+    // inside a constant run (value c) both rules end the chunk at x+w+1: RAM's
+    // window maximum is c and d[x+w] = c; AE's target c is unbeaten over (x, x+w]
+    const uint32_t *runs = ix + T_IX_CAP;
+    const int64_t limit = Lf - x < mx ? Lf : x + mx;
+    for (uint32_t r = 0; r < runs[0]; ++r) {
+        const int64_t rs = lo + (int64_t)runs[1 + 3 * r], re = lo + (int64_t)runs[2 + 3 * r];
+        if (x >= rs && x + w < re && x + w + 1 <= limit) return x + w + 1;
+    }
+    if (--budget < 0) return -1;
+    return t_step_bytes<ALGO>(fbase, x, w, mx, Lf);
+}
+
+// candidates of segment [pa, ...): index range [*i0, *i0 + K) of their
+// saturating positions; K = 0 when they are not all inside the index
+template <int ALGO>
+__device__ __forceinline__ uint32_t t_cands(const uint32_t *ix, uint32_t n, int64_t lo, int64_t pa, int64_t w,
+                                            uint32_t &i0) {
+    const int64_t clo = ALGO == ALGO_RAM ? pa - 1 : pa - w - 1;  // lowest candidate position
+    const int64_t chi = ALGO == ALGO_RAM ? pa + w - 1 : pa - 1;  // the last is N(chi)
+    if (clo < lo) return 0;
+    i0 = t_lb(ix, n, (uint32_t)(clo - lo));
+    const uint32_t i1 = t_lb(ix, n, (uint32_t)(chi - lo));
+    if (i1 >= n) return 0;
+    return i1 - i0 + 1;
+}
+__device__ __forceinline__ int64_t t_start_of(int algo, int64_t satpos, int64_t w) {
+    return algo == ALGO_RAM ? satpos + 1 : satpos + w + 1;
+}
+
+// start of candidate k of segment g (segment 0's only candidate is the
+// stream start)
+template <int ALGO>
+__device__ __forceinline__ int64_t t_cand_start(uint64_t g, const uint32_t *ix, int64_t lo, uint32_t c0, uint32_t k,
+                                                int64_t w) {
+    return g == 0 ? 0 : t_start_of(ALGO, lo + (int64_t)ix[c0 + k], w);
+}
+
+// link of a chain that exits segment g at x: the index of x among the
+// candidates of g+1 (d0 .. d0+KN-1 in the index), T_END at the stream end, or
+// T_BAD when x is not a candidate
+template <int ALGO>
+__device__ __forceinline__ uint32_t t_link(const uint32_t *ix, uint32_t n, int64_t lo, int64_t x, int64_t w,
+                                           int64_t Lf, bool last, uint32_t d0, uint32_t KN) {
+    if (last) return x >= Lf ? T_END : T_BAD;
+    const int64_t satpos = ALGO == ALGO_RAM ? x - 1 : x - w - 1;
+    if (satpos < lo) return T_BAD;
+    const uint32_t i = t_lb(ix, n, (uint32_t)(satpos - lo));
+    return (i < n && lo + (int64_t)ix[i] == satpos && i >= d0 && i < d0 + KN) ? i - d0 : T_BAD;
+}
+
+// Transfer table of segment g, phase 1: the rows of its candidates (W.tl,
+// W.tn).  A chain whose exit is not a candidate of g+1 (its last step was not
+// saturated) becomes an extra entry of g+1: its start goes to W.tex[g] and
+// its link to KN + j; the count is published in W.tnx[g] for phase 2 of g+1.
+// Returns K (the candidates; -1 when the segment cannot be resolved in index
+// space).
+template <int ALGO>
+__device__ int t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint8_t *fbase,
+                       const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi) {
+    const int lane = lane_id();
+    const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
+    uint32_t c0 = 0;
+    // no candidates (a segment that starts in a long constant run): every
+    // entry then comes as an extra entry from segment g-1
+    const uint32_t K = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, I.p, w, c0);
+    uint32_t d0 = 0, KN = 0;
+    const bool last = g == I.last;
+    if (!last) KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
+    if (K > (uint32_t)TK || KN > (uint32_t)TK) {
+        if (lane == 0) st_release_u32(W.tnx + g, 0u);
+        return -1;
+    }
+    uint32_t nx = 0;  // extra entries passed on so far
+    for (uint32_t k0 = 0; k0 < K; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        int64_t x = -1;
+        uint32_t cnt = 0;
+        if (k < K) {
+            x = t_cand_start<ALGO>(g, ix, lo, c0, k, w);
+            int budget = T_BYTE_STEPS;
+            while (x >= 0 && x < I.seg_end) {
+                ++cnt;
+                x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
+            }
+        }
+        uint32_t link = k < K && x >= 0 ? t_link<ALGO>(ix, n, lo, x, w, Lf, last, d0, KN) : T_BAD;
+        const bool extra = k < K && x >= 0 && link == T_BAD && !last;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, extra);
+        if (extra) {
+            const uint32_t j = nx + __popc(bal & ((1u << lane) - 1u));
+            if (j < (uint32_t)TEX && KN + j < (uint32_t)TK) {
+                W.tex[g * TEX + j] = x;
+                link = KN + j;
+            }
+        }
+        nx += __popc(bal);
+        if (k < K) {
+            W.tl[g * TK + k] = link;
+            W.tn[g * TK + k] = cnt;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();
+        st_release_u32(W.tnx + g, nx < (uint32_t)TEX ? nx : (uint32_t)TEX);
+    }
+    return (int)K;
+}
+
+// Phase 2: the rows of the extra entries segment g-1 passed on (rows K ..
+// K+X-1).  Their exits must be candidates of g+1 (no second hand-over).
+template <int ALGO>
+__device__ bool t_table_extras(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint8_t *fbase,
+                               const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi, uint32_t K) {
+    const int lane = lane_id();
+    const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
+    uint32_t X = 0;
+    if (g > 0) {
+        if (lane == 0) {
+            const unsigned long long t0 = globaltimer();
+            uint32_t ns = 64;
+            for (;;) {
+                X = ld_acquire_u32(W.tnx + g - 1);
+                if (X != ~0u) break;
+                if (!t_alive(W) || globaltimer() - t0 > T_TIMEOUT_NS) {
+                    X = ~0u;
+                    break;
+                }
+                __nanosleep(ns);
+                if (ns < 1024) ns <<= 1;
+            }
+        }
+        X = __shfl_sync(0xFFFFFFFFu, X, 0);
+        if (X == ~0u || K + X > (uint32_t)TK) return false;
+    }
+    uint32_t d0 = 0, KN = 0;
+    const bool last = g == I.last;
+    if (!last) KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
+    for (uint32_t j = lane; j < X; j += 32) {
+        int64_t x = W.tex[(g - 1) * TEX + j];
+        uint32_t cnt = 0;
+        int budget = T_BYTE_STEPS;
+        while (x >= 0 && x < I.seg_end) {
+            ++cnt;
+            x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
+        }
+        W.tl[g * TK + K + j] = x >= 0 ? t_link<ALGO>(ix, n, lo, x, w, Lf, last, d0, KN) : T_BAD;
+        W.tn[g * TK + K + j] = cnt;
+    }
+    if (lane == 0) W.tk[g] = K + X;
+    return true;
+}
+
+// Segments form blocks of TB: block b holds [TB b, min(TB (b+1), nsegs)).
+constexpr int TB = 32;
+__device__ __forceinline__ uint64_t t_blk_lo(uint64_t b) { return b * TB; }
+
+// gather: entry `idx` (0..TK) of a row held 4 per lane (entry u*32 + lane in r[u])
+__device__ __forceinline__ uint32_t t_gather(const uint32_t (&r)[4], uint32_t idx) {
+    const int src = (int)(idx & 31u);
+    const uint32_t v0 = __shfl_sync(0xFFFFFFFFu, r[0], src), v1 = __shfl_sync(0xFFFFFFFFu, r[1], src);
+    const uint32_t v2 = __shfl_sync(0xFFFFFFFFu, r[2], src), v3 = __shfl_sync(0xFFFFFFFFu, r[3], src);
+    const uint32_t u = idx >> 5;
+    return u == 0 ? v0 : u == 1 ? v1 : u == 2 ? v2 : v3;
+}
+
+// Compose block b's tables (the last of its walkers to publish does this):
+// for every entry candidate k of its first segment, the entry candidate and
+// the chain starts before each member (W.tp, W.tq), and the block's link and
+// start count (W.tbc, W.tbs).  Rows load four members at a time, so the
+// shuffle chain waits for one L2 round trip per four members.
+__device__ void t_compose(Work &W, uint64_t b, uint64_t nsegs) {
+    const int lane = lane_id();
+    const uint64_t hs = t_blk_lo(b), he = (b + 1) * TB < nsegs ? (b + 1) * TB : nsegs;
+    const uint32_t K0 = W.tk[hs];
+    uint32_t cur[4], acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint32_t k = (uint32_t)(u * 32 + lane);
+        cur[u] = k < K0 ? k : T_BAD;
+        acc[u] = 0;
+    }
+    for (uint64_t h0 = hs; h0 < he; h0 += 4) {
+        uint32_t L[4][4], N[4][4], Kh[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint64_t h = h0 + v;
+            Kh[v] = h < he ? W.tk[h] : 0u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                L[v][u] = h < he ? W.tl[h * TK + u * 32 + lane] : T_BAD;
+                N[v][u] = h < he ? W.tn[h * TK + u * 32 + lane] : 0u;
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint64_t h = h0 + v;
+            if (h >= he) break;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                W.tp[h * TK + u * 32 + lane] = cur[u];
+                W.tq[h * TK + u * 32 + lane] = acc[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool in = cur[u] < Kh[v];
+                const uint32_t idx = in ? cur[u] : 0u;
+                const uint32_t l = t_gather(L[v], idx), n = t_gather(N[v], idx);
+                acc[u] += in ? n : 0u;
+                cur[u] = in ? l : T_BAD;
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        W.tbc[b * TK + u * 32 + lane] = cur[u];
+        W.tbs[b * TK + u * 32 + lane] = acc[u];
+    }
+}
+
+// The scan over blocks (the last composer does it): the true chain starts
+// at segment 0's only candidate.  Rows load ahead of the shuffle chain.
+// False when some block cannot continue the chain.
+__device__ bool t_scan_blocks(Work &W, uint64_t nsegs, uint64_t *d_count) {
+    const int lane = lane_id();
+    const uint64_t NB = (nsegs + TB - 1) / TB;
+    uint32_t E = 0;
+    uint64_t O = 0;
+    for (uint64_t b0 = 0; b0 < NB; b0 += 4) {  // four blocks' rows per L2 round trip
+        uint32_t C[4][4], S[4][4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                C[v][u] = b0 + v < NB ? W.tbc[(b0 + v) * TK + u * 32 + lane] : T_BAD;
+                S[v][u] = b0 + v < NB ? W.tbs[(b0 + v) * TK + u * 32 + lane] : 0u;
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint64_t b = b0 + v;
+            if (b >= NB) break;
+            if (E >= (uint32_t)TK) {
+                if (lane == 0) t_fail(W, E == T_END ? 9 : 7, b * TB);
+                return false;
+            }
+            if (lane == 0) {
+                W.tbe[b] = E;
+                W.tbo[b] = O;
+            }
+            const uint32_t c = t_gather(C[v], E), sc = t_gather(S[v], E);
+            if (c == T_BAD) {
+                if (lane == 0) t_fail(W, 8, b * TB);
+                return false;
+            }
+            O += sc;
+            E = c;
+        }
+    }
+    if (E != T_END) {
+        if (lane == 0) t_fail(W, 11, nsegs);
+        return false;
+    }
+    if (lane == 0) {
+        W.seg_out[nsegs] = O;
+        *d_count = O;
+    }
+    return true;
+}
+
+// One T-mode attempt of walker g, before any byte walk (all 32 lanes).
+// Returns true when the call's output was produced from the tables (this
+// walker has written its part); false to fall back to the speculative walk.
+template <int ALGO>
+__device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, const SegInfo &I,
+                          uint8_t *ring, const uint8_t *fbase, uint64_t *bounds, uint64_t cap, uint64_t *d_count,
+                          int64_t pre_n) {
+    constexpr bool MAX = ALGO != ALGO_AE_MIN;
+    const int lane = lane_id();
+    const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
+    uint32_t *ix = reinterpret_cast<uint32_t *>(ring);
+    const int64_t lo = I.p - w - 1 > 0 ? I.p - w - 1 : 0;
+    const int64_t ihi = I.seg_end + mx + 1 < Lf ? I.seg_end + mx + 1 : Lf;
+    unsigned long long *tm = g_timing ? g_timing + TM_STAMPS + TM_PER_SEG * g : nullptr;
+    uint32_t n = 0;
+    if (pre_n >= 0) {  // the CTA built the index together (t_coop_index)
+        n = (uint32_t)pre_n;
+        bool mine = t_alive(W) && n <= T_IX_CAP &&
+                    (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo);
+        const int K = mine ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : -1;
+        mine = K >= 0 && t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, (uint32_t)K);
+        if (tm && lane == 0) tm[6] = globaltimer();
+        if (!mine) t_fail(W);
+    } else if (t_alive(W)) {
+        // a cheap look at the segment's first 16 KiB first: clearly sparse, no
+        // index (half the density the full check asks for: uniform bytes at
+        // w = 8 KiB give 64 +- 8 saturating bytes there, the bar is 8)
+        const int64_t shi = I.p + 16384 < ihi ? I.p + 16384 : ihi;
+        const uint32_t ns = t_index<MAX>(fbase, I.p, shi, I.p, ix, T_IDX_CAP);
+        bool mine = 2ull * ns * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(shi - I.p);
+        uint32_t why = 1;
+        if (mine) {
+            n = t_index<MAX>(fbase, lo, ihi, lo, ix, T_IX_CAP, W.ctrl + T_ALL, ix + T_IX_CAP);
+            if (tm && lane == 0) tm[5] = globaltimer();
+            // a long constant run (a zero-filled region, say): its chains keep their
+            // phases, too many to hand over; the speculative walk is the better path
+            why = n > T_IX_CAP ? 2
+                : (uint64_t)n * (uint64_t)(w + 1) < (uint64_t)T_DENSE * (uint64_t)(ihi - lo) ? 3
+                : ix[T_IX_CAP + 1 + 3 * TRUNS] >= T_LONG_RUN ? 4 : 0;
+            const int K = why == 0 ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : -1;
+            if (why == 0 && K < 0) why = 5;
+            if (why == 0 && !t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, (uint32_t)K)) why = 6;
+            mine = why == 0;
+            if (tm && lane == 0) tm[6] = globaltimer();
+        }
+        if (!mine && lane == 0) t_fail(W, why, g);
+        __syncwarp();
+    }
+    // arrive: the last walker of a block composes the block, the last composer
+    // scans the blocks.  The verdict word T_SCAN decides once (compare-and-
+    // swap from ~0): 1 = the tables produced the output, 0 = fall back.
+    const uint64_t NB = (nsegs + TB - 1) / TB;
+    const uint64_t b = g / TB;
+    const uint64_t members = ((b + 1) * TB < nsegs ? (b + 1) * TB : nsegs) - t_blk_lo(b);
+    bool composer = false, scanner = false;
+    __syncwarp();
+    if (lane == 0) {
+        if (tm) tm[2] = globaltimer();  // diagnostics: table published
+        __threadfence();
+        composer = atomicAdd(W.tblk + b, 1u) + 2u == (uint32_t)members;  // starts at ~0
+    }
+    composer = __shfl_sync(0xFFFFFFFFu, composer, 0);
+    if (composer) {
+        __threadfence();
+        if (t_alive(W)) t_compose(W, b, nsegs);
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            scanner = atomicAdd(W.ctrl + T_ARRIVE, 1u) + 2u == (uint32_t)NB;
+        }
+    }
+    scanner = __shfl_sync(0xFFFFFFFFu, scanner, 0);
+    if (scanner) {  // every block composed
+        __threadfence();
+        bool ok = t_alive(W) && nsegs >= 2;
+        if (ok) ok = t_scan_blocks(W, nsegs, d_count);
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicCAS(W.ctrl + T_SCAN, ~0u, ok ? 1u : 0u);
+            if (tm) tm[3] = globaltimer();
+        }
+    }
+    uint32_t verdict = 0;
+    if (lane == 0) {
+        const unsigned long long t0 = globaltimer();
+        uint32_t ns = 64;
+        for (;;) {
+            verdict = ld_acquire_u32(W.ctrl + T_SCAN);
+            if (verdict != ~0u) break;
+            if (!t_alive(W) || globaltimer() - t0 > T_TIMEOUT_NS) {
+                if (t_alive(W)) t_fail(W, 10, g);
+                atomicCAS(W.ctrl + T_SCAN, ~0u, 0u);  // give up (unless the scan has just decided)
+                continue;
+            }
+            __nanosleep(ns);
+            if (ns < 1024) ns <<= 1;
+        }
+    }
+    verdict = __shfl_sync(0xFFFFFFFFu, verdict, 0);
+    if (verdict != 1u) return false;
+    // this segment's part of the true chain (lane 0 walks it in index space)
+    if (lane == 0) {
+        const uint32_t Eb = W.tbe[b];
+        const uint32_t E = W.tp[g * TK + Eb];
+        uint64_t q = W.tbo[b] + W.tq[g * TK + Eb];
+        uint32_t c0 = 0;
+        const uint32_t Kc = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, I.p, w, c0);
+        // a candidate, or an extra entry handed over by segment g-1
+        int64_t x = E < Kc ? t_cand_start<ALGO>(g, ix, lo, c0, E, w) : W.tex[(g - 1) * TEX + (E - Kc)];
+        int budget = 1 << 30;  // the scan followed this chain: its table row was resolved
+        while (x < I.seg_end) {
+            if (q >= 1 && q - 1 < cap) bounds[q - 1] = (uint64_t)x;  // the stream start is not a boundary
+            ++q;
+            x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
+        }
+        if (g == nsegs - 1) {
+            const uint64_t total = W.seg_out[nsegs];
+            if (total >= 1 && total - 1 < cap) bounds[total - 1] = (uint64_t)Lf;  // the last boundary is the length
+        }
+    }
+    return true;
+}
+
+// T-mode, one segment per CTA (a small stream): the CTA's 16 warps index the
+// saturating bytes of [p - w - 1, seg_end + max_size + 1) together, one
+// sixteenth each into their own rings, and warp 0 concatenates the parts in
+// order into its ring.  Returns the entry count for warp 0 (T_IX_CAP + 1:
+// not dense or too many), or -1 when the attempt is already off.  All threads
+// of the CTA call this.
+template <int ALGO>
+__device__ int64_t t_coop_index(const Geometry &G, Work &W, uint64_t g, uint8_t *rings) {
+    constexpr bool MAX = ALGO != ALGO_AE_MIN;
+    __shared__ uint32_t s_cnt[SPEC_WARPS];
+    __shared__ int s_go;
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const SegInfo I = seg_info(G, W, g);
+    const uint8_t *fbase = G.data + I.foff;
+    const int64_t w = G.w, Lf = (int64_t)I.Lf;
+    const int64_t lo = I.p - w - 1 > 0 ? I.p - w - 1 : 0;
+    const int64_t ihi = I.seg_end + (int64_t)G.max_size + 1 < Lf ? I.seg_end + (int64_t)G.max_size + 1 : Lf;
+    uint32_t *ix = reinterpret_cast<uint32_t *>(rings + warp * RING_SMEM);
+    if (warp == 0) {  // the density sample of t_attempt
+        int go = 0;
+        if (t_alive(W)) {
+            const int64_t shi = I.p + 16384 < ihi ? I.p + 16384 : ihi;
+            const uint32_t ns = t_index<MAX>(fbase, I.p, shi, I.p, ix, T_IDX_CAP);
+            go = 2ull * ns * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(shi - I.p) ? 1 : 2;
+        }
+        if (lane == 0) s_go = go;
+    }
+    __syncthreads();
+    const int go = s_go;
+    if (go == 0) return -1;
+    if (go == 1) {
+        const int64_t part = (((ihi - lo) + 16 * SPEC_WARPS - 1) / (16 * SPEC_WARPS)) * 16;
+        const int64_t a = lo + warp * part, b = a + part < ihi ? a + part : ihi;
+        const uint32_t c = a < b ? t_index<MAX>(fbase, a, b, lo, ix, T_IX_CAP) : 0u;
+        if (lane == 0) s_cnt[warp] = c;
+    }
+    __syncthreads();
+    if (go == 2) {
+        if (warp == 0 && lane == 0) t_fail(W, 1, g);
+        return (int64_t)T_IX_CAP + 1;
+    }
+    if (warp != 0) return 0;  // only warp 0 walks the segment
+    if (lane == 0) ix[T_IX_CAP] = 0;  // no constant runs recorded on this path (its samples reject them)
+    uint32_t n = 0;
+    for (int k = 0; k < SPEC_WARPS; ++k) {
+        const uint32_t c = s_cnt[k];
+        if (c > T_IX_CAP || n + c > T_IX_CAP) return (int64_t)T_IX_CAP + 1;
+        if (k > 0) {
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(rings + k * RING_SMEM);
+            for (uint32_t i = lane; i < c; i += 32) ix[n + i] = src[i];
+        }
+        n += c;
+    }
+    __syncwarp();
+    return (int64_t)n;
+}
+
