@@ -1782,9 +1782,12 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
     stats[2] = P.Hmax;
     stats[3] = ctrl[1] == 0 ? 0 : (tables == G && G > 0 ? 2 : 1);
     if (getenv("CDC_TDEBUG")) {  // why the transfer tables gave up (diagnostics)
-        uint32_t why[2] = {0, 0};
-        CDC_CUDA(cudaMemcpy(why, W.ctrl + 12, 8, cudaMemcpyDeviceToHost));
-        fprintf(stderr, "cdc: transfer tables: reason %d at segment %u\n", (int)why[0], why[1]);
+        uint32_t why[5] = {0, 0, 0, 0, 0};
+        CDC_CUDA(cudaMemcpy(why, W.ctrl + 11, 20, cudaMemcpyDeviceToHost));
+        fprintf(stderr,
+                "cdc: transfer tables: reason %d at segment %u; unresolved chains: %d over their byte-step budget, "
+                "%d extra entries past the next segment, %d hand-overs that did not fit\n",
+                (int)why[1], why[2], (int)(why[3] + 1), (int)(why[0] + 1), (int)(why[4] + 1));
     }
     stats[4] = met;
     stats[5] = unsynced;

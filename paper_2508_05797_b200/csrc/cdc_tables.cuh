@@ -395,6 +395,7 @@ __device__ int t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I,
             }
         }
         nx += __popc(bal);
+        if (k < K && link == T_BAD) atomicAdd(W.ctrl + (x < 0 ? 14 : 15), 1u);  // diagnostics: budget / overflow
         if (k < K) {
             W.tl[g * TK + k] = link;
             W.tn[g * TK + k] = cnt;
@@ -445,7 +446,9 @@ __device__ bool t_table_extras(const Geometry &G, Work &W, uint64_t g, const Seg
             ++cnt;
             x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
         }
-        W.tl[g * TK + K + j] = x >= 0 ? t_link<ALGO>(ix, n, lo, x, w, Lf, last, d0, KN) : T_BAD;
+        const uint32_t lk = x >= 0 ? t_link<ALGO>(ix, n, lo, x, w, Lf, last, d0, KN) : T_BAD;
+        if (lk == T_BAD) atomicAdd(W.ctrl + (x < 0 ? 14 : 11), 1u);  // diagnostics: budget / second hand-over
+        W.tl[g * TK + K + j] = lk;
         W.tn[g * TK + K + j] = cnt;
     }
     if (lane == 0) W.tk[g] = K + X;
