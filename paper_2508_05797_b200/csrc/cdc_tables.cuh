@@ -179,6 +179,23 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_
     return n;
 }
 
+#ifdef CDC_T_CONST_SAMPLE
+// (experiment) true when the bytes [a, b) all equal: a density sample inside a
+// zero-filled region is then accepted.  Warp-cooperative.
+__device__ bool t_constant(const uint8_t *fbase, int64_t a, int64_t b) {
+    const uintptr_t fb = reinterpret_cast<uintptr_t>(fbase);
+    const uint32_t c = fbase[a] * 0x01010101u;
+    bool same = true;
+    for (uintptr_t ga = ((fb + (uintptr_t)a) & ~(uintptr_t)15) + (uintptr_t)lane_id() * 16; ga < fb + (uintptr_t)b;
+         ga += 32 * 16) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(ga);
+        const int64_t pos0 = (int64_t)(ga - fb);
+        if (pos0 >= a && pos0 + 16 <= b) same = same && ((v.x ^ c) | (v.y ^ c) | (v.z ^ c) | (v.w ^ c)) == 0u;
+    }
+    return __all_sync(0xFFFFFFFFu, same);
+}
+#endif
+
 // first entry of ix[0..n) that is >= r
 __device__ __forceinline__ uint32_t t_lb(const uint32_t *ix, uint32_t n, uint32_t r) {
     uint32_t a = 0, b = n;
@@ -602,14 +619,24 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         const int64_t shi = I.p + 16384 < ihi ? I.p + 16384 : ihi;
         const uint32_t ns = t_index<MAX>(fbase, I.p, shi, I.p, ix, T_IDX_CAP);
         bool mine = 2ull * ns * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(shi - I.p);
+#ifdef CDC_T_CONST_SAMPLE
+        mine = mine || t_constant(fbase, I.p, shi);
+#endif
         uint32_t why = 1;
         if (mine) {
             n = t_index<MAX>(fbase, lo, ihi, lo, ix, T_IX_CAP, W.ctrl + T_ALL, ix + T_IX_CAP);
             if (tm && lane == 0) tm[5] = globaltimer();
             // a long constant run (a zero-filled region, say): its chains keep their
             // phases, too many to hand over; the speculative walk is the better path
+#ifdef CDC_T_CONST_SAMPLE
+            uint64_t span = (uint64_t)(ihi - lo);  // (experiment) density outside the constant runs
+            for (uint32_t r = 0; r < ix[T_IX_CAP]; ++r)
+                span -= (uint64_t)(ix[T_IX_CAP + 2 + 3 * r] - ix[T_IX_CAP + 1 + 3 * r]);
+#else
+            const uint64_t span = (uint64_t)(ihi - lo);
+#endif
             why = n > T_IX_CAP ? 2
-                : (uint64_t)n * (uint64_t)(w + 1) < (uint64_t)T_DENSE * (uint64_t)(ihi - lo) ? 3
+                : (uint64_t)n * (uint64_t)(w + 1) < (uint64_t)T_DENSE * span ? 3
                 : ix[T_IX_CAP + 1 + 3 * TRUNS] >= T_LONG_RUN ? 4 : 0;
             const int K = why == 0 ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : -1;
             if (why == 0 && K < 0) why = 5;
