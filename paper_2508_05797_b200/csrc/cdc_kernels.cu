@@ -1782,8 +1782,10 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
     stats[2] = P.Hmax;
     stats[3] = ctrl[1] == 0 ? 0 : (tables == G && G > 0 ? 2 : 1);
     if (getenv("CDC_TDEBUG")) {  // why the transfer tables gave up (diagnostics)
-        uint32_t why[5] = {0, 0, 0, 0, 0};
+        uint32_t why[5] = {0, 0, 0, 0, 0}, lim = 0;
         CDC_CUDA(cudaMemcpy(why, W.ctrl + 11, 20, cudaMemcpyDeviceToHost));
+        CDC_CUDA(cudaMemcpy(&lim, W.ctrl + 10, 4, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "cdc: transfer tables: hand-over limits word %08x\n", lim + 1u);
         fprintf(stderr,
                 "cdc: transfer tables: reason %d at segment %u; unresolved chains: %d over their byte-step budget, "
                 "%d extra entries past the next segment, %d hand-overs that did not fit\n",

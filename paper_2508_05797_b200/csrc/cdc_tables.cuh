@@ -410,7 +410,13 @@ __device__ int t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I,
                 W.tex[g * TEX + j] = x;
                 link = KN + j;
             }
+#ifdef CDC_T_CONST_SAMPLE
+            else atomicAdd(W.ctrl + 10, j >= (uint32_t)TEX ? 1u : 0x10000u);  // (experiment) which limit
+#endif
         }
+#ifdef CDC_T_CONST_SAMPLE
+        if (k < K && x >= 0 && link == T_BAD && last) atomicAdd(W.ctrl + 10, 0x1000000u);
+#endif
         nx += __popc(bal);
         if (k < K && link == T_BAD) atomicAdd(W.ctrl + (x < 0 ? 14 : 15), 1u);  // diagnostics: budget / overflow
         if (k < K) {
@@ -427,7 +433,8 @@ __device__ int t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I,
 }
 
 // Phase 2: the rows of the extra entries segment g-1 passed on (rows K ..
-// K+X-1).  Their exits must be candidates of g+1 (no second hand-over).
+// K+X-1).  Their exits must be candidates of g+1 or exits this segment's
+// phase 1 already handed over (no new hand-over).
 template <int ALGO>
 __device__ bool t_table_extras(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint8_t *fbase,
                                const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi, uint32_t K) {
@@ -463,7 +470,17 @@ __device__ bool t_table_extras(const Geometry &G, Work &W, uint64_t g, const Seg
             ++cnt;
             x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
         }
-        const uint32_t lk = x >= 0 ? t_link<ALGO>(ix, n, lo, x, w, Lf, last, d0, KN) : T_BAD;
+        uint32_t lk = x >= 0 ? t_link<ALGO>(ix, n, lo, x, w, Lf, last, d0, KN) : T_BAD;
+        if (lk == T_BAD && x >= 0 && !last) {
+            // an exit this segment's own candidate chains hand over already (the
+            // chains met before the boundary): the same extra entry of g+1
+            const uint32_t nxo = ld_relaxed_u32(W.tnx + g);
+            for (uint32_t q = 0; q < nxo && q < (uint32_t)TEX; ++q)
+                if (W.tex[g * TEX + q] == x && KN + q < (uint32_t)TK) {
+                    lk = KN + q;
+                    break;
+                }
+        }
         if (lk == T_BAD) atomicAdd(W.ctrl + (x < 0 ? 14 : 11), 1u);  // diagnostics: budget / second hand-over
         W.tl[g * TK + K + j] = lk;
         W.tn[g * TK + K + j] = cnt;
