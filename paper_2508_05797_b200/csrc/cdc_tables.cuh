@@ -329,17 +329,32 @@ __device__ __forceinline__ int64_t t_next(const uint8_t *fbase, const uint32_t *
 }
 
 // candidates of segment [pa, ...): index range [*i0, *i0 + K) of their
-// saturating positions; K = 0 when they are not all inside the index
+// saturating positions (K = 0: none, a segment inside a long constant run);
+// T_UNKNOWN when the index [lo, ihi) does not decide the set.  Segments g-1
+// and g compute the set of g from different indexes and must agree on it (the
+// rows of g's extra entries follow its candidates), so "not in my index"
+// never reads as "none".
+constexpr uint32_t T_UNKNOWN = 0xFFFFFFFFu;
 template <int ALGO>
-__device__ __forceinline__ uint32_t t_cands(const uint32_t *ix, uint32_t n, int64_t lo, int64_t pa, int64_t w,
-                                            uint32_t &i0) {
-    const int64_t clo = ALGO == ALGO_RAM ? pa - 1 : pa - w - 1;  // lowest candidate position
+__device__ __forceinline__ uint32_t t_cands(const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi, int64_t Lf,
+                                            int64_t pa, int64_t w, uint32_t &i0) {
+    int64_t clo = ALGO == ALGO_RAM ? pa - 1 : pa - w - 1;  // lowest candidate position
     const int64_t chi = ALGO == ALGO_RAM ? pa + w - 1 : pa - 1;  // the last is N(chi)
-    if (clo < lo) return 0;
+    if (clo < 0) clo = 0;
+    if (clo < lo) return T_UNKNOWN;
     i0 = t_lb(ix, n, (uint32_t)(clo - lo));
     const uint32_t i1 = t_lb(ix, n, (uint32_t)(chi - lo));
-    if (i1 >= n) return 0;
-    return i1 - i0 + 1;
+    if (i1 < n) return i1 - i0 + 1;
+    return ihi >= Lf ? n - i0 : T_UNKNOWN;  // N(chi) past the stream end: every later one
+}
+// upper end of a segment's index: its chains' steps need [.., seg_end +
+// max_size + 1); RAM's candidates of the next segment reach N(seg_end + w -
+// 1), which a cap close to the window leaves outside that range
+template <int ALGO>
+__device__ __forceinline__ int64_t t_ihi(int64_t seg_end, int64_t w, int64_t mx, int64_t Lf) {
+    int64_t h = seg_end + mx + 1;
+    if (ALGO == ALGO_RAM && h < seg_end + w + 4096) h = seg_end + w + 4096;
+    return h < Lf ? h : Lf;
 }
 __device__ __forceinline__ int64_t t_start_of(int algo, int64_t satpos, int64_t w) {
     return algo == ALGO_RAM ? satpos + 1 : satpos + w + 1;
@@ -380,10 +395,10 @@ __device__ int t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I,
     uint32_t c0 = 0;
     // no candidates (a segment that starts in a long constant run): every
     // entry then comes as an extra entry from segment g-1
-    const uint32_t K = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, I.p, w, c0);
+    const uint32_t K = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, ihi, Lf, I.p, w, c0);
     uint32_t d0 = 0, KN = 0;
     const bool last = g == I.last;
-    if (!last) KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
+    if (!last) KN = t_cands<ALGO>(ix, n, lo, ihi, Lf, I.seg_end, w, d0);
     if (K > (uint32_t)TK || KN > (uint32_t)TK) {
         if (lane == 0) st_release_u32(W.tnx + g, 0u);
         return -1;
@@ -461,7 +476,7 @@ __device__ bool t_table_extras(const Geometry &G, Work &W, uint64_t g, const Seg
     }
     uint32_t d0 = 0, KN = 0;
     const bool last = g == I.last;
-    if (!last) KN = t_cands<ALGO>(ix, n, lo, I.seg_end, w, d0);
+    if (!last) KN = t_cands<ALGO>(ix, n, lo, ihi, Lf, I.seg_end, w, d0);
     for (uint32_t j = lane; j < X; j += 32) {
         int64_t x = W.tex[(g - 1) * TEX + j];
         uint32_t cnt = 0;
@@ -618,7 +633,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
     const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
     uint32_t *ix = reinterpret_cast<uint32_t *>(ring);
     const int64_t lo = I.p - w - 1 > 0 ? I.p - w - 1 : 0;
-    const int64_t ihi = I.seg_end + mx + 1 < Lf ? I.seg_end + mx + 1 : Lf;
+    const int64_t ihi = t_ihi<ALGO>(I.seg_end, w, mx, Lf);
     unsigned long long *tm = g_timing ? g_timing + TM_STAMPS + TM_PER_SEG * g : nullptr;
     uint32_t n = 0;
     if (pre_n >= 0) {  // the CTA built the index together (t_coop_index)
@@ -723,7 +738,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         const uint32_t E = W.tp[g * TK + Eb];
         uint64_t q = W.tbo[b] + W.tq[g * TK + Eb];
         uint32_t c0 = 0;
-        const uint32_t Kc = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, I.p, w, c0);
+        const uint32_t Kc = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, ihi, Lf, I.p, w, c0);
         // a candidate, or an extra entry handed over by segment g-1
         int64_t x = E < Kc ? t_cand_start<ALGO>(g, ix, lo, c0, E, w) : W.tex[(g - 1) * TEX + (E - Kc)];
         int budget = 1 << 30;  // the scan followed this chain: its table row was resolved
@@ -756,7 +771,7 @@ __device__ int64_t t_coop_index(const Geometry &G, Work &W, uint64_t g, uint8_t 
     const uint8_t *fbase = G.data + I.foff;
     const int64_t w = G.w, Lf = (int64_t)I.Lf;
     const int64_t lo = I.p - w - 1 > 0 ? I.p - w - 1 : 0;
-    const int64_t ihi = I.seg_end + (int64_t)G.max_size + 1 < Lf ? I.seg_end + (int64_t)G.max_size + 1 : Lf;
+    const int64_t ihi = t_ihi<ALGO>(I.seg_end, w, (int64_t)G.max_size, Lf);
     uint32_t *ix = reinterpret_cast<uint32_t *>(rings + warp * RING_SMEM);
     if (warp == 0) {  // the density sample of t_attempt
         int go = 0;

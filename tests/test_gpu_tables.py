@@ -52,6 +52,21 @@ def test_tables_many_small_segments(cdc):
     assert got.size == exp.size and (got == exp).all()
 
 
+@pytest.mark.parametrize("algo,slack", [("ram", 1), ("ram", 2), ("ram", 301), ("ae_max", 2), ("ae_min", 3)])
+def test_tables_tight_cap(cdc, algo, slack):
+    """max_size just above the window: nearly every chunk is cut by the cap, so
+    chain exits are rarely candidates, and RAM's candidates of a segment reach
+    past seg_end + max_size.  Both neighbours must agree on a segment's
+    candidate set (regression: an index too short to decide it read as "no
+    candidates" on one side only).  16 KiB segments, many hand-overs."""
+    d = synth.uniform((2 << 20) + 123, 40)
+    w = 5000
+    p = cdc.params(algo, window=w, max_size=w + slack, seg_bytes=16384)
+    exp = oracle.chunk(algo, d, w, w + slack)
+    got, st = _run(cdc, d, p)
+    assert got.size == exp.size and (got == exp).all(), st
+
+
 @pytest.mark.parametrize("algo", ["ram", "ae_max"])
 def test_tables_zero_region(cdc, algo):
     """A zero-filled region: steps inside it are not saturated and are read from
