@@ -62,3 +62,48 @@ def test_fuzz(cdc, case):
     exp = oracle.chunk(algo, d, w, mx)
     got = cdc.chunk(torch.from_numpy(d).cuda(), p).cpu().numpy().astype(np.uint64)
     assert got.size == exp.size and (got == exp).all(), case
+
+
+def _batch_cases(count=16, seed=20261021):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(count):
+        algo = ALGOS[i % 3]
+        kind = ["uniform", "zipf", "runs", "satedge", "small"][rng.integers(0, 5)]
+        w = int(rng.choice([1, 17, 256, 1000, 3840, 6000]))
+        mx = w + 1 + int(rng.choice([0, 5, 3 * w]))
+        nfiles = int(rng.integers(1, 400))
+        # a length mix: empty, shorter than a window, a few chunks, long files
+        sizes = rng.choice([0, 1, 7, w, w + 1, 5000, 70000, 300000], nfiles,
+                           p=[.1, .05, .05, .05, .05, .3, .3, .1]).astype(np.int64)
+        sizes = sizes + rng.integers(0, 3, nfiles) * (sizes > 0)
+        seg = int(rng.choice([0, 0, 8192, 65536]))
+        out.append((i, algo, kind, w, mx, seg, sizes))
+    return out
+
+
+@pytest.mark.parametrize("case", _batch_cases(), ids=lambda c: f"b{c[0]}-{c[1]}-{c[2]}-w{c[3]}")
+def test_fuzz_batch(cdc, case):
+    i, algo, kind, w, mx, seg, sizes = case
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    d = _data(kind, max(int(offs[-1]), 1), 500 + i)[:int(offs[-1])]
+    p = cdc.params(algo, window=w, max_size=mx, seg_bytes=seg)
+    exp, exp_bo = oracle.chunk_batch(algo, d, offs, w, mx)
+    got, bo = cdc.chunk_batch(torch.from_numpy(d).cuda(), offs, p)
+    assert (bo.cpu().numpy() == exp_bo).all()
+    assert (got.cpu().numpy().astype(np.uint64) == exp).all()
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_fuzz_large(cdc, i):
+    """Streams of 24-64 MiB: many segments per CTA, fused look-back, halos."""
+    rng = np.random.default_rng(7000 + i)
+    algo = ALGOS[i % 3]
+    kind = ["zipf", "uniform", "runs", "satedge", "zipf", "uniform"][i]
+    n = int(rng.integers(24 << 20, 64 << 20))
+    avg = int(rng.choice([512, 2048, 4096, 8192]))
+    d = _data(kind, n, 900 + i)
+    p = cdc.params(algo, avg_size=avg)
+    exp = oracle.chunk(algo, d, p.window, p.max_size)
+    got = cdc.chunk(torch.from_numpy(d).cuda(), p).cpu().numpy().astype(np.uint64)
+    assert got.size == exp.size and (got == exp).all(), (i, algo, kind, n, avg)
