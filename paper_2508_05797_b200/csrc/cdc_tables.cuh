@@ -45,6 +45,11 @@ constexpr uint32_t T_DENSE = 8;              // saturating bytes per window a se
 constexpr uint32_t T_IDX_CAP = (uint32_t)(RING_BYTES / 4);
 constexpr uint32_t T_IX_CAP = T_IDX_CAP - T_RUN_WORDS;  // index entries; the constant runs follow them
 constexpr unsigned long long T_TIMEOUT_NS = 2000000ull;  // the scanner gives up after 2 ms
+// one segment per CTA (t_coop_index): the idle rings of warps 1.. keep every
+// row's chain starts (offsets from p, entry j of row k at [j * TK + k]), so
+// the write after the verdict is a copy instead of a second walk
+constexpr int TPOS = 64;
+static_assert((SPEC_WARPS - 1) * RING_SMEM >= TK * TPOS * 4, "chain-start store does not fit the idle rings");
 // control words (ctrl[], reset to ~0 by k_reset): 6 block composers arrived,
 // 7 all-T (~0 yes, 0 no), 8 verdict (~0 pending, 1 tables, 0 fall back)
 constexpr int T_ARRIVE = 6, T_ALL = 7, T_SCAN = 8;
@@ -196,9 +201,49 @@ __device__ bool t_constant(const uint8_t *fbase, int64_t a, int64_t b) {
 }
 #endif
 
+// Bucket table over the index (in the ring's free words below the constant
+// runs): bk[c] = the first entry >= c * 256, so a lookup reads two bucket
+// words and about one entry instead of a dozen dependent loads of a binary
+// search.  ix[T_IX_CAP - 1] holds the bucket count (0: no table) whenever
+// n < T_IX_CAP; the u16 buckets sit just below it.
+constexpr int T_BK_SHIFT = 8;
+__device__ __forceinline__ const uint16_t *t_bk(const uint32_t *ix, uint32_t nb) {
+    return reinterpret_cast<const uint16_t *>(ix + T_IX_CAP - 1 - (nb + 1) / 2);
+}
+// (all lanes; after the index is final) span = ihi - lo
+__device__ void t_buckets(uint32_t *ix, uint32_t n, int64_t span) {
+    if (n >= T_IX_CAP) return;  // the header word is an entry (and such an index is refused anyway)
+    const int lane = lane_id();
+    const uint32_t nb = (uint32_t)(span >> T_BK_SHIFT) + 1;
+    const bool fit = (uint64_t)n + 1 + (nb + 1) / 2 <= (uint64_t)T_IX_CAP;
+    if (fit) {
+        uint16_t *bk = const_cast<uint16_t *>(t_bk(ix, nb));
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint32_t c0 = i == 0 ? 0u : (ix[i - 1] >> T_BK_SHIFT) + 1;
+            const uint32_t c1 = ix[i] >> T_BK_SHIFT;
+            for (uint32_t c = c0; c <= c1; ++c) bk[c] = (uint16_t)i;
+        }
+        const uint32_t t0 = n == 0 ? 0u : (ix[n - 1] >> T_BK_SHIFT) + 1;
+        for (uint32_t c = t0 + lane; c < nb; c += 32) bk[c] = (uint16_t)n;
+    }
+    __syncwarp();
+    if (lane == 0) ix[T_IX_CAP - 1] = fit ? nb : 0u;
+    __syncwarp();
+}
+
 // first entry of ix[0..n) that is >= r
 __device__ __forceinline__ uint32_t t_lb(const uint32_t *ix, uint32_t n, uint32_t r) {
     uint32_t a = 0, b = n;
+    const uint32_t nb = n < T_IX_CAP ? ix[T_IX_CAP - 1] : 0u;
+    if (nb != 0u) {
+        const uint32_t c = r >> T_BK_SHIFT;
+        if (c >= nb) return n;
+        const uint16_t *bk = t_bk(ix, nb);
+        a = bk[c];
+        const uint32_t e = c + 1 < nb ? bk[c + 1] : n;
+        while (a < e && ix[a] < r) ++a;
+        return a;
+    }
     while (a < b) {
         const uint32_t m = (a + b) >> 1;
         if (ix[m] < r) a = m + 1;
@@ -389,7 +434,7 @@ __device__ __forceinline__ uint32_t t_link(const uint32_t *ix, uint32_t n, int64
 // space).
 template <int ALGO>
 __device__ int t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint8_t *fbase,
-                       const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi) {
+                       const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi, uint32_t *pos) {
     const int lane = lane_id();
     const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
     uint32_t c0 = 0;
@@ -412,6 +457,7 @@ __device__ int t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I,
             x = t_cand_start<ALGO>(g, ix, lo, c0, k, w);
             int budget = T_BYTE_STEPS;
             while (x >= 0 && x < I.seg_end) {
+                if (pos && cnt < (uint32_t)TPOS) pos[cnt * TK + k] = (uint32_t)(x - I.p);
                 ++cnt;
                 x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
             }
@@ -452,7 +498,7 @@ __device__ int t_table(const Geometry &G, Work &W, uint64_t g, const SegInfo &I,
 // phase 1 already handed over (no new hand-over).
 template <int ALGO>
 __device__ bool t_table_extras(const Geometry &G, Work &W, uint64_t g, const SegInfo &I, const uint8_t *fbase,
-                               const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi, uint32_t K) {
+                               const uint32_t *ix, uint32_t n, int64_t lo, int64_t ihi, uint32_t K, uint32_t *pos) {
     const int lane = lane_id();
     const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
     uint32_t X = 0;
@@ -482,6 +528,7 @@ __device__ bool t_table_extras(const Geometry &G, Work &W, uint64_t g, const Seg
         uint32_t cnt = 0;
         int budget = T_BYTE_STEPS;
         while (x >= 0 && x < I.seg_end) {
+            if (pos && cnt < (uint32_t)TPOS) pos[cnt * TK + K + j] = (uint32_t)(x - I.p);
             ++cnt;
             x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
         }
@@ -525,6 +572,45 @@ __device__ __forceinline__ uint32_t t_gather(const uint32_t (&r)[4], uint32_t id
 __device__ void t_compose(Work &W, uint64_t b, uint64_t nsegs) {
     const int lane = lane_id();
     const uint64_t hs = t_blk_lo(b), he = (b + 1) * TB < nsegs ? (b + 1) * TB : nsegs;
+    // narrow tables (every member has at most 32 rows, the common case): all
+    // members' rows in one L2 round trip, one row per lane
+    const uint32_t myk = lane < (int)(he - hs) ? W.tk[hs + lane] : 0u;
+    if (__reduce_max_sync(0xFFFFFFFFu, myk) <= 32u) {
+        constexpr int HB = TB / 4;  // members per L2 round trip
+        uint32_t c1 = lane < (int)__shfl_sync(0xFFFFFFFFu, myk, 0) ? (uint32_t)lane : T_BAD, a1 = 0;
+        for (int v0 = 0; v0 < TB; v0 += HB) {
+            uint32_t L1[HB], N1[HB];
+#pragma unroll
+            for (int v = 0; v < HB; ++v) {
+                const uint64_t h = hs + v0 + v;
+                L1[v] = h < he ? W.tl[h * TK + lane] : T_BAD;
+                N1[v] = h < he ? W.tn[h * TK + lane] : 0u;
+            }
+#pragma unroll
+            for (int v = 0; v < HB; ++v) {
+                const uint64_t h = hs + v0 + v;
+                const uint32_t Kh = __shfl_sync(0xFFFFFFFFu, myk, v0 + v);
+                if (h < he) {  // uniform across the warp
+                    W.tp[h * TK + lane] = c1;
+                    W.tq[h * TK + lane] = a1;
+                }
+                const bool in = h < he && c1 < Kh;
+                const uint32_t idx = in ? c1 : 0u;
+                const uint32_t l = __shfl_sync(0xFFFFFFFFu, L1[v], (int)idx);
+                const uint32_t nn = __shfl_sync(0xFFFFFFFFu, N1[v], (int)idx);
+                if (h < he) {
+                    a1 += in ? nn : 0u;
+                    c1 = in ? l : T_BAD;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            W.tbc[b * TK + u * 32 + lane] = u == 0 ? c1 : T_BAD;
+            W.tbs[b * TK + u * 32 + lane] = u == 0 ? a1 : 0u;
+        }
+        return;
+    }
     const uint32_t K0 = W.tk[hs];
     uint32_t cur[4], acc[4];
 #pragma unroll
@@ -632,6 +718,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
     const int lane = lane_id();
     const int64_t w = G.w, mx = (int64_t)G.max_size, Lf = (int64_t)I.Lf;
     uint32_t *ix = reinterpret_cast<uint32_t *>(ring);
+    uint32_t *pos = pre_n >= 0 ? reinterpret_cast<uint32_t *>(ring + RING_SMEM) : nullptr;
     const int64_t lo = I.p - w - 1 > 0 ? I.p - w - 1 : 0;
     const int64_t ihi = t_ihi<ALGO>(I.seg_end, w, mx, Lf);
     unsigned long long *tm = g_timing ? g_timing + TM_STAMPS + TM_PER_SEG * g : nullptr;
@@ -640,8 +727,8 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         n = (uint32_t)pre_n;
         bool mine = t_alive(W) && n <= T_IX_CAP &&
                     (uint64_t)n * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(ihi - lo);
-        const int K = mine ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : -1;
-        mine = K >= 0 && t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, (uint32_t)K);
+        const int K = mine ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, pos) : -1;
+        mine = K >= 0 && t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, (uint32_t)K, pos);
         if (tm && lane == 0) tm[6] = globaltimer();
         if (!mine) t_fail(W);
     } else if (t_alive(W)) {
@@ -657,6 +744,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         uint32_t why = 1;
         if (mine) {
             n = t_index<MAX>(fbase, lo, ihi, lo, ix, T_IX_CAP, W.ctrl + T_ALL, ix + T_IX_CAP);
+            t_buckets(ix, n, ihi - lo);
             if (tm && lane == 0) tm[5] = globaltimer();
             // a long constant run (a zero-filled region, say): its chains keep their
             // phases, too many to hand over; the speculative walk is the better path
@@ -670,9 +758,9 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
             why = n > T_IX_CAP ? 2
                 : (uint64_t)n * (uint64_t)(w + 1) < (uint64_t)T_DENSE * span ? 3
                 : ix[T_IX_CAP + 1 + 3 * TRUNS] >= T_LONG_RUN ? 4 : 0;
-            const int K = why == 0 ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi) : -1;
+            const int K = why == 0 ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, pos) : -1;
             if (why == 0 && K < 0) why = 5;
-            if (why == 0 && !t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, (uint32_t)K)) why = 6;
+            if (why == 0 && !t_table_extras<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, (uint32_t)K, pos)) why = 6;
             mine = why == 0;
             if (tm && lane == 0) tm[6] = globaltimer();
         }
@@ -698,6 +786,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         if (t_alive(W)) t_compose(W, b, nsegs);
         __syncwarp();
         if (lane == 0) {
+            if (tm) tm[4] = globaltimer();  // diagnostics: block composed
             __threadfence();
             scanner = atomicAdd(W.ctrl + T_ARRIVE, 1u) + 2u == (uint32_t)NB;
         }
@@ -711,7 +800,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         if (lane == 0) {
             __threadfence();
             atomicCAS(W.ctrl + T_SCAN, ~0u, ok ? 1u : 0u);
-            if (tm) tm[3] = globaltimer();
+            if (tm) tm[5] = globaltimer();  // diagnostics: scan done (replaces the index stamp)
         }
     }
     uint32_t verdict = 0;
@@ -731,26 +820,35 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
         }
     }
     verdict = __shfl_sync(0xFFFFFFFFu, verdict, 0);
+    if (tm && lane == 0) tm[1] = globaltimer();  // diagnostics: verdict seen
     if (verdict != 1u) return false;
-    // this segment's part of the true chain (lane 0 walks it in index space)
-    if (lane == 0) {
-        const uint32_t Eb = W.tbe[b];
-        const uint32_t E = W.tp[g * TK + Eb];
-        uint64_t q = W.tbo[b] + W.tq[g * TK + Eb];
+    // this segment's part of the true chain: copied from the chain-start store
+    // when the table pass kept it, else walked again in index space by lane 0
+    const uint32_t Eb = W.tbe[b];
+    const uint32_t E = W.tp[g * TK + Eb];
+    const uint64_t q0 = W.tbo[b] + W.tq[g * TK + Eb];
+    const uint32_t cntE = W.tn[g * TK + E];
+    if (pos && cntE <= (uint32_t)TPOS) {
+        for (uint32_t j = lane; j < cntE; j += 32) {
+            const uint64_t q = q0 + j;
+            if (q >= 1 && q - 1 < cap) bounds[q - 1] = (uint64_t)I.p + pos[j * TK + E];  // the stream start is not a boundary
+        }
+    } else if (lane == 0) {
+        uint64_t q = q0;
         uint32_t c0 = 0;
         const uint32_t Kc = g == 0 ? 1u : t_cands<ALGO>(ix, n, lo, ihi, Lf, I.p, w, c0);
         // a candidate, or an extra entry handed over by segment g-1
         int64_t x = E < Kc ? t_cand_start<ALGO>(g, ix, lo, c0, E, w) : W.tex[(g - 1) * TEX + (E - Kc)];
         int budget = 1 << 30;  // the scan followed this chain: its table row was resolved
         while (x < I.seg_end) {
-            if (q >= 1 && q - 1 < cap) bounds[q - 1] = (uint64_t)x;  // the stream start is not a boundary
+            if (q >= 1 && q - 1 < cap) bounds[q - 1] = (uint64_t)x;
             ++q;
             x = t_next<ALGO>(fbase, ix, n, lo, ihi, x, w, mx, Lf, budget);
         }
-        if (g == nsegs - 1) {
-            const uint64_t total = W.seg_out[nsegs];
-            if (total >= 1 && total - 1 < cap) bounds[total - 1] = (uint64_t)Lf;  // the last boundary is the length
-        }
+    }
+    if (lane == 0 && g == nsegs - 1) {
+        const uint64_t total = W.seg_out[nsegs];
+        if (total >= 1 && total - 1 < cap) bounds[total - 1] = (uint64_t)Lf;  // the last boundary is the length
     }
     return true;
 }
@@ -809,6 +907,7 @@ __device__ int64_t t_coop_index(const Geometry &G, Work &W, uint64_t g, uint8_t 
         n += c;
     }
     __syncwarp();
+    t_buckets(ix, n, ihi - lo);
     return (int64_t)n;
 }
 

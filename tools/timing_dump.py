@@ -58,6 +58,15 @@ if (a[:, 5] > 0).any():
     tb = (a[ok, 6] - a[ok, 5]) / 1e3
     print("T-mode: from start to index built us p50 %.1f max %.1f; table us p50 %.1f max %.1f" % (
         np.percentile(ib, 50) if ib.size else 0, ib.max() if ib.size else 0, np.percentile(tb, 50) if tb.size else 0, tb.max() if tb.size else 0))
+if st["fast_path"] == 2:  # T-mode phases: tm[2] published, tm[4] composed, tm[5] scanned, tm[1] verdict, tm[3] done
+    rel = lambda v: (v - t0) / 1e3
+    comp = a[a[:, 4] > 0, 4]
+    ver = a[a[:, 1] > 0, 1]
+    print("T-mode abs us: published p50 %.1f max %.1f; composed max %.1f (%d composers); scan done %.1f; verdict seen p50 %.1f max %.1f; written p50 %.1f max %.1f" % (
+        np.percentile(rel(a[:, 2]), 50), rel(a[:, 2]).max(), rel(comp).max() if comp.size else -1, comp.size,
+        rel(a[:, 5]).max(), np.percentile(rel(ver), 50) if ver.size else -1, rel(ver).max() if ver.size else -1,
+        np.percentile(rel(a[:, 3]), 50), rel(a[:, 3]).max()))
+    sys.exit(0)
 print("walk end us (abs): p50 %.1f p90 %.1f max %.1f" % tuple(np.percentile(start + walk, [50, 90, 100])))
 print("done us (abs): p50 %.1f max %.1f" % (np.percentile(done, 50), done.max()))
 print("halo chunks: mean %.2f max %d" % (halo.mean(), halo.max()))
