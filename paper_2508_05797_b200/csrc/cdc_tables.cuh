@@ -572,42 +572,61 @@ __device__ __forceinline__ uint32_t t_gather(const uint32_t (&r)[4], uint32_t id
 __device__ void t_compose(Work &W, uint64_t b, uint64_t nsegs) {
     const int lane = lane_id();
     const uint64_t hs = t_blk_lo(b), he = (b + 1) * TB < nsegs ? (b + 1) * TB : nsegs;
-    // narrow tables (every member has at most 32 rows, the common case): all
-    // members' rows in one L2 round trip, one row per lane
+    // narrow tables (every member has at most 64 rows, the common case): two
+    // rows per lane, eight members per L2 round trip
     const uint32_t myk = lane < (int)(he - hs) ? W.tk[hs + lane] : 0u;
-    if (__reduce_max_sync(0xFFFFFFFFu, myk) <= 32u) {
-        constexpr int HB = TB / 4;  // members per L2 round trip
-        uint32_t c1 = lane < (int)__shfl_sync(0xFFFFFFFFu, myk, 0) ? (uint32_t)lane : T_BAD, a1 = 0;
+    if (__reduce_max_sync(0xFFFFFFFFu, myk) <= 64u) {
+        constexpr int HB = 8;  // members per L2 round trip
+        const uint32_t K0 = __shfl_sync(0xFFFFFFFFu, myk, 0);
+        uint32_t c2[2], a2[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const uint32_t k = (uint32_t)(u * 32 + lane);
+            c2[u] = k < K0 ? k : T_BAD;
+            a2[u] = 0;
+        }
         for (int v0 = 0; v0 < TB; v0 += HB) {
-            uint32_t L1[HB], N1[HB];
+            uint32_t L2[HB][2], N2[HB][2];
 #pragma unroll
             for (int v = 0; v < HB; ++v) {
                 const uint64_t h = hs + v0 + v;
-                L1[v] = h < he ? W.tl[h * TK + lane] : T_BAD;
-                N1[v] = h < he ? W.tn[h * TK + lane] : 0u;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    L2[v][u] = h < he ? W.tl[h * TK + u * 32 + lane] : T_BAD;
+                    N2[v][u] = h < he ? W.tn[h * TK + u * 32 + lane] : 0u;
+                }
             }
 #pragma unroll
             for (int v = 0; v < HB; ++v) {
                 const uint64_t h = hs + v0 + v;
                 const uint32_t Kh = __shfl_sync(0xFFFFFFFFu, myk, v0 + v);
                 if (h < he) {  // uniform across the warp
-                    W.tp[h * TK + lane] = c1;
-                    W.tq[h * TK + lane] = a1;
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        W.tp[h * TK + u * 32 + lane] = c2[u];
+                        W.tq[h * TK + u * 32 + lane] = a2[u];
+                    }
                 }
-                const bool in = h < he && c1 < Kh;
-                const uint32_t idx = in ? c1 : 0u;
-                const uint32_t l = __shfl_sync(0xFFFFFFFFu, L1[v], (int)idx);
-                const uint32_t nn = __shfl_sync(0xFFFFFFFFu, N1[v], (int)idx);
-                if (h < he) {
-                    a1 += in ? nn : 0u;
-                    c1 = in ? l : T_BAD;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const bool in = h < he && c2[u] < Kh;
+                    const uint32_t idx = in ? c2[u] : 0u;
+                    const int src = (int)(idx & 31u);
+                    const uint32_t l0 = __shfl_sync(0xFFFFFFFFu, L2[v][0], src);
+                    const uint32_t l1 = __shfl_sync(0xFFFFFFFFu, L2[v][1], src);
+                    const uint32_t n0 = __shfl_sync(0xFFFFFFFFu, N2[v][0], src);
+                    const uint32_t n1 = __shfl_sync(0xFFFFFFFFu, N2[v][1], src);
+                    if (h < he) {
+                        a2[u] += in ? (idx >> 5 ? n1 : n0) : 0u;
+                        c2[u] = in ? (idx >> 5 ? l1 : l0) : T_BAD;
+                    }
                 }
             }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            W.tbc[b * TK + u * 32 + lane] = u == 0 ? c1 : T_BAD;
-            W.tbs[b * TK + u * 32 + lane] = u == 0 ? a1 : 0u;
+            W.tbc[b * TK + u * 32 + lane] = u < 2 ? c2[u & 1] : T_BAD;
+            W.tbs[b * TK + u * 32 + lane] = u < 2 ? a2[u & 1] : 0u;
         }
         return;
     }
