@@ -19,7 +19,7 @@
 // q+w+1 for q in [p_g - w - 1, N(p_g - 1)], N = next saturating position;
 // segment 0: the stream start).  Before any byte walk, walker g looks at its
 // first 16 KiB; if they are dense in saturating bytes it indexes those of
-// [p_g - w - 1, seg_end + max_size + 1) (and the long constant runs) in its
+// [p_g - w - 1, t_ihi) (and the long constant runs) in its
 // idle ring, walks every candidate's chain in index space (one lane each;
 // the few steps the index cannot decide are read from the bytes) and
 // publishes, per candidate, the number of chain starts inside the segment and
@@ -392,13 +392,19 @@ __device__ __forceinline__ uint32_t t_cands(const uint32_t *ix, uint32_t n, int6
     if (i1 < n) return i1 - i0 + 1;
     return ihi >= Lf ? n - i0 : T_UNKNOWN;  // N(chi) past the stream end: every later one
 }
-// upper end of a segment's index: its chains' steps need [.., seg_end +
-// max_size + 1); RAM's candidates of the next segment reach N(seg_end + w -
-// 1), which a cap close to the window leaves outside that range
+// upper end of a segment's index.  A chain's last step inside the segment
+// starts before seg_end: AE reads its target range (x, x + w] only, RAM the
+// first saturating byte at or after x + w, which uniform-like bytes put a few
+// hundred bytes later; RAM's candidates of the next segment reach N(seg_end
+// + w - 1).  So the index stops 4 KiB (AE) or 16 KiB (RAM: room for short
+// unsaturated stretches there) past seg_end + w, not at seg_end + max_size:
+// a step that would need more is read from the bytes, a candidate set it
+// cannot decide makes the attempt fall back.  ~12 % (AE) / ~8 % (RAM) less
+// index work at the default caps.
 template <int ALGO>
 __device__ __forceinline__ int64_t t_ihi(int64_t seg_end, int64_t w, int64_t mx, int64_t Lf) {
-    int64_t h = seg_end + mx + 1;
-    if (ALGO == ALGO_RAM && h < seg_end + w + 4096) h = seg_end + w + 4096;
+    int64_t h = seg_end + w + (ALGO == ALGO_RAM ? 16384 : 4096);
+    if (ALGO != ALGO_RAM && h > seg_end + mx + 1) h = seg_end + mx + 1;  // AE never reads past the cap
     return h < Lf ? h : Lf;
 }
 __device__ __forceinline__ int64_t t_start_of(int algo, int64_t satpos, int64_t w) {
@@ -873,7 +879,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
 }
 
 // T-mode, one segment per CTA (a small stream): the CTA's 16 warps index the
-// saturating bytes of [p - w - 1, seg_end + max_size + 1) together, one
+// saturating bytes of [p - w - 1, t_ihi) together, one
 // sixteenth each into their own rings, and warp 0 concatenates the parts in
 // order into its ring.  Returns the entry count for warp 0 (T_IX_CAP + 1:
 // not dense or too many), or -1 when the attempt is already off.  All threads
