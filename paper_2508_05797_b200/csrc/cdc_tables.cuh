@@ -79,6 +79,16 @@ __device__ __forceinline__ bool t_sat_any(const uint4 &v) {
 #define CDC_TIX_G 16
 #endif
 constexpr int TIX_G = CDC_TIX_G;  // 16-byte granules per lane per step of the index pass
+#ifndef CDC_TIX_PF
+#define CDC_TIX_PF 2
+#endif
+constexpr int TIX_PF = CDC_TIX_PF;  // steps ahead the index pass asks the TMA unit to bring into L2
+// bulk L2 prefetch of [p, min(p + bytes, end)) (one lane; p 16-byte aligned)
+__device__ __forceinline__ void t_prefetch_l2(uintptr_t p, uintptr_t end, uint32_t bytes) {
+    if (p >= end) return;
+    const uint32_t sz = (uint32_t)(end - p < bytes ? end - p : bytes) & ~15u;
+    if (sz) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(sz) : "memory");
+}
 template <bool MAX>
 __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_t rel, uint32_t *ix, uint32_t cap,
                             const uint32_t *alive = nullptr, uint32_t *runs = nullptr) {
@@ -101,7 +111,11 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_
         if (ropen && nr < (uint32_t)TRUNS) ++nr;
         ropen = false;
     };
-    for (uintptr_t a = a0; a < a1; a += 32 * 16 * TIX_G) {
+    constexpr uint32_t BLK = 32 * 16 * TIX_G;
+    if (TIX_PF > 0 && lane == 0)
+        for (int k = 1; k < TIX_PF; ++k) t_prefetch_l2(a0 + (uintptr_t)k * BLK, a1, BLK);
+    for (uintptr_t a = a0; a < a1; a += BLK) {
+        if (TIX_PF > 0 && lane == 0) t_prefetch_l2(a + (uintptr_t)TIX_PF * BLK, a1, BLK);
         // the attempt may already have failed elsewhere: look every 64 KiB
         if (alive && (++step & 7) == 0 && ld_relaxed_u32(alive) == 0u) return cap + 1;
         const uintptr_t la = a + (uintptr_t)lane * 16 * TIX_G;
