@@ -63,7 +63,7 @@ __device__ __forceinline__ void t_fail(Work &W, uint32_t why = 0, uint64_t g = 0
 __device__ __forceinline__ bool t_alive(const Work &W) { return ld_relaxed_u32(W.ctrl + T_ALL) != 0u; }
 
 // index of the saturating bytes of the file positions [lo, hi): ascending
-// offsets from rel into ix; returns the count, or cap + 1 when they do not fit.
+// offsets from rel into ix; returns the count, cap + 1 when they do not fit (or the attempt is off), cap + 2 at a constant run of T_LONG_RUN bytes.
 // Each lane takes TIX_G contiguous granules of 16 bytes, so lane order is
 // position order and one warp scan of the lanes' counts places every entry.
 // any byte of a 16-byte vector equal to the saturating value (255 for MAX, 0
@@ -116,8 +116,8 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_
         for (int k = 1; k < TIX_PF; ++k) t_prefetch_l2(a0 + (uintptr_t)k * BLK, a1, BLK);
     for (uintptr_t a = a0; a < a1; a += BLK) {
         if (TIX_PF > 0 && lane == 0) t_prefetch_l2(a + (uintptr_t)TIX_PF * BLK, a1, BLK);
-        // the attempt may already have failed elsewhere: look every 64 KiB
-        if (alive && (++step & 7) == 0 && ld_relaxed_u32(alive) == 0u) return cap + 1;
+        // the attempt may already have failed elsewhere: look every 16 KiB
+        if (alive && (++step & 1) == 0 && ld_relaxed_u32(alive) == 0u) return cap + 1;
         const uintptr_t la = a + (uintptr_t)lane * 16 * TIX_G;
         // pass 1: which granules hold a saturating byte (2 integer ops per word;
         // a flag may sit in a byte outside [lo, hi), the exact pass drops it)
@@ -154,6 +154,7 @@ __device__ uint32_t t_index(const uint8_t *fbase, int64_t lo, int64_t hi, int64_
             if (whole) {
                 if (ropen && rc == c8 && (int64_t)re + rel == s0) {
                     re = (uint32_t)(s1 - rel);
+                    if (re - rs >= T_LONG_RUN) return cap + 2;  // a long constant run: give up at once
                 } else {
                     close_run();
                     ropen = true;
@@ -794,7 +795,7 @@ __device__ bool t_attempt(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs
 #else
             const uint64_t span = (uint64_t)(ihi - lo);
 #endif
-            why = n > T_IX_CAP ? 2
+            why = n == T_IX_CAP + 2 ? 4 : n > T_IX_CAP ? 2
                 : (uint64_t)n * (uint64_t)(w + 1) < (uint64_t)T_DENSE * span ? 3
                 : ix[T_IX_CAP + 1 + 3 * TRUNS] >= T_LONG_RUN ? 4 : 0;
             const int K = why == 0 ? t_table<ALGO>(G, W, g, I, fbase, ix, n, lo, ihi, pos) : -1;

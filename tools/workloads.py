@@ -109,3 +109,9 @@ if "c4big" in sel:
 if "c3" in sel:  # configs[3], one GPU's share at 8 GPUs
     data, offs = synth.many_files(12500, seed=3)
     run_batch("c3 many files (12.5k)", data, offs, "ram", 8192)
+if "v128" in sel:  # versioned bytes at 24-128 MiB: transfer tables attempted and refused (CDC_TMODE=0 to compare)
+    for mib in (24, 128):
+        v = synth.versioned(mib << 20, 1, seed=2)[-1]
+        for algo in ("ram", "ae_max"):
+            for avg in (8192, 16384):
+                run("versioned %dMiB" % mib, v, algo, avg, reps=5)
