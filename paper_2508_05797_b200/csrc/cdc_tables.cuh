@@ -911,11 +911,21 @@ __device__ int64_t t_coop_index(const Geometry &G, Work &W, uint64_t g, uint8_t 
     const int64_t lo = I.p - w - 1 > 0 ? I.p - w - 1 : 0;
     const int64_t ihi = t_ihi<ALGO>(I.seg_end, w, (int64_t)G.max_size, Lf);
     uint32_t *ix = reinterpret_cast<uint32_t *>(rings + warp * RING_SMEM);
-    if (warp == 0) {  // the density sample of t_attempt
+    // the density sample of t_attempt (the segment's first 16 KiB), one
+    // sixteenth per warp
+    const int64_t shi = I.p + 16384 < ihi ? I.p + 16384 : ihi;
+    {
+        const int64_t sp = (((shi - I.p) + 16 * SPEC_WARPS - 1) / (16 * SPEC_WARPS)) * 16;
+        const int64_t sa = I.p + warp * sp, sb = sa + sp < shi ? sa + sp : shi;
+        const uint32_t c = sa < sb ? t_index<MAX>(fbase, sa, sb, sa, ix, T_IDX_CAP) : 0u;
+        if (lane == 0) s_cnt[warp] = c;
+    }
+    __syncthreads();
+    if (warp == 0) {
         int go = 0;
         if (t_alive(W)) {
-            const int64_t shi = I.p + 16384 < ihi ? I.p + 16384 : ihi;
-            const uint32_t ns = t_index<MAX>(fbase, I.p, shi, I.p, ix, T_IDX_CAP);
+            uint64_t ns = 0;
+            for (int k = 0; k < SPEC_WARPS; ++k) ns += s_cnt[k];
             go = 2ull * ns * (uint64_t)(w + 1) >= (uint64_t)T_DENSE * (uint64_t)(shi - I.p) ? 1 : 2;
         }
         if (lane == 0) s_go = go;

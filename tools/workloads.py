@@ -115,3 +115,7 @@ if "v128" in sel:  # versioned bytes at 24-128 MiB: transfer tables attempted an
         for algo in ("ram", "ae_max"):
             for avg in (8192, 16384):
                 run("versioned %dMiB" % mib, v, algo, avg, reps=5)
+if "small" in sel:  # 16 MiB streams one segment per SM: saturated (tables) and not (refused after the sample)
+    run("zipf 16MiB", synth.zipf_bytes(16 << 20, 1.1, 1), "ae_max", 8192)
+    run("zipf 16MiB", synth.zipf_bytes(16 << 20, 1.1, 1), "ram", 8192)
+    run("versioned 16MiB", synth.versioned(16 << 20, 0, seed=2)[0], "ram", 8192)
