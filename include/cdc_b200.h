@@ -252,8 +252,10 @@ int cdc_plan_info(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint
  * {at start, at the end of its body walk (first boundary at or past the
  * segment end; 0 if none), at the end of the walk, at the end of its fused
  * write, SM id | halo chunks << 32, transfer tables: index built, table
- * built}.  NULL turns recording off.  Never set during
- * measurements.
+ * built}.  A segment the transfer tables resolve reuses the slots as {at
+ * start, verdict seen, table published, written, block composed (composers
+ * only), index built (scan done for the scanner), table built}.  NULL turns
+ * recording off.  Never set during measurements.
  */
 int cdc_debug_timing(void *d_buf);
 
