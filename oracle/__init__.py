@@ -26,6 +26,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -63,6 +64,10 @@ def _load():
         lib.oracle_chunk.restype = u64
         lib.oracle_chain_from.argtypes = [ctypes.c_int, u8p, u64, u64, u64, u64, u64, u64p, u64]
         lib.oracle_chain_from.restype = u64
+        lib.oracle_check_ends.argtypes = [ctypes.c_int, u8p, u64, u64, u64, u64p, u64, u64]
+        lib.oracle_check_ends.restype = u64
+        lib.oracle_check_batch.argtypes = [ctypes.c_int, u8p, u64p, u64p, u64p, u64, u64, u64, u64, u64p]
+        lib.oracle_check_batch.restype = u64
         _lib = lib
     return _lib
 
@@ -146,3 +151,72 @@ def chunk_batch(algo: str, data, offsets, w: int, max_size: int):
         bo[i + 1] = bo[i] + e.size
     ends = np.concatenate(outs) if outs else np.zeros(0, dtype=np.uint64)
     return ends, bo
+
+
+def _threads(threads):
+    return max(1, threads if threads else (os.cpu_count() or 1))
+
+
+def check_chunking(algo: str, data, ends, w: int, max_size: int, threads: int | None = None):
+    """Check a chunking of `data` against the definition, every chunk: returns None
+    when ``ends`` equals ``chunk(algo, data, w, max_size)``, else
+    (index, expected end, got).  Each entry is checked as
+    ends[j] == chunk_end(ends[j-1]) (ends[-1] read as 0), so the work splits
+    over host threads (ctypes releases the GIL)."""
+    d = _u8(data)
+    _check(w, max_size)
+    e = np.ascontiguousarray(ends, dtype=np.uint64)
+    n, L = e.size, d.size
+    if L == 0:
+        return None if n == 0 else (0, None, int(e[0]))
+    if n == 0:
+        return (0, chunk_end(algo, d, 0, w, max_size), None)
+    lib = _load()
+    T = min(_threads(threads), max(1, n // 64))
+    cuts = [n * t // T for t in range(T + 1)]
+
+    def part(t):
+        return int(lib.oracle_check_ends(ALGOS[algo], _p8(d), L, w, max_size, _p64(e), cuts[t], cuts[t + 1]))
+
+    with ThreadPoolExecutor(T) as ex:
+        bad = [j for t, j in enumerate(ex.map(part, range(T))) if j < cuts[t + 1]]
+    if bad:
+        j = min(bad)
+        s = int(e[j - 1]) if j else 0
+        return (j, chunk_end(algo, d, s, w, max_size) if s < L else None, int(e[j]))
+    if int(e[-1]) != L:
+        return (n, L, int(e[-1]))
+    return None
+
+
+def check_batch(algo: str, data, offsets, ends, bound_offsets, w: int, max_size: int,
+                threads: int | None = None):
+    """check_chunking for every file of a packed batch (file f: data[offsets[f]:offsets[f+1]],
+    its ends relative to the file start in ends[bound_offsets[f]:bound_offsets[f+1]]).
+    Returns None when every file's chunking equals the oracle's, else (file, entry index)."""
+    d = _u8(data)
+    _check(w, max_size)
+    offs = np.ascontiguousarray(offsets, dtype=np.uint64)
+    bo = np.ascontiguousarray(bound_offsets, dtype=np.uint64)
+    e = np.ascontiguousarray(ends, dtype=np.uint64)
+    nf = offs.size - 1
+    if bo.size != offs.size or bo[0] != 0 or (np.diff(bo.astype(np.int64)) < 0).any() or int(bo[-1]) > e.size:
+        return (-1, -1)
+    if nf <= 0:
+        return None
+    lib = _load()
+    T = min(_threads(threads), nf)
+    # split the files into T ranges of about equal bytes
+    cum = offs.astype(np.float64)
+    cuts = [0] + [int(np.searchsorted(cum, cum[-1] * t / T)) for t in range(1, T)] + [nf]
+    cuts = sorted(set(min(max(c, 0), nf) for c in cuts))
+
+    def part(i):
+        bj = ctypes.c_uint64(0)
+        f = int(lib.oracle_check_batch(ALGOS[algo], _p8(d), _p64(offs), _p64(e), _p64(bo), cuts[i], cuts[i + 1],
+                                       w, max_size, ctypes.byref(bj)))
+        return (f, int(bj.value)) if f < cuts[i + 1] else None
+
+    with ThreadPoolExecutor(len(cuts) - 1) as ex:
+        bad = [r for r in ex.map(part, range(len(cuts) - 1)) if r is not None]
+    return min(bad) if bad else None

@@ -178,3 +178,56 @@ uint64_t oracle_chain_from(int algo, const uint8_t *d, uint64_t L, uint64_t star
     }
     return n;
 }
+
+/*
+ * Verification of a chunking produced elsewhere (the CUDA path) against the
+ * definition above, one chunk at a time so that callers can split the work
+ * over host threads.  ends[0..n) is a chunking of d[0..L) exactly when
+ * ends[0] = chunk_end(0), ends[j] = chunk_end(ends[j-1]) for every j, and
+ * ends[n-1] = L -- i.e. when it equals what oracle_chunk writes (the chain is
+ * determined by its start, §2.1.2: each boundary depends only on the bytes
+ * after the chunk start).  This checks entries [j0, j1): returns the first j
+ * in that range with ends[j] != chunk_end(j ? ends[j-1] : 0), or j1.
+ */
+uint64_t oracle_check_ends(int algo, const uint8_t *d, uint64_t L, uint64_t w,
+                           uint64_t max_size, const uint64_t *ends,
+                           uint64_t j0, uint64_t j1)
+{
+    for (uint64_t j = j0; j < j1; j++) {
+        uint64_t s = j ? ends[j - 1] : 0;
+        if (s >= L || oracle_chunk_end(algo, d, L, s, w, max_size) != ends[j])
+            return j;
+    }
+    return j1;
+}
+
+/*
+ * The same for files [f0, f1) of a packed batch: file f is
+ * d[offs[f] .. offs[f+1]) and its ends (relative to the file start) are
+ * ends[bo[f] .. bo[f+1]).  A file is correct when its ends pass
+ * oracle_check_ends and the last one equals its length (none for an empty
+ * file).  Returns the first wrong file, or f1; *bad_j receives the index of
+ * the first wrong entry within that file's ends (its count if the entries
+ * are right but the count is not).
+ */
+uint64_t oracle_check_batch(int algo, const uint8_t *d, const uint64_t *offs,
+                            const uint64_t *ends, const uint64_t *bo,
+                            uint64_t f0, uint64_t f1, uint64_t w,
+                            uint64_t max_size, uint64_t *bad_j)
+{
+    for (uint64_t f = f0; f < f1; f++) {
+        uint64_t L = offs[f + 1] - offs[f];
+        uint64_t n = bo[f + 1] - bo[f];
+        const uint64_t *e = ends + bo[f];
+        uint64_t j = oracle_check_ends(algo, d + offs[f], L, w, max_size, e, 0, n);
+        if (j < n) {
+            *bad_j = j;
+            return f;
+        }
+        if ((L == 0) != (n == 0) || (n > 0 && e[n - 1] != L)) {
+            *bad_j = n;
+            return f;
+        }
+    }
+    return f1;
+}

@@ -11,7 +11,8 @@ Recipes (stated again in DESIGN.md §3, "input recipe"):
 * ``zipf_bytes(n, s, seed)``  -- i.i.d. bytes whose *rank* r in 1..256 has
   P(r) ∝ r^-s; ranks are mapped to byte values through a seeded permutation of
   0..255 (text-like skew without favouring any particular byte value).
-  BASELINE configs[1] (s = 1.1, seed 1).
+  Drawn with Walker's alias method (one uniform index and one 32-bit
+  threshold test per byte).  BASELINE configs[1] (s = 1.1, seed 1).
 * ``versioned(base_size, n_snap, seed)`` -- a uniform base with 10% of its
   64 KiB regions zero-filled, plus snapshots each derived from the previous by
   insert/delete/overwrite runs of 1..4 KiB touching ~1% of its bytes
@@ -22,10 +23,17 @@ Recipes (stated again in DESIGN.md §3, "input recipe"):
   low-entropy bytes (runs of one repeated value, run length geometric with mean
   512) (BASELINE configs[4]).
 
+Large outputs are generated in 16 MiB pieces, piece k from its own PCG64
+stream seeded by (seed, k), on a thread pool: the bytes depend only on the
+seed and the size, never on the number of threads.
+
 These stand in for the paper's datasets (Table 2), which are not
 available here; no item of any real dataset is reproduced.
 """
 from __future__ import annotations
+
+import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -37,44 +45,92 @@ __all__ = [
     "many_files",
     "alternating",
     "constant",
+    "saturation_edges",
 ]
 
-_CHUNK = 1 << 24  # generate in 16 MiB pieces to bound temporary memory
+PIECE = 1 << 24  # bytes per independently seeded piece
 
 
 def _rng(seed: int) -> np.random.Generator:
     return np.random.Generator(np.random.PCG64(seed))
 
 
+def _piece_rng(seed: int, k: int, tag: int = 0) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, tag, k])))
+
+
+def _threads() -> int:
+    return max(1, min(32, os.cpu_count() or 1))
+
+
+def _pieces(n: int, fn) -> None:
+    """Run fn(k, lo, hi) over the 16 MiB pieces of [0, n) on a thread pool."""
+    ks = range((n + PIECE - 1) // PIECE)
+    if len(ks) <= 1:
+        for k in ks:
+            fn(k, 0, n)
+        return
+    with ThreadPoolExecutor(_threads()) as ex:
+        list(ex.map(lambda k: fn(k, k * PIECE, min(n, (k + 1) * PIECE)), ks))
+
+
 def uniform(n: int, seed: int) -> np.ndarray:
     """n i.i.d. uniform bytes."""
-    return _rng(seed).integers(0, 256, size=n, dtype=np.uint8)
+    out = np.empty(n, dtype=np.uint8)
+
+    def fill(k, lo, hi):
+        out[lo:hi] = _piece_rng(seed, k, 1).integers(0, 256, size=hi - lo, dtype=np.uint8)
+
+    _pieces(n, fill)
+    return out
 
 
 def constant(n: int, value: int) -> np.ndarray:
     return np.full(n, value, dtype=np.uint8)
 
 
-def _zipf_table(s: float, rng: np.random.Generator):
-    ranks = np.arange(1, 257, dtype=np.float64)
-    p = ranks ** (-s)
-    p /= p.sum()
-    perm = rng.permutation(256).astype(np.uint8)  # rank-1 -> byte value
-    return np.cumsum(p), perm
+class _Zipf:
+    """Alias table of the Zipf(s) rank distribution over 256 values, ranks mapped
+    to byte values through a permutation drawn from `seed`."""
+
+    def __init__(self, s: float, seed: int):
+        ranks = np.arange(1, 257, dtype=np.float64)
+        p = ranks ** (-s)
+        p /= p.sum()
+        self.perm = _rng(seed).permutation(256).astype(np.uint8)  # rank-1 -> byte value
+        # Walker/Vose alias table: column i keeps rank i with probability q[i],
+        # else yields alias[i]
+        q = p * 256.0
+        alias = np.arange(256)
+        small = [i for i in range(256) if q[i] < 1.0]
+        large = [i for i in range(256) if q[i] >= 1.0]
+        while small and large:
+            a, b = small.pop(), large.pop()
+            alias[a] = b
+            q[b] -= 1.0 - q[a]
+            (small if q[b] < 1.0 else large).append(b)
+        for i in small + large:
+            q[i] = 1.0
+        self.thr = np.minimum(np.round(q * 2.0 ** 32), 2.0 ** 32).astype(np.uint64)
+        self.val_keep = self.perm
+        self.val_alias = self.perm[alias]
+
+    def draw(self, rng: np.random.Generator, m: int) -> np.ndarray:
+        col = rng.integers(0, 256, size=m, dtype=np.uint8)
+        u = rng.integers(0, 1 << 32, size=m, dtype=np.uint32)
+        keep = u.astype(np.uint64) < self.thr[col]
+        return np.where(keep, self.val_keep[col], self.val_alias[col])
 
 
-def zipf_bytes(n: int, s: float = 1.1, seed: int = 1, rng: np.random.Generator | None = None) -> np.ndarray:
+def zipf_bytes(n: int, s: float = 1.1, seed: int = 1) -> np.ndarray:
     """n i.i.d. Zipf(s)-ranked bytes (rank -> value through a seeded permutation)."""
-    rng = _rng(seed) if rng is None else rng
-    cdf, perm = _zipf_table(s, rng)
-    cdf[-1] = 1.0
+    z = _Zipf(s, seed)
     out = np.empty(n, dtype=np.uint8)
-    for lo in range(0, n, _CHUNK):
-        hi = min(n, lo + _CHUNK)
-        u = rng.random(hi - lo)
-        idx = np.searchsorted(cdf, u, side="right")
-        np.minimum(idx, 255, out=idx)
-        out[lo:hi] = perm[idx]
+
+    def fill(k, lo, hi):
+        out[lo:hi] = z.draw(_piece_rng(seed, k, 2), hi - lo)
+
+    _pieces(n, fill)
     return out
 
 
@@ -100,7 +156,7 @@ def versioned(base_size: int, n_snap: int, seed: int = 2, region: int = 64 << 10
               run_lo: int = 1024, run_hi: int = 4096) -> list[np.ndarray]:
     """Backup-like versioned data: [base, snap1, ..., snap_n_snap]."""
     rng = _rng(seed)
-    base = rng.integers(0, 256, size=base_size, dtype=np.uint8)
+    base = uniform(base_size, seed)
     n_regions = (base_size + region - 1) // region
     zero = rng.random(n_regions) < zero_frac
     for r in np.nonzero(zero)[0]:
@@ -147,36 +203,41 @@ def many_files(n_files: int, seed: int = 3, median: int = 64 << 10, sigma: float
     """Packed many-file batch: returns (data uint8[total], offsets int64[n_files+1]).
 
     File kinds are drawn per file (uniform with probability uniform_frac, else
-    Zipf-skewed); the bytes of all uniform files come from one uniform draw and
-    those of all Zipf files from one Zipf draw, split in file order."""
+    Zipf-skewed).  The packed bytes are generated piece by piece: inside piece
+    k, each file's part is drawn from piece k's generator with its file's kind."""
     sizes = file_sizes(n_files, seed, median, sigma, cap)
-    rng = _rng(seed + 1000)
+    kinds = _rng(seed + 1000).random(n_files) < uniform_frac  # True: uniform
     offsets = np.zeros(n_files + 1, dtype=np.int64)
     np.cumsum(sizes, out=offsets[1:])
-    kinds = rng.random(n_files) < uniform_frac
-    u = rng.integers(0, 256, size=int(sizes[kinds].sum()), dtype=np.uint8)
-    z = zipf_bytes(int(sizes[~kinds].sum()), zipf_s, rng=rng)
-    ui = np.split(u, np.cumsum(sizes[kinds])[:-1]) if kinds.any() else []
-    zi = np.split(z, np.cumsum(sizes[~kinds])[:-1]) if (~kinds).any() else []
-    pieces, a, b = [], 0, 0
-    for k in kinds.tolist():
-        if k:
-            pieces.append(ui[a])
-            a += 1
-        else:
-            pieces.append(zi[b])
-            b += 1
-    data = np.concatenate(pieces) if pieces else np.zeros(0, dtype=np.uint8)
-    return data, offsets
+    total = int(offsets[-1])
+    z = _Zipf(zipf_s, seed + 2000)
+    out = np.empty(total, dtype=np.uint8)
+
+    def fill(k, lo, hi):
+        rng = _piece_rng(seed, k, 3)
+        f = int(np.searchsorted(offsets, lo, side="right")) - 1
+        x = lo
+        while x < hi:
+            e = min(hi, int(offsets[f + 1]))
+            if e > x:
+                if kinds[f]:
+                    out[x:e] = rng.integers(0, 256, size=e - x, dtype=np.uint8)
+                else:
+                    out[x:e] = z.draw(rng, e - x)
+            x = e
+            f += 1
+
+    _pieces(total, fill)
+    return out, offsets
 
 
 def alternating(n: int, region: int = 256 << 20, seed: int = 5, mean_run: float = 512.0) -> np.ndarray:
     """Alternating regions: uniform random, then runs of repeated values (geometric lengths)."""
-    rng = _rng(seed)
     out = np.empty(n, dtype=np.uint8)
-    k = 0
-    for lo in range(0, n, region):
-        hi = min(n, lo + region)
+
+    def fill_region(k):
+        lo, hi = k * region, min(n, (k + 1) * region)
+        rng = _piece_rng(seed, k, 4)
         if k % 2 == 0:
             out[lo:hi] = rng.integers(0, 256, size=hi - lo, dtype=np.uint8)
         else:
@@ -186,7 +247,9 @@ def alternating(n: int, region: int = 256 << 20, seed: int = 5, mean_run: float 
             while lens.sum() < m:
                 lens = np.concatenate([lens, rng.geometric(1.0 / mean_run, size=n_runs)])
             vals = rng.integers(0, 256, size=lens.size, dtype=np.uint8)
-            seg = np.repeat(vals, lens)[:m]
-            out[lo:hi] = seg
-        k += 1
+            out[lo:hi] = np.repeat(vals, lens)[:m]
+
+    ks = range((n + region - 1) // region)
+    with ThreadPoolExecutor(_threads()) as ex:
+        list(ex.map(fill_region, ks))
     return out

@@ -279,3 +279,91 @@ def test_space_savings_closed_forms():
     y = synth.uniform(1 << 20, 10)
     t2, u2 = dedup.unique_bytes([x, y], [oracle.chunk("ram", x, w, mx), oracle.chunk("ram", y, w, mx)])
     assert t2 == u2
+
+
+# --------------------------------------------------------------------------
+# chain_from at interior (start, stop), against the brute-force predicate
+# --------------------------------------------------------------------------
+def _bf_chain(algo, d, start, stop, w, mx):
+    """Every chunk start of the chain begun at `start`, up to the first >= stop (or len)."""
+    out, s = [start], start
+    while s < stop and s < len(d):
+        s = _bf_chunk_end(algo, d, s, w, mx)
+        out.append(s)
+    return out
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_chain_from_interior_vs_bruteforce(algo):
+    rng = np.random.default_rng(17)
+    for trial in range(60):
+        n = int(rng.integers(1, 300))
+        d = rng.integers(0, int(rng.choice([3, 16, 256])), n).astype(np.uint8)
+        w = int(rng.integers(1, 12))
+        mx = int(w + 1 + rng.integers(0, 30))
+        start = int(rng.integers(0, n + 1))
+        stop = int(rng.integers(start, n + 8))
+        exp = _bf_chain(algo, d.tolist(), start, stop, w, mx)
+        assert oracle.chain_from(algo, d, start, stop, w, mx).tolist() == exp, (n, w, mx, start, stop)
+
+
+# --------------------------------------------------------------------------
+# the verifiers used at full size: check_chunking / check_batch
+# --------------------------------------------------------------------------
+def _mutations(ends, L):
+    """Plausible mistakes of a chunker: a boundary moved by one, a dropped or
+    duplicated boundary, a spurious split, a truncated or extended stream end."""
+    e = [int(x) for x in ends]
+    out = []
+    if len(e) >= 2:
+        i = len(e) // 2
+        out.append(e[:i] + [e[i] + 1] + e[i + 1:])
+        out.append(e[:i] + [e[i] - 1] + e[i + 1:])
+        out.append(e[:i] + e[i + 1:])                           # dropped
+        out.append(e[:i] + [e[i], e[i]] + e[i + 1:])            # duplicated
+        s = e[i - 1] if i else 0
+        out.append(e[:i] + [s + (e[i] - s) // 2] + e[i:])       # spurious split
+        out.append(e[:-1])                                      # truncated
+    out.append(e + [L + 1])                                     # past the end
+    out.append([x + 1 for x in e[:1]] + e[1:])                  # first boundary moved
+    return out
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_check_chunking_accepts_oracle_and_rejects_mutations(algo):
+    for gen, w, mx in (("uniform", 300, 3000), ("zipf", 1000, 8000), ("runs", 64, 600)):
+        L = 300_001
+        d = {"uniform": lambda: synth.uniform(L, 31), "zipf": lambda: synth.zipf_bytes(L, 1.1, 32),
+             "runs": lambda: np.repeat(synth.uniform(L // 50 + 1, 33), 50)[:L]}[gen]()
+        ends = oracle.chunk(algo, d, w, mx)
+        assert oracle.check_chunking(algo, d, ends, w, mx, threads=4) is None
+        for bad in _mutations(ends, L):
+            assert oracle.check_chunking(algo, d, np.array(bad, dtype=np.uint64), w, mx, threads=3) is not None
+    # empty stream, empty output
+    assert oracle.check_chunking(algo, np.zeros(0, np.uint8), np.zeros(0, np.uint64), 4, 16) is None
+    assert oracle.check_chunking(algo, np.zeros(10, np.uint8), np.zeros(0, np.uint64), 4, 16) is not None
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_check_batch_accepts_oracle_and_rejects_mutations(algo):
+    data, offs = synth.many_files(300, seed=41, median=6000, sigma=1.2, cap=60000)
+    sizes = np.diff(offs)
+    sizes[[3, 50, 299]] = 0  # empty files (the byte ranges are re-packed below)
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    data = data[:offs[-1]]
+    w, mx = 500, 4000
+    ends, bo = oracle.chunk_batch(algo, data, offs, w, mx)
+    assert oracle.check_batch(algo, data, offs, ends, bo, w, mx, threads=5) is None
+    for f in (0, 1, 137, 298):
+        a, b = int(bo[f]), int(bo[f + 1])
+        for bad in _mutations(ends[a:b], int(sizes[f])):
+            e2 = np.concatenate([ends[:a], np.array(bad, dtype=np.uint64), ends[b:]])
+            bo2 = bo.copy()
+            bo2[f + 1:] += len(bad) - (b - a)
+            r = oracle.check_batch(algo, data, offs, e2, bo2, w, mx, threads=4)
+            assert r is not None and r[0] == f, (f, r)
+    # a non-monotone bound-offset table is rejected
+    bo3 = bo.copy()
+    bo3[10], bo3[11] = bo3[11], bo3[10]
+    if bo3[10] != bo3[11]:
+        assert oracle.check_batch(algo, data, offs, ends, bo3, w, mx) is not None
