@@ -52,7 +52,7 @@ extern "C" {
 
 typedef enum {
     CDC_OK = 0,
-    CDC_ERR_INVALID = -1,     /* bad argument (null pointer, w == 0, max_size <= w, ...) */
+    CDC_ERR_INVALID = -1,     /* bad argument (null pointer, w == 0 or >= 2^31, max_size <= w, ...) */
     CDC_ERR_CUDA = -2,        /* a CUDA runtime call failed (message has the CUDA error) */
     CDC_ERR_WORKSPACE = -3,   /* workspace smaller than cdc_workspace_size() */
     CDC_ERR_CAPACITY = -4,    /* host entry point: output capacity too small */
@@ -68,7 +68,7 @@ typedef enum { CDC_GT = 0, CDC_GEQ = 1, CDC_LT = 2, CDC_LEQ = 3, CDC_EQ = 4 } cd
 
 typedef struct {
     int32_t  algo;        /* cdc_algo */
-    uint32_t window;      /* w >= 1: the fixed-size window of §2.1.2 */
+    uint32_t window;      /* 1 <= w < 2^31: the fixed-size window of §2.1.2 */
     uint64_t max_size;    /* chunk length cap, > window */
     uint64_t seg_bytes;   /* speculation segment size S (0 = automatic); multiple of 16 */
     uint64_t halo_bytes;  /* max speculative halo walk past a segment end (0 = automatic) */
@@ -148,6 +148,32 @@ int cdc_chunk_batch(const cdc_params *p, const uint8_t *d_data,
  */
 int cdc_chunk_host(const cdc_params *p, const uint8_t *h_data, uint64_t len,
                    uint64_t *h_bounds, uint64_t bounds_cap, uint64_t *h_count);
+
+/*
+ * End-to-end batch entry point with HOST buffers (BASELINE configs[3] end to
+ * end): stream f is h_data[h_file_offsets[f] - h_file_offsets[0] ..
+ * h_file_offsets[f+1] - h_file_offsets[0]), h_file_offsets a host
+ * uint64[nfiles+1], non-decreasing.  The files are cut into up to 8 groups of
+ * whole files (about 1 GiB each); group k's host-to-device copy runs on a copy
+ * stream while group k-1 is chunked (cdc_chunk_batch per group), then the
+ * boundaries come back.  Output as cdc_chunk_batch's, on the host:
+ * h_bounds (uint64[bounds_cap]) gets every file's exclusive end offsets
+ * relative to its own start, h_bound_offsets (uint64[nfiles+1]) the per-file
+ * ranges, *h_count the total.  Synchronous; pinned h_data copies at full PCIe
+ * speed.  Device memory is managed by the library (cached per device and
+ * calling thread).  Returns CDC_ERR_CAPACITY (with *h_count and
+ * h_bound_offsets set) when bounds_cap is too small.
+ */
+int cdc_chunk_batch_host(const cdc_params *p, const uint8_t *h_data, const uint64_t *h_file_offsets,
+                         uint64_t nfiles, uint64_t *h_bounds, uint64_t bounds_cap, uint64_t *h_bound_offsets,
+                         uint64_t *h_count);
+
+/*
+ * Host-only: the first byte of every speculation segment of a single stream of
+ * `len` bytes with these parameters (the plan cdc_chunk uses):
+ * writes min(n, starts_cap) starts to starts[] and n to *n_out.
+ */
+int cdc_plan_segments(const cdc_params *p, uint64_t len, uint64_t *starts, uint64_t starts_cap, uint64_t *n_out);
 
 /*
  * Speculative chain from an arbitrary start (range sharding across GPUs,

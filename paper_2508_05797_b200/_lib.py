@@ -44,6 +44,8 @@ SIGNATURES = {
     "cdc_chunk": ([_P, _vp, _u64, _vp, _u64, _vp, _vp, _sz, _vp], ctypes.c_int),
     "cdc_chunk_batch": ([_P, _vp, _vp, _u64, _u64, _u64, _vp, _u64, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
     "cdc_chunk_host": ([_P, _vp, _u64, _vp, _u64, ctypes.POINTER(_u64)], ctypes.c_int),
+    "cdc_chunk_batch_host": ([_P, _vp, _vp, _u64, _vp, _u64, _vp, ctypes.POINTER(_u64)], ctypes.c_int),
+    "cdc_plan_segments": ([_P, _u64, _vp, _u64, ctypes.POINTER(_u64)], ctypes.c_int),
     "cdc_chain": ([_P, _vp, _u64, _u64, _u64, _vp, _u64, _vp, _vp], ctypes.c_int),
     "cdc_first_common": ([_vp, _u64, _vp, _u64, _vp, _vp], ctypes.c_int),
     "cdc_extreme_byte_search": ([_vp, _vp, _vp, _u64, _i32, _vp, _vp, _vp], ctypes.c_int),

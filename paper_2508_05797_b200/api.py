@@ -5,6 +5,7 @@ device memory (CUDA tensors) and the stream.  Names follow include/cdc_b200.h.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 import numpy as np
@@ -21,6 +22,7 @@ __all__ = [
     "chunk_async", "chunk", "chunk_batch", "chunk_batch_async", "chunk_host", "chain",
     "extreme_byte_search", "range_scan", "first_common", "last_launch_count", "abi_version",
     "profile_enable", "profile_collect", "KERNELS", "stats", "plan_info", "segment_starts",
+    "chunk_batch_host",
 ]
 
 
@@ -58,13 +60,12 @@ def plan_info(p: cdc_params, nfiles: int, total_len: int, max_len: int) -> dict:
 
 
 def segment_starts(p: cdc_params, length: int) -> list:
-    """First byte of every speculation segment of a single stream (cdc_plan_info's rule)."""
-    n = plan_info(p, 1, length, length)["segments"]
-    if n == 0:
-        return []
-    q = length // n
-    mask = ~4095 if q >= (64 << 10) else ~15
-    return [(k * q) & mask for k in range(n)]
+    """First byte of every speculation segment of a single stream (cdc_plan_segments)."""
+    n = ctypes.c_uint64()
+    check(lib.cdc_plan_segments(ctypes.byref(p), length, None, 0, ctypes.byref(n)))
+    out = np.zeros(max(n.value, 1), dtype=np.uint64)
+    check(lib.cdc_plan_segments(ctypes.byref(p), length, out.ctypes.data, out.size, ctypes.byref(n)))
+    return out[:n.value].astype(np.int64).tolist()
 
 
 def abi_version() -> int:
@@ -112,6 +113,36 @@ def _stream_ptr(stream) -> int:
     return s.cuda_stream
 
 
+class _Ctx:
+    def __init__(self, caller):
+        self.caller = caller
+        self.out = []
+
+    def hand_over(self, *tensors):
+        """Tensors returned to the caller: the caller's stream may use (and free) them."""
+        self.out.extend(tensors)
+        return tensors[0] if len(tensors) == 1 else tensors
+
+
+@contextlib.contextmanager
+def _on(stream):
+    """Run a wrapper's whole body (allocations, fills, launches, the final count
+    read) on `stream`, after the work already queued on the caller's current
+    stream; afterwards the caller's stream waits for `stream`, and the tensors
+    handed over are recorded as used by the caller's stream."""
+    if stream is None:
+        yield _Ctx(None)
+        return
+    caller = torch.cuda.current_stream()
+    stream.wait_stream(caller)
+    ctx = _Ctx(caller)
+    with torch.cuda.stream(stream):
+        yield ctx
+    caller.wait_stream(stream)
+    for t in ctx.out:
+        t.record_stream(caller)
+
+
 def _dev_u8(data: torch.Tensor) -> torch.Tensor:
     if not (isinstance(data, torch.Tensor) and data.is_cuda and data.dtype == torch.uint8):
         raise TypeError("data must be a CUDA uint8 tensor")
@@ -135,11 +166,13 @@ def chunk(data: torch.Tensor, p: cdc_params, stream=None) -> torch.Tensor:
     data = _dev_u8(data)
     n = data.numel()
     cap = max_boundaries(p, n)
-    bounds = torch.empty(max(cap, 1), dtype=torch.int64, device=data.device)
-    count = torch.zeros(1, dtype=torch.int64, device=data.device)
-    ws = _workspace(workspace_size(p, 1, n, n), data.device)
-    chunk_async(data, p, bounds, count, ws, stream)
-    m = int(count.item())
+    with _on(stream) as c:
+        bounds = torch.empty(max(cap, 1), dtype=torch.int64, device=data.device)
+        count = torch.zeros(1, dtype=torch.int64, device=data.device)
+        ws = _workspace(workspace_size(p, 1, n, n), data.device)
+        chunk_async(data, p, bounds, count, ws)
+        m = int(count.item())
+        c.hand_over(bounds)
     if m > cap:
         raise CdcError(f"boundary count {m} exceeds capacity {cap}")
     return bounds[:m]
@@ -158,21 +191,23 @@ def chunk_batch_async(data: torch.Tensor, file_offsets: torch.Tensor, total_len:
 def chunk_batch(data: torch.Tensor, file_offsets, p: cdc_params, stream=None):
     """Per-file boundaries of a packed batch: (bounds int64[total], bound_offsets int64[nfiles+1])."""
     data = _dev_u8(data)
-    offs = torch.as_tensor(np.asarray(file_offsets, dtype=np.int64)).to(data.device)
-    nfiles = offs.numel() - 1
-    sizes = (offs[1:] - offs[:-1]).cpu()
+    offs_h = np.asarray(file_offsets, dtype=np.int64)
+    nfiles = offs_h.size - 1
+    sizes = np.diff(offs_h)
     total = int(sizes.sum()) if nfiles else 0
     max_len = int(sizes.max()) if nfiles else 0
-    cap = int(sum(max_boundaries(p, int(s)) for s in sizes.tolist())) if nfiles < 4096 else \
-        total // (p.window + 1) + nfiles
-    bounds = torch.empty(max(cap, 1), dtype=torch.int64, device=data.device)
-    bo = torch.zeros(nfiles + 1, dtype=torch.int64, device=data.device)
-    count = torch.zeros(1, dtype=torch.int64, device=data.device)
-    ws = _workspace(workspace_size(p, nfiles, total, max_len), data.device)
-    check(lib.cdc_chunk_batch(ctypes.byref(p), data.data_ptr(), offs.data_ptr(), nfiles, total, max_len,
-                              bounds.data_ptr(), cap, bo.data_ptr(), count.data_ptr(), ws.data_ptr(), ws.numel(),
-                              _stream_ptr(stream)))
-    m = int(count.item())
+    cap = total // (p.window + 1) + nfiles  # every chunk but a file's last holds > w bytes
+    with _on(stream) as c:
+        offs = torch.from_numpy(offs_h.copy()).to(data.device)
+        bounds = torch.empty(max(cap, 1), dtype=torch.int64, device=data.device)
+        bo = torch.zeros(nfiles + 1, dtype=torch.int64, device=data.device)
+        count = torch.zeros(1, dtype=torch.int64, device=data.device)
+        ws = _workspace(workspace_size(p, nfiles, total, max_len), data.device)
+        check(lib.cdc_chunk_batch(ctypes.byref(p), data.data_ptr(), offs.data_ptr(), nfiles, total, max_len,
+                                  bounds.data_ptr(), cap, bo.data_ptr(), count.data_ptr(), ws.data_ptr(), ws.numel(),
+                                  _stream_ptr(None)))
+        m = int(count.item())
+        c.hand_over(bounds, bo)
     if m > cap:
         raise CdcError(f"boundary count {m} exceeds capacity {cap}")
     return bounds[:m], bo
@@ -190,17 +225,38 @@ def chunk_host(data: np.ndarray, p: cdc_params, out: np.ndarray | None = None) -
     return out[:n.value]
 
 
+def chunk_batch_host(data: np.ndarray, file_offsets, p: cdc_params, out: np.ndarray | None = None):
+    """cdc_chunk_batch_host: packed host bytes + host file offsets in, host per-file boundaries out
+    (copies inside the call, pipelined by file groups).  Returns (bounds uint64[total], bound_offsets
+    uint64[nfiles+1])."""
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    offs = np.ascontiguousarray(file_offsets, dtype=np.uint64)
+    nfiles = offs.size - 1
+    if nfiles < 1:
+        raise CdcError("need at least one file")
+    cap = int(offs[-1] - offs[0]) // (p.window + 1) + nfiles
+    if out is None or out.size < cap:
+        out = np.empty(max(cap, 1), dtype=np.uint64)
+    bo = np.zeros(nfiles + 1, dtype=np.uint64)
+    n = ctypes.c_uint64()
+    check(lib.cdc_chunk_batch_host(ctypes.byref(p), data.ctypes.data, offs.ctypes.data, nfiles, out.ctypes.data,
+                                   out.size, bo.ctypes.data, ctypes.byref(n)))
+    return out[:n.value], bo
+
+
 def chain(data: torch.Tensor, p: cdc_params, start: int, stop: int, cap: int | None = None,
           stream=None) -> torch.Tensor:
     """Chunk starts of the chain begun at `start`, up to the first start >= stop."""
     data = _dev_u8(data)
     if cap is None:
         cap = max_boundaries(p, max(0, min(stop, data.numel()) - start)) + 2
-    out = torch.empty(cap, dtype=torch.int64, device=data.device)
-    cnt = torch.zeros(1, dtype=torch.int64, device=data.device)
-    check(lib.cdc_chain(ctypes.byref(p), data.data_ptr(), data.numel(), start, stop, out.data_ptr(), cap,
-                        cnt.data_ptr(), _stream_ptr(stream)))
-    m = int(cnt.item())
+    with _on(stream) as c:
+        out = torch.empty(cap, dtype=torch.int64, device=data.device)
+        cnt = torch.zeros(1, dtype=torch.int64, device=data.device)
+        check(lib.cdc_chain(ctypes.byref(p), data.data_ptr(), data.numel(), start, stop, out.data_ptr(), cap,
+                            cnt.data_ptr(), _stream_ptr(None)))
+        m = int(cnt.item())
+        c.hand_over(out)
     if m > cap:
         raise CdcError(f"chain length {m} exceeds capacity {cap}")
     return out[:m]
@@ -211,9 +267,11 @@ def first_common(a: torch.Tensor, b: torch.Tensor, stream=None) -> torch.Tensor:
     if not (a.is_cuda and b.is_cuda and a.dtype == torch.int64 and b.dtype == torch.int64):
         raise TypeError("a and b must be CUDA int64 tensors")
     a, b = a.contiguous(), b.contiguous()
-    out = torch.empty(2, dtype=torch.int64, device=a.device)
-    check(lib.cdc_first_common(a.data_ptr(), a.numel(), b.data_ptr(), b.numel(), out.data_ptr(), _stream_ptr(stream)))
-    return out
+    with _on(stream) as c:
+        out = torch.empty(2, dtype=torch.int64, device=a.device)
+        check(lib.cdc_first_common(a.data_ptr(), a.numel(), b.data_ptr(), b.numel(), out.data_ptr(),
+                                   _stream_ptr(None)))
+        return c.hand_over(out)
 
 
 def _regions(offsets, lengths, device):
@@ -225,24 +283,26 @@ def _regions(offsets, lengths, device):
 def extreme_byte_search(data: torch.Tensor, offsets, lengths, mode: str = "max", stream=None):
     """§4.1 on many regions: (values uint8[n], leftmost positions int64[n])."""
     data = _dev_u8(data)
-    off, ln = _regions(offsets, lengths, data.device)
-    n = off.numel()
-    if n and int(ln.min()) < 1:
+    if np.size(lengths) and int(np.min(lengths)) < 1:
         raise CdcError("empty region")
-    val = torch.empty(n, dtype=torch.uint8, device=data.device)
-    pos = torch.empty(n, dtype=torch.int64, device=data.device)
-    check(lib.cdc_extreme_byte_search(data.data_ptr(), off.data_ptr(), ln.data_ptr(), n, MODES[mode],
-                                      val.data_ptr(), pos.data_ptr(), _stream_ptr(stream)))
-    return val, pos
+    with _on(stream) as c:
+        off, ln = _regions(offsets, lengths, data.device)
+        n = off.numel()
+        val = torch.empty(n, dtype=torch.uint8, device=data.device)
+        pos = torch.empty(n, dtype=torch.int64, device=data.device)
+        check(lib.cdc_extreme_byte_search(data.data_ptr(), off.data_ptr(), ln.data_ptr(), n, MODES[mode],
+                                          val.data_ptr(), pos.data_ptr(), _stream_ptr(None)))
+        return c.hand_over(val, pos)
 
 
 def range_scan(data: torch.Tensor, offsets, lengths, targets, cmp: str, stream=None) -> torch.Tensor:
     """§4.2 on many regions: first matching offset per region (region length if none)."""
     data = _dev_u8(data)
-    off, ln = _regions(offsets, lengths, data.device)
-    tg = torch.as_tensor(np.asarray(targets, dtype=np.uint8)).to(data.device)
-    n = off.numel()
-    pos = torch.empty(n, dtype=torch.int64, device=data.device)
-    check(lib.cdc_range_scan(data.data_ptr(), off.data_ptr(), ln.data_ptr(), tg.data_ptr(), n, CMPS[cmp],
-                             pos.data_ptr(), _stream_ptr(stream)))
-    return pos
+    with _on(stream) as c:
+        off, ln = _regions(offsets, lengths, data.device)
+        tg = torch.as_tensor(np.asarray(targets, dtype=np.uint8)).to(data.device)
+        n = off.numel()
+        pos = torch.empty(n, dtype=torch.int64, device=data.device)
+        check(lib.cdc_range_scan(data.data_ptr(), off.data_ptr(), ln.data_ptr(), tg.data_ptr(), n, CMPS[cmp],
+                                 pos.data_ptr(), _stream_ptr(None)))
+        return c.hand_over(pos)

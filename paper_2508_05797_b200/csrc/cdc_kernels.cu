@@ -122,10 +122,10 @@ __device__ __forceinline__ void file_bounds(const Geometry &G, uint64_t f, uint6
 // to 4 KiB (16 B for short files), the last one ending at len: lengths differ
 // by less than one alignment unit plus n bytes (none is tiny, none twice as
 // long) and every start is aligned for the TMA ring.
-__device__ __forceinline__ uint64_t nseg_of(uint64_t len, uint64_t S) {
+__host__ __device__ __forceinline__ uint64_t nseg_of(uint64_t len, uint64_t S) {
     return len == 0 ? 0 : (len < S ? 1 : len / S);
 }
-__device__ __forceinline__ int64_t seg_start(uint64_t k, uint64_t n, uint64_t len) {
+__host__ __device__ __forceinline__ int64_t seg_start(uint64_t k, uint64_t n, uint64_t len) {
     const uint64_t q = len / n;
     const uint64_t align = q >= (64u << 10) ? 4095u : 15u;
     return k >= n ? (int64_t)len : (int64_t)((k * q) & ~align);
@@ -1389,6 +1389,8 @@ int check_params(const cdc_params *p) {
     if (!p) return fail(CDC_ERR_INVALID, "null params");
     if (p->algo < CDC_RAM || p->algo > CDC_AE_MIN) return fail(CDC_ERR_INVALID, "unknown algorithm");
     if (p->window < 1) return fail(CDC_ERR_INVALID, "window must be >= 1");
+    // device code keeps w + 1 in 32-bit signed arithmetic
+    if (p->window >= (1u << 31)) return fail(CDC_ERR_INVALID, "window must be < 2^31");
     if (p->max_size <= p->window) return fail(CDC_ERR_INVALID, "max_size must exceed window");
     if (p->seg_bytes % 16) return fail(CDC_ERR_INVALID, "seg_bytes must be a multiple of 16");
     if (p->seg_bytes && p->seg_bytes >= (1ull << 31)) return fail(CDC_ERR_INVALID, "seg_bytes too large");
@@ -1396,15 +1398,25 @@ int check_params(const cdc_params *p) {
     return CDC_OK;
 }
 
-int g_num_sms = 0;
+// Per-device host state: the SM count and whether the kernels' dynamic shared
+// memory opt-in (a per-device function attribute) has been set on the device.
+constexpr int MAX_DEVICES = 64;
+#define CDC_HOST_GROUPS_MAX 8
+constexpr uint64_t CDC_HOST_GROUP_BYTES = 1ull << 30;  // cdc_chunk_batch_host: pipeline group size
+int g_num_sms[MAX_DEVICES] = {0};
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return (dev >= 0 && dev < MAX_DEVICES) ? dev : 0;
+}
 int num_sms() {
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
+    const int dev = current_device();
+    if (!g_num_sms[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        g_num_sms[dev] = n > 0 ? n : 148;
     }
-    return g_num_sms;
+    return g_num_sms[dev];
 }
 
 struct Plan {
@@ -1438,17 +1450,21 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     // (batches of many small files keep 64 windows: their segments are mostly whole
     // files, and the fix-up walkers continue any halo that gives up)
     const uint64_t hw = nfiles > 1 ? 64ull : 1024ull;
+    const uint64_t w1 = (uint64_t)p->window + 1;
     uint64_t H = p->halo_bytes ? p->halo_bytes
-                               : std::min<uint64_t>(std::max<uint64_t>(2 * S, hw * (p->window + 1)), 64ull << 20);
+                               : std::min<uint64_t>(std::max<uint64_t>(2 * S, hw * w1), 64ull << 20);
     if (H >= (1ull << 31)) H = (1ull << 31) - 1;
     P.S = S;
     P.Hmax = H;
     P.nfiles = nfiles;
     P.max_segs = (nfiles <= 1) ? (max_len + S - 1) / S + 1 : total_len / S + nfiles + 1;
-    P.cap_list = 2 * S / (p->window + 1) + 2;  // the last segment of a file holds up to 2S bytes
-    P.cap_halo = H / (p->window + 1) + 3;
+    // a segment holds less than 2S + 4096 + n bytes (n = segments of its file,
+    // at most max_len / S): seg_start rounds starts down to 4 KiB, and
+    // floor(len / n) < 2S.  Every chunk but a file's last is longer than w.
+    P.cap_list = (2 * S + 4096 + max_len / S + 1) / w1 + 2;
+    P.cap_halo = H / w1 + 3;
     P.pool_cap = P.max_segs * P.cap_halo;  // one slice of cap_halo entries per segment
-    P.poolb_cap = total_len / (p->window + 1) + 2;
+    P.poolb_cap = total_len / w1 + 2;
     P.exc_cap = P.max_segs;
     const uint64_t G = P.max_segs;
     size_t sz[] = {
@@ -1553,16 +1569,17 @@ template <int ALGO>
 int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::Work &W, uint64_t *d_bounds,
                     uint64_t cap, uint64_t *d_count, uint64_t *file_out, cudaStream_t st, bool batch,
                     uint64_t total_len) {
-    static bool attr_set = false;
+    static bool attr_set[MAX_DEVICES] = {false};  // per device: the opt-in is a per-context attribute
     const int spec_smem = cdc::SPEC_WARPS * cdc::RING_SMEM + 128;
-    if (!attr_set) {
+    const int dev = current_device();
+    if (!attr_set[dev]) {
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_fixup<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       cdc::FIX_SMEM));
-        attr_set = true;
+        attr_set[dev] = true;
     }
     int launches = 0;
     ProfCall pc{};
@@ -1671,19 +1688,39 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     }
 }
 
-// cached device buffers for cdc_chunk_host
+// cached device buffers for cdc_chunk_host / cdc_chunk_batch_host, one set per
+// device and calling thread (kept until the thread exits)
 struct HostCache {
-    int dev = -1;
     uint8_t *data = nullptr;
     size_t data_cap = 0;
     uint64_t *bounds = nullptr;
     size_t bounds_cap = 0;
     void *ws = nullptr;
     size_t ws_cap = 0;
-    uint64_t *count = nullptr;
-    cudaStream_t st = nullptr;
+    uint64_t *count = nullptr;      // [0] count, then per-group counts (batch)
+    uint64_t *offs = nullptr;       // batch: rebased file offsets of every group
+    size_t offs_cap = 0;
+    uint64_t *bo = nullptr;         // batch: per-group bound offsets
+    size_t bo_cap = 0;
+    cudaStream_t st = nullptr;      // compute
+    cudaStream_t cp = nullptr;      // host-to-device copies (batch pipeline)
+    cudaEvent_t ev[CDC_HOST_GROUPS_MAX];
+    bool init = false;
 };
-thread_local HostCache g_hc;
+thread_local HostCache g_hc[MAX_DEVICES];
+
+int host_cache(HostCache *&C) {
+    const int dev = current_device();
+    C = &g_hc[dev];
+    if (!C->init) {
+        CDC_CUDA(cudaStreamCreateWithFlags(&C->st, cudaStreamNonBlocking));
+        CDC_CUDA(cudaStreamCreateWithFlags(&C->cp, cudaStreamNonBlocking));
+        for (int i = 0; i < CDC_HOST_GROUPS_MAX; ++i) CDC_CUDA(cudaEventCreateWithFlags(&C->ev[i], cudaEventDisableTiming));
+        CDC_CUDA(cudaMalloc(&C->count, 8 * (CDC_HOST_GROUPS_MAX + 1)));
+        C->init = true;
+    }
+    return CDC_OK;
+}
 
 int ensure(void **p, size_t &cap, size_t need) {
     if (cap >= need && *p) return CDC_OK;
@@ -1891,21 +1928,15 @@ int cdc_chunk_host(const cdc_params *p, const uint8_t *h_data, uint64_t len, uin
     int rc = check_params(p);
     if (rc) return rc;
     if ((!h_data && len) || !h_count || (!h_bounds && bounds_cap)) return fail(CDC_ERR_INVALID, "null pointer");
-    HostCache &C = g_hc;
-    int dev = 0;
-    CDC_CUDA(cudaGetDevice(&dev));
-    if (C.dev != dev) {
-        C = HostCache();
-        C.dev = dev;
-        CDC_CUDA(cudaStreamCreateWithFlags(&C.st, cudaStreamNonBlocking));
-    }
+    HostCache *Cp = nullptr;
+    if ((rc = host_cache(Cp))) return rc;
+    HostCache &C = *Cp;
     size_t wsb = 0;
     if ((rc = cdc_workspace_size(p, 1, len, len, &wsb))) return rc;
     const uint64_t maxb = cdc_max_boundaries(p, len);
     if ((rc = ensure((void **)&C.data, C.data_cap, len + 32))) return rc;
     if ((rc = ensure((void **)&C.bounds, C.bounds_cap, maxb * 8))) return rc;
     if ((rc = ensure(&C.ws, C.ws_cap, wsb))) return rc;
-    if (!C.count) CDC_CUDA(cudaMalloc(&C.count, 8));
     CDC_CUDA(cudaMemcpyAsync(C.data, h_data, len, cudaMemcpyHostToDevice, C.st));
     if ((rc = cdc_chunk(p, C.data, len, C.bounds, maxb, C.count, C.ws, C.ws_cap, C.st))) return rc;
     uint64_t n = 0;
@@ -1921,6 +1952,120 @@ int cdc_chunk_host(const cdc_params *p, const uint8_t *h_data, uint64_t len, uin
     return CDC_OK;
 }
 
+int cdc_plan_segments(const cdc_params *p, uint64_t len, uint64_t *starts, uint64_t starts_cap, uint64_t *n_out) {
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!n_out || (!starts && starts_cap)) return fail(CDC_ERR_INVALID, "null pointer");
+    Plan P;
+    make_plan(p, 1, len, len, P);
+    const uint64_t n = cdc::nseg_of(len, P.S);
+    *n_out = n;
+    for (uint64_t k = 0; k < n && k < starts_cap; ++k) starts[k] = (uint64_t)cdc::seg_start(k, n, len);
+    return CDC_OK;
+}
+
+int cdc_chunk_batch_host(const cdc_params *p, const uint8_t *h_data, const uint64_t *h_file_offsets,
+                         uint64_t nfiles, uint64_t *h_bounds, uint64_t bounds_cap, uint64_t *h_bound_offsets,
+                         uint64_t *h_count) {
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!h_file_offsets || !h_bound_offsets || !h_count || (!h_bounds && bounds_cap))
+        return fail(CDC_ERR_INVALID, "null pointer");
+    if (nfiles == 0) return fail(CDC_ERR_INVALID, "nfiles must be >= 1");
+    const uint64_t total = h_file_offsets[nfiles] - h_file_offsets[0];
+    if (total && !h_data) return fail(CDC_ERR_INVALID, "null data");
+    for (uint64_t f = 0; f < nfiles; ++f)
+        if (h_file_offsets[f + 1] < h_file_offsets[f]) return fail(CDC_ERR_INVALID, "file offsets decrease");
+    HostCache *Cp = nullptr;
+    if ((rc = host_cache(Cp))) return rc;
+    HostCache &C = *Cp;
+    // groups of whole files of about total / ngroups bytes each: group k's copy
+    // overlaps group k-1's chunking
+    const uint64_t ngroups_want = std::min<uint64_t>(
+        std::max<uint64_t>(total / CDC_HOST_GROUP_BYTES, 1), CDC_HOST_GROUPS_MAX);
+    std::vector<uint64_t> gf{0};  // first file of each group
+    for (uint64_t k = 1; k < ngroups_want; ++k) {
+        const uint64_t target = h_file_offsets[0] + total / ngroups_want * k;
+        uint64_t lo = gf.back(), hi = nfiles;  // first file starting at or after target
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (h_file_offsets[mid] < target) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo > gf.back() && lo < nfiles) gf.push_back(lo);
+    }
+    gf.push_back(nfiles);
+    const size_t ng = gf.size() - 1;
+    // per-group plan: workspace, bound capacity (every chunk but a file's last holds > w bytes)
+    const uint64_t w1 = (uint64_t)p->window + 1;
+    std::vector<uint64_t> gb(ng + 1, 0), gmax(ng, 0), gcap(ng + 1, 0);
+    size_t ws_max = 0;
+    for (size_t k = 0; k < ng; ++k) {
+        uint64_t mx = 0, cap = 0;
+        for (uint64_t f = gf[k]; f < gf[k + 1]; ++f) {
+            const uint64_t L = h_file_offsets[f + 1] - h_file_offsets[f];
+            mx = std::max(mx, L);
+            cap += L / w1 + 1;
+        }
+        gb[k + 1] = h_file_offsets[gf[k + 1]] - h_file_offsets[0];
+        gmax[k] = mx;
+        gcap[k + 1] = gcap[k] + cap;
+        size_t wsb = 0;
+        if ((rc = cdc_workspace_size(p, gf[k + 1] - gf[k], gb[k + 1] - gb[k], mx, &wsb))) return rc;
+        ws_max = std::max(ws_max, round_up(wsb, 256));
+    }
+    if ((rc = ensure((void **)&C.data, C.data_cap, total + 32))) return rc;
+    if ((rc = ensure((void **)&C.bounds, C.bounds_cap, std::max<uint64_t>(gcap[ng], 1) * 8))) return rc;
+    if ((rc = ensure(&C.ws, C.ws_cap, ws_max))) return rc;
+    if ((rc = ensure((void **)&C.offs, C.offs_cap, (nfiles + ng) * 8))) return rc;
+    if ((rc = ensure((void **)&C.bo, C.bo_cap, (nfiles + ng) * 8))) return rc;
+    // rebased offsets of every group (host staging, then one copy)
+    std::vector<uint64_t> ro(nfiles + ng);
+    for (size_t k = 0; k < ng; ++k)
+        for (uint64_t f = gf[k]; f <= gf[k + 1]; ++f) ro[f + k] = h_file_offsets[f] - h_file_offsets[gf[k]];
+    CDC_CUDA(cudaMemcpyAsync(C.offs, ro.data(), ro.size() * 8, cudaMemcpyHostToDevice, C.cp));
+    for (size_t k = 0; k < ng; ++k) {
+        const uint64_t nb = gb[k + 1] - gb[k];
+        if (nb)
+            CDC_CUDA(cudaMemcpyAsync(C.data + gb[k], h_data + h_file_offsets[gf[k]], nb, cudaMemcpyHostToDevice,
+                                     C.cp));
+        CDC_CUDA(cudaEventRecord(C.ev[k], C.cp));
+    }
+    int launches = 0;
+    for (size_t k = 0; k < ng; ++k) {
+        CDC_CUDA(cudaStreamWaitEvent(C.st, C.ev[k], 0));
+        const uint64_t nf = gf[k + 1] - gf[k];
+        // one workspace: the groups' pipelines are ordered on the compute stream
+        if ((rc = cdc_chunk_batch(p, C.data + gb[k], C.offs + gf[k] + k, nf, gb[k + 1] - gb[k], gmax[k],
+                                  C.bounds + gcap[k], gcap[k + 1] - gcap[k], C.bo + gf[k] + k, C.count + 1 + k, C.ws,
+                                  C.ws_cap, C.st)))
+            return rc;
+        launches += g_launches;
+    }
+    // per-group bound offsets back to the host, then the boundaries of each group
+    std::vector<uint64_t> hbo(nfiles + ng);
+    CDC_CUDA(cudaMemcpyAsync(hbo.data(), C.bo, hbo.size() * 8, cudaMemcpyDeviceToHost, C.st));
+    CDC_CUDA(cudaStreamSynchronize(C.st));
+    uint64_t n = 0;
+    for (size_t k = 0; k < ng; ++k) {
+        const uint64_t nf = gf[k + 1] - gf[k];
+        const uint64_t *b = hbo.data() + gf[k] + k;
+        const uint64_t m = b[nf];
+        if (m > gcap[k + 1] - gcap[k]) return fail(CDC_ERR_CUDA, "internal: group bound capacity exceeded");
+        for (uint64_t i = 0; i < nf; ++i) h_bound_offsets[gf[k] + i] = n + b[i];
+        const uint64_t room = n < bounds_cap ? bounds_cap - n : 0;
+        const uint64_t mm = m < room ? m : room;
+        if (mm) CDC_CUDA(cudaMemcpyAsync(h_bounds + n, C.bounds + gcap[k], mm * 8, cudaMemcpyDeviceToHost, C.st));
+        n += m;
+    }
+    h_bound_offsets[nfiles] = n;
+    *h_count = n;
+    CDC_CUDA(cudaStreamSynchronize(C.st));
+    g_launches = launches;
+    if (n > bounds_cap) return fail(CDC_ERR_CAPACITY, "bounds_cap too small");
+    return CDC_OK;
+}
+
 int cdc_chain(const cdc_params *p, const uint8_t *d_data, uint64_t len, uint64_t start, uint64_t stop,
               uint64_t *d_starts, uint64_t starts_cap, uint64_t *d_count, void *stream) {
     int rc = check_params(p);
@@ -1928,12 +2073,13 @@ int cdc_chain(const cdc_params *p, const uint8_t *d_data, uint64_t len, uint64_t
     if (!d_count || (!d_starts && starts_cap) || (!d_data && len)) return fail(CDC_ERR_INVALID, "null pointer");
     if (start > len) return fail(CDC_ERR_INVALID, "start beyond len");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[MAX_DEVICES] = {false};
+    const int dev = current_device();
+    if (!attr[dev]) {
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM + 128));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM + 128));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_chain<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::RING_SMEM + 128));
-        attr = true;
+        attr[dev] = true;
     }
     switch (p->algo) {
     case CDC_RAM:

@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -68,3 +69,40 @@ def test_invalid_calls_fail_without_gpu(lib):
     assert lib.lib.cdc_chunk(ctypes.byref(p), None, 0, None, 0, None, None, 0, None) == -1
     assert lib.lib.cdc_chunk_host(ctypes.byref(p), None, 10, None, 0, ctypes.byref(n)) == -1
     assert b"null" in lib.lib.cdc_last_error()
+
+
+def test_plan_segments_host_only(lib):
+    from paper_2508_05797_b200 import api
+    for algo, avg, n in (("ae_max", 4096, 256 << 20), ("ram", 8192, 16 << 20), ("ram", 8192, 1 << 30),
+                         ("ram", 8192, 100_000), ("ae_min", 512, (3 << 20) + 7)):
+        p = api.params(algo, avg_size=avg)
+        st = api.segment_starts(p, n)
+        info = api.plan_info(p, 1, n, n)
+        assert len(st) == info["segments"] >= 1
+        assert st[0] == 0 and all(b > a for a, b in zip(st, st[1:])) and st[-1] < n
+        align = 4096 if n // len(st) >= (64 << 10) else 16
+        assert all(s % align == 0 for s in st)
+        # no segment is tiny or more than twice the segment size plus an alignment unit
+        lens = np.diff(st + [n])
+        assert lens.max() < 2 * info["seg_bytes"] + 4096 + len(st)
+    assert api.segment_starts(api.params("ram", avg_size=8192), 0) == []
+
+
+def test_huge_window_rejected_not_crashing(lib):
+    """window + 1 must not wrap in 32 bits (it used to divide by zero in the planner)."""
+    from paper_2508_05797_b200 import api
+    p = api.params("ram", window=0xFFFFFFFF, max_size=1 << 40)
+    with pytest.raises(api.CdcError):
+        api.workspace_size(p, 1, 1 << 33, 1 << 33)
+    with pytest.raises(api.CdcError):
+        api.plan_info(p, 1, 1 << 33, 1 << 33)
+    p = api.params("ram", window=(1 << 31) - 1, max_size=1 << 40)
+    assert api.workspace_size(p, 1, 1 << 33, 1 << 33) > 0
+
+
+def test_batch_host_rejects_bad_offsets(lib):
+    from paper_2508_05797_b200 import api
+    p = api.params("ram", avg_size=8192)
+    data = np.zeros(100, np.uint8)
+    with pytest.raises(api.CdcError):
+        api.chunk_batch_host(data, np.array([0, 60, 50, 100], np.uint64), p)

@@ -46,7 +46,7 @@ CASES = {
     "ae_min_runs": ("ae_min", lambda n: synth.alternating(n, region=1 << 18, seed=5), 3 << 20, 250, 1000,
                     64 << 10),
     # a halo too short for the chains to meet: exercises the fix-up walk
-    "ram_uniform_fixup": ("ram", lambda n: synth.uniform(n, 6), 2 << 20, 2000, 8000, 16400),
+    "ram_uniform_fixup": ("ram", lambda n: synth.uniform(n, 6), 2 << 20, 2000, 8000, 12000),
 }
 
 
