@@ -1,19 +1,35 @@
 #!/usr/bin/env python
 """bench.py -- chunking throughput of the B200 CDC hot path (driver contract).
 
-One step = one cdc_chunk call over the whole resident stream: speculative
-segment chunking with the fused look-back resolution and boundary write
-(k_speculate), and the fix-up kernel (k_fixup, which exits at once when the
-fused fast path succeeded) -- every row of DESIGN.md §0(a).  Workload at N=1 = BASELINE.json
-configs[1]: AE (AE-Max) at a 4 KiB target average, one 256 MiB stream of
-Zipf(s=1.1) bytes, seed 1.  With N ranks (torchrun) every rank chunks its own
-256 MiB stream (the configs[1] stream, seed 1, on every rank): the work shards with no collective on the data
-path ("scaling": "weak").
+Headline workload (N=1): BASELINE.json configs[3] at full size, the largest
+configuration that fits one GPU -- 100,000 files with lognormal sizes (median
+64 KiB, sigma 1.5, capped at 16 MiB: 18.67 GiB; BASELINE.json's "~8 GiB" is not
+what its stated distribution gives), 70 % uniform / 30 % Zipf(1.1) content,
+RAM at an 8 KiB average.  One step = one cdc_chunk_batch call over all the
+resident files: the batch segment table (k_seg_prefix), the list reset
+(k_reset), the speculative walkers (k_speculate: Extreme Byte Search, Range
+Scan and the RAM rule, DESIGN.md §0 rows a1-a3, a5) and the chain resolver and
+boundary write (k_fixup, row a4).
+
+With N ranks (torchrun) the same 100,000 files are split N ways by
+shard.file_range (contiguous, byte-balanced file ranges; "files shard
+directly", north_star (4)): each rank chunks its share with one
+cdc_chunk_batch call and no data-path collective ("scaling": "strong").
+
+Secondary keys in the same JSON line:
+  configs1        configs[1] (AE-Max 4 KiB, one 256 MiB Zipf stream) on every
+                  rank, with its own roofline (the round-1 headline);
+  configs4_sharded  configs[4]: the 64 GiB alternating stream split by byte
+                  range with a halo over the N ranks (shard.chunk_sharded: NCCL
+                  all_gather of segment-edge chain states), RAM and AE-Max at
+                  8 KiB, timed through the public API;
+  paper_cpu_vector  the paper's own CPU-vector numbers, as context only.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
---impl reference times the CPU oracle (oracle/, plain C, one host core) on the
-same workload, one 32 MiB slice per step; under torchrun only rank 0 runs it.
+--impl reference times the CPU oracle (oracle/, plain C) on the host cores on
+the same configs[3] workload, one ~1 GiB range of files per step; under
+torchrun only rank 0 runs it.
 """
 from __future__ import annotations
 
@@ -24,6 +40,7 @@ import statistics
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -31,19 +48,34 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "chunking GB/s of input (1/2/4/8 B200) and % of HBM roofline; boundaries == oracle"
-ALGO, AVG, STREAM = "ae_max", 4096, 256 << 20
-WORKLOAD = "configs[1]: AE (AE-Max) avg 4 KiB, single 256 MiB stream of Zipf(s=1.1) bytes, seed 1"
-REF_SLICE = 32 << 20
+NFILES, FSEED, C3_ALGO, C3_AVG = 100_000, 3, "ram", 8192
+WORKLOAD = ("configs[3]: 100,000 files, lognormal sizes (median 64 KiB, sigma 1.5, capped at 16 MiB; 18.67 GiB), "
+            "70% uniform / 30% Zipf(1.1) bytes, RAM avg 8 KiB, one cdc_chunk_batch call per rank")
+C1_ALGO, C1_AVG, C1_STREAM = "ae_max", 4096, 256 << 20
+C4_LEN = 64 << 30
+REF_SAMPLE = 1 << 30          # --impl reference: bytes of files per step
+CPU_SAMPLE = 4 << 30          # cpu_baseline: bytes of files in the sample
+
+# PAPER.md's own numbers (single CPU core, its datasets), quoted as context only
+PAPER_CPU = {
+    "note": "PAPER.md single-core numbers on its real datasets and CPUs; context, not a target",
+    "VAE-Max/VAE-Min/VMAXP/VRAM, AVX-512, 8 KB chunks (PAPER.md l.661-665, sec. 6 throughput)": "6.5-29.9 GB/s",
+    "VRAM-EBS (Extreme Byte Search only) on DEB (l.737)": "18.5 GB/s",
+    "RAM, NEON-128, ARM v8 Atlas (l.797)": "2.91 GB/s",
+    "RAM, VSX-128, IBM Power 8 (l.803)": "8.54 GB/s",
+    "unaccelerated AE-Max/AE-Min/MAXP/RAM (l.663)": "1.5-1.7 GB/s",
+    "machines (l.430-437)": "Intel Emerald Rapids Xeon Gold 5512U, Skylake Xeon Silver 4114, AMD EPYC 7302P, "
+                            "ARM v8 Atlas, IBM Power 8 (CloudLab)",
+}
 
 
-def load_traffic():
-    """DRAM traffic per k_speculate launch from the committed ncu --set full capture
-    (profiles/ncu_k_speculate_latest.json), or None."""
+def load_traffic(name):
+    """DRAM traffic per k_speculate launch from a committed ncu --set full capture, or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_k_speculate_latest.json")) as f:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             t = json.load(f)
-        return float(t["traffic_bytes"]) / 1e9, "dram__bytes_read.sum + dram__bytes_write.sum per launch (GB), " \
-            "profiles/ncu_k_speculate_latest.json"
+        return float(t["traffic_bytes"]) / 1e9, f"dram__bytes_read.sum + dram__bytes_write.sum per launch (GB), " \
+            f"profiles/{name}"
     except Exception:
         return None, None
 
@@ -119,92 +151,334 @@ def dist_env():
     return world, rank, local
 
 
+def c3_window():
+    return C3_AVG - 256, 4 * C3_AVG  # cdc_params_default's window / cap (reading R4, R5)
+
+
+def oracle_files(data, offs, files, threads):
+    """The oracle as it stands (oracle.chunk per file), files spread over host threads."""
+    import oracle
+    w, mx = c3_window()
+
+    def one(f):
+        return oracle.chunk(C3_ALGO, data[offs[f]:offs[f + 1]], w, mx).size
+
+    with ThreadPoolExecutor(threads) as ex:
+        return sum(ex.map(one, files, chunksize=64))
+
+
 def run_reference(args, world, rank):
-    """CPU oracle arm: rank 0 only, on the box's host cores."""
+    """CPU oracle arm (rank 0 only): the configs[3] workload on the box's host cores,
+    each step one contiguous ~1 GiB range of files (rotating through the batch)."""
     if rank != 0:
         return 0
-    import oracle
     import synth
-    data = synth.zipf_bytes(STREAM, 1.1, 1)
-    w, mx = AVG - 256, 4 * AVG  # same window / cap as the GPU arm's cdc_params_default
-    nsl = STREAM // REF_SLICE
+    offs = synth.many_files_offsets(NFILES, FSEED)
+    nsteps = args.warmup + args.steps
+    # contiguous file ranges of ~REF_SAMPLE bytes, as many as the run needs
+    starts = [0]
+    while len(starts) <= nsteps and starts[-1] < NFILES:
+        starts.append(int(np.searchsorted(offs, offs[starts[-1]] + REF_SAMPLE)))
+    ranges = [(a, min(b, NFILES)) for a, b in zip(starts, starts[1:]) if b > a]
+    f_lo, f_hi = ranges[0][0], ranges[-1][1]
+    data, loc = synth.many_files(NFILES, FSEED, files=(f_lo, f_hi))
+    threads = os.cpu_count() or 1
+    w, mx = c3_window()
 
     def step(i):
-        sl = data[(i % nsl) * REF_SLICE:((i % nsl) + 1) * REF_SLICE]
-        return oracle.chunk(ALGO, sl, w, mx).size
+        a, b = ranges[i % len(ranges)]
+        oracle_files(data, loc, range(a - f_lo, b - f_lo), threads)
+        return int(offs[b] - offs[a])
 
     for i in range(args.warmup):
         step(i)
+    nbytes = 0
     t0 = time.perf_counter()
     for i in range(args.steps):
-        step(i)
+        nbytes += step(args.warmup + i)
     dt = time.perf_counter() - t0
-    gbs = args.steps * REF_SLICE / dt / 1e9
+    gbs = nbytes / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "algo": ALGO, "avg_size": AVG, "window": w, "max_size": mx,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "algo": C3_ALGO, "avg_size": C3_AVG, "window": w, "max_size": mx,
                    "parallelism": "cpu oracle, rank 0 only"},
-        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"one {REF_SLICE >> 20} MiB slice of the 256 MiB stream per step"},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                         "sample": f"per step one contiguous range of ~{REF_SAMPLE >> 30} GiB of the 100,000 files, "
+                                   f"oracle.chunk per file on {threads} threads"},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline(data_np, w, mx):
-    """The oracle as it stands on one host core over the full 256 MiB stream (one pass)."""
-    import oracle
+def cpu_baseline(data, offs):
+    """The oracle (oracle.chunk per file, as it stands) on all host cores over the first
+    ~4 GiB of files of this rank's share."""
+    threads = os.cpu_count() or 1
+    nf = int(np.searchsorted(offs, CPU_SAMPLE))
+    nf = max(1, min(nf, offs.size - 1))
     t0 = time.perf_counter()
-    oracle.chunk(ALGO, data_np, w, mx)
+    oracle_files(data, offs, range(nf), threads)
     dt = time.perf_counter() - t0
-    return {"value": round(data_np.size / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": "the full 256 MiB configs[1] stream, one pass, C oracle (gcc -O2), 1 thread"}
+    nb = int(offs[nf] - offs[0])
+    return {"value": round(nb / dt / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"the first {nf} files ({nb / 2**30:.2f} GiB) of the configs[3] batch, oracle.chunk per file "
+                      f"(C, gcc -O2) on {threads} threads, one pass ({dt:.1f} s)"}
 
 
-def measure_e2e(cdc, p, data_np, cap, world, dist, dev, steps):
-    """Same metric through cdc_chunk_host: pinned host bytes in, host boundaries out."""
-    import torch
-    pinned = torch.empty(STREAM, dtype=torch.uint8, pin_memory=True)
-    pinned.copy_(torch.from_numpy(data_np))
+def timed(run, steps, stream, dist, dev, torch):
+    """Device time of `steps` steps (CUDA events on the launch stream, barrier +
+    synchronize on both sides), max over ranks, in ms."""
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    return float(ms.item())
+
+
+def make_graph(torch, dev, stream, fn, reps):
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        for _ in range(reps):
+            fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    torch.cuda.synchronize()
+    return g
+
+
+def kernel_profile(cdc, step, steps, torch):
+    """Per-kernel CUDA events on the launch stream over `steps` direct-launch steps."""
+    cdc.profile_enable(True)
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    cdc.profile_enable(False)
+    return cdc.profile_collect()
+
+
+def measure_c3(args, cdc, torch, dist, dev, world, rank, local):
+    import synth
+    from paper_2508_05797_b200 import shard
+    offs_all = synth.many_files_offsets(NFILES, FSEED)
+    f0, f1 = shard.file_range(offs_all, world, rank)
+    data_np, offs = synth.many_files(NFILES, FSEED, files=(f0, f1))
+    nf = f1 - f0
+    total = int(offs[-1])
+    max_len = int(np.diff(offs).max()) if nf else 0
+    p = cdc.params(C3_ALGO, avg_size=C3_AVG)
+    data = torch.from_numpy(data_np).to(dev)
+    od = torch.from_numpy(offs).to(dev)
+    cap = total // (p.window + 1) + nf
+    bounds = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+    bo = torch.zeros(nf + 1, dtype=torch.int64, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(cdc.workspace_size(p, nf, total, max_len), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        cdc.chunk_batch_async(data, od, total, max_len, p, bounds, bo, count, ws, stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    n_bounds = int(count.item())
+    launches = cdc.last_launch_count()
+    checked = None
+    if args.check:
+        import oracle
+        bad = oracle.check_batch(C3_ALGO, data_np, offs, bounds[:n_bounds].cpu().numpy().astype(np.uint64),
+                                 bo.cpu().numpy().astype(np.uint64), p.window, p.max_size)
+        assert bad is None, f"boundary mismatch vs oracle at {bad}"
+        checked = "every chunk of this rank's files == oracle (oracle.check_batch)"
+    stats = cdc.stats(p, ws, nf, total, max_len)
+    graph = None if args.no_graph else make_graph(torch, dev, stream, step, 1)
+
+    def run(k):
+        for _ in range(k):
+            graph.replay() if graph is not None else step()
+
+    with ClockSampler(local) as clk:
+        t_end = time.perf_counter() + 0.3  # load the GPU so clock samples reflect the timed region
+        while time.perf_counter() < t_end:
+            run(1)
+            torch.cuda.synchronize()
+        ms = timed(run, args.steps, stream, dist, dev, torch)
+        prof = kernel_profile(cdc, step, args.steps, torch)
+    assert int(count.item()) == n_bounds, "boundary count changed between steps"
+    # global boundary count: one all_gather of the per-rank counts (shard.chunk_files_sharded's exchange)
+    n_all = n_bounds
+    bytes_all = total
+    if dist is not None:
+        t = torch.tensor([n_bounds, total], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        n_all, bytes_all = int(t[0]), int(t[1])
+    res = {"ms": ms, "bytes_rank": total, "bytes_all": bytes_all, "boundaries": n_all, "files": (f0, f1),
+           "prof": prof, "launches": launches, "stats": stats, "clocks": clk.summary(), "checked": checked,
+           "graph": graph is not None, "p": p}
+    if not args.no_e2e:
+        res["e2e"] = measure_e2e_c3(cdc, torch, p, data_np, offs, dist, dev, world, args.steps)
+    if not args.no_cpu_baseline and world == 1 and rank == 0:
+        res["cpu_baseline"] = cpu_baseline(data_np, offs)
+    del data, ws, bounds
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_e2e_c3(cdc, torch, p, data_np, offs, dist, dev, world, steps):
+    """The same metric through cdc_chunk_batch_host: pinned host bytes in (grouped,
+    pipelined H2D copies inside the call), host boundaries out."""
+    pinned = torch.empty(data_np.size, dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = data_np
     host_in = pinned.numpy()
-    host_out = np.empty(cap, dtype=np.uint64)
-    cdc.chunk_host(host_in, p, host_out)
-    e2e_steps = max(3, min(steps, 20))
+    out = np.empty(int(offs[-1]) // (p.window + 1) + offs.size, dtype=np.uint64)
+    b, bo = cdc.chunk_batch_host(host_in, offs, p, out)
+    n = b.size
+    k = max(3, min(steps, 5))
     if dist is not None:
         dist.barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        nb = cdc.chunk_host(host_in, p, host_out).size
-    e2e_s = time.perf_counter() - t0
-    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    for _ in range(k):
+        b, bo = cdc.chunk_batch_host(host_in, offs, p, out)
+    dt = time.perf_counter() - t0
+    tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+    tb = torch.tensor([float(data_np.size)], dtype=torch.float64, device=dev)
     if dist is not None:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    return {"value": round(STREAM * world * e2e_steps / float(e2e_t.item()) / 1e9, 3), "unit": "GB/s",
-            "h2d_bytes_per_step": STREAM, "d2h_bytes_per_step": 8 + 8 * nb,
-            "timing": "wall clock around the synchronous cdc_chunk_host call (pinned input)"}
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tb)
+    del pinned
+    return {"value": round(float(tb.item()) * k / float(tt.item()) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": int(data_np.size + offs.nbytes), "d2h_bytes_per_step": int(8 * n + bo.nbytes),
+            "timing": f"wall clock around {k} synchronous cdc_chunk_batch_host calls (pinned input), max over ranks"}
+
+
+def measure_c1(args, cdc, torch, dist, dev, world):
+    """configs[1] on every rank (secondary; round 1's headline): 256 MiB Zipf stream,
+    AE-Max 4 KiB; CUDA graph of two steps over two device copies (L2 never warm)."""
+    import synth
+    data_np = synth.zipf_bytes(C1_STREAM, 1.1, 1)
+    bufs = [torch.from_numpy(data_np).to(dev) for _ in range(2)]
+    p = cdc.params(C1_ALGO, avg_size=C1_AVG)
+    cap = cdc.max_boundaries(p, C1_STREAM)
+    bounds = torch.empty(cap, dtype=torch.int64, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(cdc.workspace_size(p, 1, C1_STREAM, C1_STREAM), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    it = [0]
+
+    def step():
+        cdc.chunk_async(bufs[it[0] & 1], p, bounds, count, ws, stream)
+        it[0] += 1
+
+    for _ in range(4):
+        step()
+    torch.cuda.synchronize()
+    n_bounds = int(count.item())
+    if args.check:
+        import oracle
+        bad = oracle.check_chunking(C1_ALGO, data_np, bounds[:n_bounds].cpu().numpy().astype(np.uint64),
+                                    p.window, p.max_size)
+        assert bad is None, f"configs[1] mismatch vs oracle at {bad}"
+    graph = make_graph(torch, dev, stream, step, 2)
+
+    def run(k):
+        for _ in range(k // 2):
+            graph.replay()
+        if k % 2:
+            step()
+
+    steps = max(args.steps, 20)
+    ms = timed(run, steps, stream, dist, dev, torch)
+    prof = kernel_profile(cdc, step, steps, torch)
+    peak, peak_src = load_peaks()
+    spec_ms = prof["k_speculate"][0] / max(1, prof["k_speculate"][1])
+    traffic, traffic_src = load_traffic("ncu_k_speculate_c1.json")
+    out = {
+        "workload": "configs[1]: AE-Max avg 4 KiB, single 256 MiB stream of Zipf(s=1.1) bytes, seed 1, on every rank",
+        "value": round(C1_STREAM * world * steps / (ms / 1e3) / 1e9, 2), "unit": "GB/s",
+        "ms_per_step": round(ms / steps, 4), "steps": steps, "boundaries": n_bounds, "scaling": "weak",
+        "roofline": {"bound": "hbm", "kernel": "k_speculate",
+                     "achieved": round(C1_STREAM / (spec_ms / 1e3) / 1e9, 1), "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(C1_STREAM / (spec_ms / 1e3) / 1e9 / peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src, "kernel_ms": round(spec_ms, 4),
+                     "step_frac": round(C1_STREAM * steps / (ms / 1e3) / 1e9 / peak, 4)},
+        "timing": "CUDA graph (2 steps per replay), events on the launch stream, max over ranks; kernel_ms from "
+                  "per-kernel events in a second pass of direct launches",
+    }
+    del bufs, ws, bounds
+    torch.cuda.empty_cache()
+    return out
+
+
+def measure_c4(args, cdc, torch, dist, dev, world, rank):
+    """configs[4]: one 64 GiB stream split by byte range with a halo over the ranks
+    (shard.chunk_sharded through the public API; NCCL all_gather of edge chain
+    states), RAM and AE-Max at 8 KiB."""
+    import synth
+    from paper_2508_05797_b200 import shard
+    out = {"workload": "configs[4]: one 64 GiB stream of alternating 256 MiB regions (uniform / runs of one value, "
+                       "geometric mean 512), split by byte range with a halo over the ranks (shard.chunk_sharded)",
+           "stream_bytes": C4_LEN, "scaling": "strong", "unit": "GB/s"}
+    buf = None
+    for algo in ("ram", "ae_max"):
+        p = cdc.params(algo, avg_size=8192)
+        halo = shard.default_halo(p.max_size, p.window)
+        pl = shard.plan(C4_LEN, world, rank, halo)
+        if buf is None:
+            buf = torch.from_numpy(synth.alternating(C4_LEN, region=256 << 20, seed=5,
+                                                     part=(pl.a, pl.buf_end))).to(dev)
+        comm = shard.DistComm() if dist is not None else None
+        backend = shard.CudaBackend()
+        res = [None]
+
+        def run(k):
+            for _ in range(k):
+                res[0] = shard.chunk_sharded(buf, pl, p, backend, comm)
+
+        run(1)
+        steps = max(3, min(args.steps, 10))
+        ms = timed(run, steps, torch.cuda.current_stream(dev), dist, dev, torch)
+        out[algo] = {"value": round(C4_LEN * steps / (ms / 1e3) / 1e9, 2), "ms_per_step": round(ms / steps, 3),
+                     "steps": steps, "boundaries": int(res[0][2]), "halo_bytes": halo}
+    out["timing"] = ("CUDA events on the current stream around shard.chunk_sharded (allocations, the local "
+                     "cdc_chunk, the all_gather and the resync included), barrier + synchronize, max over ranks")
+    del buf
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--check", action="store_true", help="verify the boundaries against the oracle once")
-    ap.add_argument("--seg-bytes", type=int, default=0, help="speculation segment size (0 = library default)")
+    ap.add_argument("--check", action="store_true", help="verify every boundary against the oracle once")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end host-buffer measurement")
     ap.add_argument("--no-graph", action="store_true", help="time direct launches instead of a CUDA graph")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the configs[1] and configs[4] keys")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, world, rank)
 
     import torch
-    import synth
     import paper_2508_05797_b200 as cdc
 
     torch.cuda.set_device(local)
@@ -214,144 +488,57 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    # every rank chunks its own copy of the configs[1] stream (seed 1): equal work
-    # per rank for weak scaling (another seed permutes which byte value is the
-    # rare 255 and changes AE-Max's chunk statistics)
-    data_np = synth.zipf_bytes(STREAM, 1.1, 1)
-    # two device copies of the stream at different addresses, used alternately, so
-    # that no step finds the previous step's lines in L2 (126 MB < 2 x 256 MiB)
-    bufs = [torch.from_numpy(data_np).to(dev) for _ in range(2)]
-    data = bufs[0]
-    p = cdc.params(ALGO, avg_size=AVG, seg_bytes=args.seg_bytes)
-    cap = cdc.max_boundaries(p, STREAM)
-    bounds = torch.empty(cap, dtype=torch.int64, device=dev)
-    count = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws = torch.empty(cdc.workspace_size(p, 1, STREAM, STREAM), dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
-
-    it = [0]
-
-    def step():
-        cdc.chunk_async(bufs[it[0] & 1], p, bounds, count, ws, stream)
-        it[0] += 1
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-    n_bounds = int(count.item())
-    if args.check and rank == 0:
-        import oracle
-        exp = oracle.chunk(ALGO, data_np, p.window, p.max_size)
-        got = bounds[:n_bounds].cpu().numpy().astype(np.uint64)
-        assert got.size == exp.size and (got == exp).all(), "boundary mismatch vs oracle"
-    launches_per_step = cdc.last_launch_count()
-    path_stats = cdc.stats(p, ws, 1, STREAM, STREAM)
-
-    # The timed region replays a CUDA graph of two steps (one per input copy):
-    # the three launches of a step (k_reset, k_speculate, k_fixup; the last
-    # exits at once when the fused fast path succeeded) without
-    # host launch overhead.  --no-graph times direct launches instead.
-    graph = None
-    if not args.no_graph:
-        side = torch.cuda.Stream(dev)
-        side.wait_stream(stream)
-        with torch.cuda.stream(side):
-            for b in bufs:
-                cdc.chunk_async(b, p, bounds, count, ws)
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            for b in bufs:
-                cdc.chunk_async(b, p, bounds, count, ws)
-        torch.cuda.synchronize()
-
-    def run(k):
-        if graph is None:
-            for _ in range(k):
-                step()
-            return
-        for _ in range(k // 2):
-            graph.replay()
-        if k % 2:
-            step()
-
-    # keep the GPU loaded ~0.3 s so clock samples reflect the timed region
-    with ClockSampler(local) as clk:
-        t_end = time.perf_counter() + 0.3
-        while time.perf_counter() < t_end:
-            run(2)
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        run(args.steps)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        # second pass, same K steps as direct launches with CUDA events around
-        # every kernel on the launch stream: the per-kernel durations below
-        cdc.profile_enable(True)
-        ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev2.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev3.record(stream)
-        torch.cuda.synchronize()
-        cdc.profile_enable(False)
-        profiled_ms = ev2.elapsed_time(ev3)
-    torch.cuda.synchronize()
-    got_n = int(count.item())
-    assert got_n == n_bounds, "boundary count changed between steps"
-    prof = cdc.profile_collect()
-    if dist is not None:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    total_bytes = STREAM * world * args.steps
-    gbs = total_bytes / (ms_max / 1e3) / 1e9
-
-    # roofline of the dominant kernel (k_speculate): algorithmic bytes per launch = the
-    # stream (each input byte read once); duration = its CUDA-event time on the launch stream
-    spec_ms, spec_n = prof["k_speculate"]
-    spec_avg_ms = spec_ms / max(1, spec_n)
-    peak, peak_src = load_peaks()
-    traffic_gb, traffic_src = load_traffic()
-    achieved = STREAM / (spec_avg_ms / 1e3) / 1e9
-    share = {k: round(prof[k][0] / max(1e-9, sum(prof[x][0] for x in cdc.KERNELS)), 4) for k in cdc.KERNELS}
-
-    # end to end through the public host API (pinned host input, copies inside the call)
-    e2e = None if args.no_e2e else measure_e2e(cdc, p, data_np, cap, world, dist, dev, args.steps)
+    c1 = None if args.no_secondary else measure_c1(args, cdc, torch, dist, dev, world)
+    c3 = measure_c3(args, cdc, torch, dist, dev, world, rank, local)
+    c4 = None if args.no_secondary else measure_c4(args, cdc, torch, dist, dev, world, rank)
 
     if rank == 0:
+        ms = c3["ms"]
+        gbs = c3["bytes_all"] * args.steps / (ms / 1e3) / 1e9
+        prof = c3["prof"]
+        spec_ms = prof["k_speculate"][0] / max(1, prof["k_speculate"][1])
+        step_ms = ms / args.steps
+        peak, peak_src = load_peaks()
+        traffic, traffic_src = load_traffic("ncu_k_speculate_c3.json")
+        achieved = c3["bytes_rank"] / (spec_ms / 1e3) / 1e9
+        ksum = sum(prof[k][0] for k in cdc.KERNELS)
+        p = c3["p"]
         line = {
             "metric": METRIC, "value": round(gbs, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "algo": ALGO, "avg_size": AVG, "window": p.window,
-                       "max_size": p.max_size, "stream_bytes": STREAM, "boundaries": n_bounds,
-                       "l2": "no flush: input (256 MiB per rank) larger than L2 (126 MB), and consecutive steps "
-                             "alternate between two device copies of it",
-                       "parallelism": f"dp{world}: one independent stream per rank, no data-path collective"},
-            "roofline": {"bound": "hbm", "kernel": "k_speculate", "achieved": round(achieved, 1),
-                         "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic_gb,
-                         "traffic_source": traffic_src, "algorithmic_gb_per_launch": round(STREAM / 1e9, 4),
-                         "kernel_ms": round(spec_avg_ms, 4), "share_of_step": share},
-            "gpu_launches": launches_per_step * args.steps,
-            "path": path_stats,
-            "timing": {"value": "CUDA graph of the step (2 steps per replay), CUDA events on the launch stream, "
-                                "max over ranks" if graph is not None else "direct launches, CUDA events, max over ranks",
-                       "kernel_ms": "per-kernel CUDA events on the launch stream in a second pass of K direct-launch steps",
-                       "ms_per_step_direct_launch_with_kernel_events": round(profiled_ms / args.steps, 4)},
-            "clocks": clk.summary(),
-            "e2e": e2e,
+            "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "algo": C3_ALGO, "avg_size": C3_AVG, "window": p.window,
+                       "max_size": p.max_size, "files": NFILES, "total_bytes": c3["bytes_all"],
+                       "rank0_files": list(c3["files"]), "rank0_bytes": c3["bytes_rank"],
+                       "boundaries": c3["boundaries"],
+                       "l2": "no flush: the resident input (18.67 GiB / N per rank) is far larger than L2 (126 MB)",
+                       "parallelism": f"files{world}: contiguous byte-balanced file ranges per rank "
+                                      f"(shard.file_range), no data-path collective"},
+            "roofline": {"bound": "hbm", "kernel": "k_speculate", "achieved": round(achieved, 1), "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_gb_per_launch": round(c3["bytes_rank"] / 1e9, 4),
+                         "per_unit": "1 byte read per input byte (DESIGN.md §5)",
+                         "kernel_ms": round(spec_ms, 4),
+                         "share_of_step": {k: round(prof[k][0] / max(1e-9, ksum), 4) for k in cdc.KERNELS}},
+            "gpu_launches": c3["launches"] * args.steps,
+            "path": c3["stats"],
+            "timing": {"value": ("CUDA graph of one step" if c3["graph"] else "direct launches")
+                       + ", CUDA events on the launch stream, barrier + synchronize, max over ranks",
+                       "kernel_ms": "per-kernel CUDA events on the launch stream in a second pass of K direct-launch "
+                                    "steps"},
+            "clocks": c3["clocks"],
+            "e2e": c3.get("e2e"),
         }
-        if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(data_np, p.window, p.max_size)
+        if c3.get("checked"):
+            line["checked"] = c3["checked"]
+        if "cpu_baseline" in c3:
+            line["cpu_baseline"] = c3["cpu_baseline"]
+        if c1 is not None:
+            line["configs1"] = c1
+        if c4 is not None:
+            line["configs4_sharded"] = c4
+        line["paper_cpu_vector"] = PAPER_CPU
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

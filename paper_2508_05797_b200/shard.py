@@ -94,6 +94,9 @@ class CudaBackend:
     def chain(self, buf: torch.Tensor, p, start: int, stop: int) -> torch.Tensor:
         return self.api.chain(buf, p, start, stop)
 
+    def chunk_batch(self, data: torch.Tensor, file_offsets, p):
+        return self.api.chunk_batch(data, file_offsets, p)
+
 
 @dataclass
 class LocalPass:
@@ -157,6 +160,8 @@ class ThreadComm:
         comm = self
 
         class _R:
+            rank = None
+
             def all_gather(self, x):
                 return comm._swap(rank, x)
 
@@ -164,7 +169,9 @@ class ThreadComm:
                 parts = comm._swap(rank, x)
                 x.copy_(torch.stack(parts).sum(0))
                 return x
-        return _R()
+        r = _R()
+        r.rank = rank
+        return r
 
 
 def exchange(lp: LocalPass, pl: ShardPlan, K: int, comm):
@@ -239,3 +246,48 @@ def chunk_sharded(buf: torch.Tensor, pl: ShardPlan, p, backend=None, comm=None):
     if pl.last:
         U = torch.cat([U, torch.tensor([pl.total], dtype=torch.int64, device=U.device)])
     return U, sum(counts[:pl.rank]), sum(counts)
+
+
+# ---------------------------------------------------------------------- files
+def file_range(offsets, world: int, rank: int) -> tuple[int, int]:
+    """Files shard directly (north_star (4)): rank r takes the contiguous files
+    [f0, f1) whose first bytes fall in the r-th of `world` equal byte ranges of
+    the packed batch (byte-balanced, no file split; no data-path collective)."""
+    import numpy as np
+    offs = np.asarray(offsets, dtype=np.int64)
+    nf = offs.size - 1
+    total = int(offs[-1] - offs[0])
+
+    def cut(r):
+        if r <= 0:
+            return 0
+        if r >= world:
+            return nf
+        # first file starting at or after the r-th byte cut
+        return int(np.searchsorted(offs[:-1], offs[0] + total * r // world, side="left"))
+    return cut(rank), cut(rank + 1)
+
+
+def chunk_files_sharded(data: torch.Tensor, file_offsets, p, comm=None, backend=None):
+    """Chunk this rank's files (data: its packed bytes on the device; file_offsets:
+    host int64[nf+1] relative to data) with one cdc_chunk_batch call, then one
+    all_gather of the per-rank counts places its boundaries in the global list.
+    Returns (bounds int64[m] per-file ends, bound_offsets int64[nf+1] local,
+    this rank's output offset, the global boundary count)."""
+    backend = backend or CudaBackend()
+    bounds, bo = backend.chunk_batch(data, file_offsets, p)
+    m = bounds.numel()
+    if comm is None:
+        return bounds, bo, 0, m
+    x = torch.tensor([m], dtype=torch.int64, device=bounds.device)
+    counts = [int(t.item()) for t in comm.all_gather(x)]
+    rank = counts_rank(comm)
+    return bounds, bo, sum(counts[:rank]), sum(counts)
+
+
+def counts_rank(comm) -> int:
+    r = getattr(comm, "rank", None)
+    if r is not None:
+        return r
+    import torch.distributed as dist
+    return dist.get_rank(getattr(comm, "group", None))

@@ -43,6 +43,7 @@ __all__ = [
     "versioned",
     "file_sizes",
     "many_files",
+    "many_files_offsets",
     "alternating",
     "constant",
     "saturation_edges",
@@ -198,22 +199,34 @@ def file_sizes(n_files: int, seed: int = 3, median: int = 64 << 10, sigma: float
     return sz
 
 
+def many_files_offsets(n_files: int, seed: int = 3, median: int = 64 << 10, sigma: float = 1.5,
+                       cap: int = 16 << 20) -> np.ndarray:
+    """File offsets int64[n_files+1] of many_files' packed batch (no bytes drawn)."""
+    sizes = file_sizes(n_files, seed, median, sigma, cap)
+    offsets = np.zeros(n_files + 1, dtype=np.int64)
+    np.cumsum(sizes, out=offsets[1:])
+    return offsets
+
+
 def many_files(n_files: int, seed: int = 3, median: int = 64 << 10, sigma: float = 1.5,
-               cap: int = 16 << 20, uniform_frac: float = 0.7, zipf_s: float = 1.1):
+               cap: int = 16 << 20, uniform_frac: float = 0.7, zipf_s: float = 1.1, files=None):
     """Packed many-file batch: returns (data uint8[total], offsets int64[n_files+1]).
 
     File kinds are drawn per file (uniform with probability uniform_frac, else
     Zipf-skewed).  The packed bytes are generated piece by piece: inside piece
-    k, each file's part is drawn from piece k's generator with its file's kind."""
-    sizes = file_sizes(n_files, seed, median, sigma, cap)
+    k, each file's part is drawn from piece k's generator with its file's kind.
+    files=(f0, f1) returns only files [f0, f1) -- the same bytes as the slice of
+    the whole batch -- with offsets relative to file f0 (a rank's share)."""
+    offsets = many_files_offsets(n_files, seed, median, sigma, cap)
     kinds = _rng(seed + 1000).random(n_files) < uniform_frac  # True: uniform
-    offsets = np.zeros(n_files + 1, dtype=np.int64)
-    np.cumsum(sizes, out=offsets[1:])
-    total = int(offsets[-1])
+    f0, f1 = (0, n_files) if files is None else files
+    lo0, hi0 = int(offsets[f0]), int(offsets[f1])
     z = _Zipf(zipf_s, seed + 2000)
-    out = np.empty(total, dtype=np.uint8)
+    out = np.empty(hi0 - lo0, dtype=np.uint8)
 
     def fill(k, lo, hi):
+        # piece k of the whole batch covers [k PIECE, (k+1) PIECE); draw it from
+        # its start so that a slice equals the whole batch's bytes
         rng = _piece_rng(seed, k, 3)
         f = int(np.searchsorted(offsets, lo, side="right")) - 1
         x = lo
@@ -221,25 +234,34 @@ def many_files(n_files: int, seed: int = 3, median: int = 64 << 10, sigma: float
             e = min(hi, int(offsets[f + 1]))
             if e > x:
                 if kinds[f]:
-                    out[x:e] = rng.integers(0, 256, size=e - x, dtype=np.uint8)
+                    v = rng.integers(0, 256, size=e - x, dtype=np.uint8)
                 else:
-                    out[x:e] = z.draw(rng, e - x)
+                    v = z.draw(rng, e - x)
+                a, b = max(x, lo0), min(e, hi0)
+                if a < b:
+                    out[a - lo0:b - lo0] = v[a - x:b - x]
             x = e
             f += 1
 
-    _pieces(total, fill)
-    return out, offsets
+    k0, k1 = lo0 // PIECE, (hi0 + PIECE - 1) // PIECE
+    total = int(offsets[-1])
+    with ThreadPoolExecutor(_threads()) as ex:
+        list(ex.map(lambda k: fill(k, k * PIECE, min(total, (k + 1) * PIECE)), range(k0, k1)))
+    return out, offsets[f0:f1 + 1] - lo0
 
 
-def alternating(n: int, region: int = 256 << 20, seed: int = 5, mean_run: float = 512.0) -> np.ndarray:
-    """Alternating regions: uniform random, then runs of repeated values (geometric lengths)."""
-    out = np.empty(n, dtype=np.uint8)
+def alternating(n: int, region: int = 256 << 20, seed: int = 5, mean_run: float = 512.0,
+                part=None) -> np.ndarray:
+    """Alternating regions: uniform random, then runs of repeated values (geometric lengths).
+    part=(lo, hi) returns only bytes [lo, hi) of the n-byte stream (a rank's range + halo)."""
+    lo0, hi0 = (0, n) if part is None else part
+    out = np.empty(hi0 - lo0, dtype=np.uint8)
 
     def fill_region(k):
         lo, hi = k * region, min(n, (k + 1) * region)
         rng = _piece_rng(seed, k, 4)
         if k % 2 == 0:
-            out[lo:hi] = rng.integers(0, 256, size=hi - lo, dtype=np.uint8)
+            v = rng.integers(0, 256, size=hi - lo, dtype=np.uint8)
         else:
             m = hi - lo
             n_runs = int(m / mean_run * 1.2) + 16
@@ -247,9 +269,11 @@ def alternating(n: int, region: int = 256 << 20, seed: int = 5, mean_run: float 
             while lens.sum() < m:
                 lens = np.concatenate([lens, rng.geometric(1.0 / mean_run, size=n_runs)])
             vals = rng.integers(0, 256, size=lens.size, dtype=np.uint8)
-            out[lo:hi] = np.repeat(vals, lens)[:m]
+            v = np.repeat(vals, lens)[:m]
+        a, b = max(lo, lo0), min(hi, hi0)
+        out[a - lo0:b - lo0] = v[a - lo:b - lo]
 
-    ks = range((n + region - 1) // region)
+    ks = range(lo0 // region, (hi0 + region - 1) // region)
     with ThreadPoolExecutor(_threads()) as ex:
         list(ex.map(fill_region, ks))
     return out

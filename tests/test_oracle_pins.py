@@ -367,3 +367,4 @@ def test_check_batch_accepts_oracle_and_rejects_mutations(algo):
     bo3[10], bo3[11] = bo3[11], bo3[10]
     if bo3[10] != bo3[11]:
         assert oracle.check_batch(algo, data, offs, ends, bo3, w, mx) is not None
+

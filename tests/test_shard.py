@@ -38,6 +38,10 @@ class OracleBackend:
         return torch.from_numpy(oracle.chain_from(p.algo, buf.numpy(), start, stop, p.window, p.max_size)
                                 .astype(np.int64))
 
+    def chunk_batch(self, data, offs, p):
+        e, bo = oracle.chunk_batch(p.algo, data.numpy(), offs, p.window, p.max_size)
+        return torch.from_numpy(e.astype(np.int64)), torch.from_numpy(bo)
+
 
 CASES = {
     # name: (algo, generator, n, w, max_size, halo)
@@ -172,3 +176,123 @@ def test_shard_gpu_config4_shape(algo, cuda_ok):
     exp = oracle.chunk(algo, data, p.window, p.max_size).astype(np.int64)
     halo = shard.default_halo(p.max_size, p.window)
     _check(_threads(8, data, p, halo, shard.CudaBackend(), to="cuda"), exp)
+
+
+# --------------------------------------------------------------------------
+# file sharding (north_star (4): "files shard directly")
+# --------------------------------------------------------------------------
+def _files():
+    data, offs = synth.many_files(400, seed=43, median=20000, sigma=1.5, cap=1 << 20)
+    return data, offs, SimpleNamespace(algo="ram", window=1000, max_size=8000)
+
+
+def _file_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        data, offs, p = _files()
+        f0, f1 = shard.file_range(offs, world, rank)
+        local = offs[f0:f1 + 1] - offs[f0]
+        buf = torch.from_numpy(np.ascontiguousarray(data[offs[f0]:offs[f1]]))
+        b, bo, off, total = shard.chunk_files_sharded(buf, local, p, shard.DistComm(), OracleBackend())
+        np.save(os.path.join(out_dir, f"f{rank}.npy"), np.concatenate([[f0, f1, off, total], bo.numpy(), b.numpy()]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_file_range_partitions_byte_balanced():
+    _, offs, _ = _files()
+    for world in (1, 2, 3, 8):
+        rs = [shard.file_range(offs, world, r) for r in range(world)]
+        assert rs[0][0] == 0 and rs[-1][1] == offs.size - 1
+        assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
+        total = offs[-1]
+        for f0, f1 in rs:  # every rank's bytes are within one largest file of the share
+            assert abs(int(offs[f1] - offs[f0]) - total / world) <= int(np.diff(offs).max()) + 1
+
+
+def test_files_gloo_world2(tmp_path):
+    import torch.multiprocessing as tmp
+    world = 2
+    tmp.spawn(_file_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    data, offs, p = _files()
+    exp, exp_bo = oracle.chunk_batch(p.algo, data, offs, p.window, p.max_size)
+    got = []
+    for r in range(world):
+        a = np.load(tmp_path / f"f{r}.npy")
+        f0, f1, off, total = (int(x) for x in a[:4])
+        nf = f1 - f0
+        bo = a[4:4 + nf + 1]
+        b = a[4 + nf + 1:]
+        assert total == exp.size and off == int(exp_bo[f0])
+        assert (bo + off == exp_bo[f0:f1 + 1]).all()
+        got.append(b)
+    assert (np.concatenate(got).astype(np.uint64) == exp).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_files_gpu_threads(world, cuda_ok):
+    """File sharding with the CUDA backend, ranks emulated by host threads."""
+    import paper_2508_05797_b200 as cdc
+    data, offs, p0 = _files()
+    p = cdc.params("ram", window=p0.window, max_size=p0.max_size)
+    exp, exp_bo = oracle.chunk_batch("ram", data, offs, p.window, p.max_size)
+    comm = shard.ThreadComm(world)
+    res = [None] * world
+
+    def work(r):
+        f0, f1 = shard.file_range(offs, world, r)
+        buf = torch.from_numpy(np.ascontiguousarray(data[offs[f0]:offs[f1]])).cuda()
+        b, bo, off, total = shard.chunk_files_sharded(buf, offs[f0:f1 + 1] - offs[f0], p, comm.for_rank(r))
+        res[r] = (f0, f1, b.cpu().numpy(), bo.cpu().numpy(), off, total)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for f0, f1, b, bo, off, total in res:
+        assert total == exp.size and off == int(exp_bo[f0]) and (bo + off == exp_bo[f0:f1 + 1]).all()
+    assert (np.concatenate([r[2] for r in res]).astype(np.uint64) == exp).all()
+
+
+def _nccl_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    import paper_2508_05797_b200 as cdc
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        comm = shard.DistComm()
+        data, exp, p0 = _expected("ram_zipf")
+        p = cdc.params("ram", window=p0.window, max_size=p0.max_size)
+        pl = shard.plan(data.size, world, rank, CASES["ram_zipf"][5])
+        U, off, total = shard.chunk_sharded(torch.from_numpy(data).cuda(), pl, p, shard.CudaBackend(), comm)
+        # a real NCCL collective on the exchange's message shape
+        x = torch.arange(5, dtype=torch.int64, device="cuda")
+        parts = comm.all_gather(x)
+        y = comm.all_reduce_sum(torch.ones(3, dtype=torch.int64, device="cuda"))
+        fd, fo, fp = _files()
+        pf = cdc.params("ram", window=fp.window, max_size=fp.max_size)
+        b, bo, foff, ftotal = shard.chunk_files_sharded(torch.from_numpy(fd).cuda(), fo, pf, comm)
+        np.save(os.path.join(out_dir, "nccl.npy"), np.concatenate(
+            [[off, total, len(parts), int(parts[0].sum()), int(y.sum()), foff, ftotal], U.cpu().numpy(),
+             b.cpu().numpy()]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_distcomm_nccl_world1(cuda_ok, tmp_path):
+    """DistComm over a real NCCL process group (world size 1: gpurun has one GPU)
+    runs the range-sharded and file-sharded paths end to end."""
+    import torch.multiprocessing as tmp
+    tmp.spawn(_nccl_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    a = np.load(tmp_path / "nccl.npy")
+    off, total, nparts, s, ysum, foff, ftotal = (int(x) for x in a[:7])
+    _, exp, _ = _expected("ram_zipf")
+    fd, fo, fp = _files()
+    fexp, _ = oracle.chunk_batch("ram", fd, fo, fp.window, fp.max_size)
+    assert (off, total, nparts, s, ysum, foff, ftotal) == (0, exp.size, 1, 10, 3, 0, fexp.size)
+    assert (a[7:7 + total] == exp).all()
+    assert (a[7 + total:].astype(np.uint64) == fexp).all()
