@@ -290,8 +290,8 @@ def measure_c3(args, cdc, torch, dist, dev, world, rank, local):
     ws = torch.empty(cdc.workspace_size(p, nf, total, max_len), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        cdc.chunk_batch_async(data, od, total, max_len, p, bounds, bo, count, ws, stream)
+    def step():  # on the current stream (the graph capture's stream while capturing)
+        cdc.chunk_batch_async(data, od, total, max_len, p, bounds, bo, count, ws)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -380,8 +380,8 @@ def measure_c1(args, cdc, torch, dist, dev, world):
     stream = torch.cuda.current_stream(dev)
     it = [0]
 
-    def step():
-        cdc.chunk_async(bufs[it[0] & 1], p, bounds, count, ws, stream)
+    def step():  # on the current stream (the graph capture's stream while capturing)
+        cdc.chunk_async(bufs[it[0] & 1], p, bounds, count, ws)
         it[0] += 1
 
     for _ in range(4):

@@ -71,6 +71,8 @@ struct Work {
     uint32_t *pool;              // fix-up walker starts: segment g's slice [g cap_halo, (g+1) cap_halo), relative to seg_end
     uint64_t *seg_first;         // nfiles+1 (batch)
     uint32_t *seg_file;          // G: file of each segment (batch)
+    uint64_t *lofs;              // G+1: first list entry of each segment (batch: lists sized by
+                                 // segment length); null for a single stream (g * cap_list)
     uint64_t *file_out;          // nfiles+1 (single stream: internal)
     uint32_t *misc;              // [0] G, [1] n_exc, [2] n_ranges, [3] overflow flags
     // transfer tables (T-mode, saturated streams): per segment TK candidates
@@ -169,6 +171,16 @@ __device__ __forceinline__ SegInfo seg_info(const Geometry &G, const Work &W, ui
     return I;
 }
 
+// Published list of segment g: its first entry and its capacity.  A batch
+// sizes each list by its segment's length (k_seg_prefix); a single stream's
+// segments share one capacity.
+__device__ __forceinline__ uint64_t list_off(const Work &W, uint64_t g) {
+    return W.lofs ? W.lofs[g] : g * W.cap_list;
+}
+__device__ __forceinline__ uint64_t list_cap(const Work &W, uint64_t g) {
+    return W.lofs ? W.lofs[g + 1] - W.lofs[g] : W.cap_list;
+}
+
 // global index and first byte (file-relative) of the segment of file position e
 __device__ __forceinline__ int64_t seg_of_pos(const SegInfo &I, int64_t e, uint64_t, int64_t &pj) {
     const uint64_t n = I.last - I.first + 1;
@@ -204,6 +216,8 @@ struct ListProbe {
     uint32_t cursor;     // monotone cursor in list(j)
     uint32_t wb;         // first entry index of the cached window (~0: none)
     uint32_t wv;         // this lane's cached entry wb + lane
+    const uint32_t *lst; // list(j) and its capacity
+    uint64_t cap;
 
     __device__ void reset() {
         j = -1;
@@ -221,10 +235,10 @@ struct ListProbe {
             hi = k + 1 < n ? seg_start(k + 1, n, I.Lf) : (int64_t)I.Lf;
             cursor = 0;
             wb = ~0u;
+            lst = W.list + list_off(W, (uint64_t)j);
+            cap = list_cap(W, (uint64_t)j);
         }
         jo = j;
-        const uint32_t *lst = W.list + (uint64_t)j * W.cap_list;
-        const uint64_t cap = W.cap_list;
         const uint32_t r = (uint32_t)(e - lo);
         const int lane = lane_id();
         while (cursor < cap) {
@@ -560,7 +574,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     em.G = &G;
     em.W = &W;
     em.I = seg_info(G, W, g);
-    em.list = W.list + g * W.cap_list;
+    em.list = W.list + list_off(W, g);
     em.halo = W.halo + g * W.cap_halo;
     em.pub = W.pub + g;
     em.cnt = 1;
@@ -763,7 +777,7 @@ __device__ void recheck_halo(const Geometry &G, Work &W, uint64_t g) {
             int64_t pj;
             j = seg_of_pos(I, e, G.S, pj);
             const uint32_t r = (uint32_t)(e - pj);
-            const uint32_t *lst = W.list + (uint64_t)j * W.cap_list;
+            const uint32_t *lst = W.list + list_off(W, (uint64_t)j);
             uint32_t lo = 0, hi = W.cnt[j];
             while (lo < hi) {
                 const uint32_t mid = (lo + hi) >> 1;
@@ -889,7 +903,7 @@ __device__ void resolve_block(const Geometry &G, Work &W, uint64_t *d_count, uin
                 em.overflow = false;
                 const uint32_t hc = W.hcnt[g];
                 const int64_t last = hc ? I.seg_end + (int64_t)W.halo[g * W.cap_halo + hc - 1]
-                                        : I.p + (int64_t)W.list[g * W.cap_list + W.cnt[g] - 1];
+                                        : I.p + (int64_t)W.list[list_off(W, g) + W.cnt[g] - 1];
                 run_chain<ALGO>(R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
                                 stream_policy(), em);
                 if (lane == 0) {
@@ -1051,7 +1065,7 @@ __device__ void write_segment(const Geometry &G, const Work &W, const uint64_t *
     const uint32_t e = W.entry[g], cnt = W.cnt[g], tail = W.tail[g], wc = exc ? W.wcnt[g] : 0u;
     const uint32_t oc = exc ? W.ocnt[g] : 0u;
     const uint64_t A = cnt - e, n = A + tail + wc + oc, base = W.seg_out[g];
-    const uint32_t *lst = W.list + g * W.cap_list;
+    const uint32_t *lst = W.list + list_off(W, g);
     const uint32_t *hl = W.halo + g * W.cap_halo;
     for (uint64_t i = lane; i < n; i += 32) {
         uint64_t v;
@@ -1102,28 +1116,100 @@ __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_
 }
 
 // ------------------------------------------------------------------ K0 batch segment table
-__global__ void __launch_bounds__(RESOLVE_THREADS) k_seg_prefix(const uint64_t *file_off, uint64_t nfiles,
-                                                                uint64_t S, uint64_t *seg_first,
-                                                                uint32_t *seg_file) {
-    __shared__ uint64_t scratch[64];
-    __shared__ uint64_t s_carry;
-    if (threadIdx.x == 0) s_carry = 0;
+// One CTA; SP_RPT consecutive files per thread per tile.  Writes seg_first
+// (first segment of each file), seg_file (segment -> file) and lofs (first
+// list entry of each segment: a segment of len bytes gets len / (w+1) + 2
+// entries -- every chunk but a file's last is longer than w).
+constexpr int SP_RPT = 8;
+__device__ __forceinline__ void block_exclusive_scan2(uint64_t &a, uint64_t &b, uint64_t &ta, uint64_t &tb,
+                                                      uint64_t *scratch) {
+    // scratch: 4 x 32 words
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint64_t x = a, y = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, x, o), v = __shfl_up_sync(0xFFFFFFFFu, y, o);
+        if (lane >= o) {
+            x += u;
+            y += v;
+        }
+    }
+    if (lane == 31) {
+        scratch[warp] = x;
+        scratch[32 + warp] = y;
+    }
     __syncthreads();
-    for (uint64_t base = 0; base < nfiles; base += blockDim.x) {
-        const uint64_t f = base + threadIdx.x;
-        uint64_t n = 0;
-        if (f < nfiles) n = nseg_of(file_off[f + 1] - file_off[f], S);
-        uint64_t tot;
-        uint64_t pos = block_exclusive_scan(n, tot, scratch) + s_carry;
-        if (f < nfiles) {
-            seg_first[f] = pos;
-            for (uint64_t i = 0; i < n; ++i) seg_file[pos + i] = (uint32_t)f;  // segment -> file map
+    if (warp == 0) {
+        uint64_t sx = lane < nw ? scratch[lane] : 0, sy = lane < nw ? scratch[32 + lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, sx, o), v = __shfl_up_sync(0xFFFFFFFFu, sy, o);
+            if (lane >= o) {
+                sx += u;
+                sy += v;
+            }
+        }
+        scratch[64 + lane] = sx;
+        scratch[96 + lane] = sy;
+    }
+    __syncthreads();
+    const uint64_t px = warp ? scratch[64 + warp - 1] : 0, py = warp ? scratch[96 + warp - 1] : 0;
+    ta = scratch[64 + nw - 1];
+    tb = scratch[96 + nw - 1];
+    __syncthreads();
+    a = px + x - a;
+    b = py + y - b;
+}
+
+__global__ void __launch_bounds__(RESOLVE_THREADS) k_seg_prefix(const uint64_t *file_off, uint64_t nfiles,
+                                                                uint64_t S, uint64_t w1, uint64_t *seg_first,
+                                                                uint32_t *seg_file, uint64_t *lofs) {
+    __shared__ uint64_t scratch[128];
+    __shared__ uint64_t s_carry[2];
+    if (threadIdx.x == 0) s_carry[0] = s_carry[1] = 0;
+    __syncthreads();
+    const uint64_t TILE = (uint64_t)blockDim.x * SP_RPT;
+    for (uint64_t base = 0; base < nfiles; base += TILE) {
+        const uint64_t f0 = base + (uint64_t)threadIdx.x * SP_RPT;
+        uint64_t ns = 0, nl = 0;
+        for (int i = 0; i < SP_RPT; ++i) {
+            const uint64_t f = f0 + i;
+            if (f >= nfiles) break;
+            const uint64_t len = file_off[f + 1] - file_off[f];
+            const uint64_t n = nseg_of(len, S);
+            ns += n;
+            nl += len / w1 + 2 * n;  // sum over the file's segments of seg_len / w1 + 2 (floor of a sum >= sum of floors)
+        }
+        uint64_t ts, tl;
+        block_exclusive_scan2(ns, nl, ts, tl, scratch);
+        uint64_t ps = s_carry[0] + ns, pl = s_carry[1] + nl;
+        for (int i = 0; i < SP_RPT; ++i) {
+            const uint64_t f = f0 + i;
+            if (f >= nfiles) break;
+            const uint64_t len = file_off[f + 1] - file_off[f];
+            const uint64_t n = nseg_of(len, S);
+            seg_first[f] = ps;
+            uint64_t used = 0;
+            for (uint64_t k = 0; k < n; ++k) {  // segment -> file map and list offsets
+                const uint64_t sl = (uint64_t)(seg_start(k + 1, n, len) - seg_start(k, n, len));
+                seg_file[ps + k] = (uint32_t)f;
+                lofs[ps + k] = pl + used;
+                used += sl / w1 + 2;
+            }
+            ps += n;
+            pl += len / w1 + 2 * n;
         }
         __syncthreads();
-        if (threadIdx.x == 0) s_carry += tot;
+        if (threadIdx.x == 0) {
+            s_carry[0] += ts;
+            s_carry[1] += tl;
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) seg_first[nfiles] = s_carry;
+    if (threadIdx.x == 0) {
+        seg_first[nfiles] = s_carry[0];
+        lofs[s_carry[0]] = s_carry[1];
+    }
 }
 
 // ------------------------------------------------------------------ chain API kernel
@@ -1467,8 +1553,11 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     P.poolb_cap = total_len / w1 + 2;
     P.exc_cap = P.max_segs;
     const uint64_t G = P.max_segs;
+    // lists: a single stream's segments share one capacity; a batch sizes each
+    // segment's list by its length (k_seg_prefix), len / (w+1) + 2 entries
+    const uint64_t list_entries = nfiles > 1 ? total_len / w1 + 2 * G + 2 : G * P.cap_list;
     size_t sz[] = {
-        G * P.cap_list * 4,  // 0 list   } reset to 0xFF by k_reset at every call
+        list_entries * 4,    // 0 list   } reset to 0xFF by k_reset at every call
         G * 20 + 64 + (G / 32 + 1) * 12,  // 1 pub, status, ctrl, grp, tblk, tnx }
         G * P.cap_halo * 4,  // 2 halo
         G * 4,               // 3 cnt
@@ -1503,9 +1592,10 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
         (G / cdc::TB + 2) * 4,            // 32 tbe
         (G / cdc::TB + 2) * 8,            // 33 tbo
         G * cdc::TEX * 8,                 // 34 tex
+        (G + 2) * 8,                      // 35 lofs (batch)
     };
     size_t o = 0;
-    for (int i = 0; i < 35; ++i) {
+    for (int i = 0; i < 36; ++i) {
         P.off[i] = o;
         o += round_up(sz[i], 256);
     }
@@ -1556,6 +1646,7 @@ cdc::Work carve(const Plan &P, void *ws) {
     W.tbe = (uint32_t *)(b + P.off[32]);
     W.tbo = (uint64_t *)(b + P.off[33]);
     W.tex = (int64_t *)(b + P.off[34]);
+    W.lofs = nullptr;  // set by run_chunk for batch calls (slot 35)
     W.poolb_cap = P.poolb_cap;
     W.cap_list = P.cap_list;
     W.cap_halo = P.cap_halo;
@@ -1591,8 +1682,8 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     };
     mark(0);
     if (batch) {
-        cdc::k_seg_prefix<<<1, cdc::RESOLVE_THREADS, 0, st>>>(G.file_off, G.nfiles, G.S, W.seg_first,
-                                                              W.seg_file);
+        cdc::k_seg_prefix<<<1, cdc::RESOLVE_THREADS, 0, st>>>(G.file_off, G.nfiles, G.S, (uint64_t)p->window + 1,
+                                                              W.seg_first, W.seg_file, W.lofs);
         CDC_KCHECK("k_seg_prefix", st);
         ++launches;
         pc.used[0] = true;
@@ -1642,7 +1733,8 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     mark(2);
     {
         // a small grid: it exits at once in the common case; writers stride over segments otherwise
-        const uint64_t fblocks = std::min<uint64_t>((nseg_ub + 31) / 32, FIX_BLOCKS);
+        // (a batch: the writers of every segment's boundaries span the GPU, two CTAs per SM)
+        const uint64_t fblocks = std::min<uint64_t>((nseg_ub + 31) / 32, batch ? 2 * nsm : FIX_BLOCKS);
         CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_fixup<ALGO>), dim3((unsigned)(fblocks ? fblocks : 1)),
                             dim3(cdc::RESOLVE_THREADS), (size_t)cdc::FIX_SMEM, st, G, W, d_count, file_out, d_bounds,
                             cap));
@@ -1669,6 +1761,9 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     make_plan(p, nfiles, total_len, max_len, P);
     if (ws_bytes < P.bytes) return fail(CDC_ERR_WORKSPACE, "workspace too small");
     cdc::Work W = carve(P, ws);
+    // a batch's lists are sized per segment (k_seg_prefix); for nfiles == 1 the
+    // single-stream list region (G x cap_list) holds them as well
+    if (batch) W.lofs = reinterpret_cast<uint64_t *>(static_cast<uint8_t *>(ws) + P.off[35]);
     cdc::Geometry G;
     G.data = d_data;
     G.file_off = batch ? d_file_off : nullptr;
