@@ -624,6 +624,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
         W.sa[g] = em.sa;
         W.sb[g] = em.sb;
         if (!normal) atomicAnd(W.ctrl + 1, 0u);  // the fast path's output is void
+        if (em.sj != SJ_LAST && em.sj != (int32_t)(g + 1)) atomicAnd(W.ctrl + 2, 0u);  // (batch_resolve)
     }
     // stage this segment's chain starts (list, then the halo tail) in the ring's
     // shared memory as offsets from p, so the write after the look-back needs no
@@ -737,6 +738,43 @@ __device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t &t
     total = scratch[32 + nw - 1];
     __syncthreads();
     return warp_prefix + x - v;
+}
+
+// Decoupled look-back over tiles (k_seg_prefix, the batch resolve): a word is
+// a flag (top two bits) and a non-negative 62-bit value; k_reset leaves ~0 =
+// not ready.  Every word is self-contained, so relaxed accesses suffice.
+constexpr unsigned long long TL_AGG = 1ull << 62;  // the tile's own total
+constexpr unsigned long long TL_INC = 2ull << 62;  // the inclusive prefix through the tile
+constexpr unsigned long long TL_VAL = (1ull << 62) - 1;
+__device__ __forceinline__ void tile_publish(unsigned long long *w, unsigned long long flag, uint64_t v) {
+    asm volatile("st.relaxed.gpu.u64 [%0], %1;" ::"l"(w), "l"(flag | (v & TL_VAL)) : "memory");
+}
+// All 32 lanes: the exclusive prefix of tile t from the words st[k * stride],
+// k < t, read 32 at a time from t-1 downwards until an inclusive one.
+__device__ uint64_t tile_lookback(const unsigned long long *st, uint64_t stride, uint64_t t) {
+    const int lane = lane_id();
+    uint64_t excl = 0;
+    int64_t k = (int64_t)t - 1;
+    while (k >= 0) {
+        const int64_t i = k - lane;
+        const unsigned long long wd = i >= 0 ? ld_relaxed_u64(st + (uint64_t)i * stride) : TL_INC;
+        const unsigned long long fl = wd & ~TL_VAL;
+        const uint32_t inc = __ballot_sync(0xFFFFFFFFu, fl == TL_INC);
+        const uint32_t bad = __ballot_sync(0xFFFFFFFFu, fl != TL_INC && fl != TL_AGG);
+        const int fi = inc ? __ffs(inc) - 1 : 31;  // lanes 0..fi are needed
+        const uint32_t need = fi == 31 ? 0xFFFFFFFFu : ((2u << fi) - 1u);
+        if (bad & need) {
+            __nanosleep(100);
+            continue;
+        }
+        uint64_t v = (lane <= fi && i >= 0) ? (uint64_t)(wd & TL_VAL) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        excl += v;
+        if (inc) break;
+        k -= 32;
+    }
+    return excl;
 }
 
 constexpr int RPT = 8;           // resolve_block: consecutive segments per thread in the count scan
@@ -1079,6 +1117,108 @@ __device__ void write_segment(const Geometry &G, const Work &W, const uint64_t *
     }
 }
 
+// A batch whose every segment's chain met the next segment's chain (or ended
+// its file; k_speculate clears ctrl[CT_BATCH_NORMAL] otherwise): every CTA
+// scans tiles of BR_RPT x 1024 segments' output counts (entry(g) = sb(g-1),
+// 0 at a file's first segment) chained by a decoupled look-back, then, once
+// every tile is done, writes its share of the segments' boundaries and the
+// per-file offsets.  Tiles are taken from a ticket by running CTAs, so the
+// wait for all tiles cannot block on a CTA that has not started.
+constexpr int BR_RPT = 2;
+constexpr int CT_BATCH_NORMAL = 2, CT_BR_TICKET = 7, CT_BR_DONE = 8, CT_SP_TICKET = 6;
+__device__ void batch_resolve(const Geometry &G, Work &W, uint64_t nsegs, uint64_t *d_count, uint64_t *file_out,
+                              uint64_t *bounds, uint64_t cap) {
+    __shared__ uint64_t scratch[64];
+    __shared__ uint64_t s_ex;
+    __shared__ uint32_t s_t;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t BT = (uint64_t)blockDim.x * BR_RPT;
+    const uint64_t ntiles = (nsegs + BT - 1) / BT;
+    for (;;) {
+        if (tid == 0) s_t = atomicAdd(W.ctrl + CT_BR_TICKET, 1u) + 1u;  // the counter starts at ~0
+        __syncthreads();
+        const uint64_t t = s_t;
+        if (t >= ntiles) break;  // uniform across the CTA
+        uint32_t nloc[BR_RPT];
+        uint64_t sum = 0;
+#pragma unroll
+        for (int i = 0; i < BR_RPT; ++i) {
+            const uint64_t g = t * BT + (uint64_t)tid * BR_RPT + i;
+            uint32_t n = 0;
+            if (g < nsegs) {
+                const bool first = W.seg_first[W.seg_file[g]] == g;
+                const uint32_t e = first ? 0u : W.sb[g - 1];
+                const uint32_t tail = W.sj[g] >= 0 ? W.sa[g] : 0u;
+                W.entry[g] = e;
+                W.tail[g] = tail;
+                n = W.cnt[g] - e + tail;
+            }
+            nloc[i] = n;
+            sum += n;
+        }
+        uint64_t tot;
+        uint64_t pos = block_exclusive_scan(sum, tot, scratch);  // (its barriers also order the read of s_t)
+        if (warp == 0) {
+            uint64_t ex = 0;
+            if (t == 0) {
+                if (lane == 0) tile_publish(W.grp, TL_INC, tot);
+            } else {
+                if (lane == 0) tile_publish(W.grp + t, TL_AGG, tot);
+                ex = tile_lookback(W.grp, 1, t);
+                if (lane == 0) tile_publish(W.grp + t, TL_INC, ex + tot);
+            }
+            if (lane == 0) s_ex = ex;
+        }
+        __syncthreads();
+        pos += s_ex;
+#pragma unroll
+        for (int i = 0; i < BR_RPT; ++i) {
+            const uint64_t g = t * BT + (uint64_t)tid * BR_RPT + i;
+            if (g < nsegs) W.seg_out[g] = pos;
+            pos += nloc[i];
+        }
+        if (t == ntiles - 1 && tid == 0) {
+            W.seg_out[nsegs] = s_ex + tot;
+            *d_count = s_ex + tot;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(W.ctrl + CT_BR_DONE, 1u);
+        }
+    }
+    if (tid == 0) {
+        while (ld_acquire_u32(W.ctrl + CT_BR_DONE) + 1u != (uint32_t)ntiles) __nanosleep(256);
+    }
+    __syncthreads();
+    // boundaries, one warp per segment
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t g = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < nsegs; g += nw) {
+        const SegInfo I = seg_info(G, W, g);
+        const uint64_t fo = W.seg_out[I.first];
+        if (g == I.first && lane == 0 && I.Lf > 0) {
+            const uint64_t q = W.seg_out[I.last + 1] - 1;  // a file's last boundary is its length
+            if (q < cap) bounds[q] = I.Lf;
+        }
+        const uint32_t e = W.entry[g], A = W.cnt[g] - e, n = A + W.tail[g];
+        const uint64_t base = W.seg_out[g];
+        const uint32_t *lst = W.list + list_off(W, g);
+        const uint32_t *hl = W.halo + g * W.cap_halo;
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint64_t v = i < A ? (uint64_t)I.p + lst[e + i] : (uint64_t)I.seg_end + hl[i - A];
+            const uint64_t q = base + i;
+            if (q == fo) continue;  // the file's first start (0) is not a boundary
+            if (q - 1 < cap) bounds[q - 1] = v;
+        }
+    }
+    // per-file output offsets
+    const uint64_t total = W.seg_out[nsegs];
+    for (uint64_t f = (uint64_t)blockIdx.x * blockDim.x + tid; f <= G.nfiles; f += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t sf = W.seg_first[f];
+        file_out[f] = sf >= nsegs ? total : W.seg_out[sf];
+    }
+}
+
 // K2 (fix-up, one launch): when k_speculate's fused fast path succeeded this
 // exits at once (a batch still needs its per-file offsets, computed by the
 // first CTA).  Otherwise the CTA that draws ticket 0 resolves the true chain
@@ -1093,6 +1233,11 @@ __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_
     pdl_wait();  // k_speculate has completed and its writes are visible
     if (threadIdx.x == 0) stamp(TM_FIX_WAITED);
     const uint64_t nsegs = total_segs(G, W);
+    if (G.file_off != nullptr && nsegs > 0 && W.ctrl[CT_BATCH_NORMAL] != 0u) {
+        batch_resolve(G, W, nsegs, d_count, file_out, bounds, cap);
+        if (threadIdx.x == 0) stamp(TM_FIX_END);
+        return;
+    }
     const bool fast = nsegs > 0 && W.ctrl[1] != 0u;
     if (fast && G.file_off == nullptr) {
         if (threadIdx.x == 0) stamp(TM_FIX_END);
@@ -1116,11 +1261,12 @@ __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_
 }
 
 // ------------------------------------------------------------------ K0 batch segment table
-// One CTA; SP_RPT consecutive files per thread per tile.  Writes seg_first
-// (first segment of each file), seg_file (segment -> file) and lofs (first
-// list entry of each segment: a segment of len bytes gets len / (w+1) + 2
-// entries -- every chunk but a file's last is longer than w).
-constexpr int SP_RPT = 8;
+// Tiles of SP_THREADS x SP_RPT consecutive files, taken from a ticket by a
+// small grid, chained by a decoupled look-back (tile_lookback).  Writes
+// seg_first (first segment of each file), seg_file (segment -> file) and lofs
+// (first list entry of each segment: a segment of len bytes gets
+// len / (w+1) + 2 entries -- every chunk but a file's last is longer than w).
+constexpr int SP_THREADS = 256, SP_RPT = 4;
 __device__ __forceinline__ void block_exclusive_scan2(uint64_t &a, uint64_t &b, uint64_t &ta, uint64_t &tb,
                                                       uint64_t *scratch) {
     // scratch: 4 x 32 words
@@ -1161,16 +1307,30 @@ __device__ __forceinline__ void block_exclusive_scan2(uint64_t &a, uint64_t &b, 
     b = py + y - b;
 }
 
-__global__ void __launch_bounds__(RESOLVE_THREADS) k_seg_prefix(const uint64_t *file_off, uint64_t nfiles,
-                                                                uint64_t S, uint64_t w1, uint64_t *seg_first,
-                                                                uint32_t *seg_file, uint64_t *lofs) {
+// st: two look-back words per tile (segments, list entries), reset to ~0 by k_reset;
+// ticket: ctrl[SP_TICKET] (reset to ~0)
+__global__ void __launch_bounds__(SP_THREADS) k_seg_prefix(const uint64_t *file_off, uint64_t nfiles, uint64_t S,
+                                                           uint64_t w1, uint64_t *seg_first, uint32_t *seg_file,
+                                                           uint64_t *lofs, unsigned long long *st,
+                                                           uint32_t *ticket) {
     __shared__ uint64_t scratch[128];
-    __shared__ uint64_t s_carry[2];
-    if (threadIdx.x == 0) s_carry[0] = s_carry[1] = 0;
-    __syncthreads();
-    const uint64_t TILE = (uint64_t)blockDim.x * SP_RPT;
-    for (uint64_t base = 0; base < nfiles; base += TILE) {
-        const uint64_t f0 = base + (uint64_t)threadIdx.x * SP_RPT;
+    __shared__ uint64_t s_ex[2];
+    __shared__ uint32_t s_t;
+    pdl_trigger();  // k_speculate may launch now; it waits for this grid's completion
+    pdl_wait();     // k_reset has completed (look-back words and ticket)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t TILE = (uint64_t)SP_THREADS * SP_RPT;
+    const uint64_t ntiles = (nfiles + TILE - 1) / TILE;
+    if (nfiles == 0 && blockIdx.x == 0 && tid == 0) {
+        seg_first[0] = 0;
+        lofs[0] = 0;
+    }
+    for (;;) {
+        if (tid == 0) s_t = atomicAdd(ticket, 1u) + 1u;  // the counter starts at ~0
+        __syncthreads();
+        const uint64_t t = s_t;
+        if (t >= ntiles) break;  // uniform across the CTA
+        const uint64_t f0 = t * TILE + (uint64_t)tid * SP_RPT;
         uint64_t ns = 0, nl = 0;
         for (int i = 0; i < SP_RPT; ++i) {
             const uint64_t f = f0 + i;
@@ -1181,8 +1341,33 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_seg_prefix(const uint64_t *
             nl += len / w1 + 2 * n;  // sum over the file's segments of seg_len / w1 + 2 (floor of a sum >= sum of floors)
         }
         uint64_t ts, tl;
-        block_exclusive_scan2(ns, nl, ts, tl, scratch);
-        uint64_t ps = s_carry[0] + ns, pl = s_carry[1] + nl;
+        block_exclusive_scan2(ns, nl, ts, tl, scratch);  // (its barriers also order the read of s_t)
+        if (warp == 0) {
+            uint64_t es = 0, el = 0;
+            if (t == 0) {
+                if (lane == 0) {
+                    tile_publish(st, TL_INC, ts);
+                    tile_publish(st + 1, TL_INC, tl);
+                }
+            } else {
+                if (lane == 0) {
+                    tile_publish(st + 2 * t, TL_AGG, ts);
+                    tile_publish(st + 2 * t + 1, TL_AGG, tl);
+                }
+                es = tile_lookback(st, 2, t);
+                el = tile_lookback(st + 1, 2, t);
+                if (lane == 0) {
+                    tile_publish(st + 2 * t, TL_INC, es + ts);
+                    tile_publish(st + 2 * t + 1, TL_INC, el + tl);
+                }
+            }
+            if (lane == 0) {
+                s_ex[0] = es;
+                s_ex[1] = el;
+            }
+        }
+        __syncthreads();
+        uint64_t ps = s_ex[0] + ns, pl = s_ex[1] + nl;
         for (int i = 0; i < SP_RPT; ++i) {
             const uint64_t f = f0 + i;
             if (f >= nfiles) break;
@@ -1199,16 +1384,11 @@ __global__ void __launch_bounds__(RESOLVE_THREADS) k_seg_prefix(const uint64_t *
             ps += n;
             pl += len / w1 + 2 * n;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            s_carry[0] += ts;
-            s_carry[1] += tl;
+        if (t == ntiles - 1 && tid == 0) {
+            seg_first[nfiles] = s_ex[0] + ts;
+            lofs[s_ex[0] + ts] = s_ex[1] + tl;
         }
         __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        seg_first[nfiles] = s_carry[0];
-        lofs[s_carry[0]] = s_carry[1];
     }
 }
 
@@ -1681,14 +1861,8 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         }
     };
     mark(0);
-    if (batch) {
-        cdc::k_seg_prefix<<<1, cdc::RESOLVE_THREADS, 0, st>>>(G.file_off, G.nfiles, G.S, (uint64_t)p->window + 1,
-                                                              W.seg_first, W.seg_file, W.lofs);
-        CDC_KCHECK("k_seg_prefix", st);
-        ++launches;
-        pc.used[0] = true;
-    }
-    // reset the published lists (list entries -> LIST_EMPTY, pub -> PUB_OPEN)
+    // reset the published lists (list entries -> LIST_EMPTY, pub -> PUB_OPEN) and
+    // the look-back, ticket and flag words
     {
         const uint64_t n16 = P.reset_bytes / 16;  // reset_bytes is a multiple of 256
         const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());
@@ -1696,6 +1870,17 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         CDC_KCHECK("k_reset", st);
     }
     ++launches;
+    if (batch) {
+        // segment table (launched with PDL behind the reset; k_speculate behind it)
+        const uint64_t tiles = (G.nfiles + cdc::SP_THREADS * cdc::SP_RPT - 1) / (cdc::SP_THREADS * cdc::SP_RPT);
+        const unsigned sb = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, 2 * (uint64_t)num_sms()));
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_seg_prefix), dim3(sb), dim3(cdc::SP_THREADS), 0,
+                            st, G.file_off, G.nfiles, G.S, (uint64_t)p->window + 1, W.seg_first, W.seg_file,
+                            W.lofs, W.status, W.ctrl + cdc::CT_SP_TICKET));
+        CDC_KCHECK("k_seg_prefix", st);
+        ++launches;
+        pc.used[0] = true;
+    }
     mark(1);
     // segments: exact for a single stream (nseg_of), an upper bound for a batch
     const uint64_t nseg_ub = batch ? P.max_segs
