@@ -793,4 +793,181 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     __syncwarp();
 }
 
+// ---------------------------------------------------------------- sparse walker
+// Saturated chunks need only a few bytes ("sparse walk"):
+//   RAM (§2.1.2 l.198): a window [s, s+w) that holds 0xFF has maximum 0xFF, so
+//     the chunk ends after the first 0xFF in [s+w, limit), else at limit -- the
+//     rest of the window is never needed;
+//   AE-Max (l.169; AE-Min with 0x00): if the first saturating byte q of
+//     [s, s+w] exists, every earlier target is beaten within w bytes (q is at
+//     most w after it) and nothing beats q, so the chunk ends at q+w+1 (at
+//     limit when q+w >= limit); when s+w >= limit it ends at limit whatever
+//     the bytes.
+// sparse_chain walks such chunks with plain 16-byte global loads of SPR-byte
+// regions at the decisive positions (one dependent round trip per chunk on
+// uniform bytes) instead of streaming every byte through the TMA ring.  At the
+// first chunk it cannot decide this way it stops and returns false with the
+// chunk's start in `resume`: the caller continues with run_chain from there.
+// Returns true when the walk ended (emitter stop, stream end, exhaustion), with
+// the same emitter calls run_chain would have made.
+#ifndef CDC_SPV
+#define CDC_SPV 2
+#endif
+constexpr int SPV = CDC_SPV;       // 16-byte vectors per lane per region
+constexpr int SPR = SPV * BLK;     // region bytes
+
+struct SpReg {      // one loaded region [P, P + SPR) of file positions (P 16-byte aligned in memory)
+    int64_t P;
+    uint32_t m[SPV];  // lane's saturation masks: bit j of m[v] <=> byte P + 512 v + 16 lane + j saturates
+};
+
+template <bool MAX>
+__device__ __forceinline__ void sp_load(SpReg &r, const uint8_t *__restrict__ fbase, int64_t x, int64_t Lf) {
+    const int64_t a = (int64_t)(reinterpret_cast<uintptr_t>(fbase + x) & 15u);
+    r.P = x - a;
+    const int lane = lane_id();
+    uint4 d[SPV];
+#pragma unroll
+    for (int v = 0; v < SPV; ++v) {  // every load first, then the tests
+        const int64_t q = r.P + v * BLK + 16 * lane;
+        d[v] = make_uint4(MAX ? 0u : ~0u, MAX ? 0u : ~0u, MAX ? 0u : ~0u, MAX ? 0u : ~0u);
+        if (q < Lf) d[v] = __ldg(reinterpret_cast<const uint4 *>(fbase + q));  // granule holds a byte < Lf
+    }
+#pragma unroll
+    for (int v = 0; v < SPV; ++v) r.m[v] = sat_mask16<MAX>(d[v]);
+}
+// first saturating position in [lo, hi) within the region (positions outside
+// the region are not examined), or -1
+__device__ __forceinline__ int64_t sp_first(const SpReg &r, int64_t lo, int64_t hi) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int v = 0; v < SPV; ++v) {
+        const int64_t q = r.P + v * BLK + 16 * lane;
+        const int64_t a64 = lo - q, b64 = hi - q;
+        const int a = a64 < 0 ? 0 : (a64 > 16 ? 16 : (int)a64);
+        const int b = b64 < 0 ? 0 : (b64 > 16 ? 16 : (int)b64);
+        const uint32_t keep = a < b ? (((1u << b) - 1u) & ~((1u << a) - 1u)) : 0u;
+        const uint32_t mm = r.m[v] & keep;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mm != 0u);
+        if (bal) {
+            const int L = __ffs(bal) - 1;
+            const uint32_t mL = __shfl_sync(0xFFFFFFFFu, mm, L);
+            return r.P + v * BLK + 16 * L + (__ffs(mL) - 1);
+        }
+    }
+    return -1;
+}
+
+template <int ALGO, class Emit>
+__device__ bool sparse_chain(const uint8_t *__restrict__ fbase, int64_t Lf, int64_t start, int64_t read_end,
+                             uint32_t w, uint64_t max_size, Emit &emit, int64_t &resume) {
+    constexpr bool MAX = (ALGO != ALGO_AE_MIN);
+    const int64_t W = (int64_t)w;
+    if (read_end > Lf) read_end = Lf;
+    int64_t s = start;
+    if constexpr (ALGO == ALGO_RAM) {
+        SpReg r;            // the region that held the last boundary byte (bytes after it are the next window's)
+        bool have = false;
+        for (;;) {
+            if (s + W >= Lf) {  // the window does not fit: a single final chunk
+                emit.end();
+                return true;
+            }
+            const int64_t limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
+            const int64_t wend = s + W < read_end ? s + W : read_end;  // window bytes we may read
+            bool sat = have && r.P + SPR > s && sp_first(r, s, wend) >= 0;
+            SpReg sc;
+            sp_load<true>(sc, fbase, s + W, Lf);  // the scan region, issued before any probe of the window
+            if (!sat) {
+                int64_t x = (have && r.P + SPR > s) ? r.P + SPR : s;
+                while (!sat && x < wend) {
+                    SpReg hr;
+                    sp_load<true>(hr, fbase, x, Lf);
+                    sat = sp_first(hr, x, wend) >= 0;
+                    x = hr.P + SPR;
+                }
+                if (!sat) {  // no 0xFF in the window (or past read_end): the ring walker decides this chunk
+                    resume = s;
+                    return false;
+                }
+            }
+            // the first 0xFF in [s + w, limit)
+            const int64_t hi = limit < read_end ? limit : read_end;
+            int64_t x = s + W, e;
+            for (;;) {
+                const int64_t pos = sp_first(sc, x, hi);
+                if (pos >= 0) {
+                    e = pos + 1;
+                    break;
+                }
+                x = sc.P + SPR;
+                if (x >= hi) {
+                    if (hi == limit) {
+                        e = limit;  // cap or end of stream
+                        break;
+                    }
+                    emit.exhausted(read_end);
+                    return true;
+                }
+                sp_load<true>(sc, fbase, x, Lf);
+            }
+            if (e >= Lf) {
+                emit.end();
+                return true;
+            }
+            if (emit.boundary(e)) return true;
+            s = e;
+            r = sc;
+            have = true;
+        }
+    } else {
+        for (;;) {
+            const int64_t limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
+            int64_t e;
+            if (s + W >= limit) {
+                e = limit;  // no target's window fits before the limit
+            } else {
+                // q = the first saturating byte of [s, s + w]
+                const int64_t hi = s + W + 1;
+                if (hi > read_end) {
+                    resume = s;
+                    return false;
+                }
+                int64_t x = s, q = -1;
+                while (q < 0 && x < hi) {
+                    SpReg rg;
+                    sp_load<MAX>(rg, fbase, x, Lf);
+                    q = sp_first(rg, x, hi);
+                    x = rg.P + SPR;
+                }
+                if (q < 0) {  // no saturating byte: the ring walker decides this chunk
+                    resume = s;
+                    return false;
+                }
+                e = q + W < limit ? q + W + 1 : limit;
+            }
+            if (e >= Lf) {
+                emit.end();
+                return true;
+            }
+            if (emit.boundary(e)) return true;
+            s = e;
+        }
+    }
+}
+
+// The walk of a chain from a chunk start: sparse while the chunks saturate,
+// then the TMA-ring walker from the first chunk the sparse walk cannot decide.
+template <int ALGO, class Emit>
+__device__ __forceinline__ void walk_chain(bool sparse, const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf,
+                                           int64_t start, int64_t read_end, uint32_t w, uint64_t max_size,
+                                           const L2Pol &pol, Emit &emit) {
+    if (sparse) {
+        int64_t resume = start;
+        if (sparse_chain<ALGO>(fbase, Lf, start, read_end, w, max_size, emit, resume)) return;
+        start = resume;
+    }
+    run_chain<ALGO>(R, fbase, Lf, start, read_end, w, max_size, pol, emit);
+}
+
 }  // namespace cdc

@@ -108,6 +108,7 @@ struct Geometry {
     uint32_t w;
     uint64_t max_size;
     int tmode;       // walkers may try transfer tables (single stream, one co-resident wave)
+    int sparse;      // walkers start with the sparse walk (sparse_chain; long windows)
 };
 
 __device__ __forceinline__ void file_bounds(const Geometry &G, uint64_t f, uint64_t &off, uint64_t &len) {
@@ -603,7 +604,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
                                         : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
     // the segment's head is read again by the previous segment's halo walk: keep it in L2
     const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
-    run_chain<ALGO>(R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
+    walk_chain<ALGO>(G.sparse != 0, R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
     em.publish();
     if (tm && lane == 0) {
         tm[TM_PER_SEG * g + 2] = globaltimer();
@@ -942,7 +943,7 @@ __device__ void resolve_block(const Geometry &G, Work &W, uint64_t *d_count, uin
                 const uint32_t hc = W.hcnt[g];
                 const int64_t last = hc ? I.seg_end + (int64_t)W.halo[g * W.cap_halo + hc - 1]
                                         : I.p + (int64_t)W.list[list_off(W, g) + W.cnt[g] - 1];
-                run_chain<ALGO>(R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
+                walk_chain<ALGO>(G.sparse != 0, R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
                                 stream_policy(), em);
                 if (lane == 0) {
                     W.sj[g] = em.overflow ? SJ_UNSYNCED : em.sj;
@@ -997,7 +998,7 @@ __device__ void resolve_block(const Geometry &G, Work &W, uint64_t *d_count, uin
                         em.overflow = false;
                         const uint32_t wc = W.wcnt[g];
                         const int64_t last = I.seg_end + (int64_t)W.pool[W.woff[g] + wc - 1];
-                        run_chain<ALGO>(R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
+                        walk_chain<ALGO>(G.sparse != 0, R, G.data + I.foff, (int64_t)I.Lf, last, (int64_t)I.Lf, G.w, G.max_size,
                                         stream_policy(), em);
                         overflow |= em.overflow;
                         if (lane == 0) {
@@ -1414,7 +1415,7 @@ struct ChainEmit {
 template <int ALGO>
 __global__ void __launch_bounds__(32) k_chain(const uint8_t *data, uint64_t len, uint64_t start, uint64_t stop,
                                               uint32_t w, uint64_t max_size, uint64_t *out, uint64_t cap,
-                                              uint64_t *count) {
+                                              uint64_t *count, int sparse) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *rb = align_smem(smem);
     WarpRing R{rb, reinterpret_cast<uint64_t *>(rb + RING_BYTES)};
@@ -1422,7 +1423,8 @@ __global__ void __launch_bounds__(32) k_chain(const uint8_t *data, uint64_t len,
     if (lane_id() == 0 && cap > 0) out[0] = start;
     em.n = 1;
     if (start < stop && start < len)
-        run_chain<ALGO>(R, data, (int64_t)len, (int64_t)start, (int64_t)len, w, max_size, stream_policy(), em);
+        walk_chain<ALGO>(sparse != 0, R, data, (int64_t)len, (int64_t)start, (int64_t)len, w, max_size, stream_policy(),
+                         em);
     if (lane_id() == 0) *count = em.n;
 }
 
@@ -1610,6 +1612,23 @@ bool sync_debug() {
 #define CDC_T_MAX_SEG (256ull << 10)
 #endif
 constexpr uint64_t T_MAX_SEG = CDC_T_MAX_SEG;
+
+// Sparse walk (sparse_chain) for windows of at least SPARSE_MIN_W bytes: with
+// shorter windows a chunk is little longer than the region a sparse step
+// loads, and the streaming ring walker is faster.  CDC_SPARSE=0 disables it
+// (a debugging and A/B knob).
+#ifndef CDC_SPARSE_MIN_W
+#define CDC_SPARSE_MIN_W 2048
+#endif
+constexpr uint32_t SPARSE_MIN_W = CDC_SPARSE_MIN_W;
+int sparse_on(uint32_t w) {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("CDC_SPARSE");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v && w >= SPARSE_MIN_W ? 1 : 0;
+}
 
 // CDC_TMODE=0 disables the transfer-table attempt (a debugging and testing knob)
 int tmode_on() {
@@ -1959,6 +1978,7 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     G.w = p->window;
     G.max_size = p->max_size;
     G.tmode = 0;
+    G.sparse = sparse_on(p->window);
     uint64_t *file_out = batch ? d_bound_off : W.file_out;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (p->algo) {
@@ -2364,15 +2384,15 @@ int cdc_chain(const cdc_params *p, const uint8_t *d_data, uint64_t len, uint64_t
     switch (p->algo) {
     case CDC_RAM:
         cdc::k_chain<0><<<1, 32, cdc::RING_SMEM + 128, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
-                                                       starts_cap, d_count);
+                                                       starts_cap, d_count, sparse_on(p->window));
         break;
     case CDC_AE_MAX:
         cdc::k_chain<1><<<1, 32, cdc::RING_SMEM + 128, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
-                                                       starts_cap, d_count);
+                                                       starts_cap, d_count, sparse_on(p->window));
         break;
     default:
         cdc::k_chain<2><<<1, 32, cdc::RING_SMEM + 128, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
-                                                       starts_cap, d_count);
+                                                       starts_cap, d_count, sparse_on(p->window));
     }
     g_launches = 1;
     CDC_CUDA(cudaGetLastError());
