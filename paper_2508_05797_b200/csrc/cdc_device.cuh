@@ -803,156 +803,273 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
 //     most w after it) and nothing beats q, so the chunk ends at q+w+1 (at
 //     limit when q+w >= limit); when s+w >= limit it ends at limit whatever
 //     the bytes.
-// sparse_chain walks such chunks with plain 16-byte global loads of SPR-byte
-// regions at the decisive positions (one dependent round trip per chunk on
-// uniform bytes) instead of streaming every byte through the TMA ring.  At the
-// first chunk it cannot decide this way it stops and returns false with the
-// chunk's start in `resume`: the caller continues with run_chain from there.
-// Returns true when the walk ended (emitter stop, stream end, exhaustion), with
-// the same emitter calls run_chain would have made.
-#ifndef CDC_SPV
-#define CDC_SPV 2
+// A chunk's *decisive bytes* start at x = s+w (RAM) or x = s (AE).  The next
+// chunk's start is at least s + 2w + 1 (RAM: its own decisive start is past
+// s + 2w + 1) or s + w + 1 (AE), so at the start of each chunk the walker
+// already issues a bulk copy (TMA, into its idle ring) of the SP_SPEC bytes
+// from there: the next chunk's decisive bytes, unless the two chunks' waits
+// for a saturating byte add up to more than SP_SPEC.  With one copy always in
+// flight behind the one being waited for, a chunk costs about half a memory
+// round trip, and only ~SP_SPEC bytes per chunk are read.  A scan that runs
+// past its region continues with copies of SP_SPEC bytes into a third slot;
+// RAM's window test looks at the bytes after the last boundary (still in the
+// slot that held it), then probes the window.  At the first chunk that cannot
+// be decided this way it stops and returns false with the chunk's start in
+// `resume` (the caller continues with run_chain from there).  Returns true
+// when the walk ended (emitter stop, stream end, exhaustion) with the emitter
+// calls run_chain would have made.
+#ifndef CDC_SP_SPEC
+#define CDC_SP_SPEC 2048
 #endif
-constexpr int SPV = CDC_SPV;       // 16-byte vectors per lane per region
-constexpr int SPR = SPV * BLK;     // region bytes
+constexpr int SP_SPEC = CDC_SP_SPEC;  // bytes per speculative or continuation copy (multiple of 16, <= SP_SLOT)
+constexpr int SP_SLOT = 4096;         // slot stride in the ring: slots 0/1 alternate per chunk, slot 2 continues
+static_assert(RING_BYTES >= 3 * SP_SLOT, "sparse walk needs three slots in the ring");
+static_assert(SP_SPEC % 16 == 0 && SP_SPEC <= SP_SLOT, "SP_SPEC");
 
-struct SpReg {      // one loaded region [P, P + SPR) of file positions (P 16-byte aligned in memory)
-    int64_t P;
-    uint32_t m[SPV];  // lane's saturation masks: bit j of m[v] <=> byte P + 512 v + 16 lane + j saturates
-};
-
+// First saturating byte in [lo, hi) among the slot's bytes [P, P + n) (file
+// positions), or -1: one 512-byte block per step, exact per-byte masks
+// (sat_mask16), one ballot per block.
+// (more: set when the same block holds another such byte in (result, hi))
 template <bool MAX>
-__device__ __forceinline__ void sp_load(SpReg &r, const uint8_t *__restrict__ fbase, int64_t x, int64_t Lf) {
-    const int64_t a = (int64_t)(reinterpret_cast<uintptr_t>(fbase + x) & 15u);
-    r.P = x - a;
-    const int lane = lane_id();
-    uint4 d[SPV];
-#pragma unroll
-    for (int v = 0; v < SPV; ++v) {  // every load first, then the tests
-        const int64_t q = r.P + v * BLK + 16 * lane;
-        d[v] = make_uint4(MAX ? 0u : ~0u, MAX ? 0u : ~0u, MAX ? 0u : ~0u, MAX ? 0u : ~0u);
-        if (q < Lf) d[v] = __ldg(reinterpret_cast<const uint4 *>(fbase + q));  // granule holds a byte < Lf
-    }
-#pragma unroll
-    for (int v = 0; v < SPV; ++v) r.m[v] = sat_mask16<MAX>(d[v]);
-}
-// first saturating position in [lo, hi) within the region (positions outside
-// the region are not examined), or -1
-__device__ __forceinline__ int64_t sp_first(const SpReg &r, int64_t lo, int64_t hi) {
-    const int lane = lane_id();
-#pragma unroll
-    for (int v = 0; v < SPV; ++v) {
-        const int64_t q = r.P + v * BLK + 16 * lane;
-        const int64_t a64 = lo - q, b64 = hi - q;
-        const int a = a64 < 0 ? 0 : (a64 > 16 ? 16 : (int)a64);
-        const int b = b64 < 0 ? 0 : (b64 > 16 ? 16 : (int)b64);
-        const uint32_t keep = a < b ? (((1u << b) - 1u) & ~((1u << a) - 1u)) : 0u;
-        const uint32_t mm = r.m[v] & keep;
-        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mm != 0u);
+__device__ __forceinline__ int64_t sm_first(const uint8_t *sp, int64_t P, int n, int64_t lo, int64_t hi,
+                                            bool *more = nullptr) {
+    if (lo < P) lo = P;
+    if (hi > P + n) hi = P + n;
+    if (lo >= hi) return -1;
+    const int a = (int)(lo - P), b = (int)(hi - P);
+    const int l16 = lane_id() * 16;
+    for (int B = a & ~(BLK - 1); B < b; B += BLK) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(sp + B + l16);
+        const int q = B + l16;
+        const int ka = min(max(a - q, 0), 16), kb = min(max(b - q, 0), 16);
+        const uint32_t m = sat_mask16<MAX>(v) & ((1u << kb) - 1u) & ~((1u << ka) - 1u);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m != 0u);
         if (bal) {
             const int L = __ffs(bal) - 1;
-            const uint32_t mL = __shfl_sync(0xFFFFFFFFu, mm, L);
-            return r.P + v * BLK + 16 * L + (__ffs(mL) - 1);
+            const uint32_t mL = __shfl_sync(0xFFFFFFFFu, m, L);
+            if (more) *more = (mL & (mL - 1u)) != 0u || (bal >> L) > 1u;
+            return P + B + 16 * L + (__ffs(mL) - 1);
         }
     }
     return -1;
 }
+#ifndef CDC_SP_FIND
+#define CDC_SP_FIND 0
+#endif
+template <int CMP>
+__device__ __forceinline__ int64_t sm_find(const uint8_t *sp, int64_t P, int n, int64_t lo, int64_t hi,
+                                           uint32_t target);
+// the sparse walk's region search for the saturating value (CDC_SP_FIND: 0 =
+// sm_first, 1 = the ring walker's Range Scan)
+template <bool MAX>
+__device__ __forceinline__ int64_t sm_sat(const uint8_t *sp, int64_t P, int n, int64_t lo, int64_t hi) {
+    if (CDC_SP_FIND == 0) return sm_first<MAX>(sp, P, n, lo, hi);
+    return sm_find<MAX ? CMP_GEQ : CMP_LEQ>(sp, P, n, lo, hi, MAX ? 255u : 0u);
+}
 
+// First byte of the slot's region [P, P + n) (file positions) in [lo, hi) that
+// satisfies (byte CMP target), or -1: the ring walker's block-level Range Scan
+// (stage_find_block: a per-lane extreme over 16-byte vectors, four blocks in
+// flight, one ballot per block) and its in-lane locate.
+template <int CMP>
+__device__ __forceinline__ int64_t sm_find(const uint8_t *sp, int64_t P, int n, int64_t lo, int64_t hi,
+                                           uint32_t target) {
+    if (lo < P) lo = P;
+    if (hi > P + n) hi = P + n;
+    if (lo >= hi) return -1;
+    const int a = (int)(lo - P), b = (int)(hi - P);
+    uint32_t bal = 0, lm = 0;
+    bool has = false;
+    const int Bk = stage_find_block<CMP>(sp, a, b, target, bal, lm, has);
+    if (Bk < 0) return -1;
+    return P + stage_locate<CMP>(sp, Bk, bal, a, b, target);
+}
+
+#ifdef CDC_SPTIME  // diagnostic: sparse walk cycle accounting into g_evt[11..15] (tools/sparse_probe.py)
+#define SPT_DECL long long spt_acc[5] = {0, 0, 0, 0, 0}, spt_t = 0, spt_0 = clock64();
+#define SPT_BEGIN spt_t = clock64()
+#define SPT_ADD(i) spt_acc[i] += clock64() - spt_t
+#define SPT_FLUSH                                                                       \
+    if (lane == 0) {                                                                    \
+        spt_acc[4] = clock64() - spt_0;                                                 \
+        for (int q = 0; q < 5; ++q) atomicAdd(&g_evt[11 + q], (unsigned long long)spt_acc[q]); \
+    }
+#else
+#define SPT_DECL
+#define SPT_BEGIN
+#define SPT_ADD(i)
+#define SPT_FLUSH
+#endif
 template <int ALGO, class Emit>
-__device__ bool sparse_chain(const uint8_t *__restrict__ fbase, int64_t Lf, int64_t start, int64_t read_end,
-                             uint32_t w, uint64_t max_size, Emit &emit, int64_t &resume) {
+__device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf, int64_t start,
+                             int64_t read_end, uint32_t w, uint64_t max_size, Emit &emit, int64_t &resume) {
     constexpr bool MAX = (ALGO != ALGO_AE_MIN);
+    constexpr bool RAM = (ALGO == ALGO_RAM);
+    const int lane = lane_id();
     const int64_t W = (int64_t)w;
     if (read_end > Lf) read_end = Lf;
+    const uint64_t pol = l2_evict_first_policy();
+    if (lane == 0) {
+        for (int i = 0; i < 3; ++i) mbar_init(&R.bar[i], 1);
+        fence_barrier_init();
+    }
+    __syncwarp();
+    uint32_t pend = 0, par = 0;  // per slot: copy in flight; parity of its next completion
+    // copy of the bytes from x (rounded down to 16 B, at most nb bytes, not past the
+    // granule holding byte Lf - 1) into slot `slot`; P, N: the region's start and size
+    auto issue = [&](int slot, int64_t x, int nb, int64_t &P, int &N) {
+        P = x - (int64_t)(reinterpret_cast<uintptr_t>(fbase + x) & 15u);
+        const int64_t avail = ((Lf - P) + 15) & ~static_cast<int64_t>(15);
+        N = (int)(avail < (int64_t)nb ? (avail > 0 ? avail : 0) : (int64_t)nb);
+        if (N > 0) {
+            uint64_t *bar = &R.bar[slot];
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "elect.sync _|p, 0xffffffff;\n\t"
+                "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+                "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%2], [%3], %1, [%0], %4;\n\t"
+                "}" ::"r"(smem_addr(bar)), "r"((uint32_t)N), "r"(smem_addr(R.buf + slot * SP_SLOT)), "l"(fbase + P),
+                "l"(pol)
+                : "memory");
+            pend |= 1u << slot;
+        }
+    };
+    auto wait = [&](int slot) {
+        if ((pend >> slot) & 1u) {
+            mbar_wait(&R.bar[slot], (par >> slot) & 1u);
+            par ^= 1u << slot;
+            pend &= ~(1u << slot);
+        }
+    };
+    SPT_DECL
+    auto finish = [&](bool r) -> bool {
+        SPT_FLUSH
+        wait(0);
+        wait(1);
+        wait(2);
+        __syncwarp();
+        if (lane == 0)
+            for (int i = 0; i < 3; ++i) mbar_inval(&R.bar[i]);
+        __syncwarp();
+        return r;
+    };
+    const int64_t GAP = RAM ? 2 * W + 1 : W + 1;  // the next chunk's decisive bytes start at or after s + GAP
     int64_t s = start;
-    if constexpr (ALGO == ALGO_RAM) {
-        SpReg r;            // the region that held the last boundary byte (bytes after it are the next window's)
-        bool have = false;
-        for (;;) {
-            if (s + W >= Lf) {  // the window does not fit: a single final chunk
-                emit.end();
-                return true;
+    int cur = 0;        // slot of this chunk's speculative region (alternates 0 / 1)
+    int64_t cP = 0;     // ... its region [cP, cP + cN)
+    int cN = 0;
+    int rs = -1;        // RAM: slot holding the bytes right after s, its region [rP, rP + rN)
+    int64_t rP = 0;
+    int rN = 0;
+    int64_t P2 = 0;     // continuation slot 2's region
+    int N2 = 0;
+    bool wsat = false;  // RAM: this chunk's window is known to hold a 0xFF
+    for (;;) {
+        if (RAM && s + W >= Lf) {  // the window does not fit: a single final chunk
+            emit.end();
+            return finish(true);
+        }
+        const int64_t limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
+        SPT_BEGIN;
+        if (RAM && !wsat) {  // does the window [s, s+w) hold a 0xFF?
+            const int64_t wend = s + W < read_end ? s + W : read_end;
+            bool sat = false;
+            int64_t x = s;
+            if (rs >= 0) {
+                sat = sm_sat<true>(R.buf + rs * SP_SLOT, rP, rN, s, wend) >= 0;
+                if (rP + rN > x) x = rP + rN;
             }
-            const int64_t limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
-            const int64_t wend = s + W < read_end ? s + W : read_end;  // window bytes we may read
-            bool sat = have && r.P + SPR > s && sp_first(r, s, wend) >= 0;
-            SpReg sc;
-            sp_load<true>(sc, fbase, s + W, Lf);  // the scan region, issued before any probe of the window
-            if (!sat) {
-                int64_t x = (have && r.P + SPR > s) ? r.P + SPR : s;
-                while (!sat && x < wend) {
-                    SpReg hr;
-                    sp_load<true>(hr, fbase, x, Lf);
-                    sat = sp_first(hr, x, wend) >= 0;
-                    x = hr.P + SPR;
-                }
-                if (!sat) {  // no 0xFF in the window (or past read_end): the ring walker decides this chunk
-                    resume = s;
-                    return false;
-                }
+            while (!sat && x < wend) {
+                CNT(15);
+                wait(2);
+                issue(2, x, SP_SPEC, P2, N2);
+                if (N2 <= 0) break;
+                wait(2);
+                sat = sm_sat<true>(R.buf + 2 * SP_SLOT, P2, N2, x, wend) >= 0;
+                x = P2 + N2;
             }
-            // the first 0xFF in [s + w, limit)
-            const int64_t hi = limit < read_end ? limit : read_end;
-            int64_t x = s + W, e;
-            for (;;) {
-                const int64_t pos = sp_first(sc, x, hi);
+            if (!sat) {  // the ring walker decides this chunk
+                resume = s;
+                return finish(false);
+            }
+        }
+        SPT_ADD(0);
+        const int nxt = cur ^ 1;
+        int64_t nP = 0;
+        int nN = 0;
+        wait(nxt);  // (the last chunk's region, already consumed)
+        if (s + GAP < Lf) issue(nxt, s + GAP, SP_SPEC, nP, nN);
+        int64_t e;
+        if (!RAM && s + W >= limit) {
+            e = limit;  // no target's window fits before the limit
+        } else {
+            const int64_t x0 = RAM ? s + W : s;
+            const int64_t hi = RAM ? (limit < read_end ? limit : read_end) : s + W + 1;
+            if (!RAM && hi > read_end) {
+                resume = s;
+                return finish(false);
+            }
+            if (!(cN > 0 && cP <= x0 && x0 < cP + cN)) {  // not covered by the speculative copy
+                CNT(13);
+                wait(cur);
+                issue(cur, x0, SP_SPEC, cP, cN);
+            }
+            SPT_BEGIN;
+            wait(cur);
+            SPT_ADD(1);
+            SPT_BEGIN;
+            int slot = cur;
+            int64_t P = cP;
+            int N = cN;
+            bool more = false;  // (RAM: another 0xFF within 512 bytes after the boundary byte)
+            int64_t pos = CDC_SP_FIND == 0 ? sm_first<MAX>(R.buf + cur * SP_SLOT, cP, cN, x0, hi, &more)
+                                           : sm_sat<MAX>(R.buf + cur * SP_SLOT, cP, cN, x0, hi);
+            while (pos < 0 && P + N < hi && N > 0) {  // continue past the region
+                const int64_t x = P + N > x0 ? P + N : x0;
+                CNT(14);
+                wait(2);
+                issue(2, x, SP_SPEC, P2, N2);
+                wait(2);
+                slot = 2;
+                P = P2;
+                N = N2;
+                pos = CDC_SP_FIND == 0 ? sm_first<MAX>(R.buf + 2 * SP_SLOT, P2, N2, x, hi, &more)
+                                       : sm_sat<MAX>(R.buf + 2 * SP_SLOT, P2, N2, x, hi);
+            }
+            if (RAM) {
                 if (pos >= 0) {
                     e = pos + 1;
-                    break;
-                }
-                x = sc.P + SPR;
-                if (x >= hi) {
-                    if (hi == limit) {
-                        e = limit;  // cap or end of stream
-                        break;
-                    }
+                } else if (hi == limit) {
+                    e = limit;  // cap or end of stream
+                } else {
                     emit.exhausted(read_end);
-                    return true;
+                    return finish(true);
                 }
-                sp_load<true>(sc, fbase, x, Lf);
-            }
-            if (e >= Lf) {
-                emit.end();
-                return true;
-            }
-            if (emit.boundary(e)) return true;
-            s = e;
-            r = sc;
-            have = true;
-        }
-    } else {
-        for (;;) {
-            const int64_t limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
-            int64_t e;
-            if (s + W >= limit) {
-                e = limit;  // no target's window fits before the limit
+                rs = slot;
+                rP = P;
+                rN = N;
+                wsat = pos >= 0 && more;  // the next window [e, e + w) holds that 0xFF (w >= 512)
             } else {
-                // q = the first saturating byte of [s, s + w]
-                const int64_t hi = s + W + 1;
-                if (hi > read_end) {
+                if (pos < 0) {  // no saturating byte in [s, s+w]: the ring walker decides this chunk
                     resume = s;
-                    return false;
+                    return finish(false);
                 }
-                int64_t x = s, q = -1;
-                while (q < 0 && x < hi) {
-                    SpReg rg;
-                    sp_load<MAX>(rg, fbase, x, Lf);
-                    q = sp_first(rg, x, hi);
-                    x = rg.P + SPR;
-                }
-                if (q < 0) {  // no saturating byte: the ring walker decides this chunk
-                    resume = s;
-                    return false;
-                }
-                e = q + W < limit ? q + W + 1 : limit;
+                e = pos + W < limit ? pos + W + 1 : limit;
             }
-            if (e >= Lf) {
-                emit.end();
-                return true;
-            }
-            if (emit.boundary(e)) return true;
-            s = e;
+            SPT_ADD(2);
         }
+        if (e >= Lf) {
+            emit.end();
+            return finish(true);
+        }
+        SPT_BEGIN;
+        const bool stop_ = emit.boundary(e);
+        SPT_ADD(3);
+        if (stop_) return finish(true);
+        s = e;
+        cur = nxt;
+        cP = nP;
+        cN = nN;
     }
 }
 
@@ -964,7 +1081,7 @@ __device__ __forceinline__ void walk_chain(bool sparse, const WarpRing &R, const
                                            const L2Pol &pol, Emit &emit) {
     if (sparse) {
         int64_t resume = start;
-        if (sparse_chain<ALGO>(fbase, Lf, start, read_end, w, max_size, emit, resume)) return;
+        if (sparse_chain<ALGO>(R, fbase, Lf, start, read_end, w, max_size, emit, resume)) return;
         start = resume;
     }
     run_chain<ALGO>(R, fbase, Lf, start, read_end, w, max_size, pol, emit);

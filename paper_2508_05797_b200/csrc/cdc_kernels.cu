@@ -71,6 +71,7 @@ struct Work {
     uint32_t *pool;              // fix-up walker starts: segment g's slice [g cap_halo, (g+1) cap_halo), relative to seg_end
     uint64_t *seg_first;         // nfiles+1 (batch)
     uint32_t *seg_file;          // G: file of each segment (batch)
+    uint32_t *lpt;               // batch: long segments by size class (LptLists; counters in tnx, bitmap in tblk)
     uint64_t *lofs;              // G+1: first list entry of each segment (batch: lists sized by
                                  // segment length); null for a single stream (g * cap_list)
     uint64_t *file_out;          // nfiles+1 (single stream: internal)
@@ -92,6 +93,29 @@ struct Work {
 enum : int32_t { SJ_UNSYNCED = -1, SJ_STREAM_END = -2, SJ_LAST = -3, SJ_TABLE = -4 };
 constexpr int DYN_TICKET = 9;  // ctrl[9] (reset to ~0): a batch's per-warp segment tickets
 
+// Largest-first order of a batch's long segments (k_speculate's tickets): a
+// segment of at least 2^LPT_MIN_LOG2 bytes goes into the list of its size
+// class b = min(floor(log2(len)) - LPT_MIN_LOG2, LPT_CLASSES - 1); tickets take
+// the classes from the largest down, then the other segments in file order.
+// A walker that starts a 16 MiB file last would otherwise finish alone, long
+// after every other walker (the longest walks set the batch's tail).
+constexpr int LPT_MIN_LOG2 = 20, LPT_CLASSES = 6;
+__host__ __device__ __forceinline__ uint64_t lpt_cap(uint64_t total, int b) {
+    return (total >> (LPT_MIN_LOG2 + b)) + 1;
+}
+__host__ __device__ __forceinline__ uint64_t lpt_base(uint64_t total, int b) {
+    uint64_t o = 0;
+    for (int i = 0; i < b; ++i) o += lpt_cap(total, i);
+    return o;
+}
+struct LptLists {
+    uint32_t *cnt;   // LPT_CLASSES counters (reset to ~0)
+    uint32_t *map;   // one bit per segment, cleared for a listed one (reset to all ones)
+    uint32_t *list;  // class b: [lpt_base(b), lpt_base(b) + lpt_cap(b))
+    uint64_t total;  // batch bytes
+};
+
+
 // dynamic shared memory follows the kernel's static shared variables: round the
 // ring up to 128 bytes (TMA destinations need 16, LDS.128 16; launches add 128)
 __device__ __forceinline__ uint8_t *align_smem(uint8_t *p) {
@@ -102,6 +126,7 @@ struct Geometry {
     const uint8_t *data;
     const uint64_t *file_off;  // null => single stream of length L
     uint64_t L;
+    uint64_t total;  // bytes of the stream or batch (as planned)
     uint64_t nfiles;
     uint64_t S;      // segment bytes
     uint64_t Hmax;   // halo cap
@@ -544,7 +569,21 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
         if (lane_id() == 0) t = atomicAdd(W.ctrl + DYN_TICKET, 1u) + 1u;  // counter starts at ~0
         return __shfl_sync(0xFFFFFFFFu, t, 0);
     };
-    uint64_t g = spw == 0 ? ticket() : (uint64_t)s_ticket * spw + warp;
+    // a batch: tickets take the listed long segments, largest class first, then
+    // every other segment in order (a listed one met there is skipped)
+    auto next_seg = [&]() -> uint64_t {
+        for (;;) {
+            uint64_t t = ticket();
+            const uint64_t total = G.total;
+            for (int b = LPT_CLASSES - 1; b >= 0; --b) {
+                const uint64_t c = (uint64_t)(W.tnx[b] + 1u);
+                if (t < c) return W.lpt[lpt_base(total, b) + t];
+                t -= c;
+            }
+            if (t >= nsegs || ((W.tblk[t >> 5] >> (t & 31)) & 1u)) return t;
+        }
+    };
+    uint64_t g = spw == 0 ? next_seg() : (uint64_t)s_ticket * spw + warp;
     int64_t pre_n = -1;
     if constexpr (TM) {
         if (spw == 1) {  // one segment per CTA: its 16 warps build the index together
@@ -557,7 +596,7 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
         speculate_segment<ALGO, TM>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused,
                                     pre_n);
         if (spw != 0) break;
-        g = ticket();
+        g = next_seg();
     }
     if (lane_id() == 0) stamp(TM_SPEC_END);
 }
@@ -625,7 +664,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
         W.sa[g] = em.sa;
         W.sb[g] = em.sb;
         if (!normal) atomicAnd(W.ctrl + 1, 0u);  // the fast path's output is void
-        if (em.sj != SJ_LAST && em.sj != (int32_t)(g + 1)) atomicAnd(W.ctrl + 2, 0u);  // (batch_resolve)
+        if (em.sj == SJ_UNSYNCED) atomicAnd(W.ctrl + 2, 0u);  // (batch_resolve needs every halo decided)
     }
     // stage this segment's chain starts (list, then the halo tail) in the ring's
     // shared memory as offsets from p, so the write after the look-back needs no
@@ -1118,21 +1157,68 @@ __device__ void write_segment(const Geometry &G, const Work &W, const uint64_t *
     }
 }
 
-// A batch whose every segment's chain met the next segment's chain (or ended
-// its file; k_speculate clears ctrl[CT_BATCH_NORMAL] otherwise): every CTA
-// scans tiles of BR_RPT x 1024 segments' output counts (entry(g) = sb(g-1),
-// 0 at a file's first segment) chained by a decoupled look-back, then, once
-// every tile is done, writes its share of the segments' boundaries and the
-// per-file offsets.  Tiles are taken from a ticket by running CTAs, so the
-// wait for all tiles cannot block on a CTA that has not started.
+// A batch whose every halo was decided (it met a later segment's chain of its
+// file, or reached the file's end; k_speculate clears ctrl[CT_BATCH_NORMAL]
+// otherwise).  Phase 0: one thread per file follows the true chain through
+// the file's segments (segment g's halo leads to its sync target sj(g) with
+// entry sb(g); segments it jumps over, and every segment after a halo that
+// reached the file's end, are skipped).  Phase 1: every CTA scans tiles of
+// BR_RPT x 1024 segments' output counts, chained by a decoupled look-back.
+// Phase 2: once every tile is done, every CTA writes its share of the
+// segments' boundaries and the per-file offsets.  Work is taken from tickets
+// by running CTAs, so the waits for a phase cannot block on a CTA that has
+// not started.
 constexpr int BR_RPT = 2;
 constexpr int CT_BATCH_NORMAL = 2, CT_BR_TICKET = 7, CT_BR_DONE = 8, CT_SP_TICKET = 6;
+constexpr int CT_BR0_TICKET = 10, CT_BR0_DONE = 11;  // (batch only: T-mode, which uses them, is single-stream)
 __device__ void batch_resolve(const Geometry &G, Work &W, uint64_t nsegs, uint64_t *d_count, uint64_t *file_out,
                               uint64_t *bounds, uint64_t cap) {
     __shared__ uint64_t scratch[64];
     __shared__ uint64_t s_ex;
     __shared__ uint32_t s_t;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // phase 0: the true chain through each file's segments
+    const uint64_t nblk0 = (G.nfiles + blockDim.x - 1) / blockDim.x;
+    for (;;) {
+        if (tid == 0) s_t = atomicAdd(W.ctrl + CT_BR0_TICKET, 1u) + 1u;  // the counter starts at ~0
+        __syncthreads();
+        const uint64_t t = s_t;
+        __syncthreads();
+        if (t >= nblk0) break;  // uniform across the CTA
+        const uint64_t f = t * blockDim.x + tid;
+        if (f < G.nfiles) {
+            const uint64_t a = W.seg_first[f], b = W.seg_first[f + 1];
+            uint32_t e = 0;
+            uint64_t h = a;
+            while (h < b) {
+                W.entry[h] = e;
+                W.skipped[h] = 0;
+                const int32_t sj = W.sj[h];
+                if (sj == SJ_LAST) {
+                    W.tail[h] = 0;
+                    break;
+                }
+                if (sj < 0) {  // SJ_STREAM_END: the halo carries the chain to the file's end
+                    W.tail[h] = W.hcnt[h];
+                    for (uint64_t k = h + 1; k < b; ++k) W.skipped[k] = 1;
+                    break;
+                }
+                W.tail[h] = W.sa[h];
+                for (uint64_t k = h + 1; k < (uint64_t)sj; ++k) W.skipped[k] = 1;
+                e = W.sb[h];
+                h = (uint64_t)sj;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(W.ctrl + CT_BR0_DONE, 1u);
+        }
+    }
+    if (tid == 0) {
+        while (ld_acquire_u32(W.ctrl + CT_BR0_DONE) + 1u != (uint32_t)nblk0) __nanosleep(256);
+    }
+    __syncthreads();
     const uint64_t BT = (uint64_t)blockDim.x * BR_RPT;
     const uint64_t ntiles = (nsegs + BT - 1) / BT;
     for (;;) {
@@ -1146,14 +1232,7 @@ __device__ void batch_resolve(const Geometry &G, Work &W, uint64_t nsegs, uint64
         for (int i = 0; i < BR_RPT; ++i) {
             const uint64_t g = t * BT + (uint64_t)tid * BR_RPT + i;
             uint32_t n = 0;
-            if (g < nsegs) {
-                const bool first = W.seg_first[W.seg_file[g]] == g;
-                const uint32_t e = first ? 0u : W.sb[g - 1];
-                const uint32_t tail = W.sj[g] >= 0 ? W.sa[g] : 0u;
-                W.entry[g] = e;
-                W.tail[g] = tail;
-                n = W.cnt[g] - e + tail;
-            }
+            if (g < nsegs && !W.skipped[g]) n = W.cnt[g] - W.entry[g] + W.tail[g];
             nloc[i] = n;
             sum += n;
         }
@@ -1195,6 +1274,7 @@ __device__ void batch_resolve(const Geometry &G, Work &W, uint64_t nsegs, uint64
     // boundaries, one warp per segment
     const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
     for (uint64_t g = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < nsegs; g += nw) {
+        if (W.skipped[g]) continue;  // (never a file's first segment)
         const SegInfo I = seg_info(G, W, g);
         const uint64_t fo = W.seg_out[I.first];
         if (g == I.first && lane == 0 && I.Lf > 0) {
@@ -1313,7 +1393,7 @@ __device__ __forceinline__ void block_exclusive_scan2(uint64_t &a, uint64_t &b, 
 __global__ void __launch_bounds__(SP_THREADS) k_seg_prefix(const uint64_t *file_off, uint64_t nfiles, uint64_t S,
                                                            uint64_t w1, uint64_t *seg_first, uint32_t *seg_file,
                                                            uint64_t *lofs, unsigned long long *st,
-                                                           uint32_t *ticket) {
+                                                           uint32_t *ticket, LptLists lpt) {
     __shared__ uint64_t scratch[128];
     __shared__ uint64_t s_ex[2];
     __shared__ uint32_t s_t;
@@ -1381,6 +1461,14 @@ __global__ void __launch_bounds__(SP_THREADS) k_seg_prefix(const uint64_t *file_
                 seg_file[ps + k] = (uint32_t)f;
                 lofs[ps + k] = pl + used;
                 used += sl / w1 + 2;
+                if (sl >> LPT_MIN_LOG2) {
+                    const uint64_t g = ps + k;
+                    int b = 63 - __clzll((long long)(sl >> LPT_MIN_LOG2));
+                    b = b < LPT_CLASSES - 1 ? b : LPT_CLASSES - 1;
+                    const uint32_t i = atomicAdd(lpt.cnt + b, 1u) + 1u;  // the counter starts at ~0
+                    lpt.list[lpt_base(lpt.total, b) + i] = (uint32_t)g;
+                    atomicAnd(lpt.map + (g >> 5), ~(1u << (g & 31)));
+                }
             }
             ps += n;
             pl += len / w1 + 2 * n;
@@ -1725,6 +1813,12 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
         const uint64_t target = (uint64_t)num_sms() * SEGS_PER_SM;
         // floor(len / target): floor(len / S) = target segments of ~equal length
         S = total_len / target;
+        // a batch: segments are taken largest first (LptLists), so only a file
+        // longer than every other walker's share sets the tail -- cut such files
+        // into segments shorter than one walker's share (a file's segments are
+        // [S, 2S) long).  Long windows keep whole-share segments: their halos
+        // re-synchronise slowly on saturated bytes.
+        if (nfiles > 1 && p->window <= 8192) S /= 2;
         const uint64_t lo = std::max<uint64_t>(64 << 10, round_up(4 * p->max_size, 128));
         if (S < lo) S = lo;
         if (S > (256ull << 20)) S = 256ull << 20;
@@ -1792,9 +1886,10 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
         (G / cdc::TB + 2) * 8,            // 33 tbo
         G * cdc::TEX * 8,                 // 34 tex
         (G + 2) * 8,                      // 35 lofs (batch)
+        (2 * (total_len >> cdc::LPT_MIN_LOG2) + cdc::LPT_CLASSES + 1) * 4,  // 36 lpt lists (batch)
     };
     size_t o = 0;
-    for (int i = 0; i < 36; ++i) {
+    for (int i = 0; i < 37; ++i) {
         P.off[i] = o;
         o += round_up(sz[i], 256);
     }
@@ -1845,7 +1940,8 @@ cdc::Work carve(const Plan &P, void *ws) {
     W.tbe = (uint32_t *)(b + P.off[32]);
     W.tbo = (uint64_t *)(b + P.off[33]);
     W.tex = (int64_t *)(b + P.off[34]);
-    W.lofs = nullptr;  // set by run_chunk for batch calls (slot 35)
+    W.lofs = nullptr;  // set by run_chunk for batch calls (slots 35, 36)
+    W.lpt = nullptr;
     W.poolb_cap = P.poolb_cap;
     W.cap_list = P.cap_list;
     W.cap_halo = P.cap_halo;
@@ -1895,7 +1991,8 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         const unsigned sb = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, 2 * (uint64_t)num_sms()));
         CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_seg_prefix), dim3(sb), dim3(cdc::SP_THREADS), 0,
                             st, G.file_off, G.nfiles, G.S, (uint64_t)p->window + 1, W.seg_first, W.seg_file,
-                            W.lofs, W.status, W.ctrl + cdc::CT_SP_TICKET));
+                            W.lofs, W.status, W.ctrl + cdc::CT_SP_TICKET,
+                            cdc::LptLists{W.tnx, W.tblk, W.lpt, total_len}));
         CDC_KCHECK("k_seg_prefix", st);
         ++launches;
         pc.used[0] = true;
@@ -1967,11 +2064,15 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     cdc::Work W = carve(P, ws);
     // a batch's lists are sized per segment (k_seg_prefix); for nfiles == 1 the
     // single-stream list region (G x cap_list) holds them as well
-    if (batch) W.lofs = reinterpret_cast<uint64_t *>(static_cast<uint8_t *>(ws) + P.off[35]);
+    if (batch) {
+        W.lofs = reinterpret_cast<uint64_t *>(static_cast<uint8_t *>(ws) + P.off[35]);
+        W.lpt = reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(ws) + P.off[36]);
+    }
     cdc::Geometry G;
     G.data = d_data;
     G.file_off = batch ? d_file_off : nullptr;
     G.L = batch ? 0 : total_len;
+    G.total = total_len;
     G.nfiles = batch ? nfiles : 1;
     G.S = P.S;
     G.Hmax = P.Hmax;

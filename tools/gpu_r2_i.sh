@@ -1,0 +1,4 @@
+python tools/c3_timing.py > gpurun_out/c3t.log 2>&1; echo c3t rc=$?
+python tools/sparse_probe.py > gpurun_out/sp4.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "batch or config3 or many or fuzz or chain or sparse" > gpurun_out/t7.log 2>&1; echo tests rc=$?
+tail -2 gpurun_out/t7.log
