@@ -1706,7 +1706,7 @@ constexpr uint64_t T_MAX_SEG = CDC_T_MAX_SEG;
 // loads, and the streaming ring walker is faster.  CDC_SPARSE=0 disables it
 // (a debugging and A/B knob).
 #ifndef CDC_SPARSE_MIN_W
-#define CDC_SPARSE_MIN_W 2048
+#define CDC_SPARSE_MIN_W 4096
 #endif
 constexpr uint32_t SPARSE_MIN_W = CDC_SPARSE_MIN_W;
 int sparse_on(uint32_t w) {
