@@ -24,6 +24,10 @@
 namespace cdc {
 
 constexpr int BLK = 512;               // bytes per warp block: 32 lanes x 16 B
+#ifndef CDC_YIELD_SAT
+#define CDC_YIELD_SAT 2
+#endif
+constexpr int YIELD_SAT = CDC_YIELD_SAT;  // saturated chunks after which the ring walker yields to the sparse walk
 #ifndef CDC_STAGE
 #define CDC_STAGE 6144
 #endif
@@ -482,6 +486,11 @@ __device__ __forceinline__ uint32_t sat_mask16(const uint4 &v) {
 // the bytes below read_end are exhausted first, emit.exhausted(c).  Bytes are
 // read only below read_end.  All 32 lanes call this with identical arguments.
 //
+// yield_at (the sparse walk's partner, walk_chain): when non-null, the walk
+// stops after YIELD_SAT consecutive saturated chunks (RAM: window maximum 0xFF;
+// AE: an unbeaten saturating target) and stores the next chunk's start there
+// (-1 otherwise), so that the sparse walk takes over again.
+//
 // Semantics are those of the oracle (oracle/cdc_oracle.c), with the chunk
 // limit = min(Lf, s + max_size) (reading R5):
 //   RAM:    M = max d[s, s+w); the chunk ends after the first i in [s+w, limit)
@@ -499,7 +508,8 @@ __device__ __forceinline__ uint32_t sat_mask16(const uint4 &v) {
 // AE target no byte can beat -- a direct jump to its deadline.
 template <int ALGO, class Emit>
 __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf, int64_t start,
-                          int64_t read_end, uint32_t w, uint64_t max_size, const L2Pol &pol, Emit &emit) {
+                          int64_t read_end, uint32_t w, uint64_t max_size, const L2Pol &pol, Emit &emit,
+                          int64_t *yield_at = nullptr) {
     constexpr bool MAX = (ALGO != ALGO_AE_MIN);
     constexpr uint32_t SAT = MAX ? 255u : 0u;  // a target nothing can beat
     constexpr int FAR = 1 << 30;
@@ -558,6 +568,9 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
         }
     }
 
+    if (yield_at) *yield_at = -1;
+    int sat_run = 0;        // consecutive saturated chunks (yield_at)
+    bool last_sat = false;  // the chunk ending at the next boundary is saturated
     // a boundary at e: returns true when the walk stops
     auto on_boundary = [&](int64_t e) -> bool {
         if (e >= Lf) {
@@ -565,6 +578,13 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
             return true;
         }
         if (emit.boundary(e)) return true;
+        if (yield_at) {
+            sat_run = last_sat ? sat_run + 1 : 0;
+            if (sat_run >= YIELD_SAT && e + (int64_t)w < Lf) {
+                *yield_at = e;  // the sparse walk continues with the chunk at e
+                return true;
+            }
+        }
         s = e;
         c = e;
         limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
@@ -629,6 +649,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                     cr = hi;
                     if (cr == hor) {
                         M = wsat ? 255u : warp_ext<true>(acc);
+                        last_sat = M == 255u;
                         scanning = true;
                         hor = FAR;
                     }
@@ -752,6 +773,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                 if (cr == hor && hor <= limr) er = hor;  // target unbeaten over its window
                 else if (cr == limr) er = limr;         // cap or end of stream
                 else break;                             // stage exhausted
+                last_sat = er == hor && ext == SAT;
                 ET_VAR(e3)
                 ET_BEGIN(e3);
                 if (event(er)) {
@@ -1074,17 +1096,24 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
 }
 
 // The walk of a chain from a chunk start: sparse while the chunks saturate,
-// then the TMA-ring walker from the first chunk the sparse walk cannot decide.
+// the TMA-ring walker from the first chunk the sparse walk cannot decide, and
+// back to the sparse walk after YIELD_SAT saturated chunks in a row.
 template <int ALGO, class Emit>
 __device__ __forceinline__ void walk_chain(bool sparse, const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf,
                                            int64_t start, int64_t read_end, uint32_t w, uint64_t max_size,
                                            const L2Pol &pol, Emit &emit) {
-    if (sparse) {
+    if (!sparse) {
+        run_chain<ALGO>(R, fbase, Lf, start, read_end, w, max_size, pol, emit);
+        return;
+    }
+    for (;;) {
         int64_t resume = start;
         if (sparse_chain<ALGO>(R, fbase, Lf, start, read_end, w, max_size, emit, resume)) return;
-        start = resume;
+        int64_t y = -1;
+        run_chain<ALGO>(R, fbase, Lf, resume, read_end, w, max_size, pol, emit, &y);
+        if (y < 0) return;
+        start = y;
     }
-    run_chain<ALGO>(R, fbase, Lf, start, read_end, w, max_size, pol, emit);
 }
 
 }  // namespace cdc

@@ -16,7 +16,8 @@ avg = int(os.environ.get("AVG", "4096"))
 seg = int(os.environ.get("SEG", "0"))
 kind = os.environ.get("DATA", "zipf")
 d = (synth.zipf_bytes(n, 1.1, 1) if kind == "zipf" else
-     synth.alternating(n, region=256 << 20, seed=5) if kind == "alt" else synth.uniform(n, 0))
+     synth.alternating(n, region=256 << 20, seed=5) if kind == "alt" else
+     synth.versioned(n, 0, seed=2)[0] if kind == "ver" else synth.uniform(n, 0))
 t = torch.from_numpy(d).cuda()
 p = cdc.params(algo, avg_size=avg, seg_bytes=seg)
 ws = torch.empty(cdc.workspace_size(p, 1, n, n), dtype=torch.uint8, device="cuda")
