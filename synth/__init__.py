@@ -40,6 +40,7 @@ import numpy as np
 __all__ = [
     "uniform",
     "zipf_bytes",
+    "patchwork",
     "versioned",
     "file_sizes",
     "many_files",
@@ -149,6 +150,38 @@ def saturation_edges(n: int, seed: int = 6, p: float = 1 / 700) -> np.ndarray:
         nxt = rng.random(n - 1) < 0.5
         out[1:][(out[:-1] == 255) & nxt] = 254
         out[1:][(out[:-1] == 0) & nxt] = 1
+    return out
+
+
+def patchwork(n: int, seed: int = 11, piece_lo: int = 2048, piece_hi: int = 65536) -> np.ndarray:
+    """Pieces of random lengths in [piece_lo, piece_hi) drawn from different
+    kinds of bytes: uniform, Zipf(1.1) with the seed-1 permutation (0xFF is its
+    rarest value), constant 0x00, constant 0xFF, uniform over 0..199 (no 0xFF),
+    uniform over 56..255 (no 0x00), and saturation edges.  Streams that are
+    saturated only in stretches, switching often (test data; no chunking logic)."""
+    rng = _rng(seed)
+    z = _Zipf(1.1, 1)
+    out = np.empty(n, dtype=np.uint8)
+    x = 0
+    while x < n:
+        m = min(n - x, int(rng.integers(piece_lo, piece_hi)))
+        k = int(rng.integers(0, 7))
+        if k == 0:
+            v = rng.integers(0, 256, m, dtype=np.uint8)
+        elif k == 1:
+            v = z.draw(rng, m)
+        elif k == 2:
+            v = np.zeros(m, dtype=np.uint8)
+        elif k == 3:
+            v = np.full(m, 255, dtype=np.uint8)
+        elif k == 4:
+            v = rng.integers(0, 200, m, dtype=np.uint8)
+        elif k == 5:
+            v = rng.integers(56, 256, m, dtype=np.uint8)
+        else:
+            v = saturation_edges(m, int(rng.integers(0, 1 << 30)), p=1 / 300)
+        out[x:x + m] = v
+        x += m
     return out
 
 
