@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcdc_b200.so")
 SOURCES = [os.path.join(CSRC, "cdc_kernels.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "cdc_device.cuh"), os.path.join(CSRC, "cdc_tables.cuh"),
-                  os.path.join(os.path.dirname(HERE), "include", "cdc_b200.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cuh")] + [
+    os.path.join(os.path.dirname(HERE), "include", "cdc_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

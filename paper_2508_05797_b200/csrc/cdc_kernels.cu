@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -134,6 +135,7 @@ struct Geometry {
     uint64_t max_size;
     int tmode;       // walkers may try transfer tables (single stream, one co-resident wave)
     int sparse;      // walkers start with the sparse walk (sparse_chain; long windows)
+    const uint32_t *gate;  // non-null: run only if *gate != 0 (the fallback behind the K-phase pipeline)
 };
 
 __device__ __forceinline__ void file_bounds(const Geometry &G, uint64_t f, uint64_t &off, uint64_t &len) {
@@ -394,8 +396,9 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 // K0': reset of the published-list region (list entries, publish, look-back
 // and ticket words) to all-ones; lets k_speculate launch early (PDL).
-__global__ void __launch_bounds__(256) k_reset(uint4 *p, uint64_t n16) {
+__global__ void __launch_bounds__(256) k_reset(uint4 *p, uint64_t n16, const uint32_t *gate) {
     pdl_trigger();
+    if (gate && *gate == 0) return;
     if (threadIdx.x == 0) stamp(TM_RESET_BEGIN);
     const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
@@ -553,6 +556,7 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) stamp(TM_SPEC_BEGIN);
     pdl_wait();  // the reset of the published lists has completed
+    if (G.gate && *G.gate == 0) return;  // the K-phase pipeline produced the output
     if (threadIdx.x == 0) {
         stamp(TM_SPEC_WAITED);
         s_ticket = atomicAdd(W.ctrl, 1u) + 1u;  // counter starts at ~0
@@ -1312,6 +1316,7 @@ __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_
     __shared__ uint32_t s_role;
     if (threadIdx.x == 0) stamp(TM_FIX_BEGIN);
     pdl_wait();  // k_speculate has completed and its writes are visible
+    if (G.gate && *G.gate == 0) return;  // the K-phase pipeline produced the output
     if (threadIdx.x == 0) stamp(TM_FIX_WAITED);
     const uint64_t nsegs = total_segs(G, W);
     if (G.file_off != nullptr && nsegs > 0 && W.ctrl[CT_BATCH_NORMAL] != 0u) {
@@ -1340,6 +1345,8 @@ __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_
     for (uint64_t g = (uint64_t)role * 32 + (threadIdx.x >> 5); g < nsegs; g += (uint64_t)gridDim.x * 32)
         write_segment(G, W, file_out, bounds, cap, g);
 }
+
+#include "cdc_kphase.cuh"  // K-phase speculation: single streams with long windows
 
 // ------------------------------------------------------------------ K0 batch segment table
 // Tiles of SP_THREADS x SP_RPT consecutive files, taken from a ticket by a
@@ -1709,12 +1716,13 @@ constexpr uint64_t T_MAX_SEG = CDC_T_MAX_SEG;
 #define CDC_SPARSE_MIN_W 4096
 #endif
 constexpr uint32_t SPARSE_MIN_W = CDC_SPARSE_MIN_W;
-int sparse_on(uint32_t w) {
+int sparse_on(uint32_t w, uint64_t max_size) {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("CDC_SPARSE");
         v = (e && e[0] == '0') ? 0 : 1;
     }
+    (void)max_size;
     return v && w >= SPARSE_MIN_W ? 1 : 0;
 }
 
@@ -1796,7 +1804,37 @@ struct Plan {
     uint64_t S, Hmax, max_segs, cap_list, cap_halo, pool_cap, exc_cap, nfiles, poolb_cap;
     size_t bytes, reset_bytes;
     size_t off[40];
+    // K-phase speculation (cdc_kphase.cuh): kK chains per segment (0 = off)
+    uint32_t kK, kG, kD, kcap;
+    uint64_t kS, kHk;
+    size_t koff[4], kreset_bytes;
 };
+
+// CDC_KPHASE in the environment: 0 disables K-phase speculation, 1..8 forces
+// that many chains per segment; by default 8 for windows of 12 KiB and more
+// (RAM / AE at 16 KiB), else 4.  CDC_KSEGS overrides its segment count.
+std::atomic<int> g_kphase{-2};  // cdc_set_kphase (-2: not read from the environment yet)
+int kphase_k(uint32_t w) {
+    int v = g_kphase.load();
+    if (v == -2) {
+        const char *e = getenv("CDC_KPHASE");
+        v = e ? atoi(e) : -1;
+        int expect = -2;
+        g_kphase.compare_exchange_strong(expect, v);
+        v = g_kphase.load();
+    }
+    if (v == 0) return 0;
+    if (v > 0) return std::min(v, cdc::KP_MAXK);
+    return w >= 12288 ? 8 : 4;
+}
+uint64_t kphase_segs() {
+    static long long v = -2;
+    if (v == -2) {
+        const char *e = getenv("CDC_KSEGS");
+        v = e ? atoll(e) : 0;
+    }
+    return v > 0 ? (uint64_t)v : 0;
+}
 
 uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
@@ -1893,8 +1931,76 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
         P.off[i] = o;
         o += round_up(sz[i], 256);
     }
-    P.bytes = o;
     P.reset_bytes = P.off[2];
+    // K-phase speculation: a single stream whose window takes the sparse walk,
+    // when the transfer tables are not tried (their segments are longer than
+    // T_MAX_SEG); same segments as the ordinary plan, K nodes each
+    P.kK = 0;
+    const int K = nfiles <= 1 ? kphase_k(p->window) : 0;
+    const bool tm = tmode_on() && p->window >= 4096 && S <= T_MAX_SEG;
+    if (K > 0 && total_len > 0 && sparse_on(p->window, p->max_size) && !tm) {
+        uint64_t Sk = S;
+        if (kphase_segs()) Sk = std::max<uint64_t>(round_up(total_len / kphase_segs(), 4096), 64 << 10);
+        uint64_t Gk = cdc::nseg_of(total_len, Sk);
+        if (Gk * K > cdc::KNODE_MAX) {
+            Sk = round_up(total_len / (cdc::KNODE_MAX / K) + 1, 4096);
+            Gk = cdc::nseg_of(total_len, Sk);
+        }
+        const uint64_t Hk = p->halo_bytes ? p->halo_bytes : 512 * w1;
+        const uint64_t body = (2 * Sk + 4096 + Gk + 1) / w1 + 2;  // (the same bound as cap_list)
+        const uint64_t capk = round_up(body + Hk / w1 + 4, 4);
+        if (Gk >= 8 && Gk * K <= cdc::KNODE_MAX && capk < 65536) {
+            const uint64_t N = Gk * K, NB = (Gk + cdc::KB - 1) / cdc::KB;
+            P.kK = (uint32_t)K;
+            P.kG = (uint32_t)Gk;
+            P.kS = Sk;
+            P.kHk = Hk;
+            P.kcap = (uint32_t)capk;
+            P.kD = std::max<uint32_t>(16u, ((p->window + 256u) / (uint32_t)K) & ~15u);
+            size_t ksz[] = {
+                N * capk * 4 + round_up(N * 4, 256) + 256,  // list, pub, ctrl } reset
+                N * 4 * 4,                                  // nxt, idx, bxi, bval
+                NB * 16,                                    // ent
+                256,                                        // gate
+            };
+            for (int i = 0; i < 4; ++i) {
+                P.koff[i] = o;
+                o += round_up(ksz[i], 256);
+            }
+            P.kreset_bytes = round_up(ksz[0], 256);
+        }
+    }
+    P.bytes = o;
+}
+
+cdc::KGeo kgeo(const cdc_params *p, const Plan &P, const uint8_t *data, uint64_t len) {
+    cdc::KGeo Q;
+    Q.data = data;
+    Q.L = len;
+    Q.G = P.kG;
+    Q.K = P.kK;
+    Q.D = P.kD;
+    Q.capk = P.kcap;
+    Q.w = p->window;
+    Q.max_size = p->max_size;
+    Q.Hk = P.kHk;
+    Q.sparse = sparse_on(p->window, p->max_size);
+    return Q;
+}
+cdc::KWork kcarve(const Plan &P, void *ws) {
+    uint8_t *b = static_cast<uint8_t *>(ws);
+    const uint64_t N = (uint64_t)P.kG * P.kK;
+    cdc::KWork K;
+    K.list = reinterpret_cast<uint32_t *>(b + P.koff[0]);
+    K.pub = K.list + N * P.kcap;
+    K.ctrl = reinterpret_cast<uint32_t *>(b + P.koff[0] + N * P.kcap * 4 + round_up(N * 4, 256));
+    K.nxt = reinterpret_cast<uint32_t *>(b + P.koff[1]);
+    K.idx = K.nxt + N;
+    K.bxi = K.idx + N;
+    K.bval = reinterpret_cast<int32_t *>(K.bxi + N);
+    K.ent = reinterpret_cast<uint64_t *>(b + P.koff[2]);
+    K.gate = reinterpret_cast<uint32_t *>(b + P.koff[3]);
+    return K;
 }
 
 cdc::Work carve(const Plan &P, void *ws) {
@@ -1965,6 +2071,9 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
                                       spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_fixup<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       cdc::FIX_SMEM));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_kspec<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, spec_smem));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_kres2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(cdc::KNODE_MAX * 8)));
         attr_set[dev] = true;
     }
     int launches = 0;
@@ -1976,12 +2085,40 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         }
     };
     mark(0);
+    if (P.kK) {
+        // K-phase speculation (cdc_kphase.cuh); the ordinary pipeline behind it
+        // runs only if its gate opens (a halo on the true chain gave up)
+        const cdc::KGeo Q = kgeo(p, P, G.data, total_len);
+        const cdc::KWork KW = kcarve(P, W.list);
+        const uint64_t N = (uint64_t)Q.G * Q.K, NB = (Q.G + cdc::KB - 1) / cdc::KB;
+        const uint64_t n16 = P.kreset_bytes / 16;
+        const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());
+        cdc::k_reset<<<rb ? rb : 1, 256, 0, st>>>(reinterpret_cast<uint4 *>(KW.list), n16, nullptr);
+        CDC_KCHECK("k_reset (K-phase)", st);
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kspec<ALGO>),
+                            dim3((unsigned)std::min<uint64_t>((N + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS,
+                                                              (uint64_t)num_sms())),
+                            dim3(cdc::SPEC_WARPS * 32), (size_t)spec_smem, st, Q, KW));
+        CDC_KCHECK("k_kspec", st);
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres1),
+                            dim3((unsigned)((NB + cdc::KRES1_WARPS - 1) / cdc::KRES1_WARPS)),
+                            dim3(cdc::KRES1_WARPS * 32), 0, st, Q, KW));
+        CDC_KCHECK("k_kres1", st);
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres2), dim3(1), dim3(1024), (size_t)(N * 8), st,
+                            Q, KW, d_count));
+        CDC_KCHECK("k_kres2", st);
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres3), dim3((unsigned)((NB + 7) / 8)), dim3(256), 0,
+                            st, Q, KW, d_bounds, cap));
+        CDC_KCHECK("k_kres3", st);
+        launches += 5;
+        G.gate = KW.gate;
+    }
     // reset the published lists (list entries -> LIST_EMPTY, pub -> PUB_OPEN) and
     // the look-back, ticket and flag words
     {
         const uint64_t n16 = P.reset_bytes / 16;  // reset_bytes is a multiple of 256
         const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());
-        cdc::k_reset<<<rb ? rb : 1, 256, 0, st>>>(reinterpret_cast<uint4 *>(W.list), n16);
+        cdc::k_reset<<<rb ? rb : 1, 256, 0, st>>>(reinterpret_cast<uint4 *>(W.list), n16, G.gate);
         CDC_KCHECK("k_reset", st);
     }
     ++launches;
@@ -2079,7 +2216,8 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     G.w = p->window;
     G.max_size = p->max_size;
     G.tmode = 0;
-    G.sparse = sparse_on(p->window);
+    G.sparse = sparse_on(p->window, p->max_size);
+    G.gate = nullptr;
     uint64_t *file_out = batch ? d_bound_off : W.file_out;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (p->algo) {
@@ -2143,6 +2281,16 @@ const char *cdc_last_error(void) { return g_err.c_str(); }
 
 int cdc_last_launch_count(void) { return g_launches; }
 
+int cdc_set_kphase(int k) {
+    if (k < -1 || k > cdc::KP_MAXK) return fail(CDC_ERR_INVALID, "k must be -1 (default), 0 (off) or 1..8");
+    if (k == -1) {
+        const char *e = getenv("CDC_KPHASE");
+        k = e ? atoi(e) : -1;
+    }
+    g_kphase.store(k);
+    return CDC_OK;
+}
+
 // diagnostic (CDC_EVTIME builds): read and reset the 16 cycle buckets
 extern "C" int cdc_debug_evtime(unsigned long long *out) {
     CDC_CUDA(cudaMemcpyFromSymbol(out, cdc::g_evt, 16 * sizeof(unsigned long long)));
@@ -2194,6 +2342,35 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
     make_plan(p, nfiles ? nfiles : 1, total_len, max_len, P);
     cdc::Work W = carve(P, const_cast<void *>(d_workspace));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (P.kK && nfiles <= 1) {  // K-phase: node statistics unless the gate sent the call to the ordinary pipeline
+        const cdc::KWork KW = kcarve(P, const_cast<void *>(d_workspace));
+        uint32_t gate = 1;
+        CDC_CUDA(cudaMemcpyAsync(&gate, KW.gate, 4, cudaMemcpyDeviceToHost, st));
+        CDC_CUDA(cudaStreamSynchronize(st));
+        if (gate == 0) {
+            const uint64_t N = (uint64_t)P.kG * P.kK;
+            std::vector<uint32_t> nx(N), cn(N);
+            CDC_CUDA(cudaMemcpyAsync(nx.data(), KW.nxt, N * 4, cudaMemcpyDeviceToHost, st));
+            CDC_CUDA(cudaMemcpyAsync(cn.data(), KW.pub, N * 4, cudaMemcpyDeviceToHost, st));
+            CDC_CUDA(cudaStreamSynchronize(st));
+            uint64_t met = 0, uns = 0, other = 0, walked = 0;
+            for (uint64_t v = 0; v < N; ++v) {
+                if (nx[v] < cdc::KN_VOID) ++met;
+                else if (nx[v] == cdc::KN_UNSYNC) ++uns;
+                else ++other;
+                walked += cn[v];
+            }
+            stats[0] = P.kG;
+            stats[1] = P.kS;
+            stats[2] = P.kHk;
+            stats[3] = 3;  // resolved by K-phase speculation (stats[4..6] count nodes)
+            stats[4] = met;
+            stats[5] = uns;
+            stats[6] = other;
+            stats[7] = walked;
+            return CDC_OK;
+        }
+    }
     uint64_t G = 0;
     if (nfiles <= 1 && P.S) G = max_len == 0 ? 0 : (max_len < P.S ? 1 : max_len / P.S);
     if (nfiles > 1) CDC_CUDA(cudaMemcpyAsync(&G, W.seg_first + nfiles, 8, cudaMemcpyDeviceToHost, st));
@@ -2485,15 +2662,15 @@ int cdc_chain(const cdc_params *p, const uint8_t *d_data, uint64_t len, uint64_t
     switch (p->algo) {
     case CDC_RAM:
         cdc::k_chain<0><<<1, 32, cdc::RING_SMEM + 128, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
-                                                       starts_cap, d_count, sparse_on(p->window));
+                                                       starts_cap, d_count, sparse_on(p->window, p->max_size));
         break;
     case CDC_AE_MAX:
         cdc::k_chain<1><<<1, 32, cdc::RING_SMEM + 128, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
-                                                       starts_cap, d_count, sparse_on(p->window));
+                                                       starts_cap, d_count, sparse_on(p->window, p->max_size));
         break;
     default:
         cdc::k_chain<2><<<1, 32, cdc::RING_SMEM + 128, st>>>(d_data, len, start, stop, p->window, p->max_size, d_starts,
-                                                       starts_cap, d_count, sparse_on(p->window));
+                                                       starts_cap, d_count, sparse_on(p->window, p->max_size));
     }
     g_launches = 1;
     CDC_CUDA(cudaGetLastError());
