@@ -294,7 +294,7 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
  * tables is chunked with k chains per segment, started k-th of a chunk length
  * apart, so that a chain entering a segment meets one of them within a few
  * chunks (the boundaries are the same; only the work differs).  k = -1
- * restores the default (8 chains for windows >= 12 KiB, else 4, or the
+ * restores the default (4 chains for RAM with windows >= 12 KiB, else 2, or the
  * CDC_KPHASE environment variable), 0 disables it, 1..8 forces k.  Process-
  * wide; it changes cdc_workspace_size's result, so set it before sizing a
  * workspace.  Returns CDC_ERR_INVALID for other values.

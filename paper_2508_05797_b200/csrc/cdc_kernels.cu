@@ -1811,10 +1811,11 @@ struct Plan {
 };
 
 // CDC_KPHASE in the environment: 0 disables K-phase speculation, 1..8 forces
-// that many chains per segment; by default 8 for windows of 12 KiB and more
-// (RAM / AE at 16 KiB), else 4.  CDC_KSEGS overrides its segment count.
+// that many chains per segment; by default 4 for RAM with windows of 12 KiB and
+// more (RAM at 16 KiB), else 2 (measured on configs[2]'s 1 GiB base, DESIGN.md
+// §6).  CDC_KSEGS overrides its segment count.
 std::atomic<int> g_kphase{-2};  // cdc_set_kphase (-2: not read from the environment yet)
-int kphase_k(uint32_t w) {
+int kphase_k(int algo, uint32_t w) {
     int v = g_kphase.load();
     if (v == -2) {
         const char *e = getenv("CDC_KPHASE");
@@ -1825,7 +1826,7 @@ int kphase_k(uint32_t w) {
     }
     if (v == 0) return 0;
     if (v > 0) return std::min(v, cdc::KP_MAXK);
-    return w >= 12288 ? 8 : 4;
+    return (algo == CDC_RAM && w >= 12288) ? 4 : 2;
 }
 uint64_t kphase_segs() {
     static long long v = -2;
@@ -1934,11 +1935,17 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     P.reset_bytes = P.off[2];
     // K-phase speculation: a single stream whose window takes the sparse walk,
     // when the transfer tables are not tried (their segments are longer than
-    // T_MAX_SEG); same segments as the ordinary plan, K nodes each
+    // T_MAX_SEG) and the segments are short next to the distance at which
+    // chains started at random offsets meet on saturated bytes (mean ~600 KB
+    // at RAM 8 KiB, ~2 MB at 16 KiB: configs[2]); longer segments amortise
+    // their halos (configs[4]'s 8 GiB per GPU: 3.6 MB segments, where K
+    // chains would only multiply the body walks).  Same segments as the
+    // ordinary plan, K nodes each.
     P.kK = 0;
-    const int K = nfiles <= 1 ? kphase_k(p->window) : 0;
+    const int K = nfiles <= 1 ? kphase_k(p->algo, p->window) : 0;
     const bool tm = tmode_on() && p->window >= 4096 && S <= T_MAX_SEG;
-    if (K > 0 && total_len > 0 && sparse_on(p->window, p->max_size) && !tm) {
+    const uint64_t kmax_seg = kphase_segs() ? ~0ull : (p->window >= 12288 ? 4ull << 20 : 1ull << 20);
+    if (K > 0 && total_len > 0 && sparse_on(p->window, p->max_size) && !tm && S <= kmax_seg) {
         uint64_t Sk = S;
         if (kphase_segs()) Sk = std::max<uint64_t>(round_up(total_len / kphase_segs(), 4096), 64 << 10);
         uint64_t Gk = cdc::nseg_of(total_len, Sk);
@@ -1946,7 +1953,7 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
             Sk = round_up(total_len / (cdc::KNODE_MAX / K) + 1, 4096);
             Gk = cdc::nseg_of(total_len, Sk);
         }
-        const uint64_t Hk = p->halo_bytes ? p->halo_bytes : 512 * w1;
+        const uint64_t Hk = p->halo_bytes ? p->halo_bytes : 1024 * w1;
         const uint64_t body = (2 * Sk + 4096 + Gk + 1) / w1 + 2;  // (the same bound as cap_list)
         const uint64_t capk = round_up(body + Hk / w1 + 4, 4);
         if (Gk >= 8 && Gk * K <= cdc::KNODE_MAX && capk < 65536) {
