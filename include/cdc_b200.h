@@ -289,6 +289,18 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
               const void *d_workspace, uint64_t *stats, void *stream);
 
 /*
+ * Bytes that k_speculate's walkers copied from global memory into their
+ * shared-memory rings during the last call that used d_workspace (ring
+ * stages of the TMA walker plus the sparse walk's regions; DESIGN.md §5's
+ * per-unit figure), into *out.  This is what bench.py's roofline divides by
+ * the kernel time.  Synchronises `stream`.  Arguments as for cdc_stats.
+ * Transfer-table index passes, K-phase walkers and k_fixup's walkers are not
+ * counted.
+ */
+int cdc_fetched(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len,
+                const void *d_workspace, uint64_t *out, void *stream);
+
+/*
  * K-phase speculation: a single stream whose window takes the
  * sparse walk (w >= 4096) and whose segments are too long for the transfer
  * tables is chunked with k chains per segment, started k-th of a chunk length

@@ -21,7 +21,7 @@ __all__ = [
     "CdcError", "ALGOS", "params", "window_for_avg", "max_boundaries", "workspace_size",
     "chunk_async", "chunk", "chunk_batch", "chunk_batch_async", "chunk_host", "chain",
     "extreme_byte_search", "range_scan", "first_common", "last_launch_count", "abi_version",
-    "profile_enable", "profile_collect", "KERNELS", "stats", "plan_info", "segment_starts",
+    "profile_enable", "profile_collect", "KERNELS", "stats", "fetched", "plan_info", "segment_starts",
     "chunk_batch_host", "set_kphase",
 ]
 
@@ -50,6 +50,14 @@ def stats(p: cdc_params, workspace: torch.Tensor, nfiles: int, total_len: int, m
     check(lib.cdc_stats(ctypes.byref(p), nfiles, total_len, max_len, workspace.data_ptr(), out, _stream_ptr(stream)))
     keys = ["segments", "seg_bytes", "halo_cap", "fast_path", "synced", "unsynced", "skipped_or_end", "halo_chunks"]
     return {k: int(out[i]) for i, k in enumerate(keys)}
+
+
+def fetched(p: cdc_params, workspace: torch.Tensor, nfiles: int, total_len: int, max_len: int, stream=None) -> int:
+    """Bytes k_speculate's walkers copied from global memory in the last call on `workspace` (synchronises)."""
+    out = ctypes.c_uint64()
+    check(lib.cdc_fetched(ctypes.byref(p), nfiles, total_len, max_len, workspace.data_ptr(), ctypes.byref(out),
+                          _stream_ptr(stream)))
+    return int(out.value)
 
 
 def plan_info(p: cdc_params, nfiles: int, total_len: int, max_len: int) -> dict:

@@ -38,6 +38,19 @@ constexpr int STAGE = CDC_STAGE;       // bytes per TMA stage (12 warp blocks)
 constexpr int NST = CDC_NST;           // ring depth per warp (12 KiB)
 constexpr int RING_BYTES = STAGE * NST;
 constexpr int RING_SMEM = (RING_BYTES + NST * 8 + 127) / 128 * 128;  // keeps every ring 128-byte aligned
+// R.bar[FETCH_SLOT]: bytes this warp's bulk copies fetched (ring stages and
+// sparse-walk regions), flushed into the workspace by k_speculate (cdc_fetched)
+constexpr int FETCH_SLOT = 4;
+static_assert(RING_BYTES + 8 * (FETCH_SLOT + 1) <= RING_SMEM, "fetch counter after the ring's mbarriers");
+// A ring of NST stages of STG bytes (the default is STAGE; the batch kernel
+// uses a smaller one so that more walkers fit an SM): its bytes and its
+// shared-memory stride (bytes + mbarriers + fetch counter, 128-byte aligned).
+template <int STG>
+struct Ring {
+    static constexpr int BYTES = STG * NST;
+    static constexpr int SMEM = (BYTES + 8 * (FETCH_SLOT + 1) + 127) / 128 * 128;
+};
+static_assert(Ring<STAGE>::SMEM == RING_SMEM, "default ring stride");
 
 enum { ALGO_RAM = 0, ALGO_AE_MAX = 1, ALGO_AE_MIN = 2 };
 enum { CMP_GT = 0, CMP_GEQ = 1, CMP_LT = 2, CMP_LEQ = 3, CMP_EQ = 4 };
@@ -506,7 +519,7 @@ __device__ __forceinline__ uint32_t sat_mask16(const uint4 &v) {
 // three tight loops: the RAM window's Extreme Byte Search (stage_window_max), a
 // block-level Range Scan for the next event (stage_find_block), or -- for an
 // AE target no byte can beat -- a direct jump to its deadline.
-template <int ALGO, class Emit>
+template <int ALGO, int STG = STAGE, class Emit>
 __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf, int64_t start,
                           int64_t read_end, uint32_t w, uint64_t max_size, const L2Pol &pol, Emit &emit,
                           int64_t *yield_at = nullptr) {
@@ -520,7 +533,7 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
                                                           ~static_cast<uintptr_t>(15));
     const int64_t B0 = g0 - fbase;
     const int64_t nbytes = ((read_end - B0) + 15) & ~static_cast<int64_t>(15);
-    const int64_t nstages = (nbytes + STAGE - 1) / STAGE;
+    const int64_t nstages = (nbytes + STG - 1) / STG;
 
     if (lane == 0) {
         for (int i = 0; i < NST; ++i) mbar_init(&R.bar[i], 1);
@@ -531,11 +544,11 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     int64_t issued = 0;
     auto issue = [&](int64_t k, int slot) {
         // operands computed by every lane (uniform, no divergent region); one elected lane issues
-        const int64_t off = k * STAGE;
-        const uint32_t bytes = (uint32_t)(nbytes - off < STAGE ? nbytes - off : STAGE);
+        const int64_t off = k * STG;
+        const uint32_t bytes = (uint32_t)(nbytes - off < STG ? nbytes - off : STG);
         const uint64_t policy = B0 + off < pol.keep_until ? pol.keep : pol.stream;
         uint64_t *bar = &R.bar[slot];
-        uint8_t *dst = R.buf + slot * STAGE;
+        uint8_t *dst = R.buf + slot * STG;
         const uint8_t *src = g0 + off;
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -609,14 +622,14 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
     ET_BEGIN(et_t1);
     for (; k < nstages && !stop; ++k) {
         CNT(0);
-        const int64_t SB = B0 + k * STAGE;
+        const int64_t SB = B0 + k * STG;
         mbar_wait(&R.bar[slot], parity);
-        const uint8_t *sp = R.buf + slot * STAGE;
+        const uint8_t *sp = R.buf + slot * STG;
         auto rel = [&](int64_t x) -> int {  // x >= SB
             const int64_t d = x - SB;
             return d > FAR ? FAR : (int)d;
         };
-        const int endr = rel(read_end) < STAGE ? rel(read_end) : STAGE;
+        const int endr = rel(read_end) < STG ? rel(read_end) : STG;
         int cr = (int)(c - SB);
         int limr = rel(limit);
         // RAM: window end s+w while not scanning; AE: target deadline t+w+1
@@ -810,8 +823,10 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
         }
     }
     __syncwarp();
-    if (lane == 0)
+    if (lane == 0) {
         for (int i = 0; i < NST; ++i) mbar_inval(&R.bar[i]);  // the ring may be re-initialised by the caller
+        R.bar[FETCH_SLOT] += (uint64_t)(issued * STG < nbytes ? issued * STG : nbytes);
+    }
     __syncwarp();
 }
 
@@ -844,8 +859,11 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
 #define CDC_SP_SPEC 2048
 #endif
 constexpr int SP_SPEC = CDC_SP_SPEC;  // bytes per speculative or continuation copy (multiple of 16, <= SP_SLOT)
-constexpr int SP_SLOT = 4096;         // slot stride in the ring: slots 0/1 alternate per chunk, slot 2 continues
-static_assert(RING_BYTES >= 3 * SP_SLOT, "sparse walk needs three slots in the ring");
+#ifndef CDC_SP_SLOT
+#define CDC_SP_SLOT 2048
+#endif
+constexpr int SP_SLOT = CDC_SP_SLOT;  // slot stride in the ring: slots 0/1 alternate per chunk, slot 2 continues
+static_assert(Ring<3072>::BYTES >= 3 * SP_SLOT, "sparse walk needs three slots in every ring (stages of >= 3 KiB)");
 static_assert(SP_SPEC % 16 == 0 && SP_SPEC <= SP_SLOT, "SP_SPEC");
 
 // First saturating byte in [lo, hi) among the slot's bytes [P, P + n) (file
@@ -854,7 +872,7 @@ static_assert(SP_SPEC % 16 == 0 && SP_SPEC <= SP_SLOT, "SP_SPEC");
 // (more: set when the same block holds another such byte in (result, hi))
 template <bool MAX>
 __device__ __forceinline__ int64_t sm_first(const uint8_t *sp, int64_t P, int n, int64_t lo, int64_t hi,
-                                            bool *more = nullptr) {
+                                                  bool *more = nullptr) {
     if (lo < P) lo = P;
     if (hi > P + n) hi = P + n;
     if (lo >= hi) return -1;
@@ -937,6 +955,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
     }
     __syncwarp();
     uint32_t pend = 0, par = 0;  // per slot: copy in flight; parity of its next completion
+    uint32_t fetched = 0;        // bytes copied by this call (flushed into R.bar[FETCH_SLOT] at the end)
     // copy of the bytes from x (rounded down to 16 B, at most nb bytes, not past the
     // granule holding byte Lf - 1) into slot `slot`; P, N: the region's start and size
     auto issue = [&](int slot, int64_t x, int nb, int64_t &P, int &N) {
@@ -945,6 +964,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
         N = (int)(avail < (int64_t)nb ? (avail > 0 ? avail : 0) : (int64_t)nb);
         if (N > 0) {
             uint64_t *bar = &R.bar[slot];
+            fetched += (uint32_t)N;
             asm volatile(
                 "{\n\t.reg .pred p;\n\t"
                 "elect.sync _|p, 0xffffffff;\n\t"
@@ -970,8 +990,10 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
         wait(1);
         wait(2);
         __syncwarp();
-        if (lane == 0)
+        if (lane == 0) {
             for (int i = 0; i < 3; ++i) mbar_inval(&R.bar[i]);
+            R.bar[FETCH_SLOT] += fetched;
+        }
         __syncwarp();
         return r;
     };
@@ -1098,19 +1120,19 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
 // The walk of a chain from a chunk start: sparse while the chunks saturate,
 // the TMA-ring walker from the first chunk the sparse walk cannot decide, and
 // back to the sparse walk after YIELD_SAT saturated chunks in a row.
-template <int ALGO, class Emit>
+template <int ALGO, int STG = STAGE, class Emit>
 __device__ __forceinline__ void walk_chain(bool sparse, const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf,
                                            int64_t start, int64_t read_end, uint32_t w, uint64_t max_size,
                                            const L2Pol &pol, Emit &emit) {
     if (!sparse) {
-        run_chain<ALGO>(R, fbase, Lf, start, read_end, w, max_size, pol, emit);
+        run_chain<ALGO, STG>(R, fbase, Lf, start, read_end, w, max_size, pol, emit);
         return;
     }
     for (;;) {
         int64_t resume = start;
         if (sparse_chain<ALGO>(R, fbase, Lf, start, read_end, w, max_size, emit, resume)) return;
         int64_t y = -1;
-        run_chain<ALGO>(R, fbase, Lf, resume, read_end, w, max_size, pol, emit, &y);
+        run_chain<ALGO, STG>(R, fbase, Lf, resume, read_end, w, max_size, pol, emit, &y);
         if (y < 0) return;
         start = y;
     }

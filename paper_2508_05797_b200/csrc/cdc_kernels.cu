@@ -41,11 +41,27 @@ constexpr int SPEC_WARPS = CDC_SPEC_WARPS;  // warps (segments) per CTA in k_spe
 #define CDC_SPEC_CTAS_PER_SM 1
 #endif
 constexpr int SPEC_CTAS_PER_SM = CDC_SPEC_CTAS_PER_SM;  // resident k_speculate CTAs per SM (smem-bound)
+// The batch kernel's walkers (mostly the sparse walk, whose chunks are bound by
+// per-warp latency): 20 warps per SM with 2 x 5 KiB rings (96 registers)
+// instead of 16 with 2 x 6 KiB (configs[3] 1.65 -> 1.54 ms; a single stream's
+// ring walker is faster with the larger rings: configs[1] 0.0654 vs 0.0715 ms)
+#ifndef CDC_BATCH_WARPS
+#define CDC_BATCH_WARPS 20
+#endif
+#ifndef CDC_BATCH_STAGE
+#define CDC_BATCH_STAGE 5120
+#endif
+constexpr int BATCH_WARPS = CDC_BATCH_WARPS;
+constexpr int BATCH_STAGE = CDC_BATCH_STAGE;
+static_assert(BATCH_WARPS * Ring<BATCH_STAGE>::SMEM + 128 <= 227 * 1024, "batch rings exceed shared memory");
 #ifndef CDC_HEAD_KEEP
 #define CDC_HEAD_KEEP 12288
 #endif
 constexpr int HEAD_KEEP = CDC_HEAD_KEEP;  // bytes of each segment head kept in L2 for the halo re-read
 constexpr int RESOLVE_THREADS = 1024;
+#ifndef CDC_PUB_RELEASE
+#define CDC_PUB_RELEASE 0  // 1: publish a list's final count with a release store (A/B)
+#endif
 
 // ------------------------------------------------------------------ workspace
 struct Work {
@@ -56,6 +72,7 @@ struct Work {
     unsigned long long *pub;     // PUB_OPEN, or the final list length
     unsigned long long *status;  // look-back words (ST_* flag | 62-bit signed value), reset to ~0
     uint32_t *ctrl;              // [0] CTA ticket counter, [1] fast path valid (~0) / failed (0); reset to ~0
+    unsigned long long *fetched; // bytes k_speculate's walkers copied from global memory, minus one (reset to ~0)
     unsigned long long *grp;     // look-back group sums (reset to ~0)
     uint32_t *tblk;              // T-mode: per block of 32 segments, tables published (reset to ~0)
     int32_t *sj;                 // sync target segment, or SJ_* code
@@ -344,7 +361,11 @@ struct SpecEmit {
     __device__ void publish() {
         if (!published) {
             if (lane_id() == 0) {
-                st_release_u64(pub, (unsigned long long)cnt);
+                // relaxed: a reader that sees the final count but not yet an
+                // entry below it reads the entry as undecided and keeps walking
+                // (ListProbe::probe returns -1), so no fence is needed
+                if (CDC_PUB_RELEASE) st_release_u64(pub, (unsigned long long)cnt);
+                else asm volatile("st.relaxed.gpu.u64 [%0], %1;" ::"l"(pub), "l"((unsigned long long)cnt) : "memory");
                 if (tbody) *tbody = globaltimer();
             }
             published = true;
@@ -534,7 +555,7 @@ template <int ALGO>
 __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_count, uint64_t *file_out,
                                                 uint64_t *bounds, uint64_t cap);
 
-template <int ALGO, bool TM>
+template <int ALGO, bool TM, int STG, bool FUSE>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
                                   uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused,
                                   int64_t pre_n = -1);
@@ -547,8 +568,10 @@ __device__ int64_t t_coop_index(const Geometry &G, Work &W, uint64_t g, uint8_t 
 // behind it with PDL) only checks that it did.
 // TM: the variant that tries the transfer tables (saturated streams); the
 // other one carries none of their code, so the common path keeps its registers.
-template <int ALGO, bool TM>
-__global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate(Geometry G, Work W, uint64_t *bounds,
+// NW warps per CTA with rings of 2 x STG bytes; FUSE: carries the fused
+// look-back and write (the batch instance: BATCH_WARPS, BATCH_STAGE, no fused write).
+template <int ALGO, bool TM, int NW = SPEC_WARPS, int STG = STAGE, bool FUSE = true>
+__global__ void __launch_bounds__(NW * 32, SPEC_CTAS_PER_SM) k_speculate(Geometry G, Work W, uint64_t *bounds,
                                                                   uint64_t cap, uint64_t *d_count, int fused,
                                                                   int spw) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -596,23 +619,29 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, SPEC_CTAS_PER_SM) k_speculate
         }
     }
     if (spw != 0 && warp >= spw) return;
+    constexpr int RS = Ring<STG>::SMEM;
+    uint64_t *fetch = reinterpret_cast<uint64_t *>(align_smem(smem) + warp * RS + Ring<STG>::BYTES) + FETCH_SLOT;
+    if (lane_id() == 0) *fetch = 0;
     while (g < nsegs) {  // one call site, so the walker is inlined once
-        speculate_segment<ALGO, TM>(G, W, g, nsegs, align_smem(smem) + warp * RING_SMEM, bounds, cap, d_count, fused,
-                                    pre_n);
+        speculate_segment<ALGO, TM, STG, FUSE>(G, W, g, nsegs, align_smem(smem) + warp * RS, bounds, cap, d_count,
+                                               FUSE ? fused : 0, pre_n);
         if (spw != 0) break;
         g = next_seg();
     }
+    if (lane_id() == 0 && *fetch) atomicAdd(W.fetched, (unsigned long long)*fetch);
     if (lane_id() == 0) stamp(TM_SPEC_END);
 }
 
 #include "cdc_tables.cuh"  // T-mode: transfer tables for saturated streams
 
-template <int ALGO, bool TM>
+template <int ALGO, bool TM, int STG, bool FUSE>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
                                   uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused,
                                   int64_t pre_n) {
+    if constexpr (!FUSE) fused = 0;
     const int lane = lane_id();
-    WarpRing R{wbase, reinterpret_cast<uint64_t *>(wbase + RING_BYTES)};
+    static_assert(!TM || STG == STAGE, "the transfer tables use the default ring");
+    WarpRing R{wbase, reinterpret_cast<uint64_t *>(wbase + Ring<STG>::BYTES)};
 
     SpecEmit em;
     em.G = &G;
@@ -647,7 +676,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
                                         : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
     // the segment's head is read again by the previous segment's halo walk: keep it in L2
     const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
-    walk_chain<ALGO>(G.sparse != 0, R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
+    walk_chain<ALGO, STG>(G.sparse != 0, R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
     em.publish();
     if (tm && lane == 0) {
         tm[TM_PER_SEG * g + 2] = globaltimer();
@@ -675,7 +704,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
     // global round trip (falls back to the global lists when they do not fit)
     uint32_t *stg = reinterpret_cast<uint32_t *>(wbase);
     const uint32_t nst = em.cnt + tail;
-    const bool staged = nst <= (uint32_t)(RING_BYTES / 4);
+    const bool staged = nst <= (uint32_t)(Ring<STG>::BYTES / 4);
     if (fused && normal && staged) {
         const uint32_t hoff = (uint32_t)(em.I.seg_end - em.I.p);
         for (uint32_t i = lane; i < nst; i += 32)
@@ -1844,12 +1873,13 @@ uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 // TMA stage, at least 64 KiB and 4 max-size chunks, so that the
 // re-synchronisation halo (a few chunks on typical data) is small next to it.
 constexpr uint64_t SEGS_PER_SM = (uint64_t)cdc::SPEC_WARPS * cdc::SPEC_CTAS_PER_SM;
+constexpr uint64_t BATCH_SEGS_PER_SM = (uint64_t)cdc::BATCH_WARPS * cdc::SPEC_CTAS_PER_SM;
 constexpr uint64_t FIX_BLOCKS = 16;  // k_fixup grid cap
 
 void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, Plan &P) {
     uint64_t S = p->seg_bytes;
     if (!S) {
-        const uint64_t target = (uint64_t)num_sms() * SEGS_PER_SM;
+        const uint64_t target = (uint64_t)num_sms() * (nfiles > 1 ? BATCH_SEGS_PER_SM : SEGS_PER_SM);
         // floor(len / target): floor(len / S) = target segments of ~equal length
         S = total_len / target;
         // a batch: segments are taken largest first (LptLists), so only a file
@@ -1890,7 +1920,7 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     const uint64_t list_entries = nfiles > 1 ? total_len / w1 + 2 * G + 2 : G * P.cap_list;
     size_t sz[] = {
         list_entries * 4,    // 0 list   } reset to 0xFF by k_reset at every call
-        G * 20 + 64 + (G / 32 + 1) * 12,  // 1 pub, status, ctrl, grp, tblk, tnx }
+        G * 20 + 72 + (G / 32 + 1) * 12,  // 1 pub, status, ctrl, fetched, grp, tblk, tnx }
         G * P.cap_halo * 4,  // 2 halo
         G * 4,               // 3 cnt
         G * 4,               // 4 hcnt
@@ -2017,7 +2047,8 @@ cdc::Work carve(const Plan &P, void *ws) {
     W.pub = (unsigned long long *)(b + P.off[1]);
     W.status = W.pub + P.max_segs;
     W.ctrl = reinterpret_cast<uint32_t *>(W.status + P.max_segs);
-    W.grp = W.status + P.max_segs + 8;
+    W.fetched = W.status + P.max_segs + 8;
+    W.grp = W.status + P.max_segs + 9;
     W.tblk = reinterpret_cast<uint32_t *>(W.grp + P.max_segs / 32 + 1);
     W.tnx = W.tblk + P.max_segs / 32 + 1;
     W.halo = (uint32_t *)(b + P.off[2]);
@@ -2070,8 +2101,11 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
                     uint64_t total_len) {
     static bool attr_set[MAX_DEVICES] = {false};  // per device: the opt-in is a per-context attribute
     const int spec_smem = cdc::SPEC_WARPS * cdc::RING_SMEM + 128;
+    const int batch_smem = cdc::BATCH_WARPS * cdc::Ring<cdc::BATCH_STAGE>::SMEM + 128;
     const int dev = current_device();
     if (!attr_set[dev]) {
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO, false, cdc::BATCH_WARPS, cdc::BATCH_STAGE, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, batch_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2152,7 +2186,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     // ticket, which balances files of very different sizes)
     const int spw = batch ? 0
                           : (int)std::min<uint64_t>(std::max<uint64_t>((nseg_ub + nsm - 1) / nsm, 1), cdc::SPEC_WARPS);
-    const uint64_t blocks = batch ? std::min<uint64_t>((nseg_ub + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS,
+    const uint64_t blocks = batch ? std::min<uint64_t>((nseg_ub + cdc::BATCH_WARPS - 1) / cdc::BATCH_WARPS,
                                                        nsm * cdc::SPEC_CTAS_PER_SM)
                                   : (nseg_ub + spw - 1) / spw;
     // transfer tables: a single stream of at least two segments, windows long
@@ -2166,11 +2200,12 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         // dynamic tickets (a batch) the waits would queue behind the largest file,
         // so a batch leaves the splice and the writes to k_fixup
         int fused = (!batch && P.cap_list + P.cap_halo < (1u << 23)) ? fused_mode() : 0;
-        const void *kspec = G.tmode ? reinterpret_cast<const void *>(cdc::k_speculate<ALGO, true>)
-                                    : reinterpret_cast<const void *>(cdc::k_speculate<ALGO, false>);
-        CDC_CUDA(launch_pdl(kspec, dim3((unsigned)blocks),
-                            dim3(cdc::SPEC_WARPS * 32), (size_t)spec_smem, st, G, W, d_bounds, cap, d_count, fused,
-                            spw));
+        const void *kspec =
+            batch ? reinterpret_cast<const void *>(cdc::k_speculate<ALGO, false, cdc::BATCH_WARPS, cdc::BATCH_STAGE, false>)
+            : G.tmode ? reinterpret_cast<const void *>(cdc::k_speculate<ALGO, true>)
+                      : reinterpret_cast<const void *>(cdc::k_speculate<ALGO, false>);
+        CDC_CUDA(launch_pdl(kspec, dim3((unsigned)blocks), dim3((batch ? cdc::BATCH_WARPS : cdc::SPEC_WARPS) * 32),
+                            (size_t)(batch ? batch_smem : spec_smem), st, G, W, d_bounds, cap, d_count, fused, spw));
         CDC_KCHECK("k_speculate", st);
         ++launches;
         pc.used[1] = true;
@@ -2337,6 +2372,22 @@ int cdc_plan_info(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint
 int cdc_debug_timing(void *d_buf) {
     unsigned long long *p = static_cast<unsigned long long *>(d_buf);
     CDC_CUDA(cudaMemcpyToSymbol(cdc::g_timing, &p, sizeof(p)));
+    return CDC_OK;
+}
+
+int cdc_fetched(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, const void *d_workspace,
+                uint64_t *out, void *stream) {
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!d_workspace || !out) return fail(CDC_ERR_INVALID, "null pointer");
+    Plan P;
+    make_plan(p, nfiles ? nfiles : 1, total_len, max_len, P);
+    const cdc::Work W = carve(P, const_cast<void *>(d_workspace));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned long long v = 0;
+    CDC_CUDA(cudaMemcpyAsync(&v, W.fetched, 8, cudaMemcpyDeviceToHost, st));
+    CDC_CUDA(cudaStreamSynchronize(st));
+    *out = (uint64_t)(v + 1ull);  // the reset leaves ~0
     return CDC_OK;
 }
 
