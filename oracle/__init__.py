@@ -10,7 +10,8 @@ Contents
 --------
 * ``cdc_oracle.c`` (loaded through ctypes): Extreme Byte Search (§4.1), Range
   Scan (§4.2), RAM (§2.1.2 Fig. 2c, §4.3), AE-Max / AE-Min (§2.1.2 Fig. 2a,
-  §4.3), whole-stream chunking, chains from arbitrary starts.
+  §4.3), MAXP (§2.1.2 Fig. 2b l.173/l.196, §4.3 l.361; ``window`` is its
+  per-side window h), whole-stream chunking, chains from arbitrary starts.
 * ``pyref``: the same operations as pure-Python loops (small inputs only),
   written in the *single-pass* formulation (running extreme + deadline) rather
   than the paper's target/window formulation, so the two cross-check each
@@ -32,7 +33,7 @@ import numpy as np
 
 from . import dedup, pyref  # noqa: F401
 
-ALGOS = {"ram": 0, "ae_max": 1, "ae_min": 2}
+ALGOS = {"ram": 0, "ae_max": 1, "ae_min": 2, "maxp": 3}
 MODES = {"max": 0, "min": 1}
 CMPS = {"gt": 0, "geq": 1, "lt": 2, "leq": 3, "eq": 4}
 

@@ -24,7 +24,7 @@
 
 enum { OR_MAX = 0, OR_MIN = 1 };
 enum { OR_GT = 0, OR_GEQ = 1, OR_LT = 2, OR_LEQ = 3, OR_EQ = 4 };
-enum { OR_RAM = 0, OR_AE_MAX = 1, OR_AE_MIN = 2 };
+enum { OR_RAM = 0, OR_AE_MAX = 1, OR_AE_MIN = 2, OR_MAXP = 3 };
 
 /*
  * Extreme Byte Search -- PAPER.md §4.1 (lines 324-330): "identifies the
@@ -133,9 +133,53 @@ uint64_t oracle_ae_chunk_end(const uint8_t *d, uint64_t L, uint64_t s,
     }
 }
 
+/*
+ * MAXP -- PAPER.md §2.1.2 (line 173, Fig. 2b, and line 196) and §4.3 (line
+ * 361): "MAXP identifies target bytes in the data stream that are local
+ * maxima, i.e., they are greater than a fixed number of bytes before and
+ * after them.  When such target bytes are found, chunk boundaries are
+ * inserted at their locations"; "MAXP works by sliding two fixed-size windows
+ * over the data, tracking the maximum values from both windows.  These
+ * windows are located one byte apart ... and the byte between them is the
+ * target byte.  When the target byte's value is greater than the maximum
+ * value from both windows, a chunk boundary is inserted"; "A chunk boundary
+ * is inserted right after such a byte is found".
+ *
+ * Readings (M1-M4): the two windows hold h = w bytes each,
+ * [t-h, t) and (t, t+h], and the test is strict (M1); the target is the last
+ * byte of its chunk (M2, as R2); the left window starts at the chunk start,
+ * so the first target examined is s + h (M3); the right window must lie
+ * inside the stream (M4); max_size caps the chunk (R5).
+ *
+ * "greater than the maximum value from both windows" is "greater than every
+ * byte of both windows"; the loop below stops at the first window byte that
+ * is not smaller, which decides the same predicate.
+ */
+static int oracle_maxp_is_target(const uint8_t *d, uint64_t L, uint64_t t, uint64_t h)
+{
+    if (t < h || t + h >= L)              /* both windows must lie in the stream */
+        return 0;
+    for (uint64_t j = 1; j <= h; j++)
+        if (d[t - j] >= d[t] || d[t + j] >= d[t])
+            return 0;
+    return 1;
+}
+
+uint64_t oracle_maxp_chunk_end(const uint8_t *d, uint64_t L, uint64_t s,
+                               uint64_t h, uint64_t max_size)
+{
+    uint64_t limit = (L - s < max_size) ? L : s + max_size;     /* R5 cap */
+    for (uint64_t t = s + h; t < limit; t++)                     /* chunk [s, t+1) fits */
+        if (oracle_maxp_is_target(d, L, t, h))
+            return t + 1;                                        /* boundary right after the target */
+    return limit;
+}
+
 uint64_t oracle_chunk_end(int algo, const uint8_t *d, uint64_t L, uint64_t s,
                           uint64_t w, uint64_t max_size)
 {
+    if (algo == OR_MAXP)
+        return oracle_maxp_chunk_end(d, L, s, w, max_size);
     if (algo == OR_RAM)
         return oracle_ram_chunk_end(d, L, s, w, max_size);
     return oracle_ae_chunk_end(d, L, s, w, max_size,

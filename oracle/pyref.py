@@ -45,7 +45,24 @@ def ae_chunk_end(d, s, w, max_size, mode="max"):
     return limit
 
 
+def maxp_chunk_end(d, s, h, max_size):
+    """PAPER.md §2.1.2, as written there: two h-byte windows one byte
+    apart slide over the chunk; the target byte between them ends the chunk
+    when it is greater than the maximum of both windows (Python max over the
+    two slices, not the C oracle's early-exit loop)."""
+    L = len(d)
+    limit = min(L, s + max_size)
+    for t in range(s + h, limit):
+        if t + h >= L:
+            break
+        if d[t] > max(d[t - h:t]) and d[t] > max(d[t + 1:t + h + 1]):
+            return t + 1
+    return limit
+
+
 def chunk_end(algo, d, s, w, max_size):
+    if algo == "maxp":
+        return maxp_chunk_end(d, s, w, max_size)
     if algo == "ram":
         return ram_chunk_end(d, s, w, max_size)
     return ae_chunk_end(d, s, w, max_size, "max" if algo == "ae_max" else "min")

@@ -368,3 +368,133 @@ def test_check_batch_accepts_oracle_and_rejects_mutations(algo):
     if bo3[10] != bo3[11]:
         assert oracle.check_batch(algo, data, offs, ends, bo3, w, mx) is not None
 
+
+
+# --------------------------------------------------------------------------
+# MAXP (§2.1.2 l.173 and l.196, §4.3 l.361; readings M1-M4)
+# --------------------------------------------------------------------------
+def _bf_maxp_chunk(d, h, max_size):
+    """Brute force from the definition with Python all(): the chunk from s ends
+    right after the first t in [s+h, limit) whose h bytes before and h bytes
+    after all lie in the stream and are all smaller than d[t]."""
+    L, out, s = len(d), [], 0
+    while s < L:
+        limit = min(L, s + max_size)
+        e = limit
+        for t in range(s + h, limit):
+            if t - h >= 0 and t + h <= L - 1 and all(x < d[t] for x in d[t - h:t]) and \
+                    all(x < d[t] for x in d[t + 1:t + h + 1]):
+                e = t + 1
+                break
+        out.append(e)
+        s = e
+    return out
+
+
+def _local_maxima(d, h):
+    """Every t in [h, L-h) with d[t] > max(d[t-h:t]) and d[t] > max(d[t+1:t+h+1]),
+    from numpy sliding-window maxima (independent of the oracle's loops)."""
+    d = np.asarray(d, dtype=np.int16)
+    L = d.size
+    if L < 2 * h + 1:
+        return np.zeros(0, dtype=np.int64)
+    win = np.lib.stride_tricks.sliding_window_view(d, h).max(axis=1)  # win[i] = max d[i:i+h]
+    t = np.arange(h, L - h)
+    ok = (d[t] > win[t - h]) & (d[t] > win[t + 1])
+    return t[ok]
+
+
+def test_maxp_single_peak_and_constant():
+    d = np.zeros(100, np.uint8)
+    d[30] = 255
+    # the peak ends the first chunk; the zeros after it have no local maximum: caps, then the stream end
+    assert oracle.chunk("maxp", d, 5, 40).tolist() == [31, 71, 100]
+    assert pyref.chunk("maxp", d.tolist(), 5, 40) == [31, 71, 100]
+    # a constant stream has no strict local maximum: every chunk is capped
+    assert oracle.chunk("maxp", np.full(100, 0x42, np.uint8), 3, 10).tolist() == list(range(10, 101, 10))
+    # a peak closer than h to the chunk start, or whose right window passes the stream end, is no boundary
+    assert oracle.chunk("maxp", d, 31, 90).tolist() == [90, 100]
+    d2 = np.zeros(40, np.uint8)
+    d2[36] = 9
+    assert oracle.chunk("maxp", d2, 4, 60).tolist() == [40]
+    # two equal peaks within h of each other: neither is a strict local maximum
+    d3 = np.zeros(100, np.uint8)
+    d3[40] = d3[43] = 7
+    assert oracle.chunk("maxp", d3, 5, 200).tolist() == [100]
+    d3[43] = 6  # now 40 is one, 43 (within h of a larger byte) is not
+    assert oracle.chunk("maxp", d3, 5, 200).tolist() == [41, 100]
+
+
+def test_maxp_exhaustive_small_alphabet():
+    count = 0
+    for n in range(1, 8):
+        for tup in itertools.product([0, 1, 2], repeat=n):
+            d = list(tup)
+            arr = np.array(d, dtype=np.uint8)
+            for h in (1, 2, 3):
+                for mx in (h + 1, h + 2, 7):
+                    exp = _bf_maxp_chunk(d, h, mx)
+                    assert oracle.chunk("maxp", arr, h, mx).tolist() == exp, (d, h, mx)
+                    assert pyref.chunk("maxp", d, h, mx) == exp
+                    count += 1
+    assert count > 10000
+
+
+def test_maxp_random_vs_bruteforce_and_pyref():
+    rng = np.random.default_rng(17)
+    for trial in range(60):
+        n = int(rng.integers(1, 500))
+        hi = int(rng.choice([2, 4, 16, 256]))
+        d = rng.integers(0, hi, n).astype(np.uint8)
+        h = int(rng.integers(1, 20))
+        mx = int(h + 1 + rng.integers(0, 80))
+        exp = _bf_maxp_chunk(d.tolist(), h, mx)
+        assert oracle.chunk("maxp", d, h, mx).tolist() == exp, (n, h, mx)
+        assert pyref.chunk("maxp", d.tolist(), h, mx) == exp
+
+
+@pytest.mark.parametrize("gen", ["uniform", "zipf"])
+def test_maxp_invariants_and_local_maxima(gen):
+    L = 1 << 20
+    d = synth.uniform(L, 21) if gen == "uniform" else synth.zipf_bytes(L, 1.1, 22)
+    h, mx = 64, 2048
+    ends = oracle.chunk("maxp", d, h, mx)
+    lens = _lens(ends)
+    assert int(ends[-1]) == L and (lens > 0).all()
+    assert (lens[:-1] >= h + 1).all() and (lens <= mx).all()
+    q = set(_local_maxima(d, h).tolist())
+    s = 0
+    for e in ends.tolist():
+        if e - s < mx and e < L:          # a content boundary: its last byte is a local maximum ...
+            assert e - 1 in q
+        # ... and no earlier position of the chunk's candidate range is one
+        assert not any(t in q for t in range(s + h, e - 1))
+        s = e
+    # without a cap the chain visits every local maximum (two are more than h apart)
+    ends2 = oracle.chunk("maxp", d, h, L + 1)
+    assert (ends2[:-1] - 1).tolist() == sorted(q)
+
+
+def test_maxp_local_maximum_density_closed_form():
+    """On i.i.d. uniform bytes a byte is a strict maximum of its 2h neighbours
+    with probability P(h) = sum_v (1/256) (v/256)^(2h); with no cap the chain
+    ends a chunk at every local maximum, so the boundary count is ~ (L - 2h) P(h).
+    A non-strict test (>=), a one-sided window or a window of 2h bytes on one
+    side move the count by far more than the sampling error."""
+    L, h = 4 << 20, 64
+    d = synth.uniform(L, 23)
+    n = oracle.chunk("maxp", d, h, L + 1).size - 1
+    p = sum((v / 256.0) ** (2 * h) for v in range(256)) / 256.0
+    expect = (L - 2 * h) * p
+    assert abs(n - expect) < 5 * math.sqrt(expect), (n, expect)
+
+
+def test_maxp_check_chunking_accepts_oracle_and_rejects_mutations():
+    for gen, h, mx in (("uniform", 100, 3000), ("zipf", 300, 8000), ("runs", 20, 600)):
+        L = 300_001
+        d = {"uniform": lambda: synth.uniform(L, 34), "zipf": lambda: synth.zipf_bytes(L, 1.1, 35),
+             "runs": lambda: np.repeat(synth.uniform(L // 50 + 1, 36), 50)[:L]}[gen]()
+        ends = oracle.chunk("maxp", d, h, mx)
+        assert oracle.check_chunking("maxp", d, ends, h, mx, threads=4) is None
+        for bad in _mutations(ends, L):
+            assert oracle.check_chunking("maxp", d, np.array(bad, dtype=np.uint64), h, mx, threads=3) is not None
