@@ -59,8 +59,15 @@ typedef enum {
     CDC_ERR_NO_DEVICE = -5    /* no sm_100 device present */
 } cdc_status;
 
-/* Algorithms: PAPER.md §2.1.2 (RAM, AE-Max, AE-Min). */
-typedef enum { CDC_RAM = 0, CDC_AE_MAX = 1, CDC_AE_MIN = 2 } cdc_algo;
+/*
+ * Algorithms: PAPER.md §2.1.2 (RAM, AE-Max, AE-Min, MAXP).  MAXP (l.173,
+ * l.196; §4.3 l.361; readings M1-M5): the chunk from s ends right after the
+ * first byte t in [s+h, s+max_size) that is greater than every byte of
+ * [t-h, t) and of (t, t+h] (both windows inside the stream), with h = window
+ * (at most 65536); single streams only (cdc_chunk, cdc_chunk_host; the batch,
+ * chain and diagnostics entry points return CDC_ERR_INVALID for it).
+ */
+typedef enum { CDC_RAM = 0, CDC_AE_MAX = 1, CDC_AE_MIN = 2, CDC_MAXP = 3 } cdc_algo;
 
 /* Extreme Byte Search modes (§4.1) and Range Scan comparators (§4.2). */
 typedef enum { CDC_EXT_MAX = 0, CDC_EXT_MIN = 1 } cdc_extreme_mode;
@@ -84,7 +91,10 @@ const char *cdc_last_error(void);
  * Window size for a target average chunk size (reading R4):
  * on i.i.d. uniform bytes both RAM and AE chunks average w + 256 bytes when
  * w >> 256 (window, then a geometric wait for the top byte value), so
- * w = avg - 256 for avg >= 512, and w = avg/2 below.  Writes *window.
+ * w = avg - 256 for avg >= 512, and w = avg/2 below.  MAXP (reading M5): the
+ * smallest h whose local maxima on uniform bytes are at least avg bytes apart
+ * on average, 1 / P(h) >= avg with P(h) = sum_v (1/256) (v/256)^(2h)
+ * (h = 447 for 8 KiB).  Writes *window.
  */
 int cdc_window_for_avg(int32_t algo, uint64_t avg_size, uint32_t *window);
 

@@ -13,7 +13,7 @@ import torch
 
 from ._lib import CdcError, cdc_params, check, lib
 
-ALGOS = {"ram": 0, "ae_max": 1, "ae_min": 2}
+ALGOS = {"ram": 0, "ae_max": 1, "ae_min": 2, "maxp": 3}
 MODES = {"max": 0, "min": 1}
 CMPS = {"gt": 0, "geq": 1, "lt": 2, "leq": 3, "eq": 4}
 

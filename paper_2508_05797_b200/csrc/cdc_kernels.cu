@@ -20,6 +20,7 @@
 //                    exclusive chunk end offsets (uint64).
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -1376,6 +1377,7 @@ __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_
 }
 
 #include "cdc_kphase.cuh"  // K-phase speculation: single streams with long windows
+#include "cdc_maxp.cuh"    // MAXP: local maxima in one pass, then the chain over them
 
 // ------------------------------------------------------------------ K0 batch segment table
 // Tiles of SP_THREADS x SP_RPT consecutive files, taken from a ticket by a
@@ -1797,8 +1799,10 @@ cudaError_t launch_pdl(const void *fn, dim3 grid, dim3 block, size_t smem, cudaS
 
 int check_params(const cdc_params *p) {
     if (!p) return fail(CDC_ERR_INVALID, "null params");
-    if (p->algo < CDC_RAM || p->algo > CDC_AE_MIN) return fail(CDC_ERR_INVALID, "unknown algorithm");
+    if (p->algo < CDC_RAM || p->algo > CDC_MAXP) return fail(CDC_ERR_INVALID, "unknown algorithm");
     if (p->window < 1) return fail(CDC_ERR_INVALID, "window must be >= 1");
+    if (p->algo == CDC_MAXP && p->window > cdc::MX_HMAX)
+        return fail(CDC_ERR_INVALID, "MAXP window must be <= 65536 (a tile's shared memory holds both windows)");
     // device code keeps w + 1 in 32-bit signed arithmetic
     if (p->window >= (1u << 31)) return fail(CDC_ERR_INVALID, "window must be < 2^31");
     if (p->max_size <= p->window) return fail(CDC_ERR_INVALID, "max_size must exceed window");
@@ -2229,6 +2233,112 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     return CDC_OK;
 }
 
+// ------------------------------------------------------------------ MAXP (cdc_maxp.cuh)
+struct MaxpPlan {
+    cdc::MaxpGeo Q;
+    uint64_t nlt;           // link / write tiles
+    uint64_t ngc;           // k_maxp_gather CTAs
+    size_t off_q, off_qt, off_qn, off_f, off_ncap, off_jl, off_reset, reset_bytes, bytes;
+    uint32_t smem;          // k_maxp_scan dynamic shared memory
+};
+uint32_t maxp_smem(uint64_t h, uint32_t &buf, uint32_t &ccap) {
+    buf = (uint32_t)round_up(cdc::MX_TILE + 2 * h + 32, 128);
+    ccap = (uint32_t)(cdc::MX_TILE / (h + 1) + 2);
+    return buf + 3 * (buf / 16) + 16 + 2 * ccap + 128;
+}
+void maxp_plan(const cdc_params *p, uint64_t L, MaxpPlan &P) {
+    cdc::MaxpGeo &Q = P.Q;
+    Q.data = nullptr;
+    Q.L = L;
+    Q.h = p->window;
+    Q.M = p->max_size;
+    Q.ntiles = (L + cdc::MX_TILE - 1) / cdc::MX_TILE;
+    Q.qcap = L / (Q.h + 1) + 2;  // two local maxima are more than h apart
+    P.smem = maxp_smem(Q.h, Q.buf, Q.ccap);
+    P.nlt = (Q.qcap + 1 + cdc::MX_ETILE - 1) / cdc::MX_ETILE;
+    P.ngc = (Q.ntiles + cdc::MX_GTILES - 1) / cdc::MX_GTILES;
+    size_t o = 0;
+    P.off_q = o;
+    o = round_up(o + Q.qcap * 8, 256);
+    P.off_qt = o;
+    o = round_up(o + Q.ntiles * Q.ccap * 2, 256);
+    P.off_qn = o;
+    o = round_up(o + Q.ntiles * 4, 256);
+    P.off_f = o;
+    o = round_up(o + (Q.qcap + 1) * 8, 256);
+    P.off_ncap = o;
+    o = round_up(o + (Q.qcap + 1) * 8, 256);
+    P.off_jl = o;
+    o = round_up(o + (Q.qcap + 1) * 8, 256);
+    P.off_reset = o;  // tst, lst, wst, ctrl, nq, nj, on -- reset to all-ones by k_reset
+    P.reset_bytes = round_up(P.ngc * 8 + 2 * P.nlt * 8 + 32 + 16 + (Q.qcap + 1), 256);
+    P.bytes = o + P.reset_bytes;
+}
+cdc::MaxpWork maxp_carve(const MaxpPlan &P, void *ws) {
+    uint8_t *b = static_cast<uint8_t *>(ws);
+    cdc::MaxpWork X;
+    X.q = reinterpret_cast<uint64_t *>(b + P.off_q);
+    X.qt = reinterpret_cast<uint16_t *>(b + P.off_qt);
+    X.qn = reinterpret_cast<uint32_t *>(b + P.off_qn);
+    X.f = reinterpret_cast<int64_t *>(b + P.off_f);
+    X.ncap = reinterpret_cast<uint64_t *>(b + P.off_ncap);
+    X.jl = reinterpret_cast<int64_t *>(b + P.off_jl);
+    unsigned long long *r = reinterpret_cast<unsigned long long *>(b + P.off_reset);
+    X.tst = r;
+    X.lst = r + P.ngc;
+    X.wst = X.lst + P.nlt;
+    X.ctrl = reinterpret_cast<uint32_t *>(X.wst + P.nlt);
+    X.nq = reinterpret_cast<unsigned long long *>(X.ctrl + 8);
+    X.nj = X.nq + 1;
+    X.on = reinterpret_cast<uint8_t *>(X.nj + 1);
+    return X;
+}
+
+int launch_maxp(const cdc_params *p, const uint8_t *d_data, uint64_t L, uint64_t *d_bounds, uint64_t cap,
+                uint64_t *d_count, void *ws, size_t ws_bytes, cudaStream_t st) {
+    MaxpPlan P;
+    maxp_plan(p, L, P);
+    if (ws_bytes < P.bytes) return fail(CDC_ERR_WORKSPACE, "workspace too small");
+    if (L == 0) {
+        CDC_CUDA(cudaMemsetAsync(d_count, 0, 8, st));
+        g_launches = 0;
+        return CDC_OK;
+    }
+    P.Q.data = d_data;
+    const cdc::MaxpWork X = maxp_carve(P, ws);
+    static bool attr[MAX_DEVICES] = {false};
+    const int dev = current_device();
+    if (!attr[dev]) {  // the largest window's tile (per device: a context attribute)
+        uint32_t b, c;
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_maxp_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)maxp_smem(cdc::MX_HMAX, b, c)));
+        attr[dev] = true;
+    }
+    const uint64_t nsm = (uint64_t)num_sms();
+    const uint64_t n16 = P.reset_bytes / 16;
+    cdc::k_reset<<<(unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * nsm), 256, 0, st>>>(
+        reinterpret_cast<uint4 *>(static_cast<uint8_t *>(ws) + P.off_reset), n16, nullptr);
+    CDC_KCHECK("k_reset (MAXP)", st);
+    int per_sm = 0;
+    CDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cdc::k_maxp_scan, cdc::MX_THREADS, P.smem));
+    const uint64_t sblocks = std::min<uint64_t>(P.Q.ntiles, nsm * (uint64_t)std::max(per_sm, 1));
+    cdc::k_maxp_scan<<<(unsigned)sblocks, cdc::MX_THREADS, P.smem, st>>>(P.Q, X);
+    CDC_KCHECK("k_maxp_scan", st);
+    cdc::k_maxp_gather<<<(unsigned)P.ngc, cdc::MX_GTILES, 0, st>>>(P.Q, X);
+    CDC_KCHECK("k_maxp_gather", st);
+    // element tiles: one per CTA (the grid covers the capacity; CTAs past nQ exit)
+    const unsigned eblocks = (unsigned)std::min<uint64_t>(P.nlt, 16 * nsm);
+    cdc::k_maxp_link<<<eblocks, cdc::MX_ETILE, 0, st>>>(P.Q, X);
+    CDC_KCHECK("k_maxp_link", st);
+    cdc::k_maxp_path<<<1, 256, 0, st>>>(P.Q, X);
+    CDC_KCHECK("k_maxp_path", st);
+    cdc::k_maxp_write<<<eblocks, cdc::MX_ETILE, 0, st>>>(P.Q, X, d_bounds, cap, d_count);
+    CDC_KCHECK("k_maxp_write", st);
+    g_launches = 6;
+    CDC_CUDA(cudaGetLastError());
+    return CDC_OK;
+}
+
 int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file_off, uint64_t nfiles,
               uint64_t total_len, uint64_t max_len, uint64_t *d_bounds, uint64_t cap, uint64_t *d_bound_off,
               uint64_t *d_count, void *ws, size_t ws_bytes, void *stream, bool batch) {
@@ -2237,6 +2347,11 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     if (!d_count || (!d_bounds && cap) || (total_len && !d_data) || !ws)
         return fail(CDC_ERR_INVALID, "null pointer argument");
     if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(CDC_ERR_INVALID, "workspace must be 256-byte aligned");
+    if (p->algo == CDC_MAXP) {
+        if (batch) return fail(CDC_ERR_INVALID, "MAXP: single streams only (cdc_chunk / cdc_chunk_host)");
+        return launch_maxp(p, d_data, total_len, d_bounds, cap, d_count, ws, ws_bytes,
+                           static_cast<cudaStream_t>(stream));
+    }
     Plan P;
     make_plan(p, nfiles, total_len, max_len, P);
     if (ws_bytes < P.bytes) return fail(CDC_ERR_WORKSPACE, "workspace too small");
@@ -2360,6 +2475,7 @@ extern "C" int cdc_debug_wait_ns(unsigned long long *ns) {
 int cdc_plan_info(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t max_len, uint64_t *out) {
     int rc = check_params(p);
     if (rc) return rc;
+    if (p->algo == CDC_MAXP) return fail(CDC_ERR_INVALID, "not defined for MAXP (no speculative segments)");
     if (!out) return fail(CDC_ERR_INVALID, "null out");
     Plan P;
     make_plan(p, nfiles ? nfiles : 1, total_len, max_len, P);
@@ -2379,6 +2495,7 @@ int cdc_fetched(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64
                 uint64_t *out, void *stream) {
     int rc = check_params(p);
     if (rc) return rc;
+    if (p->algo == CDC_MAXP) return fail(CDC_ERR_INVALID, "not defined for MAXP (no speculative segments)");
     if (!d_workspace || !out) return fail(CDC_ERR_INVALID, "null pointer");
     Plan P;
     make_plan(p, nfiles ? nfiles : 1, total_len, max_len, P);
@@ -2395,6 +2512,7 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
               uint64_t *stats, void *stream) {
     int rc = check_params(p);
     if (rc) return rc;
+    if (p->algo == CDC_MAXP) return fail(CDC_ERR_INVALID, "not defined for MAXP (no speculative segments)");
     if (!d_workspace || !stats) return fail(CDC_ERR_INVALID, "null pointer");
     Plan P;
     make_plan(p, nfiles ? nfiles : 1, total_len, max_len, P);
@@ -2509,8 +2627,22 @@ int cdc_profile_collect(double *ms_sum, uint64_t *launches, uint64_t *calls) {
 
 int cdc_window_for_avg(int32_t algo, uint64_t avg_size, uint32_t *window) {
     if (!window) return fail(CDC_ERR_INVALID, "null window");
-    if (algo < CDC_RAM || algo > CDC_AE_MIN) return fail(CDC_ERR_INVALID, "unknown algorithm");
+    if (algo < CDC_RAM || algo > CDC_MAXP) return fail(CDC_ERR_INVALID, "unknown algorithm");
     if (avg_size < 2 || avg_size > (1ull << 31)) return fail(CDC_ERR_INVALID, "avg_size out of range");
+    if (algo == CDC_MAXP) {
+        // reading M5: on i.i.d. uniform bytes a byte is a strict maximum of its 2h
+        // neighbours with probability P(h) = sum_v (1/256) (v/256)^(2h); local maxima
+        // (the chunk ends) are then 1/P(h) bytes apart on average: the smallest h
+        // with 1/P(h) >= avg (at most MX_HMAX)
+        uint32_t h = 1;
+        for (; h < cdc::MX_HMAX; ++h) {
+            double pr = 0.0;
+            for (int v = 1; v < 256; ++v) pr += std::pow(v / 256.0, 2.0 * h);
+            if (256.0 / pr >= (double)avg_size) break;
+        }
+        *window = h;
+        return CDC_OK;
+    }
     *window = (uint32_t)(avg_size >= 512 ? avg_size - 256 : avg_size / 2);
     return CDC_OK;
 }
@@ -2537,6 +2669,13 @@ int cdc_workspace_size(const cdc_params *p, uint64_t nfiles, uint64_t total_len,
     int rc = check_params(p);
     if (rc) return rc;
     if (!bytes) return fail(CDC_ERR_INVALID, "null bytes");
+    if (p->algo == CDC_MAXP) {
+        if (nfiles > 1) return fail(CDC_ERR_INVALID, "MAXP: single streams only");
+        MaxpPlan M;
+        maxp_plan(p, total_len, M);
+        *bytes = M.bytes;
+        return CDC_OK;
+    }
     Plan P;
     make_plan(p, nfiles ? nfiles : 1, total_len, max_len, P);
     *bytes = P.bytes;
@@ -2591,6 +2730,7 @@ int cdc_chunk_host(const cdc_params *p, const uint8_t *h_data, uint64_t len, uin
 int cdc_plan_segments(const cdc_params *p, uint64_t len, uint64_t *starts, uint64_t starts_cap, uint64_t *n_out) {
     int rc = check_params(p);
     if (rc) return rc;
+    if (p->algo == CDC_MAXP) return fail(CDC_ERR_INVALID, "not defined for MAXP (no speculative segments)");
     if (!n_out || (!starts && starts_cap)) return fail(CDC_ERR_INVALID, "null pointer");
     Plan P;
     make_plan(p, 1, len, len, P);
@@ -2706,6 +2846,7 @@ int cdc_chain(const cdc_params *p, const uint8_t *d_data, uint64_t len, uint64_t
               uint64_t *d_starts, uint64_t starts_cap, uint64_t *d_count, void *stream) {
     int rc = check_params(p);
     if (rc) return rc;
+    if (p->algo == CDC_MAXP) return fail(CDC_ERR_INVALID, "not defined for MAXP (no speculative segments)");
     if (!d_count || (!d_starts && starts_cap) || (!d_data && len)) return fail(CDC_ERR_INVALID, "null pointer");
     if (start > len) return fail(CDC_ERR_INVALID, "start beyond len");
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -1,0 +1,433 @@
+// cdc_maxp.cuh -- MAXP on sm_100a (§2.1.2 l.173 and l.196, §4.3 l.361).
+//
+// MAXP ends a chunk right after a target byte that is greater than the h bytes
+// before it and the h bytes after it ("the target byte's value is greater than
+// the maximum value from both windows", l.196; readings M1-M4 in DESIGN.md §2).
+// Whether a byte is such a local maximum does not depend on where chunks
+// start, so the GPU form splits the method in two ("MAXP"):
+//
+//  1. k_maxp_scan (HBM-bound, one pass over the bytes): every tile of MX_TILE
+//     candidate positions is copied with its two h-byte margins into shared
+//     memory by one TMA bulk copy; the local maxima of the tile are found with
+//     Extreme Byte Searches over 16-byte granules (§4.1: one max per granule,
+//     then the van Herk / Gil-Werman window maximum over K0 granules on each
+//     side), and only the rare granules whose maximum beats both neighbouring
+//     windows are checked byte by byte.  Each tile writes its maxima to its
+//     own slot (no tile waits for another); k_maxp_gather then concatenates
+//     the slots in stream order (a scan of the tile counts) into one
+//     ascending list q[].
+//  2. The chain (what depends on chunk starts): from a start s the chunk ends
+//     after the first local maximum in [s+h, s+max_size) (M3, R5), else it is
+//     capped.  Two local maxima are more than h apart, so after a content
+//     boundary at q[i] the next one is q[i+1] unless the gap exceeds max_size;
+//     only capped stretches can skip a maximum (one that falls within h of a
+//     cap start).  k_maxp_link computes for every element i (and the stream
+//     start, i = -1) where its chunk run ends, f(i), and its cap count;
+//     k_maxp_path walks the (rare) runs that skip maxima, in order, and marks
+//     the skipped ones; k_maxp_write scans the per-element boundary counts
+//     (decoupled look-back) and writes caps and content boundaries.
+//
+// Nothing here is shared with oracle/ (tests compare the two element by element).
+// (Included by cdc_kernels.cu inside namespace cdc.)
+
+constexpr int MX_TILE = 32768;         // candidate positions per scan tile
+constexpr int MX_THREADS = 256;        // k_maxp_scan
+constexpr uint32_t MX_HMAX = 65536;    // largest window per side a tile's shared memory holds
+constexpr int MX_ETILE = 256;          // elements per link / write tile (one thread each)
+constexpr int MX_GTILES = 1024;        // scan tiles per k_maxp_gather CTA (one thread each)
+
+struct MaxpGeo {
+    const uint8_t *data;
+    uint64_t L, h, M;      // stream length, window per side, max_size
+    uint64_t ntiles;       // scan tiles
+    uint64_t qcap;         // capacity of q (L / (h+1) + 2: local maxima are > h apart)
+    uint32_t buf;          // bytes of a tile's byte buffer in shared memory
+    uint32_t ccap;         // candidates per tile (uint16 offsets)
+};
+struct MaxpWork {
+    uint64_t *q;                 // local maxima, ascending (qcap)
+    uint16_t *qt;                // scan tile t's maxima (offsets from the tile start): [t * ccap, ...)
+    uint32_t *qn;                // ... and their number
+    int64_t *f;                  // element e = i + 1 (i in [-1, nQ)): the element where i's run ends (nQ: the stream end)
+    uint64_t *ncap;              // ... and the number of capped chunks in that run
+    int64_t *jl;                 // elements whose run skips a local maximum, ascending
+    // reset to ~0 (all-ones) before every call:
+    unsigned long long *tst;     // gather CTAs' look-back words
+    unsigned long long *lst;     // link tiles' look-back words
+    unsigned long long *wst;     // write tiles' look-back words
+    uint32_t *ctrl;              // [0] scan ticket, [1] link ticket, [2] write ticket, [3] gather ticket
+    unsigned long long *nq;      // number of local maxima (written by the last scan tile)
+    unsigned long long *nj;      // number of skipping runs (last link tile)
+    uint8_t *on;                 // element e: 0xFF on the chain, 0 skipped
+};
+
+// byte-wise maximum of a 16-byte granule (four 4-way byte maxima, then the word's bytes)
+__device__ __forceinline__ uint32_t granule_max(const uint4 &v) {
+    uint32_t m = __vmaxu4(__vmaxu4(v.x, v.y), __vmaxu4(v.z, v.w));
+    m = __vmaxu4(m, m >> 16);
+    m = __vmaxu4(m, m >> 8);
+    return m & 0xFFu;
+}
+
+// block-wide exclusive scan of one 32-bit value per thread (MX_THREADS or 1024 threads)
+__device__ __forceinline__ uint32_t mx_block_scan(uint32_t v, uint32_t &total, uint32_t *scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) scratch[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t s = lane < nw ? scratch[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, s, o);
+            if (lane >= o) s += y;
+        }
+        scratch[32 + lane] = s;
+    }
+    __syncthreads();
+    const uint32_t before = warp ? scratch[32 + warp - 1] : 0u;
+    total = scratch[32 + nw - 1];
+    __syncthreads();
+    return before + x - v;
+}
+
+// Tile t's exclusive prefix of a count, published as TL_AGG then TL_INC
+// (warp 0; the result is returned to every thread through `slot`).
+__device__ __forceinline__ uint64_t mx_tile_prefix(unsigned long long *st, uint64_t t, uint64_t cnt, uint64_t *slot) {
+    if (threadIdx.x < 32) {
+        uint64_t excl = 0;
+        if (t == 0) {
+            if (threadIdx.x == 0) tile_publish(st, TL_INC, cnt);
+        } else {
+            if (threadIdx.x == 0) tile_publish(st + t, TL_AGG, cnt);
+            excl = tile_lookback(st, 1, t);
+            if (threadIdx.x == 0) tile_publish(st + t, TL_INC, excl + cnt);
+        }
+        if (threadIdx.x == 0) *slot = excl;
+    }
+    __syncthreads();
+    const uint64_t r = *slot;
+    __syncthreads();
+    return r;
+}
+
+// K1: local maxima, tile by tile in ticket order.
+__global__ void __launch_bounds__(MX_THREADS) k_maxp_scan(MaxpGeo Q, MaxpWork X) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t s_tile, s_scr[64], s_cnt;
+    uint8_t *buf = align_smem(smem);                       // tile bytes (Q.buf)
+    uint8_t *gm = buf + Q.buf;                             // granule maxima
+    const uint32_t NGmax = Q.buf / 16;
+    uint8_t *pf = gm + NGmax, *sf = pf + NGmax;            // van Herk prefix / suffix maxima
+    uint16_t *cand = reinterpret_cast<uint16_t *>(sf + NGmax + (16 - (3 * NGmax) % 16) % 16);
+    const int tid = threadIdx.x;
+    const uint64_t h = Q.h, L = Q.L;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (;;) {
+        if (tid == 0) s_tile = atomicAdd(X.ctrl, 1u) + 1u;  // the counter starts at ~0
+        __syncthreads();
+        const uint64_t t = s_tile;
+        if (t >= Q.ntiles) break;
+        // candidate positions of the tile: [ca, cb) inside [h, L - h)
+        const uint64_t a = t * MX_TILE, b = a + MX_TILE < L ? a + MX_TILE : L;
+        const uint64_t ca = a > h ? a : h;
+        const uint64_t cb = (L > h && b > L - h) ? L - h : (L > h ? b : 0);
+        uint32_t count = 0;
+        bool ranked = false;  // the long-window path writes its slot itself
+        if (tid == 0) s_cnt = 0;
+        if (ca < cb) {
+            // bytes [lo, hi) = [ca - h, cb + h): one bulk copy of the 16-byte granules holding them
+            const uint64_t lo = ca - h, hi = cb + h;
+            const uintptr_t A0 = reinterpret_cast<uintptr_t>(Q.data + lo) & ~static_cast<uintptr_t>(15);
+            const uintptr_t A1 = (reinterpret_cast<uintptr_t>(Q.data + hi) + 15) & ~static_cast<uintptr_t>(15);
+            const uint32_t nbytes = (uint32_t)(A1 - A0);
+            const uint32_t off0 = (uint32_t)(reinterpret_cast<uintptr_t>(Q.data + lo) - A0);
+            if (tid == 0) {
+                mbar_arrive_expect_tx(&bar, nbytes);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_addr(buf)),
+                    "l"(reinterpret_cast<const uint8_t *>(A0)), "r"(nbytes), "r"(smem_addr(&bar))
+                    : "memory");
+            }
+            mbar_wait(&bar, phase);
+            phase ^= 1u;
+            // bytes of the first and last granule outside [lo, hi) are not the stream's:
+            // the granule maxima read them as zeros (a zero is never a strict maximum and
+            // never beats one; the byte-level tests below only read inside [lo, hi)).  The
+            // buffer itself is never written by a thread: only the bulk copy writes it.
+            const uint32_t vend = off0 + (uint32_t)(hi - lo);
+            const uint32_t NG = nbytes / 16;
+            // buffer offset of stream position x: x - lo + off0
+            const int64_t cbase = (int64_t)off0 - (int64_t)lo;
+            const uint32_t c_lo = (uint32_t)((int64_t)ca + cbase), c_hi = (uint32_t)((int64_t)cb + cbase);
+            if (h >= 31) {
+                const uint32_t K0 = (uint32_t)((h - 15) / 16);  // granules wholly inside each window
+                for (uint32_t j = tid; j < NG; j += MX_THREADS) {
+                    uint4 v = *reinterpret_cast<const uint4 *>(buf + 16 * j);
+                    if (j == 0 || j == NG - 1) {  // keep bytes [off0, vend) of the granule
+                        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            const uint32_t x = 16 * j + k;
+                            if (x < off0 || x >= vend) w[k >> 2] &= ~(0xFFu << (8 * (k & 3)));
+                        }
+                        v = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                    gm[j] = (uint8_t)vext16<true>(v);  // Extreme Byte Search leaf (DPX byte maxima)
+                }
+                __syncthreads();
+                // van Herk / Gil-Werman: prefix and suffix maxima inside blocks of K0 granules
+                for (uint32_t blk = tid; blk * K0 < NG; blk += MX_THREADS) {
+                    const uint32_t j0 = blk * K0, j1 = j0 + K0 < NG ? j0 + K0 : NG;
+                    uint8_t m = 0;
+                    for (uint32_t j = j0; j < j1; ++j) {
+                        m = gm[j] > m ? gm[j] : m;
+                        pf[j] = m;
+                    }
+                    m = 0;
+                    for (uint32_t j = j1; j-- > j0;) {
+                        m = gm[j] > m ? gm[j] : m;
+                        sf[j] = m;
+                    }
+                }
+                __syncthreads();
+                // granules that hold candidate positions; the rare candidates are appended
+                // in any order and ranked afterwards (at most ccap of them)
+                const uint32_t g_lo = c_lo / 16, g_hi = (c_hi + 15) / 16;
+                for (uint32_t j = g_lo + tid; j < g_hi; j += MX_THREADS) {
+                    const uint32_t m = gm[j];
+                    if (m == 0 || j < K0 || j + K0 >= NG) continue;
+                    // window maxima over granules [j-K0, j-1] and [j+1, j+K0] (inside the
+                    // buffer for every candidate of the tile)
+                    const uint32_t lm = max((uint32_t)sf[j - K0], (uint32_t)pf[j - 1]);
+                    const uint32_t rm = max((uint32_t)sf[j + 1], (uint32_t)pf[j + K0]);
+                    if (m <= lm || m <= rm) continue;
+                    // the granule's maximum must be unique (its bytes are within 15 <= h)
+                    const uint8_t *gp = buf + 16 * j;
+                    int nm = 0, at = 0;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        if (gp[k] == m) {
+                            ++nm;
+                            at = k;
+                        }
+                    const uint32_t tpos = 16 * j + at;
+                    if (nm != 1 || tpos < c_lo || tpos >= c_hi) continue;
+                    // the bytes of both windows outside the K0 whole granules
+                    bool ok = true;
+                    const uint32_t l0 = tpos - (uint32_t)h, l1 = 16 * (j - K0);
+                    for (uint32_t x = l0; x < l1 && ok; ++x) ok = buf[x] < m;
+                    const uint32_t r0b = 16 * (j + K0 + 1), r1 = tpos + (uint32_t)h;
+                    for (uint32_t x = r0b; x <= r1 && ok; ++x) ok = buf[x] < m;
+                    if (ok) {
+                        const uint32_t k = atomicAdd(&s_cnt, 1u);
+                        if (k < Q.ccap) cand[k] = (uint16_t)(tpos - c_lo + (uint32_t)(ca - a));
+                    }
+                }
+                __syncthreads();
+                count = s_cnt < Q.ccap ? s_cnt : Q.ccap;
+                // rank by position (distinct), written straight into the tile's slot
+                for (uint32_t i = tid; i < count; i += MX_THREADS) {
+                    const uint16_t v = cand[i];
+                    uint32_t r = 0;
+                    for (uint32_t k = 0; k < count; ++k) r += cand[k] < v;
+                    X.qt[t * Q.ccap + r] = v;
+                }
+                ranked = true;
+            } else {
+                // short windows: every position, exact test (early exit at the first byte not smaller)
+                for (uint32_t r0 = c_lo; r0 < c_hi; r0 += MX_THREADS) {
+                    const uint32_t x = r0 + tid;
+                    bool ok = false;
+                    if (x < c_hi) {
+                        const uint32_t m = buf[x];
+                        ok = m > 0;
+                        for (uint32_t k = 1; k <= (uint32_t)h && ok; ++k) ok = buf[x - k] < m && buf[x + k] < m;
+                    }
+                    uint32_t tot;
+                    const uint32_t o = mx_block_scan(ok ? 1u : 0u, tot, s_scr);
+                    if (ok && count + o < Q.ccap) cand[count + o] = (uint16_t)(x - c_lo + (uint32_t)(ca - a));
+                    count += tot;
+                }
+            }
+        }
+        __syncthreads();  // the last round's candidates are written
+        // this tile's maxima into its own slot (k_maxp_gather orders the slots)
+        if (!ranked)
+            for (uint32_t i = tid; i < count; i += MX_THREADS) X.qt[t * Q.ccap + i] = cand[i];
+        if (tid == 0) X.qn[t] = count;
+        __syncthreads();
+    }
+    if (tid == 0) mbar_inval(&bar);
+}
+
+// K1b: the tiles' maxima concatenated in stream order: one thread per scan
+// tile, a block scan of the counts, a decoupled look-back over the CTAs.
+__global__ void __launch_bounds__(MX_GTILES) k_maxp_gather(MaxpGeo Q, MaxpWork X) {
+    __shared__ uint32_t s_tile, s_scr[64];
+    __shared__ uint64_t s_slot;
+    if (threadIdx.x == 0) s_tile = atomicAdd(X.ctrl + 3, 1u) + 1u;  // CTAs in ticket order
+    __syncthreads();
+    const uint64_t g = s_tile;
+    const uint64_t t = g * MX_GTILES + threadIdx.x;
+    const uint32_t n = t < Q.ntiles ? X.qn[t] : 0u;
+    uint32_t tot;
+    const uint32_t o = mx_block_scan(n, tot, s_scr);
+    const uint64_t excl = mx_tile_prefix(X.tst, g, tot, &s_slot);
+    const uint64_t base = t * (uint64_t)MX_TILE;
+    for (uint32_t i = 0; i < n; ++i) X.q[excl + o + i] = base + X.qt[t * Q.ccap + i];
+    if ((g + 1) * MX_GTILES >= Q.ntiles && threadIdx.x == 0) *X.nq = excl + tot;
+}
+
+// Where the chunk run that starts after element i ends (i = -1: the stream
+// start): the first local maximum q[f] in [s+h, s+M) of the current start s
+// ends it; capped chunks move s by M; maxima within h of a start are skipped
+// (M3).  f = nQ: the run ends at the stream end.  Mirrors the chain rule of
+// PAPER.md §2.1.2 l.196 with R5's cap, one start at a time.
+__device__ __forceinline__ void maxp_run(const MaxpGeo &Q, const uint64_t *q, uint64_t nQ, int64_t i, int64_t &f,
+                                         uint64_t &ncap) {
+    const uint64_t L = Q.L, h = Q.h, M = Q.M;
+    uint64_t s = i < 0 ? 0 : q[i] + 1;
+    uint64_t j = (uint64_t)(i + 1);
+    ncap = 0;
+    for (;;) {
+        while (j < nQ && q[j] < s + h) ++j;                  // too close to the chunk start
+        const uint64_t limit = (L - s < M) ? L : s + M;
+        if (j < nQ && q[j] < limit) {                        // content boundary right after q[j]
+            f = (int64_t)j;
+            return;
+        }
+        if (limit == L) {                                    // the chunk ends at the stream end
+            f = (int64_t)nQ;
+            return;
+        }
+        if (j >= nQ) {                                       // capped chunks up to the stream end
+            ncap += (L - s - 1) / M;
+            f = (int64_t)nQ;
+            return;
+        }
+        const uint64_t k = (q[j] - s) / M;                   // >= 1: capped chunks before q[j]'s
+        ncap += k;
+        s += k * M;
+    }
+}
+
+// K2: every element's run; the runs that skip a maximum, listed in order.
+__global__ void __launch_bounds__(MX_ETILE) k_maxp_link(MaxpGeo Q, MaxpWork X) {
+    __shared__ uint32_t s_tile, s_scr[64];
+    __shared__ uint64_t s_slot;
+    const uint64_t nQ = *X.nq;
+    const uint64_t ntl = (nQ + 1 + MX_ETILE - 1) / MX_ETILE;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(X.ctrl + 1, 1u) + 1u;
+        __syncthreads();
+        const uint64_t t = s_tile;
+        if (t >= ntl) break;
+        const uint64_t e = t * MX_ETILE + threadIdx.x;
+        bool jump = false;
+        int64_t i = (int64_t)e - 1, f = 0;
+        if (e <= nQ) {
+            uint64_t nc;
+            maxp_run(Q, X.q, nQ, i, f, nc);
+            X.f[e] = f;
+            X.ncap[e] = nc;
+            jump = f > i + 1;
+        }
+        uint32_t tot;
+        const uint32_t o = mx_block_scan(jump ? 1u : 0u, tot, s_scr);
+        const uint64_t excl = mx_tile_prefix(X.lst, t, tot, &s_slot);
+        if (jump) X.jl[excl + o] = i;
+        if (t == ntl - 1 && threadIdx.x == 0) *X.nj = excl + tot;
+        __syncthreads();
+    }
+}
+
+// K3 (one warp): the skipping runs in stream order.  A run is on the chain
+// unless an earlier run on the chain jumped over its element; the elements a
+// chain run jumps over are marked off the chain.  (Runs skip maxima only in
+// capped stretches, so the list is short.)
+constexpr int MX_PATH_BATCH = 2048;  // skipping runs staged in shared memory per round
+__global__ void __launch_bounds__(256) k_maxp_path(MaxpGeo Q, MaxpWork X) {
+    __shared__ int64_t s_i[MX_PATH_BATCH], s_f[MX_PATH_BATCH];
+    __shared__ int64_t s_cur;
+    const uint64_t nj = *X.nj;
+    if (threadIdx.x == 0) s_cur = INT64_MIN;  // f of the last run on the chain that skipped maxima
+    for (uint64_t k0 = 0; k0 < nj; k0 += MX_PATH_BATCH) {
+        const uint64_t m = nj - k0 < MX_PATH_BATCH ? nj - k0 : MX_PATH_BATCH;
+        __syncthreads();
+        for (uint64_t k = threadIdx.x; k < m; k += blockDim.x) {
+            const int64_t i = X.jl[k0 + k];
+            s_i[k] = i;
+            s_f[k] = X.f[i + 1];
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            int64_t cur = s_cur;
+            for (uint64_t k = 0; k < m; ++k) {
+                const int64_t i = s_i[k];
+                if (i < cur) continue;  // inside that run: not on the chain
+                const int64_t f = s_f[k];
+                for (int64_t x = i + 1 + (int64_t)threadIdx.x; x < f; x += 32) X.on[x + 1] = 0;
+                cur = f;
+            }
+            if (threadIdx.x == 0) s_cur = cur;
+        }
+    }
+}
+
+// K4: boundaries.  Element e on the chain contributes its capped chunks and the
+// chunk that ends its run; a decoupled look-back over the counts gives the
+// output offsets; each warp writes its 32 elements' runs with all lanes.
+__global__ void __launch_bounds__(MX_ETILE) k_maxp_write(MaxpGeo Q, MaxpWork X, uint64_t *bounds, uint64_t cap,
+                                                         uint64_t *d_count) {
+    __shared__ uint32_t s_tile, s_scr[64];
+    __shared__ uint64_t s_slot;
+    const uint64_t nQ = *X.nq;
+    const uint64_t ntl = (nQ + 1 + MX_ETILE - 1) / MX_ETILE;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(X.ctrl + 2, 1u) + 1u;
+        __syncthreads();
+        const uint64_t t = s_tile;
+        if (t >= ntl) break;
+        const uint64_t e = t * MX_ETILE + threadIdx.x;
+        uint64_t n = 0, nc = 0, s = 0, end = 0;
+        if (e <= nQ && X.on[e] != 0) {
+            nc = X.ncap[e];
+            n = nc + 1;
+            s = e == 0 ? 0 : X.q[e - 1] + 1;
+            const int64_t f = X.f[e];
+            end = f < (int64_t)nQ ? X.q[f] + 1 : Q.L;
+        }
+        // per-thread counts can exceed 32 bits only for runs of > 4 G capped chunks
+        uint32_t tot;
+        const uint32_t o32 = mx_block_scan((uint32_t)n, tot, s_scr);
+        const uint64_t excl = mx_tile_prefix(X.wst, t, tot, &s_slot);
+        const uint64_t o = excl + o32;
+        for (int r = 0; r < 32; ++r) {
+            const uint64_t rn = __shfl_sync(0xFFFFFFFFu, n, r);
+            if (rn == 0) continue;
+            const uint64_t ro = __shfl_sync(0xFFFFFFFFu, o, r), rs = __shfl_sync(0xFFFFFFFFu, s, r);
+            const uint64_t rc = rn - 1, re = __shfl_sync(0xFFFFFFFFu, end, r);
+            for (uint64_t k = lane; k <= rc; k += 32) {
+                const uint64_t idx = ro + k;
+                if (idx < cap) bounds[idx] = k < rc ? rs + (k + 1) * Q.M : re;
+            }
+        }
+        if (t == ntl - 1 && threadIdx.x == 0) *d_count = excl + tot;
+        __syncthreads();
+    }
+}
+

@@ -106,3 +106,26 @@ def test_batch_host_rejects_bad_offsets(lib):
     data = np.zeros(100, np.uint8)
     with pytest.raises(api.CdcError):
         api.chunk_batch_host(data, np.array([0, 60, 50, 100], np.uint64), p)
+
+
+def test_maxp_window_for_avg_closed_form(lib):
+    """Reading M5: h is the smallest window whose local maxima on uniform bytes
+    are at least avg bytes apart on average, 1/P(h) >= avg with
+    P(h) = sum_v (1/256) (v/256)^(2h) (computed here independently)."""
+    from paper_2508_05797_b200 import api
+    v = np.arange(256) / 256.0
+
+    def spacing(h):
+        return 256.0 / float((v ** (2 * h)).sum())
+
+    for avg in (64, 512, 4096, 8192, 16384):
+        h = api.window_for_avg("maxp", avg)
+        assert spacing(h) >= avg and (h == 1 or spacing(h - 1) < avg), (avg, h)
+    assert api.window_for_avg("maxp", 8192) == 447
+    # workspace sizing is host-only; batches are not defined for MAXP
+    p = api.params("maxp", avg_size=8192)
+    assert api.workspace_size(p, 1, 1 << 30, 1 << 30) > (1 << 30) // 448 * 8
+    with pytest.raises(api.CdcError):
+        api.workspace_size(p, 4, 1 << 20, 1 << 18)
+    with pytest.raises(api.CdcError):
+        api.workspace_size(api.params("maxp", window=65537, max_size=1 << 20), 1, 1 << 20, 1 << 20)
