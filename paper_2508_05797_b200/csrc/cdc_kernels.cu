@@ -2311,7 +2311,7 @@ int launch_maxp(const cdc_params *p, const uint8_t *d_data, uint64_t L, uint64_t
     if (!attr[dev]) {  // the largest window's tile (per device: a context attribute)
         uint32_t b, c;
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_maxp_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)maxp_smem(cdc::MX_HMAX, b, c)));
+                                      (int)maxp_smem(cdc::MX_HMAX, b, c)));  // (<= 227 KB: static_assert below)
         attr[dev] = true;
     }
     const uint64_t nsm = (uint64_t)num_sms();
@@ -2323,16 +2323,21 @@ int launch_maxp(const cdc_params *p, const uint8_t *d_data, uint64_t L, uint64_t
     CDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cdc::k_maxp_scan, cdc::MX_THREADS, P.smem));
     const uint64_t sblocks = std::min<uint64_t>(P.Q.ntiles, nsm * (uint64_t)std::max(per_sm, 1));
     cdc::k_maxp_scan<<<(unsigned)sblocks, cdc::MX_THREADS, P.smem, st>>>(P.Q, X);
+    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
     CDC_KCHECK("k_maxp_scan", st);
     cdc::k_maxp_gather<<<(unsigned)P.ngc, cdc::MX_GTILES, 0, st>>>(P.Q, X);
+    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
     CDC_KCHECK("k_maxp_gather", st);
     // element tiles: one per CTA (the grid covers the capacity; CTAs past nQ exit)
     const unsigned eblocks = (unsigned)std::min<uint64_t>(P.nlt, 16 * nsm);
     cdc::k_maxp_link<<<eblocks, cdc::MX_ETILE, 0, st>>>(P.Q, X);
+    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
     CDC_KCHECK("k_maxp_link", st);
     cdc::k_maxp_path<<<1, 256, 0, st>>>(P.Q, X);
+    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
     CDC_KCHECK("k_maxp_path", st);
     cdc::k_maxp_write<<<eblocks, cdc::MX_ETILE, 0, st>>>(P.Q, X, d_bounds, cap, d_count);
+    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
     CDC_KCHECK("k_maxp_write", st);
     g_launches = 6;
     CDC_CUDA(cudaGetLastError());
