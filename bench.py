@@ -426,6 +426,66 @@ def measure_c1(args, cdc, torch, dist, dev, world):
     return out
 
 
+MX_STREAM = 1 << 30
+
+
+def measure_maxp(args, cdc, torch, dist, dev, world):
+    """MAXP (§2.1.2 l.173/l.196; not in BASELINE's configs -- the algorithm
+    the paper accelerates besides AE and RAM): one 1 GiB uniform stream per rank at
+    the 8 KiB default (h = 447); CUDA graph of one call; the 1 GiB input exceeds L2."""
+    import synth
+    data_np = synth.uniform(MX_STREAM, 2)
+    data = torch.from_numpy(data_np).to(dev)
+    p = cdc.params("maxp", avg_size=8192)
+    cap = cdc.max_boundaries(p, MX_STREAM)
+    bounds = torch.empty(cap, dtype=torch.int64, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(cdc.workspace_size(p, 1, MX_STREAM, MX_STREAM), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        cdc.chunk_async(data, p, bounds, count, ws)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    n_bounds = int(count.item())
+    launches = cdc.last_launch_count()
+    if args.check:
+        import oracle
+        bad = oracle.check_chunking("maxp", data_np, bounds[:n_bounds].cpu().numpy().astype(np.uint64),
+                                    p.window, p.max_size)
+        assert bad is None, f"MAXP mismatch vs oracle at {bad}"
+    graph = make_graph(torch, dev, stream, step, 1)
+
+    def run(k):
+        for _ in range(k):
+            graph.replay()
+
+    steps = max(args.steps, 10)
+    ms = timed(run, steps, stream, dist, dev, torch)
+    peak, peak_src = load_peaks()
+    call_gbs = MX_STREAM * steps / (ms / 1e3) / 1e9
+    tile = 32768  # k_maxp_scan reads each 32 KiB tile with both h-byte margins
+    read = MX_STREAM + (MX_STREAM // tile) * 2 * p.window
+    out = {
+        "workload": "MAXP avg 8 KiB (window h = 447 per side, max_size 32 KiB), one 1 GiB stream of uniform bytes, "
+                    "seed 2, on every rank",
+        "value": round(call_gbs * world, 2), "unit": "GB/s", "ms_per_step": round(ms / steps, 4), "steps": steps,
+        "boundaries": n_bounds, "scaling": "weak", "gpu_launches": launches * steps,
+        "roofline": {"bound": "hbm", "kernel": "k_maxp_scan..k_maxp_write (whole call)",
+                     "achieved": round(read * steps / (ms / 1e3) / 1e9, 1), "peak": peak, "peak_source": peak_src,
+                     "unit": "GB/s", "frac": round(read * steps / (ms / 1e3) / 1e9 / peak, 4),
+                     "algorithmic_gb_per_launch": round(read / 1e9, 4),
+                     "per_unit": "every input byte read once, plus the two h-byte margins of each 32 KiB tile "
+                                 "(DESIGN.md §5, MAXP)"},
+        "timing": "CUDA graph of one call, events on the launch stream, max over ranks",
+    }
+    del data, ws, bounds
+    torch.cuda.empty_cache()
+    return out
+
+
 def measure_c4(args, cdc, torch, dist, dev, world, rank):
     """configs[4]: one 64 GiB stream split by byte range with a halo over the ranks
     (shard.chunk_sharded through the public API; NCCL all_gather of edge chain
@@ -492,6 +552,7 @@ def main():
     c1 = None if args.no_secondary else measure_c1(args, cdc, torch, dist, dev, world)
     c3 = measure_c3(args, cdc, torch, dist, dev, world, rank, local)
     c4 = None if args.no_secondary else measure_c4(args, cdc, torch, dist, dev, world, rank)
+    mx = None if args.no_secondary else measure_maxp(args, cdc, torch, dist, dev, world)
 
     if rank == 0:
         ms = c3["ms"]
@@ -549,6 +610,8 @@ def main():
             line["configs1"] = c1
         if c4 is not None:
             line["configs4_sharded"] = c4
+        if mx is not None:
+            line["maxp"] = mx
         line["paper_cpu_vector"] = PAPER_CPU
         print(json.dumps(line), flush=True)
     if dist is not None:
