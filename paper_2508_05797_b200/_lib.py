@@ -11,6 +11,7 @@ import os
 from .build import LIB
 
 # CDC_LIB selects another build of the same library (tuning variants under build/)
+_DEFAULT_LIB = LIB
 LIB = os.environ.get("CDC_LIB", LIB)
 if not os.path.exists(LIB):
     raise ImportError(
@@ -62,6 +63,8 @@ SIGNATURES = {
 }
 
 for _name, (_args, _res) in SIGNATURES.items():
+    if LIB != _DEFAULT_LIB and not hasattr(lib, _name):
+        continue  # an older tuning build under build/ (CDC_LIB) may lack newer entry points
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = _res
