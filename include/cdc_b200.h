@@ -64,8 +64,9 @@ typedef enum {
  * l.196; §4.3 l.361; readings M1-M5): the chunk from s ends right after the
  * first byte t in [s+h, s+max_size) that is greater than every byte of
  * [t-h, t) and of (t, t+h] (both windows inside the stream), with h = window
- * (at most 65536); single streams only (cdc_chunk, cdc_chunk_host; the batch,
- * chain and diagnostics entry points return CDC_ERR_INVALID for it).
+ * (at most 65536).  cdc_chunk, cdc_chunk_batch and the host entry points
+ * accept it; cdc_chain, cdc_stats, cdc_fetched, cdc_plan_info and
+ * cdc_plan_segments (speculative segments) return CDC_ERR_INVALID for it.
  */
 typedef enum { CDC_RAM = 0, CDC_AE_MAX = 1, CDC_AE_MIN = 2, CDC_MAXP = 3 } cdc_algo;
 

@@ -2238,7 +2238,9 @@ struct MaxpPlan {
     cdc::MaxpGeo Q;
     uint64_t nlt;           // link / write tiles
     uint64_t ngc;           // k_maxp_gather CTAs
-    size_t off_q, off_qt, off_qn, off_f, off_ncap, off_jl, off_reset, reset_bytes, bytes;
+    uint64_t nfc;           // k_maxp_files CTAs
+    size_t off_tfirst, off_tfile, off_qt, off_qn, off_qx, off_efile, off_estart, off_f, off_ncap, off_jl;
+    size_t off_reset, reset_bytes, bytes;
     uint32_t smem;          // k_maxp_scan dynamic shared memory
 };
 uint32_t maxp_smem(uint64_t h, uint32_t &buf, uint32_t &ccap) {
@@ -2246,46 +2248,59 @@ uint32_t maxp_smem(uint64_t h, uint32_t &buf, uint32_t &ccap) {
     ccap = (uint32_t)(cdc::MX_TILE / (h + 1) + 2);
     return buf + 3 * (buf / 16) + 16 + 2 * ccap + 128;
 }
-void maxp_plan(const cdc_params *p, uint64_t L, MaxpPlan &P) {
+// nfiles streams totalling total bytes (a single stream: nfiles = 1)
+void maxp_plan(const cdc_params *p, uint64_t nfiles, uint64_t total, MaxpPlan &P) {
     cdc::MaxpGeo &Q = P.Q;
     Q.data = nullptr;
-    Q.L = L;
+    Q.file_off = nullptr;
+    Q.nfiles = nfiles;
+    Q.L = total;
     Q.h = p->window;
     Q.M = p->max_size;
-    Q.ntiles = (L + cdc::MX_TILE - 1) / cdc::MX_TILE;
-    Q.qcap = L / (Q.h + 1) + 2;  // two local maxima are more than h apart
+    Q.ntiles = total / cdc::MX_TILE + nfiles;           // >= sum of max(1, ceil(len / MX_TILE))
+    Q.qcap = total / (Q.h + 1) + 2 * nfiles + 2;         // maxima are > h apart; one start per file
     P.smem = maxp_smem(Q.h, Q.buf, Q.ccap);
-    P.nlt = (Q.qcap + 1 + cdc::MX_ETILE - 1) / cdc::MX_ETILE;
+    P.nlt = (Q.qcap + cdc::MX_ETILE - 1) / cdc::MX_ETILE;
     P.ngc = (Q.ntiles + cdc::MX_GTILES - 1) / cdc::MX_GTILES;
+    P.nfc = (nfiles + cdc::MX_FTHREADS - 1) / cdc::MX_FTHREADS;
     size_t o = 0;
-    P.off_q = o;
-    o = round_up(o + Q.qcap * 8, 256);
-    P.off_qt = o;
-    o = round_up(o + Q.ntiles * Q.ccap * 2, 256);
-    P.off_qn = o;
-    o = round_up(o + Q.ntiles * 4, 256);
-    P.off_f = o;
-    o = round_up(o + (Q.qcap + 1) * 8, 256);
-    P.off_ncap = o;
-    o = round_up(o + (Q.qcap + 1) * 8, 256);
-    P.off_jl = o;
-    o = round_up(o + (Q.qcap + 1) * 8, 256);
-    P.off_reset = o;  // tst, lst, wst, ctrl, nq, nj, on -- reset to all-ones by k_reset
-    P.reset_bytes = round_up(P.ngc * 8 + 2 * P.nlt * 8 + 32 + 16 + (Q.qcap + 1), 256);
+    auto take = [&](size_t bytes) {
+        const size_t at = o;
+        o = round_up(o + bytes, 256);
+        return at;
+    };
+    P.off_tfirst = take((nfiles + 1) * 8);
+    P.off_tfile = take(Q.ntiles * 4);
+    P.off_qt = take(Q.ntiles * Q.ccap * 2);
+    P.off_qn = take(Q.ntiles * 4);
+    P.off_qx = take(Q.qcap * 8);
+    P.off_efile = take(Q.qcap * 4);
+    P.off_estart = take((nfiles + 1) * 8);
+    P.off_f = take(Q.qcap * 8);
+    P.off_ncap = take(Q.qcap * 8);
+    P.off_jl = take(Q.qcap * 8);
+    P.off_reset = o;  // fst, tst, lst, wst, ctrl, nq, nj, on -- reset to all-ones by k_reset
+    P.reset_bytes = round_up((P.nfc + P.ngc + 2 * P.nlt) * 8 + 32 + 16 + Q.qcap, 256);
     P.bytes = o + P.reset_bytes;
 }
 cdc::MaxpWork maxp_carve(const MaxpPlan &P, void *ws) {
     uint8_t *b = static_cast<uint8_t *>(ws);
     cdc::MaxpWork X;
-    X.q = reinterpret_cast<uint64_t *>(b + P.off_q);
+    X.tfirst = reinterpret_cast<uint64_t *>(b + P.off_tfirst);
+    X.tfile = reinterpret_cast<uint32_t *>(b + P.off_tfile);
     X.qt = reinterpret_cast<uint16_t *>(b + P.off_qt);
     X.qn = reinterpret_cast<uint32_t *>(b + P.off_qn);
+    X.qx = reinterpret_cast<int64_t *>(b + P.off_qx);
+    X.efile = reinterpret_cast<uint32_t *>(b + P.off_efile);
+    X.estart = reinterpret_cast<uint64_t *>(b + P.off_estart);
     X.f = reinterpret_cast<int64_t *>(b + P.off_f);
     X.ncap = reinterpret_cast<uint64_t *>(b + P.off_ncap);
     X.jl = reinterpret_cast<int64_t *>(b + P.off_jl);
+    X.bo = nullptr;
     unsigned long long *r = reinterpret_cast<unsigned long long *>(b + P.off_reset);
-    X.tst = r;
-    X.lst = r + P.ngc;
+    X.fst = r;
+    X.tst = X.fst + P.nfc;
+    X.lst = X.tst + P.ngc;
     X.wst = X.lst + P.nlt;
     X.ctrl = reinterpret_cast<uint32_t *>(X.wst + P.nlt);
     X.nq = reinterpret_cast<unsigned long long *>(X.ctrl + 8);
@@ -2294,18 +2309,18 @@ cdc::MaxpWork maxp_carve(const MaxpPlan &P, void *ws) {
     return X;
 }
 
-int launch_maxp(const cdc_params *p, const uint8_t *d_data, uint64_t L, uint64_t *d_bounds, uint64_t cap,
-                uint64_t *d_count, void *ws, size_t ws_bytes, cudaStream_t st) {
+// MAXP over one stream (d_file_off null, nfiles 1) or a packed batch (d_bound_off
+// receives each file's first output index).
+int launch_maxp(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file_off, uint64_t nfiles,
+                uint64_t total, uint64_t *d_bounds, uint64_t cap, uint64_t *d_bound_off, uint64_t *d_count, void *ws,
+                size_t ws_bytes, cudaStream_t st) {
     MaxpPlan P;
-    maxp_plan(p, L, P);
+    maxp_plan(p, nfiles, total, P);
     if (ws_bytes < P.bytes) return fail(CDC_ERR_WORKSPACE, "workspace too small");
-    if (L == 0) {
-        CDC_CUDA(cudaMemsetAsync(d_count, 0, 8, st));
-        g_launches = 0;
-        return CDC_OK;
-    }
     P.Q.data = d_data;
-    const cdc::MaxpWork X = maxp_carve(P, ws);
+    P.Q.file_off = d_file_off;
+    cdc::MaxpWork X = maxp_carve(P, ws);
+    X.bo = d_bound_off;
     static bool attr[MAX_DEVICES] = {false};
     const int dev = current_device();
     if (!attr[dev]) {  // the largest window's tile (per device: a context attribute)
@@ -2318,29 +2333,32 @@ int launch_maxp(const cdc_params *p, const uint8_t *d_data, uint64_t L, uint64_t
     const uint64_t n16 = P.reset_bytes / 16;
     cdc::k_reset<<<(unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * nsm), 256, 0, st>>>(
         reinterpret_cast<uint4 *>(static_cast<uint8_t *>(ws) + P.off_reset), n16, nullptr);
+    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
     CDC_KCHECK("k_reset (MAXP)", st);
+    cdc::k_maxp_files<<<(unsigned)P.nfc, cdc::MX_FTHREADS, 0, st>>>(P.Q, X);
+    CDC_CUDA(cudaGetLastError());
+    CDC_KCHECK("k_maxp_files", st);
     int per_sm = 0;
     CDC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cdc::k_maxp_scan, cdc::MX_THREADS, P.smem));
     const uint64_t sblocks = std::min<uint64_t>(P.Q.ntiles, nsm * (uint64_t)std::max(per_sm, 1));
     cdc::k_maxp_scan<<<(unsigned)sblocks, cdc::MX_THREADS, P.smem, st>>>(P.Q, X);
-    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
+    CDC_CUDA(cudaGetLastError());
     CDC_KCHECK("k_maxp_scan", st);
     cdc::k_maxp_gather<<<(unsigned)P.ngc, cdc::MX_GTILES, 0, st>>>(P.Q, X);
-    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
+    CDC_CUDA(cudaGetLastError());
     CDC_KCHECK("k_maxp_gather", st);
-    // element tiles: one per CTA (the grid covers the capacity; CTAs past nQ exit)
+    // element tiles: CTAs take them from a ticket (the grid covers the capacity; CTAs past the count exit)
     const unsigned eblocks = (unsigned)std::min<uint64_t>(P.nlt, 16 * nsm);
     cdc::k_maxp_link<<<eblocks, cdc::MX_ETILE, 0, st>>>(P.Q, X);
-    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
+    CDC_CUDA(cudaGetLastError());
     CDC_KCHECK("k_maxp_link", st);
     cdc::k_maxp_path<<<1, 256, 0, st>>>(P.Q, X);
-    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
+    CDC_CUDA(cudaGetLastError());
     CDC_KCHECK("k_maxp_path", st);
     cdc::k_maxp_write<<<eblocks, cdc::MX_ETILE, 0, st>>>(P.Q, X, d_bounds, cap, d_count);
-    CDC_CUDA(cudaGetLastError());  // a launch error stops the pipeline here
-    CDC_KCHECK("k_maxp_write", st);
-    g_launches = 6;
     CDC_CUDA(cudaGetLastError());
+    CDC_KCHECK("k_maxp_write", st);
+    g_launches = 7;
     return CDC_OK;
 }
 
@@ -2352,11 +2370,9 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     if (!d_count || (!d_bounds && cap) || (total_len && !d_data) || !ws)
         return fail(CDC_ERR_INVALID, "null pointer argument");
     if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(CDC_ERR_INVALID, "workspace must be 256-byte aligned");
-    if (p->algo == CDC_MAXP) {
-        if (batch) return fail(CDC_ERR_INVALID, "MAXP: single streams only (cdc_chunk / cdc_chunk_host)");
-        return launch_maxp(p, d_data, total_len, d_bounds, cap, d_count, ws, ws_bytes,
-                           static_cast<cudaStream_t>(stream));
-    }
+    if (p->algo == CDC_MAXP)
+        return launch_maxp(p, d_data, batch ? d_file_off : nullptr, batch ? nfiles : 1, total_len, d_bounds, cap,
+                           batch ? d_bound_off : nullptr, d_count, ws, ws_bytes, static_cast<cudaStream_t>(stream));
     Plan P;
     make_plan(p, nfiles, total_len, max_len, P);
     if (ws_bytes < P.bytes) return fail(CDC_ERR_WORKSPACE, "workspace too small");
@@ -2675,9 +2691,8 @@ int cdc_workspace_size(const cdc_params *p, uint64_t nfiles, uint64_t total_len,
     if (rc) return rc;
     if (!bytes) return fail(CDC_ERR_INVALID, "null bytes");
     if (p->algo == CDC_MAXP) {
-        if (nfiles > 1) return fail(CDC_ERR_INVALID, "MAXP: single streams only");
         MaxpPlan M;
-        maxp_plan(p, total_len, M);
+        maxp_plan(p, nfiles ? nfiles : 1, total_len, M);
         *bytes = M.bytes;
         return CDC_OK;
     }

@@ -15,7 +15,11 @@
 //     windows are checked byte by byte.  Each tile writes its maxima to its
 //     own slot (no tile waits for another); k_maxp_gather then concatenates
 //     the slots in stream order (a scan of the tile counts) into one
-//     ascending list q[].
+//     ascending list of elements: per file, a virtual "file start" element
+//     followed by the file's maxima (file-relative positions).
+//  0. (k_maxp_files) A batch: tiles never cross files; every file gets
+//     max(1, ceil(len / MX_TILE)) tiles, the tile table comes from a scan of
+//     those counts.  A single stream is a batch of one file.
 //  2. The chain (what depends on chunk starts): from a start s the chunk ends
 //     after the first local maximum in [s+h, s+max_size) (M3, R5), else it is
 //     capped.  Two local maxima are more than h apart, so after a content
@@ -38,28 +42,46 @@ constexpr int MX_GTILES = 1024;        // scan tiles per k_maxp_gather CTA (one 
 
 struct MaxpGeo {
     const uint8_t *data;
-    uint64_t L, h, M;      // stream length, window per side, max_size
-    uint64_t ntiles;       // scan tiles
-    uint64_t qcap;         // capacity of q (L / (h+1) + 2: local maxima are > h apart)
+    const uint64_t *file_off;  // batch: nfiles+1 file offsets into data; null: one stream of L bytes
+    uint64_t nfiles;
+    uint64_t L, h, M;      // stream (or batch) length, window per side, max_size
+    uint64_t ntiles;       // scan tiles (an upper bound for a batch: the files' count is on the device)
+    uint64_t qcap;         // element capacity (L / (h+1) + 2 nfiles + 2: local maxima are > h apart)
     uint32_t buf;          // bytes of a tile's byte buffer in shared memory
     uint32_t ccap;         // candidates per tile (uint16 offsets)
 };
 struct MaxpWork {
-    uint64_t *q;                 // local maxima, ascending (qcap)
+    uint64_t *tfirst;            // nfiles+1: first scan tile of each file (the last: the tile count)
+    uint32_t *tfile;             // file of each scan tile
     uint16_t *qt;                // scan tile t's maxima (offsets from the tile start): [t * ccap, ...)
     uint32_t *qn;                // ... and their number
-    int64_t *f;                  // element e = i + 1 (i in [-1, nQ)): the element where i's run ends (nQ: the stream end)
+    int64_t *qx;                 // elements: a file's start (-1), then its maxima (file-relative), file by file
+    uint32_t *efile;             // file of each element
+    uint64_t *estart;            // nfiles+1: each file's start element (the last: the element count)
+    int64_t *f;                  // element e: the element where e's chunk run ends (estart[file+1]: the file end)
     uint64_t *ncap;              // ... and the number of capped chunks in that run
     int64_t *jl;                 // elements whose run skips a local maximum, ascending
+    uint64_t *bo;                // batch: nfiles+1 output offsets of each file's boundaries (null: one stream)
     // reset to ~0 (all-ones) before every call:
+    unsigned long long *fst;     // file-table CTAs' look-back words
     unsigned long long *tst;     // gather CTAs' look-back words
     unsigned long long *lst;     // link tiles' look-back words
     unsigned long long *wst;     // write tiles' look-back words
-    uint32_t *ctrl;              // [0] scan ticket, [1] link ticket, [2] write ticket, [3] gather ticket
-    unsigned long long *nq;      // number of local maxima (written by the last scan tile)
+    uint32_t *ctrl;              // tickets: [0] scan, [1] link, [2] write, [3] gather, [4] file table
+    unsigned long long *nq;      // number of elements (written by the last gather CTA)
     unsigned long long *nj;      // number of skipping runs (last link tile)
     uint8_t *on;                 // element e: 0xFF on the chain, 0 skipped
 };
+
+__device__ __forceinline__ void mx_file(const MaxpGeo &Q, uint64_t F, uint64_t &off, uint64_t &len) {
+    if (Q.file_off == nullptr) {
+        off = 0;
+        len = Q.L;
+    } else {
+        off = Q.file_off[F];
+        len = Q.file_off[F + 1] - off;
+    }
+}
 
 // byte-wise maximum of a 16-byte granule (four 4-way byte maxima, then the word's bytes)
 __device__ __forceinline__ uint32_t granule_max(const uint4 &v) {
@@ -116,6 +138,40 @@ __device__ __forceinline__ uint64_t mx_tile_prefix(unsigned long long *st, uint6
     return r;
 }
 
+constexpr int MX_FTHREADS = 1024;  // k_maxp_files: files per CTA (one thread each)
+// K0: the tile table: file F owns tiles [tfirst[F], tfirst[F+1]), max(1, ceil(len/MX_TILE))
+// of them (an empty file keeps one, so that every file has a start element).
+__global__ void __launch_bounds__(MX_FTHREADS) k_maxp_files(MaxpGeo Q, MaxpWork X) {
+    __shared__ uint32_t s_tile, s_scr[64];
+    __shared__ uint64_t s_slot;
+    if (threadIdx.x == 0) s_tile = atomicAdd(X.ctrl + 4, 1u) + 1u;
+    __syncthreads();
+    const uint64_t g = s_tile;
+    const uint64_t F = g * MX_FTHREADS + threadIdx.x;
+    uint32_t n = 0;
+    uint64_t off = 0, len = 0;
+    if (F < Q.nfiles) {
+        mx_file(Q, F, off, len);
+        n = len == 0 ? 1u : (uint32_t)((len + MX_TILE - 1) / MX_TILE);
+    }
+    uint32_t tot;
+    const uint32_t o = mx_block_scan(n, tot, s_scr);
+    const uint64_t excl = mx_tile_prefix(X.fst, g, tot, &s_slot);
+    if (F < Q.nfiles) X.tfirst[F] = excl + o;
+    // tile -> file map (a single stream has none: its scan and gather know the file is 0); each
+    // warp writes its 32 files' tiles with all lanes, so one large file is not one thread's loop
+    if (Q.file_off != nullptr) {
+        const int lane = threadIdx.x & 31;
+        for (int r = 0; r < 32; ++r) {
+            const uint32_t rn = __shfl_sync(0xFFFFFFFFu, n, r);
+            const uint64_t rt = __shfl_sync(0xFFFFFFFFu, excl + o, r);
+            const uint32_t rF = __shfl_sync(0xFFFFFFFFu, (uint32_t)F, r);
+            for (uint32_t k = lane; k < rn; k += 32) X.tfile[rt + k] = rF;
+        }
+    }
+    if ((g + 1) * MX_FTHREADS >= Q.nfiles && threadIdx.x == 0) X.tfirst[Q.nfiles] = excl + tot;
+}
+
 // K1: local maxima, tile by tile in ticket order.
 __global__ void __launch_bounds__(MX_THREADS) k_maxp_scan(MaxpGeo Q, MaxpWork X) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -127,7 +183,8 @@ __global__ void __launch_bounds__(MX_THREADS) k_maxp_scan(MaxpGeo Q, MaxpWork X)
     uint8_t *pf = gm + NGmax, *sf = pf + NGmax;            // van Herk prefix / suffix maxima
     uint16_t *cand = reinterpret_cast<uint16_t *>(sf + NGmax + (16 - (3 * NGmax) % 16) % 16);
     const int tid = threadIdx.x;
-    const uint64_t h = Q.h, L = Q.L;
+    const uint64_t h = Q.h;
+    const uint64_t ntot = X.tfirst[Q.nfiles];
     if (tid == 0) {
         mbar_init(&bar, 1);
         fence_barrier_init();
@@ -138,9 +195,17 @@ __global__ void __launch_bounds__(MX_THREADS) k_maxp_scan(MaxpGeo Q, MaxpWork X)
         if (tid == 0) s_tile = atomicAdd(X.ctrl, 1u) + 1u;  // the counter starts at ~0
         __syncthreads();
         const uint64_t t = s_tile;
-        if (t >= Q.ntiles) break;
-        // candidate positions of the tile: [ca, cb) inside [h, L - h)
-        const uint64_t a = t * MX_TILE, b = a + MX_TILE < L ? a + MX_TILE : L;
+        if (t >= ntot) break;
+        // the tile's file and its candidate positions [ca, cb) inside [h, L - h) (file-relative;
+        // a single stream skips the table lookups, which would sit before the copy)
+        uint64_t foff = 0, L = Q.L, a = t * MX_TILE;
+        if (Q.file_off != nullptr) {
+            const uint32_t F = X.tfile[t];
+            mx_file(Q, F, foff, L);
+            a = (t - X.tfirst[F]) * MX_TILE;
+        }
+        const uint8_t *data = Q.data + foff;
+        const uint64_t b = a + MX_TILE < L ? a + MX_TILE : L;
         const uint64_t ca = a > h ? a : h;
         const uint64_t cb = (L > h && b > L - h) ? L - h : (L > h ? b : 0);
         uint32_t count = 0;
@@ -149,10 +214,10 @@ __global__ void __launch_bounds__(MX_THREADS) k_maxp_scan(MaxpGeo Q, MaxpWork X)
         if (ca < cb) {
             // bytes [lo, hi) = [ca - h, cb + h): one bulk copy of the 16-byte granules holding them
             const uint64_t lo = ca - h, hi = cb + h;
-            const uintptr_t A0 = reinterpret_cast<uintptr_t>(Q.data + lo) & ~static_cast<uintptr_t>(15);
-            const uintptr_t A1 = (reinterpret_cast<uintptr_t>(Q.data + hi) + 15) & ~static_cast<uintptr_t>(15);
+            const uintptr_t A0 = reinterpret_cast<uintptr_t>(data + lo) & ~static_cast<uintptr_t>(15);
+            const uintptr_t A1 = (reinterpret_cast<uintptr_t>(data + hi) + 15) & ~static_cast<uintptr_t>(15);
             const uint32_t nbytes = (uint32_t)(A1 - A0);
-            const uint32_t off0 = (uint32_t)(reinterpret_cast<uintptr_t>(Q.data + lo) - A0);
+            const uint32_t off0 = (uint32_t)(reinterpret_cast<uintptr_t>(data + lo) - A0);
             if (tid == 0) {
                 mbar_arrive_expect_tx(&bar, nbytes);
                 asm volatile(
@@ -273,52 +338,71 @@ __global__ void __launch_bounds__(MX_THREADS) k_maxp_scan(MaxpGeo Q, MaxpWork X)
     if (tid == 0) mbar_inval(&bar);
 }
 
-// K1b: the tiles' maxima concatenated in stream order: one thread per scan
-// tile, a block scan of the counts, a decoupled look-back over the CTAs.
+// K1b: the elements, file by file: one thread per scan tile, a block scan of
+// the tile counts and a decoupled look-back over the CTAs give the tile's
+// first element; file F's start element sits before its first tile's maxima.
 __global__ void __launch_bounds__(MX_GTILES) k_maxp_gather(MaxpGeo Q, MaxpWork X) {
     __shared__ uint32_t s_tile, s_scr[64];
     __shared__ uint64_t s_slot;
     if (threadIdx.x == 0) s_tile = atomicAdd(X.ctrl + 3, 1u) + 1u;  // CTAs in ticket order
     __syncthreads();
+    const uint64_t ntot = X.tfirst[Q.nfiles];
     const uint64_t g = s_tile;
     const uint64_t t = g * MX_GTILES + threadIdx.x;
-    const uint32_t n = t < Q.ntiles ? X.qn[t] : 0u;
+    const uint32_t n = t < ntot ? X.qn[t] : 0u;
     uint32_t tot;
     const uint32_t o = mx_block_scan(n, tot, s_scr);
     const uint64_t excl = mx_tile_prefix(X.tst, g, tot, &s_slot);
-    const uint64_t base = t * (uint64_t)MX_TILE;
-    for (uint32_t i = 0; i < n; ++i) X.q[excl + o + i] = base + X.qt[t * Q.ccap + i];
-    if ((g + 1) * MX_GTILES >= Q.ntiles && threadIdx.x == 0) *X.nq = excl + tot;
+    if (t < ntot) {
+        const uint32_t F = Q.file_off != nullptr ? X.tfile[t] : 0u;
+        const uint64_t t0 = Q.file_off != nullptr ? X.tfirst[F] : 0u;
+        const uint64_t e0 = excl + o + F + 1;  // maxima before this tile, plus the starts of files 0..F
+        if (t == t0) {                          // the file's start element
+            X.qx[e0 - 1] = -1;
+            X.efile[e0 - 1] = F;
+            X.estart[F] = e0 - 1;
+        }
+        const int64_t a = (int64_t)(t - t0) * MX_TILE;
+        for (uint32_t i = 0; i < n; ++i) {
+            X.qx[e0 + i] = a + X.qt[t * Q.ccap + i];
+            X.efile[e0 + i] = F;
+        }
+    }
+    if ((g + 1) * MX_GTILES >= ntot && threadIdx.x == 0) {
+        *X.nq = excl + tot + Q.nfiles;
+        X.estart[Q.nfiles] = excl + tot + Q.nfiles;
+    }
 }
 
-// Where the chunk run that starts after element i ends (i = -1: the stream
-// start): the first local maximum q[f] in [s+h, s+M) of the current start s
-// ends it; capped chunks move s by M; maxima within h of a start are skipped
-// (M3).  f = nQ: the run ends at the stream end.  Mirrors the chain rule of
-// PAPER.md §2.1.2 l.196 with R5's cap, one start at a time.
-__device__ __forceinline__ void maxp_run(const MaxpGeo &Q, const uint64_t *q, uint64_t nQ, int64_t i, int64_t &f,
-                                         uint64_t &ncap) {
-    const uint64_t L = Q.L, h = Q.h, M = Q.M;
-    uint64_t s = i < 0 ? 0 : q[i] + 1;
-    uint64_t j = (uint64_t)(i + 1);
+// Where the chunk run that starts at element e ends: its start s is the file
+// start (qx[e] < 0) or right after the maximum qx[e]; the first maximum q[j] in
+// [s+h, s+M) ends the chunk; capped chunks move s by M; maxima within h of a
+// start are skipped (M3).  f = jend (the next file's start element): the run
+// ends at the file end.  Mirrors the chain rule of PAPER.md §2.1.2 l.196 with
+// R5's cap, one start at a time.
+__device__ __forceinline__ void maxp_run(const MaxpGeo &Q, const int64_t *q, uint64_t L, uint64_t e, uint64_t jend,
+                                         int64_t &f, uint64_t &ncap) {
+    const uint64_t h = Q.h, M = Q.M;
+    uint64_t s = q[e] < 0 ? 0 : (uint64_t)q[e] + 1;
+    uint64_t j = e + 1;
     ncap = 0;
     for (;;) {
-        while (j < nQ && q[j] < s + h) ++j;                  // too close to the chunk start
+        while (j < jend && (uint64_t)q[j] < s + h) ++j;      // too close to the chunk start
         const uint64_t limit = (L - s < M) ? L : s + M;
-        if (j < nQ && q[j] < limit) {                        // content boundary right after q[j]
+        if (j < jend && (uint64_t)q[j] < limit) {            // content boundary right after q[j]
             f = (int64_t)j;
             return;
         }
-        if (limit == L) {                                    // the chunk ends at the stream end
-            f = (int64_t)nQ;
+        if (limit == L) {                                    // the chunk ends at the file end
+            f = (int64_t)jend;
             return;
         }
-        if (j >= nQ) {                                       // capped chunks up to the stream end
+        if (j >= jend) {                                     // capped chunks up to the file end
             ncap += (L - s - 1) / M;
-            f = (int64_t)nQ;
+            f = (int64_t)jend;
             return;
         }
-        const uint64_t k = (q[j] - s) / M;                   // >= 1: capped chunks before q[j]'s
+        const uint64_t k = ((uint64_t)q[j] - s) / M;         // >= 1: capped chunks before q[j]'s
         ncap += k;
         s += k * M;
     }
@@ -328,8 +412,8 @@ __device__ __forceinline__ void maxp_run(const MaxpGeo &Q, const uint64_t *q, ui
 __global__ void __launch_bounds__(MX_ETILE) k_maxp_link(MaxpGeo Q, MaxpWork X) {
     __shared__ uint32_t s_tile, s_scr[64];
     __shared__ uint64_t s_slot;
-    const uint64_t nQ = *X.nq;
-    const uint64_t ntl = (nQ + 1 + MX_ETILE - 1) / MX_ETILE;
+    const uint64_t nE = *X.nq;
+    const uint64_t ntl = (nE + MX_ETILE - 1) / MX_ETILE;
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(X.ctrl + 1, 1u) + 1u;
         __syncthreads();
@@ -337,27 +421,30 @@ __global__ void __launch_bounds__(MX_ETILE) k_maxp_link(MaxpGeo Q, MaxpWork X) {
         if (t >= ntl) break;
         const uint64_t e = t * MX_ETILE + threadIdx.x;
         bool jump = false;
-        int64_t i = (int64_t)e - 1, f = 0;
-        if (e <= nQ) {
+        if (e < nE) {
+            const uint32_t F = X.efile[e];
+            uint64_t off, L;
+            mx_file(Q, F, off, L);
+            int64_t f;
             uint64_t nc;
-            maxp_run(Q, X.q, nQ, i, f, nc);
+            maxp_run(Q, X.qx, L, e, X.estart[F + 1], f, nc);
             X.f[e] = f;
             X.ncap[e] = nc;
-            jump = f > i + 1;
+            jump = f > (int64_t)e + 1;
         }
         uint32_t tot;
         const uint32_t o = mx_block_scan(jump ? 1u : 0u, tot, s_scr);
         const uint64_t excl = mx_tile_prefix(X.lst, t, tot, &s_slot);
-        if (jump) X.jl[excl + o] = i;
+        if (jump) X.jl[excl + o] = (int64_t)e;
         if (t == ntl - 1 && threadIdx.x == 0) *X.nj = excl + tot;
         __syncthreads();
     }
 }
 
-// K3 (one warp): the skipping runs in stream order.  A run is on the chain
+// K3 (one CTA): the skipping runs in stream order.  A run is on the chain
 // unless an earlier run on the chain jumped over its element; the elements a
 // chain run jumps over are marked off the chain.  (Runs skip maxima only in
-// capped stretches, so the list is short.)
+// capped stretches, so the list is short; a run never passes its file's end.)
 constexpr int MX_PATH_BATCH = 2048;  // skipping runs staged in shared memory per round
 __global__ void __launch_bounds__(256) k_maxp_path(MaxpGeo Q, MaxpWork X) {
     __shared__ int64_t s_i[MX_PATH_BATCH], s_f[MX_PATH_BATCH];
@@ -368,18 +455,18 @@ __global__ void __launch_bounds__(256) k_maxp_path(MaxpGeo Q, MaxpWork X) {
         const uint64_t m = nj - k0 < MX_PATH_BATCH ? nj - k0 : MX_PATH_BATCH;
         __syncthreads();
         for (uint64_t k = threadIdx.x; k < m; k += blockDim.x) {
-            const int64_t i = X.jl[k0 + k];
-            s_i[k] = i;
-            s_f[k] = X.f[i + 1];
+            const int64_t e = X.jl[k0 + k];
+            s_i[k] = e;
+            s_f[k] = X.f[e];
         }
         __syncthreads();
         if (threadIdx.x < 32) {
             int64_t cur = s_cur;
             for (uint64_t k = 0; k < m; ++k) {
-                const int64_t i = s_i[k];
-                if (i < cur) continue;  // inside that run: not on the chain
+                const int64_t e = s_i[k];
+                if (e < cur) continue;  // inside that run: not on the chain
                 const int64_t f = s_f[k];
-                for (int64_t x = i + 1 + (int64_t)threadIdx.x; x < f; x += 32) X.on[x + 1] = 0;
+                for (int64_t x = e + 1 + (int64_t)threadIdx.x; x < f; x += 32) X.on[x] = 0;
                 cur = f;
             }
             if (threadIdx.x == 0) s_cur = cur;
@@ -388,14 +475,16 @@ __global__ void __launch_bounds__(256) k_maxp_path(MaxpGeo Q, MaxpWork X) {
 }
 
 // K4: boundaries.  Element e on the chain contributes its capped chunks and the
-// chunk that ends its run; a decoupled look-back over the counts gives the
-// output offsets; each warp writes its 32 elements' runs with all lanes.
+// chunk that ends its run (a file start of an empty file: none); a decoupled
+// look-back over the counts gives the output offsets (a batch: a file's start
+// element's offset is the file's first output); each warp writes its 32
+// elements' runs with all lanes.  Ends are file-relative.
 __global__ void __launch_bounds__(MX_ETILE) k_maxp_write(MaxpGeo Q, MaxpWork X, uint64_t *bounds, uint64_t cap,
                                                          uint64_t *d_count) {
     __shared__ uint32_t s_tile, s_scr[64];
     __shared__ uint64_t s_slot;
-    const uint64_t nQ = *X.nq;
-    const uint64_t ntl = (nQ + 1 + MX_ETILE - 1) / MX_ETILE;
+    const uint64_t nE = *X.nq;
+    const uint64_t ntl = (nE + MX_ETILE - 1) / MX_ETILE;
     const int lane = threadIdx.x & 31;
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(X.ctrl + 2, 1u) + 1u;
@@ -404,18 +493,28 @@ __global__ void __launch_bounds__(MX_ETILE) k_maxp_write(MaxpGeo Q, MaxpWork X, 
         if (t >= ntl) break;
         const uint64_t e = t * MX_ETILE + threadIdx.x;
         uint64_t n = 0, nc = 0, s = 0, end = 0;
-        if (e <= nQ && X.on[e] != 0) {
-            nc = X.ncap[e];
-            n = nc + 1;
-            s = e == 0 ? 0 : X.q[e - 1] + 1;
-            const int64_t f = X.f[e];
-            end = f < (int64_t)nQ ? X.q[f] + 1 : Q.L;
+        bool fstart = false;
+        uint32_t F = 0;
+        if (e < nE) {
+            F = X.efile[e];
+            const int64_t qe = X.qx[e];
+            fstart = qe < 0;
+            uint64_t off, L;
+            mx_file(Q, F, off, L);
+            if (X.on[e] != 0 && L > 0) {
+                nc = X.ncap[e];
+                n = nc + 1;
+                s = fstart ? 0 : (uint64_t)qe + 1;
+                const int64_t f = X.f[e];
+                end = f < (int64_t)X.estart[F + 1] ? (uint64_t)X.qx[f] + 1 : L;
+            }
         }
         // per-thread counts can exceed 32 bits only for runs of > 4 G capped chunks
         uint32_t tot;
         const uint32_t o32 = mx_block_scan((uint32_t)n, tot, s_scr);
         const uint64_t excl = mx_tile_prefix(X.wst, t, tot, &s_slot);
         const uint64_t o = excl + o32;
+        if (fstart && X.bo) X.bo[F] = o;
         for (int r = 0; r < 32; ++r) {
             const uint64_t rn = __shfl_sync(0xFFFFFFFFu, n, r);
             if (rn == 0) continue;
@@ -426,8 +525,10 @@ __global__ void __launch_bounds__(MX_ETILE) k_maxp_write(MaxpGeo Q, MaxpWork X, 
                 if (idx < cap) bounds[idx] = k < rc ? rs + (k + 1) * Q.M : re;
             }
         }
-        if (t == ntl - 1 && threadIdx.x == 0) *d_count = excl + tot;
+        if (t == ntl - 1 && threadIdx.x == 0) {
+            *d_count = excl + tot;
+            if (X.bo) X.bo[Q.nfiles] = excl + tot;
+        }
         __syncthreads();
     }
 }
-

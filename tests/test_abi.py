@@ -125,7 +125,6 @@ def test_maxp_window_for_avg_closed_form(lib):
     # workspace sizing is host-only; batches are not defined for MAXP
     p = api.params("maxp", avg_size=8192)
     assert api.workspace_size(p, 1, 1 << 30, 1 << 30) > (1 << 30) // 448 * 8
-    with pytest.raises(api.CdcError):
-        api.workspace_size(p, 4, 1 << 20, 1 << 18)
+    assert api.workspace_size(p, 4, 1 << 20, 1 << 18) > 0  # batches of several streams
     with pytest.raises(api.CdcError):
         api.workspace_size(api.params("maxp", window=65537, max_size=1 << 20), 1, 1 << 20, 1 << 20)

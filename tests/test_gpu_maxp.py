@@ -145,6 +145,50 @@ def test_maxp_rejected_where_undefined(cdc):
     p = cdc.params("maxp", avg_size=8192)
     d = torch.from_numpy(synth.uniform(100000, 2)).cuda()
     with pytest.raises(cdc.CdcError):
-        cdc.chunk_batch(d, [0, 50000, 100000], p)
-    with pytest.raises(cdc.CdcError):
         cdc.chunk(d, cdc.params("maxp", window=65537, max_size=1 << 20))
+    with pytest.raises(cdc.CdcError):
+        cdc.stats(p, torch.empty(1 << 20, dtype=torch.uint8, device="cuda"), 1, 100000, 100000)
+
+
+def _check_batch(cdc, data, offs, h, mx):
+    p = cdc.params("maxp", window=h, max_size=mx)
+    b, bo = cdc.chunk_batch(torch.from_numpy(np.ascontiguousarray(data)).cuda(), offs, p)
+    got, gbo = b.cpu().numpy().astype(np.uint64), bo.cpu().numpy().astype(np.int64)
+    exp, ebo = oracle.chunk_batch("maxp", data, offs, h, mx)
+    assert np.array_equal(gbo, ebo), (h, mx, np.nonzero(gbo != ebo)[0][:5])
+    assert np.array_equal(got, exp), (h, mx)
+
+
+@pytest.mark.parametrize("h,mx", [(3, 40), (31, 700), (447, 32768), (2000, 9000)])
+def test_maxp_batch_random(cdc, h, mx):
+    """Packed batches: empty files, files shorter than h or 2h+1, files of several
+    tiles with ragged tails, each file chunked on its own (file-relative ends)."""
+    rng = np.random.default_rng(h)
+    for trial in range(4):
+        n = int(rng.integers(1, 300))
+        sizes = rng.choice([0, 1, 5, h, 2 * h, 2 * h + 1, 3000, TILE - 1, TILE + 7, 3 * TILE + 555], n)
+        sizes = np.where(rng.random(n) < 0.3, rng.integers(0, 200000, n), sizes)
+        offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        gen = [lambda m: synth.uniform(m, 40 + trial), lambda m: synth.zipf_bytes(m, 1.1, 41 + trial),
+               lambda m: _sparse_peaks(m, 42 + trial, 1 / 300, top=8)][trial % 3]
+        data = gen(int(max(offs[-1], 1)))[:offs[-1]]
+        _check_batch(cdc, data, offs, h, mx)
+
+
+def test_maxp_batch_all_empty_and_single(cdc):
+    _check_batch(cdc, np.zeros(0, np.uint8), np.zeros(4, np.int64), 447, 32768)
+    d = synth.uniform(5 * TILE + 3, 44)
+    _check_batch(cdc, d, np.array([0, d.size], np.int64), 447, 32768)
+
+
+def test_maxp_batch_many_files_configs3_shape(cdc):
+    """12,500 files of configs[3]'s size distribution and content mix at 8 KiB,
+    every chunk of every file verified (check_batch), and the host entry point."""
+    data, offs = synth.many_files(12500, seed=3)
+    p = cdc.params("maxp", avg_size=8192)
+    b, bo = cdc.chunk_batch(torch.from_numpy(data).cuda(), offs, p)
+    got, gbo = b.cpu().numpy().astype(np.uint64), bo.cpu().numpy().astype(np.uint64)
+    assert oracle.check_batch("maxp", data, offs, got, gbo, p.window, p.max_size) is None
+    hb, hbo = cdc.chunk_batch_host(data[:offs[2000]], offs[:2001], p)
+    assert np.array_equal(np.asarray(hb, dtype=np.uint64), got[:gbo[2000]])
+    assert np.array_equal(np.asarray(hbo, dtype=np.uint64), gbo[:2001])
