@@ -60,6 +60,9 @@ static_assert(BATCH_WARPS * Ring<BATCH_STAGE>::SMEM + 128 <= 227 * 1024, "batch 
 #endif
 constexpr int HEAD_KEEP = CDC_HEAD_KEEP;  // bytes of each segment head kept in L2 for the halo re-read
 constexpr int RESOLVE_THREADS = 1024;
+#ifndef CDC_RING_OPAQUE
+#define CDC_RING_OPAQUE 1  // keep k_speculate's ring pointer in a register (A/B knob)
+#endif
 #ifndef CDC_PUB_RELEASE
 #define CDC_PUB_RELEASE 0  // 1: publish a list's final count with a release store (A/B)
 #endif
@@ -621,10 +624,14 @@ __global__ void __launch_bounds__(NW * 32, SPEC_CTAS_PER_SM) k_speculate(Geometr
     }
     if (spw != 0 && warp >= spw) return;
     constexpr int RS = Ring<STG>::SMEM;
-    uint64_t *fetch = reinterpret_cast<uint64_t *>(align_smem(smem) + warp * RS + Ring<STG>::BYTES) + FETCH_SLOT;
+    // the warp's ring: kept in a register (opaque to the compiler), so that the
+    // walk does not rebuild it (thread index, alignment, multiply) at every use
+    uint8_t *ring = align_smem(smem) + warp * RS;
+    if (CDC_RING_OPAQUE) asm volatile("" : "+l"(ring));
+    uint64_t *fetch = reinterpret_cast<uint64_t *>(ring + Ring<STG>::BYTES) + FETCH_SLOT;
     if (lane_id() == 0) *fetch = 0;
     while (g < nsegs) {  // one call site, so the walker is inlined once
-        speculate_segment<ALGO, TM, STG, FUSE>(G, W, g, nsegs, align_smem(smem) + warp * RS, bounds, cap, d_count,
+        speculate_segment<ALGO, TM, STG, FUSE>(G, W, g, nsegs, ring, bounds, cap, d_count,
                                                FUSE ? fused : 0, pre_n);
         if (spw != 0) break;
         g = next_seg();
