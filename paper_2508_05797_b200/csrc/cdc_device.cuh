@@ -473,16 +473,18 @@ __device__ __forceinline__ int stage_locate(const uint8_t *sp, int Bk, uint32_t 
     return base + __ffs(__ballot_sync(0xFFFFFFFFu, hit)) - 1;
 }
 
-// Saturating-byte masks (transfer tables, cdc_kernels.cu).  Exact per-byte
-// test for the saturating value (255 for MAX, 0 for MIN): a byte of t is zero
-// iff bit 7 of ((t & 0x7F..7F) + 0x7F..7F) | t is clear (no carry crosses a
-// byte).  The four flags of a word gather into 4 bits with one multiply (bits
-// 0, 8, 16, 24 -> 21..24; all partial products are distinct bits).
+// Saturating-byte masks (the sparse walk, the transfer tables).  Exact per-byte
+// test for the saturating value: 0x80 marks each byte of x equal to 255 (MAX:
+// (b & 0x7F) + 1 carries into bit 7 only for 0x7F, and b's own bit 7 must be
+// set) or 0 (MIN: (b & 0x7F) + 0x7F | b has bit 7 clear only for 0); no carry
+// crosses a byte.  One multiply gathers the four flags (bits 7, 15, 23, 31)
+// into bits 28..31: flag k meets constant bit 21 - 7k, and every other partial
+// product lands on a distinct bit below 28 or above 31.
 template <bool MAX>
 __device__ __forceinline__ uint32_t sat_nibble(uint32_t x) {
-    const uint32_t t = MAX ? ~x : x;
-    const uint32_t z = ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t | 0x7F7F7F7Fu);  // 0x80 per zero byte of t
-    return (((z >> 7) * 0x00204081u) >> 21) & 0xFu;
+    const uint32_t f = MAX ? ((x & 0x7F7F7F7Fu) + 0x01010101u) & x & 0x80808080u
+                           : ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+    return (f * 0x00204081u) >> 28;
 }
 // bit i set iff byte i of a lane's 16-byte vector is the saturating value
 template <bool MAX>
