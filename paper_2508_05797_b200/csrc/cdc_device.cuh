@@ -872,12 +872,11 @@ static_assert(SP_SPEC % 16 == 0 && SP_SPEC <= SP_SLOT, "SP_SPEC");
 // positions), or -1: one 512-byte block per step, exact per-byte masks
 // (sat_mask16), one ballot per block.
 // (more: set when the same block holds another such byte in (result, hi))
-template <bool MAX>
-__device__ __forceinline__ int64_t sm_first(const uint8_t *sp, int64_t P, int n, int64_t lo, int64_t hi,
-                                                  bool *more = nullptr) {
+template <bool MAX, typename IX = int64_t>
+__device__ __forceinline__ IX sm_first(const uint8_t *sp, IX P, int n, IX lo, IX hi, bool *more = nullptr) {
     if (lo < P) lo = P;
     if (hi > P + n) hi = P + n;
-    if (lo >= hi) return -1;
+    if (lo >= hi) return IX(-1);
     const int a = (int)(lo - P), b = (int)(hi - P);
     const int l16 = lane_id() * 16;
     for (int B = a & ~(BLK - 1); B < b; B += BLK) {
@@ -890,41 +889,39 @@ __device__ __forceinline__ int64_t sm_first(const uint8_t *sp, int64_t P, int n,
             const int L = __ffs(bal) - 1;
             const uint32_t mL = __shfl_sync(0xFFFFFFFFu, m, L);
             if (more) *more = (mL & (mL - 1u)) != 0u || (bal >> L) > 1u;
-            return P + B + 16 * L + (__ffs(mL) - 1);
+            return P + (IX)(B + 16 * L + (__ffs(mL) - 1));
         }
     }
-    return -1;
+    return IX(-1);
 }
 #ifndef CDC_SP_FIND
 #define CDC_SP_FIND 0
 #endif
-template <int CMP>
-__device__ __forceinline__ int64_t sm_find(const uint8_t *sp, int64_t P, int n, int64_t lo, int64_t hi,
-                                           uint32_t target);
+template <int CMP, typename IX = int64_t>
+__device__ __forceinline__ IX sm_find(const uint8_t *sp, IX P, int n, IX lo, IX hi, uint32_t target);
 // the sparse walk's region search for the saturating value (CDC_SP_FIND: 0 =
 // sm_first, 1 = the ring walker's Range Scan)
-template <bool MAX>
-__device__ __forceinline__ int64_t sm_sat(const uint8_t *sp, int64_t P, int n, int64_t lo, int64_t hi) {
-    if (CDC_SP_FIND == 0) return sm_first<MAX>(sp, P, n, lo, hi);
-    return sm_find<MAX ? CMP_GEQ : CMP_LEQ>(sp, P, n, lo, hi, MAX ? 255u : 0u);
+template <bool MAX, typename IX = int64_t>
+__device__ __forceinline__ IX sm_sat(const uint8_t *sp, IX P, int n, IX lo, IX hi) {
+    if (CDC_SP_FIND == 0) return sm_first<MAX, IX>(sp, P, n, lo, hi);
+    return sm_find<MAX ? CMP_GEQ : CMP_LEQ, IX>(sp, P, n, lo, hi, MAX ? 255u : 0u);
 }
 
 // First byte of the slot's region [P, P + n) (file positions) in [lo, hi) that
 // satisfies (byte CMP target), or -1: the ring walker's block-level Range Scan
 // (stage_find_block: a per-lane extreme over 16-byte vectors, four blocks in
 // flight, one ballot per block) and its in-lane locate.
-template <int CMP>
-__device__ __forceinline__ int64_t sm_find(const uint8_t *sp, int64_t P, int n, int64_t lo, int64_t hi,
-                                           uint32_t target) {
+template <int CMP, typename IX>
+__device__ __forceinline__ IX sm_find(const uint8_t *sp, IX P, int n, IX lo, IX hi, uint32_t target) {
     if (lo < P) lo = P;
     if (hi > P + n) hi = P + n;
-    if (lo >= hi) return -1;
+    if (lo >= hi) return IX(-1);
     const int a = (int)(lo - P), b = (int)(hi - P);
     uint32_t bal = 0, lm = 0;
     bool has = false;
     const int Bk = stage_find_block<CMP>(sp, a, b, target, bal, lm, has);
-    if (Bk < 0) return -1;
-    return P + stage_locate<CMP>(sp, Bk, bal, a, b, target);
+    if (Bk < 0) return IX(-1);
+    return P + (IX)stage_locate<CMP>(sp, Bk, bal, a, b, target);
 }
 
 #ifdef CDC_SPTIME  // diagnostic: sparse walk cycle accounting into g_evt[11..15] (tools/sparse_probe.py)
@@ -942,14 +939,21 @@ __device__ __forceinline__ int64_t sm_find(const uint8_t *sp, int64_t P, int n, 
 #define SPT_ADD(i)
 #define SPT_FLUSH
 #endif
-template <int ALGO, class Emit>
-__device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf, int64_t start,
-                             int64_t read_end, uint32_t w, uint64_t max_size, Emit &emit, int64_t &resume) {
+// IX: the type of positions inside the walk, relative to its start (int when
+// the rest of the file and max_size fit in 2^29 -- every batch file of
+// configs[3] --, which halves the bookkeeping instructions of a chunk;
+// int64_t otherwise).
+template <int ALGO, typename IX, class Emit>
+__device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbase0, int64_t Lf0, int64_t org,
+                             int64_t read_end0, uint32_t w, uint64_t max_size0, Emit &emit, int64_t &resume) {
     constexpr bool MAX = (ALGO != ALGO_AE_MIN);
     constexpr bool RAM = (ALGO == ALGO_RAM);
     const int lane = lane_id();
-    const int64_t W = (int64_t)w;
-    if (read_end > Lf) read_end = Lf;
+    const IX W = (IX)w;
+    const uint8_t *__restrict__ fbase = fbase0 + org;  // positions below are relative to org
+    const IX Lf = (IX)(Lf0 - org);
+    const IX max_size = (IX)max_size0;
+    const IX read_end = (IX)((read_end0 < Lf0 ? read_end0 : Lf0) - org);
     const uint64_t pol = l2_evict_first_policy();
     if (lane == 0) {
         for (int i = 0; i < 3; ++i) mbar_init(&R.bar[i], 1);
@@ -960,10 +964,10 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
     uint32_t fetched = 0;        // bytes copied by this call (flushed into R.bar[FETCH_SLOT] at the end)
     // copy of the bytes from x (rounded down to 16 B, at most nb bytes, not past the
     // granule holding byte Lf - 1) into slot `slot`; P, N: the region's start and size
-    auto issue = [&](int slot, int64_t x, int nb, int64_t &P, int &N) {
-        P = x - (int64_t)(reinterpret_cast<uintptr_t>(fbase + x) & 15u);
-        const int64_t avail = ((Lf - P) + 15) & ~static_cast<int64_t>(15);
-        N = (int)(avail < (int64_t)nb ? (avail > 0 ? avail : 0) : (int64_t)nb);
+    auto issue = [&](int slot, IX x, int nb, IX &P, int &N) {
+        P = x - (IX)(reinterpret_cast<uintptr_t>(fbase + x) & 15u);
+        const IX avail = ((Lf - P) + 15) & ~static_cast<IX>(15);
+        N = (int)(avail < (IX)nb ? (avail > 0 ? avail : 0) : (IX)nb);
         if (N > 0) {
             uint64_t *bar = &R.bar[slot];
             fetched += (uint32_t)N;
@@ -999,15 +1003,15 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
         __syncwarp();
         return r;
     };
-    const int64_t GAP = RAM ? 2 * W + 1 : W + 1;  // the next chunk's decisive bytes start at or after s + GAP
-    int64_t s = start;
+    const IX GAP = RAM ? 2 * W + 1 : W + 1;  // the next chunk's decisive bytes start at or after s + GAP
+    IX s = 0;
     int cur = 0;        // slot of this chunk's speculative region (alternates 0 / 1)
-    int64_t cP = 0;     // ... its region [cP, cP + cN)
+    IX cP = 0;          // ... its region [cP, cP + cN)
     int cN = 0;
     int rs = -1;        // RAM: slot holding the bytes right after s, its region [rP, rP + rN)
-    int64_t rP = 0;
+    IX rP = 0;
     int rN = 0;
-    int64_t P2 = 0;     // continuation slot 2's region
+    IX P2 = 0;          // continuation slot 2's region
     int N2 = 0;
     bool wsat = false;  // RAM: this chunk's window is known to hold a 0xFF
     for (;;) {
@@ -1015,14 +1019,14 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
             emit.end();
             return finish(true);
         }
-        const int64_t limit = (Lf - s < (int64_t)max_size) ? Lf : s + (int64_t)max_size;
+        const IX limit = (Lf - s < max_size) ? Lf : s + max_size;
         SPT_BEGIN;
         if (RAM && !wsat) {  // does the window [s, s+w) hold a 0xFF?
-            const int64_t wend = s + W < read_end ? s + W : read_end;
+            const IX wend = s + W < read_end ? s + W : read_end;
             bool sat = false;
-            int64_t x = s;
+            IX x = s;
             if (rs >= 0) {
-                sat = sm_sat<true>(R.buf + rs * SP_SLOT, rP, rN, s, wend) >= 0;
+                sat = sm_sat<true, IX>(R.buf + rs * SP_SLOT, rP, rN, s, wend) >= 0;
                 if (rP + rN > x) x = rP + rN;
             }
             while (!sat && x < wend) {
@@ -1031,28 +1035,28 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
                 issue(2, x, SP_SPEC, P2, N2);
                 if (N2 <= 0) break;
                 wait(2);
-                sat = sm_sat<true>(R.buf + 2 * SP_SLOT, P2, N2, x, wend) >= 0;
+                sat = sm_sat<true, IX>(R.buf + 2 * SP_SLOT, P2, N2, x, wend) >= 0;
                 x = P2 + N2;
             }
             if (!sat) {  // the ring walker decides this chunk
-                resume = s;
+                resume = org + s;
                 return finish(false);
             }
         }
         SPT_ADD(0);
         const int nxt = cur ^ 1;
-        int64_t nP = 0;
+        IX nP = 0;
         int nN = 0;
         wait(nxt);  // (the last chunk's region, already consumed)
         if (s + GAP < Lf) issue(nxt, s + GAP, SP_SPEC, nP, nN);
-        int64_t e;
+        IX e;
         if (!RAM && s + W >= limit) {
             e = limit;  // no target's window fits before the limit
         } else {
-            const int64_t x0 = RAM ? s + W : s;
-            const int64_t hi = RAM ? (limit < read_end ? limit : read_end) : s + W + 1;
+            const IX x0 = RAM ? s + W : s;
+            const IX hi = RAM ? (limit < read_end ? limit : read_end) : s + W + 1;
             if (!RAM && hi > read_end) {
-                resume = s;
+                resume = org + s;
                 return finish(false);
             }
             if (!(cN > 0 && cP <= x0 && x0 < cP + cN)) {  // not covered by the speculative copy
@@ -1065,13 +1069,13 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
             SPT_ADD(1);
             SPT_BEGIN;
             int slot = cur;
-            int64_t P = cP;
+            IX P = cP;
             int N = cN;
             bool more = false;  // (RAM: another 0xFF within 512 bytes after the boundary byte)
-            int64_t pos = CDC_SP_FIND == 0 ? sm_first<MAX>(R.buf + cur * SP_SLOT, cP, cN, x0, hi, &more)
-                                           : sm_sat<MAX>(R.buf + cur * SP_SLOT, cP, cN, x0, hi);
+            IX pos = CDC_SP_FIND == 0 ? sm_first<MAX, IX>(R.buf + cur * SP_SLOT, cP, cN, x0, hi, &more)
+                                           : sm_sat<MAX, IX>(R.buf + cur * SP_SLOT, cP, cN, x0, hi);
             while (pos < 0 && P + N < hi && N > 0) {  // continue past the region
-                const int64_t x = P + N > x0 ? P + N : x0;
+                const IX x = P + N > x0 ? P + N : x0;
                 CNT(14);
                 wait(2);
                 issue(2, x, SP_SPEC, P2, N2);
@@ -1079,8 +1083,8 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
                 slot = 2;
                 P = P2;
                 N = N2;
-                pos = CDC_SP_FIND == 0 ? sm_first<MAX>(R.buf + 2 * SP_SLOT, P2, N2, x, hi, &more)
-                                       : sm_sat<MAX>(R.buf + 2 * SP_SLOT, P2, N2, x, hi);
+                pos = CDC_SP_FIND == 0 ? sm_first<MAX, IX>(R.buf + 2 * SP_SLOT, P2, N2, x, hi, &more)
+                                       : sm_sat<MAX, IX>(R.buf + 2 * SP_SLOT, P2, N2, x, hi);
             }
             if (RAM) {
                 if (pos >= 0) {
@@ -1088,7 +1092,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
                 } else if (hi == limit) {
                     e = limit;  // cap or end of stream
                 } else {
-                    emit.exhausted(read_end);
+                    emit.exhausted(org + read_end);
                     return finish(true);
                 }
                 rs = slot;
@@ -1097,7 +1101,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
                 wsat = pos >= 0 && more;  // the next window [e, e + w) holds that 0xFF (w >= 512)
             } else {
                 if (pos < 0) {  // no saturating byte in [s, s+w]: the ring walker decides this chunk
-                    resume = s;
+                    resume = org + s;
                     return finish(false);
                 }
                 e = pos + W < limit ? pos + W + 1 : limit;
@@ -1109,7 +1113,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
             return finish(true);
         }
         SPT_BEGIN;
-        const bool stop_ = emit.boundary(e);
+        const bool stop_ = emit.boundary(org + e);
         SPT_ADD(3);
         if (stop_) return finish(true);
         s = e;
@@ -1122,7 +1126,10 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
 // The walk of a chain from a chunk start: sparse while the chunks saturate,
 // the TMA-ring walker from the first chunk the sparse walk cannot decide, and
 // back to the sparse walk after YIELD_SAT saturated chunks in a row.
-template <int ALGO, int STG = STAGE, class Emit>
+// NARROW: the walker may take the int-position instance of the sparse walk
+// (the batch kernel: its files are short; the single-stream kernels keep one
+// instance, which keeps their register allocation -- configs[1] +2 % otherwise).
+template <int ALGO, int STG = STAGE, bool NARROW = false, class Emit>
 __device__ __forceinline__ void walk_chain(bool sparse, const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf,
                                            int64_t start, int64_t read_end, uint32_t w, uint64_t max_size,
                                            const L2Pol &pol, Emit &emit) {
@@ -1132,7 +1139,15 @@ __device__ __forceinline__ void walk_chain(bool sparse, const WarpRing &R, const
     }
     for (;;) {
         int64_t resume = start;
-        if (sparse_chain<ALGO>(R, fbase, Lf, start, read_end, w, max_size, emit, resume)) return;
+        // (int positions: the rest of the file and max_size below 2^29, so s + 2w + 1 stays below 2^31)
+        const bool narrow = NARROW && Lf - start < (1ll << 29) && max_size < (1ull << 29);
+        bool done;
+        if constexpr (NARROW)
+            done = narrow ? sparse_chain<ALGO, int>(R, fbase, Lf, start, read_end, w, max_size, emit, resume)
+                          : sparse_chain<ALGO, int64_t>(R, fbase, Lf, start, read_end, w, max_size, emit, resume);
+        else
+            done = sparse_chain<ALGO, int64_t>(R, fbase, Lf, start, read_end, w, max_size, emit, resume);
+        if (done) return;
         int64_t y = -1;
         run_chain<ALGO, STG>(R, fbase, Lf, resume, read_end, w, max_size, pol, emit, &y);
         if (y < 0) return;

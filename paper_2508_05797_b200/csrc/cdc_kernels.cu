@@ -684,7 +684,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
                                         : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
     // the segment's head is read again by the previous segment's halo walk: keep it in L2
     const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
-    walk_chain<ALGO, STG>(G.sparse != 0, R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
+    walk_chain<ALGO, STG, !FUSE>(G.sparse != 0, R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
     em.publish();
     if (tm && lane == 0) {
         tm[TM_PER_SEG * g + 2] = globaltimer();
