@@ -104,6 +104,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         if (clock64() - t0 > 20000000000ll) __trap();
     }
 }
+// the same on a 32-bit shared-window address (the sparse walk keeps its ring's)
+__device__ __forceinline__ bool mbar_try_wait_s(uint32_t a, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t a, uint32_t parity) {
+    if (mbar_try_wait_s(a, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait_s(a, parity)) {
+        if (clock64() - t0 > 20000000000ll) __trap();
+    }
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -894,6 +918,29 @@ __device__ __forceinline__ IX sm_first(const uint8_t *sp, IX P, int n, IX lo, IX
     }
     return IX(-1);
 }
+// sm_first on a 32-bit shared-window address sp, the lane's byte offset l16 =
+// 16 * lane passed in (the sparse walk keeps both in registers)
+template <bool MAX, typename IX>
+__device__ __forceinline__ IX sm_first_s(uint32_t sp, int l16, IX P, int n, IX lo, IX hi, bool *more = nullptr) {
+    if (lo < P) lo = P;
+    if (hi > P + n) hi = P + n;
+    if (lo >= hi) return IX(-1);
+    const int a = (int)(lo - P), b = (int)(hi - P);
+    for (int B = a & ~(BLK - 1); B < b; B += BLK) {
+        const uint4 v = lds128(sp + (uint32_t)(B + l16));
+        const int q = B + l16;
+        const int ka = min(max(a - q, 0), 16), kb = min(max(b - q, 0), 16);
+        const uint32_t m = sat_mask16<MAX>(v) & ((1u << kb) - 1u) & ~((1u << ka) - 1u);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m != 0u);
+        if (bal) {
+            const int L = __ffs(bal) - 1;
+            const uint32_t mL = __shfl_sync(0xFFFFFFFFu, m, L);
+            if (more) *more = (mL & (mL - 1u)) != 0u || (bal >> L) > 1u;
+            return P + (IX)(B + 16 * L + (__ffs(mL) - 1));
+        }
+    }
+    return IX(-1);
+}
 #ifndef CDC_SP_FIND
 #define CDC_SP_FIND 0
 #endif
@@ -960,6 +1007,19 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
         fence_barrier_init();
     }
     __syncwarp();
+    // shared-window addresses of the slots and their mbarriers, and the lane's byte
+    // offset, kept in registers (opaque: not rebuilt from the thread index per use)
+    uint32_t sbuf = smem_addr(R.buf), sbar = smem_addr(R.bar);
+    int l16 = lane * 16;
+    asm volatile("" : "+r"(sbuf), "+r"(sbar), "+r"(l16));
+    auto find = [&](int slot, IX P, int n, IX lo, IX hi, bool *more) -> IX {
+        if (CDC_SP_FIND == 0) return sm_first_s<MAX, IX>(sbuf + slot * SP_SLOT, l16, P, n, lo, hi, more);
+        return sm_sat<MAX, IX>(R.buf + slot * SP_SLOT, P, n, lo, hi);
+    };
+    auto find_ff = [&](int slot, IX P, int n, IX lo, IX hi) -> IX {  // RAM's window test: a 0xFF
+        if (CDC_SP_FIND == 0) return sm_first_s<true, IX>(sbuf + slot * SP_SLOT, l16, P, n, lo, hi);
+        return sm_sat<true, IX>(R.buf + slot * SP_SLOT, P, n, lo, hi);
+    };
     uint32_t pend = 0, par = 0;  // per slot: copy in flight; parity of its next completion
     uint32_t fetched = 0;        // bytes copied by this call (flushed into R.bar[FETCH_SLOT] at the end)
     // copy of the bytes from x (rounded down to 16 B, at most nb bytes, not past the
@@ -969,14 +1029,13 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
         const IX avail = ((Lf - P) + 15) & ~static_cast<IX>(15);
         N = (int)(avail < (IX)nb ? (avail > 0 ? avail : 0) : (IX)nb);
         if (N > 0) {
-            uint64_t *bar = &R.bar[slot];
             fetched += (uint32_t)N;
             asm volatile(
                 "{\n\t.reg .pred p;\n\t"
                 "elect.sync _|p, 0xffffffff;\n\t"
                 "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
                 "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%2], [%3], %1, [%0], %4;\n\t"
-                "}" ::"r"(smem_addr(bar)), "r"((uint32_t)N), "r"(smem_addr(R.buf + slot * SP_SLOT)), "l"(fbase + P),
+                "}" ::"r"(sbar + 8 * slot), "r"((uint32_t)N), "r"(sbuf + slot * SP_SLOT), "l"(fbase + P),
                 "l"(pol)
                 : "memory");
             pend |= 1u << slot;
@@ -984,7 +1043,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
     };
     auto wait = [&](int slot) {
         if ((pend >> slot) & 1u) {
-            mbar_wait(&R.bar[slot], (par >> slot) & 1u);
+            mbar_wait_s(sbar + 8 * slot, (par >> slot) & 1u);
             par ^= 1u << slot;
             pend &= ~(1u << slot);
         }
@@ -1026,7 +1085,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
             bool sat = false;
             IX x = s;
             if (rs >= 0) {
-                sat = sm_sat<true, IX>(R.buf + rs * SP_SLOT, rP, rN, s, wend) >= 0;
+                sat = find_ff(rs, rP, rN, s, wend) >= 0;
                 if (rP + rN > x) x = rP + rN;
             }
             while (!sat && x < wend) {
@@ -1035,7 +1094,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
                 issue(2, x, SP_SPEC, P2, N2);
                 if (N2 <= 0) break;
                 wait(2);
-                sat = sm_sat<true, IX>(R.buf + 2 * SP_SLOT, P2, N2, x, wend) >= 0;
+                sat = find_ff(2, P2, N2, x, wend) >= 0;
                 x = P2 + N2;
             }
             if (!sat) {  // the ring walker decides this chunk
@@ -1072,8 +1131,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
             IX P = cP;
             int N = cN;
             bool more = false;  // (RAM: another 0xFF within 512 bytes after the boundary byte)
-            IX pos = CDC_SP_FIND == 0 ? sm_first<MAX, IX>(R.buf + cur * SP_SLOT, cP, cN, x0, hi, &more)
-                                           : sm_sat<MAX, IX>(R.buf + cur * SP_SLOT, cP, cN, x0, hi);
+            IX pos = find(cur, cP, cN, x0, hi, &more);
             while (pos < 0 && P + N < hi && N > 0) {  // continue past the region
                 const IX x = P + N > x0 ? P + N : x0;
                 CNT(14);
@@ -1083,8 +1141,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
                 slot = 2;
                 P = P2;
                 N = N2;
-                pos = CDC_SP_FIND == 0 ? sm_first<MAX, IX>(R.buf + 2 * SP_SLOT, P2, N2, x, hi, &more)
-                                       : sm_sat<MAX, IX>(R.buf + 2 * SP_SLOT, P2, N2, x, hi);
+                pos = find(2, P2, N2, x, hi, &more);
             }
             if (RAM) {
                 if (pos >= 0) {
