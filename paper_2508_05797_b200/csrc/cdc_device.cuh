@@ -998,7 +998,9 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
     const int lane = lane_id();
     const IX W = (IX)w;
     const uint8_t *__restrict__ fbase = fbase0 + org;  // positions below are relative to org
-    const IX Lf = (IX)(Lf0 - org);
+    // (the int instance clamps a distant file end to 2^30: every position it forms stays
+    // below that, so every comparison with the file end comes out as with the real one)
+    const IX Lf = (IX)(sizeof(IX) == 4 && Lf0 - org > (1ll << 30) ? (1ll << 30) : Lf0 - org);
     const IX max_size = (IX)max_size0;
     const IX read_end = (IX)((read_end0 < Lf0 ? read_end0 : Lf0) - org);
     const uint64_t pol = l2_evict_first_policy();
@@ -1183,23 +1185,31 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
 // The walk of a chain from a chunk start: sparse while the chunks saturate,
 // the TMA-ring walker from the first chunk the sparse walk cannot decide, and
 // back to the sparse walk after YIELD_SAT saturated chunks in a row.
-// NARROW: the walker may take the int-position instance of the sparse walk
-// (the batch kernel: its files are short; the single-stream kernels keep one
-// instance, which keeps their register allocation -- configs[1] +2 % otherwise).
-template <int ALGO, int STG = STAGE, bool NARROW = false, class Emit>
+// SPM: which sparse walks the kernel carries -- 0 none (its launches never set
+// `sparse`; configs[1]'s window is below the sparse walk's minimum, and without
+// that code its walker keeps fewer registers), 1 the int64-position instance,
+// 2 also the int-position instance, taken when the walk's byte range and
+// max_size are below 2^28 (every walk of a batch, of K-phase and of a
+// single-stream segment of a few hundred MB).
+template <int ALGO, int STG = STAGE, int SPM = 1, class Emit>
 __device__ __forceinline__ void walk_chain(bool sparse, const WarpRing &R, const uint8_t *__restrict__ fbase, int64_t Lf,
                                            int64_t start, int64_t read_end, uint32_t w, uint64_t max_size,
                                            const L2Pol &pol, Emit &emit) {
+    if constexpr (SPM == 0) {
+        run_chain<ALGO, STG>(R, fbase, Lf, start, read_end, w, max_size, pol, emit);
+        return;
+    }
     if (!sparse) {
         run_chain<ALGO, STG>(R, fbase, Lf, start, read_end, w, max_size, pol, emit);
         return;
     }
-    for (;;) {
+    if constexpr (SPM != 0) for (;;) {
         int64_t resume = start;
-        // (int positions: the rest of the file and max_size below 2^29, so s + 2w + 1 stays below 2^31)
-        const bool narrow = NARROW && Lf - start < (1ll << 29) && max_size < (1ull << 29);
+        // (int positions: read_end - start and max_size below 2^28 keep every position the
+        // walk forms below 2^30; the file end is clamped to 2^30 beyond that)
+        const bool narrow = SPM == 2 && read_end - start < (1ll << 28) && max_size < (1ull << 28);
         bool done;
-        if constexpr (NARROW)
+        if constexpr (SPM == 2)
             done = narrow ? sparse_chain<ALGO, int>(R, fbase, Lf, start, read_end, w, max_size, emit, resume)
                           : sparse_chain<ALGO, int64_t>(R, fbase, Lf, start, read_end, w, max_size, emit, resume);
         else

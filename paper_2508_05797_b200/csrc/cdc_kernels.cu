@@ -559,7 +559,7 @@ template <int ALGO>
 __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_count, uint64_t *file_out,
                                                 uint64_t *bounds, uint64_t cap);
 
-template <int ALGO, bool TM, int STG, bool FUSE>
+template <int ALGO, bool TM, int STG, bool FUSE, int SPM>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
                                   uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused,
                                   int64_t pre_n = -1);
@@ -574,7 +574,7 @@ __device__ int64_t t_coop_index(const Geometry &G, Work &W, uint64_t g, uint8_t 
 // other one carries none of their code, so the common path keeps its registers.
 // NW warps per CTA with rings of 2 x STG bytes; FUSE: carries the fused
 // look-back and write (the batch instance: BATCH_WARPS, BATCH_STAGE, no fused write).
-template <int ALGO, bool TM, int NW = SPEC_WARPS, int STG = STAGE, bool FUSE = true>
+template <int ALGO, bool TM, int NW = SPEC_WARPS, int STG = STAGE, bool FUSE = true, int SPM = 2>
 __global__ void __launch_bounds__(NW * 32, SPEC_CTAS_PER_SM) k_speculate(Geometry G, Work W, uint64_t *bounds,
                                                                   uint64_t cap, uint64_t *d_count, int fused,
                                                                   int spw) {
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(NW * 32, SPEC_CTAS_PER_SM) k_speculate(Geometr
     uint64_t *fetch = reinterpret_cast<uint64_t *>(ring + Ring<STG>::BYTES) + FETCH_SLOT;
     if (lane_id() == 0) *fetch = 0;
     while (g < nsegs) {  // one call site, so the walker is inlined once
-        speculate_segment<ALGO, TM, STG, FUSE>(G, W, g, nsegs, ring, bounds, cap, d_count,
+        speculate_segment<ALGO, TM, STG, FUSE, SPM>(G, W, g, nsegs, ring, bounds, cap, d_count,
                                                FUSE ? fused : 0, pre_n);
         if (spw != 0) break;
         g = next_seg();
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(NW * 32, SPEC_CTAS_PER_SM) k_speculate(Geometr
 
 #include "cdc_tables.cuh"  // T-mode: transfer tables for saturated streams
 
-template <int ALGO, bool TM, int STG, bool FUSE>
+template <int ALGO, bool TM, int STG, bool FUSE, int SPM>
 __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, uint64_t g, uint64_t nsegs, uint8_t *wbase,
                                   uint64_t *bounds, uint64_t cap, uint64_t *d_count, int fused,
                                   int64_t pre_n) {
@@ -684,7 +684,7 @@ __device__ __forceinline__ void speculate_segment(const Geometry &G, Work &W, ui
                                         : em.I.seg_end + (int64_t)G.Hmax + (int64_t)G.max_size;
     // the segment's head is read again by the previous segment's halo walk: keep it in L2
     const L2Pol pol{l2_evict_first_policy(), l2_evict_last_policy(), em.I.p + (int64_t)HEAD_KEEP};
-    walk_chain<ALGO, STG, !FUSE>(G.sparse != 0, R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
+    walk_chain<ALGO, STG, SPM>(G.sparse != 0, R, fbase, (int64_t)em.I.Lf, em.I.p, read_end, G.w, G.max_size, pol, em);
     em.publish();
     if (tm && lane == 0) {
         tm[TM_PER_SEG * g + 2] = globaltimer();
@@ -2119,6 +2119,8 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, batch_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       spec_smem));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO, false, cdc::SPEC_WARPS, cdc::STAGE, true, 0>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_speculate<ALGO, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_fixup<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2214,7 +2216,8 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         const void *kspec =
             batch ? reinterpret_cast<const void *>(cdc::k_speculate<ALGO, false, cdc::BATCH_WARPS, cdc::BATCH_STAGE, false>)
             : G.tmode ? reinterpret_cast<const void *>(cdc::k_speculate<ALGO, true>)
-                      : reinterpret_cast<const void *>(cdc::k_speculate<ALGO, false>);
+            : G.sparse ? reinterpret_cast<const void *>(cdc::k_speculate<ALGO, false>)
+                       : reinterpret_cast<const void *>(cdc::k_speculate<ALGO, false, cdc::SPEC_WARPS, cdc::STAGE, true, 0>);
         CDC_CUDA(launch_pdl(kspec, dim3((unsigned)blocks), dim3((batch ? cdc::BATCH_WARPS : cdc::SPEC_WARPS) * 32),
                             (size_t)(batch ? batch_smem : spec_smem), st, G, W, d_bounds, cap, d_count, fused, spw));
         CDC_KCHECK("k_speculate", st);

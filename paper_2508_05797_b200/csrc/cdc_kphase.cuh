@@ -307,7 +307,7 @@ __device__ void knode_walk(const KGeo &Q, const KWork &KW, const WarpRing &R, ui
     if (walk) {
         int64_t read_end = pe + (int64_t)Q.Hk + (int64_t)Q.max_size;
         if (g + 1 == Q.G || read_end > (int64_t)Q.L) read_end = (int64_t)Q.L;
-        walk_chain<ALGO>(Q.sparse != 0, R, Q.data, (int64_t)Q.L, s, read_end, Q.w, Q.max_size, stream_policy(), em);
+        walk_chain<ALGO, STAGE, 2>(Q.sparse != 0, R, Q.data, (int64_t)Q.L, s, read_end, Q.w, Q.max_size, stream_policy(), em);
     }
     __syncwarp();
     if (lane == 0) {
