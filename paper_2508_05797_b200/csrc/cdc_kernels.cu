@@ -177,6 +177,7 @@ __host__ __device__ __forceinline__ uint64_t nseg_of(uint64_t len, uint64_t S) {
     return len == 0 ? 0 : (len < S ? 1 : len / S);
 }
 __host__ __device__ __forceinline__ int64_t seg_start(uint64_t k, uint64_t n, uint64_t len) {
+    if (n == 1) return k >= 1 ? (int64_t)len : 0;  // (most batch files: no 64-bit division)
     const uint64_t q = len / n;
     const uint64_t align = q >= (64u << 10) ? 4095u : 15u;
     return k >= n ? (int64_t)len : (int64_t)((k * q) & ~align);
@@ -1312,25 +1313,43 @@ __device__ void batch_resolve(const Geometry &G, Work &W, uint64_t nsegs, uint64
         while (ld_acquire_u32(W.ctrl + CT_BR_DONE) + 1u != (uint32_t)ntiles) __nanosleep(256);
     }
     __syncthreads();
-    // boundaries, one warp per segment
-    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t g = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < nsegs; g += nw) {
-        if (W.skipped[g]) continue;  // (never a file's first segment)
-        const SegInfo I = seg_info(G, W, g);
-        const uint64_t fo = W.seg_out[I.first];
-        if (g == I.first && lane == 0 && I.Lf > 0) {
-            const uint64_t q = W.seg_out[I.last + 1] - 1;  // a file's last boundary is its length
-            if (q < cap) bounds[q] = I.Lf;
+    // boundaries: each warp takes 32 consecutive segments; lane k loads segment
+    // g0+k's record (32 records' dependent loads in flight together), then the
+    // warp writes the 32 segments' boundaries one after another with all lanes
+    const uint64_t nwg = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t g0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32; g0 < nsegs; g0 += nwg * 32) {
+        const uint64_t g = g0 + lane;
+        uint32_t n = 0, A = 0;
+        uint64_t base = 0, fo = 0, p = 0, se = 0, lp = 0;
+        if (g < nsegs && !W.skipped[g]) {  // (a skipped segment is never a file's first)
+            const SegInfo I = seg_info(G, W, g);
+            fo = W.seg_out[I.first];
+            if (g == I.first && I.Lf > 0) {
+                const uint64_t q = W.seg_out[I.last + 1] - 1;  // a file's last boundary is its length
+                if (q < cap) bounds[q] = I.Lf;
+            }
+            const uint32_t e = W.entry[g];
+            A = W.cnt[g] - e;
+            n = A + W.tail[g];
+            base = W.seg_out[g];
+            p = (uint64_t)I.p;
+            se = (uint64_t)I.seg_end;
+            lp = list_off(W, g) + e;
         }
-        const uint32_t e = W.entry[g], A = W.cnt[g] - e, n = A + W.tail[g];
-        const uint64_t base = W.seg_out[g];
-        const uint32_t *lst = W.list + list_off(W, g);
-        const uint32_t *hl = W.halo + g * W.cap_halo;
-        for (uint32_t i = lane; i < n; i += 32) {
-            const uint64_t v = i < A ? (uint64_t)I.p + lst[e + i] : (uint64_t)I.seg_end + hl[i - A];
-            const uint64_t q = base + i;
-            if (q == fo) continue;  // the file's first start (0) is not a boundary
-            if (q - 1 < cap) bounds[q - 1] = v;
+        for (int r = 0; r < 32; ++r) {
+            const uint32_t rn = __shfl_sync(0xFFFFFFFFu, n, r);
+            if (rn == 0) continue;
+            const uint32_t rA = __shfl_sync(0xFFFFFFFFu, A, r);
+            const uint64_t rb = __shfl_sync(0xFFFFFFFFu, base, r), rfo = __shfl_sync(0xFFFFFFFFu, fo, r);
+            const uint64_t rp = __shfl_sync(0xFFFFFFFFu, p, r), rse = __shfl_sync(0xFFFFFFFFu, se, r);
+            const uint64_t rlp = __shfl_sync(0xFFFFFFFFu, lp, r);
+            const uint32_t *hl = W.halo + (g0 + r) * W.cap_halo;
+            for (uint32_t i = lane; i < rn; i += 32) {
+                const uint64_t v = i < rA ? rp + W.list[rlp + i] : rse + hl[i - rA];
+                const uint64_t q = rb + i;
+                if (q == rfo) continue;  // the file's first start (0) is not a boundary
+                if (q - 1 < cap) bounds[q - 1] = v;
+            }
         }
     }
     // per-file output offsets
