@@ -889,7 +889,9 @@ constexpr int SP_SPEC = CDC_SP_SPEC;  // bytes per speculative or continuation c
 #define CDC_SP_SLOT 2048
 #endif
 constexpr int SP_SLOT = CDC_SP_SLOT;  // slot stride in the ring: slots 0/1 alternate per chunk, slot 2 continues
-static_assert(Ring<3072>::BYTES >= 3 * SP_SLOT, "sparse walk needs three slots in every ring (stages of >= 3 KiB)");
+constexpr int SP_NSLOT = 4;           // slots 0/1: speculative regions; 2/3: continuation regions (ping-pong)
+static_assert(SP_NSLOT <= FETCH_SLOT, "one mbarrier per sparse-walk slot before the fetch counter");
+static_assert(Ring<4096>::BYTES >= SP_NSLOT * SP_SLOT, "sparse walk needs four slots in every ring (stages of >= 4 KiB)");
 static_assert(SP_SPEC % 16 == 0 && SP_SPEC <= SP_SLOT, "SP_SPEC");
 
 // First saturating byte in [lo, hi) among the slot's bytes [P, P + n) (file
@@ -1005,7 +1007,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
     const IX read_end = (IX)((read_end0 < Lf0 ? read_end0 : Lf0) - org);
     const uint64_t pol = l2_evict_first_policy();
     if (lane == 0) {
-        for (int i = 0; i < 3; ++i) mbar_init(&R.bar[i], 1);
+        for (int i = 0; i < SP_NSLOT; ++i) mbar_init(&R.bar[i], 1);
         fence_barrier_init();
     }
     __syncwarp();
@@ -1050,15 +1052,47 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
             pend &= ~(1u << slot);
         }
     };
+    // Continuation regions (a stretch without a saturating byte: the rest of a
+    // chunk past its speculative copy, or RAM's window probes) alternate between
+    // slots 2 and 3.  From the second region of a run on, the region after the
+    // one to be scanned is copied into the other slot first, so two copies are
+    // in flight and a long stretch (a zero-filled region) costs half a round
+    // trip per region instead of one.  cont() returns the slot holding the
+    // region that starts at x (its [Pc, Pc + Nc)); cs, pf, pfP, pfN, run: the
+    // run's state (the next slot, the slot and region of a copy issued ahead).
+    auto cont = [&](IX x, IX hi, int &cs, int &pf, IX &pfP, int &pfN, bool &run, IX &Pc, int &Nc) -> int {
+        int s_;
+        if (pf >= 0 && pfP == x) {
+            s_ = pf;
+            Pc = pfP;
+            Nc = pfN;
+        } else {
+            s_ = cs;
+            wait(s_);
+            issue(s_, x, SP_SPEC, Pc, Nc);
+        }
+        pf = -1;
+        if (run && Nc > 0 && Pc + Nc < hi) {
+            const int o = s_ ^ 1;
+            wait(o);
+            issue(o, Pc + Nc, SP_SPEC, pfP, pfN);
+            pf = o;
+        }
+        run = true;
+        cs = s_ ^ 1;
+        wait(s_);
+        return s_;
+    };
     SPT_DECL
     auto finish = [&](bool r) -> bool {
         SPT_FLUSH
         wait(0);
         wait(1);
         wait(2);
+        wait(3);
         __syncwarp();
         if (lane == 0) {
-            for (int i = 0; i < 3; ++i) mbar_inval(&R.bar[i]);
+            for (int i = 0; i < SP_NSLOT; ++i) mbar_inval(&R.bar[i]);
             R.bar[FETCH_SLOT] += fetched;
         }
         __syncwarp();
@@ -1090,13 +1124,14 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
                 sat = find_ff(rs, rP, rN, s, wend) >= 0;
                 if (rP + rN > x) x = rP + rN;
             }
+            int cs = 2, pf = -1, pfN = 0;
+            IX pfP = 0;
+            bool run = false;
             while (!sat && x < wend) {
                 CNT(15);
-                wait(2);
-                issue(2, x, SP_SPEC, P2, N2);
+                const int s2 = cont(x, wend, cs, pf, pfP, pfN, run, P2, N2);
                 if (N2 <= 0) break;
-                wait(2);
-                sat = find_ff(2, P2, N2, x, wend) >= 0;
+                sat = find_ff(s2, P2, N2, x, wend) >= 0;
                 x = P2 + N2;
             }
             if (!sat) {  // the ring walker decides this chunk
@@ -1134,16 +1169,16 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
             int N = cN;
             bool more = false;  // (RAM: another 0xFF within 512 bytes after the boundary byte)
             IX pos = find(cur, cP, cN, x0, hi, &more);
+            int cs = 2, pf = -1, pfN = 0;
+            IX pfP = 0;
+            bool run = false;
             while (pos < 0 && P + N < hi && N > 0) {  // continue past the region
                 const IX x = P + N > x0 ? P + N : x0;
                 CNT(14);
-                wait(2);
-                issue(2, x, SP_SPEC, P2, N2);
-                wait(2);
-                slot = 2;
+                slot = cont(x, hi, cs, pf, pfP, pfN, run, P2, N2);
                 P = P2;
                 N = N2;
-                pos = find(2, P2, N2, x, hi, &more);
+                pos = find(slot, P2, N2, x, hi, &more);
             }
             if (RAM) {
                 if (pos >= 0) {

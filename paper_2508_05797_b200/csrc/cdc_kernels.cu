@@ -55,6 +55,7 @@ constexpr int SPEC_CTAS_PER_SM = CDC_SPEC_CTAS_PER_SM;  // resident k_speculate 
 constexpr int BATCH_WARPS = CDC_BATCH_WARPS;
 constexpr int BATCH_STAGE = CDC_BATCH_STAGE;
 static_assert(BATCH_WARPS * Ring<BATCH_STAGE>::SMEM + 128 <= 227 * 1024, "batch rings exceed shared memory");
+static_assert(Ring<BATCH_STAGE>::BYTES >= SP_NSLOT * SP_SLOT && Ring<STAGE>::BYTES >= SP_NSLOT * SP_SLOT, "sparse-walk slots exceed a ring");
 #ifndef CDC_HEAD_KEEP
 #define CDC_HEAD_KEEP 12288
 #endif
@@ -2275,7 +2276,8 @@ struct MaxpPlan {
 uint32_t maxp_smem(uint64_t h, uint32_t &buf, uint32_t &ccap) {
     buf = (uint32_t)round_up(cdc::MX_TILE + 2 * h + 32, 128);
     ccap = (uint32_t)(cdc::MX_TILE / (h + 1) + 2);
-    return buf + 3 * (buf / 16) + 16 + 2 * ccap + 128;
+    const uint32_t ng = buf / 16, nb = ng / cdc::MX_BG + 1;  // granule maxima, block maxima, survivors, candidates
+    return buf + ng + ((nb + 1) & ~1u) + 2 * (ng / 2 + 1) + 2 * ccap + 128;
 }
 // nfiles streams totalling total bytes (a single stream: nfiles = 1)
 void maxp_plan(const cdc_params *p, uint64_t nfiles, uint64_t total, MaxpPlan &P) {

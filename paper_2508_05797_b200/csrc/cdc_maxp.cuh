@@ -10,9 +10,11 @@
 //     candidate positions is copied with its two h-byte margins into shared
 //     memory by one TMA bulk copy; the local maxima of the tile are found with
 //     Extreme Byte Searches over 16-byte granules (§4.1: one max per granule,
-//     then the van Herk / Gil-Werman window maximum over K0 granules on each
-//     side), and only the rare granules whose maximum beats both neighbouring
-//     windows are checked byte by byte.  Each tile writes its maxima to its
+//     then one per block of MX_BG granules by shuffles).  A local maximum is
+//     its block's maximum and beats the NBK blocks on each side that lie
+//     wholly inside its windows, so only blocks that pass this filter (a few
+//     percent on uniform bytes) get the exact test: one warp checks the
+//     K0 whole granules on each side and the window bytes beyond them.  Each tile writes its maxima to its
 //     own slot (no tile waits for another); k_maxp_gather then concatenates
 //     the slots in stream order (a scan of the tile counts) into one
 //     ascending list of elements: per file, a virtual "file start" element
@@ -34,11 +36,15 @@
 // Nothing here is shared with oracle/ (tests compare the two element by element).
 // (Included by cdc_kernels.cu inside namespace cdc.)
 
-constexpr int MX_TILE = 32768;         // candidate positions per scan tile
+#ifndef CDC_MX_TILE
+#define CDC_MX_TILE 32768
+#endif
+constexpr int MX_TILE = CDC_MX_TILE;   // candidate positions per scan tile
 constexpr int MX_THREADS = 256;        // k_maxp_scan
 constexpr uint32_t MX_HMAX = 65536;    // largest window per side a tile's shared memory holds
 constexpr int MX_ETILE = 256;          // elements per link / write tile (one thread each)
 constexpr int MX_GTILES = 1024;        // scan tiles per k_maxp_gather CTA (one thread each)
+constexpr int MX_BG = 8;               // granules per block of k_maxp_scan's block filter (lanes per shuffle group)
 
 struct MaxpGeo {
     const uint8_t *data;
@@ -172,16 +178,18 @@ __global__ void __launch_bounds__(MX_FTHREADS) k_maxp_files(MaxpGeo Q, MaxpWork 
     if ((g + 1) * MX_FTHREADS >= Q.nfiles && threadIdx.x == 0) X.tfirst[Q.nfiles] = excl + tot;
 }
 
-// K1: local maxima, tile by tile in ticket order.
+// K1: local maxima, tile by tile (static schedule, the next tile prefetched into L2).
 __global__ void __launch_bounds__(MX_THREADS) k_maxp_scan(MaxpGeo Q, MaxpWork X) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t bar;
-    __shared__ uint32_t s_tile, s_scr[64], s_cnt;
+    __shared__ uint32_t s_scr[64], s_cnt, s_ns;
     uint8_t *buf = align_smem(smem);                       // tile bytes (Q.buf)
     uint8_t *gm = buf + Q.buf;                             // granule maxima
     const uint32_t NGmax = Q.buf / 16;
-    uint8_t *pf = gm + NGmax, *sf = pf + NGmax;            // van Herk prefix / suffix maxima
-    uint16_t *cand = reinterpret_cast<uint16_t *>(sf + NGmax + (16 - (3 * NGmax) % 16) % 16);
+    const uint32_t NBmax = NGmax / MX_BG + 1;
+    uint8_t *bm = gm + NGmax;                              // block maxima (MX_BG granules)
+    uint16_t *surv = reinterpret_cast<uint16_t *>(bm + ((NBmax + 1) & ~1u));  // blocks (granules) that pass the filter
+    uint16_t *cand = surv + NGmax / 2 + 1;
     const int tid = threadIdx.x;
     const uint64_t h = Q.h;
     const uint64_t ntot = X.tfirst[Q.nfiles];
@@ -191,26 +199,52 @@ __global__ void __launch_bounds__(MX_THREADS) k_maxp_scan(MaxpGeo Q, MaxpWork X)
     }
     __syncthreads();
     uint32_t phase = 0;
-    for (;;) {
-        if (tid == 0) s_tile = atomicAdd(X.ctrl, 1u) + 1u;  // the counter starts at ~0
-        __syncthreads();
-        const uint64_t t = s_tile;
-        if (t >= ntot) break;
-        // the tile's file and its candidate positions [ca, cb) inside [h, L - h) (file-relative;
-        // a single stream skips the table lookups, which would sit before the copy)
-        uint64_t foff = 0, L = Q.L, a = t * MX_TILE;
+    // the tile's file and its candidate positions [ca, cb) inside [h, L - h) (file-relative;
+    // a single stream skips the table lookups)
+    auto tile_range = [&](uint64_t t, uint64_t &foff, uint64_t &L, uint64_t &a, uint64_t &ca, uint64_t &cb) {
+        foff = 0;
+        L = Q.L;
+        a = t * MX_TILE;
         if (Q.file_off != nullptr) {
             const uint32_t F = X.tfile[t];
             mx_file(Q, F, foff, L);
             a = (t - X.tfirst[F]) * MX_TILE;
         }
-        const uint8_t *data = Q.data + foff;
         const uint64_t b = a + MX_TILE < L ? a + MX_TILE : L;
-        const uint64_t ca = a > h ? a : h;
-        const uint64_t cb = (L > h && b > L - h) ? L - h : (L > h ? b : 0);
+        ca = a > h ? a : h;
+        cb = (L > h && b > L - h) ? L - h : (L > h ? b : 0);
+    };
+    // tiles blockIdx.x, + gridDim.x, ... (one wave of CTAs); while a tile is copied and
+    // scanned, its CTA's next tile is already being fetched into L2 (one bulk prefetch)
+#ifndef CDC_MX_PF
+#define CDC_MX_PF 0
+#endif
+#ifndef CDC_MX_STATIC
+#define CDC_MX_STATIC 0
+#endif
+    __shared__ uint32_t s_tile;
+    for (uint64_t t = blockIdx.x;; t += gridDim.x) {
+        if (!CDC_MX_STATIC) {
+            if (tid == 0) s_tile = atomicAdd(X.ctrl, 1u) + 1u;  // the counter starts at ~0
+            __syncthreads();
+            t = s_tile;
+        }
+        if (t >= ntot) break;
+        if (CDC_MX_PF && tid == 0 && t + gridDim.x < ntot) {
+            uint64_t pfo, pL, pa, pca, pcb;
+            tile_range(t + gridDim.x, pfo, pL, pa, pca, pcb);
+            if (pca < pcb) {
+                const uintptr_t p0 = reinterpret_cast<uintptr_t>(Q.data + pfo + (pca - h)) & ~static_cast<uintptr_t>(15);
+                const uintptr_t p1 = (reinterpret_cast<uintptr_t>(Q.data + pfo + (pcb + h)) + 15) & ~static_cast<uintptr_t>(15);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"((uint32_t)(p1 - p0)) : "memory");
+            }
+        }
+        uint64_t foff, L, a, ca, cb;
+        tile_range(t, foff, L, a, ca, cb);
+        const uint8_t *data = Q.data + foff;
         uint32_t count = 0;
         bool ranked = false;  // the long-window path writes its slot itself
-        if (tid == 0) s_cnt = 0;
+        if (tid == 0) s_cnt = s_ns = 0;
         if (ca < cb) {
             // bytes [lo, hi) = [ca - h, cb + h): one bulk copy of the 16-byte granules holding them
             const uint64_t lo = ca - h, hi = cb + h;
@@ -239,64 +273,89 @@ __global__ void __launch_bounds__(MX_THREADS) k_maxp_scan(MaxpGeo Q, MaxpWork X)
             const uint32_t c_lo = (uint32_t)((int64_t)ca + cbase), c_hi = (uint32_t)((int64_t)cb + cbase);
             if (h >= 31) {
                 const uint32_t K0 = (uint32_t)((h - 15) / 16);  // granules wholly inside each window
-                for (uint32_t j = tid; j < NG; j += MX_THREADS) {
-                    uint4 v = *reinterpret_cast<const uint4 *>(buf + 16 * j);
-                    if (j == 0 || j == NG - 1) {  // keep bytes [off0, vend) of the granule
-                        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                // blocks of MX_BG granules: for every granule j of block b, the blocks
+                // b - NBK .. b + NBK lie wholly inside the granules [j - K0, j + K0]
+                const uint32_t NBK = K0 >= MX_BG - 1 ? (K0 - (MX_BG - 1)) / MX_BG : 0;
+                const uint32_t NB = (NG + MX_BG - 1) / MX_BG;
+                // 1. granule maxima (the Extreme Byte Search leaf, DPX byte maxima), and the
+                //    block maxima from the MX_BG lanes of a block (consecutive granules)
+                for (uint32_t j0 = 0; j0 < NG; j0 += MX_THREADS) {  // uniform trip count (shuffles)
+                    const uint32_t j = j0 + tid;
+                    uint32_t m = 0;
+                    if (j < NG) {
+                        uint4 v = *reinterpret_cast<const uint4 *>(buf + 16 * j);
+                        if (j == 0 || j == NG - 1) {  // keep bytes [off0, vend) of the granule
+                            uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                        for (int k = 0; k < 16; ++k) {
-                            const uint32_t x = 16 * j + k;
-                            if (x < off0 || x >= vend) w[k >> 2] &= ~(0xFFu << (8 * (k & 3)));
+                            for (int k = 0; k < 16; ++k) {
+                                const uint32_t x = 16 * j + k;
+                                if (x < off0 || x >= vend) w[k >> 2] &= ~(0xFFu << (8 * (k & 3)));
+                            }
+                            v = make_uint4(w[0], w[1], w[2], w[3]);
                         }
-                        v = make_uint4(w[0], w[1], w[2], w[3]);
+                        m = vext16<true>(v);
+                        gm[j] = (uint8_t)m;
                     }
-                    gm[j] = (uint8_t)vext16<true>(v);  // Extreme Byte Search leaf (DPX byte maxima)
+#pragma unroll
+                    for (int o = 1; o < MX_BG; o <<= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+                    if ((tid & (MX_BG - 1)) == 0 && j < NG) bm[j / MX_BG] = (uint8_t)m;
                 }
                 __syncthreads();
-                // van Herk / Gil-Werman: prefix and suffix maxima inside blocks of K0 granules
-                for (uint32_t blk = tid; blk * K0 < NG; blk += MX_THREADS) {
-                    const uint32_t j0 = blk * K0, j1 = j0 + K0 < NG ? j0 + K0 : NG;
-                    uint8_t m = 0;
-                    for (uint32_t j = j0; j < j1; ++j) {
-                        m = gm[j] > m ? gm[j] : m;
-                        pf[j] = m;
+                // 2. block filter: a local maximum of block b is the block's maximum (the block
+                //    lies inside its windows) and beats blocks b-NBK..b+NBK; survivors are listed
+                //    (windows shorter than a block, K0 < MX_BG - 1: granule by granule instead,
+                //    a granule's maximum beating the K0 granules on each side; such granules
+                //    are more than K0 apart, at most NG / 2 + 1 of them)
+                const bool gmode = K0 < MX_BG - 1;
+                if (gmode) {
+                    for (uint32_t g = c_lo / 16 + tid; g < (c_hi + 15) / 16; g += MX_THREADS) {
+                        const uint32_t m = gm[g];
+                        bool ok = m != 0u && g >= K0 && g + K0 < NG;
+                        for (uint32_t k = 1; k <= K0 && ok; ++k) ok = gm[g - k] < m && gm[g + k] < m;
+                        if (ok) surv[atomicAdd(&s_ns, 1u)] = (uint16_t)g;
                     }
-                    m = 0;
-                    for (uint32_t j = j1; j-- > j0;) {
-                        m = gm[j] > m ? gm[j] : m;
-                        sf[j] = m;
+                } else {
+                    const uint32_t b_lo = (c_lo / 16) / MX_BG, b_hi = ((c_hi + 15) / 16 + MX_BG - 1) / MX_BG;
+                    for (uint32_t b = b_lo + tid; b < b_hi; b += MX_THREADS) {
+                        const uint32_t m = bm[b];
+                        bool ok = m != 0u && b >= NBK && b + NBK < NB;
+                        for (uint32_t k = 1; k <= NBK && ok; ++k) ok = bm[b - k] < m && bm[b + k] < m;
+                        if (ok) surv[atomicAdd(&s_ns, 1u)] = (uint16_t)b;
                     }
                 }
                 __syncthreads();
-                // granules that hold candidate positions; the rare candidates are appended
-                // in any order and ranked afterwards (at most ccap of them)
-                const uint32_t g_lo = c_lo / 16, g_hi = (c_hi + 15) / 16;
-                for (uint32_t j = g_lo + tid; j < g_hi; j += MX_THREADS) {
-                    const uint32_t m = gm[j];
-                    if (m == 0 || j < K0 || j + K0 >= NG) continue;
-                    // window maxima over granules [j-K0, j-1] and [j+1, j+K0] (inside the
-                    // buffer for every candidate of the tile)
-                    const uint32_t lm = max((uint32_t)sf[j - K0], (uint32_t)pf[j - 1]);
-                    const uint32_t rm = max((uint32_t)sf[j + 1], (uint32_t)pf[j + K0]);
-                    if (m <= lm || m <= rm) continue;
-                    // the granule's maximum must be unique (its bytes are within 15 <= h)
-                    const uint8_t *gp = buf + 16 * j;
-                    int nm = 0, at = 0;
-#pragma unroll
-                    for (int k = 0; k < 16; ++k)
-                        if (gp[k] == m) {
-                            ++nm;
-                            at = k;
-                        }
-                    const uint32_t tpos = 16 * j + at;
-                    if (nm != 1 || tpos < c_lo || tpos >= c_hi) continue;
-                    // the bytes of both windows outside the K0 whole granules
+                // 3. one warp per surviving block: the exact test of its maximum (PAPER.md l.196:
+                //    greater than every byte of both h-byte windows), in any order; ranked below
+                const uint32_t ns = s_ns;
+                const int lane = tid & 31;
+                for (uint32_t i = (uint32_t)tid >> 5; i < ns; i += MX_THREADS / 32) {
+                    uint32_t j, m;
+                    if (gmode) {
+                        j = surv[i];
+                        m = gm[j];
+                    } else {
+                        const uint32_t b = surv[i];
+                        m = bm[b];
+                        // the block's granule holding m (two of them: neither byte is a strict maximum)
+                        const uint32_t jb = MX_BG * b + (uint32_t)lane;
+                        const uint32_t hg = __ballot_sync(0xFFFFFFFFu, lane < MX_BG && jb < NG && gm[jb] == m);
+                        if (__popc(hg) != 1) continue;
+                        j = MX_BG * b + (uint32_t)(__ffs(hg) - 1);
+                    }
+                    if (j < K0 || j + K0 >= NG) continue;
+                    // the granule's byte holding m, unique (its bytes are within 15 <= h)
+                    const uint32_t hb = __ballot_sync(0xFFFFFFFFu, lane < 16 && buf[16 * j + lane] == m);
+                    if (__popc(hb) != 1) continue;
+                    const uint32_t tpos = 16 * j + (uint32_t)(__ffs(hb) - 1);
+                    if (tpos < c_lo || tpos >= c_hi) continue;
+                    // every other granule of [j-K0, j+K0], then the window bytes outside them
                     bool ok = true;
+                    for (uint32_t q = j - K0 + (uint32_t)lane; q <= j + K0; q += 32) ok = ok && (q == j || gm[q] < m);
                     const uint32_t l0 = tpos - (uint32_t)h, l1 = 16 * (j - K0);
-                    for (uint32_t x = l0; x < l1 && ok; ++x) ok = buf[x] < m;
+                    for (uint32_t x = l0 + (uint32_t)lane; x < l1; x += 32) ok = ok && buf[x] < m;
                     const uint32_t r0b = 16 * (j + K0 + 1), r1 = tpos + (uint32_t)h;
-                    for (uint32_t x = r0b; x <= r1 && ok; ++x) ok = buf[x] < m;
-                    if (ok) {
+                    for (uint32_t x = r0b + (uint32_t)lane; x <= r1; x += 32) ok = ok && buf[x] < m;
+                    if (__all_sync(0xFFFFFFFFu, ok) && lane == 0) {
                         const uint32_t k = atomicAdd(&s_cnt, 1u);
                         if (k < Q.ccap) cand[k] = (uint16_t)(tpos - c_lo + (uint32_t)(ca - a));
                     }
