@@ -324,6 +324,21 @@ int cdc_fetched(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64
  */
 int cdc_set_kphase(int k);
 
+/*
+ * Dense-index mode (RAM §2.1.2 l.198 and AE l.169 on streams
+ * whose every window holds the saturating byte): a single stream of 1-64 MiB
+ * with default segments (seg_bytes = halo_bytes = 0), 4096 <= window <= 24 KiB
+ * and max_size >= 2 window + 2 is first tried as one recurrence over the
+ * positions of the saturating byte (k_dense_index, k_dense_write); the kernels
+ * verify that the stream is saturated everywhere and otherwise hand the call
+ * to the ordinary pipeline on the device (the boundaries are the same; only
+ * the work differs).  on = -1 restores the default (on, or the CDC_DENSE
+ * environment variable), 0 disables it, 1 enables it.  Process-wide; it
+ * changes cdc_workspace_size's result, so set it before sizing a workspace.
+ * Returns CDC_ERR_INVALID for other values.
+ */
+int cdc_set_dense(int on);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,6 +58,7 @@ SIGNATURES = {
     "cdc_stats": ([_P, _u64, _u64, _u64, _vp, ctypes.POINTER(_u64), _vp], ctypes.c_int),
     "cdc_fetched": ([_P, _u64, _u64, _u64, _vp, ctypes.POINTER(_u64), _vp], ctypes.c_int),
     "cdc_set_kphase": ([ctypes.c_int], ctypes.c_int),
+    "cdc_set_dense": ([ctypes.c_int], ctypes.c_int),
     "cdc_profile_collect": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
                             ctypes.c_int),
 }

@@ -22,7 +22,7 @@ __all__ = [
     "chunk_async", "chunk", "chunk_batch", "chunk_batch_async", "chunk_host", "chain",
     "extreme_byte_search", "range_scan", "first_common", "last_launch_count", "abi_version",
     "profile_enable", "profile_collect", "KERNELS", "stats", "fetched", "plan_info", "segment_starts",
-    "chunk_batch_host", "set_kphase",
+    "chunk_batch_host", "set_kphase", "set_dense",
 ]
 
 
@@ -87,6 +87,11 @@ def last_launch_count() -> int:
 def set_kphase(k: int) -> None:
     """K-phase speculation (cdc_set_kphase): -1 default, 0 off, 1..8 chains per segment (process-wide)."""
     check(lib.cdc_set_kphase(k))
+
+
+def set_dense(on: int) -> None:
+    """Dense-index mode (cdc_set_dense): -1 default, 0 off, 1 on (process-wide)."""
+    check(lib.cdc_set_dense(int(on)))
 
 
 def window_for_avg(algo: str, avg_size: int) -> int:

@@ -40,7 +40,7 @@ constexpr int RING_BYTES = STAGE * NST;
 constexpr int RING_SMEM = (RING_BYTES + NST * 8 + 127) / 128 * 128;  // keeps every ring 128-byte aligned
 // R.bar[FETCH_SLOT]: bytes this warp's bulk copies fetched (ring stages and
 // sparse-walk regions), flushed into the workspace by k_speculate (cdc_fetched)
-constexpr int FETCH_SLOT = 4;
+constexpr int FETCH_SLOT = 5;
 static_assert(RING_BYTES + 8 * (FETCH_SLOT + 1) <= RING_SMEM, "fetch counter after the ring's mbarriers");
 // A ring of NST stages of STG bytes (the default is STAGE; the batch kernel
 // uses a smaller one so that more walkers fit an SM): its bytes and its
@@ -866,15 +866,17 @@ __device__ void run_chain(const WarpRing &R, const uint8_t *__restrict__ fbase, 
 //     most w after it) and nothing beats q, so the chunk ends at q+w+1 (at
 //     limit when q+w >= limit); when s+w >= limit it ends at limit whatever
 //     the bytes.
-// A chunk's *decisive bytes* start at x = s+w (RAM) or x = s (AE).  The next
-// chunk's start is at least s + 2w + 1 (RAM: its own decisive start is past
-// s + 2w + 1) or s + w + 1 (AE), so at the start of each chunk the walker
-// already issues a bulk copy (TMA, into its idle ring) of the SP_SPEC bytes
-// from there: the next chunk's decisive bytes, unless the two chunks' waits
-// for a saturating byte add up to more than SP_SPEC.  With one copy always in
-// flight behind the one being waited for, a chunk costs about half a memory
-// round trip, and only ~SP_SPEC bytes per chunk are read.  A scan that runs
-// past its region continues with copies of SP_SPEC bytes into a third slot;
+// A chunk's *decisive bytes* start at x = s+w (RAM) or x = s (AE).  Every
+// chunk but a stream's last is longer than w, so the decisive bytes of the
+// k-th chunk after this one start at or after s + GAP + (k-1)(w+1), GAP =
+// 2w+1 (RAM) or w+1 (AE).  At the start of each chunk the walker already
+// issues a bulk copy (TMA, into its idle ring) of the SP_SPEC bytes from there
+// for k = SP_DEPTH: those chunks' decisive bytes, unless the waits for a
+// saturating byte of the chunks up to it add up to more than SP_SPEC.  With
+// SP_DEPTH copies in flight behind the one being waited for, a chunk costs
+// 1/(SP_DEPTH+1) of a memory round trip, and only ~SP_SPEC bytes per chunk are
+// read.  A scan that runs past its region continues with copies of SP_SPEC
+// bytes into the continuation slots;
 // RAM's window test looks at the bytes after the last boundary (still in the
 // slot that held it), then probes the window.  At the first chunk that cannot
 // be decided this way it stops and returns false with the chunk's start in
@@ -888,10 +890,23 @@ constexpr int SP_SPEC = CDC_SP_SPEC;  // bytes per speculative or continuation c
 #ifndef CDC_SP_SLOT
 #define CDC_SP_SLOT 2048
 #endif
-constexpr int SP_SLOT = CDC_SP_SLOT;  // slot stride in the ring: slots 0/1 alternate per chunk, slot 2 continues
-constexpr int SP_NSLOT = 4;           // slots 0/1: speculative regions; 2/3: continuation regions (ping-pong)
+constexpr int SP_SLOT = CDC_SP_SLOT;  // slot stride in the ring
+// Speculative copies in flight: at the start of chunk n the walker issues the
+// copy for chunk n + SP_DEPTH (whose decisive bytes start at or after
+// s + GAP + (SP_DEPTH - 1)(w + 1): every chunk is longer than w), so a chunk
+// costs ~1/(SP_DEPTH + 1) of a memory round trip while the overshoots of
+// SP_DEPTH + 1 chunks add up to less than SP_SPEC.  Measured: a
+// lone walker waits only ~105 of its ~1,400 cycles per chunk for the copy, and
+// SP_DEPTH 2 is slower everywhere (configs[3] 1.20 -> 1.28 ms), so 1 it is.
+#ifndef CDC_SP_DEPTH
+#define CDC_SP_DEPTH 1
+#endif
+constexpr int SP_DEPTH = CDC_SP_DEPTH;
+static_assert(SP_DEPTH == 1 || SP_DEPTH == 2, "SP_DEPTH");
+constexpr int SP_CS0 = SP_DEPTH + 1;      // slots 0..SP_DEPTH rotate per chunk (speculative regions);
+constexpr int SP_NSLOT = SP_DEPTH + 3;    // SP_CS0, SP_CS0 + 1: continuation regions (ping-pong)
 static_assert(SP_NSLOT <= FETCH_SLOT, "one mbarrier per sparse-walk slot before the fetch counter");
-static_assert(Ring<4096>::BYTES >= SP_NSLOT * SP_SLOT, "sparse walk needs four slots in every ring (stages of >= 4 KiB)");
+static_assert(Ring<5120>::BYTES >= SP_NSLOT * SP_SLOT, "sparse walk needs SP_NSLOT slots in every ring (stages of >= 5 KiB)");
 static_assert(SP_SPEC % 16 == 0 && SP_SPEC <= SP_SLOT, "SP_SPEC");
 
 // First saturating byte in [lo, hi) among the slot's bytes [P, P + n) (file
@@ -1073,23 +1088,20 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
         }
         pf = -1;
         if (run && Nc > 0 && Pc + Nc < hi) {
-            const int o = s_ ^ 1;
+            const int o = s_ == SP_CS0 ? SP_CS0 + 1 : SP_CS0;
             wait(o);
             issue(o, Pc + Nc, SP_SPEC, pfP, pfN);
             pf = o;
         }
         run = true;
-        cs = s_ ^ 1;
+        cs = s_ == SP_CS0 ? SP_CS0 + 1 : SP_CS0;
         wait(s_);
         return s_;
     };
     SPT_DECL
     auto finish = [&](bool r) -> bool {
         SPT_FLUSH
-        wait(0);
-        wait(1);
-        wait(2);
-        wait(3);
+        for (int i = 0; i < SP_NSLOT; ++i) wait(i);
         __syncwarp();
         if (lane == 0) {
             for (int i = 0; i < SP_NSLOT; ++i) mbar_inval(&R.bar[i]);
@@ -1100,13 +1112,17 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
     };
     const IX GAP = RAM ? 2 * W + 1 : W + 1;  // the next chunk's decisive bytes start at or after s + GAP
     IX s = 0;
-    int cur = 0;        // slot of this chunk's speculative region (alternates 0 / 1)
+    const IX GAP2 = GAP + W + 1;  // (SP_DEPTH 2) ... and those of the chunk after it at or after s + GAP2
+    int cur = 0;        // slot of this chunk's speculative region (slots 0..SP_DEPTH in rotation)
     IX cP = 0;          // ... its region [cP, cP + cN)
     int cN = 0;
+    int n1 = 1, n2 = 2; // (SP_DEPTH 2) slots of the next chunk's region [aP, aP + aN) and of the one after it
+    IX aP = 0;
+    int aN = 0;
     int rs = -1;        // RAM: slot holding the bytes right after s, its region [rP, rP + rN)
     IX rP = 0;
     int rN = 0;
-    IX P2 = 0;          // continuation slot 2's region
+    IX P2 = 0;          // the continuation slots' current region
     int N2 = 0;
     bool wsat = false;  // RAM: this chunk's window is known to hold a 0xFF
     for (;;) {
@@ -1124,7 +1140,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
                 sat = find_ff(rs, rP, rN, s, wend) >= 0;
                 if (rP + rN > x) x = rP + rN;
             }
-            int cs = 2, pf = -1, pfN = 0;
+            int cs = SP_CS0, pf = -1, pfN = 0;
             IX pfP = 0;
             bool run = false;
             while (!sat && x < wend) {
@@ -1140,11 +1156,16 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
             }
         }
         SPT_ADD(0);
-        const int nxt = cur ^ 1;
+        const int nxt = SP_DEPTH == 1 ? (cur ^ 1) : n2;
         IX nP = 0;
         int nN = 0;
         wait(nxt);  // (the last chunk's region, already consumed)
-        if (s + GAP < Lf) issue(nxt, s + GAP, SP_SPEC, nP, nN);
+        if constexpr (SP_DEPTH == 1) {
+            if (s + GAP < Lf) issue(nxt, s + GAP, SP_SPEC, nP, nN);
+        } else {
+            if (aN <= 0 && s + GAP < Lf) issue(n1, s + GAP, SP_SPEC, aP, aN);  // (the walk's first chunk)
+            if (s + GAP2 < Lf) issue(nxt, s + GAP2, SP_SPEC, nP, nN);
+        }
         IX e;
         if (!RAM && s + W >= limit) {
             e = limit;  // no target's window fits before the limit
@@ -1169,7 +1190,7 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
             int N = cN;
             bool more = false;  // (RAM: another 0xFF within 512 bytes after the boundary byte)
             IX pos = find(cur, cP, cN, x0, hi, &more);
-            int cs = 2, pf = -1, pfN = 0;
+            int cs = SP_CS0, pf = -1, pfN = 0;
             IX pfP = 0;
             bool run = false;
             while (pos < 0 && P + N < hi && N > 0) {  // continue past the region
@@ -1211,9 +1232,19 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
         SPT_ADD(3);
         if (stop_) return finish(true);
         s = e;
-        cur = nxt;
-        cP = nP;
-        cN = nN;
+        if constexpr (SP_DEPTH == 1) {
+            cur = nxt;
+            cP = nP;
+            cN = nN;
+        } else {
+            n2 = cur;  // consumed: the next chunk's copy goes there
+            cur = n1;
+            cP = aP;
+            cN = aN;
+            n1 = nxt;
+            aP = nP;
+            aN = nN;
+        }
     }
 }
 

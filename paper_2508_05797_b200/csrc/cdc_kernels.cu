@@ -1404,6 +1404,7 @@ __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_
 }
 
 #include "cdc_kphase.cuh"  // K-phase speculation: single streams with long windows
+#include "cdc_dense.cuh"   // dense-index mode: small single streams saturated everywhere
 #include "cdc_maxp.cuh"    // MAXP: local maxima in one pass, then the chain over them
 
 // ------------------------------------------------------------------ K0 batch segment table
@@ -1868,7 +1869,24 @@ struct Plan {
     uint32_t kK, kG, kD, kcap;
     uint64_t kS, kHk;
     size_t koff[4], kreset_bytes;
+    // dense-index mode (cdc_dense.cuh): dG segments of dS bytes (0 = off)
+    uint32_t dG, dS, dsteps, dext;
+    size_t doff[6];
 };
+
+// cdc_set_dense / CDC_DENSE in the environment: 0 disables the dense-index mode
+std::atomic<int> g_dense{-2};  // (-2: not read from the environment yet)
+bool dense_on() {
+    int v = g_dense.load();
+    if (v == -2) {
+        const char *e = getenv("CDC_DENSE");
+        v = e ? atoi(e) : -1;
+        int expect = -2;
+        g_dense.compare_exchange_strong(expect, v);
+        v = g_dense.load();
+    }
+    return v != 0;
+}
 
 // CDC_KPHASE in the environment: 0 disables K-phase speculation, 1..8 forces
 // that many chains per segment; by default 4 for RAM with windows of 12 KiB and
@@ -2038,7 +2056,64 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
             P.kreset_bytes = round_up(ksz[0], 256);
         }
     }
+    // Dense-index mode: a single stream of 1-64 MiB with the default segments,
+    // a window the sparse walk would take and a cap no saturated chunk reaches.
+    // Whether the stream is saturated everywhere is found out by the kernels;
+    // the ordinary pipeline runs behind their gate otherwise.
+    P.dG = 0;
+    if (nfiles <= 1 && dense_on() && p->seg_bytes == 0 && p->halo_bytes == 0 && p->window >= 4096 &&
+        p->window <= cdc::DN_WMAX && p->max_size >= 2ull * p->window + 2 && total_len >= (1ull << 20) &&
+        total_len <= (64ull << 20)) {
+        const uint64_t nsm = (uint64_t)num_sms();
+        const uint64_t Sd = std::min<uint64_t>(std::max<uint64_t>(round_up((total_len + nsm - 1) / nsm, 4096), cdc::DN_SMIN),
+                                               cdc::DN_SMAX);
+        const uint64_t Gd = total_len / Sd;
+        if (Gd >= 2 && Gd <= (uint64_t)cdc::DN_GMAX) {
+            P.dG = (uint32_t)Gd;
+            P.dS = (uint32_t)Sd;
+            P.dsteps = (uint32_t)(2 * Sd / w1 + 2);
+            P.dext = 2 * p->window + 32;
+            size_t dsz[] = {
+                256,                                             // ctrl (reset)
+                256,                                             // gate
+                (Gd + 1) * 4,                                    // nc
+                Gd * cdc::DN_CAND * 4,                           // tab
+                Gd * cdc::DN_CAND * (size_t)P.dsteps * 4,        // rows
+                Gd * 8,                                          // ent
+            };
+            for (int i = 0; i < 6; ++i) {
+                P.doff[i] = o;
+                o += round_up(dsz[i], 256);
+            }
+            P.kK = 0;  // (one gate: the two modes never share a call)
+        }
+    }
     P.bytes = o;
+}
+
+cdc::DGeo dgeo(const cdc_params *p, const Plan &P, const uint8_t *data, uint64_t len) {
+    cdc::DGeo Q;
+    Q.data = data;
+    Q.L = len;
+    Q.G = P.dG;
+    Q.S = P.dS;
+    Q.w = p->window;
+    Q.steps = P.dsteps;
+    Q.ext = P.dext;
+    Q.ram = p->algo == CDC_RAM ? 1 : 0;
+    Q.max = p->algo == CDC_AE_MIN ? 0 : 1;
+    return Q;
+}
+cdc::DWork dcarve(const Plan &P, void *ws) {
+    uint8_t *b = static_cast<uint8_t *>(ws);
+    cdc::DWork X;
+    X.ctrl = reinterpret_cast<uint32_t *>(b + P.doff[0]);
+    X.gate = reinterpret_cast<uint32_t *>(b + P.doff[1]);
+    X.nc = reinterpret_cast<uint32_t *>(b + P.doff[2]);
+    X.tab = reinterpret_cast<uint32_t *>(b + P.doff[3]);
+    X.rows = reinterpret_cast<uint32_t *>(b + P.doff[4]);
+    X.ent = reinterpret_cast<uint64_t *>(b + P.doff[5]);
+    return X;
 }
 
 cdc::KGeo kgeo(const cdc_params *p, const Plan &P, const uint8_t *data, uint64_t len) {
@@ -2148,6 +2223,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_kspec<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_kres2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(cdc::KNODE_MAX * 8)));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_dense_index, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::DN_SMEM));
         attr_set[dev] = true;
     }
     int launches = 0;
@@ -2159,6 +2235,23 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         }
     };
     mark(0);
+    if (P.dG && !batch) {
+        // dense-index mode (cdc_dense.cuh); the ordinary pipeline behind it runs
+        // only if its gate opens (the stream is not saturated everywhere)
+        const cdc::DGeo Q = dgeo(p, P, G.data, total_len);
+        const cdc::DWork X = dcarve(P, W.list);
+        cdc::k_reset<<<1, 256, 0, st>>>(reinterpret_cast<uint4 *>(X.ctrl), 16, nullptr);
+        CDC_KCHECK("k_reset (dense)", st);
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_dense_index),
+                            dim3((unsigned)std::min<uint64_t>(Q.G, (uint64_t)num_sms())), dim3(cdc::DN_THREADS),
+                            (size_t)cdc::DN_SMEM, st, Q, X));
+        CDC_KCHECK("k_dense_index", st);
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_dense_write), dim3((Q.G + 7) / 8), dim3(256), 0, st, Q,
+                            X, d_bounds, cap, d_count));
+        CDC_KCHECK("k_dense_write", st);
+        launches += 3;
+        G.gate = X.gate;
+    }
     if (P.kK) {
         // K-phase speculation (cdc_kphase.cuh); the ordinary pipeline behind it
         // runs only if its gate opens (a halo on the true chain gave up)
@@ -2490,6 +2583,16 @@ const char *cdc_last_error(void) { return g_err.c_str(); }
 
 int cdc_last_launch_count(void) { return g_launches; }
 
+int cdc_set_dense(int on) {
+    if (on < -1 || on > 1) return fail(CDC_ERR_INVALID, "on must be -1 (default), 0 (off) or 1 (on)");
+    if (on == -1) {
+        const char *e = getenv("CDC_DENSE");
+        on = e ? atoi(e) : -1;
+    }
+    g_dense.store(on);
+    return CDC_OK;
+}
+
 int cdc_set_kphase(int k) {
     if (k < -1 || k > cdc::KP_MAXK) return fail(CDC_ERR_INVALID, "k must be -1 (default), 0 (off) or 1..8");
     if (k == -1) {
@@ -2570,6 +2673,21 @@ int cdc_stats(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_t
     make_plan(p, nfiles ? nfiles : 1, total_len, max_len, P);
     cdc::Work W = carve(P, const_cast<void *>(d_workspace));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (P.dG && nfiles <= 1) {  // dense-index mode, unless its gate sent the call to the ordinary pipeline
+        const cdc::DWork X = dcarve(P, const_cast<void *>(d_workspace));
+        uint32_t gate = 1;
+        CDC_CUDA(cudaMemcpyAsync(&gate, X.gate, 4, cudaMemcpyDeviceToHost, st));
+        CDC_CUDA(cudaStreamSynchronize(st));
+        if (gate == 0) {
+            stats[0] = P.dG;
+            stats[1] = P.dS;
+            stats[2] = P.dext;
+            stats[3] = 4;  // resolved by the dense-index mode
+            stats[4] = P.dG;
+            stats[5] = stats[6] = stats[7] = 0;
+            return CDC_OK;
+        }
+    }
     if (P.kK && nfiles <= 1) {  // K-phase: node statistics unless the gate sent the call to the ordinary pipeline
         const cdc::KWork KW = kcarve(P, const_cast<void *>(d_workspace));
         uint32_t gate = 1;

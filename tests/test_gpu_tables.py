@@ -15,7 +15,9 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(scope="module")
 def cdc(cuda_ok):
     import paper_2508_05797_b200 as m
-    return m
+    m.set_dense(0)  # (the dense-index mode would take these streams first: tests/test_gpu_dense.py)
+    yield m
+    m.set_dense(-1)
 
 
 def _run(cdc, d, p):
