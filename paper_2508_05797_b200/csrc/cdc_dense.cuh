@@ -34,13 +34,15 @@
 //   loads every table into shared memory, follows the true chain through the
 //   segments (one lookup per segment) and writes each segment's entry row and
 //   output offset: no CTA ever waits for another.
-// k_dense_write  one warp per segment copies the entry row's elements to the
-//   output as chunk ends.
+// k_dense_finish  one warp per segment copies the entry row's elements to the
+//   output as chunk ends (or, when the gate opened, resets the ordinary
+//   pipeline's lists).
 #pragma once
 
-constexpr int DN_THREADS = 512;
+constexpr int DN_THREADS = 768;
 constexpr int DN_WARPS = DN_THREADS / 32;
-constexpr int DN_WCAP = 256;        // saturating positions per warp's share of a segment's region
+constexpr int DN_NV = 11;           // 512-byte blocks a warp keeps in flight (a 128 KiB region in one round)
+constexpr int DN_WCAP = 128;        // saturating positions per warp's share of a segment's region
 constexpr int DN_ICAP = 4096;       // ... per segment region
 constexpr int DN_CAND = 128;        // candidates (table rows) per segment
 constexpr int DN_BKT = 1536;        // 256-byte buckets per segment region
@@ -49,7 +51,8 @@ constexpr uint32_t DN_END = 0xFFFFu;
 constexpr uint32_t DN_SMAX = 128u << 10, DN_SMIN = 64u << 10;  // segment bytes
 constexpr uint32_t DN_WMAX = 24u << 10;                         // largest window
 constexpr int DN_SMEM = 150 << 10;  // dynamic shared memory of k_dense_index
-constexpr int DN_TCAP = (DN_SMEM - 4 * (DN_GMAX + 1) - 64) / 4;  // table entries the resolver holds
+constexpr int DN_TCAP = (DN_SMEM - 8 * (DN_GMAX + 1) - 8 * DN_WARPS * DN_CAND - 64) / 4;  // table entries the resolver holds
+constexpr uint32_t DN_BAD = 0xFFFEu;  // (resolver) a row that is no candidate of its segment
 
 struct DGeo {
     const uint8_t *data;
@@ -71,12 +74,29 @@ struct DWork {
 };
 
 __device__ __forceinline__ void dn_fail(const DWork &X) { atomicExch(X.ctrl + 1, 0u); }
+// diagnostic stamps (cdc_debug_timing, tools/dense_timing.py): per segment {start, index built,
+// checked + buckets, table published, ticket}; after the G segments {resolve begin, tables loaded, done}
+__device__ __forceinline__ void dn_stamp(uint32_t g, int k) {
+    unsigned long long *tm = g_timing;
+    if (tm != nullptr && threadIdx.x == 0) tm[TM_STAMPS + (uint64_t)TM_PER_SEG * g + k] = globaltimer();
+}
+
+// does the 16-byte vector hold the saturating byte?  (the zero-byte test of (x - 0x01010101) & ~x &
+// 0x80808080, on ~x for 0xFF: nonzero iff some byte is zero; two operations per word)
+template <bool MAX>
+__device__ __forceinline__ bool dn_any_sat(const uint4 &v) {
+    auto z = [](uint32_t x) -> uint32_t {
+        return MAX ? ((~x - 0x01010101u) & x & 0x80808080u) : ((x - 0x01010101u) & ~x & 0x80808080u);
+    };
+    return (z(v.x) | z(v.y) | z(v.z) | z(v.w)) != 0u;
+}
 
 template <bool MAX>
-__device__ void dn_segment(const DGeo &Q, const DWork &X, uint32_t g, uint8_t *smem) {
+__device__ __forceinline__ void dn_segment(const DGeo &Q, const DWork &X, uint32_t g, uint8_t *smem) {
     uint32_t *wl = reinterpret_cast<uint32_t *>(smem);                  // DN_WARPS x DN_WCAP
     uint32_t *pos = wl + DN_WARPS * DN_WCAP;                            // DN_ICAP (+1)
-    uint16_t *bkt = reinterpret_cast<uint16_t *>(pos + DN_ICAP + 4);    // DN_BKT
+    uint16_t *succ = reinterpret_cast<uint16_t *>(pos + DN_ICAP + 4);   // DN_ICAP: index of the next chain element
+    uint16_t *bkt = succ + DN_ICAP;                                      // DN_BKT
     __shared__ uint32_t s_wc[DN_WARPS + 1];
     __shared__ uint32_t s_bad;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -91,31 +111,37 @@ __device__ void dn_segment(const DGeo &Q, const DWork &X, uint32_t g, uint8_t *s
     const uint32_t ng = (R + mis + 15u) / 16u;
     const uint32_t nblk = (ng + 31u) / 32u, bpw = (nblk + DN_WARPS - 1) / DN_WARPS;
     if (threadIdx.x == 0) s_bad = 0;
-    // ---- the warp's share: blocks [b0, b1) of 32 granules, eight in flight
+    dn_stamp(g, 0);
+    // ---- the warp's share: blocks [b0, b1) of 32 granules, DN_NV in flight
     uint32_t wc = 0;
     const uint32_t b0 = min(nblk, (uint32_t)warp * bpw), b1 = min(nblk, b0 + bpw);
     uint32_t *mine = wl + warp * DN_WCAP;
-    for (uint32_t b = b0; b < b1; b += 8) {
-        uint4 v[8];
+    for (uint32_t b = b0; b < b1; b += DN_NV) {
+        uint4 v[DN_NV];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < DN_NV; ++k) {
             const uint32_t gi = (b + k) * 32u + (uint32_t)lane;
             v[k] = (b + k < b1 && gi < ng) ? __ldcs(gran + gi) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < DN_NV; ++k) {
             const uint32_t gi = (b + k) * 32u + (uint32_t)lane;
             const int q = (int)(gi * 16u) - (int)mis;  // region-relative position of the granule's first byte
-            uint32_t m = 0;
-            if (b + k < b1 && gi < ng) {
-                const int ka = min(max(-q, 0), 16), kb = min(max((int)R - q, 0), 16);
-                m = sat_mask16<MAX>(v[k]) & ((1u << kb) - 1u) & ~((1u << ka) - 1u);
-            }
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m != 0u);
+            const bool any = b + k < b1 && gi < ng && dn_any_sat<MAX>(v[k]);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, any);
+            if (k == 0 && b == b0) dn_stamp(g, 5);
             if (bal == 0u) continue;
+            uint32_t m = 0;
+            if (any) {
+                m = sat_mask16<MAX>(v[k]);
+                if (q < 0 || q + 16 > (int)R) {  // (the region's first and last granule)
+                    const int ka = min(max(-q, 0), 16), kb = min(max((int)R - q, 0), 16);
+                    m &= ((1u << kb) - 1u) & ~((1u << ka) - 1u);
+                }
+            }
             const uint32_t c = (uint32_t)__popc(m);
             uint32_t rank, tot;
-            if (__ballot_sync(0xFFFFFFFFu, c > 1u) == 0u) {  // at most one per granule
+            if (__ballot_sync(0xFFFFFFFFu, any && c != 1u) == 0u) {  // one per granule that holds any
                 rank = (uint32_t)__popc(bal & ((1u << lane) - 1u));
                 tot = (uint32_t)__popc(bal);
             } else {
@@ -142,6 +168,7 @@ __device__ void dn_segment(const DGeo &Q, const DWork &X, uint32_t g, uint8_t *s
         }
         if (wc >= 0xFFFF0000u) break;
     }
+    dn_stamp(g, 6);
     if (lane == 0) s_wc[warp] = wc;
     __syncthreads();
     // ---- compact the warps' lists into pos[0, n)
@@ -159,6 +186,7 @@ __device__ void dn_segment(const DGeo &Q, const DWork &X, uint32_t g, uint8_t *s
     }
     for (uint32_t i = lane; i < wc; i += 32) pos[base + i] = mine[i];
     __syncthreads();
+    dn_stamp(g, 1);
     // ---- the density condition on this segment's positions, and the bucket table
     const uint32_t nb = R / 256u + 1u;  // buckets 0..nb (bkt[k]: first index with pos >= 256 k)
     bool bad = false;
@@ -179,6 +207,7 @@ __device__ void dn_segment(const DGeo &Q, const DWork &X, uint32_t g, uint8_t *s
         if (threadIdx.x == 0) dn_fail(X);
         return;
     }
+    dn_stamp(g, 2);
     auto lower = [&](uint32_t t) -> uint32_t {  // first index with pos >= t
         const uint32_t k = t >> 8;
         if (k > nb) return n;
@@ -192,14 +221,16 @@ __device__ void dn_segment(const DGeo &Q, const DWork &X, uint32_t g, uint8_t *s
         if (threadIdx.x == 0) dn_fail(X);
         return;
     }
+    // every position's successor in the chain, all at once; a row then only chases indices
+    for (uint32_t i = threadIdx.x; i < iend; i += DN_THREADS) succ[i] = (uint16_t)lower(pos[i] + Q.w + 1u);
+    __syncthreads();
     if (threadIdx.x < ncand) {
         const uint32_t r = threadIdx.x;
         uint32_t *row = X.rows + ((uint64_t)g * DN_CAND + r) * Q.steps;
         uint32_t i = r, cnt = 0, ex = DN_END;
         bool ok = true;
         for (;;) {
-            const uint32_t x = pos[i];
-            if (x >= Sg) {
+            if (i >= iend) {  // the first element past the segment
                 ex = i - iend;
                 break;
             }
@@ -207,8 +238,8 @@ __device__ void dn_segment(const DGeo &Q, const DWork &X, uint32_t g, uint8_t *s
                 ok = false;
                 break;
             }
-            row[cnt++] = x;
-            i = lower(x + Q.w + 1u);
+            row[cnt++] = pos[i];
+            i = succ[i];
             if (i >= n) {
                 ok = hi == (int64_t)Q.L;  // the chain ends with the stream
                 ex = DN_END;
@@ -227,65 +258,173 @@ __device__ void dn_segment(const DGeo &Q, const DWork &X, uint32_t g, uint8_t *s
     }
 }
 
-// The true chain through the segments (the CTA that drew the last ticket).
-__device__ void dn_resolve(const DGeo &Q, const DWork &X, uint8_t *smem) {
-    uint32_t *toff = reinterpret_cast<uint32_t *>(smem);  // G + 1
-    uint32_t *stab = toff + DN_GMAX + 1;                   // the tables, packed
-    __shared__ uint32_t s_tot;
+// The true chain through the segments (the CTA that drew the last ticket):
+// every table in shared memory, then three short passes instead of one walk
+// over all G segments -- warp b takes the block of BS consecutive segments
+// [b BS, (b+1) BS) and follows every candidate of its first segment through the
+// block (exit row, elements); one thread follows the true entry through the
+// DN_WARPS blocks; each warp follows its block's true entry again and writes
+// the segments' entries.
+__device__ __forceinline__ void dn_resolve(const DGeo &Q, const DWork &X, uint8_t *smem) {
+    uint32_t *toff = reinterpret_cast<uint32_t *>(smem);  // G + 1: where segment g's table starts in stab
+    uint32_t *tcnt = toff + DN_GMAX + 1;                   // G: its rows
+    uint32_t *bex = tcnt + DN_GMAX + 1;                    // DN_WARPS x DN_CAND: a block's exit row per entry row
+    uint32_t *bacc = bex + DN_WARPS * DN_CAND;             // ... and its elements
+    uint32_t *stab = bacc + DN_WARPS * DN_CAND;            // the tables
+    __shared__ uint32_t s_tot, s_fail;
+    __shared__ uint32_t s_brow[DN_WARPS];
+    __shared__ unsigned long long s_boff[DN_WARPS];
     const uint32_t G = Q.G;
-    for (uint32_t g = threadIdx.x; g < G; g += DN_THREADS) toff[g + 1] = min(__ldcg(X.nc + g), (uint32_t)DN_CAND);
-    __syncthreads();
-    if (threadIdx.x < 32) {  // exclusive prefix of the candidate counts: toff[g] = entries before segment g
-        uint32_t run = 0;
-        for (uint32_t g0 = 0; g0 < G; g0 += 32) {
-            const uint32_t g = g0 + threadIdx.x;
-            const uint32_t c = g < G ? toff[g + 1] : 0u;
-            uint32_t inc = c;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    dn_stamp(G, 0);
+    if (threadIdx.x == 0) s_fail = 0;
+    if (threadIdx.x < DN_WARPS) s_brow[threadIdx.x] = DN_END;
+    bool fail = false;
+    if (G * (uint32_t)DN_CAND <= (uint32_t)DN_TCAP) {
+        // few segments: every table at a fixed stride of DN_CAND rows, so the table loads need not wait
+        // for the candidate counts (rows past a segment's count are never looked at): one round trip
+        for (uint32_t g = threadIdx.x; g < G; g += DN_THREADS) {
+            tcnt[g] = min(__ldcg(X.nc + g), (uint32_t)DN_CAND);
+            toff[g] = g * DN_CAND;
+        }
+        for (uint32_t j0 = warp; j0 < G; j0 += DN_WARPS * 4) {
+            uint32_t v[4][DN_CAND / 32];
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-                if ((int)threadIdx.x >= d) inc += t;
+            for (int a = 0; a < 4; ++a) {
+                const uint32_t g = j0 + a * DN_WARPS;
+#pragma unroll
+                for (int q = 0; q < DN_CAND / 32; ++q)
+                    v[a][q] = g < G ? __ldcg(X.tab + (uint64_t)g * DN_CAND + lane + 32 * q) : 0u;
             }
-            __syncwarp();
-            if (g < G) toff[g + 1] = run + inc;
-            run += __shfl_sync(0xFFFFFFFFu, inc, 31);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const uint32_t g = j0 + a * DN_WARPS;
+#pragma unroll
+                for (int q = 0; q < DN_CAND / 32; ++q)
+                    if (g < G) stab[g * DN_CAND + lane + 32 * q] = v[a][q];
+            }
         }
-        if (threadIdx.x == 0) {
-            toff[0] = 0;
-            s_tot = run;
+        fail = __ldcg(X.ctrl + 1) != 0xFFFFFFFFu;
+    } else {
+        for (uint32_t g = threadIdx.x; g < G; g += DN_THREADS) tcnt[g] = min(__ldcg(X.nc + g), (uint32_t)DN_CAND);
+        __syncthreads();
+        if (threadIdx.x < 32) {  // exclusive prefix of the candidate counts: toff[g] = entries before segment g
+            uint32_t run = 0;
+            for (uint32_t g0 = 0; g0 < G; g0 += 32) {
+                const uint32_t g = g0 + threadIdx.x;
+                const uint32_t c = g < G ? tcnt[g] : 0u;
+                uint32_t inc = c;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                    if ((int)threadIdx.x >= d) inc += t;
+                }
+                if (g < G) toff[g] = run + inc - c;
+                run += __shfl_sync(0xFFFFFFFFu, inc, 31);
+            }
+            if (threadIdx.x == 0) s_tot = run;
+        }
+        __syncthreads();
+        fail = __ldcg(X.ctrl + 1) != 0xFFFFFFFFu || s_tot > (uint32_t)DN_TCAP;
+        if (!fail) {  // the tables, packed: four segments' loads in flight per warp
+            for (uint32_t j0 = warp; j0 < G; j0 += DN_WARPS * 4) {
+                uint32_t v[4][DN_CAND / 32];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const uint32_t g = j0 + a * DN_WARPS;
+                    const uint32_t c = g < G ? tcnt[g] : 0u;
+#pragma unroll
+                    for (int q = 0; q < DN_CAND / 32; ++q) {
+                        const uint32_t r = lane + 32 * q;
+                        v[a][q] = r < c ? __ldcg(X.tab + (uint64_t)g * DN_CAND + r) : 0u;
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const uint32_t g = j0 + a * DN_WARPS;
+                    const uint32_t c = g < G ? tcnt[g] : 0u;
+#pragma unroll
+                    for (int q = 0; q < DN_CAND / 32; ++q) {
+                        const uint32_t r = lane + 32 * q;
+                        if (r < c) stab[toff[g] + r] = v[a][q];
+                    }
+                }
+            }
         }
     }
     __syncthreads();
-    bool fail = __ldcg(X.ctrl + 1) != 0xFFFFFFFFu || s_tot > (uint32_t)DN_TCAP;
-    if (!fail) {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        for (uint32_t g = warp; g < G; g += DN_WARPS) {
-            const uint32_t c = toff[g + 1] - toff[g];
-            for (uint32_t r = lane; r < c; r += 32) stab[toff[g] + r] = __ldcg(X.tab + (uint64_t)g * DN_CAND + r);
+    dn_stamp(G, 1);
+    const uint32_t BS = (G + DN_WARPS - 1) / DN_WARPS;
+    const uint32_t g0 = min(G, (uint32_t)warp * BS), g1 = min(G, g0 + BS);
+    if (!fail && g0 < g1) {  // pass 1: every candidate of the block's first segment through the block
+        const uint32_t c0 = tcnt[g0];
+        for (uint32_t r = lane; r < c0; r += 32) {
+            uint32_t row = r, acc = 0;
+            for (uint32_t g = g0; g < g1; ++g) {
+                if (row >= tcnt[g]) {
+                    row = DN_BAD;
+                    break;
+                }
+                const uint32_t t = stab[toff[g] + row];
+                acc += t & 0xFFFFu;
+                row = t >> 16;
+                if (row == DN_END) break;
+            }
+            bex[warp * DN_CAND + r] = row;
+            bacc[warp * DN_CAND + r] = acc;
         }
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    if (!fail) {
+    if (threadIdx.x == 0 && !fail) {  // pass 2: the true chain, block by block
         uint32_t row = __ldcg(X.nc + G);
-        uint64_t off = 0;
-        uint32_t g = 0;
-        for (; g < G; ++g) {
-            if (row >= toff[g + 1] - toff[g]) {
+        unsigned long long off = 0;
+        bool ended = false;
+        for (int b = 0; b < DN_WARPS && (uint32_t)b * BS < G; ++b) {
+            const uint32_t f = (uint32_t)b * BS;
+            if (row >= tcnt[f]) {
                 fail = true;
                 break;
             }
-            X.ent[g] = (uint64_t)row | (off << 32);
-            const uint32_t t = stab[toff[g] + row];
-            off += t & 0xFFFFu;
-            row = t >> 16;
-            if (row == DN_END) break;
+            s_brow[b] = row;
+            s_boff[b] = off;
+            const uint32_t ex = bex[b * DN_CAND + row];
+            off += bacc[b * DN_CAND + row];
+            if (ex == DN_BAD) {
+                fail = true;
+                break;
+            }
+            if (ex == DN_END) {
+                ended = true;
+                break;
+            }
+            row = ex;
         }
-        if (g == G) fail = true;  // (the last segment's chains all end with the stream)
-        for (++g; g < G; ++g) X.ent[g] = ~0ull;
-        if (off >= (1ull << 32)) fail = true;
+        if (!ended || off >= (1ull << 32)) fail = true;  // (the last segment's chains all end with the stream)
+        if (fail) s_fail = 1;
     }
-    *X.gate = fail ? 1u : 0u;
+    __syncthreads();
+    if (lane == 0 && !fail && !s_fail && g0 < g1) {  // pass 3: the segments' entries
+        uint32_t row = s_brow[warp];
+        unsigned long long off = s_boff[warp];
+        uint32_t g = g0;
+        if (row != DN_END) {
+            for (; g < g1; ++g) {
+                X.ent[g] = (uint64_t)row | (off << 32);
+                const uint32_t t = stab[toff[g] + row];
+                off += t & 0xFFFFu;
+                row = t >> 16;
+                if (row == DN_END) {
+                    ++g;
+                    break;
+                }
+            }
+        }
+        for (; g < g1; ++g) X.ent[g] = ~0ull;  // the chain ended before these
+    }
+    if (threadIdx.x == 0) {
+        *X.gate = (fail || s_fail) ? 1u : 0u;
+        dn_stamp(G, 2);
+    }
 }
 
 __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_index(DGeo Q, DWork X) {
@@ -302,8 +441,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_index(DGeo Q, DWork X) 
         }
         __threadfence();  // this segment's table and rows before its ticket
         __syncthreads();
+        dn_stamp(g, 3);
         if (threadIdx.x == 0) s_last = atomicAdd(X.ctrl, 1u) + 1u == Q.G - 1u ? 1u : 0u;  // the counter starts at ~0
         __syncthreads();
+        dn_stamp(g, 4);
         if (s_last) {
             __threadfence();
             dn_resolve(Q, X, smem);
@@ -312,12 +453,23 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_index(DGeo Q, DWork X) 
     }
 }
 
-__global__ void __launch_bounds__(256) k_dense_write(DGeo Q, DWork X, uint64_t *bounds, uint64_t cap, uint64_t *d_count) {
+// After k_dense_index: when its gate is shut, one warp per segment copies the
+// entry row's elements to the output as chunk ends; when it is open, this is
+// the ordinary pipeline's list reset (k_reset's loop over [p, p + n16)), so the
+// fallback costs no extra launch and the dense path none for the reset.
+__global__ void __launch_bounds__(256) k_dense_finish(DGeo Q, DWork X, uint64_t *bounds, uint64_t cap, uint64_t *d_count,
+                                                      uint4 *rst, uint64_t n16) {
     pdl_wait();
     pdl_trigger();
+    if (*X.gate != 0u) {
+        const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u);
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
+            rst[i] = ones;
+        return;
+    }
     const int lane = threadIdx.x & 31;
     const uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (g >= Q.G || *X.gate != 0u) return;
+    if (g >= Q.G) return;
     const uint64_t e = X.ent[g];
     if (e == ~0ull) return;
     const uint32_t row = (uint32_t)e;

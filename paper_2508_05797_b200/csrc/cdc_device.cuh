@@ -1116,9 +1116,9 @@ __device__ bool sparse_chain(const WarpRing &R, const uint8_t *__restrict__ fbas
     int cur = 0;        // slot of this chunk's speculative region (slots 0..SP_DEPTH in rotation)
     IX cP = 0;          // ... its region [cP, cP + cN)
     int cN = 0;
-    int n1 = 1, n2 = 2; // (SP_DEPTH 2) slots of the next chunk's region [aP, aP + aN) and of the one after it
-    IX aP = 0;
-    int aN = 0;
+    [[maybe_unused]] int n1 = 1, n2 = 2; // (SP_DEPTH 2) slots of the next chunk's region [aP, aP + aN) and of the one after it
+    [[maybe_unused]] IX aP = 0;
+    [[maybe_unused]] int aN = 0;
     int rs = -1;        // RAM: slot holding the bytes right after s, its region [rP, rP + rN)
     IX rP = 0;
     int rN = 0;

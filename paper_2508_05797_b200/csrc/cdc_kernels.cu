@@ -424,6 +424,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // K0': reset of the published-list region (list entries, publish, look-back
 // and ticket words) to all-ones; lets k_speculate launch early (PDL).
 __global__ void __launch_bounds__(256) k_reset(uint4 *p, uint64_t n16, const uint32_t *gate) {
+    if (gate) pdl_wait();  // (a gated reset is launched with PDL behind the kernels that write its gate)
     pdl_trigger();
     if (gate && *gate == 0) return;
     if (threadIdx.x == 0) stamp(TM_RESET_BEGIN);
@@ -2235,6 +2236,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         }
     };
     mark(0);
+    bool dense_reset = false;  // the reset below is part of k_dense_finish
     if (P.dG && !batch) {
         // dense-index mode (cdc_dense.cuh); the ordinary pipeline behind it runs
         // only if its gate opens (the stream is not saturated everywhere)
@@ -2246,11 +2248,15 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
                             dim3((unsigned)std::min<uint64_t>(Q.G, (uint64_t)num_sms())), dim3(cdc::DN_THREADS),
                             (size_t)cdc::DN_SMEM, st, Q, X));
         CDC_KCHECK("k_dense_index", st);
-        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_dense_write), dim3((Q.G + 7) / 8), dim3(256), 0, st, Q,
-                            X, d_bounds, cap, d_count));
-        CDC_KCHECK("k_dense_write", st);
+        // (k_dense_finish writes the output, or is the ordinary pipeline's list reset when the gate opened)
+        const uint64_t n16 = P.reset_bytes / 16;
+        const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_dense_finish), dim3(std::max(rb, (Q.G + 7) / 8)),
+                            dim3(256), 0, st, Q, X, d_bounds, cap, d_count, reinterpret_cast<uint4 *>(W.list), n16));
+        CDC_KCHECK("k_dense_finish", st);
         launches += 3;
         G.gate = X.gate;
+        dense_reset = true;
     }
     if (P.kK) {
         // K-phase speculation (cdc_kphase.cuh); the ordinary pipeline behind it
@@ -2282,13 +2288,17 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     }
     // reset the published lists (list entries -> LIST_EMPTY, pub -> PUB_OPEN) and
     // the look-back, ticket and flag words
-    {
+    if (!dense_reset) {
         const uint64_t n16 = P.reset_bytes / 16;  // reset_bytes is a multiple of 256
         const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());
-        cdc::k_reset<<<rb ? rb : 1, 256, 0, st>>>(reinterpret_cast<uint4 *>(W.list), n16, G.gate);
+        if (G.gate)
+            CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_reset), dim3(rb ? rb : 1), dim3(256), 0, st,
+                                reinterpret_cast<uint4 *>(W.list), n16, G.gate));
+        else
+            cdc::k_reset<<<rb ? rb : 1, 256, 0, st>>>(reinterpret_cast<uint4 *>(W.list), n16, G.gate);
         CDC_KCHECK("k_reset", st);
+        ++launches;
     }
-    ++launches;
     if (batch) {
         // segment table (launched with PDL behind the reset; k_speculate behind it)
         const uint64_t tiles = (G.nfiles + cdc::SP_THREADS * cdc::SP_RPT - 1) / (cdc::SP_THREADS * cdc::SP_RPT);

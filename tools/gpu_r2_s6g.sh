@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_dense.py tests/test_gpu_kphase.py -x -q --tb=short > gpurun_out/t_dense.log 2>&1; echo dense rc=$?; tail -3 gpurun_out/t_dense.log
+timeout 300 python tools/dense_timing.py
+N=$((64<<20)) STAMPS=0 timeout 300 python tools/dense_timing.py
+ONLY="c2" timeout 600 python tools/workloads.py 2>&1 | grep base | cut -c1-72
