@@ -273,12 +273,17 @@ __device__ __forceinline__ void dn_resolve(const DGeo &Q, const DWork &X, uint8_
     uint32_t *stab = bacc + DN_WARPS * DN_CAND;            // the tables
     __shared__ uint32_t s_tot, s_fail;
     __shared__ uint32_t s_brow[DN_WARPS];
-    __shared__ unsigned long long s_boff[DN_WARPS];
+    __shared__ uint32_t s_boff[DN_WARPS];
     const uint32_t G = Q.G;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     dn_stamp(G, 0);
-    if (threadIdx.x == 0) s_fail = 0;
+    __shared__ uint32_t s_r0;
+    if (threadIdx.x == 0) {
+        s_fail = 0;
+        s_r0 = __ldcg(X.nc + G);  // the entry row of segment 0
+    }
     if (threadIdx.x < DN_WARPS) s_brow[threadIdx.x] = DN_END;
+    const bool gave_up = __ldcg(X.ctrl + 1) != 0xFFFFFFFFu;  // (read along with the tables)
     bool fail = false;
     if (G * (uint32_t)DN_CAND <= (uint32_t)DN_TCAP) {
         // few segments: every table at a fixed stride of DN_CAND rows, so the table loads need not wait
@@ -288,23 +293,24 @@ __device__ __forceinline__ void dn_resolve(const DGeo &Q, const DWork &X, uint8_
             toff[g] = g * DN_CAND;
         }
         for (uint32_t j0 = warp; j0 < G; j0 += DN_WARPS * 4) {
-            uint32_t v[4][DN_CAND / 32];
+            uint32_t v[4][DN_CAND / 32], c[4];
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
                 const uint32_t g = j0 + a * DN_WARPS;
+                c[a] = g < G ? __ldcg(X.nc + g) : 0u;
 #pragma unroll
                 for (int q = 0; q < DN_CAND / 32; ++q)
                     v[a][q] = g < G ? __ldcg(X.tab + (uint64_t)g * DN_CAND + lane + 32 * q) : 0u;
             }
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
+            for (int a = 0; a < 4; ++a) {  // (rows past the segment's count: never written, marked as no candidates)
                 const uint32_t g = j0 + a * DN_WARPS;
 #pragma unroll
                 for (int q = 0; q < DN_CAND / 32; ++q)
-                    if (g < G) stab[g * DN_CAND + lane + 32 * q] = v[a][q];
+                    if (g < G) stab[g * DN_CAND + lane + 32 * q] = (uint32_t)(lane + 32 * q) < c[a] ? v[a][q] : DN_BAD << 16;
             }
         }
-        fail = __ldcg(X.ctrl + 1) != 0xFFFFFFFFu;
+        fail = gave_up;
     } else {
         for (uint32_t g = threadIdx.x; g < G; g += DN_THREADS) tcnt[g] = min(__ldcg(X.nc + g), (uint32_t)DN_CAND);
         __syncthreads();
@@ -325,7 +331,7 @@ __device__ __forceinline__ void dn_resolve(const DGeo &Q, const DWork &X, uint8_
             if (threadIdx.x == 0) s_tot = run;
         }
         __syncthreads();
-        fail = __ldcg(X.ctrl + 1) != 0xFFFFFFFFu || s_tot > (uint32_t)DN_TCAP;
+        fail = gave_up || s_tot > (uint32_t)DN_TCAP;
         if (!fail) {  // the tables, packed: four segments' loads in flight per warp
             for (uint32_t j0 = warp; j0 < G; j0 += DN_WARPS * 4) {
                 uint32_t v[4][DN_CAND / 32];
@@ -354,70 +360,61 @@ __device__ __forceinline__ void dn_resolve(const DGeo &Q, const DWork &X, uint8_
     }
     __syncthreads();
     dn_stamp(G, 1);
+    const bool stride = G * (uint32_t)DN_CAND <= (uint32_t)DN_TCAP;
     const uint32_t BS = (G + DN_WARPS - 1) / DN_WARPS;
     const uint32_t g0 = min(G, (uint32_t)warp * BS), g1 = min(G, g0 + BS);
-    if (!fail && g0 < g1) {  // pass 1: every candidate of the block's first segment through the block
+    if (!fail && g0 < g1) {  // pass 1: every row of the block's first segment through the block, four per lane
+        uint32_t row[DN_CAND / 32], acc[DN_CAND / 32];
         const uint32_t c0 = tcnt[g0];
-        for (uint32_t r = lane; r < c0; r += 32) {
-            uint32_t row = r, acc = 0;
-            for (uint32_t g = g0; g < g1; ++g) {
-                if (row >= tcnt[g]) {
-                    row = DN_BAD;
-                    break;
+#pragma unroll
+        for (int q = 0; q < DN_CAND / 32; ++q) {
+            row[q] = (uint32_t)(lane + 32 * q) < c0 ? (uint32_t)(lane + 32 * q) : DN_BAD;
+            acc[q] = 0;
+        }
+        for (uint32_t g = g0; g < g1; ++g) {
+            const uint32_t lim = stride ? (uint32_t)DN_CAND : tcnt[g], o = toff[g];
+#pragma unroll
+            for (int q = 0; q < DN_CAND / 32; ++q) {
+                if (row[q] < lim) {
+                    const uint32_t t = stab[o + row[q]];
+                    acc[q] += t & 0xFFFFu;
+                    row[q] = t >> 16;
+                } else if (row[q] < DN_BAD) {
+                    row[q] = DN_BAD;  // (packed tables: a row that is no candidate of this segment)
                 }
-                const uint32_t t = stab[toff[g] + row];
-                acc += t & 0xFFFFu;
-                row = t >> 16;
-                if (row == DN_END) break;
             }
-            bex[warp * DN_CAND + r] = row;
-            bacc[warp * DN_CAND + r] = acc;
+        }
+#pragma unroll
+        for (int q = 0; q < DN_CAND / 32; ++q) {
+            bex[warp * DN_CAND + lane + 32 * q] = row[q];
+            bacc[warp * DN_CAND + lane + 32 * q] = acc[q];
         }
     }
     __syncthreads();
+    dn_stamp(G, 3);
     if (threadIdx.x == 0 && !fail) {  // pass 2: the true chain, block by block
-        uint32_t row = __ldcg(X.nc + G);
-        unsigned long long off = 0;
-        bool ended = false;
-        for (int b = 0; b < DN_WARPS && (uint32_t)b * BS < G; ++b) {
-            const uint32_t f = (uint32_t)b * BS;
-            if (row >= tcnt[f]) {
-                fail = true;
-                break;
-            }
+        uint32_t row = s_r0, off = 0;
+        const int nblk = (int)((G + BS - 1) / BS);
+        for (int b = 0; b < nblk; ++b) {
             s_brow[b] = row;
             s_boff[b] = off;
-            const uint32_t ex = bex[b * DN_CAND + row];
+            if (row >= (uint32_t)DN_CAND) break;  // DN_END: the chain ended; DN_BAD: give up
             off += bacc[b * DN_CAND + row];
-            if (ex == DN_BAD) {
-                fail = true;
-                break;
-            }
-            if (ex == DN_END) {
-                ended = true;
-                break;
-            }
-            row = ex;
+            row = bex[b * DN_CAND + row];
         }
-        if (!ended || off >= (1ull << 32)) fail = true;  // (the last segment's chains all end with the stream)
-        if (fail) s_fail = 1;
+        if (row != DN_END) s_fail = 1;  // (the last segment's chains all end with the stream)
     }
+    dn_stamp(G, 4);
     __syncthreads();
     if (lane == 0 && !fail && !s_fail && g0 < g1) {  // pass 3: the segments' entries
         uint32_t row = s_brow[warp];
         unsigned long long off = s_boff[warp];
         uint32_t g = g0;
-        if (row != DN_END) {
-            for (; g < g1; ++g) {
-                X.ent[g] = (uint64_t)row | (off << 32);
-                const uint32_t t = stab[toff[g] + row];
-                off += t & 0xFFFFu;
-                row = t >> 16;
-                if (row == DN_END) {
-                    ++g;
-                    break;
-                }
-            }
+        for (; g < g1 && row < (uint32_t)DN_CAND; ++g) {
+            X.ent[g] = (uint64_t)row | (off << 32);
+            const uint32_t t = stab[toff[g] + row];
+            off += t & 0xFFFFu;
+            row = t >> 16;
         }
         for (; g < g1; ++g) X.ent[g] = ~0ull;  // the chain ended before these
     }
