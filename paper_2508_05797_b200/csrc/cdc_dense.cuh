@@ -30,10 +30,10 @@
 //   segment at one of its candidates -- the positions in [p_g, p_g + w) and the
 //   first one at or after p_g + w -- and thread r follows candidate r through
 //   the segment, recording its elements (rows) and publishing (exit candidate
-//   of the next segment, element count).  The CTA that draws the last ticket
-//   loads every table into shared memory, follows the true chain through the
-//   segments (one lookup per segment) and writes each segment's entry row and
-//   output offset: no CTA ever waits for another.
+//   of the next segment, element count).  No CTA ever waits for another.
+// k_dense_resolve  one CTA (PDL behind the index kernel) loads every table into
+//   shared memory, follows the true chain through the segments in three short
+//   passes and writes each segment's entry row and output offset, and the gate.
 // k_dense_finish  one warp per segment copies the entry row's elements to the
 //   output as chunk ends (or, when the gate opened, resets the ordinary
 //   pipeline's lists).
@@ -65,7 +65,8 @@ struct DGeo {
     int max;            // 1: the saturating byte is 0xFF, 0: 0x00
 };
 struct DWork {
-    uint32_t *ctrl;     // [0] segment ticket, [1] failure flag (reset to ~0 by k_reset)
+    unsigned long long *ctrl;  // [0] the call's abort word: DN_ABORT once a segment gave up (any other value: none
+                        // did, so a fresh workspace needs no reset); k_dense_resolve leaves 0
     uint32_t *gate;     // written by the last CTA: 0 = the output is written here, 1 = run the ordinary pipeline
     uint32_t *nc;       // G: candidates per segment; nc[G]: the entry row of segment 0
     uint32_t *tab;      // G x DN_CAND: exit row << 16 | elements
@@ -73,9 +74,11 @@ struct DWork {
     uint64_t *ent;      // G: entry row | output offset << 32 (~0: the chain ended before the segment)
 };
 
-__device__ __forceinline__ void dn_fail(const DWork &X) { atomicExch(X.ctrl + 1, 0u); }
+constexpr unsigned long long DN_ABORT = 0x9E3779B97F4A7C15ull;
+__device__ __forceinline__ void dn_fail(const DWork &X) { *reinterpret_cast<volatile unsigned long long *>(X.ctrl) = DN_ABORT; }
+__device__ __forceinline__ bool dn_aborted(const DWork &X) { return __ldcg(X.ctrl) == DN_ABORT; }
 // diagnostic stamps (cdc_debug_timing, tools/dense_timing.py): per segment {start, index built,
-// checked + buckets, table published, ticket}; after the G segments {resolve begin, tables loaded, done}
+// checked + buckets, table published}; after the G segments {resolve begin, tables loaded, done, pass 1, pass 2}
 __device__ __forceinline__ void dn_stamp(uint32_t g, int k) {
     unsigned long long *tm = g_timing;
     if (tm != nullptr && threadIdx.x == 0) tm[TM_STAMPS + (uint64_t)TM_PER_SEG * g + k] = globaltimer();
@@ -258,7 +261,7 @@ __device__ __forceinline__ void dn_segment(const DGeo &Q, const DWork &X, uint32
     }
 }
 
-// The true chain through the segments (the CTA that drew the last ticket):
+// The true chain through the segments (k_dense_resolve's one CTA):
 // every table in shared memory, then three short passes instead of one walk
 // over all G segments -- warp b takes the block of BS consecutive segments
 // [b BS, (b+1) BS) and follows every candidate of its first segment through the
@@ -283,7 +286,7 @@ __device__ __forceinline__ void dn_resolve(const DGeo &Q, const DWork &X, uint8_
         s_r0 = __ldcg(X.nc + G);  // the entry row of segment 0
     }
     if (threadIdx.x < DN_WARPS) s_brow[threadIdx.x] = DN_END;
-    const bool gave_up = __ldcg(X.ctrl + 1) != 0xFFFFFFFFu;  // (read along with the tables)
+    const bool gave_up = dn_aborted(X);  // (read along with the tables)
     bool fail = false;
     if (G * (uint32_t)DN_CAND <= (uint32_t)DN_TCAP) {
         // few segments: every table at a fixed stride of DN_CAND rows, so the table loads need not wait
@@ -422,32 +425,33 @@ __device__ __forceinline__ void dn_resolve(const DGeo &Q, const DWork &X, uint8_
         *X.gate = (fail || s_fail) ? 1u : 0u;
         dn_stamp(G, 2);
     }
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_index(DGeo Q, DWork X) {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint32_t s_last, s_go;
-    pdl_wait();     // the reset of ctrl has completed
-    pdl_trigger();
+    __shared__ uint32_t s_go;
+    pdl_trigger();  // (k_dense_resolve waits for this grid's completion before it reads anything)
     for (uint32_t g = blockIdx.x; g < Q.G; g += gridDim.x) {
-        if (threadIdx.x == 0) s_go = __ldcg(X.ctrl + 1) == 0xFFFFFFFFu ? 1u : 0u;
+        if (threadIdx.x == 0) s_go = dn_aborted(X) ? 0u : 1u;
         __syncthreads();
-        if (s_go) {  // (else another segment gave up: only the tickets are left to take)
+        if (s_go) {  // (else another segment gave up: nothing left to do)
             if (Q.max) dn_segment<true>(Q, X, g, smem);
             else dn_segment<false>(Q, X, g, smem);
         }
-        __threadfence();  // this segment's table and rows before its ticket
-        __syncthreads();
         dn_stamp(g, 3);
-        if (threadIdx.x == 0) s_last = atomicAdd(X.ctrl, 1u) + 1u == Q.G - 1u ? 1u : 0u;  // the counter starts at ~0
-        __syncthreads();
-        dn_stamp(g, 4);
-        if (s_last) {
-            __threadfence();
-            dn_resolve(Q, X, smem);
-        }
         __syncthreads();
     }
+}
+
+// One CTA, launched with PDL behind k_dense_index: the true chain through the
+// segments' tables, each segment's entry row and output offset, the gate.
+__global__ void __launch_bounds__(DN_THREADS, 1) k_dense_resolve(DGeo Q, DWork X) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    pdl_wait();
+    pdl_trigger();
+    dn_resolve(Q, X, smem);
+    if (threadIdx.x == 0) *X.ctrl = 0ull;  // (after every thread's read of it: dn_resolve ends with barriers)
 }
 
 // After k_dense_index: when its gate is shut, one warp per segment copies the

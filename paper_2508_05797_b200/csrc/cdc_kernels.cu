@@ -2108,7 +2108,7 @@ cdc::DGeo dgeo(const cdc_params *p, const Plan &P, const uint8_t *data, uint64_t
 cdc::DWork dcarve(const Plan &P, void *ws) {
     uint8_t *b = static_cast<uint8_t *>(ws);
     cdc::DWork X;
-    X.ctrl = reinterpret_cast<uint32_t *>(b + P.doff[0]);
+    X.ctrl = reinterpret_cast<unsigned long long *>(b + P.doff[0]);
     X.gate = reinterpret_cast<uint32_t *>(b + P.doff[1]);
     X.nc = reinterpret_cast<uint32_t *>(b + P.doff[2]);
     X.tab = reinterpret_cast<uint32_t *>(b + P.doff[3]);
@@ -2225,6 +2225,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_kres2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(cdc::KNODE_MAX * 8)));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_dense_index, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::DN_SMEM));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_dense_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::DN_SMEM));
         attr_set[dev] = true;
     }
     int launches = 0;
@@ -2242,12 +2243,11 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         // only if its gate opens (the stream is not saturated everywhere)
         const cdc::DGeo Q = dgeo(p, P, G.data, total_len);
         const cdc::DWork X = dcarve(P, W.list);
-        cdc::k_reset<<<1, 256, 0, st>>>(reinterpret_cast<uint4 *>(X.ctrl), 16, nullptr);
-        CDC_KCHECK("k_reset (dense)", st);
-        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_dense_index),
-                            dim3((unsigned)std::min<uint64_t>(Q.G, (uint64_t)num_sms())), dim3(cdc::DN_THREADS),
-                            (size_t)cdc::DN_SMEM, st, Q, X));
+        cdc::k_dense_index<<<(unsigned)std::min<uint64_t>(Q.G, (uint64_t)num_sms()), cdc::DN_THREADS, cdc::DN_SMEM, st>>>(Q, X);
         CDC_KCHECK("k_dense_index", st);
+        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_dense_resolve), dim3(1), dim3(cdc::DN_THREADS),
+                            (size_t)cdc::DN_SMEM, st, Q, X));
+        CDC_KCHECK("k_dense_resolve", st);
         // (k_dense_finish writes the output, or is the ordinary pipeline's list reset when the gate opened)
         const uint64_t n16 = P.reset_bytes / 16;
         const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());

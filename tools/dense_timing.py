@@ -58,7 +58,7 @@ if os.environ.get("STAMPS", "1") == "1":
     lib.cdc_debug_timing(None)
     a = tm[8:].cpu().numpy().reshape(G + 1, 7).astype(np.float64)
     t0 = a[:G, 0].min()
-    for k, name in enumerate(("start", "index built", "checked+buckets", "table done", "ticket", "w0 first data", "w0 blocks done")):
+    for k, name in enumerate(("start", "index built", "checked+buckets", "table done", "(unused)", "w0 first data", "w0 blocks done")):
         v = (a[:G, k] - t0) / 1e3
         print("%-16s us: min %6.1f p50 %6.1f max %6.1f" % (name, v.min(), np.median(v), v.max()))
     print("resolve: begin %.1f  tables loaded %.1f  done %.1f us; pass 1 done %.1f  pass 2 done %.1f" % tuple((a[G, :5] - t0) / 1e3))
