@@ -158,7 +158,13 @@ struct Geometry {
     int tmode;       // walkers may try transfer tables (single stream, one co-resident wave)
     int sparse;      // walkers start with the sparse walk (sparse_chain; long windows)
     const uint32_t *gate;  // non-null: run only if *gate != 0 (the fallback behind the K-phase pipeline)
+    // non-null: the dense-index mode's gate, final before any kernel behind k_dense_finish can start (each
+    // of them triggers its dependents only after it started, k_dense_finish only after its wait for the
+    // resolver), so it is read before griddepcontrol.wait: behind a shut gate the chain of PDL launches
+    // collapses instead of each kernel waiting for the one before it
+    const uint32_t *gate0;
 };
+__device__ __forceinline__ bool gate0_shut(const uint32_t *g0) { return g0 != nullptr && __ldcg(g0) == 0u; }
 
 __device__ __forceinline__ void file_bounds(const Geometry &G, uint64_t f, uint64_t &off, uint64_t &len) {
     if (G.file_off == nullptr) {
@@ -423,7 +429,9 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 // K0': reset of the published-list region (list entries, publish, look-back
 // and ticket words) to all-ones; lets k_speculate launch early (PDL).
-__global__ void __launch_bounds__(256) k_reset(uint4 *p, uint64_t n16, const uint32_t *gate) {
+__global__ void __launch_bounds__(256) k_reset(uint4 *p, uint64_t n16, const uint32_t *gate,
+                                               const uint32_t *gate0 = nullptr) {
+    if (gate0 != nullptr && __ldcg(gate0) == 0u) return;  // (the dense-index mode wrote the output: see Geometry::gate0)
     if (gate) pdl_wait();  // (a gated reset is launched with PDL behind the kernels that write its gate)
     pdl_trigger();
     if (gate && *gate == 0) return;
@@ -585,6 +593,7 @@ __global__ void __launch_bounds__(NW * 32, SPEC_CTAS_PER_SM) k_speculate(Geometr
     __shared__ uint32_t s_ticket;
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) stamp(TM_SPEC_BEGIN);
+    if (gate0_shut(G.gate0)) return;
     pdl_wait();  // the reset of the published lists has completed
     if (G.gate && *G.gate == 0) return;  // the K-phase pipeline produced the output
     if (threadIdx.x == 0) {
@@ -1373,6 +1382,7 @@ __global__ void __launch_bounds__(1024) k_fixup(Geometry G, Work W, uint64_t *d_
                                                 uint64_t *bounds, uint64_t cap) {
     __shared__ uint32_t s_role;
     if (threadIdx.x == 0) stamp(TM_FIX_BEGIN);
+    if (gate0_shut(G.gate0)) return;
     pdl_wait();  // k_speculate has completed and its writes are visible
     if (G.gate && *G.gate == 0) return;  // the K-phase pipeline produced the output
     if (threadIdx.x == 0) stamp(TM_FIX_WAITED);
@@ -2021,14 +2031,30 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     // their halos (configs[4]'s 8 GiB per GPU: 3.6 MB segments, where K
     // chains would only multiply the body walks).  Same segments as the
     // ordinary plan, K nodes each.
+    // A small stream with default segments (the dense-index mode's range, below)
+    // takes K-phase as well, behind the dense attempt and in front of the
+    // transfer tables: the dense mode resolves what is saturated everywhere, and
+    // on anything else (versioned data with zero-filled regions) a failed table
+    // attempt leaves one speculative chain per segment, whose halos cost 2-20x
+    // the K-phase walk (64 MiB versioned, RAM 16 KiB: 7.8 ms against 0.43 ms).
+    // Such a stream has fewer nodes than walkers, so K is raised until they match.
     P.kK = 0;
-    const int K = nfiles <= 1 ? kphase_k(p->algo, p->window) : 0;
+    const bool small = nfiles <= 1 && dense_on() && p->seg_bytes == 0 && p->halo_bytes == 0 && p->window >= 4096 &&
+                       p->window <= cdc::DN_WMAX && p->max_size >= 2ull * p->window + 2 &&
+                       total_len >= (1ull << 20) && total_len <= (64ull << 20);
+    int K = nfiles <= 1 ? kphase_k(p->algo, p->window) : 0;
     const bool tm = tmode_on() && p->window >= 4096 && S <= T_MAX_SEG;
     const uint64_t kmax_seg = kphase_segs() ? ~0ull : (p->window >= 12288 ? 4ull << 20 : 1ull << 20);
-    if (K > 0 && total_len > 0 && sparse_on(p->window, p->max_size) && !tm && S <= kmax_seg) {
+    // (default segments: K-phase also in front of the transfer tables' range -- a failed table attempt on a
+    // stream saturated only in parts costs far more than the tables win on one saturated everywhere:
+    // 128 MiB versioned, RAM 16 KiB, 10.7 ms against 0.48 ms)
+    const bool prefer_k = p->seg_bytes == 0 && p->halo_bytes == 0 && dense_on();
+    if (K > 0 && total_len > 0 && sparse_on(p->window, p->max_size) && (!tm || small || prefer_k) && S <= kmax_seg) {
         uint64_t Sk = S;
         if (kphase_segs()) Sk = std::max<uint64_t>(round_up(total_len / kphase_segs(), 4096), 64 << 10);
         uint64_t Gk = cdc::nseg_of(total_len, Sk);
+        if ((small || prefer_k) && g_kphase.load() < 0 && Gk > 0)  // (the default K only: cdc_set_kphase / CDC_KPHASE force theirs)
+            K = (int)std::min<uint64_t>(cdc::KP_MAXK, std::max<uint64_t>((uint64_t)K, (uint64_t)num_sms() * cdc::SPEC_WARPS / Gk));
         if (Gk * K > cdc::KNODE_MAX) {
             Sk = round_up(total_len / (cdc::KNODE_MAX / K) + 1, 4096);
             Gk = cdc::nseg_of(total_len, Sk);
@@ -2062,9 +2088,7 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     // Whether the stream is saturated everywhere is found out by the kernels;
     // the ordinary pipeline runs behind their gate otherwise.
     P.dG = 0;
-    if (nfiles <= 1 && dense_on() && p->seg_bytes == 0 && p->halo_bytes == 0 && p->window >= 4096 &&
-        p->window <= cdc::DN_WMAX && p->max_size >= 2ull * p->window + 2 && total_len >= (1ull << 20) &&
-        total_len <= (64ull << 20)) {
+    if (small) {
         const uint64_t nsm = (uint64_t)num_sms();
         const uint64_t Sd = std::min<uint64_t>(std::max<uint64_t>(round_up((total_len + nsm - 1) / nsm, 4096), cdc::DN_SMIN),
                                                cdc::DN_SMAX);
@@ -2086,7 +2110,6 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
                 P.doff[i] = o;
                 o += round_up(dsz[i], 256);
             }
-            P.kK = 0;  // (one gate: the two modes never share a call)
         }
     }
     P.bytes = o;
@@ -2129,6 +2152,7 @@ cdc::KGeo kgeo(const cdc_params *p, const Plan &P, const uint8_t *data, uint64_t
     Q.max_size = p->max_size;
     Q.Hk = P.kHk;
     Q.sparse = sparse_on(p->window, p->max_size);
+    Q.skip = nullptr;
     return Q;
 }
 cdc::KWork kcarve(const Plan &P, void *ws) {
@@ -2238,6 +2262,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
     };
     mark(0);
     bool dense_reset = false;  // the reset below is part of k_dense_finish
+    const uint32_t *dense_gate = nullptr;
     if (P.dG && !batch) {
         // dense-index mode (cdc_dense.cuh); the ordinary pipeline behind it runs
         // only if its gate opens (the stream is not saturated everywhere)
@@ -2248,26 +2273,35 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_dense_resolve), dim3(1), dim3(cdc::DN_THREADS),
                             (size_t)cdc::DN_SMEM, st, Q, X));
         CDC_KCHECK("k_dense_resolve", st);
-        // (k_dense_finish writes the output, or is the ordinary pipeline's list reset when the gate opened)
-        const uint64_t n16 = P.reset_bytes / 16;
+        // (k_dense_finish writes the output, or is the list reset of what follows when the gate opened:
+        // K-phase's lists, else the ordinary pipeline's)
+        const uint64_t n16 = (P.kK ? P.kreset_bytes : P.reset_bytes) / 16;
+        uint4 *rst = reinterpret_cast<uint4 *>(P.kK ? (void *)kcarve(P, W.list).list : (void *)W.list);
         const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());
         CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_dense_finish), dim3(std::max(rb, (Q.G + 7) / 8)),
-                            dim3(256), 0, st, Q, X, d_bounds, cap, d_count, reinterpret_cast<uint4 *>(W.list), n16));
+                            dim3(256), 0, st, Q, X, d_bounds, cap, d_count, rst, n16));
         CDC_KCHECK("k_dense_finish", st);
         launches += 3;
         G.gate = X.gate;
+        G.gate0 = X.gate;
         dense_reset = true;
+        dense_gate = X.gate;
     }
     if (P.kK) {
         // K-phase speculation (cdc_kphase.cuh); the ordinary pipeline behind it
         // runs only if its gate opens (a halo on the true chain gave up)
-        const cdc::KGeo Q = kgeo(p, P, G.data, total_len);
+        cdc::KGeo Q = kgeo(p, P, G.data, total_len);
+        Q.skip = dense_gate;  // (behind the dense-index mode: nothing to do when its gate stayed shut)
         const cdc::KWork KW = kcarve(P, W.list);
         const uint64_t N = (uint64_t)Q.G * Q.K, NB = (Q.G + cdc::KB - 1) / cdc::KB;
-        const uint64_t n16 = P.kreset_bytes / 16;
-        const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());
-        cdc::k_reset<<<rb ? rb : 1, 256, 0, st>>>(reinterpret_cast<uint4 *>(KW.list), n16, nullptr);
-        CDC_KCHECK("k_reset (K-phase)", st);
+        if (!dense_reset) {
+            const uint64_t n16 = P.kreset_bytes / 16;
+            const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());
+            cdc::k_reset<<<rb ? rb : 1, 256, 0, st>>>(reinterpret_cast<uint4 *>(KW.list), n16, nullptr);
+            CDC_KCHECK("k_reset (K-phase)", st);
+            ++launches;
+        }
+        dense_reset = false;  // the ordinary pipeline's own (gated) reset follows
         CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kspec<ALGO>),
                             dim3((unsigned)std::min<uint64_t>((N + cdc::SPEC_WARPS - 1) / cdc::SPEC_WARPS,
                                                               (uint64_t)num_sms())),
@@ -2283,7 +2317,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres3), dim3((unsigned)((NB + 7) / 8)), dim3(256), 0,
                             st, Q, KW, d_bounds, cap));
         CDC_KCHECK("k_kres3", st);
-        launches += 5;
+        launches += 4;
         G.gate = KW.gate;
     }
     // reset the published lists (list entries -> LIST_EMPTY, pub -> PUB_OPEN) and
@@ -2293,7 +2327,7 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         const unsigned rb = (unsigned)std::min<uint64_t>((n16 + 255) / 256, 4 * (uint64_t)num_sms());
         if (G.gate)
             CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_reset), dim3(rb ? rb : 1), dim3(256), 0, st,
-                                reinterpret_cast<uint4 *>(W.list), n16, G.gate));
+                                reinterpret_cast<uint4 *>(W.list), n16, G.gate, G.gate0));
         else
             cdc::k_reset<<<rb ? rb : 1, 256, 0, st>>>(reinterpret_cast<uint4 *>(W.list), n16, G.gate);
         CDC_KCHECK("k_reset", st);
@@ -2530,6 +2564,7 @@ int run_chunk(const cdc_params *p, const uint8_t *d_data, const uint64_t *d_file
     G.tmode = 0;
     G.sparse = sparse_on(p->window, p->max_size);
     G.gate = nullptr;
+    G.gate0 = nullptr;
     uint64_t *file_out = batch ? d_bound_off : W.file_out;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (p->algo) {

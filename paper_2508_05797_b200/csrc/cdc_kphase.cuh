@@ -64,7 +64,11 @@ struct KGeo {
     uint64_t max_size;
     uint64_t Hk;        // halo cap (bytes past the segment end)
     int sparse;
+    const uint32_t *skip;  // non-null: the dense-index mode's gate; 0 there = the output is written already
 };
+// (read before griddepcontrol.wait: the gate is final before any kernel behind k_dense_finish can start,
+// see Geometry::gate0 in cdc_kernels.cu)
+__device__ __forceinline__ bool kskip(const KGeo &Q) { return Q.skip != nullptr && __ldcg(Q.skip) == 0u; }
 struct KWork {
     uint32_t *list;     // N x capk: starts - p_g (reset to LIST_EMPTY)
     uint32_t *pub;      // N: KPUB_OPEN, then the node's entry count (reset)
@@ -329,6 +333,7 @@ template <int ALGO>
 __global__ void __launch_bounds__(SPEC_WARPS * 32, 1) k_kspec(KGeo Q, KWork KW) {
     extern __shared__ __align__(128) uint8_t smem[];
     if (threadIdx.x == 0) stamp(TM_SPEC_BEGIN);
+    if (kskip(Q)) return;
     pdl_wait();  // the reset of the lists has completed
     if (threadIdx.x == 0) stamp(TM_SPEC_WAITED);
     const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -350,6 +355,7 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, 1) k_kspec(KGeo Q, KWork KW) 
 __global__ void __launch_bounds__(KRES1_WARPS * 32) k_kres1(KGeo Q, KWork KW) {
     __shared__ uint32_t s_nx[KRES1_WARPS][KB * KP_MAXK], s_ix[KRES1_WARPS][KB * KP_MAXK],
         s_cn[KRES1_WARPS][KB * KP_MAXK];
+    if (kskip(Q)) return;
     pdl_wait();
     pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -396,6 +402,7 @@ __global__ void __launch_bounds__(1024) k_kres2(KGeo Q, KWork KW, uint64_t *d_co
     uint32_t *s_bxi = reinterpret_cast<uint32_t *>(smem);
     const uint32_t N = Q.G * Q.K;
     int32_t *s_val = reinterpret_cast<int32_t *>(s_bxi + N);
+    if (kskip(Q)) return;  // (the ordinary pipeline behind looks at the dense gate first as well)
     pdl_wait();
     pdl_trigger();
     for (uint32_t v = threadIdx.x; v < N; v += blockDim.x) {
@@ -433,6 +440,7 @@ __global__ void __launch_bounds__(1024) k_kres2(KGeo Q, KWork KW, uint64_t *d_co
 
 // Level 3: one warp per block writes the true chain's starts inside the block.
 __global__ void __launch_bounds__(256) k_kres3(KGeo Q, KWork KW, uint64_t *bounds, uint64_t cap) {
+    if (kskip(Q)) return;
     pdl_wait();
     pdl_trigger();
     const int lane = lane_id();
