@@ -313,12 +313,14 @@ int cdc_fetched(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64
 
 /*
  * K-phase speculation: a single stream whose window takes the
- * sparse walk (w >= 4096) and whose segments are too long for the transfer
- * tables is chunked with k chains per segment, started k-th of a chunk length
+ * sparse walk (w >= 4096), with default segments (seg_bytes = halo_bytes = 0;
+ * with the dense-index mode off, only when they are too long for the transfer
+ * tables) is chunked with k chains per segment, started k-th of a chunk length
  * apart, so that a chain entering a segment meets one of them within a few
  * chunks (the boundaries are the same; only the work differs).  k = -1
- * restores the default (4 chains for RAM with windows >= 12 KiB, else 2, or the
- * CDC_KPHASE environment variable), 0 disables it, 1..8 forces k.  Process-
+ * restores the default (4 chains for windows >= 12 KiB -- AE only below 512 MiB --,
+ * else 2, more on streams with fewer segments than walkers; or the CDC_KPHASE
+ * environment variable), 0 disables it, 1..8 forces k.  Process-
  * wide; it changes cdc_workspace_size's result, so set it before sizing a
  * workspace.  Returns CDC_ERR_INVALID for other values.
  */
@@ -331,8 +333,9 @@ int cdc_set_kphase(int k);
  * and max_size >= 2 window + 2 is first tried as one recurrence over the
  * positions of the saturating byte (k_dense_index, k_dense_write); the kernels
  * verify that the stream is saturated everywhere and otherwise hand the call
- * to the ordinary pipeline on the device (the boundaries are the same; only
- * the work differs).  on = -1 restores the default (on, or the CDC_DENSE
+ * to K-phase speculation and then the ordinary pipeline on the device (the
+ * boundaries are the same; only the work differs).  With the mode off, default-
+ * segment streams try the transfer tables before K-phase, as before it existed.  on = -1 restores the default (on, or the CDC_DENSE
  * environment variable), 0 disables it, 1 enables it.  Process-wide; it
  * changes cdc_workspace_size's result, so set it before sizing a workspace.
  * Returns CDC_ERR_INVALID for other values.

@@ -1902,9 +1902,14 @@ bool dense_on() {
 // CDC_KPHASE in the environment: 0 disables K-phase speculation, 1..8 forces
 // that many chains per segment; by default 4 for RAM with windows of 12 KiB and
 // more (RAM at 16 KiB), else 2 (measured on configs[2]'s 1 GiB base, DESIGN.md
-// §6).  CDC_KSEGS overrides its segment count.
+// §6).  AE with such windows also takes 4 below 512 MiB: on a stream without
+// zero-filled regions two chains half a chunk apart meet only after ~(w / 2 /
+// 362)^2 = 500 chunks (uniform 256 MiB, AE-Max 16 KiB: 0.90 ms with K = 2, 0.29 ms
+// with 4), while configs[2]'s 1 GiB streams, whose zero-filled regions bring AE
+// chains together, run 15 % faster with 2 (0.38 against 0.45 ms).  CDC_KSEGS
+// overrides its segment count.
 std::atomic<int> g_kphase{-2};  // cdc_set_kphase (-2: not read from the environment yet)
-int kphase_k(int algo, uint32_t w) {
+int kphase_k(int algo, uint32_t w, uint64_t total_len) {
     int v = g_kphase.load();
     if (v == -2) {
         const char *e = getenv("CDC_KPHASE");
@@ -1915,7 +1920,7 @@ int kphase_k(int algo, uint32_t w) {
     }
     if (v == 0) return 0;
     if (v > 0) return std::min(v, cdc::KP_MAXK);
-    return (algo == CDC_RAM && w >= 12288) ? 4 : 2;
+    return (w >= 12288 && (algo == CDC_RAM || total_len <= (512ull << 20))) ? 4 : 2;
 }
 uint64_t kphase_segs() {
     static long long v = -2;
@@ -2042,7 +2047,7 @@ void make_plan(const cdc_params *p, uint64_t nfiles, uint64_t total_len, uint64_
     const bool small = nfiles <= 1 && dense_on() && p->seg_bytes == 0 && p->halo_bytes == 0 && p->window >= 4096 &&
                        p->window <= cdc::DN_WMAX && p->max_size >= 2ull * p->window + 2 &&
                        total_len >= (1ull << 20) && total_len <= (64ull << 20);
-    int K = nfiles <= 1 ? kphase_k(p->algo, p->window) : 0;
+    int K = nfiles <= 1 ? kphase_k(p->algo, p->window, total_len) : 0;
     const bool tm = tmode_on() && p->window >= 4096 && S <= T_MAX_SEG;
     const uint64_t kmax_seg = kphase_segs() ? ~0ull : (p->window >= 12288 ? 4ull << 20 : 1ull << 20);
     // (default segments: K-phase also in front of the transfer tables' range -- a failed table attempt on a
