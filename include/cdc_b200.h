@@ -263,7 +263,12 @@ int cdc_profile_query(int *done);
  *   [3] 1 if the fused look-back fast path produced the output, 2 if the
  *       transfer tables did (saturated streams), 0 if k_fixup's resolver and
  *       fix-up walkers ran (with CDC_TDEBUG set in the environment this
- *       call also prints why a transfer-table attempt gave up), [4] segments
+ *       call also prints why a transfer-table attempt gave up), 3 if K-phase
+ *       speculation did ([0..2] are then its segments, segment bytes and halo
+ *       cap, [4..6] its nodes that met another chain / gave up / ended or
+ *       were never reached, [7] the chain starts its walkers recorded), 4 if
+ *       the dense-index mode did ([0..2] its segments, segment bytes and the
+ *       bytes indexed past a segment; [4] = [0], [5..7] = 0), [4] segments
  *       whose chain met the
  *       next segment's chain, [5] segments whose halo walk gave up or was
  *       undecided, [6] segments whose chain skipped a later segment or reached
