@@ -471,6 +471,10 @@ def measure_c0(args, cdc, torch, dist, dev, world):
             graph.replay()
 
     steps = C0_COPIES * max(5, args.steps // 2)
+    t_end = time.perf_counter() + 0.2  # (the first key measured: bring the clocks up before a 3 ms timed region)
+    while time.perf_counter() < t_end:
+        run(C0_COPIES)
+        torch.cuda.synchronize()
     ms = timed(run, steps, stream, dist, dev, torch)
     peak, peak_src = load_peaks()
     gbs = C0_STREAM * steps / (ms / 1e3) / 1e9
