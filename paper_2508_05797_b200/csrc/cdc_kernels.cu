@@ -2253,6 +2253,8 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_kspec<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, spec_smem));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_kres2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(cdc::KNODE_MAX * 8)));
+        CDC_CUDA(cudaFuncSetAttribute(cdc::k_kres_all, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(cdc::KRES_ALL_NB * cdc::KB * cdc::KP_MAXK * 8)));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_dense_index, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::DN_SMEM));
         CDC_CUDA(cudaFuncSetAttribute(cdc::k_dense_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, cdc::DN_SMEM));
         attr_set[dev] = true;
@@ -2312,17 +2314,28 @@ int launch_pipeline(const cdc_params *p, const Plan &P, cdc::Geometry &G, cdc::W
                                                               (uint64_t)num_sms())),
                             dim3(cdc::SPEC_WARPS * 32), (size_t)spec_smem, st, Q, KW));
         CDC_KCHECK("k_kspec", st);
-        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres1),
-                            dim3((unsigned)((NB + cdc::KRES1_WARPS - 1) / cdc::KRES1_WARPS)),
-                            dim3(cdc::KRES1_WARPS * 32), 0, st, Q, KW));
-        CDC_KCHECK("k_kres1", st);
-        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres2), dim3(1), dim3(1024), (size_t)(N * 8), st,
-                            Q, KW, d_count));
-        CDC_KCHECK("k_kres2", st);
-        CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres3), dim3((unsigned)((NB + 7) / 8)), dim3(256), 0,
-                            st, Q, KW, d_bounds, cap));
-        CDC_KCHECK("k_kres3", st);
-        launches += 4;
+        if (NB <= cdc::KRES_ALL_NB) {
+            // a small stream: the three resolution levels in one CTA, which is also the
+            // ordinary pipeline's list reset when a node on the true path gave up
+            CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres_all), dim3(1), dim3(1024), (size_t)(N * 8),
+                                st, Q, KW, d_count, d_bounds, cap, reinterpret_cast<uint4 *>(W.list),
+                                (uint64_t)(P.reset_bytes / 16)));
+            CDC_KCHECK("k_kres_all", st);
+            launches += 2;
+            dense_reset = true;  // (the ordinary pipeline's reset is part of k_kres_all)
+        } else {
+            CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres1),
+                                dim3((unsigned)((NB + cdc::KRES1_WARPS - 1) / cdc::KRES1_WARPS)),
+                                dim3(cdc::KRES1_WARPS * 32), 0, st, Q, KW));
+            CDC_KCHECK("k_kres1", st);
+            CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres2), dim3(1), dim3(1024), (size_t)(N * 8), st,
+                                Q, KW, d_count));
+            CDC_KCHECK("k_kres2", st);
+            CDC_CUDA(launch_pdl(reinterpret_cast<const void *>(cdc::k_kres3), dim3((unsigned)((NB + 7) / 8)), dim3(256),
+                                0, st, Q, KW, d_bounds, cap));
+            CDC_KCHECK("k_kres3", st);
+            launches += 4;
+        }
         G.gate = KW.gate;
     }
     // reset the published lists (list entries -> LIST_EMPTY, pub -> PUB_OPEN) and

@@ -351,37 +351,33 @@ __global__ void __launch_bounds__(SPEC_WARPS * 32, 1) k_kspec(KGeo Q, KWork KW) 
     if (lane == 0) stamp(TM_SPEC_END);
 }
 
-// Level 1: per block of KB segments, every node's first exit from the block.
-__global__ void __launch_bounds__(KRES1_WARPS * 32) k_kres1(KGeo Q, KWork KW) {
-    __shared__ uint32_t s_nx[KRES1_WARPS][KB * KP_MAXK], s_ix[KRES1_WARPS][KB * KP_MAXK],
-        s_cn[KRES1_WARPS][KB * KP_MAXK];
-    if (kskip(Q)) return;
-    pdl_wait();
-    pdl_trigger();
-    const int warp = threadIdx.x >> 5, lane = lane_id();
-    const uint32_t NB = (Q.G + KB - 1) / KB, N = Q.G * Q.K;
-    const uint32_t b = blockIdx.x * KRES1_WARPS + (uint32_t)warp;
-    if (b >= NB) return;
+// Level 1: per block of KB segments, every node's first exit from the block
+// (warp slot `ws` of KRES1_WARPS works on block b).
+__device__ __forceinline__ void kres1_block(const KGeo &Q, const KWork &KW, int ws, uint32_t b,
+                                            uint32_t (*s_nx)[KB * KP_MAXK], uint32_t (*s_ix)[KB * KP_MAXK],
+                                            uint32_t (*s_cn)[KB * KP_MAXK]) {
+    const int lane = lane_id();
+    const uint32_t N = Q.G * Q.K;
     const uint32_t v0 = b * KB * Q.K, v1 = min(N, v0 + KB * Q.K);
     for (uint32_t v = v0 + lane; v < v1; v += 32) {
-        s_nx[warp][v - v0] = KW.nxt[v];
-        s_ix[warp][v - v0] = KW.idx[v];
-        s_cn[warp][v - v0] = KW.pub[v];
+        s_nx[ws][v - v0] = KW.nxt[v];
+        s_ix[ws][v - v0] = KW.idx[v];
+        s_cn[ws][v - v0] = KW.pub[v];
     }
     __syncwarp();
     for (uint32_t v = v0 + lane; v < v1; v += 32) {
         uint32_t u = v, tx, ti;
         int32_t acc = 0;
         for (;;) {
-            const uint32_t nx = s_nx[warp][u - v0];
-            const uint32_t cn = s_cn[warp][u - v0];
+            const uint32_t nx = s_nx[ws][u - v0];
+            const uint32_t cn = s_cn[ws][u - v0];
             if (nx >= KN_VOID) {  // terminal
                 acc += (int32_t)cn;
                 tx = nx == KN_END ? KX_END : nx == KN_VOID ? KX_VOID : KX_UNSYNC;
                 ti = 0;
                 break;
             }
-            const uint32_t ix = s_ix[warp][u - v0];
+            const uint32_t ix = s_ix[ws][u - v0];
             acc += (int32_t)cn - (int32_t)ix;
             if (nx < v0 || nx >= v1) {
                 tx = nx;
@@ -394,17 +390,25 @@ __global__ void __launch_bounds__(KRES1_WARPS * 32) k_kres1(KGeo Q, KWork KW) {
         KW.bval[v] = acc;
     }
     if (lane == 0) KW.ent[2 * b] = ~0ull;
+    __syncwarp();
 }
-
-// Level 2: node 0's path, block by block.
-__global__ void __launch_bounds__(1024) k_kres2(KGeo Q, KWork KW, uint64_t *d_count) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint32_t *s_bxi = reinterpret_cast<uint32_t *>(smem);
-    const uint32_t N = Q.G * Q.K;
-    int32_t *s_val = reinterpret_cast<int32_t *>(s_bxi + N);
-    if (kskip(Q)) return;  // (the ordinary pipeline behind looks at the dense gate first as well)
+__global__ void __launch_bounds__(KRES1_WARPS * 32) k_kres1(KGeo Q, KWork KW) {
+    __shared__ uint32_t s_nx[KRES1_WARPS][KB * KP_MAXK], s_ix[KRES1_WARPS][KB * KP_MAXK],
+        s_cn[KRES1_WARPS][KB * KP_MAXK];
+    if (kskip(Q)) return;
     pdl_wait();
     pdl_trigger();
+    const int warp = threadIdx.x >> 5;
+    const uint32_t NB = (Q.G + KB - 1) / KB;
+    const uint32_t b = blockIdx.x * KRES1_WARPS + (uint32_t)warp;
+    if (b >= NB) return;
+    kres1_block(Q, KW, warp, b, s_nx, s_ix, s_cn);
+}
+
+// Level 2: node 0's path, block by block (one CTA; s_bxi / s_val: N words each).
+__device__ __forceinline__ void kres2_path(const KGeo &Q, const KWork &KW, uint64_t *d_count, uint32_t *s_bxi,
+                                           int32_t *s_val) {
+    const uint32_t N = Q.G * Q.K;
     for (uint32_t v = threadIdx.x; v < N; v += blockDim.x) {
         s_bxi[v] = KW.bxi[v];
         s_val[v] = KW.bval[v];
@@ -437,16 +441,18 @@ __global__ void __launch_bounds__(1024) k_kres2(KGeo Q, KWork KW, uint64_t *d_co
     if (!fail) *d_count = total;
     *KW.gate = fail;
 }
-
-// Level 3: one warp per block writes the true chain's starts inside the block.
-__global__ void __launch_bounds__(256) k_kres3(KGeo Q, KWork KW, uint64_t *bounds, uint64_t cap) {
-    if (kskip(Q)) return;
+__global__ void __launch_bounds__(1024) k_kres2(KGeo Q, KWork KW, uint64_t *d_count) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t *s_bxi = reinterpret_cast<uint32_t *>(smem);
+    if (kskip(Q)) return;  // (the ordinary pipeline behind looks at the dense gate first as well)
     pdl_wait();
     pdl_trigger();
+    kres2_path(Q, KW, d_count, s_bxi, reinterpret_cast<int32_t *>(s_bxi + Q.G * Q.K));
+}
+
+// Level 3: one warp writes the true chain's starts inside block b.
+__device__ __forceinline__ void kres3_block(const KGeo &Q, const KWork &KW, uint32_t b, uint64_t *bounds, uint64_t cap) {
     const int lane = lane_id();
-    const uint32_t NB = (Q.G + KB - 1) / KB;
-    const uint32_t b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (b >= NB || *KW.gate != 0) return;
     const uint64_t e0 = KW.ent[2 * b];
     if (e0 == ~0ull) return;  // the true chain jumps over this block
     uint32_t v = (uint32_t)e0, ix = (uint32_t)(e0 >> 32);
@@ -470,4 +476,42 @@ __global__ void __launch_bounds__(256) k_kres3(KGeo Q, KWork KW, uint64_t *bound
         ix = nix;
     }
 }
+__global__ void __launch_bounds__(256) k_kres3(KGeo Q, KWork KW, uint64_t *bounds, uint64_t cap) {
+    if (kskip(Q)) return;
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t NB = (Q.G + KB - 1) / KB;
+    const uint32_t b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= NB || *KW.gate != 0) return;
+    kres3_block(Q, KW, b, bounds, cap);
+}
 
+// The three levels in one CTA, for streams of at most KRES_ALL_NB blocks (small
+// streams, where three launches cost more than the work): level 1 by
+// KRES1_WARPS warps over the blocks, level 2, level 3 by every warp; when a node
+// on the true path gave up, the CTA resets the ordinary pipeline's lists
+// ([rst, rst + n16)) instead, so that pipeline's own reset launch is not needed.
+constexpr uint32_t KRES_ALL_NB = 32;
+__global__ void __launch_bounds__(1024) k_kres_all(KGeo Q, KWork KW, uint64_t *d_count, uint64_t *bounds, uint64_t cap,
+                                                   uint4 *rst, uint64_t n16) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint32_t s_nx[KRES1_WARPS][KB * KP_MAXK], s_ix[KRES1_WARPS][KB * KP_MAXK],
+        s_cn[KRES1_WARPS][KB * KP_MAXK];
+    uint32_t *s_bxi = reinterpret_cast<uint32_t *>(smem);
+    if (kskip(Q)) return;
+    pdl_wait();
+    pdl_trigger();
+    const int warp = threadIdx.x >> 5;
+    const uint32_t NB = (Q.G + KB - 1) / KB;
+    if (warp < KRES1_WARPS)
+        for (uint32_t b = (uint32_t)warp; b < NB; b += KRES1_WARPS) kres1_block(Q, KW, warp, b, s_nx, s_ix, s_cn);
+    __syncthreads();  // (bxi, bval and the blocks' "no entry" marks, written and read by this CTA)
+    kres2_path(Q, KW, d_count, s_bxi, reinterpret_cast<int32_t *>(s_bxi + Q.G * Q.K));
+    __syncthreads();
+    if (*KW.gate != 0) {
+        const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u);
+        for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x) rst[i] = ones;
+        return;
+    }
+    for (uint32_t b = (uint32_t)warp; b < NB; b += blockDim.x >> 5) kres3_block(Q, KW, b, bounds, cap);
+}
