@@ -190,3 +190,28 @@ def test_dense_off_switch_and_repeats(cdc):
         assert got.size == exp.size and (got == exp).all()
     finally:
         cdc.set_dense(-1)
+
+
+@pytest.mark.parametrize("algo,avg", [("ram", 8192), ("ram", 16384), ("ae_max", 8192), ("ae_min", 16384)])
+def test_dense_then_kphase_on_versioned(cdc, algo, avg):
+    """configs[2]'s recipe at 16 MiB (uniform bytes with zero-filled regions): the dense attempt gives up,
+    K-phase speculation behind its gate produces the output (its three resolution levels in one CTA)."""
+    d = synth.versioned(16 << 20, 0, seed=5)[0]
+    p = cdc.params(algo, avg_size=avg)
+    exp = oracle.chunk(algo, d, p.window, p.max_size)
+    got, st = _run(cdc, d, p)
+    assert st["fast_path"] == 3, st
+    assert got.size == exp.size and (got == exp).all()
+
+
+def test_dense_hands_over_constant_streams(cdc):
+    """A constant stream is not saturated (the dense gate opens); whichever path behind it resolves the
+    chain (K-phase when one of its chains coincides with the true one, else the ordinary pipeline, whose
+    lists K-phase's resolver then resets: tests/test_gpu_kphase.py forces that), the output is the oracle's."""
+    for algo, val in (("ram", 0), ("ae_max", 7), ("ae_min", 255)):
+        d = np.full((6 << 20) + 321, val, dtype=np.uint8)
+        p = cdc.params(algo, avg_size=8192)
+        exp = oracle.chunk(algo, d, p.window, p.max_size)
+        got, st = _run(cdc, d, p)
+        assert st["fast_path"] != DENSE, st
+        assert got.size == exp.size and (got == exp).all()
